@@ -1,0 +1,41 @@
+"""The CPU oracle against the reference's recorded outputs (parity pin)."""
+
+import numpy as np
+import pytest
+
+import oracle
+from golden_util import TABLE_PARAMS, case_input, digest
+
+SMALL = ["ref_random_multilayer_s9", "ref_flat_plane_s7", "ref_spiral_s3",
+         "ref_ramp_over_tunnel_s6", "synth_cfg0", "synth_cfg4", "synth_two_storey_small"]
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_oracle_matches_reference(golden, name):
+    case = golden["cases"][name]
+    xyz = case_input(name, case)
+    t = oracle.build(xyz, case["d_s"], case["r_g"])
+    assert list(t["ground"].shape) == case["shape"]
+    assert [float(h) for h in t["heights"]] == case["heights"]
+    assert list(t["origin"]) == case["origin"]
+    assert digest(t["ground"]) == case["ground_sha256"]
+    assert digest(t["ceiling"]) == case["ceiling_sha256"]
+    cost = oracle.evaluate(t["ground"], t["ceiling"], case["r_g"], TABLE_PARAMS)
+    assert digest(cost) == case["cost_sha256"]
+    assert oracle.simplify(t["ground"], cost) == case["keep"]
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["synth_cfg1"])
+def test_oracle_matches_reference_large(golden, name):
+    test_oracle_matches_reference(golden, name)
+
+
+def test_oracle_inflation_cases(golden):
+    for c in golden["inflation"]:
+        w = oracle.kernel_weights(0.2, 0.4, c["r_g"])
+        assert digest(w) == c["kernel_sha256"]
+        shape = tuple(c["shape"])
+        g = np.random.default_rng(c["seed"]).uniform(0.0, 50.0, shape).astype(np.float32)
+        g[np.random.default_rng(c["seed"] + 1).uniform(size=shape) < 0.03] = 50.0
+        assert digest(oracle.inflate(g, w)) == c["out_sha256"]
