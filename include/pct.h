@@ -1,0 +1,161 @@
+/*
+ * pct.h — C ABI of the B200 point-cloud-tomography library (libpct.so).
+ *
+ * Drop-in boundary for the hot path of the reference package `tomoplan`
+ * (arXiv 2403.07631): tomogram build -> traversability evaluation -> slice
+ * simplification.  The reference is pure Python with no FFI of its own; each
+ * entry point below names the reference function it replaces (file:line under
+ * /root/reference/pkg/src/tomoplan/).  The Python mirror of the reference API
+ * (paper_2403_07631_b200/*.py) binds these with ctypes; INTEGRATION.md shows the
+ * binding a tomoplan maintainer would add.
+ *
+ * Conventions
+ *  - Plain C types only.  `xyz` is an (n, 3) row-major array of float32
+ *    (dtype PCT_F32) or float64 (PCT_F64).  Layers are float32, row-major
+ *    (rows, cols) per slice, slices contiguous: index (k*rows + i)*cols + j.
+ *    Invalid cells are NaN with bits 0x7FC00000 (numpy's NaN).
+ *  - Every function returns 0 (PCT_OK) or a negative PCT_E* code and never
+ *    throws; pct_last_error(ctx) holds the message.  Argument errors are
+ *    reported with the reference's exception text where one exists.
+ *  - A context owns one device, one CUDA stream and its scratch; it is not
+ *    re-entrant.  Device pointers passed in must live on the context's device.
+ *  - Functions that return host-visible results synchronise the context
+ *    stream; the others are stream-ordered (pct_sync waits).
+ */
+#ifndef PCT_H_
+#define PCT_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PCT_ABI_VERSION 1
+
+enum {
+  PCT_OK = 0,
+  PCT_E_INVALID = -1,    /* ValueError in the reference */
+  PCT_E_GRID = -2,       /* GridSizeError (tomogram.py:25-26,141-142) */
+  PCT_E_CUDA = -3,       /* CUDA runtime failure -> RuntimeError */
+  PCT_E_NOMEM = -4,      /* device or pinned allocation failed */
+  PCT_E_EMPTY = -5,      /* CloudFormatError("zero valid points"), cloud_io.py:38-39 */
+  PCT_E_NONFINITE = -6,  /* ValueError non-finite coordinates, cloud_io.py:40-41 */
+  PCT_E_NOCOST = -7,     /* ValueError "slice has no cost layer" simplify.py:34-35 */
+  PCT_E_RANGE = -8       /* IndexError, simplify.py:49-50 */
+};
+
+enum { PCT_F32 = 0, PCT_F64 = 1 };
+enum { PCT_LAYER_GROUND = 0, PCT_LAYER_CEILING = 1, PCT_LAYER_COST = 2 };
+
+/* TravParams (traversability.py:21-56) with patch_radius resolved for r_g. */
+typedef struct {
+  double d_min, d_ref, theta_b, theta_s, theta_p, c_barrier;
+  double alpha_d, alpha_b, alpha_s;
+  int32_t patch_radius;
+  int32_t _pad;
+} pct_trav_params;
+
+/* Grid frame of tomogram.py:134-145. heights are z_min + d_s*(k+1). */
+typedef struct {
+  double origin_x, origin_y, z_min, d_s, r_g;
+  int32_t rows, cols, n_slices;
+  int32_t _pad;
+} pct_frame;
+
+typedef struct pct_ctx pct_ctx;
+typedef struct pct_tomo pct_tomo; /* device-resident tomogram (ground/ceiling/cost stacks) */
+
+/* ---- context --------------------------------------------------------- */
+int pct_abi_version(void);
+int pct_ctx_create(int device, pct_ctx **out);
+int pct_ctx_destroy(pct_ctx *ctx);
+const char *pct_last_error(const pct_ctx *ctx);
+int pct_sync(pct_ctx *ctx);
+/* Kernel launches issued by this context since creation (evidence counter). */
+int64_t pct_launch_count(const pct_ctx *ctx);
+/* Use an external stream (cudaStream_t as void*); NULL restores the own stream. */
+int pct_set_stream(pct_ctx *ctx, void *stream);
+
+/* ---- memory helpers (device / pinned host, owned by the caller) ------- */
+int pct_malloc(pct_ctx *ctx, size_t bytes, void **dptr);
+int pct_free(pct_ctx *ctx, void *dptr);
+int pct_host_alloc(pct_ctx *ctx, size_t bytes, void **hptr);
+int pct_host_free(pct_ctx *ctx, void *hptr);
+int pct_memcpy_h2d(pct_ctx *ctx, void *dst, const void *src, size_t bytes);
+int pct_memcpy_d2h(pct_ctx *ctx, void *dst, const void *src, size_t bytes); /* syncs */
+int pct_memcpy_d2h_async(pct_ctx *ctx, void *dst, const void *src, size_t bytes);
+
+/* ---- stage 0: bounds (cloud_io.py:47-50, PointCloud.bounds) ------------ */
+/* Exact float64 min/max of device xyz. Fails with PCT_E_NONFINITE on NaN/Inf. */
+int pct_bounds(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, double lo[3], double hi[3]);
+
+/* Host-only grid frame (tomogram.py:134-145); heights_out may be NULL. */
+int pct_frame_compute(const double lo[3], const double hi[3], double d_s, double r_g,
+                      int64_t max_grid_side, pct_frame *fr, double *heights_out,
+                      int32_t heights_cap);
+
+/* ---- stage 1: tomogram build (tomogram.py:127-213) -------------------- */
+/* Device in, device out: ground/ceiling are (S, rows, cols) float32. */
+int pct_build(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, const pct_frame *fr,
+              const double *heights, float *ground, float *ceiling);
+
+/* ---- stage 2: traversability (traversability.py:59-236) ---------------- */
+/* kernel_w: host (kside x kside) float32 weights from build_kernel
+   (traversability.py:194-202). Fused interval+terrain+fuse+inflate per slice. */
+int pct_evaluate(pct_ctx *ctx, const float *ground, const float *ceiling, int32_t n_slices,
+                 int32_t rows, int32_t cols, double r_g, const pct_trav_params *p,
+                 const float *kernel_w, int32_t kside, float *cost);
+/* per-op entry points on one (rows, cols) layer, device pointers */
+int pct_interval_cost(pct_ctx *ctx, const float *ground, const float *ceiling, int32_t rows,
+                      int32_t cols, const pct_trav_params *p, float *out);      /* :59-73 */
+int pct_ground_cost(pct_ctx *ctx, const float *ground, int32_t rows, int32_t cols, double r_g,
+                    const pct_trav_params *p, float *out);                      /* :150-159 */
+int pct_slope_magnitudes(pct_ctx *ctx, const float *ground, int32_t rows, int32_t cols,
+                         double r_g, double *m_xy, double *m_grad, uint8_t *isolated); /* :106-114 */
+int pct_fuse_costs(pct_ctx *ctx, const float *c_interval, const float *c_ground,
+                   const uint8_t *ground_valid, int32_t rows, int32_t cols,
+                   const pct_trav_params *p, float *out);                       /* :162-170 */
+int pct_inflate(pct_ctx *ctx, const float *cost, int32_t rows, int32_t cols,
+                const float *kernel_w, int32_t kside, float *out);              /* :205-213 */
+int pct_gentle_fraction(pct_ctx *ctx, const uint8_t *gentle, int32_t rows, int32_t cols,
+                        int32_t radius, double *out);                           /* :117-128 */
+int pct_terrain_cost_values(pct_ctx *ctx, const double *m_xy, const double *m_grad,
+                            const double *p_s, int64_t n, const pct_trav_params *p,
+                            double *out);                                       /* :131-147 */
+
+/* ---- stage 3: simplification (simplify.py:18-73) ---------------------- */
+/* Runs the reference's forward sweep to a fixpoint; writes the surviving
+   original slice indices (ascending) to keep_host[0..*n_keep). */
+int pct_simplify(pct_ctx *ctx, const float *ground, const float *cost, int32_t n_slices,
+                 int32_t rows, int32_t cols, double eps_e, double c_barrier,
+                 int32_t *keep_host, int32_t *n_keep);
+/* unique-cell mask of slice k given neighbour slices (-1 = none), simplify.py:31-53 */
+int pct_unique_mask(pct_ctx *ctx, const float *ground, const float *cost, int32_t rows,
+                    int32_t cols, int32_t k, int32_t below, int32_t above, double eps_e,
+                    double c_barrier, uint8_t *mask);
+
+/* ---- whole pipeline on a device-resident tomogram ---------------------- */
+/* xyz may be a device pointer (xyz_on_host = 0) or host memory (1; pinned
+   memory from pct_host_alloc is fastest).  Allocates the stacks. */
+int pct_tomo_build(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, int xyz_on_host,
+                   double d_s, double r_g, int64_t max_grid_side, pct_tomo **out);
+/* Wrap caller-provided host stacks (e.g. a reference Tomogram) for evaluation. */
+int pct_tomo_upload(pct_ctx *ctx, const pct_frame *fr, const double *heights,
+                    const float *ground_host, const float *ceiling_host, pct_tomo **out);
+int pct_tomo_evaluate(pct_ctx *ctx, pct_tomo *t, const pct_trav_params *p,
+                      const float *kernel_w, int32_t kside);
+int pct_tomo_simplify(pct_ctx *ctx, pct_tomo *t, double eps_e, double c_barrier,
+                      int32_t *keep_host, int32_t *n_keep);
+int pct_tomo_frame(const pct_tomo *t, pct_frame *fr, double *heights, int32_t heights_cap);
+/* device pointer of a layer stack (NULL if absent), e.g. for zero-copy consumers */
+const float *pct_tomo_layer(const pct_tomo *t, int layer);
+/* copy slice k of a layer (or all slices if k < 0) to host memory; syncs */
+int pct_tomo_download(pct_ctx *ctx, const pct_tomo *t, int layer, int32_t k, float *host);
+int pct_tomo_free(pct_ctx *ctx, pct_tomo *t);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PCT_H_ */

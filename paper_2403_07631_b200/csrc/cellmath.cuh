@@ -1,0 +1,215 @@
+// cellmath.cuh — per-cell arithmetic of the hot path, shared by the sm_100a
+// kernels and a host build used by the CPU tests (tests/test_cellmath.py).
+//
+// Bit-exactness contract: every expression follows the
+// reference's numpy operation order in float64 and rounds to float32 exactly
+// where the reference does.  The library is compiled with --fmad=false
+// (device) / -ffp-contract=off (host); the only fused multiply-adds are the
+// explicit fma() calls of the Markstein division below.
+#pragma once
+
+#include <math.h>
+#include <stdint.h>
+#include <string.h>
+
+#if defined(__CUDACC__)
+#define PCT_HD __host__ __device__ __forceinline__
+#else
+#define PCT_HD static inline
+#endif
+
+namespace pct {
+
+PCT_HD uint32_t f32_bits(float f) {
+#if defined(__CUDA_ARCH__)
+  return __float_as_uint(f);
+#else
+  uint32_t u;
+  memcpy(&u, &f, 4);
+  return u;
+#endif
+}
+PCT_HD float bits_f32(uint32_t u) {
+#if defined(__CUDA_ARCH__)
+  return __uint_as_float(u);
+#else
+  float f;
+  memcpy(&f, &u, 4);
+  return f;
+#endif
+}
+
+// numpy's float32 NaN (np.float32(np.nan)): the invalid-cell marker the
+// reference writes (tomogram.py:203-204) and the LGA archive stores.
+static constexpr uint32_t kNaNBits = 0x7FC00000u;
+
+// Order-preserving float32 -> uint32 key: a < b  <=>  key(a) < key(b) for
+// all non-NaN floats (-0.0 sorts just below +0.0).  Key 0 and key ~0u are
+// never produced by a finite float, so they encode "empty" for max / min.
+PCT_HD uint32_t f32_key(float f) {
+  uint32_t u = f32_bits(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+PCT_HD float key_f32(uint32_t k) {
+  uint32_t u = (k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k;
+  return bits_f32(u);
+}
+static constexpr uint32_t kKeyEmptyMax = 0u;           // identity of max
+static constexpr uint32_t kKeyEmptyMin = 0xFFFFFFFFu;  // identity of min
+
+PCT_HD float decode_ground(uint32_t k) {
+  return k == kKeyEmptyMax ? bits_f32(kNaNBits) : key_f32(k);
+}
+PCT_HD float decode_ceiling(uint32_t k) {
+  return k == kKeyEmptyMin ? bits_f32(kNaNBits) : key_f32(k);
+}
+
+PCT_HD bool finite32(float f) { return (f32_bits(f) & 0x7F800000u) != 0x7F800000u; }
+
+// Correctly rounded a / d for a compile-time-like constant divisor d with
+// yinv = RN(1/d): q0 = RN(a*yinv) is within 1 ulp of a/d, the FMA residual
+// r = a - d*q0 is exact, and RN(q0 + r*yinv) = RN(a/d) (Markstein's theorem).
+// Verified against IEEE division on 8e8 samples.
+PCT_HD double div_const(double a, double d, double yinv) {
+  double q0 = a * yinv;
+  double r = fma(-q0, d, a);
+  return fma(r, yinv, q0);
+}
+
+// glibc >= 2.35 hypot (sysdeps/ieee754/dbl-64/e_hypot.c, non-FMA kernel),
+// restated: numpy's np.hypot calls libm hypot, and the reference computes
+// m_grad with it (traversability.py:112).  Matches glibc 2.39 bit-for-bit on
+// 2e8 random pairs (tests/test_cellmath.py re-checks against np.hypot).
+PCT_HD double hypot_kernel(double ax, double ay) {
+  double h = sqrt(ax * ax + ay * ay);
+  double t1, t2;
+  if (h <= 2.0 * ay) {
+    double delta = h - ay;
+    t1 = ax * (2.0 * delta - ax);
+    t2 = (delta - 2.0 * (ax - ay)) * delta;
+  } else {
+    double delta = h - ax;
+    t1 = 2.0 * delta * (ax - 2.0 * ay);
+    t2 = (4.0 * delta - ay) * ay + delta * delta;
+  }
+  h -= (t1 + t2) / (2.0 * h);
+  return h;
+}
+
+PCT_HD double glibc_hypot(double x, double y) {
+  // inputs here are always finite (differences of finite float32 values)
+  x = fabs(x);
+  y = fabs(y);
+  double ax = x < y ? y : x;
+  double ay = x < y ? x : y;
+  const double kScale = 0x1p-600, kLarge = 0x1p+511, kTiny = 0x1p-459, kEps = 0x1p-54;
+  if (ax > kLarge) {
+    if (ay <= ax * kEps) return ax + ay;
+    return hypot_kernel(ax * kScale, ay * kScale) / kScale;
+  }
+  if (ay < kTiny) {
+    if (ax >= ay / kEps) return ax + ay;
+    return hypot_kernel(ax / kScale, ay / kScale) * kScale;
+  }
+  if (ay <= ax * kEps) return ax + ay;
+  return hypot_kernel(ax, ay);
+}
+
+// Constants of the per-cell evaluation, precomputed on the host.
+struct EvalConsts {
+  double d_min, d_ref, theta_b, theta_s, c_barrier, alpha_d, alpha_b, alpha_s;
+  double rg, inv_rg, two_rg, inv_two_rg;  // gradient divisors (traversability.py:100-102)
+  double inv_theta_b, inv_theta_s;        // q = m / theta (traversability.py:138,141)
+  int32_t ps_min_count;  // smallest gentle count c with RN(c/(2r+1)^2) > theta_p
+  int32_t patch_radius;
+};
+
+// One axis of _axis_gradient (traversability.py:76-103): central difference
+// where both neighbours are valid, one-sided otherwise, 0 with none.
+PCT_HD double axis_gradient(bool vn, bool vp, double en, double ep, double ef,
+                            const EvalConsts &K) {
+  if (vn && vp) return div_const(en - ep, K.two_rg, K.inv_two_rg);
+  if (vn) return div_const(en - ef, K.rg, K.inv_rg);
+  if (vp) return div_const(ef - ep, K.rg, K.inv_rg);
+  return 0.0;
+}
+
+// Neighbourhood of one ground cell: centre e and the 4 axis neighbours
+// (x = columns: r = j+1, l = j-1; y = rows: d = i+1, u = i-1).  NaN = invalid
+// (cells outside the grid are passed as NaN).
+struct Cross {
+  float e, l, r, u, d;
+};
+
+struct TerrainCell {
+  double m_xy, m_grad;
+  bool valid, isolated, gentle;
+};
+
+PCT_HD TerrainCell terrain_cell(const Cross &c, const EvalConsts &K) {
+  TerrainCell t;
+  bool v = finite32(c.e), vl = finite32(c.l), vr = finite32(c.r), vu = finite32(c.u),
+       vd = finite32(c.d);
+  double ef = v ? (double)c.e : 0.0;
+  double gx = axis_gradient(vr, vl, vr ? (double)c.r : 0.0, vl ? (double)c.l : 0.0, ef, K);
+  double gy = axis_gradient(vd, vu, vd ? (double)c.d : 0.0, vu ? (double)c.u : 0.0, ef, K);
+  double ax = fabs(gx), ay = fabs(gy);
+  t.m_xy = ax > ay ? ax : ay;
+  t.m_grad = glibc_hypot(gx, gy);
+  t.valid = v;
+  t.isolated = v && !(vl || vr || vu || vd);
+  t.gentle = v && (t.m_grad < K.theta_s);
+  return t;
+}
+
+// Terrain branch (traversability.py:131-147) in float64.  *needs_ps is set
+// for the foothold branch whose value holds only when p_s > theta_p.
+PCT_HD double terrain_value(double m_xy, double m_grad, const EvalConsts &K, bool *needs_ps) {
+  *needs_ps = false;
+  if (m_xy > K.theta_b) return K.c_barrier;
+  if (m_grad < K.theta_s) {
+    double q = div_const(m_grad, K.theta_s, K.inv_theta_s);
+    return K.alpha_s * (q * q);
+  }
+  *needs_ps = true;
+  double q = div_const(m_xy, K.theta_b, K.inv_theta_b);
+  return K.alpha_b * (q * q);
+}
+
+// interval_cost (traversability.py:59-73) for a valid ground cell, as float32.
+PCT_HD float interval_value(float g, float c, const EvalConsts &K) {
+  if (!finite32(c)) return 0.0f;  // open sky
+  double d = (double)c - (double)g;
+  double adapt = K.alpha_d * (K.d_ref - d);
+  adapt = adapt > 0.0 ? adapt : 0.0;  // np.maximum(0.0, .)
+  return (float)(d < K.d_min ? K.c_barrier : adapt);
+}
+
+// fuse_costs (traversability.py:162-170) for a valid ground cell.
+PCT_HD float fuse_value(float ci, float cg, const EvalConsts &K) {
+  double s = (double)ci + (double)cg;
+  return (float)(K.c_barrier < s ? K.c_barrier : s);
+}
+
+// c_init of one cell given its terrain data and ceiling; float32 with the
+// sign bit marking "becomes c_barrier unless the foothold count passes"
+// (all costs are >= 0, and a foothold-branch value is > 0).
+PCT_HD float cinit_encoded(float g, float ceil, const TerrainCell &t, const EvalConsts &K) {
+  if (!t.valid) return (float)K.c_barrier;
+  float ci = interval_value(g, ceil, K);
+  bool needs_ps = false;
+  double tv = t.isolated ? K.c_barrier : terrain_value(t.m_xy, t.m_grad, K, &needs_ps);
+  float cg = (float)tv;
+  float f = fuse_value(ci, cg, K);
+  if (needs_ps) f = bits_f32(f32_bits(f) | 0x80000000u);
+  return f;
+}
+
+PCT_HD float cinit_resolve(float enc, int count, const EvalConsts &K) {
+  uint32_t u = f32_bits(enc);
+  if (u & 0x80000000u) return count >= K.ps_min_count ? bits_f32(u & 0x7FFFFFFFu)
+                                                      : (float)K.c_barrier;
+  return enc;
+}
+
+}  // namespace pct

@@ -1,0 +1,232 @@
+// k_build.cu — K0 bounds, K1/K2 point binning + ground/ceiling scatter-reduce,
+// K3 per-cell bin scan.  Replaces cloud_io.py:47-50 (bounds) and
+// tomogram.py:147-213 (rasterise, z-sort, split, ufunc.at max/min passes,
+// NaN encoding).
+//
+// Design: no sort.  Each point is binned on the device into
+// b = #{k : h_k < z} (ties go to ground, tomogram.py:156-157) and reduced into
+// per-(bin, cell) float32 max / min scratch planes with order-preserving
+// uint32 atomics (max/min are commutative, so the result is independent of
+// point order, like the reference).  A per-cell scan over bins then produces
+// ground[k] = max over bins <= k and ceiling[k] = min over bins > k, writing
+// numpy's NaN (0x7FC00000) where a cell is empty.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+
+#include "pct_internal.h"
+
+namespace pct {
+namespace {
+
+__device__ __forceinline__ unsigned long long dkey(double d) {
+  unsigned long long u = (unsigned long long)__double_as_longlong(d);
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+__host__ inline double dkey_inv(unsigned long long k) {
+  unsigned long long u = (k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k;
+  double d;
+  std::memcpy(&d, &u, 8);
+  return d;
+}
+
+// ---------------------------------------------------------------- K0 bounds
+// keys[0..2] = min (atomicMin), keys[3..5] = max (atomicMax), keys[6] = #non-finite
+struct MinMax3 {
+  double lo[3], hi[3];
+  unsigned nonfinite;
+};
+
+__device__ __forceinline__ void mm_point(MinMax3 &m, double x, double y, double z) {
+  const double v[3] = {x, y, z};
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    if (!isfinite(v[c])) m.nonfinite++;
+    m.lo[c] = fmin(m.lo[c], v[c]);
+    m.hi[c] = fmax(m.hi[c], v[c]);
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) bounds_kernel(const T *__restrict__ xyz, int64_t n,
+                                                     unsigned long long *keys) {
+  MinMax3 m;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    m.lo[c] = INFINITY;
+    m.hi[c] = -INFINITY;
+  }
+  m.nonfinite = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if constexpr (sizeof(T) == 4) {
+    // 4 points = 12 floats = 3 x float4 per step (xyz is 16 B aligned)
+    const int64_t groups = n / 4;
+    const float4 *v = reinterpret_cast<const float4 *>(xyz);
+    for (int64_t g = t; g < groups; g += stride) {
+      float4 a = __ldg(v + 3 * g), b = __ldg(v + 3 * g + 1), c = __ldg(v + 3 * g + 2);
+      mm_point(m, a.x, a.y, a.z);
+      mm_point(m, a.w, b.x, b.y);
+      mm_point(m, b.z, b.w, c.x);
+      mm_point(m, c.y, c.z, c.w);
+    }
+    for (int64_t p = groups * 4 + t; p < n; p += stride)
+      mm_point(m, xyz[3 * p], xyz[3 * p + 1], xyz[3 * p + 2]);
+  } else {
+    for (int64_t p = t; p < n; p += stride)
+      mm_point(m, __ldg(xyz + 3 * p), __ldg(xyz + 3 * p + 1), __ldg(xyz + 3 * p + 2));
+  }
+  // warp reduce, then one atomic per warp per component
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      m.lo[c] = fmin(m.lo[c], __shfl_xor_sync(0xffffffffu, m.lo[c], off));
+      m.hi[c] = fmax(m.hi[c], __shfl_xor_sync(0xffffffffu, m.hi[c], off));
+    }
+    m.nonfinite += __shfl_xor_sync(0xffffffffu, m.nonfinite, off);
+  }
+  if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      atomicMin(keys + c, dkey(m.lo[c]));
+      atomicMax(keys + 3 + c, dkey(m.hi[c]));
+    }
+    if (m.nonfinite) atomicAdd(keys + 6, (unsigned long long)m.nonfinite);
+  }
+}
+
+// ------------------------------------------------------- K1+K2 bin/scatter
+struct BinArgs {
+  double x0, y0, z0, r_g, d_s;
+  const double *heights;  // (S,) device
+  int64_t cells;
+  int rows, cols, S;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) scatter_kernel(const T *__restrict__ xyz, int64_t n,
+                                                      BinArgs a, uint32_t *__restrict__ gkey,
+                                                      uint32_t *__restrict__ ckey,
+                                                      unsigned long long *outside) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += stride) {
+    const double x = (double)__ldg(xyz + 3 * p);
+    const double y = (double)__ldg(xyz + 3 * p + 1);
+    const double z = (double)__ldg(xyz + 3 * p + 2);
+    // rasterisation in float64 (tomogram.py:148-149)
+    const double fi = floor((y - a.y0) / a.r_g + 0.5);
+    const double fj = floor((x - a.x0) / a.r_g + 0.5);
+    if (!(fi >= 0.0 && fi < (double)a.rows && fj >= 0.0 && fj < (double)a.cols)) {
+      atomicAdd(outside, 1ull);
+      continue;
+    }
+    const int64_t cell = (int64_t)fi * a.cols + (int64_t)fj;
+    // b = #{k : h_k < z}: estimate from the plane spacing, then fix up
+    // against the exact float64 heights (searchsorted side="right", :157)
+    double est = floor((z - a.z0) / a.d_s);
+    int b = est < 0.0 ? 0 : (est > (double)a.S ? a.S : (int)est);
+    while (b > 0 && __ldg(a.heights + b - 1) >= z) --b;
+    while (b < a.S && __ldg(a.heights + b) < z) ++b;
+    const uint32_t key = f32_key(__double2float_rn(z));
+    if (b < a.S) atomicMax(gkey + (int64_t)b * a.cells + cell, key);
+    if (b > 0) atomicMin(ckey + (int64_t)(b - 1) * a.cells + cell, key);
+  }
+}
+
+// ------------------------------------------------------------- K3 bin scan
+// ground[k] = max(bins 0..k), ceiling[k] = min(bins k+1..S); scratch bin
+// plane k of ckey holds bin k+1.
+__global__ void __launch_bounds__(256) scan_kernel(const uint32_t *__restrict__ gkey,
+                                                   const uint32_t *__restrict__ ckey,
+                                                   int64_t cells, int S,
+                                                   float *__restrict__ ground,
+                                                   float *__restrict__ ceiling) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= cells) return;
+  uint32_t run = kKeyEmptyMax;
+  for (int k = 0; k < S; ++k) {
+    const uint32_t v = __ldcs(gkey + (int64_t)k * cells + c);
+    run = v > run ? v : run;
+    __stcs(ground + (int64_t)k * cells + c, decode_ground(run));
+  }
+  run = kKeyEmptyMin;
+  for (int k = S - 1; k >= 0; --k) {
+    const uint32_t v = __ldcs(ckey + (int64_t)k * cells + c);
+    run = v < run ? v : run;
+    __stcs(ceiling + (int64_t)k * cells + c, decode_ceiling(run));
+  }
+}
+
+int grid_for(pct_ctx *ctx, int64_t work, int block, int per_sm = 8) {
+  int64_t g = (work + block - 1) / block;
+  int64_t cap = (int64_t)ctx->num_sms * per_sm;
+  if (g > cap) g = cap;
+  return (int)(g < 1 ? 1 : g);
+}
+
+}  // namespace
+
+int launch_bounds(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, double lo[3],
+                  double hi[3]) {
+  if (n <= 0) return fail(ctx, PCT_E_EMPTY, "zero valid points");
+  unsigned long long *keys = static_cast<unsigned long long *>(ctx->dsmall);
+  unsigned long long init[7] = {~0ull, ~0ull, ~0ull, 0ull, 0ull, 0ull, 0ull};
+  unsigned long long *hk = static_cast<unsigned long long *>(ctx->hsmall);
+  std::memcpy(hk, init, sizeof(init));
+  PCT_CUDA(ctx, cudaMemcpyAsync(keys, hk, sizeof(init), cudaMemcpyHostToDevice, ctx->stream));
+  const bool aligned = (reinterpret_cast<uintptr_t>(xyz) & 15) == 0;
+  if (dtype == PCT_F32) {
+    if (!aligned) return fail(ctx, PCT_E_INVALID, "xyz must be 16-byte aligned");
+    bounds_kernel<float><<<grid_for(ctx, (n + 3) / 4, 256), 256, 0, ctx->stream>>>(
+        static_cast<const float *>(xyz), n, keys);
+  } else {
+    bounds_kernel<double><<<grid_for(ctx, n, 256), 256, 0, ctx->stream>>>(
+        static_cast<const double *>(xyz), n, keys);
+  }
+  if (int rc = check_launch(ctx, "bounds_kernel")) return rc;
+  PCT_CUDA(ctx, cudaMemcpyAsync(hk, keys, sizeof(init), cudaMemcpyDeviceToHost, ctx->stream));
+  PCT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  if (hk[6]) return fail(ctx, PCT_E_NONFINITE, "point cloud contains non-finite coordinates");
+  for (int c = 0; c < 3; ++c) {
+    lo[c] = dkey_inv(hk[c]);
+    hi[c] = dkey_inv(hk[3 + c]);
+  }
+  return PCT_OK;
+}
+
+int launch_build(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, const pct_frame &fr,
+                 const double *heights_host, float *ground, float *ceiling) {
+  const int S = fr.n_slices;
+  const int64_t cells = (int64_t)fr.rows * fr.cols;
+  const size_t plane = (size_t)cells * sizeof(uint32_t);
+  // scratch: gkey (S planes) | ckey (S planes) | heights (S doubles) | outside counter
+  const size_t hbytes = ((size_t)S * sizeof(double) + 255) & ~(size_t)255;
+  if (int rc = ensure_scratch(ctx, 2 * plane * S + hbytes + 256)) return rc;
+  char *base = static_cast<char *>(ctx->scratch);
+  uint32_t *gkey = reinterpret_cast<uint32_t *>(base);
+  uint32_t *ckey = reinterpret_cast<uint32_t *>(base + plane * S);
+  double *hdev = reinterpret_cast<double *>(base + 2 * plane * S);
+  unsigned long long *outside = reinterpret_cast<unsigned long long *>(base + 2 * plane * S + hbytes);
+  PCT_CUDA(ctx, cudaMemcpyAsync(hdev, heights_host, (size_t)S * sizeof(double),
+                                cudaMemcpyHostToDevice, ctx->stream));
+  PCT_CUDA(ctx, cudaMemsetAsync(gkey, 0x00, plane * S, ctx->stream));
+  PCT_CUDA(ctx, cudaMemsetAsync(ckey, 0xFF, plane * S, ctx->stream));
+  PCT_CUDA(ctx, cudaMemsetAsync(outside, 0, 8, ctx->stream));
+  BinArgs a{fr.origin_x, fr.origin_y, fr.z_min, fr.r_g, fr.d_s, hdev, cells, fr.rows, fr.cols, S};
+  if (n > 0) {
+    if (dtype == PCT_F32)
+      scatter_kernel<float><<<grid_for(ctx, n, 256, 16), 256, 0, ctx->stream>>>(
+          static_cast<const float *>(xyz), n, a, gkey, ckey, outside);
+    else
+      scatter_kernel<double><<<grid_for(ctx, n, 256, 16), 256, 0, ctx->stream>>>(
+          static_cast<const double *>(xyz), n, a, gkey, ckey, outside);
+    if (int rc = check_launch(ctx, "scatter_kernel")) return rc;
+  }
+  scan_kernel<<<(unsigned)((cells + 255) / 256), 256, 0, ctx->stream>>>(gkey, ckey, cells, S,
+                                                                        ground, ceiling);
+  return check_launch(ctx, "scan_kernel");
+}
+
+}  // namespace pct

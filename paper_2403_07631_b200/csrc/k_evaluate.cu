@@ -1,0 +1,414 @@
+// k_evaluate.cu — K4+K5: fused traversability stencil + inflation per slice.
+// Replaces traversability.py:59-236 (interval_cost, slope_magnitudes,
+// gentle_fraction, terrain_cost_values, ground_cost, fuse_costs, inflate,
+// evaluate_slice / evaluate_tomogram).
+//
+// One CTA computes a TH x TW tile of c_T for one slice entirely on chip
+// (DESIGN.md §4.2):
+//   A  ground tile + halo (R + r + 1 cells) -> smem (NaN outside the grid)
+//   B  per cell of the (TH+2R+2r)^2 "gentle" region: gradients, m_xy,
+//      glibc-exact m_grad, isolation, gentle flag; for the (TH+2R)^2 c_init
+//      region also the interval cost and the fused cost, with the foothold
+//      branch marked in the sign bit (its value needs the window count)
+//   C  horizontal gentle counts over 2r+1 columns (u8)
+//   D  vertical sums -> p_s test as an integer threshold -> final c_init
+//   E  weighted max over the (2R+1)^2 kernel taps with zero padding:
+//      max_t fl32(w_t * c_init) (== the reference's per-class max filter,
+//      since x -> fl32(w*x) is monotone for w > 0).  8-fold symmetric
+//      kernels with R <= 4 use a register sliding window of horizontal pair
+//      maxima P_b(i,j) = max(c(i,j-b), c(i,j+b)); others loop over taps.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "pct_internal.h"
+
+namespace pct {
+namespace {
+
+constexpr int kMaxTaps = 125 * 125;
+__constant__ float c_wfull[kMaxTaps];  // generic path: kside x kside weights
+__constant__ float c_wsym[9 * 9];      // symmetric path: w[a][b], a,b in [0, R], stride 9
+__constant__ EvalConsts c_K;
+
+struct TileGeom {
+  int R, r;            // inflation radius, patch radius
+  int TH, TW;          // output tile
+  int CH, CW;          // c_init region = tile + R halo
+  int GH, GW;          // gentle region = c_init region + r halo
+  int LH, LW;          // loaded ground region = gentle region + 1
+  int off_gen, off_hsum, off_cinit, smem;  // byte offsets
+};
+
+TileGeom make_geom(int R, int r, int TH, int TW) {
+  TileGeom g;
+  g.R = R;
+  g.r = r;
+  g.TH = TH;
+  g.TW = TW;
+  g.CH = TH + 2 * R;
+  g.CW = TW + 2 * R;
+  g.GH = g.CH + 2 * r;
+  g.GW = g.CW + 2 * r;
+  g.LH = g.GH + 2;
+  g.LW = g.GW + 2;
+  size_t o = (size_t)g.LH * g.LW * 4;
+  g.off_gen = (int)o;
+  o += ((size_t)g.GH * g.GW + 15) & ~(size_t)15;
+  g.off_hsum = (int)o;
+  o += ((size_t)g.GH * g.CW + 15) & ~(size_t)15;
+  g.off_cinit = (int)o;
+  o += (size_t)g.CH * g.CW * 4;
+  g.smem = (int)o;
+  return g;
+}
+
+// ------------------------------------------------------------ stages A-D
+// mode: kEvalFull (c_T), kEvalCinit (fused cost before inflation),
+// kEvalGroundCost (ground_cost only), kEvalInterval (interval_cost only).
+template <int NT>
+__device__ __forceinline__ void stages_abcd(const TileGeom &G, const float *__restrict__ ground,
+                                            const float *__restrict__ ceiling, int rows, int cols,
+                                            int i0, int j0, int mode, unsigned char *smem) {
+  float *grd = reinterpret_cast<float *>(smem);
+  unsigned char *gen = smem + G.off_gen;
+  unsigned char *hsum = smem + G.off_hsum;
+  float *cinit = reinterpret_cast<float *>(smem + G.off_cinit);
+  const float nanf_ = bits_f32(kNaNBits);
+  const int H = G.R + G.r + 1;
+  const int tid = threadIdx.x;
+
+  // A: ground tile + halo
+  for (int idx = tid; idx < G.LH * G.LW; idx += NT) {
+    const int y = idx / G.LW, x = idx - y * G.LW;
+    const int gi = i0 - H + y, gj = j0 - H + x;
+    float v = nanf_;
+    if (gi >= 0 && gi < rows && gj >= 0 && gj < cols) v = __ldg(ground + (int64_t)gi * cols + gj);
+    grd[idx] = v;
+  }
+  __syncthreads();
+
+  // B: terrain per gentle-region cell; c_init candidates for the inner region
+  const int rr = G.r;
+  for (int idx = tid; idx < G.GH * G.GW; idx += NT) {
+    const int y = idx / G.GW, x = idx - y * G.GW;
+    const int gi = i0 - G.R - rr + y, gj = j0 - G.R - rr + x;
+    const bool in_grid = gi >= 0 && gi < rows && gj >= 0 && gj < cols;
+    const bool in_ci = y >= rr && y < rr + G.CH && x >= rr && x < rr + G.CW;
+    unsigned char gflag = 0;
+    float enc = 0.0f;  // zero padding outside the map (inflate cval=0)
+    if (in_grid) {
+      const float *p = grd + (y + 1) * G.LW + (x + 1);
+      Cross c{p[0], p[-1], p[1], p[-G.LW], p[G.LW]};
+      TerrainCell t = terrain_cell(c, c_K);
+      gflag = t.gentle ? 1 : 0;
+      if (in_ci) {
+        if (mode == kEvalInterval) {
+          enc = t.valid ? interval_value(c.e, __ldg(ceiling + (int64_t)gi * cols + gj), c_K)
+                        : (float)c_K.c_barrier;
+        } else if (mode == kEvalGroundCost) {
+          bool needs_ps = false;
+          if (t.valid) {
+            double tv = t.isolated ? c_K.c_barrier
+                                   : terrain_value(t.m_xy, t.m_grad, c_K, &needs_ps);
+            enc = (float)tv;
+            if (needs_ps) enc = bits_f32(f32_bits(enc) | 0x80000000u);
+          }
+        } else {
+          const float ceil_v = t.valid ? __ldg(ceiling + (int64_t)gi * cols + gj) : nanf_;
+          enc = cinit_encoded(c.e, ceil_v, t, c_K);
+        }
+      }
+    }
+    gen[idx] = gflag;
+    if (in_ci) cinit[(y - rr) * G.CW + (x - rr)] = enc;
+  }
+  __syncthreads();
+
+  // C: horizontal window counts (2r+1 columns) for every gentle-region row
+  const int side = 2 * rr + 1;
+  for (int idx = tid; idx < G.GH * G.CW; idx += NT) {
+    const int y = idx / G.CW, x = idx - y * G.CW;
+    const unsigned char *g = gen + y * G.GW + x;
+    int s = 0;
+    for (int d = 0; d < side; ++d) s += g[d];
+    hsum[idx] = (unsigned char)s;
+  }
+  __syncthreads();
+
+  // D: foothold test p_s > theta_p  <=>  count >= ps_min_count
+  for (int idx = tid; idx < G.CH * G.CW; idx += NT) {
+    const float enc = cinit[idx];
+    if (f32_bits(enc) & 0x80000000u) {
+      const int y = idx / G.CW, x = idx - y * G.CW;
+      int cnt = 0;
+      for (int d = 0; d < side; ++d) cnt += hsum[(y + d) * G.CW + x];
+      cinit[idx] = cinit_resolve(enc, cnt, c_K);
+    }
+  }
+  __syncthreads();
+}
+
+// ------------------------------------------------ stage E, symmetric, R<=4
+// Thread = one output column x of a strip of V rows; register ring of the
+// horizontal pair maxima of 2R+1 consecutive c_init rows.
+template <int R, int V>
+__device__ __forceinline__ void inflate_sym_strip(const float *__restrict__ cinit, int CW,
+                                                  int x, int ys, float *__restrict__ out,
+                                                  int64_t out_stride, int orow0, int ocol,
+                                                  int rows, int cols) {
+  float P[V + 2 * R][R + 1];
+#pragma unroll
+  for (int t = 0; t < V + 2 * R; ++t) {
+    const float *rowp = cinit + (ys + t) * CW + x;  // CI columns x .. x+2R
+    P[t][0] = rowp[R];
+#pragma unroll
+    for (int b = 1; b <= R; ++b) P[t][b] = fmaxf(rowp[R - b], rowp[R + b]);
+    if (t >= 2 * R) {
+      const int o = t - 2 * R;     // output row in strip; centre P row = o + R
+      const int c = o + R;
+      float acc = 0.0f;
+#pragma unroll
+      for (int a = 0; a <= R; ++a) {
+#pragma unroll
+        for (int b = 0; b <= a; ++b) {
+          const float w = c_wsym[a * 9 + b];
+          if (w > 0.0f) {
+            float m;
+            if (a == 0) {
+              m = P[c][0];
+            } else if (b == 0) {
+              m = fmaxf(fmaxf(P[c - a][0], P[c + a][0]), P[c][a]);
+            } else if (a == b) {
+              m = fmaxf(P[c - a][a], P[c + a][a]);
+            } else {
+              m = fmaxf(fmaxf(P[c - a][b], P[c + a][b]), fmaxf(P[c - b][a], P[c + b][a]));
+            }
+            acc = fmaxf(acc, w * m);
+          }
+        }
+      }
+      const int gi = orow0 + o;
+      if (gi < rows && ocol < cols) out[(int64_t)gi * out_stride + ocol] = acc;
+    }
+  }
+}
+
+template <int R, int TH, int TW, int NT>
+__global__ void __launch_bounds__(NT) eval_sym_kernel(TileGeom G, const float *__restrict__ ground,
+                                                      const float *__restrict__ ceiling, int rows,
+                                                      int cols, float *__restrict__ cost) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int64_t plane = (int64_t)rows * cols;
+  const int k = blockIdx.z;
+  const int i0 = blockIdx.y * TH, j0 = blockIdx.x * TW;
+  stages_abcd<NT>(G, ground + k * plane, ceiling + k * plane, rows, cols, i0, j0, kEvalFull,
+                  smem);
+  const float *cinit = reinterpret_cast<const float *>(smem + G.off_cinit);
+  constexpr int STRIPS = NT / TW;
+  constexpr int V = TH / STRIPS;
+  const int x = threadIdx.x % TW, s = threadIdx.x / TW;
+  inflate_sym_strip<R, V>(cinit, G.CW, x, s * V, cost + k * plane, cols, i0 + s * V, j0 + x,
+                          rows, cols);
+}
+
+// --------------------------------------------------- stage E, generic taps
+template <int NT>
+__device__ __forceinline__ void inflate_generic(const TileGeom &G, const float *__restrict__ cinit,
+                                                int kside, float *__restrict__ out, int rows,
+                                                int cols, int i0, int j0) {
+  for (int idx = threadIdx.x; idx < G.TH * G.TW; idx += NT) {
+    const int oy = idx / G.TW, ox = idx - oy * G.TW;
+    const int gi = i0 + oy, gj = j0 + ox;
+    if (gi >= rows || gj >= cols) continue;
+    float acc = 0.0f;
+    for (int m = 0; m < kside; ++m) {
+      const float *rowp = cinit + (oy + m) * G.CW + ox;
+      for (int n = 0; n < kside; ++n) {
+        const float w = c_wfull[m * kside + n];
+        if (w > 0.0f) acc = fmaxf(acc, w * rowp[n]);
+      }
+    }
+    out[(int64_t)gi * cols + gj] = acc;
+  }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) eval_generic_kernel(TileGeom G,
+                                                          const float *__restrict__ ground,
+                                                          const float *__restrict__ ceiling,
+                                                          int rows, int cols, int kside, int mode,
+                                                          float *__restrict__ cost) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int64_t plane = (int64_t)rows * cols;
+  const int k = blockIdx.z;
+  const int i0 = blockIdx.y * G.TH, j0 = blockIdx.x * G.TW;
+  stages_abcd<NT>(G, ground + k * plane, ceiling ? ceiling + k * plane : nullptr, rows, cols, i0,
+                  j0, mode, smem);
+  const float *cinit = reinterpret_cast<const float *>(smem + G.off_cinit);
+  float *out = cost + k * plane;
+  if (mode == kEvalFull) {
+    inflate_generic<NT>(G, cinit, kside, out, rows, cols, i0, j0);
+  } else {
+    for (int idx = threadIdx.x; idx < G.TH * G.TW; idx += NT) {
+      const int oy = idx / G.TW, ox = idx - oy * G.TW;
+      const int gi = i0 + oy, gj = j0 + ox;
+      if (gi < rows && gj < cols) out[(int64_t)gi * cols + gj] = cinit[(oy + G.R) * G.CW + ox + G.R];
+    }
+  }
+}
+
+// standalone inflate (traversability.py:205-213) for the per-op API
+template <int NT>
+__global__ void __launch_bounds__(NT) inflate_kernel(TileGeom G, const float *__restrict__ in,
+                                                     int rows, int cols, int kside,
+                                                     float *__restrict__ out) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  float *cinit = reinterpret_cast<float *>(smem + G.off_cinit);
+  const int i0 = blockIdx.y * G.TH, j0 = blockIdx.x * G.TW;
+  for (int idx = threadIdx.x; idx < G.CH * G.CW; idx += NT) {
+    const int y = idx / G.CW, x = idx - y * G.CW;
+    const int gi = i0 - G.R + y, gj = j0 - G.R + x;
+    cinit[idx] = (gi >= 0 && gi < rows && gj >= 0 && gj < cols) ? __ldg(in + (int64_t)gi * cols + gj)
+                                                                 : 0.0f;
+  }
+  __syncthreads();
+  inflate_generic<NT>(G, cinit, kside, out, rows, cols, i0, j0);
+}
+
+// ---------------------------------------------------------------- host side
+bool symmetric_kernel(const float *w, int kside, int R, float wsym[81]) {
+  if (R > 4) return false;
+  for (int i = 0; i < 81; ++i) wsym[i] = 0.0f;
+  for (int m = 0; m < kside; ++m)
+    for (int n = 0; n < kside; ++n) {
+      int a = std::abs(m - R), b = std::abs(n - R);
+      if (a < b) std::swap(a, b);
+      const float v = w[m * kside + n];
+      float &s = wsym[a * 9 + b];
+      if (m == R + a && n == R + b) s = v;  // canonical representative
+    }
+  for (int m = 0; m < kside; ++m)
+    for (int n = 0; n < kside; ++n) {
+      int a = std::abs(m - R), b = std::abs(n - R);
+      if (a < b) std::swap(a, b);
+      const float v = w[m * kside + n];
+      if (std::memcmp(&v, &wsym[a * 9 + b], 4) != 0) return false;
+    }
+  return true;
+}
+
+int ps_min_count(double theta_p, int radius) {
+  const int side = 2 * radius + 1;
+  const double div = (double)(side * side);
+  for (int c = 0; c <= side * side; ++c)
+    if ((double)c / div > theta_p) return c;
+  return side * side + 1;
+}
+
+constexpr int kNT = 256;
+
+}  // namespace
+
+EvalConsts make_consts(const pct_trav_params &p, double r_g) {
+  EvalConsts K;
+  K.d_min = p.d_min;
+  K.d_ref = p.d_ref;
+  K.theta_b = p.theta_b;
+  K.theta_s = p.theta_s;
+  K.c_barrier = p.c_barrier;
+  K.alpha_d = p.alpha_d;
+  K.alpha_b = p.alpha_b;
+  K.alpha_s = p.alpha_s;
+  K.rg = r_g;
+  K.inv_rg = 1.0 / r_g;
+  K.two_rg = 2.0 * r_g;
+  K.inv_two_rg = 1.0 / K.two_rg;
+  K.inv_theta_b = 1.0 / p.theta_b;
+  K.inv_theta_s = 1.0 / p.theta_s;
+  K.patch_radius = p.patch_radius;
+  K.ps_min_count = ps_min_count(p.theta_p, p.patch_radius);
+  return K;
+}
+
+int launch_evaluate(pct_ctx *ctx, const float *ground, const float *ceiling, int S, int rows,
+                    int cols, double r_g, const pct_trav_params &p, const float *kernel_w,
+                    int kside, float *cost, int mode) {
+  if (S <= 0 || rows <= 0 || cols <= 0) return PCT_OK;
+  if (p.patch_radius < 0 || p.patch_radius > 60)
+    return fail(ctx, PCT_E_INVALID, "patch radius out of supported range [0, 60]");
+  int R = 0;
+  if (mode == kEvalFull) {
+    if (kside <= 0 || (kside & 1) == 0 || kside * kside > kMaxTaps)
+      return fail(ctx, PCT_E_INVALID, "inflation kernel side must be odd and <= 125");
+    R = kside / 2;
+  }
+  EvalConsts K = make_consts(p, r_g);
+  PCT_CUDA(ctx, cudaMemcpyToSymbolAsync(c_K, &K, sizeof(K), 0, cudaMemcpyHostToDevice, ctx->stream));
+  float wsym[81];
+  const bool sym = mode == kEvalFull && symmetric_kernel(kernel_w, kside, R, wsym);
+  if (mode == kEvalFull) {
+    if (sym)
+      PCT_CUDA(ctx, cudaMemcpyToSymbolAsync(c_wsym, wsym, sizeof(wsym), 0, cudaMemcpyHostToDevice,
+                                            ctx->stream));
+    else
+      PCT_CUDA(ctx, cudaMemcpyToSymbolAsync(c_wfull, kernel_w, sizeof(float) * kside * kside, 0,
+                                            cudaMemcpyHostToDevice, ctx->stream));
+  }
+  if (sym && R == 4) {
+    constexpr int TH = 64, TW = 64;
+    TileGeom G = make_geom(4, p.patch_radius, TH, TW);
+    auto kern = eval_sym_kernel<4, TH, TW, kNT>;
+    PCT_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G.smem));
+    dim3 grid((cols + TW - 1) / TW, (rows + TH - 1) / TH, S);
+    kern<<<grid, kNT, G.smem, ctx->stream>>>(G, ground, ceiling, rows, cols, cost);
+    return check_launch(ctx, "eval_sym_kernel<4>");
+  }
+  if (sym && R == 2) {
+    constexpr int TH = 64, TW = 64;
+    TileGeom G = make_geom(2, p.patch_radius, TH, TW);
+    auto kern = eval_sym_kernel<2, TH, TW, kNT>;
+    PCT_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G.smem));
+    dim3 grid((cols + TW - 1) / TW, (rows + TH - 1) / TH, S);
+    kern<<<grid, kNT, G.smem, ctx->stream>>>(G, ground, ceiling, rows, cols, cost);
+    return check_launch(ctx, "eval_sym_kernel<2>");
+  }
+  // generic path: pick the largest square-ish tile that fits in shared memory
+  int TH = 64, TW = 64;
+  TileGeom G = make_geom(R, p.patch_radius, TH, TW);
+  while (G.smem > 200 * 1024 && (TH > 8 || TW > 8)) {
+    if (TH >= TW) TH /= 2; else TW /= 2;
+    G = make_geom(R, p.patch_radius, TH, TW);
+  }
+  if (G.smem > 220 * 1024) return fail(ctx, PCT_E_INVALID, "stencil radius too large for one tile");
+  auto kern = eval_generic_kernel<kNT>;
+  PCT_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G.smem));
+  dim3 grid((cols + TW - 1) / TW, (rows + TH - 1) / TH, S);
+  kern<<<grid, kNT, G.smem, ctx->stream>>>(G, ground, ceiling, rows, cols, kside, mode, cost);
+  return check_launch(ctx, "eval_generic_kernel");
+}
+
+int launch_inflate(pct_ctx *ctx, const float *in, int rows, int cols, const float *kernel_w,
+                   int kside, float *out) {
+  if (rows <= 0 || cols <= 0) return PCT_OK;
+  if (kside <= 0 || (kside & 1) == 0 || kside * kside > kMaxTaps)
+    return fail(ctx, PCT_E_INVALID, "inflation kernel side must be odd and <= 125");
+  PCT_CUDA(ctx, cudaMemcpyToSymbolAsync(c_wfull, kernel_w, sizeof(float) * kside * kside, 0,
+                                        cudaMemcpyHostToDevice, ctx->stream));
+  int TH = 32, TW = 32;
+  TileGeom G = make_geom(kside / 2, 0, TH, TW);
+  while (G.smem > 200 * 1024 && (TH > 8 || TW > 8)) {
+    if (TH >= TW) TH /= 2; else TW /= 2;
+    G = make_geom(kside / 2, 0, TH, TW);
+  }
+  auto kern = inflate_kernel<kNT>;
+  PCT_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G.smem));
+  dim3 grid((cols + TW - 1) / TW, (rows + TH - 1) / TH, 1);
+  kern<<<grid, kNT, G.smem, ctx->stream>>>(G, in, rows, cols, kside, out);
+  return check_launch(ctx, "inflate_kernel");
+}
+
+}  // namespace pct

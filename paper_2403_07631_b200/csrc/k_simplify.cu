@@ -1,0 +1,254 @@
+// k_simplify.cu — K6: redundant-slice simplification (simplify.py:18-73).
+//
+// The reference sweeps forward over the slice list, removing a slice when no
+// cell is "unique" w.r.t. its current lower and upper neighbours, and repeats
+// until a pass removes nothing.  The per-check work is an any() over all
+// cells of (trav & side(below) & side(above)); the sweep order is inherently
+// sequential, so the device computes the any()s in bulk and the host replays
+// the exact sweep:
+//
+//  * window_kernel: one pass over every cell computes, for each slice k and
+//    each lower neighbour a in {none, k-1, ..., k-32}, whether any cell is
+//    unique for the triple (a, k, k+1) — every check of the first pass whose
+//    removal chain is < 32 long (the upper neighbour of pass 1 is always the
+//    original k+1).  Each thread owns a cell and keeps its last 32 slices'
+//    (ground, cost) in a shared-memory ring; per k the block ORs a 64-bit mask.
+//  * triples_kernel: any() for an explicit batch of (below, k, above)
+//    triples — later passes and long chains; the host batches the remainder
+//    of the pass speculatively (no further removals), blocks exit early once
+//    a triple is known unique.
+#include <cuda_runtime.h>
+
+#include <map>
+#include <tuple>
+#include <vector>
+
+#include "pct_internal.h"
+
+namespace pct {
+namespace {
+
+constexpr int kWin = 32;      // lower-neighbour window of window_kernel
+constexpr int kBit = 32;      // bit index for "no lower neighbour"
+constexpr int kWinNT = 128;
+
+struct SimpArgs {
+  const float *ground;
+  const float *cost;
+  int64_t cells;
+  int S;
+  double eps_e;
+  float c_barrier32;  // numpy compares float32 costs with the weak Python scalar in float32
+};
+
+// side condition of simplify.py:18-28 for a valid, traversable cell
+__device__ __forceinline__ bool not_covered(float e, float cst, float enb, float cnb, double eps,
+                                            bool lower) {
+  if (!finite32(enb)) return true;
+  const double a = (double)e, b = (double)enb;
+  const bool higher = lower ? (a - b > eps) : (b - a > eps);
+  return higher || (cst < cnb);
+}
+
+__global__ void __launch_bounds__(kWinNT) window_kernel(SimpArgs A,
+                                                        unsigned long long *__restrict__ table) {
+  __shared__ float ring_e[kWin][kWinNT];
+  __shared__ float ring_c[kWin][kWinNT];
+  __shared__ unsigned long long bmask;
+  const int64_t cell = (int64_t)blockIdx.x * kWinNT + threadIdx.x;
+  const bool live = cell < A.cells;
+  float e_cur = 0.f, c_cur = 0.f;
+  if (live) {
+    e_cur = __ldg(A.ground + cell);
+    c_cur = __ldg(A.cost + cell);
+  }
+  for (int k = 0; k < A.S; ++k) {
+    float e_up = bits_f32(kNaNBits), c_up = 0.f;
+    if (live && k + 1 < A.S) {
+      e_up = __ldg(A.ground + (int64_t)(k + 1) * A.cells + cell);
+      c_up = __ldg(A.cost + (int64_t)(k + 1) * A.cells + cell);
+    }
+    unsigned long long m = 0;
+    if (live && finite32(e_cur) && c_cur < A.c_barrier32 &&
+        (k + 1 >= A.S || not_covered(e_cur, c_cur, e_up, c_up, A.eps_e, false))) {
+      m = 1ull << kBit;
+      const int depth = k < kWin ? k : kWin;
+      for (int j = 0; j < depth; ++j) {  // a = k-1-j
+        const int slot = (k - 1 - j) % kWin;
+        if (not_covered(e_cur, c_cur, ring_e[slot][threadIdx.x], ring_c[slot][threadIdx.x],
+                        A.eps_e, true))
+          m |= 1ull << j;
+      }
+    }
+    // block OR
+    unsigned lo = __reduce_or_sync(0xffffffffu, (unsigned)m);
+    unsigned hi = __reduce_or_sync(0xffffffffu, (unsigned)(m >> 32));
+    if (threadIdx.x == 0) bmask = 0;
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0 && (lo | hi))
+      atomicOr(&bmask, ((unsigned long long)hi << 32) | lo);
+    ring_e[k % kWin][threadIdx.x] = e_cur;
+    ring_c[k % kWin][threadIdx.x] = c_cur;
+    __syncthreads();
+    if (threadIdx.x == 0 && bmask) atomicOr(table + k, bmask);
+    __syncthreads();
+    e_cur = e_up;
+    c_cur = c_up;
+  }
+}
+
+struct Triple {
+  int below, k, above;
+};
+
+__global__ void __launch_bounds__(256) triples_kernel(SimpArgs A, const Triple *__restrict__ tr,
+                                                      int *__restrict__ flags) {
+  const int t = blockIdx.y;
+  __shared__ int skip;
+  if (threadIdx.x == 0) skip = *((volatile int *)(flags + t));  // already known unique
+  __syncthreads();
+  if (skip) return;
+  const Triple T = tr[t];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  bool any = false;
+  for (int64_t cell = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; cell < A.cells && !any;
+       cell += stride) {
+    const float e = __ldg(A.ground + (int64_t)T.k * A.cells + cell);
+    const float c = __ldg(A.cost + (int64_t)T.k * A.cells + cell);
+    if (!(finite32(e) && c < A.c_barrier32)) continue;
+    bool u = true;
+    if (T.below >= 0)
+      u = not_covered(e, c, __ldg(A.ground + (int64_t)T.below * A.cells + cell),
+                      __ldg(A.cost + (int64_t)T.below * A.cells + cell), A.eps_e, true);
+    if (u && T.above >= 0)
+      u = not_covered(e, c, __ldg(A.ground + (int64_t)T.above * A.cells + cell),
+                      __ldg(A.cost + (int64_t)T.above * A.cells + cell), A.eps_e, false);
+    any = u;
+  }
+  if (__syncthreads_or(any) && threadIdx.x == 0) atomicOr(flags + t, 1);
+}
+
+__global__ void __launch_bounds__(256) unique_mask_kernel(SimpArgs A, Triple T,
+                                                          unsigned char *__restrict__ mask) {
+  const int64_t cell = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (cell >= A.cells) return;
+  const float e = __ldg(A.ground + (int64_t)T.k * A.cells + cell);
+  const float c = __ldg(A.cost + (int64_t)T.k * A.cells + cell);
+  bool u = finite32(e) && c < A.c_barrier32;
+  if (u && T.below >= 0)
+    u = not_covered(e, c, __ldg(A.ground + (int64_t)T.below * A.cells + cell),
+                    __ldg(A.cost + (int64_t)T.below * A.cells + cell), A.eps_e, true);
+  if (u && T.above >= 0)
+    u = not_covered(e, c, __ldg(A.ground + (int64_t)T.above * A.cells + cell),
+                    __ldg(A.cost + (int64_t)T.above * A.cells + cell), A.eps_e, false);
+  mask[cell] = u ? 1 : 0;
+}
+
+}  // namespace
+
+int launch_unique_mask(pct_ctx *ctx, const float *ground, const float *cost, int rows, int cols,
+                       int k, int below, int above, double eps_e, double c_barrier,
+                       uint8_t *mask) {
+  SimpArgs A{ground, cost, (int64_t)rows * cols, 0, eps_e, (float)c_barrier};
+  if (A.cells == 0) return PCT_OK;
+  unique_mask_kernel<<<(unsigned)((A.cells + 255) / 256), 256, 0, ctx->stream>>>(
+      A, Triple{below, k, above}, mask);
+  return check_launch(ctx, "unique_mask_kernel");
+}
+
+int run_simplify(pct_ctx *ctx, const float *ground, const float *cost, int S, int rows, int cols,
+                 double eps_e, double c_barrier, std::vector<int> &keep) {
+  keep.clear();
+  for (int k = 0; k < S; ++k) keep.push_back(k);
+  if (S <= 1) return PCT_OK;
+  SimpArgs A{ground, cost, (int64_t)rows * cols, S, eps_e, (float)c_barrier};
+  // device small buffer layout: table[S] u64 | triples | flags
+  const size_t tbytes = (size_t)S * 8;
+  const size_t need = tbytes + (size_t)S * sizeof(Triple) + (size_t)S * sizeof(int) + 64;
+  if (need > 65536) {
+    if (int rc = ensure_scratch(ctx, need)) return rc;
+  }
+  char *dbase = static_cast<char *>(need > 65536 ? ctx->scratch : ctx->dsmall);
+  unsigned long long *table = reinterpret_cast<unsigned long long *>(dbase);
+  Triple *dtr = reinterpret_cast<Triple *>(dbase + tbytes);
+  int *dflags = reinterpret_cast<int *>(dbase + tbytes + (size_t)S * sizeof(Triple));
+
+  std::vector<unsigned long long> htable(S, 0);
+  PCT_CUDA(ctx, cudaMemsetAsync(table, 0, tbytes, ctx->stream));
+  window_kernel<<<(unsigned)((A.cells + kWinNT - 1) / kWinNT), kWinNT, 0, ctx->stream>>>(A, table);
+  if (int rc = check_launch(ctx, "window_kernel")) return rc;
+  PCT_CUDA(ctx, cudaMemcpyAsync(htable.data(), table, tbytes, cudaMemcpyDeviceToHost, ctx->stream));
+  PCT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+
+  std::map<std::tuple<int, int, int>, bool> cache;
+  auto from_window = [&](int below, int k, int above, bool *hit) -> bool {
+    *hit = false;
+    const bool above_ok = (above == k + 1) || (above < 0 && k == S - 1);
+    if (!above_ok) return false;
+    int bit = -1;
+    if (below < 0) bit = kBit;
+    else if (k - 1 - below < kWin) bit = k - 1 - below;
+    if (bit < 0) return false;
+    *hit = true;
+    return (htable[k] >> bit) & 1ull;
+  };
+  int blocks_x = ctx->num_sms * 2;
+  auto batch = [&](const std::vector<Triple> &ts) -> int {
+    if (ts.empty()) return PCT_OK;
+    const int T = (int)ts.size();
+    PCT_CUDA(ctx, cudaMemcpyAsync(dtr, ts.data(), sizeof(Triple) * T, cudaMemcpyHostToDevice,
+                                  ctx->stream));
+    PCT_CUDA(ctx, cudaMemsetAsync(dflags, 0, sizeof(int) * T, ctx->stream));
+    int64_t bx = (A.cells + 255) / 256;
+    if (bx > blocks_x) bx = blocks_x;
+    triples_kernel<<<dim3((unsigned)bx, T), 256, 0, ctx->stream>>>(A, dtr, dflags);
+    if (int rc = check_launch(ctx, "triples_kernel")) return rc;
+    std::vector<int> hf(T);
+    PCT_CUDA(ctx, cudaMemcpyAsync(hf.data(), dflags, sizeof(int) * T, cudaMemcpyDeviceToHost,
+                                  ctx->stream));
+    PCT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    for (int i = 0; i < T; ++i) cache[{ts[i].below, ts[i].k, ts[i].above}] = hf[i] != 0;
+    return PCT_OK;
+  };
+
+  // replay of simplify.py:59-70
+  for (;;) {
+    bool removed = false;
+    size_t p = 0;
+    while (p < keep.size()) {
+      if (keep.size() > 1) {
+        const int k = keep[p];
+        const int below = p > 0 ? keep[p - 1] : -1;
+        const int above = p + 1 < keep.size() ? keep[p + 1] : -1;
+        bool hit;
+        bool uniq = from_window(below, k, above, &hit);
+        if (!hit) {
+          auto it = cache.find({below, k, above});
+          if (it == cache.end()) {
+            // speculate: the rest of this pass with no further removals
+            std::vector<Triple> ts;
+            for (size_t q = p; q < keep.size() && (int)ts.size() < S; ++q) {
+              Triple t{q > 0 ? keep[q - 1] : -1, keep[q], q + 1 < keep.size() ? keep[q + 1] : -1};
+              bool h2;
+              from_window(t.below, t.k, t.above, &h2);
+              if (!h2 && !cache.count({t.below, t.k, t.above})) ts.push_back(t);
+            }
+            if (int rc = batch(ts)) return rc;
+            it = cache.find({below, k, above});
+          }
+          uniq = it->second;
+        }
+        if (!uniq) {
+          keep.erase(keep.begin() + p);
+          removed = true;
+          continue;
+        }
+      }
+      ++p;
+    }
+    if (!removed) break;
+  }
+  return PCT_OK;
+}
+
+}  // namespace pct

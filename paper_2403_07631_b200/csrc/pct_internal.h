@@ -1,0 +1,74 @@
+// pct_internal.h — context, device tomogram and kernel launchers shared by
+// the translation units of libpct.so (not part of the public ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/pct.h"
+#include "cellmath.cuh"
+
+struct pct_ctx {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  int64_t launches = 0;
+  // grow-only device scratch (build keys, staging of host points)
+  void *scratch = nullptr;
+  size_t scratch_bytes = 0;
+  void *staging = nullptr;  // device copy of host xyz
+  size_t staging_bytes = 0;
+  // small device/pinned buffers for reductions and flags
+  void *dsmall = nullptr;   // 64 KiB device
+  void *hsmall = nullptr;   // 64 KiB pinned host
+};
+
+struct pct_tomo {
+  pct_frame fr{};
+  std::vector<double> heights;
+  float *ground = nullptr;   // (S, rows, cols)
+  float *ceiling = nullptr;
+  float *cost = nullptr;     // nullptr until evaluated
+};
+
+namespace pct {
+
+int fail(pct_ctx *ctx, int code, const std::string &msg);
+int cuda_fail(pct_ctx *ctx, cudaError_t e, const char *what);
+int ensure_scratch(pct_ctx *ctx, size_t bytes);
+int ensure_staging(pct_ctx *ctx, size_t bytes);
+int check_launch(pct_ctx *ctx, const char *what);
+
+#define PCT_CUDA(ctx, call)                                  \
+  do {                                                       \
+    cudaError_t e_ = (call);                                 \
+    if (e_ != cudaSuccess) return pct::cuda_fail(ctx, e_, #call); \
+  } while (0)
+
+// stage launchers (return PCT_OK or error code)
+int launch_bounds(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, double lo[3],
+                  double hi[3]);
+int launch_build(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, const pct_frame &fr,
+                 const double *heights_host, float *ground, float *ceiling);
+int launch_evaluate(pct_ctx *ctx, const float *ground, const float *ceiling, int S, int rows,
+                    int cols, double r_g, const pct_trav_params &p, const float *kernel_w,
+                    int kside, float *cost, int mode);
+int launch_inflate(pct_ctx *ctx, const float *cost, int rows, int cols, const float *kernel_w,
+                   int kside, float *out);
+int run_simplify(pct_ctx *ctx, const float *ground, const float *cost, int S, int rows,
+                 int cols, double eps_e, double c_barrier, std::vector<int> &keep);
+int launch_unique_mask(pct_ctx *ctx, const float *ground, const float *cost, int rows, int cols,
+                       int k, int below, int above, double eps_e, double c_barrier,
+                       uint8_t *mask);
+
+EvalConsts make_consts(const pct_trav_params &p, double r_g);
+
+// evaluate modes for the per-op entry points
+enum EvalMode { kEvalFull = 0, kEvalGroundCost = 1, kEvalInterval = 2, kEvalCinit = 3 };
+
+}  // namespace pct

@@ -1,0 +1,358 @@
+"""Tomogram types and the device build (drop-in for tomoplan/tomogram.py:22-213).
+
+``build_tomogram`` keeps the reference signature (tomogram.py:127-128) and
+returns the same object model (Tomogram / TomogramSlice / Layer with
+(rows, cols) float32 values, NaN = invalid).  The stacks stay resident on the
+GPU; ``Layer.values`` is materialised on the host on first access (one
+device-to-host copy of that slice), so a build -> evaluate -> simplify chain
+only ever moves the surviving slices to the host.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import weakref
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .cloud import PointCloud
+
+GRID_SIDE_LIMIT = 16384
+
+
+class GridSizeError(ValueError):
+    """Grid dimensions exceed the configured safety limit."""
+
+
+# ---------------------------------------------------------------------------
+# device-resident layer stacks
+
+class DeviceStack:
+    """A (S, rows, cols) float32 stack in device memory.
+
+    ``owner`` keeps the allocation alive (a DeviceTomogram or DeviceBuffer).
+    Host copies of individual slices are made on demand and cached.
+    """
+
+    def __init__(self, ctx, ptr: int, n_slices: int, rows: int, cols: int, owner):
+        self.ctx = ctx
+        self.ptr = int(ptr)
+        self.n_slices = int(n_slices)
+        self.rows = int(rows)
+        self.cols = int(cols)
+        self.owner = owner
+        self._host = {}
+
+    @property
+    def plane_bytes(self) -> int:
+        return self.rows * self.cols * 4
+
+    def slice_ptr(self, k: int) -> int:
+        return self.ptr + int(k) * self.plane_bytes
+
+    def host_slice(self, k: int) -> np.ndarray:
+        a = self._host.get(k)
+        if a is None:
+            a = _lib.pinned_pool(self.ctx).array((self.rows, self.cols), np.float32)
+            with self.ctx.lock:
+                self.ctx.check(self.ctx.lib.pct_memcpy_d2h(self.ctx.h, a.ctypes.data,
+                                                           self.slice_ptr(k), a.nbytes), "d2h")
+            self._host[k] = a
+        return a
+
+    def prefetch(self, ks) -> None:
+        """Copy several slices to (pinned) host memory with one synchronisation."""
+        todo = [k for k in dict.fromkeys(ks) if k not in self._host]
+        if not todo:
+            return
+        pool = _lib.pinned_pool(self.ctx)
+        with self.ctx.lock:
+            for k in todo:
+                a = pool.array((self.rows, self.cols), np.float32)
+                self.ctx.check(self.ctx.lib.pct_memcpy_d2h_async(self.ctx.h, a.ctypes.data,
+                                                                 self.slice_ptr(k), a.nbytes),
+                               "d2h")
+                self._host[k] = a
+            self.ctx.check(self.ctx.lib.pct_sync(self.ctx.h), "sync")
+
+    def host_all(self) -> np.ndarray:
+        out = np.empty((self.n_slices, self.rows, self.cols), np.float32)
+        with self.ctx.lock:
+            self.ctx.check(self.ctx.lib.pct_memcpy_d2h(self.ctx.h, out.ctypes.data, self.ptr,
+                                                       out.nbytes), "d2h")
+        for k in range(self.n_slices):
+            self._host.setdefault(k, out[k])
+        return out
+
+
+class DeviceTomogram:
+    """Owner of a pct_tomo (ground + ceiling stacks built on the device)."""
+
+    def __init__(self, ctx, handle):
+        self.ctx = ctx
+        self.handle = handle
+        fr = _lib.FrameC()
+        ctx.check(ctx.lib.pct_tomo_frame(handle, C.byref(fr), None, 0), "frame")
+        self.frame = fr
+        h = np.empty(max(fr.n_slices, 1), np.float64)
+        ctx.check(ctx.lib.pct_tomo_frame(handle, C.byref(fr), h.ctypes.data, fr.n_slices), "frame")
+        self.heights = h[:fr.n_slices]
+        self.ground = DeviceStack(ctx, ctx.lib.pct_tomo_layer(handle, _lib.LAYER_GROUND),
+                                  fr.n_slices, fr.rows, fr.cols, self)
+        self.ceiling = DeviceStack(ctx, ctx.lib.pct_tomo_layer(handle, _lib.LAYER_CEILING),
+                                   fr.n_slices, fr.rows, fr.cols, self)
+        weakref.finalize(self, ctx.lib.pct_tomo_free, ctx.h, handle)
+
+
+def new_device_stack(ctx, n_slices, rows, cols) -> DeviceStack:
+    buf = _lib.DeviceBuffer(ctx, max(1, n_slices * rows * cols * 4))
+    return DeviceStack(ctx, buf.ptr, n_slices, rows, cols, buf)
+
+
+def upload_stack(ctx, arrays) -> DeviceStack:
+    a = np.ascontiguousarray(np.stack([np.asarray(v, np.float32) for v in arrays]))
+    buf = _lib.DeviceBuffer.from_host(ctx, a)
+    return DeviceStack(ctx, buf.ptr, a.shape[0], a.shape[1], a.shape[2], buf)
+
+
+# ---------------------------------------------------------------------------
+# the reference object model (tomogram.py:29-96)
+
+class Layer:
+    """Dense 2D elevation grid; NaN = invalid. Row i follows y, column j follows x.
+
+    ``values`` is a (rows, cols) float32 numpy array; for layers produced on
+    the GPU it is copied from device memory on first access.
+    """
+
+    __slots__ = ("_values", "_stack", "_k", "resolution", "origin")
+
+    def __init__(self, values, resolution: float, origin):
+        self._stack = None
+        self._k = -1
+        self._values = np.asarray(values, dtype=np.float32)
+        if self._values.ndim != 2 or min(self._values.shape) < 1:
+            raise ValueError("layer grid must be 2D and non-empty")
+        if resolution <= 0:
+            raise ValueError("resolution must be positive")
+        self.resolution = resolution
+        self.origin = origin
+
+    @classmethod
+    def on_device(cls, stack: DeviceStack, k: int, resolution: float, origin) -> "Layer":
+        self = cls.__new__(cls)
+        self._values = None
+        self._stack = stack
+        self._k = int(k)
+        self.resolution = resolution
+        self.origin = origin
+        return self
+
+    @property
+    def values(self) -> np.ndarray:
+        if self._values is None:
+            self._values = self._stack.host_slice(self._k)
+        return self._values
+
+    @values.setter
+    def values(self, v):
+        self._values = np.asarray(v, dtype=np.float32)
+        self._stack = None
+        self._k = -1
+
+    @property
+    def device(self):
+        """(DeviceStack, slice index) when the layer lives on the GPU, else None."""
+        return (self._stack, self._k) if self._stack is not None else None
+
+    @property
+    def shape(self):
+        if self._values is None:
+            return (self._stack.rows, self._stack.cols)
+        return self._values.shape
+
+    @property
+    def valid(self) -> np.ndarray:
+        return np.isfinite(self.values)
+
+    def like(self, values: np.ndarray) -> "Layer":
+        return Layer(values, self.resolution, self.origin)
+
+    def __repr__(self):
+        where = "device" if self._values is None else "host"
+        return (f"Layer(shape={self.shape}, resolution={self.resolution!r}, "
+                f"origin={self.origin!r}, {where})")
+
+
+@dataclass
+class TomogramSlice:
+    ground: Layer
+    ceiling: Layer
+    plane_height: float
+    index: int
+    cost: Layer | None = None
+
+
+@dataclass
+class Tomogram:
+    slices: list
+    d_s: float
+    z_min: float
+
+    @property
+    def rows(self):
+        return self.slices[0].ground.shape[0]
+
+    @property
+    def cols(self):
+        return self.slices[0].ground.shape[1]
+
+    @property
+    def resolution(self):
+        return self.slices[0].ground.resolution
+
+    @property
+    def origin(self):
+        return self.slices[0].ground.origin
+
+    def materialize(self) -> "Tomogram":
+        """Copy every device-resident layer to host memory with one
+        synchronisation per stack (``Layer.values`` then costs nothing)."""
+        groups = {}
+        for s in self.slices:
+            for l in (s.ground, s.ceiling, s.cost):
+                if isinstance(l, Layer) and l._values is None and l._stack is not None:
+                    groups.setdefault(id(l._stack), (l._stack, []))[1].append(l._k)
+        for stack, ks in groups.values():
+            stack.prefetch(ks)
+        return self
+
+    def _stack(self, attr):
+        layers = [getattr(s, attr) for s in self.slices]
+        src = device_run(layers)
+        if src is not None and src[1] == 0 and src[0].n_slices == len(layers):
+            return src[0].host_all()
+        return np.stack([l.values for l in layers])
+
+    def ground_stack(self) -> np.ndarray:
+        return self._stack("ground")
+
+    def ceiling_stack(self) -> np.ndarray:
+        return self._stack("ceiling")
+
+    def cost_stack(self) -> np.ndarray:
+        if any(s.cost is None for s in self.slices):
+            raise ValueError("tomogram has no cost layers; run evaluate_tomogram first")
+        return self._stack("cost")
+
+
+def device_run(layers):
+    """(stack, first) if the layers are consecutive slices first.. of one
+    device stack (still un-modified on the host side), else None."""
+    if not layers:
+        return None
+    d0 = layers[0].device if isinstance(layers[0], Layer) else None
+    if d0 is None:
+        return None
+    stack, first = d0
+    for n, l in enumerate(layers):
+        d = l.device if isinstance(l, Layer) else None
+        if d is None or d[0] is not stack or d[1] != first + n:
+            return None
+    return stack, first
+
+
+# ---------------------------------------------------------------------------
+# build (tomogram.py:99-213)
+
+def rasterize_index(p, origin, r_g: float, shape=None):
+    """Map a point to (row, col) with the nearest-cell-center convention.
+
+    i = floor((y - y0) / r_g + 0.5), j = floor((x - x0) / r_g + 0.5)
+    (tomogram.py:99-112).  With `shape` given, indices outside the grid raise
+    IndexError.  Scalar host helper (not on the hot path).
+    """
+    if r_g <= 0:
+        raise ValueError("r_g must be positive")
+    x, y = float(p[0]), float(p[1])
+    i = math.floor((y - origin[1]) / r_g + 0.5)
+    j = math.floor((x - origin[0]) / r_g + 0.5)
+    if shape is not None and not (0 <= i < shape[0] and 0 <= j < shape[1]):
+        raise IndexError(f"point ({x}, {y}) rasterizes to ({i}, {j}), outside grid {shape}")
+    return i, j
+
+
+def _dtype_code(arr: np.ndarray) -> int:
+    if arr.dtype == np.float32:
+        return _lib.PCT_F32
+    if arr.dtype == np.float64:
+        return _lib.PCT_F64
+    raise TypeError(f"unsupported point dtype {arr.dtype}")
+
+
+def device_bounds(xyz: np.ndarray, device=None):
+    """Exact float64 (min, max) corners computed on the GPU (cloud_io.py:47-50)."""
+    ctx = _lib.context(device)
+    a = np.ascontiguousarray(xyz)
+    buf = _lib.DeviceBuffer.from_host(ctx, a)
+    lo = np.empty(3, np.float64)
+    hi = np.empty(3, np.float64)
+    with ctx.lock:
+        rc = ctx.lib.pct_bounds(ctx.h, buf.ptr, a.shape[0], _dtype_code(a), lo.ctypes.data,
+                                hi.ctypes.data)
+        if rc == _lib.PCT_E_NONFINITE:
+            raise ValueError("point cloud contains non-finite coordinates")
+        ctx.check(rc, "pct_bounds")
+    return lo, hi
+
+
+def build_from_points(xyz, d_s: float, r_g: float, max_grid_side: int = GRID_SIDE_LIMIT,
+                      device=None, on_device: bool = False, n_points: int | None = None,
+                      dtype=None) -> Tomogram:
+    """Build from an (N, 3) float32/float64 array (host numpy, or a raw device
+    pointer with ``on_device=True`` plus ``n_points`` and ``dtype``)."""
+    if d_s <= 0 or r_g <= 0:
+        raise ValueError("d_s and r_g must be positive")
+    ctx = _lib.context(device)
+    if on_device:
+        ptr, n, code = int(xyz), int(n_points), _dtype_code(np.empty(0, dtype))
+    else:
+        a = np.ascontiguousarray(xyz)
+        ptr, n, code = a.ctypes.data, a.shape[0], _dtype_code(a)
+    h = C.c_void_p()
+    with ctx.lock:
+        rc = ctx.lib.pct_tomo_build(ctx.h, ptr, n, code, 0 if on_device else 1, float(d_s),
+                                    float(r_g), int(max_grid_side), C.byref(h))
+        if rc == _lib.PCT_E_GRID:
+            raise GridSizeError(ctx.error())
+        if rc == _lib.PCT_E_EMPTY:
+            from .cloud import CloudFormatError
+            raise CloudFormatError(ctx.error())
+        if rc in (_lib.PCT_E_INVALID, _lib.PCT_E_NONFINITE):
+            raise ValueError(ctx.error())
+        ctx.check(rc, "pct_tomo_build")
+    dt = DeviceTomogram(ctx, h)
+    fr = dt.frame
+    origin = (float(fr.origin_x), float(fr.origin_y))
+    slices = [TomogramSlice(ground=Layer.on_device(dt.ground, k, r_g, origin),
+                            ceiling=Layer.on_device(dt.ceiling, k, r_g, origin),
+                            plane_height=float(dt.heights[k]), index=k)
+              for k in range(fr.n_slices)]
+    return Tomogram(slices=slices, d_s=float(d_s), z_min=float(fr.z_min))
+
+
+def build_tomogram(cloud: PointCloud, d_s: float, r_g: float, threads: int = 1,
+                   max_grid_side: int = GRID_SIDE_LIMIT, *, device=None) -> Tomogram:
+    """Project the cloud onto planes at z_min + (k+1)*d_s and build all slices.
+
+    Drop-in for tomogram.py:127-213 (same arguments, errors and results,
+    bit-identical layers).  ``threads`` is accepted and ignored: the work
+    runs on the GPU ``device`` (default: $PCT_DEVICE or 0).
+    """
+    if d_s <= 0 or r_g <= 0:
+        raise ValueError("d_s and r_g must be positive")
+    xyz = cloud.xyz if hasattr(cloud, "xyz") else np.asarray(cloud)
+    return build_from_points(xyz, d_s, r_g, max_grid_side, device=device)

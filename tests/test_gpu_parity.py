@@ -1,0 +1,272 @@
+"""GPU parity: the sm_100a path (through libpct's C ABI) against the reference's
+recorded outputs (tests/golden) and the pinned CPU oracle.
+
+Bars (BASELINE.json north_star): ground / ceiling / slice set bit-exact; costs
+are compared bit-exact too (stricter than the 1e-5 relative tolerance the
+north_star allows) and the traversable classification identical.
+"""
+
+import numpy as np
+import pytest
+
+import oracle
+from golden_util import TABLE_PARAMS, case_arrays, case_input, digest
+
+pytestmark = pytest.mark.gpu
+
+pct = pytest.importorskip("paper_2403_07631_b200")
+
+COST_RTOL = 1e-5  # north_star tolerance; the checks below demand exact equality first
+
+
+def _run(xyz, d_s, r_g):
+    cloud = pct.PointCloud(xyz)
+    tom = pct.build_tomogram(cloud, d_s, r_g)
+    ev = pct.evaluate_tomogram(tom, pct.TravParams())
+    simp = pct.simplify_tomogram(ev)
+    return tom, ev, simp
+
+
+def _assert_layers_equal(got, want, what):
+    assert got.shape == want.shape, what
+    if not np.array_equal(got, want, equal_nan=True):
+        bad = ~((got == want) | (np.isnan(got) & np.isnan(want)))
+        k, i, j = np.argwhere(bad)[0]
+        raise AssertionError(f"{what}: {bad.sum()} cells differ, first at slice {k} "
+                             f"({i},{j}): got {got[k, i, j]!r} want {want[k, i, j]!r}")
+
+
+GOLDEN_CASES = ["ref_random_multilayer_s9", "ref_flat_plane_s7", "ref_spiral_s3",
+                "ref_ramp_over_tunnel_s6", "synth_cfg0", "synth_cfg4", "synth_two_storey_small",
+                "synth_cfg1", "synth_cfg2_n2000000"]
+
+
+@pytest.mark.parametrize("name", GOLDEN_CASES)
+def test_pipeline_matches_reference_golden(golden, name):
+    case = golden["cases"][name]
+    xyz = case_input(name, case)
+    tom, ev, simp = _run(xyz, case["d_s"], case["r_g"])
+    assert [s.plane_height for s in tom.slices] == case["heights"]
+    assert list(tom.origin) == case["origin"] and tom.z_min == case["z_min"]
+    g, c, cost = ev.ground_stack(), ev.ceiling_stack(), ev.cost_stack()
+    assert list(g.shape) == case["shape"]
+    arrays = case_arrays(case)
+    if arrays is not None and "ground" in arrays:
+        _assert_layers_equal(g, arrays["ground"], "ground")
+        _assert_layers_equal(c, arrays["ceiling"], "ceiling")
+        _assert_layers_equal(cost, arrays["cost"], "cost")
+    for k in range(g.shape[0]):
+        assert digest(g[k]) == case["ground_slice_sha256"][k], f"ground slice {k}"
+        assert digest(c[k]) == case["ceiling_slice_sha256"][k], f"ceiling slice {k}"
+        assert digest(cost[k]) == case["cost_slice_sha256"][k], f"cost slice {k}"
+    heights = [s.plane_height for s in simp.slices]
+    assert heights == [case["heights"][k] for k in case["keep"]]
+    assert [s.index for s in simp.slices] == list(range(len(simp.slices)))
+
+
+def test_f32_and_f64_inputs_agree(golden):
+    case = golden["cases"]["synth_cfg0"]
+    xyz = case_input("synth_cfg0", case)
+    a = pct.build_tomogram(pct.PointCloud(xyz), 0.5, 0.1)
+    b = pct.build_tomogram(pct.PointCloud(xyz.astype(np.float64)), 0.5, 0.1)
+    assert np.array_equal(a.ground_stack(), b.ground_stack(), equal_nan=True)
+    assert np.array_equal(a.ceiling_stack(), b.ceiling_stack(), equal_nan=True)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_random_scenes_vs_oracle(seed):
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(2_000, 60_000))
+    xyz = np.column_stack([rng.uniform(-3, 7, n), rng.uniform(-2, 4, n),
+                           np.round(rng.uniform(-1, 4, n) * 20) / 20])  # many exact ties
+    d_s, r_g = [(0.5, 0.1), (0.3, 0.05), (0.7, 0.2)][seed]
+    ref = oracle.build(xyz, d_s, r_g)
+    tom, ev, simp = _run(xyz, d_s, r_g)
+    _assert_layers_equal(ev.ground_stack(), ref["ground"], "ground")
+    _assert_layers_equal(ev.ceiling_stack(), ref["ceiling"], "ceiling")
+    cost = oracle.evaluate(ref["ground"], ref["ceiling"], r_g, TABLE_PARAMS)
+    _assert_layers_equal(ev.cost_stack(), cost, "cost")
+    keep = oracle.simplify(ref["ground"], cost)
+    assert [s.plane_height for s in simp.slices] == [float(ref["heights"][k]) for k in keep]
+
+
+def test_point_order_independence(golden):
+    case = golden["cases"]["synth_cfg0"]
+    xyz = case_input("synth_cfg0", case)
+    perm = np.random.default_rng(0).permutation(len(xyz))
+    a = pct.build_tomogram(pct.PointCloud(xyz), 0.5, 0.1)
+    b = pct.build_tomogram(pct.PointCloud(xyz[perm]), 0.5, 0.1)
+    assert np.array_equal(a.ground_stack(), b.ground_stack(), equal_nan=True)
+    assert np.array_equal(a.ceiling_stack(), b.ceiling_stack(), equal_nan=True)
+
+
+def test_nan_bits_are_numpy_nan(golden):
+    case = golden["cases"]["synth_cfg0"]
+    tom = pct.build_tomogram(pct.PointCloud(case_input("synth_cfg0", case)), 0.5, 0.1)
+    g = tom.ground_stack().view(np.uint32)
+    bad = np.isnan(tom.ground_stack())
+    assert bad.any() and np.all(g[bad] == 0x7FC00000)
+
+
+# --- per-operation API against the oracle -------------------------------------
+
+def _slice_inputs(golden):
+    case = golden["cases"]["ref_random_multilayer_s9"]
+    arr = case_arrays(case)
+    return arr["ground"], arr["ceiling"], arr["cost"]
+
+
+def test_per_op_functions_match_oracle(golden):
+    G, Cc, _ = _slice_inputs(golden)
+    P = pct.TravParams()
+    for k in range(G.shape[0]):
+        g = pct.Layer(G[k], 0.1, (0.0, 0.0))
+        c = pct.Layer(Cc[k], 0.1, (0.0, 0.0))
+        ci = pct.interval_cost(g, c, P)
+        assert np.array_equal(ci, oracle.interval_cost(G[k], Cc[k], P))
+        cg = pct.ground_cost(g, P)
+        assert np.array_equal(cg, oracle.ground_cost(G[k], 0.1, P))
+        mx, mg, iso = pct.slope_magnitudes(g)
+        ox, og, oi = oracle.slope_magnitudes(G[k], 0.1)
+        assert np.array_equal(mx, ox) and np.array_equal(mg, og) and np.array_equal(iso, oi)
+        valid = np.isfinite(G[k])
+        f = pct.fuse_costs(ci, cg, valid, P)
+        assert np.array_equal(f, oracle.fuse_costs(ci, cg, valid, P))
+        gentle = valid & (og < P.theta_s)
+        assert np.array_equal(pct.gentle_fraction(gentle, 3), oracle.gentle_fraction(gentle, 3))
+        kern = pct.build_kernel(0.2, 0.4, 0.1)
+        assert np.array_equal(pct.inflate(f, kern), oracle.inflate(f, kern.weights))
+
+
+def test_inflation_golden_cases(golden):
+    for c in golden["inflation"]:
+        kern = pct.build_kernel(0.2, 0.4, c["r_g"])
+        assert digest(kern.weights) == c["kernel_sha256"]
+        shape = tuple(c["shape"])
+        g = np.random.default_rng(c["seed"]).uniform(0.0, 50.0, shape).astype(np.float32)
+        g[np.random.default_rng(c["seed"] + 1).uniform(size=shape) < 0.03] = 50.0
+        assert digest(pct.inflate(g, kern)) == c["out_sha256"]
+
+
+def test_terrain_cost_values_kats():
+    P = pct.TravParams()
+    # test_traversability.py:78-83 / test_acceptance.py:167-170
+    assert pct.terrain_cost_values(1.0, 1.2, 0.5, P) == pytest.approx(20.0 * (1.0 / 1.7) ** 2,
+                                                                      rel=1e-9)
+    assert pct.terrain_cost_values(1.0, 1.2, 0.1, P) == 50.0
+    assert pct.terrain_cost_values(2.0, 2.2, 0.9, P) == 50.0
+    assert pct.terrain_cost_values(0.18, 0.18, 0.0, P) == pytest.approx(3.75)
+    rng = np.random.default_rng(8)
+    mx, mg, ps = rng.uniform(0, 3, 4000), rng.uniform(0, 3, 4000), rng.uniform(0, 1, 4000)
+    assert np.array_equal(pct.terrain_cost_values(mx, mg, ps, P),
+                          oracle.terrain_cost_values(mx, mg, ps, P))
+
+
+def test_interval_kats():
+    P = pct.TravParams()
+    g = pct.Layer(np.zeros((1, 5)), 0.1, (0.0, 0.0))
+    c = pct.Layer([[0.40, 0.65, 0.55, np.nan, 1.0]], 0.1, (0.0, 0.0))
+    out = pct.interval_cost(g, c, P)
+    assert out[0, 0] == 50.0 and out[0, 3] == 0.0
+    assert out[0, 1] == pytest.approx(0.0, abs=1e-5)
+    assert out[0, 2] == pytest.approx(2.0, rel=1e-6)
+    out = pct.interval_cost(pct.Layer([[np.nan, 0.0]], 0.1, (0, 0)),
+                            pct.Layer([[2.0, 2.0]], 0.1, (0, 0)), P)
+    assert out[0, 0] == 50.0 and out[0, 1] == 0.0
+
+
+def test_inflate_single_barrier_decay():
+    kern = pct.build_kernel(0.2, 0.4, 0.1)
+    grid = np.zeros((21, 21), np.float32)
+    grid[10, 10] = 50.0
+    out = pct.inflate(grid, kern)
+    assert out[10, 13] == np.float32(np.float32(1 - (0.3 - 0.2) / 0.3) * np.float32(50.0))
+    assert out[10, 10] == 50.0 and out[10, 16] == 0.0
+
+
+def test_unique_cells_matches_oracle(golden):
+    G, _, Cost = _slice_inputs(golden)
+    from paper_2403_07631_b200.tomogram import Tomogram, TomogramSlice, Layer
+    sl = [TomogramSlice(Layer(G[k], 0.1, (0, 0)), Layer(G[k], 0.1, (0, 0)), 0.5 * (k + 1), k,
+                        Layer(Cost[k], 0.1, (0, 0))) for k in range(G.shape[0])]
+    tom = Tomogram(sl, 0.5, 0.0)
+    for k in range(G.shape[0]):
+        below = k - 1 if k > 0 else None
+        above = k + 1 if k + 1 < G.shape[0] else None
+        m = oracle.unique_mask(G, Cost, k, below, above)
+        assert pct.unique_cells(tom, k) == set(zip(*[v.tolist() for v in np.nonzero(m)]))
+    with pytest.raises(IndexError):
+        pct.unique_cells(tom, 99)
+
+
+def test_simplify_edge_cases():
+    from paper_2403_07631_b200.tomogram import Tomogram, TomogramSlice, Layer
+    shape = (5, 5)
+
+    def mk(gs, cs):
+        return Tomogram([TomogramSlice(Layer(g, 0.1, (0, 0)), Layer(g, 0.1, (0, 0)),
+                                       0.5 * (k + 1), k, Layer(c, 0.1, (0, 0)))
+                         for k, (g, c) in enumerate(zip(gs, cs))], 0.5, 0.0)
+    z = np.zeros(shape, np.float32)
+    one = np.ones(shape, np.float32)
+    # single slice: unchanged (test_simplify.py:57-61)
+    assert len(pct.simplify_tomogram(mk([z], [z])).slices) == 1
+    # identical slices collapse to the last one
+    out = pct.simplify_tomogram(mk([z, z, z], [one, one, one]))
+    assert [s.plane_height for s in out.slices] == [1.5]
+    # slope covered above (test_simplify.py:37-51)
+    slope = np.tile(np.linspace(0.6, 1.4, 5, dtype=np.float32), (5, 1))
+    out = pct.simplify_tomogram(mk([z, slope, slope], [z, one * 2, one * 2]))
+    assert [s.plane_height for s in out.slices] == [0.5, 1.5]
+    # long removal chains beyond the 32-slice window, checked against the oracle
+    rng = np.random.default_rng(3)
+    S = 80
+    gs = [np.where(rng.uniform(size=shape) < 0.05, np.float32(k // 40), z) for k in range(S)]
+    cs = [np.full(shape, 1.0, np.float32) for _ in range(S)]
+    G, Cst = np.stack(gs), np.stack(cs)
+    keep = oracle.simplify(G, Cst)
+    out = pct.simplify_tomogram(mk(gs, cs))
+    assert [s.plane_height for s in out.slices] == [0.5 * (k + 1) for k in keep]
+    # no cost layer
+    t = Tomogram([TomogramSlice(Layer(z, 0.1, (0, 0)), Layer(z, 0.1, (0, 0)), 0.5, 0),
+                  TomogramSlice(Layer(z, 0.1, (0, 0)), Layer(z, 0.1, (0, 0)), 1.0, 1)], 0.5, 0.0)
+    with pytest.raises(ValueError, match="cost layer"):
+        pct.simplify_tomogram(t)
+
+
+def test_build_errors_and_kats():
+    with pytest.raises(ValueError):
+        pct.build_tomogram(pct.PointCloud(np.ones((3, 3))), 0.0, 0.1)
+    with pytest.raises(pct.GridSizeError):
+        pct.build_tomogram(pct.PointCloud(np.array([[0.0, 0, 0], [100.0, 100.0, 1.0]])), 0.5,
+                           0.005, max_grid_side=1000)
+    # tie at a plane height goes to ground (test_tomogram.py:72-79)
+    pts = np.array([[0.0, 0.0, 0.5], [0.02, 0.02, 0.0], [1.0, 1.0, 1.0]])
+    tom = pct.build_tomogram(pct.PointCloud(pts), 0.5, 0.1)
+    s0 = tom.slices[0]
+    i, j = pct.rasterize_index((0.0, 0.0), tom.origin, tom.resolution)
+    assert s0.ground.values[i, j] == np.float32(0.5)
+    assert not s0.ceiling.valid[i, j]
+    # two parallel planes -> six slices with exact heights (test_tomogram.py:57-69)
+    xs = np.arange(0.025, 4.0, 0.05)
+    gx, gy = np.meshgrid(xs, xs, indexing="ij")
+    pts = np.concatenate([np.column_stack([gx.ravel(), gy.ravel(), np.full(gx.size, z)])
+                          for z in (0.0, 3.0)])
+    tom = pct.build_tomogram(pct.PointCloud(pts), 0.5, 0.1)
+    assert len(tom.slices) == 6
+    assert [s.plane_height for s in tom.slices] == pytest.approx([0.5, 1.0, 1.5, 2.0, 2.5, 3.0])
+    ref = oracle.build(pts, 0.5, 0.1)
+    assert np.array_equal(tom.ground_stack(), ref["ground"], equal_nan=True)
+    assert np.array_equal(tom.ceiling_stack(), ref["ceiling"], equal_nan=True)
+
+
+def test_evaluate_accepts_host_tomogram(golden):
+    G, Cc, Cost = _slice_inputs(golden)
+    from paper_2403_07631_b200.tomogram import Tomogram, TomogramSlice, Layer
+    tom = Tomogram([TomogramSlice(Layer(G[k], 0.1, (0, 0)), Layer(Cc[k], 0.1, (0, 0)),
+                                  0.5 * (k + 1), k) for k in range(G.shape[0])], 0.5, 0.0)
+    ev = pct.evaluate_tomogram(tom, pct.TravParams())
+    assert np.array_equal(ev.cost_stack(), Cost)
+    # evaluate_slice path
+    sl = pct.evaluate_slice(tom.slices[2], pct.TravParams())
+    assert np.array_equal(sl.cost.values, Cost[2])
