@@ -75,60 +75,58 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled while the timed region runs."""
-
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    """SM clock + clock-event (throttle) reasons polled through NVML (the
+    library nvidia-smi reads) every ~0.5 ms while the timed region runs —
+    the region lasts only milliseconds, too short for nvidia-smi -lms."""
 
     def __init__(self, device):
         self.device = device
-        self.proc = None
-        self.lines = []
+        self.samples = []
+        self.stop = threading.Event()
+        self.ok = False
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml as N
+            N.nvmlInit()
+            self.N = N
+            self.hd = N.nvmlDeviceGetHandleByIndex(self.device)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(self.hd, N.NVML_CLOCK_SM)
+            self.ok = True
+            self.t = threading.Thread(target=self._poll, daemon=True)
             self.t.start()
-        except Exception:
-            self.proc = None
+        except Exception as e:  # no NVML: report unsampled
+            self.err = repr(e)
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _poll(self):
+        N = self.N
+        while not self.stop.is_set():
+            try:
+                sm = N.nvmlDeviceGetClockInfo(self.hd, N.NVML_CLOCK_SM)
+                rs = N.nvmlDeviceGetCurrentClocksEventReasons(self.hd)
+                self.samples.append((sm, rs))
+            except Exception:
+                pass
+            time.sleep(0.0005)
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(2)
-            except Exception:
-                self.proc.kill()
+        self.stop.set()
+        if self.ok:
+            self.t.join(1.0)
 
     def summary(self):
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 6:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx.append(float(parts[1]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[2:6]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        if not sm:
+        if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
-                "reasons": sorted(reasons), "samples": len(sm)}
+        N = self.N
+        names = {N.nvmlClocksEventReasonHwSlowdown: "hw_slowdown",
+                 N.nvmlClocksEventReasonHwThermalSlowdown: "hw_thermal_slowdown",
+                 N.nvmlClocksEventReasonSwThermalSlowdown: "sw_thermal_slowdown",
+                 N.nvmlClocksEventReasonSwPowerCap: "sw_power_cap"}
+        reasons = sorted({nm for _, rs in self.samples for bit, nm in names.items() if rs & bit})
+        return {"sm_mhz": statistics.median(s for s, _ in self.samples),
+                "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(self.samples),
+                "source": "NVML polled during the timed region"}
 
 
 # ---------------------------------------------------------------------------
@@ -260,9 +258,15 @@ def run_b200(args):
         with torch.cuda.stream(stream):
             flush.zero_()
 
-    for _ in range(args.warmup):
+    # warm-up: at least W steps and at least 0.5 s so the SM clock has ramped
+    t_w = time.perf_counter()
+    done = 0
+    while done < args.warmup or (time.perf_counter() - t_w < 0.5 and not args.profile):
         step()
         flush_l2()
+        done += 1
+        if done % 8 == 0:
+            torch.cuda.synchronize()
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()

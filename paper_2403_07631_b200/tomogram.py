@@ -89,7 +89,11 @@ class DeviceStack:
 
 
 class DeviceTomogram:
-    """Owner of a pct_tomo (ground + ceiling stacks built on the device)."""
+    """Owner of a pct_tomo (ground + ceiling stacks built on the device).
+
+    The stacks reference their owner, never the other way round, so the
+    device memory is released by reference counting as soon as the last
+    Layer of the tomogram is dropped (no cycle for the GC to find)."""
 
     def __init__(self, ctx, handle):
         self.ctx = ctx
@@ -100,11 +104,15 @@ class DeviceTomogram:
         h = np.empty(max(fr.n_slices, 1), np.float64)
         ctx.check(ctx.lib.pct_tomo_frame(handle, C.byref(fr), h.ctypes.data, fr.n_slices), "frame")
         self.heights = h[:fr.n_slices]
-        self.ground = DeviceStack(ctx, ctx.lib.pct_tomo_layer(handle, _lib.LAYER_GROUND),
-                                  fr.n_slices, fr.rows, fr.cols, self)
-        self.ceiling = DeviceStack(ctx, ctx.lib.pct_tomo_layer(handle, _lib.LAYER_CEILING),
-                                   fr.n_slices, fr.rows, fr.cols, self)
         weakref.finalize(self, ctx.lib.pct_tomo_free, ctx.h, handle)
+
+    def stacks(self):
+        fr, ctx = self.frame, self.ctx
+        g = DeviceStack(ctx, ctx.lib.pct_tomo_layer(self.handle, _lib.LAYER_GROUND),
+                        fr.n_slices, fr.rows, fr.cols, self)
+        c = DeviceStack(ctx, ctx.lib.pct_tomo_layer(self.handle, _lib.LAYER_CEILING),
+                        fr.n_slices, fr.rows, fr.cols, self)
+        return g, c
 
 
 def new_device_stack(ctx, n_slices, rows, cols) -> DeviceStack:
@@ -336,9 +344,10 @@ def build_from_points(xyz, d_s: float, r_g: float, max_grid_side: int = GRID_SID
         ctx.check(rc, "pct_tomo_build")
     dt = DeviceTomogram(ctx, h)
     fr = dt.frame
+    gst, cst = dt.stacks()
     origin = (float(fr.origin_x), float(fr.origin_y))
-    slices = [TomogramSlice(ground=Layer.on_device(dt.ground, k, r_g, origin),
-                            ceiling=Layer.on_device(dt.ceiling, k, r_g, origin),
+    slices = [TomogramSlice(ground=Layer.on_device(gst, k, r_g, origin),
+                            ceiling=Layer.on_device(cst, k, r_g, origin),
                             plane_height=float(dt.heights[k]), index=k)
               for k in range(fr.n_slices)]
     return Tomogram(slices=slices, d_s=float(d_s), z_min=float(fr.z_min))
