@@ -120,6 +120,7 @@ struct EvalConsts {
   double d_min, d_ref, theta_b, theta_s, c_barrier, alpha_d, alpha_b, alpha_s;
   double rg, inv_rg, two_rg, inv_two_rg;  // gradient divisors (traversability.py:100-102)
   double inv_theta_b, inv_theta_s;        // q = m / theta (traversability.py:138,141)
+  double ts2_lo, ts2_hi;  // theta_s^2 (1 -/+ 2^-40): guard band of the gentle test
   int32_t ps_min_count;  // smallest gentle count c with RN(c/(2r+1)^2) > theta_p
   int32_t patch_radius;
 };
@@ -200,6 +201,97 @@ PCT_HD float cinit_encoded(float g, float ceil, const TerrainCell &t, const Eval
   bool needs_ps = false;
   double tv = t.isolated ? K.c_barrier : terrain_value(t.m_xy, t.m_grad, K, &needs_ps);
   float cg = (float)tv;
+  float f = fuse_value(ci, cg, K);
+  if (needs_ps) f = bits_f32(f32_bits(f) | 0x80000000u);
+  return f;
+}
+
+// ---------------------------------------------------------------------------
+// Fast exact path (used by the fused kernel).  glibc's hypot is
+// h = RN(h0 - (t1+t2)/(2 h0)) with h0 = sqrt(ax*ax + ay*ay), i.e. within
+// 1 ulp of h0.  The value of m_grad only matters (a) in the comparison
+// m_grad < theta_s and (b) through float32(alpha_s * (m_grad/theta_s)^2) in
+// the gentle branch.  (a) is decided from s = ax*ax + ay*ay outside a
+// relative guard band of 2^-40 around theta_s^2; (b) is computed from h0 and
+// accepted when the float64 cost lies farther than 2^-44 (relative) from a
+// float32 rounding boundary, since h0 and h differ by < 2^-51 relative and
+// the cost by < 2^-48.  Inside either band the exact glibc value is used.
+
+// true if every double within rel*|x| of x rounds to the float f = RN32(x)
+PCT_HD bool f32_round_safe(double x, float f, double rel) {
+  if (x == 0.0) return true;
+  uint32_t b = f32_bits(f) & 0x7FFFFFFFu;
+  if (b == 0u || b >= 0x7F800000u - 1u) return false;
+  const double fd = (double)(f < 0 ? -f : f);
+  const double ax = x < 0 ? -x : x;
+  const double r = ax - fd;  // exact: |r| <= ulp(f)/2
+  const double up = (double)bits_f32(b + 1u) - fd;
+  const double dn = fd - (double)bits_f32(b - 1u);
+  const double half = 0.5 * (r >= 0.0 ? up : dn);
+  return half - (r >= 0.0 ? r : -r) > rel * ax;
+}
+
+PCT_HD float gentle_cost_from(double m, const EvalConsts &K, double *cd) {
+  const double q = div_const(m, K.theta_s, K.inv_theta_s);
+  *cd = K.alpha_s * (q * q);
+  return (float)*cd;
+}
+
+// float32 terrain cost of the gentle branch (m_grad < theta_s) for the
+// gradient (gx, gy) with s = ax*ax + ay*ay, bit-identical to the reference.
+PCT_HD float gentle_cost32(double gx, double gy, double s, const EvalConsts &K) {
+  double cd;
+  if (s == 0.0) return 0.0f;  // hypot(0, 0) = 0 exactly
+  if (s > 0x1p-900) {         // away from the subnormal range sqrt(s) is within 1 ulp
+    float f = gentle_cost_from(sqrt(s), K, &cd);
+    if (f32_round_safe(cd, f, 0x1p-44)) return f;
+  }
+  return gentle_cost_from(glibc_hypot(gx, gy), K, &cd);
+}
+
+// m_grad < theta_s from s, exact glibc hypot only inside the guard band
+PCT_HD bool below_theta_s(double gx, double gy, double s, const EvalConsts &K) {
+  if (s < K.ts2_lo) return true;
+  if (s > K.ts2_hi) return false;
+  return glibc_hypot(gx, gy) < K.theta_s;
+}
+
+struct FastCell {
+  double gx, gy, s, m_xy;
+  bool valid, isolated, gentle;
+};
+
+PCT_HD FastCell fast_terrain(const Cross &c, const EvalConsts &K) {
+  FastCell t;
+  const bool v = finite32(c.e), vl = finite32(c.l), vr = finite32(c.r), vu = finite32(c.u),
+             vd = finite32(c.d);
+  const double ef = v ? (double)c.e : 0.0;
+  t.gx = axis_gradient(vr, vl, vr ? (double)c.r : 0.0, vl ? (double)c.l : 0.0, ef, K);
+  t.gy = axis_gradient(vd, vu, vd ? (double)c.d : 0.0, vu ? (double)c.u : 0.0, ef, K);
+  const double ax = fabs(t.gx), ay = fabs(t.gy);
+  t.m_xy = ax > ay ? ax : ay;
+  t.s = ax * ax + ay * ay;
+  t.valid = v;
+  t.isolated = v && !(vl || vr || vu || vd);
+  t.gentle = v && below_theta_s(t.gx, t.gy, t.s, K);
+  return t;
+}
+
+// c_init of a cell (same encoding as cinit_encoded) from the fast terrain data
+PCT_HD float fast_cinit(float g, float ceil, const FastCell &t, const EvalConsts &K) {
+  if (!t.valid) return (float)K.c_barrier;
+  const float ci = interval_value(g, ceil, K);
+  float cg;
+  bool needs_ps = false;
+  if (t.isolated || t.m_xy > K.theta_b) {
+    cg = (float)K.c_barrier;
+  } else if (t.gentle) {
+    cg = gentle_cost32(t.gx, t.gy, t.s, K);
+  } else {
+    needs_ps = true;
+    const double q = div_const(t.m_xy, K.theta_b, K.inv_theta_b);
+    cg = (float)(K.alpha_b * (q * q));
+  }
   float f = fuse_value(ci, cg, K);
   if (needs_ps) f = bits_f32(f32_bits(f) | 0x80000000u);
   return f;

@@ -6,17 +6,21 @@
 // One CTA computes a TH x TW tile of c_T for one slice entirely on chip
 // (DESIGN.md §4.2):
 //   A  ground tile + halo (R + r + 1 cells) -> smem (NaN outside the grid)
-//   B  per cell of the (TH+2R+2r)^2 "gentle" region: gradients, m_xy,
-//      glibc-exact m_grad, isolation, gentle flag; for the (TH+2R)^2 c_init
-//      region also the interval cost and the fused cost, with the foothold
-//      branch marked in the sign bit (its value needs the window count)
-//   C  horizontal gentle counts over 2r+1 columns (u8)
-//   D  vertical sums -> p_s test as an integer threshold -> final c_init
+//   B  per cell of the (TH+2R+2r)^2 "gentle" region: gradients, gentle flag
+//      (exact glibc m_grad only inside a 2^-40 guard band); for the
+//      (TH+2R)^2 c_init region also the interval cost and the fused cost,
+//      the foothold branch marked in the sign bit
+//   C  gentle flags packed to bits, one row of words per region row
+//   D  foothold count over the (2r+1)^2 window by popcount -> p_s test as an
+//      integer threshold -> final c_init
 //   E  weighted max over the (2R+1)^2 kernel taps with zero padding:
 //      max_t fl32(w_t * c_init) (== the reference's per-class max filter,
 //      since x -> fl32(w*x) is monotone for w > 0).  8-fold symmetric
 //      kernels with R <= 4 use a register sliding window of horizontal pair
 //      maxima P_b(i,j) = max(c(i,j-b), c(i,j+b)); others loop over taps.
+// eval_fast_kernel has the whole geometry as template constants (the common
+// parameter sets); eval_generic_kernel takes it at run time and also serves
+// the per-operation entry points.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -34,124 +38,6 @@ __constant__ float c_wfull[kMaxTaps];  // generic path: kside x kside weights
 __constant__ float c_wsym[9 * 9];      // symmetric path: w[a][b], a,b in [0, R], stride 9
 __constant__ EvalConsts c_K;
 
-struct TileGeom {
-  int R, r;            // inflation radius, patch radius
-  int TH, TW;          // output tile
-  int CH, CW;          // c_init region = tile + R halo
-  int GH, GW;          // gentle region = c_init region + r halo
-  int LH, LW;          // loaded ground region = gentle region + 1
-  int off_gen, off_hsum, off_cinit, smem;  // byte offsets
-};
-
-TileGeom make_geom(int R, int r, int TH, int TW) {
-  TileGeom g;
-  g.R = R;
-  g.r = r;
-  g.TH = TH;
-  g.TW = TW;
-  g.CH = TH + 2 * R;
-  g.CW = TW + 2 * R;
-  g.GH = g.CH + 2 * r;
-  g.GW = g.CW + 2 * r;
-  g.LH = g.GH + 2;
-  g.LW = g.GW + 2;
-  size_t o = (size_t)g.LH * g.LW * 4;
-  g.off_gen = (int)o;
-  o += ((size_t)g.GH * g.GW + 15) & ~(size_t)15;
-  g.off_hsum = (int)o;
-  o += ((size_t)g.GH * g.CW + 15) & ~(size_t)15;
-  g.off_cinit = (int)o;
-  o += (size_t)g.CH * g.CW * 4;
-  g.smem = (int)o;
-  return g;
-}
-
-// ------------------------------------------------------------ stages A-D
-// mode: kEvalFull (c_T), kEvalCinit (fused cost before inflation),
-// kEvalGroundCost (ground_cost only), kEvalInterval (interval_cost only).
-template <int NT>
-__device__ __forceinline__ void stages_abcd(const TileGeom &G, const float *__restrict__ ground,
-                                            const float *__restrict__ ceiling, int rows, int cols,
-                                            int i0, int j0, int mode, unsigned char *smem) {
-  float *grd = reinterpret_cast<float *>(smem);
-  unsigned char *gen = smem + G.off_gen;
-  unsigned char *hsum = smem + G.off_hsum;
-  float *cinit = reinterpret_cast<float *>(smem + G.off_cinit);
-  const float nanf_ = bits_f32(kNaNBits);
-  const int H = G.R + G.r + 1;
-  const int tid = threadIdx.x;
-
-  // A: ground tile + halo
-  for (int idx = tid; idx < G.LH * G.LW; idx += NT) {
-    const int y = idx / G.LW, x = idx - y * G.LW;
-    const int gi = i0 - H + y, gj = j0 - H + x;
-    float v = nanf_;
-    if (gi >= 0 && gi < rows && gj >= 0 && gj < cols) v = __ldg(ground + (int64_t)gi * cols + gj);
-    grd[idx] = v;
-  }
-  __syncthreads();
-
-  // B: terrain per gentle-region cell; c_init candidates for the inner region
-  const int rr = G.r;
-  for (int idx = tid; idx < G.GH * G.GW; idx += NT) {
-    const int y = idx / G.GW, x = idx - y * G.GW;
-    const int gi = i0 - G.R - rr + y, gj = j0 - G.R - rr + x;
-    const bool in_grid = gi >= 0 && gi < rows && gj >= 0 && gj < cols;
-    const bool in_ci = y >= rr && y < rr + G.CH && x >= rr && x < rr + G.CW;
-    unsigned char gflag = 0;
-    float enc = 0.0f;  // zero padding outside the map (inflate cval=0)
-    if (in_grid) {
-      const float *p = grd + (y + 1) * G.LW + (x + 1);
-      Cross c{p[0], p[-1], p[1], p[-G.LW], p[G.LW]};
-      TerrainCell t = terrain_cell(c, c_K);
-      gflag = t.gentle ? 1 : 0;
-      if (in_ci) {
-        if (mode == kEvalInterval) {
-          enc = t.valid ? interval_value(c.e, __ldg(ceiling + (int64_t)gi * cols + gj), c_K)
-                        : (float)c_K.c_barrier;
-        } else if (mode == kEvalGroundCost) {
-          bool needs_ps = false;
-          if (t.valid) {
-            double tv = t.isolated ? c_K.c_barrier
-                                   : terrain_value(t.m_xy, t.m_grad, c_K, &needs_ps);
-            enc = (float)tv;
-            if (needs_ps) enc = bits_f32(f32_bits(enc) | 0x80000000u);
-          }
-        } else {
-          const float ceil_v = t.valid ? __ldg(ceiling + (int64_t)gi * cols + gj) : nanf_;
-          enc = cinit_encoded(c.e, ceil_v, t, c_K);
-        }
-      }
-    }
-    gen[idx] = gflag;
-    if (in_ci) cinit[(y - rr) * G.CW + (x - rr)] = enc;
-  }
-  __syncthreads();
-
-  // C: horizontal window counts (2r+1 columns) for every gentle-region row
-  const int side = 2 * rr + 1;
-  for (int idx = tid; idx < G.GH * G.CW; idx += NT) {
-    const int y = idx / G.CW, x = idx - y * G.CW;
-    const unsigned char *g = gen + y * G.GW + x;
-    int s = 0;
-    for (int d = 0; d < side; ++d) s += g[d];
-    hsum[idx] = (unsigned char)s;
-  }
-  __syncthreads();
-
-  // D: foothold test p_s > theta_p  <=>  count >= ps_min_count
-  for (int idx = tid; idx < G.CH * G.CW; idx += NT) {
-    const float enc = cinit[idx];
-    if (f32_bits(enc) & 0x80000000u) {
-      const int y = idx / G.CW, x = idx - y * G.CW;
-      int cnt = 0;
-      for (int d = 0; d < side; ++d) cnt += hsum[(y + d) * G.CW + x];
-      cinit[idx] = cinit_resolve(enc, cnt, c_K);
-    }
-  }
-  __syncthreads();
-}
-
 // ------------------------------------------------ stage E, symmetric, R<=4
 // Thread = one output column x of a strip of V rows; register ring of the
 // horizontal pair maxima of 2R+1 consecutive c_init rows.
@@ -168,7 +54,7 @@ __device__ __forceinline__ void inflate_sym_strip(const float *__restrict__ cini
 #pragma unroll
     for (int b = 1; b <= R; ++b) P[t][b] = fmaxf(rowp[R - b], rowp[R + b]);
     if (t >= 2 * R) {
-      const int o = t - 2 * R;     // output row in strip; centre P row = o + R
+      const int o = t - 2 * R;  // output row in strip; centre P row = o + R
       const int c = o + R;
       float acc = 0.0f;
 #pragma unroll
@@ -197,25 +83,234 @@ __device__ __forceinline__ void inflate_sym_strip(const float *__restrict__ cini
   }
 }
 
-template <int R, int TH, int TW, int NT>
-__global__ void __launch_bounds__(NT) eval_sym_kernel(TileGeom G, const float *__restrict__ ground,
-                                                      const float *__restrict__ ceiling, int rows,
-                                                      int cols, float *__restrict__ cost) {
+// ------------------------------------------------------------- fast kernel
+template <int R, int PR, int TH, int TW>
+struct FastGeom {
+  static constexpr int CH = TH + 2 * R, CW = TW + 2 * R;      // c_init region
+  static constexpr int GH = CH + 2 * PR, GW = CW + 2 * PR;    // gentle region
+  static constexpr int LH = GH + 2, LW = GW + 2;              // loaded ground
+  static constexpr int H = R + PR + 1;                        // ground halo
+  static constexpr int WORDS = (GW + 31) / 32 + 1;            // bit words per row (+1 pad)
+  static constexpr int GWP = WORDS * 32;                      // padded u8 row
+  static constexpr int OFF_GEN = LH * LW * 4;
+  static constexpr int OFF_BITS = OFF_GEN + GH * GWP;
+  static constexpr int OFF_CINIT = OFF_BITS + GH * WORDS * 4;
+  static constexpr int SMEM = OFF_CINIT + CH * CW * 4;
+};
+
+template <int R, int PR, int TH, int TW, int NT>
+__global__ void __launch_bounds__(NT, 3) eval_fast_kernel(const float *__restrict__ ground,
+                                                       const float *__restrict__ ceiling,
+                                                       int rows, int cols,
+                                                       float *__restrict__ cost) {
+  using G = FastGeom<R, PR, TH, TW>;
   extern __shared__ __align__(16) unsigned char smem[];
+  float *grd = reinterpret_cast<float *>(smem);
+  unsigned char *gen = smem + G::OFF_GEN;
+  uint32_t *bits = reinterpret_cast<uint32_t *>(smem + G::OFF_BITS);
+  float *cinit = reinterpret_cast<float *>(smem + G::OFF_CINIT);
   const int64_t plane = (int64_t)rows * cols;
   const int k = blockIdx.z;
   const int i0 = blockIdx.y * TH, j0 = blockIdx.x * TW;
-  stages_abcd<NT>(G, ground + k * plane, ceiling + k * plane, rows, cols, i0, j0, kEvalFull,
-                  smem);
-  const float *cinit = reinterpret_cast<const float *>(smem + G.off_cinit);
+  const float *gk = ground + k * plane;
+  const float *ck = ceiling + k * plane;
+  const float nanf_ = bits_f32(kNaNBits);
+  const int tid = threadIdx.x;
+
+  // A: ground tile + halo (NaN outside the grid)
+  for (int idx = tid; idx < G::LH * G::LW; idx += NT) {
+    const int y = idx / G::LW, x = idx - y * G::LW;
+    const int gi = i0 - G::H + y, gj = j0 - G::H + x;
+    float v = nanf_;
+    if (gi >= 0 && gi < rows && gj >= 0 && gj < cols) v = __ldg(gk + (int64_t)gi * cols + gj);
+    grd[idx] = v;
+  }
+  __syncthreads();
+
+  // B: gentle flags over the gentle region, encoded c_init over the inner region
+  for (int idx = tid; idx < G::GH * G::GW; idx += NT) {
+    const int y = idx / G::GW, x = idx - y * G::GW;
+    const int gi = i0 - R - PR + y, gj = j0 - R - PR + x;
+    const bool in_grid = gi >= 0 && gi < rows && gj >= 0 && gj < cols;
+    const bool in_ci = y >= PR && y < PR + G::CH && x >= PR && x < PR + G::CW;
+    unsigned char gflag = 0;
+    float enc = 0.0f;  // zero padding outside the map (inflate cval=0)
+    if (in_grid) {
+      const float *p = grd + (y + 1) * G::LW + (x + 1);
+      const Cross c{p[0], p[-1], p[1], p[-G::LW], p[G::LW]};
+      const FastCell t = fast_terrain(c, c_K);
+      gflag = t.gentle ? 1 : 0;
+      if (in_ci) {
+        const float cv = t.valid ? __ldg(ck + (int64_t)gi * cols + gj) : nanf_;
+        enc = fast_cinit(c.e, cv, t, c_K);
+      }
+    }
+    gen[y * G::GWP + x] = gflag;
+    if (in_ci) cinit[(y - PR) * G::CW + (x - PR)] = enc;
+  }
+  // zero the padding columns of the flag rows
+  for (int idx = tid; idx < G::GH * (G::GWP - G::GW); idx += NT) {
+    const int y = idx / (G::GWP - G::GW), x = G::GW + idx - y * (G::GWP - G::GW);
+    gen[y * G::GWP + x] = 0;
+  }
+  __syncthreads();
+
+  // C: pack the flags, 32 cells per word
+  for (int idx = tid; idx < G::GH * G::WORDS; idx += NT) {
+    const int y = idx / G::WORDS, w = idx - y * G::WORDS;
+    const uint32_t *src = reinterpret_cast<const uint32_t *>(gen + y * G::GWP + w * 32);
+    uint32_t word = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const uint32_t v = src[q];  // 4 flags, one per byte
+      word |= ((v & 1u) | ((v >> 7) & 2u) | ((v >> 14) & 4u) | ((v >> 21) & 8u)) << (4 * q);
+    }
+    bits[idx] = word;
+  }
+  __syncthreads();
+
+  // D: foothold test p_s > theta_p  <=>  count >= ps_min_count
+  constexpr int SIDE = 2 * PR + 1;
+  constexpr uint64_t MASK = (SIDE >= 64) ? ~0ull : ((1ull << SIDE) - 1ull);
+  for (int idx = tid; idx < G::CH * G::CW; idx += NT) {
+    const float enc = cinit[idx];
+    if (f32_bits(enc) & 0x80000000u) {
+      const int y = idx / G::CW, x = idx - y * G::CW;  // window rows y..y+2r, cols x..x+2r
+      const int w = x >> 5, sh = x & 31;
+      int cnt = 0;
+#pragma unroll
+      for (int d = 0; d < SIDE; ++d) {
+        const uint32_t *rw = bits + (y + d) * G::WORDS + w;
+        const uint64_t v = (uint64_t)rw[0] | ((uint64_t)rw[1] << 32);
+        cnt += __popcll((v >> sh) & MASK);
+      }
+      cinit[idx] = cinit_resolve(enc, cnt, c_K);
+    }
+  }
+  __syncthreads();
+
+  // E: inflation
   constexpr int STRIPS = NT / TW;
   constexpr int V = TH / STRIPS;
-  const int x = threadIdx.x % TW, s = threadIdx.x / TW;
-  inflate_sym_strip<R, V>(cinit, G.CW, x, s * V, cost + k * plane, cols, i0 + s * V, j0 + x,
+  const int x = tid % TW, s = tid / TW;
+  inflate_sym_strip<R, V>(cinit, G::CW, x, s * V, cost + k * plane, cols, i0 + s * V, j0 + x,
                           rows, cols);
 }
 
-// --------------------------------------------------- stage E, generic taps
+// ---------------------------------------------------------- generic kernel
+struct TileGeom {
+  int R, r;            // inflation radius, patch radius
+  int TH, TW;          // output tile
+  int CH, CW;          // c_init region = tile + R halo
+  int GH, GW;          // gentle region = c_init region + r halo
+  int LH, LW;          // loaded ground region = gentle region + 1
+  int off_gen, off_hsum, off_cinit, smem;  // byte offsets
+};
+
+TileGeom make_geom(int R, int r, int TH, int TW) {
+  TileGeom g;
+  g.R = R;
+  g.r = r;
+  g.TH = TH;
+  g.TW = TW;
+  g.CH = TH + 2 * R;
+  g.CW = TW + 2 * R;
+  g.GH = g.CH + 2 * r;
+  g.GW = g.CW + 2 * r;
+  g.LH = g.GH + 2;
+  g.LW = g.GW + 2;
+  size_t o = (size_t)g.LH * g.LW * 4;
+  g.off_gen = (int)o;
+  o += ((size_t)g.GH * g.GW + 15) & ~(size_t)15;
+  g.off_hsum = (int)o;
+  o += (((size_t)g.GH * g.CW * 2) + 15) & ~(size_t)15;
+  g.off_cinit = (int)o;
+  o += (size_t)g.CH * g.CW * 4;
+  g.smem = (int)o;
+  return g;
+}
+
+// mode: kEvalFull (c_T), kEvalCinit (fused cost before inflation),
+// kEvalGroundCost (ground_cost only), kEvalInterval (interval_cost only).
+template <int NT>
+__device__ __forceinline__ void stages_abcd(const TileGeom &G, const float *__restrict__ ground,
+                                            const float *__restrict__ ceiling, int rows, int cols,
+                                            int i0, int j0, int mode, unsigned char *smem) {
+  float *grd = reinterpret_cast<float *>(smem);
+  unsigned char *gen = smem + G.off_gen;
+  uint16_t *hsum = reinterpret_cast<uint16_t *>(smem + G.off_hsum);
+  float *cinit = reinterpret_cast<float *>(smem + G.off_cinit);
+  const float nanf_ = bits_f32(kNaNBits);
+  const int H = G.R + G.r + 1;
+  const int tid = threadIdx.x;
+
+  for (int idx = tid; idx < G.LH * G.LW; idx += NT) {
+    const int y = idx / G.LW, x = idx - y * G.LW;
+    const int gi = i0 - H + y, gj = j0 - H + x;
+    float v = nanf_;
+    if (gi >= 0 && gi < rows && gj >= 0 && gj < cols) v = __ldg(ground + (int64_t)gi * cols + gj);
+    grd[idx] = v;
+  }
+  __syncthreads();
+
+  const int rr = G.r;
+  for (int idx = tid; idx < G.GH * G.GW; idx += NT) {
+    const int y = idx / G.GW, x = idx - y * G.GW;
+    const int gi = i0 - G.R - rr + y, gj = j0 - G.R - rr + x;
+    const bool in_grid = gi >= 0 && gi < rows && gj >= 0 && gj < cols;
+    const bool in_ci = y >= rr && y < rr + G.CH && x >= rr && x < rr + G.CW;
+    unsigned char gflag = 0;
+    float enc = 0.0f;
+    if (in_grid) {
+      const float *p = grd + (y + 1) * G.LW + (x + 1);
+      Cross c{p[0], p[-1], p[1], p[-G.LW], p[G.LW]};
+      TerrainCell t = terrain_cell(c, c_K);
+      gflag = t.gentle ? 1 : 0;
+      if (in_ci) {
+        if (mode == kEvalInterval) {
+          enc = t.valid ? interval_value(c.e, __ldg(ceiling + (int64_t)gi * cols + gj), c_K)
+                        : (float)c_K.c_barrier;
+        } else if (mode == kEvalGroundCost) {
+          bool needs_ps = false;
+          if (t.valid) {
+            double tv = t.isolated ? c_K.c_barrier
+                                   : terrain_value(t.m_xy, t.m_grad, c_K, &needs_ps);
+            enc = (float)tv;
+            if (needs_ps) enc = bits_f32(f32_bits(enc) | 0x80000000u);
+          }
+        } else {
+          const float ceil_v = t.valid ? __ldg(ceiling + (int64_t)gi * cols + gj) : nanf_;
+          enc = cinit_encoded(c.e, ceil_v, t, c_K);
+        }
+      }
+    }
+    gen[idx] = gflag;
+    if (in_ci) cinit[(y - rr) * G.CW + (x - rr)] = enc;
+  }
+  __syncthreads();
+
+  const int side = 2 * rr + 1;
+  for (int idx = tid; idx < G.GH * G.CW; idx += NT) {
+    const int y = idx / G.CW, x = idx - y * G.CW;
+    const unsigned char *g = gen + y * G.GW + x;
+    int s = 0;
+    for (int d = 0; d < side; ++d) s += g[d];
+    hsum[idx] = (uint16_t)s;
+  }
+  __syncthreads();
+
+  for (int idx = tid; idx < G.CH * G.CW; idx += NT) {
+    const float enc = cinit[idx];
+    if (f32_bits(enc) & 0x80000000u) {
+      const int y = idx / G.CW, x = idx - y * G.CW;
+      int cnt = 0;
+      for (int d = 0; d < side; ++d) cnt += hsum[(y + d) * G.CW + x];
+      cinit[idx] = cinit_resolve(enc, cnt, c_K);
+    }
+  }
+  __syncthreads();
+}
+
 template <int NT>
 __device__ __forceinline__ void inflate_generic(const TileGeom &G, const float *__restrict__ cinit,
                                                 int kside, float *__restrict__ out, int rows,
@@ -283,14 +378,8 @@ __global__ void __launch_bounds__(NT) inflate_kernel(TileGeom G, const float *__
 bool symmetric_kernel(const float *w, int kside, int R, float wsym[81]) {
   if (R > 4) return false;
   for (int i = 0; i < 81; ++i) wsym[i] = 0.0f;
-  for (int m = 0; m < kside; ++m)
-    for (int n = 0; n < kside; ++n) {
-      int a = std::abs(m - R), b = std::abs(n - R);
-      if (a < b) std::swap(a, b);
-      const float v = w[m * kside + n];
-      float &s = wsym[a * 9 + b];
-      if (m == R + a && n == R + b) s = v;  // canonical representative
-    }
+  for (int a = 0; a <= R; ++a)
+    for (int b = 0; b <= a; ++b) wsym[a * 9 + b] = w[(R + a) * kside + (R + b)];
   for (int m = 0; m < kside; ++m)
     for (int n = 0; n < kside; ++n) {
       int a = std::abs(m - R), b = std::abs(n - R);
@@ -311,6 +400,18 @@ int ps_min_count(double theta_p, int radius) {
 
 constexpr int kNT = 256;
 
+template <int R, int PR>
+int launch_fast(pct_ctx *ctx, const float *ground, const float *ceiling, int S, int rows,
+                int cols, float *cost) {
+  constexpr int TH = 64, TW = 64;
+  auto kern = eval_fast_kernel<R, PR, TH, TW, kNT>;
+  constexpr int smem = FastGeom<R, PR, TH, TW>::SMEM;
+  PCT_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  dim3 grid((cols + TW - 1) / TW, (rows + TH - 1) / TH, S);
+  kern<<<grid, kNT, smem, ctx->stream>>>(ground, ceiling, rows, cols, cost);
+  return check_launch(ctx, "eval_fast_kernel");
+}
+
 }  // namespace
 
 EvalConsts make_consts(const pct_trav_params &p, double r_g) {
@@ -329,6 +430,8 @@ EvalConsts make_consts(const pct_trav_params &p, double r_g) {
   K.inv_two_rg = 1.0 / K.two_rg;
   K.inv_theta_b = 1.0 / p.theta_b;
   K.inv_theta_s = 1.0 / p.theta_s;
+  K.ts2_lo = p.theta_s * p.theta_s * (1.0 - 0x1p-40);
+  K.ts2_hi = p.theta_s * p.theta_s * (1.0 + 0x1p-40);
   K.patch_radius = p.patch_radius;
   K.ps_min_count = ps_min_count(p.theta_p, p.patch_radius);
   return K;
@@ -358,24 +461,14 @@ int launch_evaluate(pct_ctx *ctx, const float *ground, const float *ceiling, int
       PCT_CUDA(ctx, cudaMemcpyToSymbolAsync(c_wfull, kernel_w, sizeof(float) * kside * kside, 0,
                                             cudaMemcpyHostToDevice, ctx->stream));
   }
-  if (sym && R == 4) {
-    constexpr int TH = 64, TW = 64;
-    TileGeom G = make_geom(4, p.patch_radius, TH, TW);
-    auto kern = eval_sym_kernel<4, TH, TW, kNT>;
-    PCT_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G.smem));
-    dim3 grid((cols + TW - 1) / TW, (rows + TH - 1) / TH, S);
-    kern<<<grid, kNT, G.smem, ctx->stream>>>(G, ground, ceiling, rows, cols, cost);
-    return check_launch(ctx, "eval_sym_kernel<4>");
-  }
-  if (sym && R == 2) {
-    constexpr int TH = 64, TW = 64;
-    TileGeom G = make_geom(2, p.patch_radius, TH, TW);
-    auto kern = eval_sym_kernel<2, TH, TW, kNT>;
-    PCT_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G.smem));
-    dim3 grid((cols + TW - 1) / TW, (rows + TH - 1) / TH, S);
-    kern<<<grid, kNT, G.smem, ctx->stream>>>(G, ground, ceiling, rows, cols, cost);
-    return check_launch(ctx, "eval_sym_kernel<2>");
-  }
+  if (sym && R == 4 && p.patch_radius == 3)  // r_g = 0.1 with the Table-I radii
+    return launch_fast<4, 3>(ctx, ground, ceiling, S, rows, cols, cost);
+  if (sym && R == 2 && p.patch_radius == 2)  // r_g = 0.2
+    return launch_fast<2, 2>(ctx, ground, ceiling, S, rows, cols, cost);
+  if (sym && R == 3 && p.patch_radius == 3)
+    return launch_fast<3, 3>(ctx, ground, ceiling, S, rows, cols, cost);
+  if (sym && R == 4 && p.patch_radius == 4)
+    return launch_fast<4, 4>(ctx, ground, ceiling, S, rows, cols, cost);
   // generic path: pick the largest square-ish tile that fits in shared memory
   int TH = 64, TW = 64;
   TileGeom G = make_geom(R, p.patch_radius, TH, TW);

@@ -23,6 +23,9 @@ def hm():
     lib.pcth_hypot.argtypes = [P, P, C.c_int64, P]
     lib.pcth_div_const.argtypes = [P, C.c_int64, C.c_double, P]
     lib.pcth_cinit.argtypes = [P, P, C.c_int, C.c_int, C.c_double, P, C.c_int, C.c_int, P]
+    lib.pcth_fast_cells.argtypes = [P, P, C.c_int64, C.c_double, P, P, P]
+    lib.pcth_fast_cells.restype = C.c_int64
+    lib.pcth_ref_cells.argtypes = [P, P, C.c_int64, C.c_double, P, P, P]
     return lib
 
 
@@ -92,6 +95,47 @@ def test_cinit_composition_matches_oracle(hm, golden, name):
         G, Cc = arr["ground"][k], arr["ceiling"][k]
         assert np.array_equal(_cinit_host(hm, G, Cc, 0.1, TABLE_PARAMS),
                               _cinit_oracle(G, Cc, 0.1, TABLE_PARAMS))
+
+
+def _cells(hm, fn, cross, ceil, r_g):
+    P = TABLE_PARAMS
+    pv = np.array([P.d_min, P.d_ref, P.theta_b, P.theta_s, P.theta_p, P.c_barrier, P.alpha_d,
+                   P.alpha_b, P.alpha_s])
+    enc = np.empty(len(ceil), np.float32)
+    gen = np.empty(len(ceil), np.uint8)
+    r = fn(cross.ctypes.data, ceil.ctypes.data, len(ceil), C.c_double(r_g), pv.ctypes.data,
+           enc.ctypes.data, gen.ctypes.data)
+    return enc, gen, r
+
+
+@pytest.mark.parametrize("r_g", [0.1, 0.05, 0.2])
+def test_fast_guarded_path_equals_reference_path(hm, r_g):
+    """eval_fast_kernel's per-cell arithmetic (sqrt + guard instead of the
+    exact glibc hypot) must equal the reference-order path on every cell,
+    including cells steered into the theta_s guard band."""
+    hm.pcth_fast_cells.restype = C.c_int64
+    rng = np.random.default_rng(11)
+    n = 3_000_000
+    e = rng.uniform(0, 3, n).astype(np.float32)
+    scale = np.float32(r_g) * rng.choice(np.array([0.02, 0.2, 0.5, 1.0, 3.0], np.float32), n)
+    cross = np.stack([e] + [e + (rng.standard_normal(n).astype(np.float32) * scale)
+                            for _ in range(4)], axis=1).astype(np.float32)
+    # exact slope theta_s along x on a share of the cells: lands in the guard band
+    k = n // 10
+    cross[:k, 2] = (cross[:k, 0].astype(np.float64) + 0.36 * r_g).astype(np.float32)
+    cross[:k, 1] = np.nan
+    cross[:k, 3] = cross[:k, 0]
+    cross[:k, 4] = np.nan
+    holes = rng.uniform(size=cross.shape) < 0.05
+    cross[holes] = np.nan
+    ceil = (e + rng.uniform(0.3, 2.0, n)).astype(np.float32)
+    ceil[rng.uniform(size=n) < 0.3] = np.nan
+    cross = np.ascontiguousarray(cross)
+    f_enc, f_gen, exact = _cells(hm, hm.pcth_fast_cells, cross, ceil, r_g)
+    r_enc, r_gen, _ = _cells(hm, hm.pcth_ref_cells, cross, ceil, r_g)
+    assert np.array_equal(f_gen, r_gen)
+    assert np.array_equal(f_enc.view(np.uint32), r_enc.view(np.uint32))
+    assert exact > 0  # the guard paths were exercised
 
 
 def test_cinit_random_rough_terrain(hm):
