@@ -127,12 +127,13 @@ struct EvalConsts {
 
 // One axis of _axis_gradient (traversability.py:76-103): central difference
 // where both neighbours are valid, one-sided otherwise, 0 with none.
+// Branch-free form: with no valid neighbour the numerator is ef - ef = +0 and
+// the quotient +0, as in the reference.
 PCT_HD double axis_gradient(bool vn, bool vp, double en, double ep, double ef,
                             const EvalConsts &K) {
-  if (vn && vp) return div_const(en - ep, K.two_rg, K.inv_two_rg);
-  if (vn) return div_const(en - ef, K.rg, K.inv_rg);
-  if (vp) return div_const(ef - ep, K.rg, K.inv_rg);
-  return 0.0;
+  const bool both = vn && vp;
+  const double num = (vn ? en : ef) - (vp ? ep : ef);
+  return div_const(num, both ? K.two_rg : K.rg, both ? K.inv_two_rg : K.inv_rg);
 }
 
 // Neighbourhood of one ground cell: centre e and the 4 axis neighbours
@@ -239,12 +240,15 @@ PCT_HD float gentle_cost_from(double m, const EvalConsts &K, double *cd) {
 
 // float32 terrain cost of the gentle branch (m_grad < theta_s) for the
 // gradient (gx, gy) with s = ax*ax + ay*ay, bit-identical to the reference.
+// The cost from h0 = sqrt(s) is within 2^-48 (relative) of the cost from
+// glibc's hypot; if both ends of the +-2^-44 interval round to the same
+// float32, so does every value inside it (rounding is monotone).
 PCT_HD float gentle_cost32(double gx, double gy, double s, const EvalConsts &K) {
   double cd;
   if (s == 0.0) return 0.0f;  // hypot(0, 0) = 0 exactly
   if (s > 0x1p-900) {         // away from the subnormal range sqrt(s) is within 1 ulp
-    float f = gentle_cost_from(sqrt(s), K, &cd);
-    if (f32_round_safe(cd, f, 0x1p-44)) return f;
+    const float f = gentle_cost_from(sqrt(s), K, &cd);
+    if ((float)(cd * (1.0 + 0x1p-44)) == f && (float)(cd * (1.0 - 0x1p-44)) == f) return f;
   }
   return gentle_cost_from(glibc_hypot(gx, gy), K, &cd);
 }

@@ -55,7 +55,9 @@ int64_t pcth_fast_cells(const float *cross /* n x 5: e l r u d */, const float *
     if (t.valid && t.gentle && !t.isolated && !(t.m_xy > K.theta_b) && t.s != 0.0) {
       double cd;
       float f = gentle_cost_from(sqrt(t.s), K, &cd);
-      if (!(t.s > 0x1p-900 && f32_round_safe(cd, f, 0x1p-44))) ++exact;
+      if (!(t.s > 0x1p-900 && (float)(cd * (1.0 + 0x1p-44)) == f &&
+            (float)(cd * (1.0 - 0x1p-44)) == f))
+        ++exact;
     }
     if (t.valid && t.s >= K.ts2_lo && t.s <= K.ts2_hi) ++exact;
   }

@@ -33,25 +33,28 @@ __host__ inline double dkey_inv(unsigned long long k) {
 
 // ---------------------------------------------------------------- K0 bounds
 // keys[0..2] = min (atomicMin), keys[3..5] = max (atomicMax), keys[6] = #non-finite
+// min/max in the input precision (exact), widened to float64 only at the end
+template <typename T>
 struct MinMax3 {
-  double lo[3], hi[3];
+  T lo[3], hi[3];
   unsigned nonfinite;
 };
 
-__device__ __forceinline__ void mm_point(MinMax3 &m, double x, double y, double z) {
-  const double v[3] = {x, y, z};
+template <typename T>
+__device__ __forceinline__ void mm_point(MinMax3<T> &m, T x, T y, T z) {
+  const T v[3] = {x, y, z};
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
     if (!isfinite(v[c])) m.nonfinite++;
-    m.lo[c] = fmin(m.lo[c], v[c]);
-    m.hi[c] = fmax(m.hi[c], v[c]);
+    m.lo[c] = v[c] < m.lo[c] ? v[c] : m.lo[c];
+    m.hi[c] = v[c] > m.hi[c] ? v[c] : m.hi[c];
   }
 }
 
 template <typename T>
 __global__ void __launch_bounds__(256) bounds_kernel(const T *__restrict__ xyz, int64_t n,
                                                      unsigned long long *keys) {
-  MinMax3 m;
+  MinMax3<T> m;
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
     m.lo[c] = INFINITY;
@@ -82,16 +85,18 @@ __global__ void __launch_bounds__(256) bounds_kernel(const T *__restrict__ xyz, 
   for (int off = 16; off > 0; off >>= 1) {
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      m.lo[c] = fmin(m.lo[c], __shfl_xor_sync(0xffffffffu, m.lo[c], off));
-      m.hi[c] = fmax(m.hi[c], __shfl_xor_sync(0xffffffffu, m.hi[c], off));
+      const T a = __shfl_xor_sync(0xffffffffu, m.lo[c], off);
+      const T b = __shfl_xor_sync(0xffffffffu, m.hi[c], off);
+      m.lo[c] = a < m.lo[c] ? a : m.lo[c];
+      m.hi[c] = b > m.hi[c] ? b : m.hi[c];
     }
     m.nonfinite += __shfl_xor_sync(0xffffffffu, m.nonfinite, off);
   }
   if ((threadIdx.x & 31) == 0) {
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      atomicMin(keys + c, dkey(m.lo[c]));
-      atomicMax(keys + 3 + c, dkey(m.hi[c]));
+      atomicMin(keys + c, dkey((double)m.lo[c]));
+      atomicMax(keys + 3 + c, dkey((double)m.hi[c]));
     }
     if (m.nonfinite) atomicAdd(keys + 6, (unsigned long long)m.nonfinite);
   }
@@ -99,7 +104,7 @@ __global__ void __launch_bounds__(256) bounds_kernel(const T *__restrict__ xyz, 
 
 // ------------------------------------------------------- K1+K2 bin/scatter
 struct BinArgs {
-  double x0, y0, z0, r_g, d_s;
+  double x0, y0, z0, r_g, d_s, inv_rg, inv_ds;
   const double *heights;  // (S,) device
   int64_t cells;
   int rows, cols, S;
@@ -115,9 +120,10 @@ __global__ void __launch_bounds__(256) scatter_kernel(const T *__restrict__ xyz,
     const double x = (double)__ldg(xyz + 3 * p);
     const double y = (double)__ldg(xyz + 3 * p + 1);
     const double z = (double)__ldg(xyz + 3 * p + 2);
-    // rasterisation in float64 (tomogram.py:148-149)
-    const double fi = floor((y - a.y0) / a.r_g + 0.5);
-    const double fj = floor((x - a.x0) / a.r_g + 0.5);
+    // rasterisation in float64 (tomogram.py:148-149); the division is the
+    // correctly rounded Markstein form (== IEEE (y - y0) / r_g)
+    const double fi = floor(div_const(y - a.y0, a.r_g, a.inv_rg) + 0.5);
+    const double fj = floor(div_const(x - a.x0, a.r_g, a.inv_rg) + 0.5);
     if (!(fi >= 0.0 && fi < (double)a.rows && fj >= 0.0 && fj < (double)a.cols)) {
       atomicAdd(outside, 1ull);
       continue;
@@ -125,7 +131,7 @@ __global__ void __launch_bounds__(256) scatter_kernel(const T *__restrict__ xyz,
     const int64_t cell = (int64_t)fi * a.cols + (int64_t)fj;
     // b = #{k : h_k < z}: estimate from the plane spacing, then fix up
     // against the exact float64 heights (searchsorted side="right", :157)
-    double est = floor((z - a.z0) / a.d_s);
+    double est = floor((z - a.z0) * a.inv_ds);  // estimate only; fixed up exactly below
     int b = est < 0.0 ? 0 : (est > (double)a.S ? a.S : (int)est);
     while (b > 0 && __ldg(a.heights + b - 1) >= z) --b;
     while (b < a.S && __ldg(a.heights + b) < z) ++b;
@@ -145,14 +151,38 @@ __global__ void __launch_bounds__(256) scan_kernel(const uint32_t *__restrict__ 
                                                    float *__restrict__ ceiling) {
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= cells) return;
+  // batches of 8 independent loads keep enough bytes in flight per thread
+  constexpr int U = 8;
   uint32_t run = kKeyEmptyMax;
-  for (int k = 0; k < S; ++k) {
+  int k = 0;
+  for (; k + U <= S; k += U) {
+    uint32_t v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = __ldcs(gkey + (int64_t)(k + u) * cells + c);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      run = v[u] > run ? v[u] : run;
+      __stcs(ground + (int64_t)(k + u) * cells + c, decode_ground(run));
+    }
+  }
+  for (; k < S; ++k) {
     const uint32_t v = __ldcs(gkey + (int64_t)k * cells + c);
     run = v > run ? v : run;
     __stcs(ground + (int64_t)k * cells + c, decode_ground(run));
   }
   run = kKeyEmptyMin;
-  for (int k = S - 1; k >= 0; --k) {
+  k = S - 1;
+  for (; k - U + 1 >= 0; k -= U) {
+    uint32_t v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = __ldcs(ckey + (int64_t)(k - u) * cells + c);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      run = v[u] < run ? v[u] : run;
+      __stcs(ceiling + (int64_t)(k - u) * cells + c, decode_ceiling(run));
+    }
+  }
+  for (; k >= 0; --k) {
     const uint32_t v = __ldcs(ckey + (int64_t)k * cells + c);
     run = v < run ? v : run;
     __stcs(ceiling + (int64_t)k * cells + c, decode_ceiling(run));
@@ -214,7 +244,8 @@ int launch_build(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, const pct_
   PCT_CUDA(ctx, cudaMemsetAsync(gkey, 0x00, plane * S, ctx->stream));
   PCT_CUDA(ctx, cudaMemsetAsync(ckey, 0xFF, plane * S, ctx->stream));
   PCT_CUDA(ctx, cudaMemsetAsync(outside, 0, 8, ctx->stream));
-  BinArgs a{fr.origin_x, fr.origin_y, fr.z_min, fr.r_g, fr.d_s, hdev, cells, fr.rows, fr.cols, S};
+  BinArgs a{fr.origin_x, fr.origin_y, fr.z_min, fr.r_g, fr.d_s, 1.0 / fr.r_g, 1.0 / fr.d_s,
+            hdev, cells, fr.rows, fr.cols, S};
   if (n > 0) {
     if (dtype == PCT_F32)
       scatter_kernel<float><<<grid_for(ctx, n, 256, 16), 256, 0, ctx->stream>>>(

@@ -94,7 +94,8 @@ struct FastGeom {
   static constexpr int GWP = WORDS * 32;                      // padded u8 row
   static constexpr int OFF_GEN = LH * LW * 4;
   static constexpr int OFF_BITS = OFF_GEN + GH * GWP;
-  static constexpr int OFF_CINIT = OFF_BITS + GH * WORDS * 4;
+  static constexpr int OFF_FLIST = OFF_BITS + GH * WORDS * 4;  // u16 list of CI cells
+  static constexpr int OFF_CINIT = (OFF_FLIST + CH * CW * 2 + 15) / 16 * 16;
   static constexpr int SMEM = OFF_CINIT + CH * CW * 4;
 };
 
@@ -117,75 +118,117 @@ __global__ void __launch_bounds__(NT, 3) eval_fast_kernel(const float *__restric
   const float nanf_ = bits_f32(kNaNBits);
   const int tid = threadIdx.x;
 
-  // A: ground tile + halo (NaN outside the grid)
-  for (int idx = tid; idx < G::LH * G::LW; idx += NT) {
-    const int y = idx / G::LW, x = idx - y * G::LW;
-    const int gi = i0 - G::H + y, gj = j0 - G::H + x;
-    float v = nanf_;
-    if (gi >= 0 && gi < rows && gj >= 0 && gj < cols) v = __ldg(gk + (int64_t)gi * cols + gj);
-    grd[idx] = v;
-  }
-  __syncthreads();
+  __shared__ int n_flagged;
+  if (tid == 0) n_flagged = 0;
+  // interior tiles (the common case) skip every grid-bounds test
+  const bool interior = i0 - G::H >= 0 && j0 - G::H >= 0 && i0 + TH + G::H <= rows &&
+                        j0 + TW + G::H <= cols;
 
-  // B: gentle flags over the gentle region, encoded c_init over the inner region
-  for (int idx = tid; idx < G::GH * G::GW; idx += NT) {
-    const int y = idx / G::GW, x = idx - y * G::GW;
-    const int gi = i0 - R - PR + y, gj = j0 - R - PR + x;
-    const bool in_grid = gi >= 0 && gi < rows && gj >= 0 && gj < cols;
-    const bool in_ci = y >= PR && y < PR + G::CH && x >= PR && x < PR + G::CW;
-    unsigned char gflag = 0;
-    float enc = 0.0f;  // zero padding outside the map (inflate cval=0)
-    if (in_grid) {
-      const float *p = grd + (y + 1) * G::LW + (x + 1);
-      const Cross c{p[0], p[-1], p[1], p[-G::LW], p[G::LW]};
-      const FastCell t = fast_terrain(c, c_K);
-      gflag = t.gentle ? 1 : 0;
-      if (in_ci) {
-        const float cv = t.valid ? __ldg(ck + (int64_t)gi * cols + gj) : nanf_;
-        enc = fast_cinit(c.e, cv, t, c_K);
+  // A: ground tile + halo (NaN outside the grid); incremental 2D index
+  {
+    int y = tid / G::LW, x = tid - (tid / G::LW) * G::LW;
+    const float *src = gk + (int64_t)(i0 - G::H) * cols + (j0 - G::H);
+    for (int idx = tid; idx < G::LH * G::LW; idx += NT) {
+      float v;
+      if (interior) {
+        v = __ldg(src + (int64_t)y * cols + x);
+      } else {
+        const int gi = i0 - G::H + y, gj = j0 - G::H + x;
+        v = (gi >= 0 && gi < rows && gj >= 0 && gj < cols) ? __ldg(src + (int64_t)y * cols + x)
+                                                           : nanf_;
+      }
+      grd[idx] = v;
+      x += NT % G::LW;
+      y += NT / G::LW;
+      if (x >= G::LW) {
+        x -= G::LW;
+        ++y;
       }
     }
-    gen[y * G::GWP + x] = gflag;
-    if (in_ci) cinit[(y - PR) * G::CW + (x - PR)] = enc;
-  }
-  // zero the padding columns of the flag rows
-  for (int idx = tid; idx < G::GH * (G::GWP - G::GW); idx += NT) {
-    const int y = idx / (G::GWP - G::GW), x = G::GW + idx - y * (G::GWP - G::GW);
-    gen[y * G::GWP + x] = 0;
   }
   __syncthreads();
 
-  // C: pack the flags, 32 cells per word
+  // B: gentle flags over the gentle region, encoded c_init over the inner
+  // region; foothold-branch cells are appended to a list for stage D
+  uint16_t *flist = reinterpret_cast<uint16_t *>(bits + G::GH * G::WORDS);
+  {
+    int y = tid / G::GW, x = tid - (tid / G::GW) * G::GW;
+    const float *crow = ck + (int64_t)(i0 - R) * cols + (j0 - R);  // CI origin
+    for (int idx = tid; idx < G::GH * G::GW; idx += NT) {
+      const int gi = i0 - R - PR + y, gj = j0 - R - PR + x;
+      const bool in_grid = interior || (gi >= 0 && gi < rows && gj >= 0 && gj < cols);
+      const bool in_ci = y >= PR && y < PR + G::CH && x >= PR && x < PR + G::CW;
+      unsigned char gflag = 0;
+      float enc = 0.0f;  // zero padding outside the map (inflate cval=0)
+      if (in_grid) {
+        const float *p = grd + (y + 1) * G::LW + (x + 1);
+        const Cross c{p[0], p[-1], p[1], p[-G::LW], p[G::LW]};
+        const FastCell t = fast_terrain(c, c_K);
+        gflag = t.gentle ? 1 : 0;
+        if (in_ci) {
+          const float cv =
+              t.valid ? __ldg(crow + (int64_t)(y - PR) * cols + (x - PR)) : nanf_;
+          enc = fast_cinit(c.e, cv, t, c_K);
+        }
+      }
+      gen[y * G::GWP + x] = gflag;
+      const int ci_idx = (y - PR) * G::CW + (x - PR);
+      const bool flagged = in_ci && (f32_bits(enc) & 0x80000000u);
+      const unsigned act = __activemask();
+      const unsigned fm = __ballot_sync(act, flagged);
+      if (fm) {
+        const int lane = tid & 31;
+        const int leader = __ffs(fm) - 1;
+        int base = 0;
+        if (lane == leader) base = atomicAdd(&n_flagged, __popc(fm));
+        base = __shfl_sync(act, base, leader);
+        if (flagged) flist[base + __popc(fm & ((1u << lane) - 1u))] = (uint16_t)ci_idx;
+      }
+      if (in_ci) cinit[ci_idx] = enc;
+      x += NT % G::GW;
+      y += NT / G::GW;
+      if (x >= G::GW) {
+        x -= G::GW;
+        ++y;
+      }
+    }
+  }
+  __syncthreads();
+
+  // C: pack the flags, 32 cells per word (bytes past GW are masked off)
   for (int idx = tid; idx < G::GH * G::WORDS; idx += NT) {
     const int y = idx / G::WORDS, w = idx - y * G::WORDS;
-    const uint32_t *src = reinterpret_cast<const uint32_t *>(gen + y * G::GWP + w * 32);
+    const int valid_bits = G::GW - w * 32;
     uint32_t word = 0;
+    if (valid_bits > 0) {
+      const uint32_t *src = reinterpret_cast<const uint32_t *>(gen + y * G::GWP + w * 32);
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const uint32_t v = src[q];  // 4 flags, one per byte
-      word |= ((v & 1u) | ((v >> 7) & 2u) | ((v >> 14) & 4u) | ((v >> 21) & 8u)) << (4 * q);
+      for (int q = 0; q < 8; ++q) {
+        const uint32_t v = src[q];  // 4 flags, one per byte
+        word |= ((v & 1u) | ((v >> 7) & 2u) | ((v >> 14) & 4u) | ((v >> 21) & 8u)) << (4 * q);
+      }
+      if (valid_bits < 32) word &= (1u << valid_bits) - 1u;
     }
     bits[idx] = word;
   }
   __syncthreads();
 
-  // D: foothold test p_s > theta_p  <=>  count >= ps_min_count
+  // D: foothold test p_s > theta_p  <=>  count >= ps_min_count, flagged cells only
   constexpr int SIDE = 2 * PR + 1;
   constexpr uint64_t MASK = (SIDE >= 64) ? ~0ull : ((1ull << SIDE) - 1ull);
-  for (int idx = tid; idx < G::CH * G::CW; idx += NT) {
-    const float enc = cinit[idx];
-    if (f32_bits(enc) & 0x80000000u) {
-      const int y = idx / G::CW, x = idx - y * G::CW;  // window rows y..y+2r, cols x..x+2r
-      const int w = x >> 5, sh = x & 31;
-      int cnt = 0;
+  const int nf = n_flagged;
+  for (int i = tid; i < nf; i += NT) {
+    const int idx = flist[i];
+    const int y = idx / G::CW, x = idx - y * G::CW;  // window rows y..y+2r, cols x..x+2r
+    const int w = x >> 5, sh = x & 31;
+    int cnt = 0;
 #pragma unroll
-      for (int d = 0; d < SIDE; ++d) {
-        const uint32_t *rw = bits + (y + d) * G::WORDS + w;
-        const uint64_t v = (uint64_t)rw[0] | ((uint64_t)rw[1] << 32);
-        cnt += __popcll((v >> sh) & MASK);
-      }
-      cinit[idx] = cinit_resolve(enc, cnt, c_K);
+    for (int d = 0; d < SIDE; ++d) {
+      const uint32_t *rw = bits + (y + d) * G::WORDS + w;
+      const uint64_t v = (uint64_t)rw[0] | ((uint64_t)rw[1] << 32);
+      cnt += __popcll((v >> sh) & MASK);
     }
+    cinit[idx] = cinit_resolve(cinit[idx], cnt, c_K);
   }
   __syncthreads();
 

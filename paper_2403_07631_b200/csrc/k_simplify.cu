@@ -28,7 +28,7 @@
 namespace pct {
 namespace {
 
-constexpr int kWin = 32;      // lower-neighbour window of window_kernel
+constexpr int kWin = 16;      // lower-neighbour window of window_kernel (power of 2)
 constexpr int kBit = 32;      // bit index for "no lower neighbour"
 constexpr int kWinNT = 128;
 
@@ -50,9 +50,15 @@ __device__ __forceinline__ bool not_covered(float e, float cst, float enb, float
   return higher || (cst < cnb);
 }
 
+// lower-side test with the neighbour's elevation already widened (NaN = invalid)
+__device__ __forceinline__ bool not_covered_below(double e, float cst, double enb, float cnb,
+                                                  double eps) {
+  return isnan(enb) || (e - enb > eps) || (cst < cnb);
+}
+
 __global__ void __launch_bounds__(kWinNT) window_kernel(SimpArgs A,
                                                         unsigned long long *__restrict__ table) {
-  __shared__ float ring_e[kWin][kWinNT];
+  __shared__ double ring_e[kWin][kWinNT];
   __shared__ float ring_c[kWin][kWinNT];
   __shared__ unsigned long long bmask;
   const int64_t cell = (int64_t)blockIdx.x * kWinNT + threadIdx.x;
@@ -73,10 +79,11 @@ __global__ void __launch_bounds__(kWinNT) window_kernel(SimpArgs A,
         (k + 1 >= A.S || not_covered(e_cur, c_cur, e_up, c_up, A.eps_e, false))) {
       m = 1ull << kBit;
       const int depth = k < kWin ? k : kWin;
+      const double ed = (double)e_cur;
       for (int j = 0; j < depth; ++j) {  // a = k-1-j
-        const int slot = (k - 1 - j) % kWin;
-        if (not_covered(e_cur, c_cur, ring_e[slot][threadIdx.x], ring_c[slot][threadIdx.x],
-                        A.eps_e, true))
+        const int slot = (k - 1 - j) & (kWin - 1);
+        if (not_covered_below(ed, c_cur, ring_e[slot][threadIdx.x], ring_c[slot][threadIdx.x],
+                              A.eps_e))
           m |= 1ull << j;
       }
     }
@@ -87,8 +94,8 @@ __global__ void __launch_bounds__(kWinNT) window_kernel(SimpArgs A,
     __syncthreads();
     if ((threadIdx.x & 31) == 0 && (lo | hi))
       atomicOr(&bmask, ((unsigned long long)hi << 32) | lo);
-    ring_e[k % kWin][threadIdx.x] = e_cur;
-    ring_c[k % kWin][threadIdx.x] = c_cur;
+    ring_e[k & (kWin - 1)][threadIdx.x] = (double)e_cur;  // NaN stays NaN
+    ring_c[k & (kWin - 1)][threadIdx.x] = c_cur;
     __syncthreads();
     if (threadIdx.x == 0 && bmask) atomicOr(table + k, bmask);
     __syncthreads();
