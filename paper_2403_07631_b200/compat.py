@@ -1,0 +1,67 @@
+"""Install the GPU path into an existing ``tomoplan`` (the reference package).
+
+    import tomoplan
+    from paper_2403_07631_b200 import compat
+    compat.install(tomoplan)      # tomoplan.build_tomogram & co. now run on the B200
+
+Replaces the hot-path entry points everywhere the reference binds them:
+the package namespace (tomoplan/__init__.py:14-45), the defining modules
+(tomogram.py, traversability.py, simplify.py) and the modules that imported
+them by name (cli.py:20, bench.py:19).  Everything downstream (planner,
+trajectory, LGA save/load, CLI) consumes the returned objects by duck
+typing: ``Tomogram.slices[k].ground/ceiling/cost.values`` are (rows, cols)
+float32 numpy arrays, ``ground_stack()`` / ``cost_stack()`` exist.
+``uninstall()`` restores the originals.
+"""
+
+from __future__ import annotations
+
+import importlib
+
+from . import simplify as _simp
+from . import tomogram as _tomo
+from . import traversability as _trav
+
+# name -> replacement
+REPLACEMENTS = {
+    "build_tomogram": _tomo.build_tomogram,
+    "evaluate_tomogram": _trav.evaluate_tomogram,
+    "evaluate_slice": _trav.evaluate_slice,
+    "interval_cost": _trav.interval_cost,
+    "ground_cost": _trav.ground_cost,
+    "slope_magnitudes": _trav.slope_magnitudes,
+    "gentle_fraction": _trav.gentle_fraction,
+    "terrain_cost_values": _trav.terrain_cost_values,
+    "fuse_costs": _trav.fuse_costs,
+    "inflate": _trav.inflate,
+    "simplify_tomogram": _simp.simplify_tomogram,
+    "unique_cells": _simp.unique_cells,
+}
+
+MODULES = ("", ".tomogram", ".traversability", ".simplify", ".cli", ".bench")
+
+_saved: list = []
+
+
+def install(package=None) -> list:
+    """Patch ``package`` (default: ``import tomoplan``); returns the patched
+    (module, name) pairs."""
+    pkg = package if package is not None else importlib.import_module("tomoplan")
+    patched = []
+    for suffix in MODULES:
+        try:
+            mod = importlib.import_module(pkg.__name__ + suffix) if suffix else pkg
+        except Exception:  # e.g. bench needs matplotlib
+            continue
+        for name, fn in REPLACEMENTS.items():
+            if hasattr(mod, name) and getattr(mod, name) is not fn:
+                _saved.append((mod, name, getattr(mod, name)))
+                setattr(mod, name, fn)
+                patched.append((mod.__name__, name))
+    return patched
+
+
+def uninstall() -> None:
+    while _saved:
+        mod, name, orig = _saved.pop()
+        setattr(mod, name, orig)

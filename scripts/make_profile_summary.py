@@ -1,0 +1,53 @@
+"""Copy the ncu evidence of one gpurun call into profiles/ (tracked).
+
+    python scripts/make_profile_summary.py <tag> <round-name> [config]
+
+Writes profiles/<round>_launches.csv (per-launch device time + DRAM bytes of one
+bench step, from `ncu --metrics gpu__time_duration.sum,dram__bytes_*`),
+profiles/<round>_<kernel>_ncu.txt (the --set full details page of the top
+kernel + its SASS opcode histogram) and updates profiles/ncu_traffic.json
+(DRAM bytes per launch of the evaluate kernel, read by bench.py)."""
+import collections, csv, io, json, re, subprocess, sys
+from pathlib import Path
+
+tag, rnd = sys.argv[1], sys.argv[2]
+cfg = sys.argv[3] if len(sys.argv) > 3 else "cfg1"
+out = Path("profiles"); out.mkdir(exist_ok=True)
+src = Path(f"gpurun_out/launches_{tag}.csv")
+rows = [r for r in csv.reader(l for l in src.read_text().splitlines() if not l.startswith("=="))]
+h = rows[0]; ki, mi, vi, ii = (h.index(x) for x in ("Kernel Name", "Metric Name", "Metric Value", "ID"))
+per = collections.OrderedDict()
+for r in rows[1:]:
+    per.setdefault(r[ii], {"kernel": r[ki]})[r[mi]] = float(r[vi].replace(",", ""))
+launches = list(per.values())
+half = launches[len(launches) // 2:]  # the timed step (after the warm-up step)
+half = [v for v in half if "pct::" in v["kernel"]]  # the L2 flush between steps is not in the step
+tot = sum(v.get("gpu__time_duration.sum", 0) for v in half)
+with open(out / f"{rnd}_launches.csv", "w") as f:
+    f.write("kernel,time_us,share,dram_read_MB,dram_write_MB\n")
+    for v in half:
+        t = v.get("gpu__time_duration.sum", 0)
+        f.write(f"\"{v['kernel'][:90]}\",{t/1e3:.1f},{t/tot:.3f},"
+                f"{v.get('dram__bytes_read.sum',0)/1e6:.1f},{v.get('dram__bytes_write.sum',0)/1e6:.1f}\n")
+rep = Path(f"gpurun_out/prof_{tag}.ncu-rep")
+if rep.exists():
+    det = subprocess.run(["ncu", "-i", str(rep), "--page", "details", "--csv"], capture_output=True, text=True).stdout
+    lines = list(csv.reader(io.StringIO(det)))
+    hh = lines[0]
+    kname = lines[1][hh.index("Kernel Name")] if len(lines) > 1 else "?"
+    short = re.sub(r"[^a-z_]", "", kname.split("(")[0].split("::")[-1].split("<")[0])
+    body = [f"ncu --set full --clock-control none, report {rep.name}", f"kernel: {kname}", ""]
+    si, mi2, vi2, ui = (hh.index(x) for x in ("Section Name", "Metric Name", "Metric Value", "Metric Unit"))
+    for r in lines[1:]:
+        body.append(f"{r[si][:30]:30s} {r[mi2][:55]:55s} {r[vi2]} {r[ui]}")
+    ops = subprocess.run([sys.executable, "scripts/ncu_ops.py", str(rep), "24"], capture_output=True, text=True).stdout
+    (out / f"{rnd}_{short}_ncu.txt").write_text("\n".join(body) + "\n\nSASS opcode histogram:\n" + ops)
+    m = {r[mi2]: r[vi2] for r in lines[1:]}
+tr_path = out / "ncu_traffic.json"
+tr = json.loads(tr_path.read_text()) if tr_path.exists() else {}
+for v in half:
+    if "eval" in v["kernel"]:
+        tr[cfg] = {"kernel": v["kernel"][:80], "eval_dram_bytes": v.get("dram__bytes_read.sum", 0) + v.get("dram__bytes_write.sum", 0),
+                   "eval_time_us_ncu": v.get("gpu__time_duration.sum", 0) / 1e3, "source": f"{rnd}_launches.csv"}
+tr_path.write_text(json.dumps(tr, indent=1))
+print("wrote", sorted(p.name for p in out.iterdir()))
