@@ -240,6 +240,8 @@ __global__ void __launch_bounds__(NT, 3) eval_fast_kernel(const float *__restric
                           rows, cols);
 }
 
+#include "k_eval_incr.cuh"
+
 // ---------------------------------------------------------- generic kernel
 struct TileGeom {
   int R, r;            // inflation radius, patch radius
@@ -443,9 +445,33 @@ int ps_min_count(double theta_p, int radius) {
 
 constexpr int kNT = 256;
 
+// slice-incremental kernel: runs of consecutive slices per CTA, run length
+// chosen so the grid still fills ~2 waves of 2 CTAs per SM
+template <int R, int PR>
+int launch_incr(pct_ctx *ctx, const float *ground, const float *ceiling, int S, int rows,
+                int cols, float *cost) {
+  constexpr int TH = 64, TW = 64;
+  auto kern = eval_incr_kernel<R, PR, TH, TW, kNT>;
+  constexpr int smem = IncrGeom<R, PR, TH, TW>::SMEM;
+  PCT_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  const int tx = (cols + TW - 1) / TW, ty = (rows + TH - 1) / TH;
+  const int64_t tiles = (int64_t)tx * ty;
+  const int64_t target = 4LL * ctx->num_sms;  // CTAs wanted
+  int run = (int)std::max<int64_t>(4, (S * tiles + target - 1) / target);
+  if (const char *e = getenv("PCT_EVAL_RUN")) run = std::max(1, atoi(e));
+  run = std::min(run, S);
+  const int chunks = (S + run - 1) / run;
+  dim3 grid(tx, ty, chunks);
+  kern<<<grid, kNT, smem, ctx->stream>>>(ground, ceiling, rows, cols, S, run, cost);
+  return check_launch(ctx, "eval_incr_kernel");
+}
+
 template <int R, int PR>
 int launch_fast(pct_ctx *ctx, const float *ground, const float *ceiling, int S, int rows,
                 int cols, float *cost) {
+  const char *mode = getenv("PCT_EVAL_KERNEL");
+  if (!(mode && mode[0] == 'f') && S > 1)  // default: incremental
+    return launch_incr<R, PR>(ctx, ground, ceiling, S, rows, cols, cost);
   constexpr int TH = 64, TW = 64;
   auto kern = eval_fast_kernel<R, PR, TH, TW, kNT>;
   constexpr int smem = FastGeom<R, PR, TH, TW>::SMEM;

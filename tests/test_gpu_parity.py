@@ -64,6 +64,22 @@ def test_pipeline_matches_reference_golden(golden, name):
     assert [s.index for s in simp.slices] == list(range(len(simp.slices)))
 
 
+@pytest.mark.parametrize("run", ["1", "2", "5", "64"])
+def test_incremental_runs_match_full_kernel(golden, monkeypatch, run):
+    """The slice-incremental kernel gives the same bytes for any run length
+    as the full per-slice kernel (PCT_EVAL_KERNEL=fast)."""
+    case = golden["cases"]["synth_cfg0"]
+    tom = pct.build_tomogram(pct.PointCloud(case_input("synth_cfg0", case)), 0.5, 0.1)
+    monkeypatch.setenv("PCT_EVAL_KERNEL", "fast")
+    full = pct.evaluate_tomogram(tom, pct.TravParams()).cost_stack()
+    monkeypatch.setenv("PCT_EVAL_KERNEL", "incr")
+    monkeypatch.setenv("PCT_EVAL_RUN", run)
+    inc = pct.evaluate_tomogram(tom, pct.TravParams()).cost_stack()
+    assert np.array_equal(full.view(np.uint32), inc.view(np.uint32))
+    for k in range(full.shape[0]):
+        assert digest(inc[k]) == case["cost_slice_sha256"][k]
+
+
 def test_f32_and_f64_inputs_agree(golden):
     case = golden["cases"]["synth_cfg0"]
     xyz = case_input("synth_cfg0", case)
