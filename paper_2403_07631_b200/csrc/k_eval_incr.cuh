@@ -118,6 +118,8 @@ template <int R, int PR, int TH, int TW, int NT>
 __global__ void __launch_bounds__(NT, 2) eval_incr_kernel(const float *__restrict__ ground,
                                                           const float *__restrict__ ceiling,
                                                           int rows, int cols, int S, int run,
+                                                          int tiles_x, int n_tiles, int n_items,
+                                                          int *__restrict__ next_item,
                                                           float *__restrict__ cost) {
   using G = IncrGeom<R, PR, TH, TW>;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -135,12 +137,10 @@ __global__ void __launch_bounds__(NT, 2) eval_incr_kernel(const float *__restric
   uint32_t *ichg = reinterpret_cast<uint32_t *>(smem + G::O_ICHG);
   uint16_t *list = reinterpret_cast<uint16_t *>(smem + G::O_LIST);
   __shared__ int cnt;
+  __shared__ int item_s;
 
   const int tid = threadIdx.x;
   const int64_t plane = (int64_t)rows * cols;
-  const int i0 = blockIdx.y * TH, j0 = blockIdx.x * TW;
-  const int k0 = blockIdx.z * run;
-  const int k1 = min(S, k0 + run);
   const float nanf_ = bits_f32(kNaNBits);
   const float cb32 = (float)c_K.c_barrier;
   constexpr int SIDE = 2 * PR + 1;
@@ -149,6 +149,18 @@ __global__ void __launch_bounds__(NT, 2) eval_incr_kernel(const float *__restric
   constexpr int V = TH / STRIPS;
   const int ox = tid % TW, strip = tid / TW;
   float outv[V];
+
+  // persistent CTAs pull (tile, slice run) items; runs of one tile differ in
+  // cost (first slice full, the rest incremental), so balance dynamically
+  for (;;) {
+  if (tid == 0) item_s = atomicAdd(next_item, 1);
+  __syncthreads();
+  const int item = item_s;
+  if (item >= n_items) break;
+  const int tile = item % n_tiles, chunk = item / n_tiles;
+  const int i0 = (tile / tiles_x) * TH, j0 = (tile % tiles_x) * TW;
+  const int k0 = chunk * run;
+  const int k1 = min(S, k0 + run);
 
   // persistent state starts "unknown": force a full first slice
   for (int i = tid; i < G::LH * G::LW; i += NT) grd[i] = bits_f32(0x7FFFFFFFu);  // never loaded
@@ -174,25 +186,47 @@ __global__ void __launch_bounds__(NT, 2) eval_incr_kernel(const float *__restric
     if (tid == 0) cnt = 0;
     __syncthreads();
 
-    // ---- A: load ground region and CI ceiling, note changed cells
-    for (int idx = tid; idx < G::LH * G::LW; idx += NT) {
-      const int y = idx / G::LW, x = idx - y * G::LW;
-      const int gi = i0 - G::H + y, gj = j0 - G::H + x;
-      float v = nanf_;
-      if (gi >= 0 && gi < rows && gj >= 0 && gj < cols) v = __ldg(gk + (int64_t)gi * cols + gj);
-      if (f32_bits(v) != f32_bits(grd[idx])) {
-        grd[idx] = v;
-        atomicOr(&gchg[y * G::LWW + (x >> 5)], 1u << (x & 31));
+    // ---- A: load ground region and CI ceiling (all loads of a thread in
+    // flight together), note changed cells
+    {
+      constexpr int NA = (G::LH * G::LW + NT - 1) / NT;
+      constexpr int NC = (G::CH * G::CW + NT - 1) / NT;
+      float va[NA], vc[NC];
+#pragma unroll
+      for (int u = 0; u < NA; ++u) {
+        const int idx = tid + u * NT;
+        const int y = idx / G::LW, x = idx - y * G::LW;
+        const int gi = i0 - G::H + y, gj = j0 - G::H + x;
+        va[u] = (idx < G::LH * G::LW && gi >= 0 && gi < rows && gj >= 0 && gj < cols)
+                    ? __ldg(gk + (int64_t)gi * cols + gj)
+                    : nanf_;
       }
-    }
-    for (int idx = tid; idx < G::CH * G::CW; idx += NT) {
-      const int y = idx / G::CW, x = idx - y * G::CW;
-      const int gi = i0 - R + y, gj = j0 - R + x;
-      float v = nanf_;
-      if (gi >= 0 && gi < rows && gj >= 0 && gj < cols) v = __ldg(ck + (int64_t)gi * cols + gj);
-      if (f32_bits(v) != f32_bits(ceil_s[idx])) {
-        ceil_s[idx] = v;
-        atomicOr(&cchg[y * G::CWW + (x >> 5)], 1u << (x & 31));
+#pragma unroll
+      for (int u = 0; u < NC; ++u) {
+        const int idx = tid + u * NT;
+        const int y = idx / G::CW, x = idx - y * G::CW;
+        const int gi = i0 - R + y, gj = j0 - R + x;
+        vc[u] = (idx < G::CH * G::CW && gi >= 0 && gi < rows && gj >= 0 && gj < cols)
+                    ? __ldg(ck + (int64_t)gi * cols + gj)
+                    : nanf_;
+      }
+#pragma unroll
+      for (int u = 0; u < NA; ++u) {
+        const int idx = tid + u * NT;
+        if (idx < G::LH * G::LW && f32_bits(va[u]) != f32_bits(grd[idx])) {
+          const int y = idx / G::LW, x = idx - y * G::LW;
+          grd[idx] = va[u];
+          atomicOr(&gchg[y * G::LWW + (x >> 5)], 1u << (x & 31));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < NC; ++u) {
+        const int idx = tid + u * NT;
+        if (idx < G::CH * G::CW && f32_bits(vc[u]) != f32_bits(ceil_s[idx])) {
+          const int y = idx / G::CW, x = idx - y * G::CW;
+          ceil_s[idx] = vc[u];
+          atomicOr(&cchg[y * G::CWW + (x >> 5)], 1u << (x & 31));
+        }
       }
     }
     __syncthreads();
@@ -336,4 +370,5 @@ __global__ void __launch_bounds__(NT, 2) eval_incr_kernel(const float *__restric
     }
     __syncthreads();
   }
+  }  // work items
 }

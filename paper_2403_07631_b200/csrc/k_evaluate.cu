@@ -456,13 +456,18 @@ int launch_incr(pct_ctx *ctx, const float *ground, const float *ceiling, int S, 
   PCT_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const int tx = (cols + TW - 1) / TW, ty = (rows + TH - 1) / TH;
   const int64_t tiles = (int64_t)tx * ty;
-  const int64_t target = 4LL * ctx->num_sms;  // CTAs wanted
+  const int64_t slots = 2LL * ctx->num_sms;   // resident CTAs (2 per SM)
+  const int64_t target = 4 * slots;           // work items wanted for balance
   int run = (int)std::max<int64_t>(4, (S * tiles + target - 1) / target);
   if (const char *e = getenv("PCT_EVAL_RUN")) run = std::max(1, atoi(e));
   run = std::min(run, S);
-  const int chunks = (S + run - 1) / run;
-  dim3 grid(tx, ty, chunks);
-  kern<<<grid, kNT, smem, ctx->stream>>>(ground, ceiling, rows, cols, S, run, cost);
+  const int64_t items = tiles * ((S + run - 1) / run);
+  if (items > INT32_MAX || tiles > INT32_MAX) return fail(ctx, PCT_E_INVALID, "grid too large");
+  int *counter = reinterpret_cast<int *>(static_cast<char *>(ctx->dsmall) + 65536 - 64);
+  PCT_CUDA(ctx, cudaMemsetAsync(counter, 0, sizeof(int), ctx->stream));
+  const unsigned grid = (unsigned)std::min<int64_t>(items, slots);
+  kern<<<grid, kNT, smem, ctx->stream>>>(ground, ceiling, rows, cols, S, run, tx, (int)tiles,
+                                         (int)items, counter, cost);
   return check_launch(ctx, "eval_incr_kernel");
 }
 
