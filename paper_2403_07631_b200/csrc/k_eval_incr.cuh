@@ -114,8 +114,8 @@ __device__ __forceinline__ void inflate_strip_regs(const float *__restrict__ cin
   }
 }
 
-template <int R, int PR, int TH, int TW, int NT>
-__global__ void __launch_bounds__(NT, 2) eval_incr_kernel(const float *__restrict__ ground,
+template <int R, int PR, int TH, int TW, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) eval_incr_kernel(const float *__restrict__ ground,
                                                           const float *__restrict__ ceiling,
                                                           int rows, int cols, int S, int run,
                                                           int tiles_x, int n_tiles, int n_items,

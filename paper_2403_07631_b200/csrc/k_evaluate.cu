@@ -83,6 +83,73 @@ __device__ __forceinline__ void inflate_sym_strip(const float *__restrict__ cini
   }
 }
 
+// --------------------------------------- stage E, symmetric, 4 < R <= 8
+// A (2R+1) x (R+1) ring does not fit in registers; the pair maxima P_b are
+// split between two warp roles: LO owns b in [0, B0], HI owns b in
+// [B0+1, R].  Every tap group (a, b) contributes w_ab * max(P_b(i+-a)) from
+// the owner of b and w_ab * max(P_a(i+-b)) from the owner of a; since
+// x -> fl32(w x) is monotone, max over both partials is the full result.
+// The row loop is unrolled by template recursion (nvcc's #pragma unroll gives
+// up on this body size and would move the ring to local memory).
+template <int R, int BL, int NB, int V, int T>
+__device__ __forceinline__ void half_step(float (&P)[V + 2 * R][NB], const float *__restrict__ cinit,
+                                          int CW, int x, int ys, float *__restrict__ part,
+                                          int pstride) {
+  if constexpr (T < V + 2 * R) {
+    const float *rowp = cinit + (ys + T) * CW + x;
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      const int b = BL + j;
+      P[T][j] = b == 0 ? rowp[R] : fmaxf(rowp[R - b], rowp[R + b]);
+    }
+    if constexpr (T >= 2 * R) {
+      constexpr int o = T - 2 * R, c = o + R;
+      float acc = 0.0f;
+#pragma unroll
+      for (int a = 0; a <= R; ++a) {
+#pragma unroll
+        for (int b = 0; b <= a; ++b) {
+          const float w = c_wsym[a * 9 + b];
+          if (w > 0.0f) {
+            const bool own_b = b >= BL && b < BL + NB;
+            const bool own_a = a >= BL && a < BL + NB;
+            const int jb = own_b ? b - BL : 0, ja = own_a ? a - BL : 0;  // in-range indices
+            float m = 0.0f;
+            bool any = false;
+            if (a == 0) {
+              if (own_b) { m = P[c][jb]; any = true; }
+            } else if (b == 0) {
+              if (own_b) { m = fmaxf(P[c - a][jb], P[c + a][jb]); any = true; }
+              if (own_a) { m = any ? fmaxf(m, P[c][ja]) : P[c][ja]; any = true; }
+            } else if (a == b) {
+              if (own_a) { m = fmaxf(P[c - a][ja], P[c + a][ja]); any = true; }
+            } else {
+              if (own_b) { m = fmaxf(P[c - a][jb], P[c + a][jb]); any = true; }
+              if (own_a) {
+                const float q = fmaxf(P[c - b][ja], P[c + b][ja]);
+                m = any ? fmaxf(m, q) : q;
+                any = true;
+              }
+            }
+            if (any) acc = fmaxf(acc, w * m);
+          }
+        }
+      }
+      part[(ys + o) * pstride + x] = acc;
+    }
+    half_step<R, BL, NB, V, T + 1>(P, cinit, CW, x, ys, part, pstride);
+  }
+}
+
+template <int R, int B0, int V, bool HI>
+__device__ __forceinline__ void inflate_half_strip(const float *__restrict__ cinit, int CW, int x,
+                                                   int ys, float *__restrict__ part, int pstride) {
+  constexpr int BL = HI ? B0 + 1 : 0;
+  constexpr int NB = HI ? R - B0 : B0 + 1;
+  float P[V + 2 * R][NB];
+  half_step<R, BL, NB, V, 0>(P, cinit, CW, x, ys, part, pstride);
+}
+
 // ------------------------------------------------------------- fast kernel
 template <int R, int PR, int TH, int TW>
 struct FastGeom {
@@ -99,8 +166,8 @@ struct FastGeom {
   static constexpr int SMEM = OFF_CINIT + CH * CW * 4;
 };
 
-template <int R, int PR, int TH, int TW, int NT>
-__global__ void __launch_bounds__(NT, 3) eval_fast_kernel(const float *__restrict__ ground,
+template <int R, int PR, int TH, int TW, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) eval_fast_kernel(const float *__restrict__ ground,
                                                        const float *__restrict__ ceiling,
                                                        int rows, int cols,
                                                        float *__restrict__ cost) {
@@ -233,11 +300,41 @@ __global__ void __launch_bounds__(NT, 3) eval_fast_kernel(const float *__restric
   __syncthreads();
 
   // E: inflation
-  constexpr int STRIPS = NT / TW;
-  constexpr int V = TH / STRIPS;
-  const int x = tid % TW, s = tid / TW;
-  inflate_sym_strip<R, V>(cinit, G::CW, x, s * V, cost + k * plane, cols, i0 + s * V, j0 + x,
-                          rows, cols);
+  if constexpr (R <= 4) {
+    constexpr int STRIPS = NT / TW;
+    constexpr int V = TH / STRIPS;
+    const int x = tid % TW, s = tid / TW;
+    inflate_sym_strip<R, V>(cinit, G::CW, x, s * V, cost + k * plane, cols, i0 + s * V, j0 + x,
+                            rows, cols);
+  } else {
+    // warps: [strip][role][column half]; partial maxima of both roles go to
+    // the (now dead) ground region, then are merged and stored coalesced
+    static_assert(TW == 64 && NT == 256, "split inflation layout");
+    constexpr int V = TH / 2;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int x = (warp & 1) * 32 + lane;
+    const bool hi = (warp >> 1) & 1;
+    const int s = warp >> 2;
+    float *part_lo = grd;
+    float *part_hi = grd + TH * TW;
+    // two sub-strips of V/2 rows keep the fully unrolled ring in registers
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+      if (hi)
+        inflate_half_strip<R, R / 2, V / 2, true>(cinit, G::CW, x, s * V + h * (V / 2), part_hi,
+                                                  TW);
+      else
+        inflate_half_strip<R, R / 2, V / 2, false>(cinit, G::CW, x, s * V + h * (V / 2), part_lo,
+                                                   TW);
+    }
+    __syncthreads();
+    float *out = cost + k * plane;
+    for (int idx = tid; idx < TH * TW; idx += NT) {
+      const int oy = idx / TW, ox = idx - oy * TW;
+      const int gi = i0 + oy, gj = j0 + ox;
+      if (gi < rows && gj < cols) out[(int64_t)gi * cols + gj] = fmaxf(part_lo[idx], part_hi[idx]);
+    }
+  }
 }
 
 #include "k_eval_incr.cuh"
@@ -421,7 +518,7 @@ __global__ void __launch_bounds__(NT) inflate_kernel(TileGeom G, const float *__
 
 // ---------------------------------------------------------------- host side
 bool symmetric_kernel(const float *w, int kside, int R, float wsym[81]) {
-  if (R > 4) return false;
+  if (R > 8) return false;
   for (int i = 0; i < 81; ++i) wsym[i] = 0.0f;
   for (int a = 0; a <= R; ++a)
     for (int b = 0; b <= a; ++b) wsym[a * 9 + b] = w[(R + a) * kside + (R + b)];
@@ -447,18 +544,21 @@ constexpr int kNT = 256;
 
 // slice-incremental kernel: runs of consecutive slices per CTA, run length
 // chosen so the grid still fills ~2 waves of 2 CTAs per SM
-template <int R, int PR>
-int launch_incr(pct_ctx *ctx, const float *ground, const float *ceiling, int S, int rows,
-                int cols, float *cost) {
-  constexpr int TH = 64, TW = 64;
-  auto kern = eval_incr_kernel<R, PR, TH, TW, kNT>;
+template <int R, int PR, int TH, int TW, int NT, int MINB>
+int launch_incr_t(pct_ctx *ctx, const float *ground, const float *ceiling, int S, int rows,
+                  int cols, float *cost) {
+  auto kern = eval_incr_kernel<R, PR, TH, TW, NT, MINB>;
   constexpr int smem = IncrGeom<R, PR, TH, TW>::SMEM;
   PCT_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const int tx = (cols + TW - 1) / TW, ty = (rows + TH - 1) / TH;
   const int64_t tiles = (int64_t)tx * ty;
-  const int64_t slots = 2LL * ctx->num_sms;   // resident CTAs (2 per SM)
-  const int64_t target = 4 * slots;           // work items wanted for balance
-  int run = (int)std::max<int64_t>(4, (S * tiles + target - 1) / target);
+  int per_sm = 0;
+  PCT_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
+  const int64_t slots = (int64_t)std::max(1, per_sm) * ctx->num_sms;  // resident CTAs
+  // runs of 12 slices (measured best on cfg1), shorter if the grid would
+  // otherwise not get ~2 work items per resident CTA
+  int run = 12;
+  while (run > 4 && tiles * ((S + run - 1) / run) < 2 * slots) run /= 2;
   if (const char *e = getenv("PCT_EVAL_RUN")) run = std::max(1, atoi(e));
   run = std::min(run, S);
   const int64_t items = tiles * ((S + run - 1) / run);
@@ -466,19 +566,33 @@ int launch_incr(pct_ctx *ctx, const float *ground, const float *ceiling, int S, 
   int *counter = reinterpret_cast<int *>(static_cast<char *>(ctx->dsmall) + 65536 - 64);
   PCT_CUDA(ctx, cudaMemsetAsync(counter, 0, sizeof(int), ctx->stream));
   const unsigned grid = (unsigned)std::min<int64_t>(items, slots);
-  kern<<<grid, kNT, smem, ctx->stream>>>(ground, ceiling, rows, cols, S, run, tx, (int)tiles,
-                                         (int)items, counter, cost);
+  kern<<<grid, NT, smem, ctx->stream>>>(ground, ceiling, rows, cols, S, run, tx, (int)tiles,
+                                        (int)items, counter, cost);
   return check_launch(ctx, "eval_incr_kernel");
 }
 
+// Kernel choice for symmetric kernels with compiled geometry: the
+// slice-incremental kernel when there are enough slices to amortise each
+// run's full first slice and enough 32x32 tiles to fill the GPU (measured:
+// cfg1 297 us vs 386 us; small maps are faster with the per-slice kernel).
+// PCT_EVAL_KERNEL=fast|incr, PCT_EVAL_TILE=32|64 and PCT_EVAL_RUN override.
 template <int R, int PR>
 int launch_fast(pct_ctx *ctx, const float *ground, const float *ceiling, int S, int rows,
                 int cols, float *cost) {
-  const char *mode = getenv("PCT_EVAL_KERNEL");
-  if (!(mode && mode[0] == 'f') && S > 1)  // default: incremental
-    return launch_incr<R, PR>(ctx, ground, ceiling, S, rows, cols, cost);
+  bool incr = false;
+  if constexpr (R <= 4) {
+    const int64_t tiles32 = (int64_t)((rows + 31) / 32) * ((cols + 31) / 32);
+    incr = S >= 8 && tiles32 >= 2LL * ctx->num_sms;
+    if (const char *m = getenv("PCT_EVAL_KERNEL")) incr = m[0] == 'i' && S > 1;
+    if (incr) {
+      const char *t = getenv("PCT_EVAL_TILE");
+      if (t && atoi(t) == 64)
+        return launch_incr_t<R, PR, 64, 64, 256, 2>(ctx, ground, ceiling, S, rows, cols, cost);
+      return launch_incr_t<R, PR, 32, 32, 128, 4>(ctx, ground, ceiling, S, rows, cols, cost);
+    }
+  }
   constexpr int TH = 64, TW = 64;
-  auto kern = eval_fast_kernel<R, PR, TH, TW, kNT>;
+  auto kern = eval_fast_kernel<R, PR, TH, TW, kNT, (R <= 4 ? 3 : 2)>;
   constexpr int smem = FastGeom<R, PR, TH, TW>::SMEM;
   PCT_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   dim3 grid((cols + TW - 1) / TW, (rows + TH - 1) / TH, S);
@@ -543,6 +657,8 @@ int launch_evaluate(pct_ctx *ctx, const float *ground, const float *ceiling, int
     return launch_fast<3, 3>(ctx, ground, ceiling, S, rows, cols, cost);
   if (sym && R == 4 && p.patch_radius == 4)
     return launch_fast<4, 4>(ctx, ground, ceiling, S, rows, cols, cost);
+  if (sym && R == 8 && p.patch_radius == 6)  // r_g = 0.05 with the Table-I radii
+    return launch_fast<8, 6>(ctx, ground, ceiling, S, rows, cols, cost);
   // generic path: pick the largest square-ish tile that fits in shared memory
   int TH = 64, TW = 64;
   TileGeom G = make_geom(R, p.patch_radius, TH, TW);
