@@ -92,13 +92,29 @@ __global__ void __launch_bounds__(256) bounds_kernel(const T *__restrict__ xyz, 
     }
     m.nonfinite += __shfl_xor_sync(0xffffffffu, m.nonfinite, off);
   }
+  // block reduce through shared memory: one atomic per block and component
+  // (per-warp atomics on 6 addresses serialised in L2 and dominated the kernel)
+  __shared__ unsigned long long red[8][7];
+  const int warp = threadIdx.x >> 5;
   if ((threadIdx.x & 31) == 0) {
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      atomicMin(keys + c, dkey((double)m.lo[c]));
-      atomicMax(keys + 3 + c, dkey((double)m.hi[c]));
+      red[warp][c] = dkey((double)m.lo[c]);
+      red[warp][3 + c] = dkey((double)m.hi[c]);
     }
-    if (m.nonfinite) atomicAdd(keys + 6, (unsigned long long)m.nonfinite);
+    red[warp][6] = m.nonfinite;
+  }
+  __syncthreads();
+  if (threadIdx.x < 7) {
+    const int c = threadIdx.x;
+    unsigned long long v = red[0][c];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+      const unsigned long long u = red[w][c];
+      v = c < 3 ? (u < v ? u : v) : (c < 6 ? (u > v ? u : v) : v + u);
+    }
+    if (c < 3) atomicMin(keys + c, v);
+    else if (c < 6) atomicMax(keys + c, v);
+    else if (v) atomicAdd(keys + 6, v);
   }
 }
 

@@ -19,6 +19,7 @@
 //    a triple is known unique.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <map>
 #include <tuple>
 #include <vector>
@@ -56,52 +57,57 @@ __device__ __forceinline__ bool not_covered_below(double e, float cst, double en
   return isnan(enb) || (e - enb > eps) || (cst < cnb);
 }
 
+// Persistent blocks walk cells grid-stride; a thread owns one cell at a time
+// and walks its slices; warps OR their masks into a per-block table in
+// shared memory (no block barrier per slice), flushed once at the end.
 __global__ void __launch_bounds__(kWinNT) window_kernel(SimpArgs A,
                                                         unsigned long long *__restrict__ table) {
   __shared__ double ring_e[kWin][kWinNT];
   __shared__ float ring_c[kWin][kWinNT];
-  __shared__ unsigned long long bmask;
-  const int64_t cell = (int64_t)blockIdx.x * kWinNT + threadIdx.x;
-  const bool live = cell < A.cells;
-  float e_cur = 0.f, c_cur = 0.f;
-  if (live) {
-    e_cur = __ldg(A.ground + cell);
-    c_cur = __ldg(A.cost + cell);
-  }
-  for (int k = 0; k < A.S; ++k) {
-    float e_up = bits_f32(kNaNBits), c_up = 0.f;
-    if (live && k + 1 < A.S) {
-      e_up = __ldg(A.ground + (int64_t)(k + 1) * A.cells + cell);
-      c_up = __ldg(A.cost + (int64_t)(k + 1) * A.cells + cell);
+  extern __shared__ unsigned long long btab[];  // [S]
+  for (int k = threadIdx.x; k < A.S; k += kWinNT) btab[k] = 0ull;
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * kWinNT;
+  const int64_t span = (A.cells + kWinNT - 1) / kWinNT * kWinNT;  // whole warps iterate together
+  for (int64_t cell = (int64_t)blockIdx.x * kWinNT + threadIdx.x; cell < span; cell += stride) {
+    const bool live = cell < A.cells;
+    float e_cur = 0.f, c_cur = 0.f;
+    if (live) {
+      e_cur = __ldg(A.ground + cell);
+      c_cur = __ldg(A.cost + cell);
     }
-    unsigned long long m = 0;
-    if (live && finite32(e_cur) && c_cur < A.c_barrier32 &&
-        (k + 1 >= A.S || not_covered(e_cur, c_cur, e_up, c_up, A.eps_e, false))) {
-      m = 1ull << kBit;
-      const int depth = k < kWin ? k : kWin;
-      const double ed = (double)e_cur;
-      for (int j = 0; j < depth; ++j) {  // a = k-1-j
-        const int slot = (k - 1 - j) & (kWin - 1);
-        if (not_covered_below(ed, c_cur, ring_e[slot][threadIdx.x], ring_c[slot][threadIdx.x],
-                              A.eps_e))
-          m |= 1ull << j;
+    for (int k = 0; k < A.S; ++k) {
+      float e_up = bits_f32(kNaNBits), c_up = 0.f;
+      if (live && k + 1 < A.S) {
+        e_up = __ldg(A.ground + (int64_t)(k + 1) * A.cells + cell);
+        c_up = __ldg(A.cost + (int64_t)(k + 1) * A.cells + cell);
       }
+      unsigned long long m = 0;
+      if (live && finite32(e_cur) && c_cur < A.c_barrier32 &&
+          (k + 1 >= A.S || not_covered(e_cur, c_cur, e_up, c_up, A.eps_e, false))) {
+        m = 1ull << kBit;
+        const int depth = k < kWin ? k : kWin;
+        const double ed = (double)e_cur;
+        for (int j = 0; j < depth; ++j) {  // a = k-1-j
+          const int slot = (k - 1 - j) & (kWin - 1);
+          if (not_covered_below(ed, c_cur, ring_e[slot][threadIdx.x], ring_c[slot][threadIdx.x],
+                                A.eps_e))
+            m |= 1ull << j;
+        }
+      }
+      const unsigned lo = __reduce_or_sync(0xffffffffu, (unsigned)m);
+      const unsigned hi = __reduce_or_sync(0xffffffffu, (unsigned)(m >> 32));
+      if ((threadIdx.x & 31) == 0 && (lo | hi))
+        atomicOr(&btab[k], ((unsigned long long)hi << 32) | lo);
+      ring_e[k & (kWin - 1)][threadIdx.x] = (double)e_cur;  // NaN stays NaN; own column only
+      ring_c[k & (kWin - 1)][threadIdx.x] = c_cur;
+      e_cur = e_up;
+      c_cur = c_up;
     }
-    // block OR
-    unsigned lo = __reduce_or_sync(0xffffffffu, (unsigned)m);
-    unsigned hi = __reduce_or_sync(0xffffffffu, (unsigned)(m >> 32));
-    if (threadIdx.x == 0) bmask = 0;
-    __syncthreads();
-    if ((threadIdx.x & 31) == 0 && (lo | hi))
-      atomicOr(&bmask, ((unsigned long long)hi << 32) | lo);
-    ring_e[k & (kWin - 1)][threadIdx.x] = (double)e_cur;  // NaN stays NaN
-    ring_c[k & (kWin - 1)][threadIdx.x] = c_cur;
-    __syncthreads();
-    if (threadIdx.x == 0 && bmask) atomicOr(table + k, bmask);
-    __syncthreads();
-    e_cur = e_up;
-    c_cur = c_up;
   }
+  __syncthreads();
+  for (int k = threadIdx.x; k < A.S; k += kWinNT)
+    if (btab[k]) atomicOr(table + k, btab[k]);
 }
 
 struct Triple {
@@ -182,7 +188,15 @@ int run_simplify(pct_ctx *ctx, const float *ground, const float *cost, int S, in
 
   std::vector<unsigned long long> htable(S, 0);
   PCT_CUDA(ctx, cudaMemsetAsync(table, 0, tbytes, ctx->stream));
-  window_kernel<<<(unsigned)((A.cells + kWinNT - 1) / kWinNT), kWinNT, 0, ctx->stream>>>(A, table);
+  {
+    const size_t tab_smem = (size_t)S * 8;
+    if (tab_smem > 160 * 1024) return fail(ctx, PCT_E_INVALID, "too many slices for simplify");
+    PCT_CUDA(ctx, cudaFuncSetAttribute(window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)tab_smem));
+    const int64_t blocks_needed = (A.cells + kWinNT - 1) / kWinNT;
+    const unsigned grid = (unsigned)std::min<int64_t>(blocks_needed, 6LL * ctx->num_sms);
+    window_kernel<<<grid, kWinNT, tab_smem, ctx->stream>>>(A, table);
+  }
   if (int rc = check_launch(ctx, "window_kernel")) return rc;
   PCT_CUDA(ctx, cudaMemcpyAsync(htable.data(), table, tbytes, cudaMemcpyDeviceToHost, ctx->stream));
   PCT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
