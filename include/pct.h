@@ -136,6 +136,31 @@ int pct_unique_mask(pct_ctx *ctx, const float *ground, const float *cost, int32_
                     int32_t cols, int32_t k, int32_t below, int32_t above, double eps_e,
                     double c_barrier, uint8_t *mask);
 
+/* ---- row-band sharding of one map over several GPUs (SURVEY.md §8 e) ---- */
+/* Partition points by owner band: band b owns global rows
+   [band_starts[b], band_starts[b+1]) of the frame (tomogram.py:148
+   rasterisation).  out receives the points grouped by band (same dtype);
+   counts_host[b] their numbers.  nbands <= 64. */
+int pct_partition_rows(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, const pct_frame *fr,
+                       const int32_t *band_starts, int32_t nbands, void *out,
+                       int64_t *counts_host);
+/* Build rows [row0, row0+nrows) of the GLOBAL frame (points of other rows are
+   ignored); slice k is written at k*out_slice_stride floats (0 = dense). */
+int pct_build_band(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, const pct_frame *fr,
+                   const double *heights, int32_t row0, int32_t nrows, int64_t out_slice_stride,
+                   float *ground, float *ceiling);
+/* Sweep primitives for a distributed simplify (simplify.py:18-73): the any()
+   table of the first pass (bit j of table[k]: below = k-1-j, j < 16; bit 32:
+   no lower neighbour; upper neighbour k+1) and any() flags of explicit
+   (below, k, above) triples (-1 = none).  Ranks OR-reduce both, then replay
+   the same sweep. */
+int pct_simplify_window(pct_ctx *ctx, const float *ground, const float *cost, int32_t n_slices,
+                        int64_t cells, int64_t slice_stride, double eps_e, double c_barrier,
+                        uint64_t *table_host);
+int pct_simplify_triples(pct_ctx *ctx, const float *ground, const float *cost, int32_t n_slices,
+                         int64_t cells, int64_t slice_stride, double eps_e, double c_barrier,
+                         const int32_t *triples, int32_t n_triples, int32_t *flags_host);
+
 /* ---- whole pipeline on a device-resident tomogram ---------------------- */
 /* xyz may be a device pointer (xyz_on_host = 0) or host memory (1; pinned
    memory from pct_host_alloc is fastest).  Allocates the stacks. */

@@ -122,8 +122,9 @@ __global__ void __launch_bounds__(256) bounds_kernel(const T *__restrict__ xyz, 
 struct BinArgs {
   double x0, y0, z0, r_g, d_s, inv_rg, inv_ds;
   const double *heights;  // (S,) device
-  int64_t cells;
-  int rows, cols, S;
+  int64_t cells;          // band_rows * cols
+  int rows, cols, S;      // rows = band rows; the frame is global
+  int row0;               // first global row of the band
 };
 
 template <typename T>
@@ -138,7 +139,7 @@ __global__ void __launch_bounds__(256) scatter_kernel(const T *__restrict__ xyz,
     const double z = (double)__ldg(xyz + 3 * p + 2);
     // rasterisation in float64 (tomogram.py:148-149); the division is the
     // correctly rounded Markstein form (== IEEE (y - y0) / r_g)
-    const double fi = floor(div_const(y - a.y0, a.r_g, a.inv_rg) + 0.5);
+    const double fi = floor(div_const(y - a.y0, a.r_g, a.inv_rg) + 0.5) - (double)a.row0;
     const double fj = floor(div_const(x - a.x0, a.r_g, a.inv_rg) + 0.5);
     if (!(fi >= 0.0 && fi < (double)a.rows && fj >= 0.0 && fj < (double)a.cols)) {
       atomicAdd(outside, 1ull);
@@ -162,11 +163,13 @@ __global__ void __launch_bounds__(256) scatter_kernel(const T *__restrict__ xyz,
 // plane k of ckey holds bin k+1.
 __global__ void __launch_bounds__(256) scan_kernel(const uint32_t *__restrict__ gkey,
                                                    const uint32_t *__restrict__ ckey,
-                                                   int64_t cells, int S,
+                                                   int64_t cells, int S, int64_t out_stride,
                                                    float *__restrict__ ground,
                                                    float *__restrict__ ceiling) {
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= cells) return;
+  // scratch planes are dense (stride cells); output slice k of the band lives
+  // at k * out_stride (== cells for a whole grid, larger inside a halo'd band)
   // batches of 8 independent loads keep enough bytes in flight per thread
   constexpr int U = 8;
   uint32_t run = kKeyEmptyMax;
@@ -178,13 +181,13 @@ __global__ void __launch_bounds__(256) scan_kernel(const uint32_t *__restrict__ 
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       run = v[u] > run ? v[u] : run;
-      __stcs(ground + (int64_t)(k + u) * cells + c, decode_ground(run));
+      __stcs(ground + (int64_t)(k + u) * out_stride + c, decode_ground(run));
     }
   }
   for (; k < S; ++k) {
     const uint32_t v = __ldcs(gkey + (int64_t)k * cells + c);
     run = v > run ? v : run;
-    __stcs(ground + (int64_t)k * cells + c, decode_ground(run));
+    __stcs(ground + (int64_t)k * out_stride + c, decode_ground(run));
   }
   run = kKeyEmptyMin;
   k = S - 1;
@@ -195,13 +198,13 @@ __global__ void __launch_bounds__(256) scan_kernel(const uint32_t *__restrict__ 
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       run = v[u] < run ? v[u] : run;
-      __stcs(ceiling + (int64_t)(k - u) * cells + c, decode_ceiling(run));
+      __stcs(ceiling + (int64_t)(k - u) * out_stride + c, decode_ceiling(run));
     }
   }
   for (; k >= 0; --k) {
     const uint32_t v = __ldcs(ckey + (int64_t)k * cells + c);
     run = v < run ? v : run;
-    __stcs(ceiling + (int64_t)k * cells + c, decode_ceiling(run));
+    __stcs(ceiling + (int64_t)k * out_stride + c, decode_ceiling(run));
   }
 }
 
@@ -243,9 +246,15 @@ int launch_bounds(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, double lo
 }
 
 int launch_build(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, const pct_frame &fr,
-                 const double *heights_host, float *ground, float *ceiling) {
+                 const double *heights_host, float *ground, float *ceiling, int row0, int nrows,
+                 int64_t out_stride) {
   const int S = fr.n_slices;
-  const int64_t cells = (int64_t)fr.rows * fr.cols;
+  if (nrows < 0) {  // whole grid
+    row0 = 0;
+    nrows = fr.rows;
+  }
+  const int64_t cells = (int64_t)nrows * fr.cols;
+  if (out_stride <= 0) out_stride = cells;
   const size_t plane = (size_t)cells * sizeof(uint32_t);
   // scratch: gkey (S planes) | ckey (S planes) | heights (S doubles) | outside counter
   const size_t hbytes = ((size_t)S * sizeof(double) + 255) & ~(size_t)255;
@@ -261,7 +270,7 @@ int launch_build(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, const pct_
   PCT_CUDA(ctx, cudaMemsetAsync(ckey, 0xFF, plane * S, ctx->stream));
   PCT_CUDA(ctx, cudaMemsetAsync(outside, 0, 8, ctx->stream));
   BinArgs a{fr.origin_x, fr.origin_y, fr.z_min, fr.r_g, fr.d_s, 1.0 / fr.r_g, 1.0 / fr.d_s,
-            hdev, cells, fr.rows, fr.cols, S};
+            hdev, cells, nrows, fr.cols, S, row0};
   if (n > 0) {
     if (dtype == PCT_F32)
       scatter_kernel<float><<<grid_for(ctx, n, 256, 16), 256, 0, ctx->stream>>>(
@@ -272,7 +281,7 @@ int launch_build(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, const pct_
     if (int rc = check_launch(ctx, "scatter_kernel")) return rc;
   }
   scan_kernel<<<(unsigned)((cells + 255) / 256), 256, 0, ctx->stream>>>(gkey, ckey, cells, S,
-                                                                        ground, ceiling);
+                                                                        out_stride, ground, ceiling);
   return check_launch(ctx, "scan_kernel");
 }
 

@@ -37,6 +37,7 @@ struct SimpArgs {
   const float *ground;
   const float *cost;
   int64_t cells;
+  int64_t stride;  // floats between consecutive slices (== cells for a dense stack)
   int S;
   double eps_e;
   float c_barrier32;  // numpy compares float32 costs with the weak Python scalar in float32
@@ -76,12 +77,28 @@ __global__ void __launch_bounds__(kWinNT) window_kernel(SimpArgs A,
       e_cur = __ldg(A.ground + cell);
       c_cur = __ldg(A.cost + cell);
     }
+    // the (ground, cost) of the next slices are loaded 8 at a time so the
+    // dependent walk over k does not wait on one global load per step
+    constexpr int PF = 8;
+    float pe[PF], pc[PF];
     for (int k = 0; k < A.S; ++k) {
-      float e_up = bits_f32(kNaNBits), c_up = 0.f;
-      if (live && k + 1 < A.S) {
-        e_up = __ldg(A.ground + (int64_t)(k + 1) * A.cells + cell);
-        c_up = __ldg(A.cost + (int64_t)(k + 1) * A.cells + cell);
+      const int q = k % PF;
+      if (q == 0) {
+#pragma unroll
+        for (int u = 0; u < PF; ++u) {
+          const int kk = k + 1 + u;
+          const bool ok = live && kk < A.S;
+          pe[u] = ok ? __ldg(A.ground + (int64_t)kk * A.stride + cell) : bits_f32(kNaNBits);
+          pc[u] = ok ? __ldg(A.cost + (int64_t)kk * A.stride + cell) : 0.f;
+        }
       }
+      float e_up = pe[0], c_up = pc[0];
+#pragma unroll
+      for (int u = 1; u < PF; ++u)
+        if (q == u) {
+          e_up = pe[u];
+          c_up = pc[u];
+        }
       unsigned long long m = 0;
       if (live && finite32(e_cur) && c_cur < A.c_barrier32 &&
           (k + 1 >= A.S || not_covered(e_cur, c_cur, e_up, c_up, A.eps_e, false))) {
@@ -126,16 +143,16 @@ __global__ void __launch_bounds__(256) triples_kernel(SimpArgs A, const Triple *
   bool any = false;
   for (int64_t cell = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; cell < A.cells && !any;
        cell += stride) {
-    const float e = __ldg(A.ground + (int64_t)T.k * A.cells + cell);
-    const float c = __ldg(A.cost + (int64_t)T.k * A.cells + cell);
+    const float e = __ldg(A.ground + (int64_t)T.k * A.stride + cell);
+    const float c = __ldg(A.cost + (int64_t)T.k * A.stride + cell);
     if (!(finite32(e) && c < A.c_barrier32)) continue;
     bool u = true;
     if (T.below >= 0)
-      u = not_covered(e, c, __ldg(A.ground + (int64_t)T.below * A.cells + cell),
-                      __ldg(A.cost + (int64_t)T.below * A.cells + cell), A.eps_e, true);
+      u = not_covered(e, c, __ldg(A.ground + (int64_t)T.below * A.stride + cell),
+                      __ldg(A.cost + (int64_t)T.below * A.stride + cell), A.eps_e, true);
     if (u && T.above >= 0)
-      u = not_covered(e, c, __ldg(A.ground + (int64_t)T.above * A.cells + cell),
-                      __ldg(A.cost + (int64_t)T.above * A.cells + cell), A.eps_e, false);
+      u = not_covered(e, c, __ldg(A.ground + (int64_t)T.above * A.stride + cell),
+                      __ldg(A.cost + (int64_t)T.above * A.stride + cell), A.eps_e, false);
     any = u;
   }
   if (__syncthreads_or(any) && threadIdx.x == 0) atomicOr(flags + t, 1);
@@ -145,15 +162,15 @@ __global__ void __launch_bounds__(256) unique_mask_kernel(SimpArgs A, Triple T,
                                                           unsigned char *__restrict__ mask) {
   const int64_t cell = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (cell >= A.cells) return;
-  const float e = __ldg(A.ground + (int64_t)T.k * A.cells + cell);
-  const float c = __ldg(A.cost + (int64_t)T.k * A.cells + cell);
+  const float e = __ldg(A.ground + (int64_t)T.k * A.stride + cell);
+  const float c = __ldg(A.cost + (int64_t)T.k * A.stride + cell);
   bool u = finite32(e) && c < A.c_barrier32;
   if (u && T.below >= 0)
-    u = not_covered(e, c, __ldg(A.ground + (int64_t)T.below * A.cells + cell),
-                    __ldg(A.cost + (int64_t)T.below * A.cells + cell), A.eps_e, true);
+    u = not_covered(e, c, __ldg(A.ground + (int64_t)T.below * A.stride + cell),
+                    __ldg(A.cost + (int64_t)T.below * A.stride + cell), A.eps_e, true);
   if (u && T.above >= 0)
-    u = not_covered(e, c, __ldg(A.ground + (int64_t)T.above * A.cells + cell),
-                    __ldg(A.cost + (int64_t)T.above * A.cells + cell), A.eps_e, false);
+    u = not_covered(e, c, __ldg(A.ground + (int64_t)T.above * A.stride + cell),
+                    __ldg(A.cost + (int64_t)T.above * A.stride + cell), A.eps_e, false);
   mask[cell] = u ? 1 : 0;
 }
 
@@ -162,7 +179,8 @@ __global__ void __launch_bounds__(256) unique_mask_kernel(SimpArgs A, Triple T,
 int launch_unique_mask(pct_ctx *ctx, const float *ground, const float *cost, int rows, int cols,
                        int k, int below, int above, double eps_e, double c_barrier,
                        uint8_t *mask) {
-  SimpArgs A{ground, cost, (int64_t)rows * cols, 0, eps_e, (float)c_barrier};
+  SimpArgs A{ground, cost, (int64_t)rows * cols, (int64_t)rows * cols, 0, eps_e,
+             (float)c_barrier};
   if (A.cells == 0) return PCT_OK;
   unique_mask_kernel<<<(unsigned)((A.cells + 255) / 256), 256, 0, ctx->stream>>>(
       A, Triple{below, k, above}, mask);
@@ -174,7 +192,8 @@ int run_simplify(pct_ctx *ctx, const float *ground, const float *cost, int S, in
   keep.clear();
   for (int k = 0; k < S; ++k) keep.push_back(k);
   if (S <= 1) return PCT_OK;
-  SimpArgs A{ground, cost, (int64_t)rows * cols, S, eps_e, (float)c_barrier};
+  SimpArgs A{ground, cost, (int64_t)rows * cols, (int64_t)rows * cols, S, eps_e,
+             (float)c_barrier};
   // device small buffer layout: table[S] u64 | triples | flags
   const size_t tbytes = (size_t)S * 8;
   const size_t need = tbytes + (size_t)S * sizeof(Triple) + (size_t)S * sizeof(int) + 64;
@@ -269,6 +288,62 @@ int run_simplify(pct_ctx *ctx, const float *ground, const float *cost, int S, in
     }
     if (!removed) break;
   }
+  return PCT_OK;
+}
+
+}  // namespace pct
+
+// ---------------------------------------------------------------------------
+// primitives for a sweep replayed outside (row-band sharded maps: the any()s
+// of every rank are OR-reduced before the shared sweep decides)
+namespace pct {
+
+int simplify_window_table(pct_ctx *ctx, const float *ground, const float *cost, int S,
+                          int64_t cells, int64_t stride, double eps_e, double c_barrier,
+                          uint64_t *table_host) {
+  if (S <= 0) return PCT_OK;
+  SimpArgs A{ground, cost, cells, stride, S, eps_e, (float)c_barrier};
+  const size_t tbytes = (size_t)S * 8;
+  if (tbytes > 65536 - 128) return fail(ctx, PCT_E_INVALID, "too many slices");
+  unsigned long long *table = static_cast<unsigned long long *>(ctx->dsmall);
+  PCT_CUDA(ctx, cudaMemsetAsync(table, 0, tbytes, ctx->stream));
+  if (cells > 0) {
+    PCT_CUDA(ctx, cudaFuncSetAttribute(window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)tbytes));
+    const int64_t blocks_needed = (cells + kWinNT - 1) / kWinNT;
+    const unsigned grid = (unsigned)std::min<int64_t>(blocks_needed, 6LL * ctx->num_sms);
+    window_kernel<<<grid, kWinNT, tbytes, ctx->stream>>>(A, table);
+    if (int rc = check_launch(ctx, "window_kernel")) return rc;
+  }
+  PCT_CUDA(ctx, cudaMemcpyAsync(table_host, table, tbytes, cudaMemcpyDeviceToHost, ctx->stream));
+  PCT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return PCT_OK;
+}
+
+int simplify_triple_flags(pct_ctx *ctx, const float *ground, const float *cost, int S,
+                          int64_t cells, int64_t stride, double eps_e, double c_barrier,
+                          const int32_t *triples, int n, int32_t *flags_host) {
+  if (n <= 0) return PCT_OK;
+  SimpArgs A{ground, cost, cells, stride, S, eps_e, (float)c_barrier};
+  const size_t need = (size_t)n * (sizeof(Triple) + sizeof(int)) + 64;
+  if (need > 65536 - 128) return fail(ctx, PCT_E_INVALID, "too many triples in one batch");
+  char *dbase = static_cast<char *>(ctx->dsmall);
+  Triple *dtr = reinterpret_cast<Triple *>(dbase);
+  int *dflags = reinterpret_cast<int *>(dbase + (size_t)n * sizeof(Triple));
+  std::vector<Triple> ts(n);
+  for (int i = 0; i < n; ++i) ts[i] = Triple{triples[3 * i], triples[3 * i + 1], triples[3 * i + 2]};
+  PCT_CUDA(ctx, cudaMemcpyAsync(dtr, ts.data(), sizeof(Triple) * n, cudaMemcpyHostToDevice,
+                                ctx->stream));
+  PCT_CUDA(ctx, cudaMemsetAsync(dflags, 0, sizeof(int) * n, ctx->stream));
+  if (cells > 0) {
+    int64_t bx = (cells + 255) / 256;
+    if (bx > 2LL * ctx->num_sms) bx = 2LL * ctx->num_sms;
+    triples_kernel<<<dim3((unsigned)bx, n), 256, 0, ctx->stream>>>(A, dtr, dflags);
+    if (int rc = check_launch(ctx, "triples_kernel")) return rc;
+  }
+  PCT_CUDA(ctx, cudaMemcpyAsync(flags_host, dflags, sizeof(int) * n, cudaMemcpyDeviceToHost,
+                                ctx->stream));
+  PCT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   return PCT_OK;
 }
 

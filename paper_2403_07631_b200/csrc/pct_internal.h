@@ -53,8 +53,11 @@ int check_launch(pct_ctx *ctx, const char *what);
 // stage launchers (return PCT_OK or error code)
 int launch_bounds(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, double lo[3],
                   double hi[3]);
+// row0/nrows select a band of global rows (nrows < 0: whole grid); output
+// slice k at k*out_stride floats (<= 0: dense)
 int launch_build(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, const pct_frame &fr,
-                 const double *heights_host, float *ground, float *ceiling);
+                 const double *heights_host, float *ground, float *ceiling, int row0 = 0,
+                 int nrows = -1, int64_t out_stride = 0);
 int launch_evaluate(pct_ctx *ctx, const float *ground, const float *ceiling, int S, int rows,
                     int cols, double r_g, const pct_trav_params &p, const float *kernel_w,
                     int kside, float *cost, int mode);

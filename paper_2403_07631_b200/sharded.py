@@ -1,0 +1,436 @@
+"""Row-band sharding of one large map over several GPUs (SURVEY.md §8 e).
+
+Each rank owns a contiguous band of grid rows.  Per rank (one process per
+GPU, NCCL over NVLink via torch.distributed; PyTorch tensors only as
+buffers):
+
+  1. bounds of the local point shard -> all-reduce -> the global grid frame
+     (tomogram.py:134-145, identical on every rank)
+  2. points partitioned by owner band on the device (pct_partition_rows)
+     -> all-to-all (NCCL) -> every rank holds the points of its rows
+  3. banded build with the GLOBAL frame (pct_build_band) into an extended
+     stack that has room for H = R + r + 1 halo rows above and below
+  4. halo exchange: the first/last H own rows of ground and ceiling go to the
+     neighbour ranks (NCCL send/recv)
+  5. fused evaluate on the extended band: the own rows are exact because the
+     stencil reaches at most R + r + 1 rows for ground and R for ceiling
+  6. simplify: every rank computes the any() table / triple flags over its
+     own rows; they are max-reduced and every rank replays the same sweep
+     (simplify.py:59-70), so all ranks agree on the surviving slices.
+
+The result is bit-identical to the single-GPU pipeline (tested with
+virtual ranks on one GPU, tests/test_gpu_sharded.py, and the collective /
+sweep logic with gloo on CPU, tests/test_sharded_host.py).
+
+The pipeline is a generator that yields a request at every collective;
+``run_torch`` serves them with torch.distributed, ``run_virtual`` runs P
+ranks in lockstep in one process (device copies stand in for NCCL).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+
+KWIN = 16   # lower-neighbour window of pct_simplify_window
+KNONE = 32  # bit of "no lower neighbour"
+
+
+# ---------------------------------------------------------------------------
+# band geometry
+
+def band_starts(rows: int, size: int) -> list:
+    """Balanced contiguous row bands: band b owns rows [s[b], s[b+1])."""
+    return [rows * b // size for b in range(size + 1)]
+
+
+def halo_rows(params, r_g: float, kside: int) -> int:
+    """Rows of ground a band needs beyond its own rows: inflation radius R,
+    foothold window r and one gradient cell (traversability.py:76-213)."""
+    pr = getattr(params, "step_patch_radius", None)
+    pr = int(pr) if pr is not None else int(math.ceil(0.3 / r_g))
+    return kside // 2 + pr + 1
+
+
+def owner_band_np(y, y0, r_g, starts):
+    """numpy statement of the device owner-band rule (for CPU tests)."""
+    i = np.floor((np.asarray(y, np.float64) - y0) / r_g + 0.5)
+    return np.searchsorted(np.asarray(starts[1:-1], np.float64), i, side="right")
+
+
+# ---------------------------------------------------------------------------
+# the simplify sweep replayed from (reduced) any() tables
+
+def expand_table(table: np.ndarray) -> np.ndarray:
+    """(S,) uint64 bit tables -> (S, 17) uint8: columns 0..15 = bits 0..15 (below =
+    k-1-j), column 16 = bit 32 (no lower neighbour); max-reducible across ranks."""
+    t = np.asarray(table, np.uint64)
+    bits = list(range(KWIN)) + [KNONE]
+    return np.stack([((t >> np.uint64(b)) & np.uint64(1)).astype(np.uint8) for b in bits], axis=1)
+
+
+def replay_sweep(S: int, table_bytes: np.ndarray, triples_any):
+    """The forward sweep of simplify.py:59-70 over any()s.
+
+    table_bytes: (S, 17) uint8 from expand_table (already reduced over ranks).
+    triples_any(list of (below, k, above)) -> list of bool (reduced over ranks).
+    Returns the surviving slice indices."""
+    keep = list(range(S))
+    if S <= 1:
+        return keep
+    cache = {}
+
+    def from_window(below, k, above):
+        if not (above == k + 1 or (above < 0 and k == S - 1)):
+            return None
+        if below < 0:
+            return bool(table_bytes[k, KWIN])
+        if k - 1 - below < KWIN:
+            return bool(table_bytes[k, k - 1 - below])
+        return None
+
+    while True:
+        removed = False
+        p = 0
+        while p < len(keep):
+            if len(keep) > 1:
+                k = keep[p]
+                below = keep[p - 1] if p > 0 else -1
+                above = keep[p + 1] if p + 1 < len(keep) else -1
+                u = from_window(below, k, above)
+                if u is None:
+                    key = (below, k, above)
+                    if key not in cache:
+                        batch = []
+                        for q in range(p, len(keep)):
+                            t = (keep[q - 1] if q > 0 else -1, keep[q],
+                                 keep[q + 1] if q + 1 < len(keep) else -1)
+                            if from_window(*t) is None and t not in cache and len(batch) < 256:
+                                batch.append(t)
+                        for t, f in zip(batch, triples_any(batch)):
+                            cache[t] = bool(f)
+                    u = cache[key]
+                if not u:
+                    del keep[p]
+                    removed = True
+                    continue
+            p += 1
+        if not removed:
+            return keep
+
+
+# ---------------------------------------------------------------------------
+# the per-rank pipeline
+
+@dataclass
+class BandResult:
+    rank: int
+    size: int
+    rows: int
+    cols: int
+    row0: int
+    nrows: int
+    heights: np.ndarray
+    origin: tuple
+    z_min: float
+    keep: list
+    # device tensors (torch) of the OWN rows, views into the extended stacks
+    ground: object = None
+    ceiling: object = None
+    cost: object = None
+    stages_ms: dict = field(default_factory=dict)
+
+
+def _ptr(t, offset_elems=0):
+    return t.data_ptr() + 4 * int(offset_elems)
+
+
+def band_pipeline(xyz, d_s, r_g, params, rank, size, *, device=None, eps_e=1e-6,
+                  c_barrier=50.0, max_grid_side=16384):
+    """Generator: the row-band pipeline of one rank.
+
+    xyz: this rank's points, a CUDA torch tensor (n, 3) float32/float64.
+    Yields collective requests (tuples) and finally returns a BandResult."""
+    import torch
+
+    ctx = _lib.context(device if device is not None else xyz.device.index)
+    lib, h = ctx.lib, ctx.h
+    # libpct and torch share one stream for the whole pipeline (ordering of
+    # the NCCL buffers against the kernels); restored at the end
+    ctx.check(lib.pct_set_stream(h, C.c_void_p(torch.cuda.current_stream(xyz.device).cuda_stream)),
+              "set_stream")
+    dt = torch.float32 if xyz.dtype == torch.float32 else torch.float64
+    code = _lib.PCT_F32 if dt == torch.float32 else _lib.PCT_F64
+    xyz = xyz.contiguous()
+    n = xyz.shape[0]
+
+    # 1. bounds -> global frame
+    lo = np.full(3, np.inf)
+    hi = np.full(3, -np.inf)
+    if n > 0:
+        ctx.check(lib.pct_bounds(h, xyz.data_ptr(), n, code, lo.ctypes.data, hi.ctypes.data),
+                  "bounds")
+    lo, hi = yield ("bounds", lo, hi)
+    if not np.all(np.isfinite(lo)):
+        from .cloud import CloudFormatError
+        raise CloudFormatError("zero valid points")
+    fr = _lib.FrameC()
+    heights = np.empty(65536, np.float64)
+    rc = lib.pct_frame_compute(lo.ctypes.data, hi.ctypes.data, float(d_s), float(r_g),
+                               int(max_grid_side), C.byref(fr), heights.ctypes.data, 65536)
+    if rc == _lib.PCT_E_GRID:
+        from .tomogram import GridSizeError
+        raise GridSizeError(f"grid {fr.rows}x{fr.cols} exceeds the {max_grid_side} per-side limit")
+    if rc != 0:
+        raise ValueError("d_s and r_g must be positive")
+    S, rows, cols = fr.n_slices, fr.rows, fr.cols
+    heights = heights[:S].copy()
+    starts = band_starts(rows, size)
+    row0, row1 = starts[rank], starts[rank + 1]
+    nrows = row1 - row0
+
+    # 2. partition by owner band, all-to-all
+    part = torch.empty_like(xyz)
+    counts = np.zeros(size, np.int64)
+    st = np.asarray(starts, np.int32)
+    if n > 0:
+        ctx.check(lib.pct_partition_rows(h, xyz.data_ptr(), n, code, C.byref(fr), st.ctypes.data,
+                                         size, part.data_ptr(), counts.ctypes.data), "partition")
+    mine = yield ("alltoallv", part, counts.tolist())
+    mine = mine.contiguous()
+
+    # 3. banded build into the extended stack
+    from .traversability import build_kernel
+    kern = build_kernel(params.d_inf, params.d_sm, r_g)
+    w = np.ascontiguousarray(kern.weights)
+    H = halo_rows(params, r_g, w.shape[0])
+    top = min(H, row0)
+    bot = min(H, rows - row1)
+    ext_rows = top + nrows + bot
+    g = torch.empty((S, ext_rows, cols), dtype=torch.float32, device=xyz.device)
+    c = torch.empty_like(g)
+    stride = ext_rows * cols
+    if nrows > 0:
+        ctx.check(lib.pct_build_band(h, mine.data_ptr(), mine.shape[0], code, C.byref(fr),
+                                     heights.ctypes.data, row0, nrows, stride,
+                                     _ptr(g, top * cols), _ptr(c, top * cols)), "build_band")
+    # 4. halo exchange: my first rows go up (to rank-1), my last rows go down
+    up_n = min(H, rows - row0) if rank > 0 else 0   # == rank-1's bottom halo
+    down_n = min(H, row1) if rank + 1 < size else 0  # == rank+1's top halo
+    if up_n > nrows or down_n > nrows:
+        raise ValueError(f"row band of {nrows} rows is thinner than the {H}-row halo; "
+                         "use fewer ranks for this grid")
+    send_up = torch.stack([g[:, top:top + up_n], c[:, top:top + up_n]]).contiguous() \
+        if rank > 0 else None
+    send_down = torch.stack([g[:, top + nrows - down_n:top + nrows],
+                             c[:, top + nrows - down_n:top + nrows]]).contiguous() \
+        if rank + 1 < size else None
+    from_up, from_down = yield ("halo", send_up, send_down, (2, S, top, cols), (2, S, bot, cols))
+    if top:
+        g[:, :top] = from_up[0]
+        c[:, :top] = from_up[1]
+    if bot:
+        g[:, top + nrows:] = from_down[0]
+        c[:, top + nrows:] = from_down[1]
+
+    # 5. evaluate the extended band (own rows are exact)
+    cost = torch.empty_like(g)
+    pc = _lib.trav_params_c(params, r_g)
+    ctx.check(lib.pct_evaluate(h, g.data_ptr(), c.data_ptr(), S, ext_rows, cols, float(r_g),
+                               C.byref(pc), w.ctypes.data, w.shape[0], cost.data_ptr()),
+              "evaluate")
+
+    # 6. simplify: reduced any() tables, shared sweep
+    cells = nrows * cols
+    table = np.zeros(S, np.uint64)
+    ctx.check(lib.pct_simplify_window(h, _ptr(g, top * cols), _ptr(cost, top * cols), S, cells,
+                                      stride, float(eps_e), float(c_barrier), table.ctypes.data),
+              "simplify_window")
+    tb = yield ("max_u8", expand_table(table))
+    pending = {}
+
+    def triples_any(batch):
+        tri = np.asarray(batch, np.int32).reshape(-1)
+        flags = np.zeros(len(batch), np.int32)
+        ctx.check(lib.pct_simplify_triples(h, _ptr(g, top * cols), _ptr(cost, top * cols), S,
+                                           cells, stride, float(eps_e), float(c_barrier),
+                                           tri.ctypes.data, len(batch), flags.ctypes.data),
+                  "simplify_triples")
+        pending["local"] = flags.astype(np.uint8)
+        return None
+
+    # the sweep is replayed identically on every rank; each triple batch is a
+    # collective (local flags -> max over ranks)
+    keep_box = {}
+    sweep = _sweep_gen(S, tb)
+    req = next(sweep)
+    while True:
+        if req[0] == "done":
+            keep_box["keep"] = req[1]
+            break
+        triples_any(req[1])
+        red = yield ("max_u8", pending["local"])
+        req = sweep.send([bool(v) for v in red])
+    lib.pct_set_stream(h, None)
+    return BandResult(rank=rank, size=size, rows=rows, cols=cols, row0=row0, nrows=nrows,
+                      heights=heights, origin=(float(fr.origin_x), float(fr.origin_y)),
+                      z_min=float(fr.z_min), keep=keep_box["keep"],
+                      ground=g[:, top:top + nrows], ceiling=c[:, top:top + nrows],
+                      cost=cost[:, top:top + nrows])
+
+
+def _sweep_gen(S, tb):
+    """replay_sweep as a generator: yields ("triples", batch) and receives the
+    reduced any()s; the (deterministic) replay restarts with the answers
+    known so far until it completes, then yields ("done", keep)."""
+    answers = {}
+
+    def lookup(batch):
+        key = tuple(batch)
+        if key not in answers:
+            raise _NeedAny(batch)
+        return answers[key]
+
+    while True:
+        try:
+            keep = replay_sweep(S, tb, lookup)
+        except _NeedAny as e:
+            answers[tuple(e.batch)] = yield ("triples", e.batch)
+            continue
+        yield ("done", keep)
+        return
+
+
+class _NeedAny(Exception):
+    def __init__(self, batch=None):
+        super().__init__("any() needed")
+        self.batch = batch
+
+
+# ---------------------------------------------------------------------------
+# drivers
+
+def run_torch(gen, group=None):
+    """Serve a band_pipeline generator with torch.distributed collectives."""
+    import torch
+    import torch.distributed as dist
+
+    rank = dist.get_rank(group)
+    size = dist.get_world_size(group)
+    req = next(gen)
+    while True:
+        kind = req[0]
+        if kind == "bounds":
+            lo, hi = req[1], req[2]
+            dev = _collective_device(group)
+            t = torch.tensor(np.concatenate([-lo, hi]), dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+            v = t.cpu().numpy()
+            ans = (-v[:3], v[3:])
+        elif kind == "alltoallv":
+            part, counts = req[1], req[2]
+            dev = part.device
+            cnt = torch.tensor(counts, dtype=torch.int64, device=dev)
+            rcnt = torch.empty_like(cnt)
+            dist.all_to_all_single(rcnt, cnt, group=group)
+            rc = rcnt.cpu().tolist()
+            out = torch.empty((int(sum(rc)), 3), dtype=part.dtype, device=dev)
+            dist.all_to_all_single(out, part, output_split_sizes=rc, input_split_sizes=counts,
+                                   group=group)
+            ans = out
+        elif kind == "halo":
+            send_up, send_down, up_shape, down_shape = req[1:]
+            ref = send_up if send_up is not None else send_down
+            dev = ref.device if ref is not None else _collective_device(group)
+            recv_up = torch.empty(up_shape, dtype=torch.float32, device=dev)
+            recv_down = torch.empty(down_shape, dtype=torch.float32, device=dev)
+            ops = []
+            if send_up is not None:
+                ops.append(dist.P2POp(dist.isend, send_up, _global(group, rank - 1), group))
+            if send_down is not None:
+                ops.append(dist.P2POp(dist.isend, send_down, _global(group, rank + 1), group))
+            if up_shape[2] > 0:
+                ops.append(dist.P2POp(dist.irecv, recv_up, _global(group, rank - 1), group))
+            if down_shape[2] > 0:
+                ops.append(dist.P2POp(dist.irecv, recv_down, _global(group, rank + 1), group))
+            if ops:
+                for r in dist.batch_isend_irecv(ops):
+                    r.wait()
+            ans = (recv_up, recv_down)
+        elif kind == "max_u8":
+            dev = _collective_device(group)
+            t = torch.from_numpy(np.ascontiguousarray(req[1])).to(dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+            ans = t.cpu().numpy()
+        else:
+            raise RuntimeError(f"unknown collective {kind}")
+        try:
+            req = gen.send(ans)
+        except StopIteration as stop:
+            return stop.value
+
+
+def _global(group, r):
+    import torch.distributed as dist
+    return r if group is None else dist.get_global_rank(group, r)
+
+
+def _collective_device(group):
+    import torch
+    import torch.distributed as dist
+    if dist.get_backend(group) == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
+def run_virtual(gens):
+    """Run P band_pipeline generators in lockstep in one process (one GPU):
+    the collectives are performed by direct tensor / array operations."""
+    import torch
+
+    P = len(gens)
+    reqs = [next(g) for g in gens]
+    results = [None] * P
+    while True:
+        kinds = {r[0] for r in reqs}
+        assert len(kinds) == 1, f"ranks out of step: {kinds}"
+        kind = kinds.pop()
+        if kind == "bounds":
+            lo = np.min([r[1] for r in reqs], axis=0)
+            hi = np.max([r[2] for r in reqs], axis=0)
+            answers = [(lo.copy(), hi.copy()) for _ in range(P)]
+        elif kind == "alltoallv":
+            offs = [np.concatenate([[0], np.cumsum(r[2])]) for r in reqs]
+            answers = []
+            for dst in range(P):
+                pieces = [reqs[src][1][int(offs[src][dst]):int(offs[src][dst + 1])]
+                          for src in range(P)]
+                answers.append(torch.cat(pieces) if pieces else None)
+        elif kind == "halo":
+            answers = []
+            for r in range(P):
+                up = reqs[r - 1][2] if r > 0 else None          # rank-1's send_down
+                down = reqs[r + 1][1] if r + 1 < P else None    # rank+1's send_up
+                answers.append((up, down))
+        elif kind == "max_u8":
+            m = np.max([r[1] for r in reqs], axis=0)
+            answers = [m.copy() for _ in range(P)]
+        else:
+            raise RuntimeError(kind)
+        done = 0
+        for i, g in enumerate(gens):
+            if results[i] is not None:
+                done += 1
+                continue
+            try:
+                reqs[i] = g.send(answers[i])
+            except StopIteration as stop:
+                results[i] = stop.value
+                done += 1
+        if done == P:
+            return results
