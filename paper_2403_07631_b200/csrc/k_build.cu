@@ -63,20 +63,25 @@ __global__ void __launch_bounds__(256) bounds_kernel(const T *__restrict__ xyz, 
   m.nonfinite = 0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  bool vec = false;
   if constexpr (sizeof(T) == 4) {
-    // 4 points = 12 floats = 3 x float4 per step (xyz is 16 B aligned)
-    const int64_t groups = n / 4;
-    const float4 *v = reinterpret_cast<const float4 *>(xyz);
-    for (int64_t g = t; g < groups; g += stride) {
-      float4 a = __ldg(v + 3 * g), b = __ldg(v + 3 * g + 1), c = __ldg(v + 3 * g + 2);
-      mm_point(m, a.x, a.y, a.z);
-      mm_point(m, a.w, b.x, b.y);
-      mm_point(m, b.z, b.w, c.x);
-      mm_point(m, c.y, c.z, c.w);
+    if ((reinterpret_cast<uintptr_t>(xyz) & 15) == 0) {
+      // 4 points = 12 floats = 3 x float4 per step (xyz is 16 B aligned)
+      vec = true;
+      const int64_t groups = n / 4;
+      const float4 *v = reinterpret_cast<const float4 *>(xyz);
+      for (int64_t g = t; g < groups; g += stride) {
+        float4 a = __ldg(v + 3 * g), b = __ldg(v + 3 * g + 1), c = __ldg(v + 3 * g + 2);
+        mm_point(m, a.x, a.y, a.z);
+        mm_point(m, a.w, b.x, b.y);
+        mm_point(m, b.z, b.w, c.x);
+        mm_point(m, c.y, c.z, c.w);
+      }
+      for (int64_t p = groups * 4 + t; p < n; p += stride)
+        mm_point(m, xyz[3 * p], xyz[3 * p + 1], xyz[3 * p + 2]);
     }
-    for (int64_t p = groups * 4 + t; p < n; p += stride)
-      mm_point(m, xyz[3 * p], xyz[3 * p + 1], xyz[3 * p + 2]);
-  } else {
+  }
+  if (!vec) {  // float64, or a float32 view that is not 16 B aligned
     for (int64_t p = t; p < n; p += stride)
       mm_point(m, __ldg(xyz + 3 * p), __ldg(xyz + 3 * p + 1), __ldg(xyz + 3 * p + 2));
   }
@@ -225,9 +230,7 @@ int launch_bounds(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, double lo
   unsigned long long *hk = static_cast<unsigned long long *>(ctx->hsmall);
   std::memcpy(hk, init, sizeof(init));
   PCT_CUDA(ctx, cudaMemcpyAsync(keys, hk, sizeof(init), cudaMemcpyHostToDevice, ctx->stream));
-  const bool aligned = (reinterpret_cast<uintptr_t>(xyz) & 15) == 0;
-  if (dtype == PCT_F32) {
-    if (!aligned) return fail(ctx, PCT_E_INVALID, "xyz must be 16-byte aligned");
+  if (dtype == PCT_F32) {  // float4 path when 16 B aligned, scalar otherwise
     bounds_kernel<float><<<grid_for(ctx, (n + 3) / 4, 256), 256, 0, ctx->stream>>>(
         static_cast<const float *>(xyz), n, keys);
   } else {
