@@ -2,16 +2,27 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl b200|reference]
 
-One "step" = one pass of the hot path over one synthetic map (BASELINE.json
-config C, default 1: 5M points, 0.1 m, d_s 0.4), inputs resident in HBM.
-Prints ONE JSON line (rank 0).  Under torchrun each rank processes its own
-independently seeded map (weak scaling, no data-path collective: batches of
-independent maps are distributed without communication, BASELINE config 4);
-time = max over ranks of the device time of K steps.
+One "step" = one pass of the hot path (the whole SURVEY.md §8 path, simplify
+included) over synthetic maps of BASELINE.json config C, inputs resident in
+HBM.  Prints ONE JSON line (rank 0).  Modes (by config, --mode overrides):
 
---impl reference times the reference algorithm's CPU implementation (the
-pinned numpy port in oracle/, the reference package cannot travel to the box)
-on the same map with all host threads; rank 0 only.
+  replica  (configs 0-2, default config 1 = 5M points): every rank processes
+           its own independently seeded map, no data-path collective
+           ("batches of independent maps are distributed without
+           communication"); scaling "weak".
+  sharded  (config 3, 200M points): ONE map split into row bands over the
+           ranks (device partition + NCCL all-to-all of points, halo rows by
+           NCCL send/recv, any()-tables all-reduced for simplify); "strong".
+  batch    (config 4): 256 independent 250k-point maps split over the ranks,
+           each rank runs its share per step; value also as maps/s; "strong".
+
+Timing: W warm-up steps (and >= 0.5 s so clocks ramp), then K steps each
+bracketed by CUDA events on the library's stream; L2 flushed (256 MiB write)
+between steps outside the events; barrier + synchronize around the timed
+region; max over ranks.  --impl reference times the reference algorithm's CPU
+implementation (the numpy port in oracle/, pinned to the reference's outputs;
+the reference package cannot travel to the GPU box) on all host threads,
+rank 0 only, on the same map (configs 2-3: a bounded crop, stated).
 """
 
 from __future__ import annotations
@@ -19,10 +30,8 @@ from __future__ import annotations
 import argparse
 import ctypes as C
 import json
-import math
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -37,6 +46,7 @@ from paper_2403_07631_b200 import synth  # noqa: E402
 
 METRIC = "tomogram build+eval ms/map & Mpts/s at 1/2/4/8 B200; % HBM peak; vs CPU ref"
 L2_FLUSH_BYTES = 256 << 20
+MODES = {0: "replica", 1: "replica", 2: "replica", 3: "sharded", 4: "batch"}
 
 
 def parse():
@@ -45,25 +55,21 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--mode", choices=["replica", "sharded", "batch"], default=None)
     ap.add_argument("--points", type=int, default=None, help="override the config's N")
+    ap.add_argument("--maps", type=int, default=None, help="config 4: total maps (default 256)")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--profile", action="store_true", help="1 warm-up + 1 step, no extras (ncu)")
-    return ap.parse_args()
+    a = ap.parse_args()
+    a.mode = a.mode or MODES[a.config]
+    return a
 
 
 def dist_env():
     return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
             int(os.environ.get("LOCAL_RANK", 0)))
-
-
-def workload(args, rank):
-    cfg = synth.CONFIGS[args.config]
-    n = args.points or cfg["n_points"]
-    seed = cfg["seed"] + rank
-    xyz = synth.generate(args.config, n, seed)
-    return cfg, xyz, seed
 
 
 def peaks():
@@ -72,6 +78,16 @@ def peaks():
         d = json.loads(p.read_text())
         return float(d["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured copy bandwidth)"
     return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+def cpu_model():
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
 
 
 class ClockSampler:
@@ -130,58 +146,96 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# reference arm / CPU baseline (the pinned numpy port of the reference)
+# CPU side: the reference algorithm (oracle port) on host cores
 
 def cpu_pipeline(xyz, cfg, threads):
     import oracle
     from paper_2403_07631_b200.traversability import TravParams
-    TABLE_PARAMS = TravParams()
+    params = TravParams()
     t0 = time.perf_counter()
     t = oracle.build(xyz, cfg["d_s"], cfg["r_g"], threads=threads)
     t1 = time.perf_counter()
-    cost = oracle.evaluate(t["ground"], t["ceiling"], cfg["r_g"], TABLE_PARAMS, threads=threads)
+    cost = oracle.evaluate(t["ground"], t["ceiling"], cfg["r_g"], params, threads=threads)
     t2 = time.perf_counter()
     keep = oracle.simplify(t["ground"], cost)
     t3 = time.perf_counter()
     return (t3 - t0), dict(build=t1 - t0, evaluate=t2 - t1, simplify=t3 - t2), len(keep)
 
 
-def cpu_model():
-    try:
-        for ln in Path("/proc/cpuinfo").read_text().splitlines():
-            if ln.startswith("model name"):
-                return ln.split(":", 1)[1].strip()
-    except Exception:
-        pass
-    return "unknown"
+def cpu_sample(xyz, cfg, max_points=5_000_000):
+    """The bounded CPU sample: the whole map if it has <= max_points points,
+    else the points of a corner square of the map holding about max_points."""
+    n = len(xyz)
+    if n <= max_points:
+        return xyz, "full map"
+    frac = max_points / n
+    lo = xyz.min(axis=0)
+    hi = xyz.max(axis=0)
+    side = np.sqrt(frac) * (hi[:2] - lo[:2])
+    m = (xyz[:, 0] < lo[0] + side[0]) & (xyz[:, 1] < lo[1] + side[1])
+    sub = np.ascontiguousarray(xyz[m])
+    return sub, f"corner crop {side[0]:.0f} x {side[1]:.0f} m ({len(sub)} of {n} points)"
+
+
+def workload(args, rank, world):
+    """(cfg, list of per-rank maps (xyz arrays), description)."""
+    cfg = dict(synth.CONFIGS[args.config])
+    n = args.points or cfg["n_points"]
+    if args.mode == "replica":
+        seed = cfg["seed"] + rank
+        return cfg, [synth.generate(args.config, n, seed)], f"seed {seed}"
+    if args.mode == "batch":
+        total = args.maps or cfg.get("n_maps", 256)
+        mine = list(range(rank, total, world))
+        return cfg, [synth.generate(4, n, cfg["seed"] + m) for m in mine], \
+            f"maps {total} (seeds {cfg['seed']}+m), {len(mine)} on this rank"
+    # sharded: every rank draws the same map and keeps every world-th point
+    xyz = synth.generate(args.config, n, cfg["seed"])
+    return cfg, [np.ascontiguousarray(xyz[rank::world])], f"seed {cfg['seed']}, 1/{world} points"
 
 
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    cfg, xyz, seed = workload(args, 0)
+    cfg = dict(synth.CONFIGS[args.config])
+    n = args.points or cfg["n_points"]
+    if args.config == 4:
+        maps = [synth.generate(4, n, cfg["seed"] + m) for m in range(2)]
+        desc = "2 of the batch maps per step (extrapolated per map)"
+    else:
+        full = synth.generate(args.config, n, cfg["seed"])
+        sub, how = cpu_sample(full, cfg)
+        maps, desc = [sub], how
+        del full
     threads = os.cpu_count() or 1
     for _ in range(args.warmup):
-        cpu_pipeline(xyz, cfg, threads)
+        for xyz in maps:
+            cpu_pipeline(xyz, cfg, threads)
     times, stages = [], []
     for _ in range(args.steps):
-        t, st, keep = cpu_pipeline(xyz, cfg, threads)
+        t = 0.0
+        st = {"build": 0.0, "evaluate": 0.0, "simplify": 0.0}
+        for xyz in maps:
+            dt, s, _ = cpu_pipeline(xyz, cfg, threads)
+            t += dt
+            for k in st:
+                st[k] += s[k]
         times.append(t)
         stages.append(st)
+    pts = sum(len(x) for x in maps)
     ms = 1e3 * statistics.mean(times)
-    mpts = len(xyz) / (ms * 1e3)
+    mpts = pts / (ms * 1e3)
     line = {
         "impl": "reference", "metric": METRIC, "value": mpts, "unit": "Mpts/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": f"cfg{args.config} {cfg['name']}", "n_points": len(xyz),
-                   "seed": seed, "r_g": cfg["r_g"], "d_s": cfg["d_s"]},
+        "config": {"workload": f"cfg{args.config} {cfg['name']}", "n_points": pts,
+                   "r_g": cfg["r_g"], "d_s": cfg["d_s"], "sample": desc},
         "stages_ms": {k: 1e3 * statistics.mean(s[k] for s in stages) for k in stages[0]},
         "cpu_baseline": {"value": mpts, "unit": "Mpts/s", "cores": threads, "kind": "port",
-                         "sample": f"full cfg{args.config} map per step (build+evaluate+simplify),"
-                                   f" {cpu_model()}"},
+                         "sample": f"{desc}; build+evaluate+simplify per step; {cpu_model()}"},
         "e2e": {"value": mpts, "unit": "Mpts/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -190,6 +244,59 @@ def run_reference(args):
 
 # ---------------------------------------------------------------------------
 # B200 arm
+
+class Pipeline:
+    """Stage-by-stage device pipeline over the C ABI (events between stages)."""
+
+    def __init__(self, ctx, stream, cfg):
+        import paper_2403_07631_b200 as pct
+        from paper_2403_07631_b200 import _lib
+        self.ctx, self.stream, self.cfg = ctx, stream, cfg
+        self.lib, self.h = ctx.lib, ctx.h
+        self._lib = _lib
+        p = pct.TravParams()
+        self.pc = _lib.trav_params_c(p, cfg["r_g"])
+        self.w = np.ascontiguousarray(pct.build_kernel(p.d_inf, p.d_sm, cfg["r_g"]).weights)
+        self.info = {}
+
+    def ev(self):
+        import torch
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(self.stream)
+        return e
+
+    def run(self, dxyz, n):
+        from paper_2403_07631_b200.tomogram import new_device_stack
+        _lib, lib, h, ctx = self._lib, self.lib, self.h, self.ctx
+        d_s, r_g = self.cfg["d_s"], self.cfg["r_g"]
+        e0 = self.ev()
+        lo = np.empty(3)
+        hi = np.empty(3)
+        ctx.check(lib.pct_bounds(h, dxyz.ptr, n, _lib.PCT_F32, lo.ctypes.data, hi.ctypes.data),
+                  "bounds")
+        fr = _lib.FrameC()
+        hts = np.empty(65536)
+        assert lib.pct_frame_compute(lo.ctypes.data, hi.ctypes.data, d_s, r_g, 16384,
+                                     C.byref(fr), hts.ctypes.data, 65536) == 0
+        S, R, Cc = fr.n_slices, fr.rows, fr.cols
+        g = new_device_stack(ctx, S, R, Cc)
+        c = new_device_stack(ctx, S, R, Cc)
+        cost = new_device_stack(ctx, S, R, Cc)
+        e1 = self.ev()
+        ctx.check(lib.pct_build(h, dxyz.ptr, n, _lib.PCT_F32, C.byref(fr), hts.ctypes.data,
+                                g.ptr, c.ptr), "build")
+        e2 = self.ev()
+        ctx.check(lib.pct_evaluate(h, g.ptr, c.ptr, S, R, Cc, r_g, C.byref(self.pc),
+                                   self.w.ctypes.data, self.w.shape[0], cost.ptr), "evaluate")
+        e3 = self.ev()
+        keep = np.empty(S, np.int32)
+        nk = C.c_int32()
+        ctx.check(lib.pct_simplify(h, g.ptr, cost.ptr, S, R, Cc, 1e-6, 50.0, keep.ctypes.data,
+                                   C.byref(nk)), "simplify")
+        e4 = self.ev()
+        self.info = dict(S=S, R=R, C=Cc, keep=int(nk.value), stacks=(g, c, cost))
+        return [e0, e1, e2, e3, e4]
+
 
 def run_b200(args):
     import torch
@@ -200,59 +307,43 @@ def run_b200(args):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2403_07631_b200 as pct
-    from paper_2403_07631_b200 import _lib
-    from paper_2403_07631_b200.tomogram import DeviceStack, new_device_stack
+    from paper_2403_07631_b200 import _lib, sharded
 
-    cfg, xyz, seed = workload(args, rank)
+    cfg, maps, desc = workload(args, rank, world)
     d_s, r_g = cfg["d_s"], cfg["r_g"]
-    n = len(xyz)
     ctx = _lib.context(local)
     stream = torch.cuda.Stream(device=local)
     ctx.check(ctx.lib.pct_set_stream(ctx.h, C.c_void_p(stream.cuda_stream)), "set_stream")
-    params = pct.TravParams()
-    pc = _lib.trav_params_c(params, r_g)
-    w = np.ascontiguousarray(pct.build_kernel(params.d_inf, params.d_sm, r_g).weights)
-    dxyz = _lib.DeviceBuffer.from_host(ctx, xyz)
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=f"cuda:{local}")
-    lib, h = ctx.lib, ctx.h
+    pipe = Pipeline(ctx, stream, cfg)
+    n_local = sum(len(m) for m in maps)
 
-    def ev():
-        e = torch.cuda.Event(enable_timing=True)
-        e.record(stream)
-        return e
+    if args.mode == "sharded":
+        dmaps = [torch.from_numpy(maps[0]).to(f"cuda:{local}")]
+    else:
+        dmaps = [_lib.DeviceBuffer.from_host(ctx, m) for m in maps]
 
-    state = {}
+    band_info = {}
 
     def step():
-        """One device-resident pass; returns the 5 stage events."""
-        e0 = ev()
-        lo = np.empty(3)
-        hi = np.empty(3)
-        ctx.check(lib.pct_bounds(h, dxyz.ptr, n, _lib.PCT_F32, lo.ctypes.data, hi.ctypes.data),
-                  "bounds")
-        fr = _lib.FrameC()
-        hts = np.empty(4096)
-        rc = lib.pct_frame_compute(lo.ctypes.data, hi.ctypes.data, d_s, r_g, 16384, C.byref(fr),
-                                   hts.ctypes.data, 4096)
-        assert rc == 0
-        S, R, Cc = fr.n_slices, fr.rows, fr.cols
-        g = new_device_stack(ctx, S, R, Cc)
-        c = new_device_stack(ctx, S, R, Cc)
-        cost = new_device_stack(ctx, S, R, Cc)
-        e1 = ev()
-        ctx.check(lib.pct_build(h, dxyz.ptr, n, _lib.PCT_F32, C.byref(fr), hts.ctypes.data,
-                                g.ptr, c.ptr), "build")
-        e2 = ev()
-        ctx.check(lib.pct_evaluate(h, g.ptr, c.ptr, S, R, Cc, r_g, C.byref(pc), w.ctypes.data,
-                                   w.shape[0], cost.ptr), "evaluate")
-        e3 = ev()
-        keep = np.empty(S, np.int32)
-        nk = C.c_int32()
-        ctx.check(lib.pct_simplify(h, g.ptr, cost.ptr, S, R, Cc, 1e-6, 50.0, keep.ctypes.data,
-                                   C.byref(nk)), "simplify")
-        e4 = ev()
-        state.update(S=S, R=R, C=Cc, keep=int(nk.value), stacks=(g, c, cost))
-        return (e0, e1, e2, e3, e4)
+        """One pass of the path over this rank's data; returns per-stage (start, end) events."""
+        if args.mode == "sharded":
+            with torch.cuda.stream(stream):
+                e0 = pipe.ev()
+                gen = sharded.band_pipeline(dmaps[0], d_s, r_g, pct.TravParams(), rank, world,
+                                            device=local)
+                res = sharded.run_torch(gen) if world > 1 else sharded.run_virtual([gen])[0]
+                e1 = pipe.ev()
+            band_info.update(S=len(res.heights), R=res.rows, C=res.cols, keep=len(res.keep),
+                             nrows=res.nrows, res=res)
+            return {"total": [(e0, e1)]}
+        out = {"bounds": [], "build": [], "evaluate": [], "simplify": [], "total": []}
+        for dm, m in zip(dmaps, maps):
+            e = pipe.run(dm, len(m))
+            for i, k in enumerate(["bounds", "build", "evaluate", "simplify"]):
+                out[k].append((e[i], e[i + 1]))
+            out["total"].append((e[0], e[4]))
+        return out
 
     def flush_l2():
         with torch.cuda.stream(stream):
@@ -265,88 +356,94 @@ def run_b200(args):
         step()
         flush_l2()
         done += 1
-        if done % 8 == 0:
-            torch.cuda.synchronize()
-    torch.cuda.synchronize()
+        torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
+    torch.cuda.synchronize()
     launches0 = ctx.launches
-    evs = []
+    recs = []
     with ClockSampler(local) as clk:
-        torch.cuda.synchronize()
         t_start = time.perf_counter()
         for _ in range(args.steps):
-            evs.append(step())
-            flush_l2()   # between steps, outside the per-step events
+            recs.append(step())
+            flush_l2()  # between steps, outside the step events
         torch.cuda.synchronize()
         t_wall = time.perf_counter() - t_start
+    if world > 1:
+        torch.distributed.barrier()
     launches = ctx.launches - launches0
-    stage_names = ["bounds", "build", "evaluate", "simplify"]
-    per = {k: [] for k in stage_names}
-    totals = []
-    for e in evs:
-        for i, k in enumerate(stage_names):
-            per[k].append(e[i].elapsed_time(e[i + 1]))
-        totals.append(e[0].elapsed_time(e[4]))
-    step_ms = sum(totals)  # device time of the K steps (L2 flushes excluded)
+    per = {}
+    for r in recs:
+        for k, pairs in r.items():
+            per.setdefault(k, []).append(sum(a.elapsed_time(b) for a, b in pairs))
+    step_ms = sum(per["total"])  # device time of the K steps on this rank
+    total_pts = float(n_local)
     if world > 1:
         t = torch.tensor([step_ms], device=f"cuda:{local}", dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         step_ms = float(t.item())
-        cnt = torch.tensor([float(n)], device=f"cuda:{local}", dtype=torch.float64)
+        cnt = torch.tensor([total_pts], device=f"cuda:{local}", dtype=torch.float64)
         torch.distributed.all_reduce(cnt)
         total_pts = float(cnt.item())
-    else:
-        total_pts = float(n)
     ms = step_ms / args.steps
-    value = total_pts * args.steps / (step_ms * 1e3)  # Mpts/s whole job
-    S, R, Cc = state["S"], state["R"], state["C"]
-    cs = S * R * Cc
-    ev_ms = statistics.mean(per["evaluate"])
-    peak, peak_src = peaks()
-    achieved = 12.0 * cs / (ev_ms * 1e-3) / 1e9
-    traffic = None
-    prof = ROOT / "profiles" / "ncu_traffic.json"
-    if prof.exists():
-        try:
-            tr = json.loads(prof.read_text())
-            key = f"cfg{args.config}"
-            if key in tr:
-                traffic = tr[key].get("eval_dram_bytes")
-        except Exception:
-            traffic = None
+    value = total_pts * args.steps / (step_ms * 1e3)  # Mpts/s, whole job
 
+    info = band_info if args.mode == "sharded" else pipe.info
+    S, R, Cc = info["S"], info["R"], info["C"]
+    cs = S * R * Cc
+    peak, peak_src = peaks()
     line = {
         "metric": METRIC, "value": value, "unit": "Mpts/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic",
-        "config": {"workload": f"cfg{args.config} {cfg['name']}: {n} float32 pts/rank, "
-                               f"grid {R}x{Cc}, {S} slices, r_g {r_g}, d_s {d_s}",
-                   "n_points_per_rank": n, "seed": seed, "rows": R, "cols": Cc, "slices": S,
-                   "slices_kept": state["keep"], "r_g": r_g, "d_s": d_s,
+        "higher_is_better": True, "scaling": "strong" if args.mode != "replica" else "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"cfg{args.config} {cfg['name']} ({args.mode}): "
+                               f"{int(total_pts)} float32 pts, grid {R}x{Cc}, {S} slices, "
+                               f"r_g {r_g}, d_s {d_s}",
+                   "mode": args.mode, "points_total": int(total_pts), "data_desc": desc,
+                   "rows": R, "cols": Cc, "slices": S, "slices_kept": info["keep"],
+                   "r_g": r_g, "d_s": d_s,
                    "step": "bounds+build+evaluate+simplify, device-resident points",
                    "l2": f"flushed between steps ({L2_FLUSH_BYTES >> 20} MiB write), "
                          "flush excluded from step time",
-                   "parallelism": f"{world} independent maps (one per GPU)"},
+                   "parallelism": {"replica": f"{world} independent maps (one per GPU)",
+                                   "sharded": f"1 map in {world} row bands (NCCL)",
+                                   "batch": f"{len(maps)} maps per GPU x {world}"}[args.mode]},
         "stages_ms": {k: statistics.mean(v) for k, v in per.items()},
         "wall_s_timed_region": t_wall,
-        "algorithmic_bytes_per_step": 12 * n + 28 * cs,
-        "pipeline_gbs": (12 * n + 28 * cs) / (ms * 1e-3) / 1e9,
-        "roofline": {"kernel": "eval_sym_kernel<4> (fused K4+K5)", "bound": "hbm",
-                     "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic,
-                     "algorithmic": f"12 B per cell-slice x {cs} cell-slices per launch",
-                     "peak_source": peak_src},
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
+    if args.mode == "batch":
+        line["maps_per_s"] = len(maps) * world * args.steps / (step_ms * 1e-3)
+    if args.mode != "sharded":
+        ev_ms = statistics.mean(per["evaluate"]) / len(maps)
+        n_map = n_local / len(maps)
+        achieved = 12.0 * cs / (ev_ms * 1e-3) / 1e9
+        traffic = None
+        prof = ROOT / "profiles" / "ncu_traffic.json"
+        if prof.exists():
+            try:
+                traffic = json.loads(prof.read_text()).get(f"cfg{args.config}", {}).get(
+                    "eval_dram_bytes")
+            except Exception:
+                traffic = None
+        line["algorithmic_bytes_per_map"] = 12 * n_map + 28 * cs
+        line["pipeline_gbs_per_gpu"] = (12 * n_map + 28 * cs) * len(maps) / (
+            step_ms / args.steps * 1e-3) / 1e9
+        line["roofline"] = {"kernel": "fused evaluate (K4+K5)", "bound": "hbm",
+                            "achieved": achieved, "peak": peak, "unit": "GB/s",
+                            "frac": achieved / peak, "traffic": traffic,
+                            "algorithmic": f"12 B per cell-slice x {cs} cell-slices per launch",
+                            "peak_source": peak_src}
 
-    # ---- e2e through the public API with host buffers
-    if not args.no_e2e and not args.profile:
+    # ---- e2e through the public API with host buffers (replica mode)
+    if args.mode == "replica" and not args.no_e2e and not args.profile:
+        xyz = maps[0]
         pin = _lib.PinnedBuffer(ctx, xyz.shape, np.float32)
         pin.array[...] = xyz
         cloud = pct.PointCloud(pin.array)
+        params = pct.TravParams()
         e2e_times = []
         d2h = 0
         for i in range(args.warmup + args.steps):
@@ -355,11 +452,8 @@ def run_b200(args):
             tom = pct.build_tomogram(cloud, d_s, r_g)
             evt = pct.evaluate_tomogram(tom, params)
             simp = pct.simplify_tomogram(evt).materialize()
-            chk = 0.0
             for s in simp.slices:  # the caller reads every surviving layer
-                chk += float(s.ground.values[0, 0] if np.isfinite(s.ground.values[0, 0]) else 0)
-                _ = s.ceiling.values
-                _ = s.cost.values
+                _ = s.ground.values, s.ceiling.values, s.cost.values
             t1 = time.perf_counter()
             if i >= args.warmup:
                 e2e_times.append(t1 - t0)
@@ -371,19 +465,20 @@ def run_b200(args):
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             e2e_s = float(t.item())
         line["e2e"] = {"value": total_pts / (e2e_s * 1e6), "unit": "Mpts/s",
-                       "ms_per_step": 1e3 * e2e_s, "h2d_bytes_per_step": 12 * n,
+                       "ms_per_step": 1e3 * e2e_s, "h2d_bytes_per_step": 12 * len(xyz),
                        "d2h_bytes_per_step": d2h,
                        "path": "PointCloud(pinned f32) -> build_tomogram -> evaluate_tomogram -> "
                                "simplify_tomogram -> host arrays of surviving slices"}
 
-    # ---- CPU baseline (rank 0, N=1 only): the pinned numpy port, all host threads
+    # ---- CPU baseline (rank 0, N=1 only): the reference algorithm on host cores
     if rank == 0 and world == 1 and not args.no_cpu and not args.profile:
         threads = os.cpu_count() or 1
-        t, st, _ = cpu_pipeline(xyz, cfg, threads)
-        line["cpu_baseline"] = {"value": n / (t * 1e6), "unit": "Mpts/s", "cores": threads,
-                                "kind": "port",
-                                "sample": f"1 full cfg{args.config} map (build+evaluate+simplify,"
-                                          f" {t:.1f} s), {cpu_model()}",
+        sub, how = cpu_sample(maps[0], cfg)
+        t, st, _ = cpu_pipeline(sub, cfg, threads)
+        line["cpu_baseline"] = {"value": len(sub) / (t * 1e6), "unit": "Mpts/s",
+                                "cores": threads, "kind": "port",
+                                "sample": f"{how} of cfg{args.config} (build+evaluate+simplify, "
+                                          f"{t:.1f} s), {cpu_model()}",
                                 "stages_s": st}
     if rank == 0:
         print(json.dumps(line), flush=True)
