@@ -173,6 +173,12 @@ int pct_tomo_evaluate(pct_ctx *ctx, pct_tomo *t, const pct_trav_params *p,
                       const float *kernel_w, int32_t kside);
 int pct_tomo_simplify(pct_ctx *ctx, pct_tomo *t, double eps_e, double c_barrier,
                       int32_t *keep_host, int32_t *n_keep);
+/* build -> evaluate -> simplify in one call (the whole hot path of one map;
+   keep_host needs room for the slice count, at most 65536). */
+int pct_tomo_run(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, int xyz_on_host,
+                 double d_s, double r_g, int64_t max_grid_side, const pct_trav_params *p,
+                 const float *kernel_w, int32_t kside, double eps_e, double c_barrier,
+                 pct_tomo **out, int32_t *keep_host, int32_t *n_keep);
 int pct_tomo_frame(const pct_tomo *t, pct_frame *fr, double *heights, int32_t heights_cap);
 /* device pointer of a layer stack (NULL if absent), e.g. for zero-copy consumers */
 const float *pct_tomo_layer(const pct_tomo *t, int layer);

@@ -1,0 +1,103 @@
+"""Many independent maps on one GPU (BASELINE config 4: 256 two-storey maps).
+
+Small maps are latency-bound: one map's pipeline is a handful of short
+kernels separated by two host round trips (grid frame after the bounds,
+simplify sweep).  ``BatchRunner`` keeps ``workers`` maps in flight: each
+worker thread owns a libpct context with its own CUDA stream and scratch and
+runs the whole path with one native call (``pct_tomo_run``; ctypes releases
+the GIL for its duration), so the syncs of one map overlap the kernels of
+the others.  Maps never communicate ("batches of independent maps are
+distributed without communication"); across GPUs each rank takes its share.
+
+``evaluate_maps`` is the public entry (an extension of the reference API):
+clouds in, simplified device-backed ``Tomogram`` objects out, identical to
+running build_tomogram -> evaluate_tomogram -> simplify_tomogram per cloud.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import queue
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+
+from . import _lib
+from .tomogram import GRID_SIDE_LIMIT, DeviceTomogram, Layer, Tomogram, TomogramSlice
+from .traversability import build_kernel
+
+
+class BatchRunner:
+    def __init__(self, device: int | None = None, workers: int = 8, streams=None):
+        dev = _lib.default_device() if device is None else int(device)
+        self.ctxs = [_lib.Context(dev) for _ in range(workers)]
+        if streams is not None:  # caller-provided CUDA streams (e.g. for event timing)
+            for ctx, s in zip(self.ctxs, streams):
+                ctx.check(ctx.lib.pct_set_stream(ctx.h, C.c_void_p(int(s))), "set_stream")
+        self.free = queue.Queue()
+        for c in self.ctxs:
+            self.free.put(c)
+        self.pool = ThreadPoolExecutor(workers)
+
+    def _one(self, ptr, n, code, on_host, d_s, r_g, pc, w, eps_e, c_barrier, keep_handle):
+        ctx = self.free.get()
+        try:
+            h = C.c_void_p()
+            keep = np.empty(65536, np.int32)
+            nk = C.c_int32()
+            rc = ctx.lib.pct_tomo_run(ctx.h, ptr, n, code, on_host, d_s, r_g, GRID_SIDE_LIMIT,
+                                      C.byref(pc), w.ctypes.data, w.shape[0], eps_e, c_barrier,
+                                      C.byref(h), keep.ctypes.data, C.byref(nk))
+            ctx.check(rc, "pct_tomo_run")
+            if not keep_handle:
+                ctx.lib.pct_tomo_free(ctx.h, h)
+                return None, keep[:nk.value].tolist()
+            return (ctx, h), keep[:nk.value].tolist()
+        finally:
+            self.free.put(ctx)
+
+    def run(self, maps, d_s, r_g, params, eps_e=1e-6, c_barrier=50.0, keep_handles=True):
+        """maps: list of (pointer, n_points, dtype code, on_host).  Returns, in
+        order, ((ctx, pct_tomo handle) or None, surviving slice indices)."""
+        w = np.ascontiguousarray(build_kernel(params.d_inf, params.d_sm, r_g).weights)
+        pc = _lib.trav_params_c(params, r_g)
+        futs = [self.pool.submit(self._one, int(p), int(n), code, int(on_host), float(d_s),
+                                 float(r_g), pc, w, float(eps_e), float(c_barrier), keep_handles)
+                for p, n, code, on_host in maps]
+        return [f.result() for f in futs]
+
+    def close(self):
+        self.pool.shutdown()
+
+
+def _to_tomogram(ctx, handle, keep, d_s, r_g):
+    dt = DeviceTomogram(ctx, handle)
+    gst, cst = dt.stacks()
+    from .tomogram import DeviceStack
+    fr = dt.frame
+    cost = DeviceStack(ctx, ctx.lib.pct_tomo_layer(handle, _lib.LAYER_COST), fr.n_slices,
+                       fr.rows, fr.cols, dt)
+    origin = (float(fr.origin_x), float(fr.origin_y))
+    slices = [TomogramSlice(Layer.on_device(gst, k, r_g, origin), Layer.on_device(cst, k, r_g, origin),
+                            float(dt.heights[k]), i, Layer.on_device(cost, k, r_g, origin))
+              for i, k in enumerate(keep)]
+    return Tomogram(slices=slices, d_s=float(d_s), z_min=float(fr.z_min))
+
+
+def evaluate_maps(clouds, d_s, r_g, params, *, workers=8, device=None, eps_e=1e-6,
+                  c_barrier=50.0, runner: BatchRunner | None = None):
+    """build -> evaluate -> simplify for every cloud; returns the simplified
+    tomograms (device-resident, host arrays on access)."""
+    if d_s <= 0 or r_g <= 0:
+        raise ValueError("d_s and r_g must be positive")
+    own = runner is None
+    runner = runner or BatchRunner(device, workers)
+    arrays = [np.ascontiguousarray(c.xyz if hasattr(c, "xyz") else c) for c in clouds]
+    maps = [(a.ctypes.data, a.shape[0], _lib.PCT_F32 if a.dtype == np.float32 else _lib.PCT_F64, 1)
+            for a in arrays]
+    try:
+        res = runner.run(maps, d_s, r_g, params, eps_e, c_barrier)
+    finally:
+        if own:
+            runner.close()
+    return [_to_tomogram(h[0], h[1], keep, d_s, r_g) for h, keep in res]

@@ -454,6 +454,23 @@ int pct_tomo_simplify(pct_ctx *ctx, pct_tomo *t, double eps_e, double c_barrier,
                       c_barrier, keep_host, n_keep);
 }
 
+int pct_tomo_run(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, int xyz_on_host,
+                 double d_s, double r_g, int64_t max_grid_side, const pct_trav_params *p,
+                 const float *kernel_w, int32_t kside, double eps_e, double c_barrier,
+                 pct_tomo **out, int32_t *keep_host, int32_t *n_keep) {
+  if (!out || !keep_host || !n_keep) return fail(ctx, PCT_E_INVALID, "bad arguments to pct_tomo_run");
+  pct_tomo *t = nullptr;
+  int rc = pct_tomo_build(ctx, xyz, n, dtype, xyz_on_host, d_s, r_g, max_grid_side, &t);
+  if (rc) return rc;
+  if ((rc = pct_tomo_evaluate(ctx, t, p, kernel_w, kside)) ||
+      (rc = pct_tomo_simplify(ctx, t, eps_e, c_barrier, keep_host, n_keep))) {
+    pct_tomo_free(ctx, t);
+    return rc;
+  }
+  *out = t;
+  return PCT_OK;
+}
+
 int pct_tomo_frame(const pct_tomo *t, pct_frame *fr, double *heights, int32_t heights_cap) {
   if (!t || !fr) return PCT_E_INVALID;
   *fr = t->fr;

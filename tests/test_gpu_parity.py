@@ -286,3 +286,21 @@ def test_evaluate_accepts_host_tomogram(golden):
     # evaluate_slice path
     sl = pct.evaluate_slice(tom.slices[2], pct.TravParams())
     assert np.array_equal(sl.cost.values, Cost[2])
+
+
+def test_batch_runner_matches_single_maps():
+    """evaluate_maps (concurrent contexts, one native call per map) returns the
+    same simplified tomograms as the per-map drop-in calls."""
+    from paper_2403_07631_b200 import synth
+    from paper_2403_07631_b200.batch import evaluate_maps
+    clouds = [synth.generate(4, 60_000, 1000 + m) for m in range(12)]
+    outs = evaluate_maps(clouds, 0.5, 0.1, pct.TravParams(), workers=4)
+    for xyz, got in zip(clouds, outs):
+        ev = pct.evaluate_tomogram(pct.build_tomogram(pct.PointCloud(xyz), 0.5, 0.1),
+                                   pct.TravParams())
+        want = pct.simplify_tomogram(ev)
+        assert [s.plane_height for s in got.slices] == [s.plane_height for s in want.slices]
+        for a, b in zip(got.slices, want.slices):
+            for attr in ("ground", "ceiling", "cost"):
+                assert np.array_equal(getattr(a, attr).values.view(np.uint32),
+                                      getattr(b, attr).values.view(np.uint32))
