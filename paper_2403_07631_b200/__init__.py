@@ -6,6 +6,7 @@ errors), executed by hand-written sm_100a CUDA kernels in libpct.so through
 a C ABI (include/pct.h).  There is no CPU fallback.
 """
 
+from .archive import load_tomogram, save_tomogram
 from .cloud import CloudFormatError, PointCloud
 from .simplify import DEFAULT_EPS_E, simplify_tomogram, unique_cells
 from .tomogram import (
@@ -39,5 +40,5 @@ __all__ = [
     "GRID_SIDE_LIMIT", "GridSizeError", "Layer", "Tomogram", "TomogramSlice", "build_tomogram",
     "rasterize_index", "InflationKernel", "TravParams", "build_kernel", "evaluate_slice",
     "evaluate_tomogram", "fuse_costs", "gentle_fraction", "ground_cost", "inflate",
-    "interval_cost", "slope_magnitudes", "terrain_cost_values",
+    "interval_cost", "slope_magnitudes", "terrain_cost_values", "save_tomogram", "load_tomogram",
 ]

@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import importlib
 
+from . import archive as _arch
 from . import simplify as _simp
 from . import tomogram as _tomo
 from . import traversability as _trav
@@ -36,6 +37,8 @@ REPLACEMENTS = {
     "inflate": _trav.inflate,
     "simplify_tomogram": _simp.simplify_tomogram,
     "unique_cells": _simp.unique_cells,
+    "save_tomogram": _arch.save_tomogram,   # byte-identical LGA writer (§8 f)
+    "load_tomogram": _arch.load_tomogram,
 }
 
 MODULES = ("", ".tomogram", ".traversability", ".simplify", ".cli", ".bench")

@@ -588,6 +588,8 @@ int launch_fast(pct_ctx *ctx, const float *ground, const float *ceiling, int S, 
       const char *t = getenv("PCT_EVAL_TILE");
       if (t && atoi(t) == 64)
         return launch_incr_t<R, PR, 64, 64, 256, 2>(ctx, ground, ceiling, S, rows, cols, cost);
+      if (t && atoi(t) == 16)
+        return launch_incr_t<R, PR, 16, 32, 64, 8>(ctx, ground, ceiling, S, rows, cols, cost);
       return launch_incr_t<R, PR, 32, 32, 128, 4>(ctx, ground, ceiling, S, rows, cols, cost);
     }
   }

@@ -52,10 +52,20 @@ def run_reference(xyz, d_s, r_g, threads=8):
     heights = np.array([s.plane_height for s in ev.slices])
     keep_h = [s.plane_height for s in simp.slices]
     keep = [int(np.flatnonzero(heights == h)[0]) for h in keep_h]
+    # the reference's LGA archives (tomogram.py:228-244) of the built, evaluated
+    # and simplified tomograms: the byte-exact target of save_tomogram
+    import tempfile
+    lga = {}
+    with tempfile.TemporaryDirectory() as d:
+        for key, t in (("built", tom), ("evaluated", ev), ("simplified", simp)):
+            p = Path(d) / f"{key}.lga"
+            tp.save_tomogram(t, p)
+            b = p.read_bytes()
+            lga[key] = dict(sha256=hashlib.sha256(b).hexdigest(), bytes=len(b))
     out = dict(
         ground=ev.ground_stack(), ceiling=ev.ceiling_stack(), cost=ev.cost_stack(),
         heights=heights, keep=np.array(keep, np.int64),
-        origin=np.array(ev.origin, np.float64), z_min=float(ev.z_min),
+        origin=np.array(ev.origin, np.float64), z_min=float(ev.z_min), lga=lga,
     )
     return out, (t1 - t0, t2 - t1, t3 - t2)
 
@@ -75,6 +85,7 @@ def record(name, xyz, d_s, r_g, meta, store_arrays, store_input):
         ground_slice_sha256=[digest(g) for g in out["ground"]],
         ceiling_slice_sha256=[digest(g) for g in out["ceiling"]],
         cost_slice_sha256=[digest(g) for g in out["cost"]],
+        lga=out["lga"],
         ref_seconds=dict(build=times[0], evaluate=times[1], simplify=times[2], threads=8),
     )
     if store_arrays or store_input:

@@ -304,3 +304,30 @@ def test_batch_runner_matches_single_maps():
             for attr in ("ground", "ceiling", "cost"):
                 assert np.array_equal(getattr(a, attr).values.view(np.uint32),
                                       getattr(b, attr).values.view(np.uint32))
+
+
+@pytest.mark.parametrize("name", ["ref_random_multilayer_s9", "ref_spiral_s3", "synth_cfg0",
+                                  "synth_cfg1"])
+def test_lga_archives_byte_identical(golden, tmp_path, name):
+    """save_tomogram streams device layers into the archive: the files of the
+    built, evaluated and simplified tomograms equal the reference's bytes."""
+    import hashlib
+    case = golden["cases"][name]
+    tom, ev, simp = _run(case_input(name, case), case["d_s"], case["r_g"])
+    for key, t in (("built", tom), ("evaluated", ev), ("simplified", simp)):
+        f = tmp_path / f"{key}.lga"
+        pct.save_tomogram(t, f)
+        b = f.read_bytes()
+        assert len(b) == case["lga"][key]["bytes"]
+        assert hashlib.sha256(b).hexdigest() == case["lga"][key]["sha256"], key
+        back = pct.load_tomogram(f)
+        g = tmp_path / f"{key}2.lga"
+        pct.save_tomogram(back, g)
+        assert g.read_bytes() == b
+
+
+def test_load_tomogram_errors(tmp_path):
+    f = tmp_path / "junk.lga"
+    f.write_bytes(b"not an archive at all")
+    with pytest.raises(ValueError, match="not an LGA archive"):
+        pct.load_tomogram(f)

@@ -39,3 +39,22 @@ def test_oracle_inflation_cases(golden):
         g = np.random.default_rng(c["seed"]).uniform(0.0, 50.0, shape).astype(np.float32)
         g[np.random.default_rng(c["seed"] + 1).uniform(size=shape) < 0.03] = 50.0
         assert digest(oracle.inflate(g, w)) == c["out_sha256"]
+
+
+@pytest.mark.parametrize("name", ["ref_random_multilayer_s9", "ref_spiral_s3", "synth_cfg0"])
+def test_oracle_lga_bytes_match_reference(golden, name):
+    """The LGA archive restatement reproduces the reference's archive bytes."""
+    import hashlib
+    from oracle.archive import lga_bytes
+    case = golden["cases"][name]
+    t = oracle.build(case_input(name, case), case["d_s"], case["r_g"])
+    cost = oracle.evaluate(t["ground"], t["ceiling"], case["r_g"], TABLE_PARAMS)
+    args = (t["heights"], t["origin"], case["r_g"], t["z_min"], case["d_s"])
+    built = lga_bytes(t["ground"], t["ceiling"], None, *args)
+    assert hashlib.sha256(built).hexdigest() == case["lga"]["built"]["sha256"]
+    ev = lga_bytes(t["ground"], t["ceiling"], cost, *args)
+    assert hashlib.sha256(ev).hexdigest() == case["lga"]["evaluated"]["sha256"]
+    keep = oracle.simplify(t["ground"], cost)
+    simp = lga_bytes(t["ground"][keep], t["ceiling"][keep], cost[keep], t["heights"][keep],
+                     *args[1:])
+    assert hashlib.sha256(simp).hexdigest() == case["lga"]["simplified"]["sha256"]
