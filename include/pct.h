@@ -161,6 +161,13 @@ int pct_simplify_triples(pct_ctx *ctx, const float *ground, const float *cost, i
                          int64_t cells, int64_t slice_stride, double eps_e, double c_barrier,
                          const int32_t *triples, int32_t n_triples, int32_t *flags_host);
 
+/* ---- planner context precompute (planner.py:65-93, SURVEY.md §8 f) ----- */
+/* Canonical-node arrays of an evaluated (or simplified) tomogram: canon[k]
+   = first slice of the run of equal ground (|dz| <= eps_e, both valid) that
+   contains slice k, cn[k] = the run's minimum cost (inf without ground). */
+int pct_planner_context(pct_ctx *ctx, const float *ground, const float *cost, int32_t n_slices,
+                        int32_t rows, int32_t cols, double eps_e, int32_t *canon, float *cn);
+
 /* ---- whole pipeline on a device-resident tomogram ---------------------- */
 /* xyz may be a device pointer (xyz_on_host = 0) or host memory (1; pinned
    memory from pct_host_alloc is fastest).  Allocates the stacks. */

@@ -79,6 +79,7 @@ _SIGS = {
                         _vp], C.c_int),
     "pct_simplify_window": ([_vp, _vp, _vp, _i32, _i64, _i64, _d, _d, _vp], C.c_int),
     "pct_simplify_triples": ([_vp, _vp, _vp, _i32, _i64, _i64, _d, _d, _vp, _i32, _vp], C.c_int),
+    "pct_planner_context": ([_vp, _vp, _vp, _i32, _i32, _i32, _d, _vp, _vp], C.c_int),
     "pct_tomo_build": ([_vp, _vp, _i64, C.c_int, C.c_int, _d, _d, _i64, C.POINTER(_vp)], C.c_int),
     "pct_tomo_upload": ([_vp, C.POINTER(FrameC), _vp, _vp, _vp, C.POINTER(_vp)], C.c_int),
     "pct_tomo_evaluate": ([_vp, _vp, C.POINTER(TravParamsC), _vp, _i32], C.c_int),

@@ -180,3 +180,65 @@ int pct_simplify_triples(pct_ctx *ctx, const float *ground, const float *cost, i
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Planner context precompute (SURVEY.md §8 f rank 2): the per-cell run merge
+// of planner.py:65-93 that the CPU A* consumes.  Runs of slices whose ground
+// is valid in both and differs by <= eps_e form one canonical node: canon[k]
+// = first slice of the run, cn[k] = minimum member cost of the run (inf where
+// the ground is invalid), broadcast to every member.  One thread per cell
+// column, a forward and a backward walk over k.
+namespace pct {
+namespace {
+
+__global__ void __launch_bounds__(256) planner_ctx_kernel(const float *__restrict__ ground,
+                                                          const float *__restrict__ cost, int S,
+                                                          int64_t cells, double eps_e,
+                                                          int32_t *__restrict__ canon,
+                                                          float *__restrict__ cn) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= cells) return;
+  const float inf = __int_as_float(0x7f800000);
+  float e_prev = ground[c];
+  bool v_prev = finite32(e_prev);
+  int32_t run = 0;
+  float cmin = v_prev ? cost[c] : inf;
+  canon[c] = 0;
+  cn[c] = cmin;
+  for (int k = 1; k < S; ++k) {
+    const float e = ground[(int64_t)k * cells + c];
+    const bool v = finite32(e);
+    const bool eq = v && v_prev && fabs((double)e - (double)e_prev) <= eps_e;
+    const float ck = v ? cost[(int64_t)k * cells + c] : inf;
+    if (eq) {
+      cmin = fminf(ck, cmin);  // np.minimum(cn[k], cn[k-1]); costs are never NaN
+    } else {
+      run = k;
+      cmin = ck;
+    }
+    canon[(int64_t)k * cells + c] = run;
+    cn[(int64_t)k * cells + c] = cmin;
+    e_prev = e;
+    v_prev = v;
+  }
+  // backward broadcast of the run minimum (planner.py:91-92)
+  for (int k = S - 2; k >= 0; --k)
+    if (canon[(int64_t)(k + 1) * cells + c] == canon[(int64_t)k * cells + c])
+      cn[(int64_t)k * cells + c] = cn[(int64_t)(k + 1) * cells + c];
+}
+
+}  // namespace
+}  // namespace pct
+
+extern "C" int pct_planner_context(pct_ctx *ctx, const float *ground, const float *cost,
+                                   int32_t n_slices, int32_t rows, int32_t cols, double eps_e,
+                                   int32_t *canon, float *cn) {
+  if (!ctx) return PCT_E_INVALID;
+  if (cudaSetDevice(ctx->device) != cudaSuccess) return PCT_E_CUDA;
+  if (!ground || !cost || !canon || !cn || n_slices <= 0 || rows <= 0 || cols <= 0)
+    return fail(ctx, PCT_E_INVALID, "bad arguments to pct_planner_context");
+  const int64_t cells = (int64_t)rows * cols;
+  planner_ctx_kernel<<<(unsigned)((cells + 255) / 256), 256, 0, ctx->stream>>>(
+      ground, cost, n_slices, cells, eps_e, canon, cn);
+  return check_launch(ctx, "planner_ctx_kernel");
+}

@@ -62,10 +62,18 @@ def run_reference(xyz, d_s, r_g, threads=8):
             tp.save_tomogram(t, p)
             b = p.read_bytes()
             lga[key] = dict(sha256=hashlib.sha256(b).hexdigest(), bytes=len(b))
+    # the A* planner's canonical-node arrays (planner.py:65-93) of the
+    # evaluated and the simplified tomogram: the target of the §8 f precompute
+    from tomoplan.planner import _PlannerContext
+    planner = {}
+    for key, t in (("evaluated", ev), ("simplified", simp)):
+        pc = _PlannerContext(t, 1e-6, 50.0)
+        planner[key] = dict(canon_sha256=digest(pc.canon), cn_sha256=digest(pc.cn))
     out = dict(
         ground=ev.ground_stack(), ceiling=ev.ceiling_stack(), cost=ev.cost_stack(),
         heights=heights, keep=np.array(keep, np.int64),
         origin=np.array(ev.origin, np.float64), z_min=float(ev.z_min), lga=lga,
+        planner=planner,
     )
     return out, (t1 - t0, t2 - t1, t3 - t2)
 
@@ -86,6 +94,7 @@ def record(name, xyz, d_s, r_g, meta, store_arrays, store_input):
         ceiling_slice_sha256=[digest(g) for g in out["ceiling"]],
         cost_slice_sha256=[digest(g) for g in out["cost"]],
         lga=out["lga"],
+        planner=out["planner"],
         ref_seconds=dict(build=times[0], evaluate=times[1], simplify=times[2], threads=8),
     )
     if store_arrays or store_input:

@@ -331,3 +331,17 @@ def test_load_tomogram_errors(tmp_path):
     f.write_bytes(b"not an archive at all")
     with pytest.raises(ValueError, match="not an LGA archive"):
         pct.load_tomogram(f)
+
+
+@pytest.mark.parametrize("name", ["ref_random_multilayer_s9", "ref_spiral_s3", "synth_cfg0",
+                                  "synth_cfg1"])
+def test_planner_context_matches_reference(golden, name):
+    """GPU canonical-node arrays == the reference planner's (planner.py:65-93)."""
+    from paper_2403_07631_b200.planner_ctx import attach_planner_context
+    case = golden["cases"][name]
+    _, ev, simp = _run(case_input(name, case), case["d_s"], case["r_g"])
+    for key, t in (("evaluated", ev), ("simplified", simp)):
+        pc = attach_planner_context(t)
+        assert t._planner_ctx is pc and pc.eps_e == 1e-6 and pc.c_barrier == 50.0
+        assert digest(pc.canon) == case["planner"][key]["canon_sha256"], key
+        assert digest(pc.cn) == case["planner"][key]["cn_sha256"], key

@@ -58,3 +58,18 @@ def test_oracle_lga_bytes_match_reference(golden, name):
     simp = lga_bytes(t["ground"][keep], t["ceiling"][keep], cost[keep], t["heights"][keep],
                      *args[1:])
     assert hashlib.sha256(simp).hexdigest() == case["lga"]["simplified"]["sha256"]
+
+
+@pytest.mark.parametrize("name", ["ref_random_multilayer_s9", "ref_spiral_s3", "synth_cfg0"])
+def test_oracle_planner_context_matches_reference(golden, name):
+    from oracle.planner_ctx import planner_context
+    case = golden["cases"][name]
+    t = oracle.build(case_input(name, case), case["d_s"], case["r_g"])
+    cost = oracle.evaluate(t["ground"], t["ceiling"], case["r_g"], TABLE_PARAMS)
+    canon, cn = planner_context(t["ground"], cost)
+    assert digest(canon) == case["planner"]["evaluated"]["canon_sha256"]
+    assert digest(cn) == case["planner"]["evaluated"]["cn_sha256"]
+    keep = case["keep"]
+    canon, cn = planner_context(t["ground"][keep], cost[keep])
+    assert digest(canon) == case["planner"]["simplified"]["canon_sha256"]
+    assert digest(cn) == case["planner"]["simplified"]["cn_sha256"]
