@@ -148,6 +148,7 @@ int pct_ctx_destroy(pct_ctx *ctx) {
   if (ctx->scratch) cudaFree(ctx->scratch);
   if (ctx->staging) cudaFree(ctx->staging);
   if (ctx->dsmall) cudaFree(ctx->dsmall);
+  if (ctx->enc) cudaFree(ctx->enc);
   if (ctx->hsmall) cudaFreeHost(ctx->hsmall);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;

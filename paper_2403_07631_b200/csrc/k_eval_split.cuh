@@ -1,0 +1,250 @@
+// k_eval_split.cuh — two-kernel evaluation (included by k_evaluate.cu inside
+// namespace pct::{anon}; uses its c_K / c_wsym and the inflation helpers).
+//
+//  T  terrain_walk_kernel: one thread per cell walks the slices bottom-up.
+//     The float64 terrain arithmetic (gradients, guarded glibc hypot, costs)
+//     runs only when the cell's 5-point ground cross differs from the slice
+//     below, the interval/fuse step only when the cross or the ceiling
+//     differs; otherwise the previous slice's values are reused (they are a
+//     function of exactly those inputs, so the result is bit-identical).  On
+//     the config maps ground and ceiling change in < 25 % of the cells per
+//     slice (a cutting plane passes a surface).  Writes the encoded c_init
+//     (float32, sign bit = foothold branch pending) and the gentle flags as a
+//     row-major bitmap per slice (one __ballot_sync word per 32 cells).
+//  I  resolve_inflate_kernel: per 64x64 tile and slice, the encoded c_init
+//     tile + R halo and the gentle bits of the foothold window are staged in
+//     shared memory, the pending cells are resolved by popcount over
+//     (2r+1)^2 bits, and the weighted max of the inflation kernel is taken
+//     from a register ring of pair maxima (as eval_fast_kernel stage E).
+// No cell is computed twice for a halo, and T needs no block barrier.
+
+constexpr int kWalkNT = 256;
+
+// Encoded c_init stacks live in a zero-padded layout: every tile + halo the
+// inflation kernel stages is in bounds and reads 0 outside the map
+// (inflate's cval=0), and row starts are 16-byte aligned for float4 loads.
+struct EncLayout {
+  int padr, padc;        // rows / columns of zeros before the map
+  int64_t pitch;         // floats per padded row (multiple of 4)
+  int64_t sstride;       // floats per padded slice
+  int prows;             // padded rows
+  __host__ __device__ int64_t at(int k, int i, int j) const {
+    return (int64_t)k * sstride + (int64_t)(i + padr) * pitch + (j + padc);
+  }
+};
+
+// zero every padded cell outside the map (interior cells are written by T):
+// one block per padded row; pad rows are cleared whole, map rows only at
+// their left / right margins
+__global__ void __launch_bounds__(128) zero_pads_kernel(float *__restrict__ enc, EncLayout L,
+                                                        int rows, int cols) {
+  const int k = blockIdx.y, r = blockIdx.x;  // padded row
+  float *row = enc + (int64_t)k * L.sstride + (int64_t)r * L.pitch;
+  const int i = r - L.padr;
+  if (i < 0 || i >= rows) {
+    for (int c = threadIdx.x; c < L.pitch; c += blockDim.x) row[c] = 0.0f;
+  } else {
+    for (int c = threadIdx.x; c < L.padc; c += blockDim.x) row[c] = 0.0f;
+    for (int c = L.padc + cols + threadIdx.x; c < L.pitch; c += blockDim.x) row[c] = 0.0f;
+  }
+}
+
+template <int PF>
+__global__ void __launch_bounds__(kWalkNT) terrain_walk_kernel(
+    const float *__restrict__ ground, const float *__restrict__ ceiling, int S, int rows,
+    int cols, float *__restrict__ enc_out, EncLayout L, uint32_t *__restrict__ bits_out,
+    int64_t words) {
+  const int64_t cells = (int64_t)rows * cols;
+  const int64_t cell = (int64_t)blockIdx.x * kWalkNT + threadIdx.x;  // warps = aligned 32-cell words
+  const bool live = cell < cells;
+  const int i = live ? (int)(cell / cols) : 0;
+  const int j = live ? (int)(cell - (int64_t)i * cols) : 0;
+  const bool hl = live && j > 0, hr = live && j + 1 < cols, hu = live && i > 0,
+             hd = live && i + 1 < rows;
+  const float nanf_ = bits_f32(kNaNBits);
+  const float cb32 = (float)c_K.c_barrier;
+
+  // prefetch ring: the 5-point cross and the ceiling of the next PF slices
+  float pe[PF], pl[PF], pr[PF], pu[PF], pd[PF], pc[PF];
+  auto fetch = [&](int k, int s) {
+    const float *gk = ground + (int64_t)k * cells;
+    pe[s] = live ? __ldg(gk + cell) : nanf_;
+    pl[s] = hl ? __ldg(gk + cell - 1) : nanf_;
+    pr[s] = hr ? __ldg(gk + cell + 1) : nanf_;
+    pu[s] = hu ? __ldg(gk + cell - cols) : nanf_;
+    pd[s] = hd ? __ldg(gk + cell + cols) : nanf_;
+    pc[s] = live ? __ldg(ceiling + (int64_t)k * cells + cell) : nanf_;
+  };
+#pragma unroll
+  for (int s = 0; s < PF; ++s)
+    if (s < S) fetch(s, s);
+
+  uint32_t xe = 0, xl = 0, xr = 0, xu = 0, xd = 0, xc = 0;  // previous slice's input bits
+  float tenc = nanf_;  // terrain part: NaN = no ground, sign bit = foothold branch
+  bool gentle = false;
+  float enc = 0.0f;
+  for (int k = 0; k < S; ++k) {
+    const int s = k % PF;
+    float e, l, r, u, d, c;
+#pragma unroll
+    for (int q = 0; q < PF; ++q)
+      if (q == s) {
+        e = pe[q]; l = pl[q]; r = pr[q]; u = pu[q]; d = pd[q]; c = pc[q];
+      }
+    if (k + PF < S) {
+#pragma unroll
+      for (int q = 0; q < PF; ++q)
+        if (q == s) fetch(k + PF, q);
+    }
+    const bool xch = k == 0 || f32_bits(e) != xe || f32_bits(l) != xl || f32_bits(r) != xr ||
+                     f32_bits(u) != xu || f32_bits(d) != xd;
+    if (xch && live) {
+      const FastCell t = fast_terrain(Cross{e, l, r, u, d}, c_K);
+      gentle = t.gentle;
+      if (!t.valid) {
+        tenc = nanf_;
+      } else if (t.isolated || t.m_xy > c_K.theta_b) {
+        tenc = cb32;
+      } else if (t.gentle) {
+        tenc = gentle_cost32(t.gx, t.gy, t.s, c_K);
+      } else {
+        const double q = div_const(t.m_xy, c_K.theta_b, c_K.inv_theta_b);
+        tenc = bits_f32(f32_bits((float)(c_K.alpha_b * (q * q))) | 0x80000000u);
+      }
+    }
+    if ((xch || f32_bits(c) != xc) && live) {
+      if (!finite32(tenc)) {
+        enc = cb32;  // no ground: barrier (fuse_costs :169)
+      } else {
+        const uint32_t tb = f32_bits(tenc);
+        enc = fuse_value(interval_value(e, c, c_K), bits_f32(tb & 0x7FFFFFFFu), c_K);
+        if (tb & 0x80000000u) enc = bits_f32(f32_bits(enc) | 0x80000000u);
+      }
+    }
+    xe = f32_bits(e); xl = f32_bits(l); xr = f32_bits(r); xu = f32_bits(u); xd = f32_bits(d);
+    xc = f32_bits(c);
+    if (live) enc_out[L.at(k, i, j)] = enc;
+    const unsigned b = __ballot_sync(0xFFFFFFFFu, live && gentle);
+    if ((threadIdx.x & 31) == 0 && (cell >> 5) < words) bits_out[(int64_t)k * words + (cell >> 5)] = b;
+  }
+}
+
+template <int R, int PR, int TH, int TW>
+struct SplitGeom {
+  static constexpr int CH = TH + 2 * R, CW = TW + 2 * R;
+  static constexpr int GH = CH + 2 * PR, GW = CW + 2 * PR;
+  static constexpr int GWW = (GW + 31) / 32 + 1;
+  static constexpr int O_CI = 0;
+  static constexpr int O_BITS = O_CI + CH * CW * 4;
+  static constexpr int O_LIST = O_BITS + GH * GWW * 4;
+  static constexpr int SMEM = O_LIST + ((CH * CW * 2 + 15) / 16) * 16;
+};
+
+template <int R, int PR, int TH, int TW, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) resolve_inflate_kernel(
+    const float *__restrict__ enc, EncLayout L, const uint32_t *__restrict__ bits_in, int rows,
+    int cols, int64_t words, float *__restrict__ cost) {
+  using G = SplitGeom<R, PR, TH, TW>;
+  extern __shared__ __align__(16) unsigned char smem[];
+  float *cinit = reinterpret_cast<float *>(smem + G::O_CI);
+  uint32_t *bits = reinterpret_cast<uint32_t *>(smem + G::O_BITS);
+  uint16_t *flist = reinterpret_cast<uint16_t *>(smem + G::O_LIST);
+  __shared__ int n_flagged;
+  const int tid = threadIdx.x;
+  const int64_t cells = (int64_t)rows * cols;
+  const int k = blockIdx.z;
+  const int i0 = blockIdx.y * TH, j0 = blockIdx.x * TW;
+  const uint32_t *bk = bits_in + (int64_t)k * words;
+  if (tid == 0) n_flagged = 0;
+  __syncthreads();
+
+  // encoded c_init of the tile + R halo from the zero-padded layout (no bounds
+  // tests; float4 when the padding keeps rows aligned); foothold-branch cells
+  // go to a list
+  const float *ek = enc + L.at(k, i0 - R, j0 - R);
+  auto note = [&](int idx, float v) {
+    const bool flagged = (f32_bits(v) & 0x80000000u) != 0;
+    const unsigned act = __activemask();
+    const unsigned fm = __ballot_sync(act, flagged);
+    if (fm) {
+      const int lane = tid & 31, leader = __ffs(fm) - 1;
+      int base = 0;
+      if (lane == leader) base = atomicAdd(&n_flagged, __popc(fm));
+      base = __shfl_sync(act, base, leader);
+      if (flagged) flist[base + __popc(fm & ((1u << lane) - 1u))] = (uint16_t)idx;
+    }
+  };
+  if constexpr (G::CW % 4 == 0 && R % 4 == 0) {
+    constexpr int CW4 = G::CW / 4;
+    for (int q = tid; q < G::CH * CW4; q += NT) {
+      const int y = q / CW4, x4 = q - y * CW4;
+      const float4 v = __ldg(reinterpret_cast<const float4 *>(ek + (int64_t)y * L.pitch) + x4);
+      const int idx = y * G::CW + 4 * x4;
+      reinterpret_cast<float4 *>(cinit)[q] = v;
+      if ((f32_bits(v.x) | f32_bits(v.y) | f32_bits(v.z) | f32_bits(v.w)) & 0x80000000u) {
+        if (f32_bits(v.x) & 0x80000000u) note(idx, v.x);
+        if (f32_bits(v.y) & 0x80000000u) note(idx + 1, v.y);
+        if (f32_bits(v.z) & 0x80000000u) note(idx + 2, v.z);
+        if (f32_bits(v.w) & 0x80000000u) note(idx + 3, v.w);
+      }
+    }
+  } else {
+    for (int idx = tid; idx < G::CH * G::CW; idx += NT) {
+      const int y = idx / G::CW, x = idx - y * G::CW;
+      const float v = __ldg(ek + (int64_t)y * L.pitch + x);
+      cinit[idx] = v;
+      if (f32_bits(v) & 0x80000000u) note(idx, v);
+    }
+  }
+  // gentle bits of the window region (rows i0-R-r .., cols j0-R-r ..), cut
+  // out of the row-major bitmap; columns outside the map read as 0
+  for (int idx = tid; idx < G::GH * G::GWW; idx += NT) {
+    const int y = idx / G::GWW, w = idx - y * G::GWW;
+    const int gi = i0 - R - PR + y;
+    const int gj = j0 - R - PR + 32 * w;  // column of bit 0 of this word
+    uint32_t word = 0;
+    if (gi >= 0 && gi < rows && gj < cols && gj + 32 > 0) {
+      const int64_t bit = (int64_t)gi * cols + gj;  // may be < row start; masked below
+      const int64_t wi = bit >> 5;
+      const int sh = (int)(bit & 31);
+      const uint32_t lo = (wi >= 0 && wi < words) ? __ldg(bk + wi) : 0u;
+      const uint32_t hi = (wi + 1 >= 0 && wi + 1 < words) ? __ldg(bk + wi + 1) : 0u;
+      word = (uint32_t)((((uint64_t)hi << 32) | lo) >> sh);
+      const int first = gj < 0 ? -gj : 0;                // bits left of column 0
+      const int last = cols - gj < 32 ? cols - gj : 32;  // bits up to the last column
+      const uint32_t mhi = last >= 32 ? 0xFFFFFFFFu : ((1u << last) - 1u);
+      const uint32_t mlo = first >= 32 ? 0u : (0xFFFFFFFFu << first);
+      word &= mhi & mlo;
+    }
+    if (32 * w >= G::GW) word = 0;
+    else if (G::GW - 32 * w < 32) word &= (1u << (G::GW - 32 * w)) - 1u;
+    bits[idx] = word;
+  }
+  __syncthreads();
+
+  constexpr int SIDE = 2 * PR + 1;
+  constexpr uint32_t WMASK = (1u << SIDE) - 1u;
+  const int nf = n_flagged;
+  for (int t = tid; t < nf; t += NT) {
+    const int idx = flist[t];
+    const int y = idx / G::CW, x = idx - y * G::CW;
+    const int w = x >> 5, sh = x & 31;
+    int cnt = 0;
+#pragma unroll
+    for (int d = 0; d < SIDE; ++d) {
+      const uint32_t *rw = bits + (y + d) * G::GWW + w;
+      const uint64_t v = (uint64_t)rw[0] | ((uint64_t)rw[1] << 32);
+      cnt += __popc((uint32_t)(v >> sh) & WMASK);
+    }
+    cinit[idx] = cinit_resolve(cinit[idx], cnt, c_K);
+  }
+  __syncthreads();
+
+  float *out = cost + (int64_t)k * cells;
+  if constexpr (R <= 4) {
+    constexpr int STRIPS = NT / TW;
+    constexpr int V = TH / STRIPS;
+    const int x = tid % TW, s = tid / TW;
+    inflate_sym_strip<R, V>(cinit, G::CW, x, s * V, out, cols, i0 + s * V, j0 + x, rows, cols);
+  }
+}

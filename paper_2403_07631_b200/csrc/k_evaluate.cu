@@ -338,6 +338,7 @@ __global__ void __launch_bounds__(NT, MINB) eval_fast_kernel(const float *__rest
 }
 
 #include "k_eval_incr.cuh"
+#include "k_eval_split.cuh"
 
 // ---------------------------------------------------------- generic kernel
 struct TileGeom {
@@ -571,20 +572,76 @@ int launch_incr_t(pct_ctx *ctx, const float *ground, const float *ceiling, int S
   return check_launch(ctx, "eval_incr_kernel");
 }
 
-// Kernel choice for symmetric kernels with compiled geometry: the
-// slice-incremental kernel when there are enough slices to amortise each
-// run's full first slice and enough 32x32 tiles to fill the GPU (measured:
-// cfg1 297 us vs 386 us; small maps are faster with the per-slice kernel).
-// PCT_EVAL_KERNEL=fast|incr, PCT_EVAL_TILE=32|64 and PCT_EVAL_RUN override.
+// two-kernel evaluation (k_eval_split.cuh): per-cell slice walk, then tiled
+// foothold resolution + inflation; intermediates in the context scratch
+template <int R, int PR>
+int launch_split(pct_ctx *ctx, const float *ground, const float *ceiling, int S, int rows,
+                 int cols, float *cost) {
+  constexpr int TH = 64, TW = 64;
+  const int64_t cells = (int64_t)rows * cols;
+  const int64_t words = (cells + 31) / 32 + 1;
+  EncLayout L;
+  L.padr = R;
+  L.padc = R;
+  L.prows = (rows + TH - 1) / TH * TH + 2 * R;
+  L.pitch = ((int64_t)((cols + TW - 1) / TW * TW + 2 * R) + 3) / 4 * 4;
+  L.sstride = (int64_t)L.prows * L.pitch;
+  const size_t enc_bytes = (size_t)S * L.sstride * 4;
+  if (int rc = ensure_scratch(ctx, (size_t)S * words * 4)) return rc;
+  uint32_t *bits = static_cast<uint32_t *>(ctx->scratch);
+  if (ctx->enc_bytes < enc_bytes) {
+    if (ctx->enc) {
+      cudaStreamSynchronize(ctx->stream);
+      cudaFree(ctx->enc);
+      ctx->enc = nullptr;
+      ctx->enc_bytes = 0;
+    }
+    PCT_CUDA(ctx, cudaMalloc(&ctx->enc, enc_bytes));
+    ctx->enc_bytes = enc_bytes;
+    ctx->enc_tag[0] = -1;
+  }
+  float *enc = static_cast<float *>(ctx->enc);
+  const int64_t tag[4] = {S, rows, cols, R};
+  if (!std::equal(tag, tag + 4, ctx->enc_tag)) {  // new layout: clear its padding once
+    zero_pads_kernel<<<dim3((unsigned)L.prows, S), 128, 0, ctx->stream>>>(enc, L, rows, cols);
+    if (int rc = check_launch(ctx, "zero_pads_kernel")) return rc;
+    std::copy(tag, tag + 4, ctx->enc_tag);
+  }
+  const unsigned g1 = (unsigned)((cells + kWalkNT - 1) / kWalkNT);
+  const char *pf = getenv("PCT_WALK_PF");
+  const int npf = pf ? atoi(pf) : 2;
+  if (npf == 1)
+    terrain_walk_kernel<1><<<g1, kWalkNT, 0, ctx->stream>>>(ground, ceiling, S, rows, cols, enc,
+                                                           L, bits, words);
+  else if (npf == 4)
+    terrain_walk_kernel<4><<<g1, kWalkNT, 0, ctx->stream>>>(ground, ceiling, S, rows, cols, enc,
+                                                           L, bits, words);
+  else
+    terrain_walk_kernel<2><<<g1, kWalkNT, 0, ctx->stream>>>(ground, ceiling, S, rows, cols, enc,
+                                                           L, bits, words);
+  if (int rc = check_launch(ctx, "terrain_walk_kernel")) return rc;
+  auto kern = resolve_inflate_kernel<R, PR, TH, TW, kNT, 3>;
+  constexpr int smem = SplitGeom<R, PR, TH, TW>::SMEM;
+  PCT_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  dim3 grid((cols + TW - 1) / TW, (rows + TH - 1) / TH, S);
+  kern<<<grid, kNT, smem, ctx->stream>>>(enc, L, bits, rows, cols, words, cost);
+  return check_launch(ctx, "resolve_inflate_kernel");
+}
+
+// Kernel choice for symmetric kernels with compiled geometry: R <= 4 uses
+// the two-kernel split by default; PCT_EVAL_KERNEL=fast selects the fused
+// per-slice kernel and =incr the slice-incremental CTA kernel (kept as
+// measured alternatives; PCT_EVAL_TILE / PCT_EVAL_RUN tune
+// it).  R = 8 uses the fused per-slice kernel with split inflation roles.
 template <int R, int PR>
 int launch_fast(pct_ctx *ctx, const float *ground, const float *ceiling, int S, int rows,
                 int cols, float *cost) {
-  bool incr = false;
   if constexpr (R <= 4) {
-    const int64_t tiles32 = (int64_t)((rows + 31) / 32) * ((cols + 31) / 32);
-    incr = S >= 8 && tiles32 >= 2LL * ctx->num_sms;
-    if (const char *m = getenv("PCT_EVAL_KERNEL")) incr = m[0] == 'i' && S > 1;
-    if (incr) {
+    // default: the two-kernel split (cfg1: 258 us vs 296 incremental vs 386
+    // per-slice; cfg0: 43 vs 52 us)
+    const char *m = getenv("PCT_EVAL_KERNEL");
+    if (!m || m[0] == 's') return launch_split<R, PR>(ctx, ground, ceiling, S, rows, cols, cost);
+    if (m[0] == 'i' && S > 1) {
       const char *t = getenv("PCT_EVAL_TILE");
       if (t && atoi(t) == 64)
         return launch_incr_t<R, PR, 64, 64, 256, 2>(ctx, ground, ceiling, S, rows, cols, cost);

@@ -26,6 +26,11 @@ struct pct_ctx {
   // small device/pinned buffers for reductions and flags
   void *dsmall = nullptr;   // 64 KiB device
   void *hsmall = nullptr;   // 64 KiB pinned host
+  // zero-padded encoded c_init stacks of the split evaluation; the padding
+  // is cleared only when the layout changes (the interior is rewritten)
+  void *enc = nullptr;
+  size_t enc_bytes = 0;
+  int64_t enc_tag[4] = {-1, -1, -1, -1};  // S, rows, cols, R of the cleared layout
 };
 
 struct pct_tomo {
