@@ -186,6 +186,10 @@ int pct_tomo_run(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, int xyz_on
                  double d_s, double r_g, int64_t max_grid_side, const pct_trav_params *p,
                  const float *kernel_w, int32_t kside, double eps_e, double c_barrier,
                  pct_tomo **out, int32_t *keep_host, int32_t *n_keep);
+/* Stage timing of pct_tomo_run with CUDA events on the context stream:
+   ms[0] = bounds + frame + build, ms[1] = evaluate, ms[2] = simplify. */
+int pct_set_timing(pct_ctx *ctx, int on);
+int pct_last_stage_ms(pct_ctx *ctx, float ms[3]);
 int pct_tomo_frame(const pct_tomo *t, pct_frame *fr, double *heights, int32_t heights_cap);
 /* device pointer of a layer stack (NULL if absent), e.g. for zero-copy consumers */
 const float *pct_tomo_layer(const pct_tomo *t, int layer);

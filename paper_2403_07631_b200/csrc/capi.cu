@@ -149,6 +149,8 @@ int pct_ctx_destroy(pct_ctx *ctx) {
   if (ctx->staging) cudaFree(ctx->staging);
   if (ctx->dsmall) cudaFree(ctx->dsmall);
   if (ctx->enc) cudaFree(ctx->enc);
+  for (auto e : ctx->ev)
+    if (e) cudaEventDestroy(e);
   if (ctx->hsmall) cudaFreeHost(ctx->hsmall);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
@@ -461,14 +463,37 @@ int pct_tomo_run(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, int xyz_on
                  pct_tomo **out, int32_t *keep_host, int32_t *n_keep) {
   if (!out || !keep_host || !n_keep) return fail(ctx, PCT_E_INVALID, "bad arguments to pct_tomo_run");
   pct_tomo *t = nullptr;
+  if (ctx->timing) cudaEventRecord(ctx->ev[0], ctx->stream);
   int rc = pct_tomo_build(ctx, xyz, n, dtype, xyz_on_host, d_s, r_g, max_grid_side, &t);
   if (rc) return rc;
-  if ((rc = pct_tomo_evaluate(ctx, t, p, kernel_w, kside)) ||
-      (rc = pct_tomo_simplify(ctx, t, eps_e, c_barrier, keep_host, n_keep))) {
+  if (ctx->timing) cudaEventRecord(ctx->ev[1], ctx->stream);
+  if ((rc = pct_tomo_evaluate(ctx, t, p, kernel_w, kside))) {
     pct_tomo_free(ctx, t);
     return rc;
   }
+  if (ctx->timing) cudaEventRecord(ctx->ev[2], ctx->stream);
+  if ((rc = pct_tomo_simplify(ctx, t, eps_e, c_barrier, keep_host, n_keep))) {
+    pct_tomo_free(ctx, t);
+    return rc;
+  }
+  if (ctx->timing) cudaEventRecord(ctx->ev[3], ctx->stream);
   *out = t;
+  return PCT_OK;
+}
+
+int pct_set_timing(pct_ctx *ctx, int on) {
+  CTX_GUARD(ctx);
+  if (on && !ctx->ev[0])
+    for (auto &e : ctx->ev) PCT_CUDA(ctx, cudaEventCreate(&e));
+  ctx->timing = on != 0;
+  return PCT_OK;
+}
+
+int pct_last_stage_ms(pct_ctx *ctx, float ms[3]) {
+  CTX_GUARD(ctx);
+  if (!ctx->timing || !ms) return fail(ctx, PCT_E_INVALID, "timing is off");
+  PCT_CUDA(ctx, cudaEventSynchronize(ctx->ev[3]));
+  for (int s = 0; s < 3; ++s) PCT_CUDA(ctx, cudaEventElapsedTime(ms + s, ctx->ev[s], ctx->ev[s + 1]));
   return PCT_OK;
 }
 

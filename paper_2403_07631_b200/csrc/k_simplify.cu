@@ -100,12 +100,20 @@ __global__ void __launch_bounds__(kWinNT) window_kernel(SimpArgs A,
           c_up = pc[u];
         }
       unsigned long long m = 0;
-      if (live && finite32(e_cur) && c_cur < A.c_barrier32 &&
+      // bits this block has already established for slice k need no work
+      // (a stale read only costs a redundant test)
+      const int depth = k < kWin ? k : kWin;
+      const unsigned long long want =
+          (1ull << kBit) | ((depth >= 64 ? ~0ull : (1ull << depth) - 1ull));
+      const unsigned long long known = *((volatile unsigned long long *)&btab[k]);
+      if ((known & want) != want && live && finite32(e_cur) && c_cur < A.c_barrier32 &&
           (k + 1 >= A.S || not_covered(e_cur, c_cur, e_up, c_up, A.eps_e, false))) {
         m = 1ull << kBit;
-        const int depth = k < kWin ? k : kWin;
         const double ed = (double)e_cur;
-        for (int j = 0; j < depth; ++j) {  // a = k-1-j
+        unsigned todo = (unsigned)(~known & want);  // bits 0..15 still unknown
+        while (todo) {
+          const int j = __ffs(todo) - 1;  // a = k-1-j
+          todo &= todo - 1;
           const int slot = (k - 1 - j) & (kWin - 1);
           if (not_covered_below(ed, c_cur, ring_e[slot][threadIdx.x], ring_c[slot][threadIdx.x],
                                 A.eps_e))
