@@ -248,3 +248,171 @@ __global__ void __launch_bounds__(NT, MINB) resolve_inflate_kernel(
     inflate_sym_strip<R, V>(cinit, G::CW, x, s * V, out, cols, i0 + s * V, j0 + x, rows, cols);
   }
 }
+
+// ---------------------------------------------------------------------------
+// I, TMA version: persistent CTAs; the encoded c_init tile + halo of the next
+// work item is fetched by the Tensor Memory Accelerator
+// (cp.async.bulk.tensor.3d, completion on an mbarrier) into the second of
+// two shared-memory buffers while the current item is resolved and inflated.
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra.uni WAIT%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, uint64_t *bar, int x,
+                                            int y, int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int R, int PR, int TH, int TW>
+struct TmaGeom {
+  static constexpr int CH = TH + 2 * R, CW = TW + 2 * R;
+  static constexpr int GH = CH + 2 * PR, GW = CW + 2 * PR;
+  static constexpr int GWW = (GW + 31) / 32 + 1;
+  static constexpr int BUF = ((CH * CW * 4) + 127) / 128 * 128;  // one TMA box, 128 B aligned
+  static constexpr int O_BUF = 0;                                 // 2 buffers
+  static constexpr int O_BITS = 2 * BUF;
+  static constexpr int O_LIST = O_BITS + GH * GWW * 4;
+  static constexpr int SMEM = O_LIST + ((CH * CW * 2 + 15) / 16) * 16 + 128;
+};
+
+template <int R, int PR, int TH, int TW, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) resolve_inflate_tma_kernel(
+    const __grid_constant__ CUtensorMap enc_map, const uint32_t *__restrict__ bits_in, int rows,
+    int cols, int S, int64_t words, float *__restrict__ cost) {
+  using G = TmaGeom<R, PR, TH, TW>;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  unsigned char *smem =
+      reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  uint32_t *bits = reinterpret_cast<uint32_t *>(smem + G::O_BITS);
+  uint16_t *flist = reinterpret_cast<uint16_t *>(smem + G::O_LIST);
+  __shared__ __align__(8) uint64_t bar[2];
+  __shared__ int n_flagged;
+  const int tid = threadIdx.x;
+  const int tx = (cols + TW - 1) / TW, ty = (rows + TH - 1) / TH;
+  const int tiles = tx * ty;
+  const int n_items = tiles * S;
+  const int64_t cells = (int64_t)rows * cols;
+  constexpr uint32_t BOX_BYTES = G::CH * G::CW * 4;
+  auto coords = [&](int item, int &i0, int &j0, int &k) {
+    k = item / tiles;
+    const int t = item - k * tiles;
+    i0 = (t / tx) * TH;
+    j0 = (t % tx) * TW;
+  };
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  int item = blockIdx.x;
+  if (tid == 0 && item < n_items) {
+    int i0, j0, k;
+    coords(item, i0, j0, k);
+    mbar_expect_tx(&bar[0], BOX_BYTES);
+    tma_load_3d(smem + G::O_BUF, &enc_map, &bar[0], j0, i0, k);  // padded coords
+  }
+  uint32_t phase[2] = {0u, 0u};
+  for (int it = 0; item < n_items; ++it, item += gridDim.x) {
+    const int cur = it & 1;
+    float *cinit = reinterpret_cast<float *>(smem + G::O_BUF + cur * G::BUF);
+    int i0, j0, k;
+    coords(item, i0, j0, k);
+    // prefetch the next item into the other buffer (freed by the barrier that
+    // ended the previous iteration)
+    const int nxt = item + gridDim.x;
+    if (tid == 0 && nxt < n_items) {
+      int ni0, nj0, nk;
+      coords(nxt, ni0, nj0, nk);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(&bar[cur ^ 1], BOX_BYTES);
+      tma_load_3d(smem + G::O_BUF + (cur ^ 1) * G::BUF, &enc_map, &bar[cur ^ 1], nj0, ni0, nk);
+    }
+    if (tid == 0) n_flagged = 0;
+    // gentle bits of the window region (global bitmap -> smem), overlapping the TMA
+    const uint32_t *bk = bits_in + (int64_t)k * words;
+    for (int idx = tid; idx < G::GH * G::GWW; idx += NT) {
+      const int y = idx / G::GWW, w = idx - y * G::GWW;
+      const int gi = i0 - R - PR + y;
+      const int gj = j0 - R - PR + 32 * w;
+      uint32_t word = 0;
+      if (gi >= 0 && gi < rows && gj < cols && gj + 32 > 0) {
+        const int64_t bit = (int64_t)gi * cols + gj;
+        const int64_t wi = bit >> 5;
+        const int sh = (int)(bit & 31);
+        const uint32_t lo = (wi >= 0 && wi < words) ? __ldg(bk + wi) : 0u;
+        const uint32_t hi = (wi + 1 >= 0 && wi + 1 < words) ? __ldg(bk + wi + 1) : 0u;
+        word = (uint32_t)((((uint64_t)hi << 32) | lo) >> sh);
+        const int first = gj < 0 ? -gj : 0;
+        const int last = cols - gj < 32 ? cols - gj : 32;
+        const uint32_t mhi = last >= 32 ? 0xFFFFFFFFu : ((1u << last) - 1u);
+        const uint32_t mlo = first >= 32 ? 0u : (0xFFFFFFFFu << first);
+        word &= mhi & mlo;
+      }
+      if (32 * w >= G::GW) word = 0;
+      else if (G::GW - 32 * w < 32) word &= (1u << (G::GW - 32 * w)) - 1u;
+      bits[idx] = word;
+    }
+    mbar_wait(&bar[cur], phase[cur]);
+    phase[cur] ^= 1u;
+    __syncthreads();  // bits + n_flagged visible, TMA data landed
+    // foothold-branch cells of the tile + halo
+    for (int idx = tid; idx < G::CH * G::CW; idx += NT) {
+      const bool flagged = (f32_bits(cinit[idx]) & 0x80000000u) != 0;
+      const unsigned act = __activemask();
+      const unsigned fm = __ballot_sync(act, flagged);
+      if (fm) {
+        const int lane = tid & 31, leader = __ffs(fm) - 1;
+        int base = 0;
+        if (lane == leader) base = atomicAdd(&n_flagged, __popc(fm));
+        base = __shfl_sync(act, base, leader);
+        if (flagged) flist[base + __popc(fm & ((1u << lane) - 1u))] = (uint16_t)idx;
+      }
+    }
+    __syncthreads();
+    constexpr int SIDE = 2 * PR + 1;
+    constexpr uint32_t WMASK = (1u << SIDE) - 1u;
+    const int nf = n_flagged;
+    for (int t = tid; t < nf; t += NT) {
+      const int idx = flist[t];
+      const int y = idx / G::CW, x = idx - y * G::CW;
+      const int w = x >> 5, sh = x & 31;
+      int cnt = 0;
+#pragma unroll
+      for (int d = 0; d < SIDE; ++d) {
+        const uint32_t *rw = bits + (y + d) * G::GWW + w;
+        const uint64_t v = (uint64_t)rw[0] | ((uint64_t)rw[1] << 32);
+        cnt += __popc((uint32_t)(v >> sh) & WMASK);
+      }
+      cinit[idx] = cinit_resolve(cinit[idx], cnt, c_K);
+    }
+    __syncthreads();
+    float *out = cost + (int64_t)k * cells;
+    if constexpr (R <= 4) {
+      constexpr int STRIPS = NT / TW;
+      constexpr int V = TH / STRIPS;
+      const int x = tid % TW, s = tid / TW;
+      inflate_sym_strip<R, V>(cinit, G::CW, x, s * V, out, cols, i0 + s * V, j0 + x, rows, cols);
+    }
+    __syncthreads();  // buffer `cur` and the bit rows are free again
+  }
+}

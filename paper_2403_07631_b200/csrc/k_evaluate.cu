@@ -21,6 +21,8 @@
 // eval_fast_kernel has the whole geometry as template constants (the common
 // parameter sets); eval_generic_kernel takes it at run time and also serves
 // the per-operation entry points.
+#include <cuda.h>  // CUtensorMap (the encoder is fetched with cudaGetDriverEntryPoint)
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -620,6 +622,40 @@ int launch_split(pct_ctx *ctx, const float *ground, const float *ceiling, int S,
     terrain_walk_kernel<2><<<g1, kWalkNT, 0, ctx->stream>>>(ground, ceiling, S, rows, cols, enc,
                                                            L, bits, words);
   if (int rc = check_launch(ctx, "terrain_walk_kernel")) return rc;
+  const char *tma = getenv("PCT_TMA");
+  if (!(tma && tma[0] == '0') && R % 4 == 0) {
+    // persistent TMA-pipelined resolve + inflate: a 3-D tensor map over the
+    // padded stacks, box = one c_init tile + halo
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+      void *fn = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      PCT_CUDA(ctx, cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+      if (!fn || q != cudaDriverEntryPointSuccess)
+        return fail(ctx, PCT_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+      encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    using TG = TmaGeom<R, PR, TH, TW>;
+    CUtensorMap map;
+    const cuuint64_t dims[3] = {(cuuint64_t)L.pitch, (cuuint64_t)L.prows, (cuuint64_t)S};
+    const cuuint64_t strides[2] = {(cuuint64_t)L.pitch * 4, (cuuint64_t)L.sstride * 4};
+    const cuuint32_t box[3] = {(cuuint32_t)TG::CW, (cuuint32_t)TG::CH, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    if (encode(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, enc, dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return fail(ctx, PCT_E_CUDA, "cuTensorMapEncodeTiled failed");
+    auto kt = resolve_inflate_tma_kernel<R, PR, TH, TW, kNT, 3>;
+    constexpr int tsmem = TG::SMEM;
+    PCT_CUDA(ctx, cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, tsmem));
+    int per_sm = 0;
+    PCT_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kt, kNT, tsmem));
+    const int64_t items = (int64_t)((cols + TW - 1) / TW) * ((rows + TH - 1) / TH) * S;
+    const unsigned grid = (unsigned)std::max<int64_t>(
+        1, std::min<int64_t>(items, (int64_t)std::max(1, per_sm) * ctx->num_sms));
+    kt<<<grid, kNT, tsmem, ctx->stream>>>(map, bits, rows, cols, S, words, cost);
+    return check_launch(ctx, "resolve_inflate_tma_kernel");
+  }
   auto kern = resolve_inflate_kernel<R, PR, TH, TW, kNT, 3>;
   constexpr int smem = SplitGeom<R, PR, TH, TW>::SMEM;
   PCT_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
