@@ -291,7 +291,8 @@ struct TmaGeom {
   static constexpr int O_BUF = 0;                                 // 2 buffers
   static constexpr int O_BITS = 2 * BUF;
   static constexpr int O_LIST = O_BITS + GH * GWW * 4;
-  static constexpr int SMEM = O_LIST + ((CH * CW * 2 + 15) / 16) * 16 + 128;
+  static constexpr int O_BAR = O_LIST + ((CH * CW * 2 + 15) / 16) * 16;  // 2 mbarriers + counter
+  static constexpr int SMEM = O_BAR + 32;
 };
 
 template <int R, int PR, int TH, int TW, int NT, int MINB>
@@ -299,14 +300,16 @@ __global__ void __launch_bounds__(NT, MINB) resolve_inflate_tma_kernel(
     const __grid_constant__ CUtensorMap enc_map, const uint32_t *__restrict__ bits_in, int rows,
     int cols, int S, int64_t words, float *__restrict__ cost) {
   using G = TmaGeom<R, PR, TH, TW>;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  unsigned char *smem =
-      reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  // everything lives in the dynamic region (no static __shared__), whose base
+  // is 128-byte aligned as the TMA destination requires; constant offsets
+  // keep the compiler on the shared address space (LDS/STS, not generic LD)
+  extern __shared__ __align__(128) unsigned char smem[];
   uint32_t *bits = reinterpret_cast<uint32_t *>(smem + G::O_BITS);
   uint16_t *flist = reinterpret_cast<uint16_t *>(smem + G::O_LIST);
-  __shared__ __align__(8) uint64_t bar[2];
-  __shared__ int n_flagged;
+  uint64_t *bar = reinterpret_cast<uint64_t *>(smem + G::O_BAR);
+  int &n_flagged = *reinterpret_cast<int *>(smem + G::O_BAR + 16);
   const int tid = threadIdx.x;
+  if (tid == 0 && (smem_u32(smem) & 127u) != 0u) __trap();  // TMA box alignment
   const int tx = (cols + TW - 1) / TW, ty = (rows + TH - 1) / TH;
   const int tiles = tx * ty;
   const int n_items = tiles * S;
