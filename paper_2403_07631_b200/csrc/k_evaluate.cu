@@ -43,6 +43,58 @@ __constant__ EvalConsts c_K;
 // ------------------------------------------------ stage E, symmetric, R<=4
 // Thread = one output column x of a strip of V rows; register ring of the
 // horizontal pair maxima of 2R+1 consecutive c_init rows.
+// max of n values by a balanced tree of 3-input maxima (FMNMX3); exact and
+// order-independent for non-NaN inputs
+template <int N>
+__device__ __forceinline__ float max_tree(const float (&v)[N]) {
+  if constexpr (N == 1) {
+    return v[0];
+  } else if constexpr (N == 2) {
+    return fmaxf(v[0], v[1]);
+  } else {
+    constexpr int M = (N + 2) / 3;
+    float u[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+      const int a = 3 * i;
+      u[i] = a + 2 < N ? fmaxf(fmaxf(v[a], v[a + 1]), v[a + 2])
+                       : (a + 1 < N ? fmaxf(v[a], v[a + 1]) : v[a]);
+    }
+    return max_tree<M>(u);
+  }
+}
+
+// The weighted max for output (c) of a strip from the pair-maxima ring: one
+// product per tap group (a, b), a >= b.  Groups with weight <= 0 give a
+// product <= 0, which cannot exceed the accumulator's start value 0 (the
+// reference skips them; all c_init >= 0), so no group needs a branch and the
+// whole reduction is a compile-time tree.
+template <int R, int ROWS>
+__device__ __forceinline__ float weighted_max(const float (&P)[ROWS][R + 1], int c) {
+  constexpr int NP = (R + 1) * (R + 2) / 2 + 1;
+  float v[NP];
+  int n = 0;
+#pragma unroll
+  for (int a = 0; a <= R; ++a) {
+#pragma unroll
+    for (int b = 0; b <= a; ++b) {
+      float m;
+      if (a == 0) {
+        m = P[c][0];
+      } else if (b == 0) {
+        m = fmaxf(fmaxf(P[c - a][0], P[c + a][0]), P[c][a]);
+      } else if (a == b) {
+        m = fmaxf(P[c - a][a], P[c + a][a]);
+      } else {
+        m = fmaxf(fmaxf(P[c - a][b], P[c + a][b]), fmaxf(P[c - b][a], P[c + b][a]));
+      }
+      v[n++] = c_wsym[a * 9 + b] * m;
+    }
+  }
+  v[n] = 0.0f;
+  return max_tree<NP>(v);
+}
+
 template <int R, int V>
 __device__ __forceinline__ void inflate_sym_strip(const float *__restrict__ cinit, int CW,
                                                   int x, int ys, float *__restrict__ out,
@@ -57,28 +109,7 @@ __device__ __forceinline__ void inflate_sym_strip(const float *__restrict__ cini
     for (int b = 1; b <= R; ++b) P[t][b] = fmaxf(rowp[R - b], rowp[R + b]);
     if (t >= 2 * R) {
       const int o = t - 2 * R;  // output row in strip; centre P row = o + R
-      const int c = o + R;
-      float acc = 0.0f;
-#pragma unroll
-      for (int a = 0; a <= R; ++a) {
-#pragma unroll
-        for (int b = 0; b <= a; ++b) {
-          const float w = c_wsym[a * 9 + b];
-          if (w > 0.0f) {
-            float m;
-            if (a == 0) {
-              m = P[c][0];
-            } else if (b == 0) {
-              m = fmaxf(fmaxf(P[c - a][0], P[c + a][0]), P[c][a]);
-            } else if (a == b) {
-              m = fmaxf(P[c - a][a], P[c + a][a]);
-            } else {
-              m = fmaxf(fmaxf(P[c - a][b], P[c + a][b]), fmaxf(P[c - b][a], P[c + b][a]));
-            }
-            acc = fmaxf(acc, w * m);
-          }
-        }
-      }
+      const float acc = weighted_max<R, V + 2 * R>(P, o + R);
       const int gi = orow0 + o;
       if (gi < rows && ocol < cols) out[(int64_t)gi * out_stride + ocol] = acc;
     }
