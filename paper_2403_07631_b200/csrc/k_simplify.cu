@@ -8,10 +8,10 @@
 // the exact sweep:
 //
 //  * window_kernel: one pass over every cell computes, for each slice k and
-//    each lower neighbour a in {none, k-1, ..., k-32}, whether any cell is
+//    each lower neighbour a in {none, k-1, ..., k-16}, whether any cell is
 //    unique for the triple (a, k, k+1) — every check of the first pass whose
-//    removal chain is < 32 long (the upper neighbour of pass 1 is always the
-//    original k+1).  Each thread owns a cell and keeps its last 32 slices'
+//    removal chain is <= 16 long (the upper neighbour of pass 1 is always the
+//    original k+1).  Each thread owns a cell and keeps its last 16 slices'
 //    (ground, cost) in a shared-memory ring; per k the block ORs a 64-bit mask.
 //  * triples_kernel: any() for an explicit batch of (below, k, above)
 //    triples — later passes and long chains; the host batches the remainder
@@ -52,82 +52,81 @@ __device__ __forceinline__ bool not_covered(float e, float cst, float enb, float
   return higher || (cst < cnb);
 }
 
-// lower-side test with the neighbour's elevation already widened (NaN = invalid)
-__device__ __forceinline__ bool not_covered_below(double e, float cst, double enb, float cnb,
-                                                  double eps) {
-  return isnan(enb) || (e - enb > eps) || (cst < cnb);
+// side tests with a bit-equality shortcut: equal elevations differ by 0,
+// which is not > eps_e unless eps_e < 0, so the float64 subtraction is only
+// evaluated for elevations that differ
+__device__ __forceinline__ bool higher_than(float hi, float lo, double eps) {
+  return (f32_bits(hi) != f32_bits(lo) || eps < 0.0) && ((double)hi - (double)lo > eps);
 }
 
 // Persistent blocks walk cells grid-stride; a thread owns one cell at a time
 // and walks its slices; warps OR their masks into a per-block table in
 // shared memory (no block barrier per slice), flushed once at the end.
+// Warps with no traversable, upper-uncovered cell at slice k skip the
+// lower-neighbour tests and the reductions.
 __global__ void __launch_bounds__(kWinNT) window_kernel(SimpArgs A,
                                                         unsigned long long *__restrict__ table) {
-  __shared__ double ring_e[kWin][kWinNT];
+  __shared__ float ring_e[kWin][kWinNT];
   __shared__ float ring_c[kWin][kWinNT];
   extern __shared__ unsigned long long btab[];  // [S]
   for (int k = threadIdx.x; k < A.S; k += kWinNT) btab[k] = 0ull;
   __syncthreads();
   const int64_t stride = (int64_t)gridDim.x * kWinNT;
   const int64_t span = (A.cells + kWinNT - 1) / kWinNT * kWinNT;  // whole warps iterate together
+  const float nanf_ = bits_f32(kNaNBits);
   for (int64_t cell = (int64_t)blockIdx.x * kWinNT + threadIdx.x; cell < span; cell += stride) {
     const bool live = cell < A.cells;
-    float e_cur = 0.f, c_cur = 0.f;
+    float e_cur = nanf_, c_cur = 0.f, e_up = nanf_, c_up = 0.f;
     if (live) {
       e_cur = __ldg(A.ground + cell);
       c_cur = __ldg(A.cost + cell);
+      if (A.S > 1) {
+        e_up = __ldg(A.ground + A.stride + cell);
+        c_up = __ldg(A.cost + A.stride + cell);
+      }
     }
-    // the (ground, cost) of the next slices are loaded 8 at a time so the
-    // dependent walk over k does not wait on one global load per step
-    constexpr int PF = 8;
-    float pe[PF], pc[PF];
     for (int k = 0; k < A.S; ++k) {
-      const int q = k % PF;
-      if (q == 0) {
-#pragma unroll
-        for (int u = 0; u < PF; ++u) {
-          const int kk = k + 1 + u;
-          const bool ok = live && kk < A.S;
-          pe[u] = ok ? __ldg(A.ground + (int64_t)kk * A.stride + cell) : bits_f32(kNaNBits);
-          pc[u] = ok ? __ldg(A.cost + (int64_t)kk * A.stride + cell) : 0.f;
-        }
+      // prefetch slice k+2 while slice k is tested
+      float e_nx = nanf_, c_nx = 0.f;
+      if (live && k + 2 < A.S) {
+        e_nx = __ldg(A.ground + (int64_t)(k + 2) * A.stride + cell);
+        c_nx = __ldg(A.cost + (int64_t)(k + 2) * A.stride + cell);
       }
-      float e_up = pe[0], c_up = pc[0];
-#pragma unroll
-      for (int u = 1; u < PF; ++u)
-        if (q == u) {
-          e_up = pe[u];
-          c_up = pc[u];
+      const bool up_ok = k + 1 >= A.S || !finite32(e_up) || higher_than(e_up, e_cur, A.eps_e) ||
+                         c_cur < c_up;
+      const bool cand = live && finite32(e_cur) && c_cur < A.c_barrier32 && up_ok;
+      if (__any_sync(0xffffffffu, cand)) {
+        unsigned long long m = 0;
+        const int depth = k < kWin ? k : kWin;
+        const unsigned long long want =
+            (1ull << kBit) | ((depth >= 64 ? ~0ull : (1ull << depth) - 1ull));
+        // bits this block has already established need no work (a stale
+        // read only costs a redundant test)
+        const unsigned long long known = *((volatile unsigned long long *)&btab[k]);
+        if (cand && (known & want) != want) {
+          m = 1ull << kBit;
+          unsigned todo = (unsigned)(~known & want);
+          while (todo) {
+            const int j = __ffs(todo) - 1;  // a = k-1-j
+            todo &= todo - 1;
+            const int slot = (k - 1 - j) & (kWin - 1);
+            const float ea = ring_e[slot][threadIdx.x];
+            if (!finite32(ea) || higher_than(e_cur, ea, A.eps_e) ||
+                c_cur < ring_c[slot][threadIdx.x])
+              m |= 1ull << j;
+          }
         }
-      unsigned long long m = 0;
-      // bits this block has already established for slice k need no work
-      // (a stale read only costs a redundant test)
-      const int depth = k < kWin ? k : kWin;
-      const unsigned long long want =
-          (1ull << kBit) | ((depth >= 64 ? ~0ull : (1ull << depth) - 1ull));
-      const unsigned long long known = *((volatile unsigned long long *)&btab[k]);
-      if ((known & want) != want && live && finite32(e_cur) && c_cur < A.c_barrier32 &&
-          (k + 1 >= A.S || not_covered(e_cur, c_cur, e_up, c_up, A.eps_e, false))) {
-        m = 1ull << kBit;
-        const double ed = (double)e_cur;
-        unsigned todo = (unsigned)(~known & want);  // bits 0..15 still unknown
-        while (todo) {
-          const int j = __ffs(todo) - 1;  // a = k-1-j
-          todo &= todo - 1;
-          const int slot = (k - 1 - j) & (kWin - 1);
-          if (not_covered_below(ed, c_cur, ring_e[slot][threadIdx.x], ring_c[slot][threadIdx.x],
-                                A.eps_e))
-            m |= 1ull << j;
-        }
+        const unsigned lo = __reduce_or_sync(0xffffffffu, (unsigned)m);
+        const unsigned hi = __reduce_or_sync(0xffffffffu, (unsigned)(m >> 32));
+        if ((threadIdx.x & 31) == 0 && (lo | hi))
+          atomicOr(&btab[k], ((unsigned long long)hi << 32) | lo);
       }
-      const unsigned lo = __reduce_or_sync(0xffffffffu, (unsigned)m);
-      const unsigned hi = __reduce_or_sync(0xffffffffu, (unsigned)(m >> 32));
-      if ((threadIdx.x & 31) == 0 && (lo | hi))
-        atomicOr(&btab[k], ((unsigned long long)hi << 32) | lo);
-      ring_e[k & (kWin - 1)][threadIdx.x] = (double)e_cur;  // NaN stays NaN; own column only
+      ring_e[k & (kWin - 1)][threadIdx.x] = e_cur;  // own column only
       ring_c[k & (kWin - 1)][threadIdx.x] = c_cur;
       e_cur = e_up;
       c_cur = c_up;
+      e_up = e_nx;
+      c_up = c_nx;
     }
   }
   __syncthreads();
