@@ -74,59 +74,65 @@ __global__ void __launch_bounds__(kWinNT) window_kernel(SimpArgs A,
   const int64_t stride = (int64_t)gridDim.x * kWinNT;
   const int64_t span = (A.cells + kWinNT - 1) / kWinNT * kWinNT;  // whole warps iterate together
   const float nanf_ = bits_f32(kNaNBits);
+  constexpr int KB = 4;  // slices per register block; the next block is loaded ahead
   for (int64_t cell = (int64_t)blockIdx.x * kWinNT + threadIdx.x; cell < span; cell += stride) {
     const bool live = cell < A.cells;
-    float e_cur = nanf_, c_cur = 0.f, e_up = nanf_, c_up = 0.f;
-    if (live) {
-      e_cur = __ldg(A.ground + cell);
-      c_cur = __ldg(A.cost + cell);
-      if (A.S > 1) {
-        e_up = __ldg(A.ground + A.stride + cell);
-        c_up = __ldg(A.cost + A.stride + cell);
-      }
-    }
-    for (int k = 0; k < A.S; ++k) {
-      // prefetch slice k+2 while slice k is tested
-      float e_nx = nanf_, c_nx = 0.f;
-      if (live && k + 2 < A.S) {
-        e_nx = __ldg(A.ground + (int64_t)(k + 2) * A.stride + cell);
-        c_nx = __ldg(A.cost + (int64_t)(k + 2) * A.stride + cell);
-      }
-      const bool up_ok = k + 1 >= A.S || !finite32(e_up) || higher_than(e_up, e_cur, A.eps_e) ||
-                         c_cur < c_up;
-      const bool cand = live && finite32(e_cur) && c_cur < A.c_barrier32 && up_ok;
-      if (__any_sync(0xffffffffu, cand)) {
-        unsigned long long m = 0;
-        const int depth = k < kWin ? k : kWin;
-        const unsigned long long want =
-            (1ull << kBit) | ((depth >= 64 ? ~0ull : (1ull << depth) - 1ull));
-        // bits this block has already established need no work (a stale
-        // read only costs a redundant test)
-        const unsigned long long known = *((volatile unsigned long long *)&btab[k]);
-        if (cand && (known & want) != want) {
-          m = 1ull << kBit;
-          unsigned todo = (unsigned)(~known & want);
-          while (todo) {
-            const int j = __ffs(todo) - 1;  // a = k-1-j
-            todo &= todo - 1;
-            const int slot = (k - 1 - j) & (kWin - 1);
-            const float ea = ring_e[slot][threadIdx.x];
-            if (!finite32(ea) || higher_than(e_cur, ea, A.eps_e) ||
-                c_cur < ring_c[slot][threadIdx.x])
-              m |= 1ull << j;
+    float ce[KB + 1], cc[KB + 1];  // slices k0 .. k0+KB of this cell
+    auto load = [&](int k, float &e, float &c) {
+      const bool ok = live && k < A.S;
+      e = ok ? __ldg(A.ground + (int64_t)k * A.stride + cell) : nanf_;
+      c = ok ? __ldg(A.cost + (int64_t)k * A.stride + cell) : 0.f;
+    };
+#pragma unroll
+    for (int u = 0; u <= KB; ++u) load(u, ce[u], cc[u]);
+    for (int k0 = 0; k0 < A.S; k0 += KB) {
+      float ne[KB], nc[KB];  // slices k0+KB+1 .. k0+2KB, in flight while testing
+#pragma unroll
+      for (int u = 0; u < KB; ++u) load(k0 + KB + 1 + u, ne[u], nc[u]);
+#pragma unroll
+      for (int u = 0; u < KB; ++u) {
+        const int k = k0 + u;
+        if (k >= A.S) break;  // uniform
+        const float e_cur = ce[u], c_cur = cc[u], e_up = ce[u + 1], c_up = cc[u + 1];
+        const bool up_ok = k + 1 >= A.S || !finite32(e_up) || higher_than(e_up, e_cur, A.eps_e) ||
+                           c_cur < c_up;
+        const bool cand = live && finite32(e_cur) && c_cur < A.c_barrier32 && up_ok;
+        if (__any_sync(0xffffffffu, cand)) {
+          unsigned long long m = 0;
+          const int depth = k < kWin ? k : kWin;
+          const unsigned long long want =
+              (1ull << kBit) | ((depth >= 64 ? ~0ull : (1ull << depth) - 1ull));
+          // bits this block has already established need no work (a stale
+          // read only costs a redundant test)
+          const unsigned long long known = *((volatile unsigned long long *)&btab[k]);
+          if (cand && (known & want) != want) {
+            m = 1ull << kBit;
+            unsigned todo = (unsigned)(~known & want);
+            while (todo) {
+              const int j = __ffs(todo) - 1;  // a = k-1-j
+              todo &= todo - 1;
+              const int slot = (k - 1 - j) & (kWin - 1);
+              const float ea = ring_e[slot][threadIdx.x];
+              if (!finite32(ea) || higher_than(e_cur, ea, A.eps_e) ||
+                  c_cur < ring_c[slot][threadIdx.x])
+                m |= 1ull << j;
+            }
           }
+          const unsigned lo = __reduce_or_sync(0xffffffffu, (unsigned)m);
+          const unsigned hi = __reduce_or_sync(0xffffffffu, (unsigned)(m >> 32));
+          if ((threadIdx.x & 31) == 0 && (lo | hi))
+            atomicOr(&btab[k], ((unsigned long long)hi << 32) | lo);
         }
-        const unsigned lo = __reduce_or_sync(0xffffffffu, (unsigned)m);
-        const unsigned hi = __reduce_or_sync(0xffffffffu, (unsigned)(m >> 32));
-        if ((threadIdx.x & 31) == 0 && (lo | hi))
-          atomicOr(&btab[k], ((unsigned long long)hi << 32) | lo);
+        ring_e[k & (kWin - 1)][threadIdx.x] = e_cur;  // own column only
+        ring_c[k & (kWin - 1)][threadIdx.x] = c_cur;
       }
-      ring_e[k & (kWin - 1)][threadIdx.x] = e_cur;  // own column only
-      ring_c[k & (kWin - 1)][threadIdx.x] = c_cur;
-      e_cur = e_up;
-      c_cur = c_up;
-      e_up = e_nx;
-      c_up = c_nx;
+      ce[0] = ce[KB];
+      cc[0] = cc[KB];
+#pragma unroll
+      for (int u = 0; u < KB; ++u) {
+        ce[u + 1] = ne[u];
+        cc[u + 1] = nc[u];
+      }
     }
   }
   __syncthreads();
@@ -220,7 +226,7 @@ int run_simplify(pct_ctx *ctx, const float *ground, const float *cost, int S, in
     PCT_CUDA(ctx, cudaFuncSetAttribute(window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)tab_smem));
     const int64_t blocks_needed = (A.cells + kWinNT - 1) / kWinNT;
-    const unsigned grid = (unsigned)std::min<int64_t>(blocks_needed, 6LL * ctx->num_sms);
+    const unsigned grid = (unsigned)std::min<int64_t>(blocks_needed, 12LL * ctx->num_sms);
     window_kernel<<<grid, kWinNT, tab_smem, ctx->stream>>>(A, table);
   }
   if (int rc = check_launch(ctx, "window_kernel")) return rc;
@@ -318,7 +324,7 @@ int simplify_window_table(pct_ctx *ctx, const float *ground, const float *cost, 
     PCT_CUDA(ctx, cudaFuncSetAttribute(window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)tbytes));
     const int64_t blocks_needed = (cells + kWinNT - 1) / kWinNT;
-    const unsigned grid = (unsigned)std::min<int64_t>(blocks_needed, 6LL * ctx->num_sms);
+    const unsigned grid = (unsigned)std::min<int64_t>(blocks_needed, 12LL * ctx->num_sms);
     window_kernel<<<grid, kWinNT, tbytes, ctx->stream>>>(A, table);
     if (int rc = check_launch(ctx, "window_kernel")) return rc;
   }
