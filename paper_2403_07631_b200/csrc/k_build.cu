@@ -124,6 +124,8 @@ __global__ void __launch_bounds__(256) bounds_kernel(const T *__restrict__ xyz, 
 }
 
 // ------------------------------------------------------- K1+K2 bin/scatter
+constexpr int kMaxStagedHeights = 4096;
+
 struct BinArgs {
   double x0, y0, z0, r_g, d_s, inv_rg, inv_ds;
   const double *heights;  // (S,) device
@@ -137,6 +139,14 @@ __global__ void __launch_bounds__(256) scatter_kernel(const T *__restrict__ xyz,
                                                       BinArgs a, uint32_t *__restrict__ gkey,
                                                       uint32_t *__restrict__ ckey,
                                                       unsigned long long *outside) {
+  // plane heights staged in shared memory for the bin fix-ups (dynamic
+  // shared size is 0 when S is too large; then they are read from global)
+  extern __shared__ double hsm[];
+  const bool staged = a.S <= kMaxStagedHeights;
+  if (staged)
+    for (int k = threadIdx.x; k < a.S; k += blockDim.x) hsm[k] = a.heights[k];
+  __syncthreads();
+  const double *hts = staged ? hsm : a.heights;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += stride) {
     const double x = (double)__ldg(xyz + 3 * p);
@@ -155,8 +165,8 @@ __global__ void __launch_bounds__(256) scatter_kernel(const T *__restrict__ xyz,
     // against the exact float64 heights (searchsorted side="right", :157)
     double est = floor((z - a.z0) * a.inv_ds);  // estimate only; fixed up exactly below
     int b = est < 0.0 ? 0 : (est > (double)a.S ? a.S : (int)est);
-    while (b > 0 && __ldg(a.heights + b - 1) >= z) --b;
-    while (b < a.S && __ldg(a.heights + b) < z) ++b;
+    while (b > 0 && hts[b - 1] >= z) --b;
+    while (b < a.S && hts[b] < z) ++b;
     const uint32_t key = f32_key(__double2float_rn(z));
     if (b < a.S) atomicMax(gkey + (int64_t)b * a.cells + cell, key);
     if (b > 0) atomicMin(ckey + (int64_t)(b - 1) * a.cells + cell, key);
@@ -175,10 +185,13 @@ __global__ void __launch_bounds__(256) scan_kernel(const uint32_t *__restrict__ 
   if (c >= cells) return;
   // scratch planes are dense (stride cells); output slice k of the band lives
   // at k * out_stride (== cells for a whole grid, larger inside a halo'd band)
-  // batches of 8 independent loads keep enough bytes in flight per thread
+  // batches of 8 independent loads keep enough bytes in flight per thread;
+  // blockIdx.y = 0 walks the ground planes up, = 1 the ceiling planes down
+  // (two threads per cell double the loads in flight)
   constexpr int U = 8;
   uint32_t run = kKeyEmptyMax;
   int k = 0;
+  if (blockIdx.y == 0) {
   for (; k + U <= S; k += U) {
     uint32_t v[U];
 #pragma unroll
@@ -193,6 +206,8 @@ __global__ void __launch_bounds__(256) scan_kernel(const uint32_t *__restrict__ 
     const uint32_t v = __ldcs(gkey + (int64_t)k * cells + c);
     run = v > run ? v : run;
     __stcs(ground + (int64_t)k * out_stride + c, decode_ground(run));
+  }
+  return;
   }
   run = kKeyEmptyMin;
   k = S - 1;
@@ -274,17 +289,18 @@ int launch_build(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, const pct_
   PCT_CUDA(ctx, cudaMemsetAsync(outside, 0, 8, ctx->stream));
   BinArgs a{fr.origin_x, fr.origin_y, fr.z_min, fr.r_g, fr.d_s, 1.0 / fr.r_g, 1.0 / fr.d_s,
             hdev, cells, nrows, fr.cols, S, row0};
+  const size_t hsm_bytes = S <= kMaxStagedHeights ? (size_t)S * sizeof(double) : 0;
   if (n > 0) {
     if (dtype == PCT_F32)
-      scatter_kernel<float><<<grid_for(ctx, n, 256, 16), 256, 0, ctx->stream>>>(
+      scatter_kernel<float><<<grid_for(ctx, n, 256, 16), 256, hsm_bytes, ctx->stream>>>(
           static_cast<const float *>(xyz), n, a, gkey, ckey, outside);
     else
-      scatter_kernel<double><<<grid_for(ctx, n, 256, 16), 256, 0, ctx->stream>>>(
+      scatter_kernel<double><<<grid_for(ctx, n, 256, 16), 256, hsm_bytes, ctx->stream>>>(
           static_cast<const double *>(xyz), n, a, gkey, ckey, outside);
     if (int rc = check_launch(ctx, "scatter_kernel")) return rc;
   }
-  scan_kernel<<<(unsigned)((cells + 255) / 256), 256, 0, ctx->stream>>>(gkey, ckey, cells, S,
-                                                                        out_stride, ground, ceiling);
+  scan_kernel<<<dim3((unsigned)((cells + 255) / 256), 2), 256, 0, ctx->stream>>>(
+      gkey, ckey, cells, S, out_stride, ground, ceiling);
   return check_launch(ctx, "scan_kernel");
 }
 
