@@ -29,25 +29,35 @@ with open(out / f"{rnd}_launches.csv", "w") as f:
         t = v.get("gpu__time_duration.sum", 0)
         f.write(f"\"{v['kernel'][:90]}\",{t/1e3:.1f},{t/tot:.3f},"
                 f"{v.get('dram__bytes_read.sum',0)/1e6:.1f},{v.get('dram__bytes_write.sum',0)/1e6:.1f}\n")
-rep = Path(f"gpurun_out/prof_{tag}.ncu-rep")
+rep = Path(sys.argv[4]) if len(sys.argv) > 4 else Path(f"gpurun_out/prof_{tag}.ncu-rep")
 if rep.exists():
+    # one details page (+ SASS opcode histogram) per kernel in the report
     det = subprocess.run(["ncu", "-i", str(rep), "--page", "details", "--csv"], capture_output=True, text=True).stdout
     lines = list(csv.reader(io.StringIO(det)))
     hh = lines[0]
-    kname = lines[1][hh.index("Kernel Name")] if len(lines) > 1 else "?"
-    short = re.sub(r"[^a-z_]", "", kname.split("(")[0].split("::")[-1].split("<")[0])
-    body = [f"ncu --set full --clock-control none, report {rep.name}", f"kernel: {kname}", ""]
-    si, mi2, vi2, ui = (hh.index(x) for x in ("Section Name", "Metric Name", "Metric Value", "Metric Unit"))
+    si, mi2, vi2, ui, ki2, ii2 = (hh.index(x) for x in ("Section Name", "Metric Name", "Metric Value",
+                                                         "Metric Unit", "Kernel Name", "ID"))
+    by = collections.OrderedDict()
     for r in lines[1:]:
-        body.append(f"{r[si][:30]:30s} {r[mi2][:55]:55s} {r[vi2]} {r[ui]}")
-    ops = subprocess.run([sys.executable, "scripts/ncu_ops.py", str(rep), "24"], capture_output=True, text=True).stdout
-    (out / f"{rnd}_{short}_ncu.txt").write_text("\n".join(body) + "\n\nSASS opcode histogram:\n" + ops)
-    m = {r[mi2]: r[vi2] for r in lines[1:]}
+        by.setdefault(r[ii2], []).append(r)
+    for rid, rs in by.items():
+        kname = rs[0][ki2]
+        short = re.sub(r"[^a-z_]", "", kname.split("(")[0].split("::")[-1].split("<")[0])
+        body = [f"ncu --set full --clock-control none --import-source on, report {rep.name}, launch id {rid}",
+                f"kernel: {kname}", ""]
+        for r in rs:
+            body.append(f"{r[si][:30]:30s} {r[mi2][:55]:55s} {r[vi2]} {r[ui]}")
+        ops = subprocess.run([sys.executable, "scripts/ncu_ops.py", str(rep), "24", short],
+                             capture_output=True, text=True).stdout
+        (out / f"{rnd}_{short}_ncu.txt").write_text("\n".join(body) + "\n\nSASS opcode histogram:\n" + ops)
 tr_path = out / "ncu_traffic.json"
 tr = json.loads(tr_path.read_text()) if tr_path.exists() else {}
-for v in half:
-    if "eval" in v["kernel"]:
-        tr[cfg] = {"kernel": v["kernel"][:80], "eval_dram_bytes": v.get("dram__bytes_read.sum", 0) + v.get("dram__bytes_write.sum", 0),
-                   "eval_time_us_ncu": v.get("gpu__time_duration.sum", 0) / 1e3, "source": f"{rnd}_launches.csv"}
+# the evaluate stage = every launch between the build scan and the simplify window
+ev = [v for v in half if any(x in v["kernel"] for x in ("eval", "terrain_walk", "resolve_inflate", "zero_pads"))]
+if ev:
+    tr[cfg] = {"kernels": sorted({v["kernel"][:80] for v in ev}),
+               "eval_dram_bytes": sum(v.get("dram__bytes_read.sum", 0) + v.get("dram__bytes_write.sum", 0) for v in ev),
+               "eval_time_us_ncu": sum(v.get("gpu__time_duration.sum", 0) for v in ev) / 1e3,
+               "source": f"{rnd}_launches.csv"}
 tr_path.write_text(json.dumps(tr, indent=1))
 print("wrote", sorted(p.name for p in out.iterdir()))

@@ -1,15 +1,17 @@
 """Opcode histogram + hottest basic blocks of one ncu report (SASS source page)."""
 import csv, re, sys, subprocess, collections, io
 rep = sys.argv[1]
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=sass"],
-                     capture_output=True, text=True).stdout
+cmd = ["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=sass"]
+if len(sys.argv) > 3:
+    cmd += ["-k", "regex:" + sys.argv[3], "-c", "1"]
+out = subprocess.run(cmd, capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 h = rows[1]
 ia = h.index("Source"); ie = h.index("Instructions Executed"); iw = h.index("Warp Stall Sampling (All Samples)")
 ops = collections.Counter(); st = collections.Counter(); tot = totw = 0
 seq = []
 for r in rows[2:]:
-    if len(r) <= ie: continue
+    if len(r) <= ie or not r[ie].isdigit(): continue
     src = r[ia].strip(); m = re.match(r"(@!?U?P\w+\s+)?([A-Z0-9_.]+)", src)
     if not m: continue
     op = m.group(2).split(".")[0]; n = int(r[ie] or 0); w = int(r[iw] or 0)
