@@ -43,7 +43,8 @@ enum {
   PCT_E_EMPTY = -5,      /* CloudFormatError("zero valid points"), cloud_io.py:38-39 */
   PCT_E_NONFINITE = -6,  /* ValueError non-finite coordinates, cloud_io.py:40-41 */
   PCT_E_NOCOST = -7,     /* ValueError "slice has no cost layer" simplify.py:34-35 */
-  PCT_E_RANGE = -8       /* IndexError, simplify.py:49-50 */
+  PCT_E_RANGE = -8,      /* IndexError, simplify.py:49-50 */
+  PCT_E_IO = -9          /* CloudFormatError: unreadable / truncated file, cloud_io.py:142-144 */
 };
 
 enum { PCT_F32 = 0, PCT_F64 = 1 };
@@ -167,6 +168,35 @@ int pct_simplify_triples(pct_ctx *ctx, const float *ground, const float *cost, i
    contains slice k, cn[k] = the run's minimum cost (inf without ground). */
 int pct_planner_context(pct_ctx *ctx, const float *ground, const float *cost, int32_t n_slices,
                         int32_t rows, int32_t cols, double eps_e, int32_t *canon, float *cn);
+
+/* ---- binary PCD ingest (cloud_io.py:123-146 + _keep_finite :53-55) ----- */
+/* Records of record_bytes bytes whose little-endian float32 x, y, z sit at
+   byte offsets xyz_offsets[0..2] (the numpy record dtype of cloud_io.py:
+   132-138; the caller parses the header).  Rows with a non-finite coordinate
+   are dropped; the survivors are written in record order to xyz_out, a
+   device (n_records, 3) float32 array, and counted in *n_valid (the reference
+   up-casts to float64, which is exact).  Syncs. */
+int pct_pcd_extract(pct_ctx *ctx, const void *records, int64_t n_records, int64_t record_bytes,
+                    const int64_t xyz_offsets[3], int records_on_host, float *xyz_out,
+                    int64_t *n_valid);
+/* The same straight from the file: payload at byte data_offset of path
+   (after the DATA line), read in chunks of chunk_bytes (<= 0: 64 MiB) by
+   native threads into pinned buffers, DMA'd while the next chunk is read.
+   PCT_E_IO with "<path>: truncated binary payload" if the file is short. */
+int pct_pcd_load(pct_ctx *ctx, const char *path, int64_t data_offset, int64_t n_records,
+                 int64_t record_bytes, const int64_t xyz_offsets[3], int64_t chunk_bytes,
+                 float *xyz_out, int64_t *n_valid);
+
+/* ---- trajectory ceiling inflation (trajectory.py:277-317, §8 f) -------- */
+/* For n_slices ceiling layers (device, float32, NaN = no ceiling): flat =
+   min filter over the disk of radius ceil(erosion/res) cells (<= 64) with
+   +inf for invalid / outside cells; skirted = min(60, ceil(0.8/(slope*res)))
+   Jacobi sweeps of the 8-neighbour chamfer descent skirt over flat.  Both
+   float64 (n_slices, rows, cols) device arrays, bit-identical to
+   _inflate_ceiling. */
+int pct_ceiling_inflate(pct_ctx *ctx, const float *ceiling, int32_t n_slices, int32_t rows,
+                        int32_t cols, double res, double erosion, double skirt_slope,
+                        double *flat, double *skirted);
 
 /* ---- whole pipeline on a device-resident tomogram ---------------------- */
 /* xyz may be a device pointer (xyz_on_host = 0) or host memory (1; pinned

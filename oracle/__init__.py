@@ -6,6 +6,10 @@ the three stages on the hot path:
   tomography.py      build_tomogram           tomoplan/tomogram.py:127-213
   traversability.py  evaluate_tomogram & ops  tomoplan/traversability.py:59-236
   simplify.py        simplify_tomogram        tomoplan/simplify.py:18-73
+  archive.py         LGA archive bytes        tomoplan/tomogram.py:219-276
+  planner_ctx.py     canonical-node arrays    tomoplan/planner.py:62-93
+  cloud_io.py        binary PCD payload       tomoplan/cloud_io.py:53-55,123-146
+  trajectory.py      ceiling inflation        tomoplan/trajectory.py:277-317
 
 Parity status: PINNED.  ``tests/golden/make_golden.py`` imports the reference
 package (only available in the build container, /root/reference) and records

@@ -7,7 +7,9 @@ a C ABI (include/pct.h).  There is no CPU fallback.
 """
 
 from .archive import load_tomogram, save_tomogram
+from . import cloud_io
 from .cloud import CloudFormatError, PointCloud
+from .cloud_io import DeviceCloud, load_cloud, sniff_format
 from .simplify import DEFAULT_EPS_E, simplify_tomogram, unique_cells
 from .tomogram import (
     GRID_SIDE_LIMIT,
@@ -41,4 +43,5 @@ __all__ = [
     "rasterize_index", "InflationKernel", "TravParams", "build_kernel", "evaluate_slice",
     "evaluate_tomogram", "fuse_costs", "gentle_fraction", "ground_cost", "inflate",
     "interval_cost", "slope_magnitudes", "terrain_cost_values", "save_tomogram", "load_tomogram",
+    "cloud_io", "DeviceCloud", "load_cloud", "sniff_format",
 ]

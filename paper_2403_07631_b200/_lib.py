@@ -25,6 +25,7 @@ PCT_E_EMPTY = -5
 PCT_E_NONFINITE = -6
 PCT_E_NOCOST = -7
 PCT_E_RANGE = -8
+PCT_E_IO = -9
 PCT_F32, PCT_F64 = 0, 1
 LAYER_GROUND, LAYER_CEILING, LAYER_COST = 0, 1, 2
 
@@ -80,6 +81,9 @@ _SIGS = {
     "pct_simplify_window": ([_vp, _vp, _vp, _i32, _i64, _i64, _d, _d, _vp], C.c_int),
     "pct_simplify_triples": ([_vp, _vp, _vp, _i32, _i64, _i64, _d, _d, _vp, _i32, _vp], C.c_int),
     "pct_planner_context": ([_vp, _vp, _vp, _i32, _i32, _i32, _d, _vp, _vp], C.c_int),
+    "pct_ceiling_inflate": ([_vp, _vp, _i32, _i32, _i32, _d, _d, _d, _vp, _vp], C.c_int),
+    "pct_pcd_extract": ([_vp, _vp, _i64, _i64, _vp, C.c_int, _vp, _vp], C.c_int),
+    "pct_pcd_load": ([_vp, C.c_char_p, _i64, _i64, _i64, _vp, _i64, _vp, _vp], C.c_int),
     "pct_tomo_build": ([_vp, _vp, _i64, C.c_int, C.c_int, _d, _d, _i64, C.POINTER(_vp)], C.c_int),
     "pct_tomo_upload": ([_vp, C.POINTER(FrameC), _vp, _vp, _vp, C.POINTER(_vp)], C.c_int),
     "pct_tomo_evaluate": ([_vp, _vp, C.POINTER(TravParamsC), _vp, _i32], C.c_int),

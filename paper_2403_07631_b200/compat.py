@@ -6,7 +6,7 @@
 
 Replaces the hot-path entry points everywhere the reference binds them:
 the package namespace (tomoplan/__init__.py:14-45), the defining modules
-(tomogram.py, traversability.py, simplify.py) and the modules that imported
+(tomogram.py, traversability.py, simplify.py, cloud_io.py) and the modules that imported
 them by name (cli.py:20, bench.py:19).  Everything downstream (planner,
 trajectory, LGA save/load, CLI) consumes the returned objects by duck
 typing: ``Tomogram.slices[k].ground/ceiling/cost.values`` are (rows, cols)
@@ -19,6 +19,8 @@ from __future__ import annotations
 import importlib
 
 from . import archive as _arch
+from . import cloud_io as _cio
+from . import trajectory as _traj
 from . import simplify as _simp
 from . import tomogram as _tomo
 from . import traversability as _trav
@@ -39,9 +41,12 @@ REPLACEMENTS = {
     "unique_cells": _simp.unique_cells,
     "save_tomogram": _arch.save_tomogram,   # byte-identical LGA writer (§8 f)
     "load_tomogram": _arch.load_tomogram,
+    "load_cloud": _cio.load_cloud,          # binary PCD straight to HBM (§8 f)
+    "_inflate_ceiling": _traj.inflate_ceiling,  # trajectory.py:277-317 (§8 f)
 }
 
-MODULES = ("", ".tomogram", ".traversability", ".simplify", ".cli", ".bench")
+MODULES = ("", ".tomogram", ".traversability", ".simplify", ".cloud_io", ".trajectory", ".cli",
+           ".bench")
 
 _saved: list = []
 

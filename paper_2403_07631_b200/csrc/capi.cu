@@ -152,6 +152,7 @@ int pct_ctx_destroy(pct_ctx *ctx) {
   for (auto e : ctx->ev)
     if (e) cudaEventDestroy(e);
   if (ctx->hsmall) cudaFreeHost(ctx->hsmall);
+  if (ctx->pinned_io) cudaFreeHost(ctx->pinned_io);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
   return PCT_OK;

@@ -21,8 +21,10 @@ struct pct_ctx {
   // grow-only device scratch (build keys, staging of host points)
   void *scratch = nullptr;
   size_t scratch_bytes = 0;
-  void *staging = nullptr;  // device copy of host xyz
+  void *staging = nullptr;  // device copy of host xyz / PCD payload chunks
   size_t staging_bytes = 0;
+  void *pinned_io = nullptr;  // pinned double buffer of the PCD file reader
+  size_t pinned_io_bytes = 0;
   // small device/pinned buffers for reductions and flags
   void *dsmall = nullptr;   // 64 KiB device
   void *hsmall = nullptr;   // 64 KiB pinned host

@@ -306,11 +306,16 @@ def device_bounds(xyz: np.ndarray, device=None):
     ctx = _lib.context(device)
     a = np.ascontiguousarray(xyz)
     buf = _lib.DeviceBuffer.from_host(ctx, a)
+    return bounds_on_device(ctx, buf.ptr, a.shape[0], a.dtype)
+
+
+def bounds_on_device(ctx, ptr: int, n: int, dtype):
+    """(min, max) of n device-resident points at ``ptr`` (float32/float64)."""
     lo = np.empty(3, np.float64)
     hi = np.empty(3, np.float64)
     with ctx.lock:
-        rc = ctx.lib.pct_bounds(ctx.h, buf.ptr, a.shape[0], _dtype_code(a), lo.ctypes.data,
-                                hi.ctypes.data)
+        rc = ctx.lib.pct_bounds(ctx.h, ptr, int(n), _dtype_code(np.empty(0, dtype)),
+                                lo.ctypes.data, hi.ctypes.data)
         if rc == _lib.PCT_E_NONFINITE:
             raise ValueError("point cloud contains non-finite coordinates")
         ctx.check(rc, "pct_bounds")
@@ -363,5 +368,10 @@ def build_tomogram(cloud: PointCloud, d_s: float, r_g: float, threads: int = 1,
     """
     if d_s <= 0 or r_g <= 0:
         raise ValueError("d_s and r_g must be positive")
+    dev = getattr(cloud, "device_points", None)
+    if dev is not None:  # HBM-resident cloud (binary PCD ingest): no host round trip
+        ptr, n, dtype, dev_id = dev()
+        return build_from_points(ptr, d_s, r_g, max_grid_side, device=dev_id, on_device=True,
+                                 n_points=n, dtype=dtype)
     xyz = cloud.xyz if hasattr(cloud, "xyz") else np.asarray(cloud)
     return build_from_points(xyz, d_s, r_g, max_grid_side, device=device)
