@@ -301,6 +301,13 @@ PCT_HD float fast_cinit(float g, float ceil, const FastCell &t, const EvalConsts
   return f;
 }
 
+// as cinit_resolve with the test count >= ps_min_count already decided
+PCT_HD float cinit_resolve_ok(float enc, bool ok, const EvalConsts &K) {
+  const uint32_t u = f32_bits(enc);
+  if (u & 0x80000000u) return ok ? bits_f32(u & 0x7FFFFFFFu) : (float)K.c_barrier;
+  return enc;
+}
+
 PCT_HD float cinit_resolve(float enc, int count, const EvalConsts &K) {
   uint32_t u = f32_bits(enc);
   if (u & 0x80000000u) return count >= K.ps_min_count ? bits_f32(u & 0x7FFFFFFFu)

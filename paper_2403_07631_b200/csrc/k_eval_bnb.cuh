@@ -1,0 +1,552 @@
+// k_eval_bnb.cuh — resolve + branch-and-bound inflation (included by
+// k_evaluate.cu inside namespace pct::{anon}, after k_eval_split.cuh whose TMA
+// helpers, EncLayout and terrain walk it shares).
+//
+// inflate (traversability.py:205-213) is out = max_k fl32(w_k * M_k), M_k the
+// max of c_init over the taps of weight class k (w_1 > w_2 > ... > 0).  All
+// c_init >= 0 and x -> fl32(w x) is monotone, so with U >= every M_k:
+//   * once acc >= fl32(w_k * U), no class k' >= k can raise acc (branch and
+//     bound over the classes in weight order);
+//   * class 1 (weight 1 for Table-I parameters: the disk d <= d_inf) is a
+//     small disk whose max D1 is a separable max filter.
+// Per tile and slice:
+//   P0  gentle bits of the foothold window (global bitmap -> smem), TMA'd
+//       encoded c_init tile + halo; vertical gentle counts of the (2r+1)-row
+//       window, bit-sliced (one plane per count bit, 32 columns per word);
+//       foothold-branch cells resolved in place (3-4 funnel-shift popcounts)
+//   P1  maxima of aligned R x R blocks of c_init, and the horizontal maxima
+//       planes H_h(y, x) = max c(y, x-h .. x+h) the disk needs
+//   P2  U(output block) = max of its 3 x 3 neighbouring blocks (covers every
+//       tap of the (2R+1)^2 window); D1 per output from the planes; outputs
+//       with fl32(w_1 D1) >= fl32(w_2 U) are final (~80 % on the config maps),
+//       the rest go to a list
+//   P3  listed outputs walk the remaining classes (compiled ring offsets,
+//       bnb_rings.h) until the bound stops them
+// The class structure is compiled per R (R=4: r_g 0.1, R=8: r_g 0.05 with the
+// Table-I d_inf / d_sm); the host checks the caller's kernel against it and
+// otherwise keeps the full-tap kernels.
+
+#include "bnb_rings.h"
+
+constexpr int kBnbMaxClasses = 64;
+__constant__ float c_bw[kBnbMaxClasses + 1];  // class weights, descending; c_bw[n] = 0
+
+// half-widths of the class-1 disk per row offset |a|
+template <int R>
+struct DiskShape;
+template <>
+struct DiskShape<4> {  // a^2 + b^2 <= 4: 13 taps
+  static constexpr int A = 2;
+  static constexpr int h[3] = {2, 1, 0};
+};
+template <>
+struct DiskShape<8> {  // a^2 + b^2 <= 16: 49 taps
+  static constexpr int A = 4;
+  static constexpr int h[5] = {4, 3, 3, 2, 0};
+};
+
+constexpr int count_bits(int n) { return n < 2 ? 1 : 1 + count_bits(n / 2); }
+
+template <int R, int PR, int TH, int TW>
+struct BnbGeom {
+  static constexpr int CH = TH + 2 * R, CW = TW + 2 * R;  // c_init tile + halo
+  static constexpr int GH = CH + 2 * PR, GW = CW + 2 * PR;
+  static constexpr int GWW = (GW + 31) / 32 + 1;
+  static constexpr int CWW = (CW + 31) / 32;            // words of one foothold-ok row
+  static constexpr int SIDE = 2 * PR + 1;
+  static constexpr int NVP = count_bits(SIDE);          // bit planes of a column count
+  static constexpr int NSB = count_bits(SIDE * SIDE);   // bit planes of a window count
+  static constexpr int BUF = ((CH * CW * 4) + 127) / 128 * 128;
+  static constexpr int NBUF = 3;              // previous, current, prefetched slice
+  static constexpr int NPL = R == 4 ? 1 : 2;  // planes: R=4 H1; R=8 H3, H2
+  static constexpr int PLANE = CH * TW;       // floats per plane
+  static constexpr int NBY = CH / R, NBX = CW / R;  // c_init blocks (upper bound)
+  static constexpr int QY = TH / R, QX = TW / R;    // output blocks (upper bound)
+  static constexpr int CBY = CH / 4, CBX = CW / 4;  // 4x4 c_init change blocks
+  static constexpr int DBY = TH / 4, DBX = TW / 4;  // 4x4 output dirty blocks
+  static constexpr int SPAN = (3 + 2 * R) / 4 + 1;  // change blocks under one dirty block
+  // regions (no aliasing: without a barrier at the end of a slice, P0 of the
+  // next slice overlaps P3 / P4 of this one)
+  static constexpr int O_BUF = 0;
+  static constexpr int O_PL = NBUF * BUF;
+  static constexpr int O_BITS = O_PL + NPL * PLANE * 4;
+  static constexpr int O_OK = O_BITS + ((GH * GWW * 4 + 15) / 16) * 16;
+  static constexpr int O_OT = O_OK + ((CH * CWW * 4 + 15) / 16) * 16;  // output tile
+  static constexpr int O_SL = O_OT + TH * TW * 4;                      // u16 list
+  static constexpr int O_BM = O_SL + ((TH * TW * 2 + 15) / 16) * 16;
+  static constexpr int O_U = O_BM + ((NBY * NBX * 4 + 15) / 16) * 16;
+  static constexpr int O_CB = O_U + ((QY * QX * 4 + 15) / 16) * 16;     // u8 change blocks
+  static constexpr int O_DB = O_CB + ((CBY * CBX + 15) / 16) * 16;      // u8 dirty blocks
+  static constexpr int O_BAR = O_DB + ((DBY * DBX + 15) / 16) * 16;
+  static constexpr int SMEM = O_BAR + 128;  // 3 mbarriers, 3 x 2 coordinate slots, warp counts
+  static_assert(TH % R == 0 && TW % R == 0 && CW % 4 == 0 && R % 4 == 0, "bnb tile geometry");
+  static_assert(TH * TW <= 65536, "u16 output indices");
+  static_assert((TH * (TW / 4)) % 32 == 0, "warp-uniform output loop (ballots)");
+  static_assert(SIDE <= 31 && NSB <= 10, "foothold window");
+};
+
+__device__ __forceinline__ float fmax3(float a, float b, float c) { return fmaxf(fmaxf(a, b), c); }
+__device__ __forceinline__ float4 lds4(const float *p) { return *reinterpret_cast<const float4 *>(p); }
+
+// full adder on 32 bit-slices: s = a ^ b ^ c, k = majority(a, b, c)
+__device__ __forceinline__ void fadd(uint32_t a, uint32_t b, uint32_t c, uint32_t &s,
+                                     uint32_t &k) {
+  s = a ^ b ^ c;
+  k = (a & b) | (c & (a ^ b));
+}
+
+// per-column counts of N one-bit rows, bit-sliced into NB planes
+template <int N, int NB>
+__device__ __forceinline__ void column_count(const uint32_t (&x)[N], uint32_t (&o)[NB]) {
+  if constexpr (N == 7 && NB == 3) {
+    uint32_t s1, c1, s2, c2, c3;
+    fadd(x[0], x[1], x[2], s1, c1);
+    fadd(x[3], x[4], x[5], s2, c2);
+    fadd(s1, s2, x[6], o[0], c3);
+    fadd(c1, c2, c3, o[1], o[2]);
+  } else if constexpr (N == 13 && NB == 4) {
+    uint32_t s1, c1, s2, c2, s3, c3, s4, c4, t1, d1, d2, u1, e1, u2, e2;
+    fadd(x[0], x[1], x[2], s1, c1);
+    fadd(x[3], x[4], x[5], s2, c2);
+    fadd(x[6], x[7], x[8], s3, c3);
+    fadd(x[9], x[10], x[11], s4, c4);
+    fadd(s1, s2, s3, t1, d1);
+    fadd(t1, s4, x[12], o[0], d2);
+    fadd(c1, c2, c3, u1, e1);
+    fadd(c4, d1, d2, u2, e2);
+    o[1] = u1 ^ u2;
+    fadd(e1, e2, u1 & u2, o[2], o[3]);
+  } else {  // ripple accumulation
+#pragma unroll
+    for (int p = 0; p < NB; ++p) o[p] = 0u;
+#pragma unroll
+    for (int d = 0; d < N; ++d) {
+      uint32_t c = x[d];
+#pragma unroll
+      for (int p = 0; p < NB; ++p) {
+        const uint32_t t = o[p] & c;
+        o[p] ^= c;
+        c = t;
+      }
+    }
+  }
+}
+
+// a += b << sh on bit-sliced numbers (NA planes, result truncated to NA)
+template <int NA, int NB>
+__device__ __forceinline__ void bs_add(uint32_t (&a)[NA], const uint32_t (&b)[NB], int sh) {
+  uint32_t c = 0u;
+#pragma unroll
+  for (int p = 0; p < NA; ++p) {
+    const int q = p - sh;
+    const uint32_t y = (q >= 0 && q < NB) ? b[q] : 0u;
+    const uint32_t s = a[p] ^ y ^ c;
+    c = (a[p] & y) | (c & (a[p] ^ y));
+    a[p] = s;
+  }
+}
+
+// 32 lanes of "a >= t" for a bit-sliced a (NA planes) and a scalar t
+template <int NA>
+__device__ __forceinline__ uint32_t bs_ge(const uint32_t (&a)[NA], int t) {
+  if (t <= 0) return 0xFFFFFFFFu;
+  if (t >= (1 << NA)) return 0u;
+  uint32_t borrow = 0u;  // a - t, from bit 0 up
+#pragma unroll
+  for (int p = 0; p < NA; ++p) {
+    const uint32_t tb = ((t >> p) & 1) ? 0xFFFFFFFFu : 0u;
+    borrow = (~a[p] & tb) | (~(a[p] ^ tb) & borrow);
+  }
+  return ~borrow;
+}
+
+// max over the ring taps T .. E-1 (compile-time offsets)
+template <int R, int CW, int T, int E>
+__device__ __forceinline__ float ring_max(const float *__restrict__ ctr, float m) {
+  using RG = BnbRings<R>;
+  if constexpr (T + 1 < E) {
+    constexpr int o0 = RG::dy(T) * CW + RG::dx(T), o1 = RG::dy(T + 1) * CW + RG::dx(T + 1);
+    return ring_max<R, CW, T + 2, E>(ctr, fmax3(m, ctr[o0], ctr[o1]));
+  } else if constexpr (T < E) {
+    constexpr int o0 = RG::dy(T) * CW + RG::dx(T);
+    return fmaxf(m, ctr[o0]);
+  } else {
+    return m;
+  }
+}
+
+// remaining classes K.. of the listed output at ctr under the bound U
+template <int R, int CW, int K>
+__device__ __forceinline__ void slow_classes(const float *__restrict__ ctr, float U, bool live,
+                                             float &acc) {
+  using RG = BnbRings<R>;
+  if constexpr (K < RG::NCLS) {
+    const float wk = c_bw[K];
+    live = live && acc < wk * U;
+    if (!__any_sync(0xFFFFFFFFu, live)) return;
+    if (live) acc = fmaxf(acc, wk * ring_max<R, CW, RG::start(K), RG::start(K + 1)>(ctr, 0.0f));
+    slow_classes<R, CW, K + 1>(ctr, U, live, acc);
+  }
+}
+
+// Persistent CTAs over work items = (tile, run of consecutive slices).  The
+// first slice of a run computes every output; later slices compare the
+// resolved c_init tile + halo with the previous slice's (kept in the third
+// TMA buffer) per 4 x 4 block and recompute only the 4 x 4 output blocks
+// whose (2R+1)^2 windows touch a changed block: an output is a function of
+// the resolved c_init in its window alone, so the others keep their values
+// (the output tile lives in shared memory and is stored every slice).
+template <int R, int PR, int TH, int TW, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) resolve_inflate_bnb_kernel(
+    const __grid_constant__ CUtensorMap enc_map, const uint32_t *__restrict__ bits_in, int rows,
+    int cols, int S, int run, int64_t words, float *__restrict__ cost) {
+  using G = BnbGeom<R, PR, TH, TW>;
+  constexpr int NWARP = NT / 32;
+  constexpr int WSEG = TH * TW / NWARP;  // list entries per warp (its P2 outputs)
+  static_assert((TH * TW) % NWARP == 0 && NWARP <= 32, "warp list segments");
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint32_t *bits = reinterpret_cast<uint32_t *>(smem + G::O_BITS);
+  uint32_t *okb = reinterpret_cast<uint32_t *>(smem + G::O_OK);   // [CH][CWW]
+  float *planes = reinterpret_cast<float *>(smem + G::O_PL);
+  float *ot = reinterpret_cast<float *>(smem + G::O_OT);
+  uint16_t *slist = reinterpret_cast<uint16_t *>(smem + G::O_SL);
+  uint32_t *bm = reinterpret_cast<uint32_t *>(smem + G::O_BM);    // block maxima (float bits)
+  float *ub = reinterpret_cast<float *>(smem + G::O_U);
+  unsigned char *chg = smem + G::O_CB;
+  unsigned char *dirty = smem + G::O_DB;
+  uint64_t *bar = reinterpret_cast<uint64_t *>(smem + G::O_BAR);  // [3]
+  int *slot = reinterpret_cast<int *>(smem + G::O_BAR + 32);      // [3][2]
+  int *wcnt = reinterpret_cast<int *>(smem + G::O_BAR + 64);      // [NWARP]
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  uint16_t *wlist = slist + warp * WSEG;
+  if (tid == 0 && (smem_u32(smem) & 127u) != 0u) __trap();
+  const int tx = (cols + TW - 1) / TW, ty = (rows + TH - 1) / TH;
+  const int tiles = tx * ty;
+  const int nruns = (S + run - 1) / run;
+  const int n_items = tiles * nruns;
+  const int64_t cells = (int64_t)rows * cols;
+  constexpr uint32_t BOX_BYTES = G::CH * G::CW * 4;
+  const float w0 = c_bw[0], w1 = c_bw[1];
+  // thread 0 walks the CTA's step sequence one step ahead of the others:
+  // step = (item, slice); it records the tile origin and slice of each step
+  // in the slot of the buffer it loads
+  int nx_item = blockIdx.x, nx_k = (blockIdx.x / tiles) * run;
+  auto issue = [&](int buf) {
+    const int r = nx_item / tiles, t = nx_item - r * tiles;
+    const int ti = t / tx;
+    const int i0 = ti * TH, j0 = (t - ti * tx) * TW;
+    slot[buf * 2] = i0 * 65536 + j0 / TW;  // rows < 2^15, tiles of >= 32 columns
+    slot[buf * 2 + 1] = nx_k | ((nx_k == r * run) ? 0x40000000 : 0);  // first slice of its run
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(&bar[buf], BOX_BYTES);
+    tma_load_3d(smem + G::O_BUF + buf * G::BUF, &enc_map, &bar[buf], j0, i0, nx_k);
+    if (++nx_k >= min(S, (r + 1) * run)) {
+      nx_item += gridDim.x;
+      nx_k = (nx_item / tiles) * run;
+    }
+  };
+  if (tid == 0) {
+#pragma unroll
+    for (int b = 0; b < G::NBUF; ++b) mbar_init(&bar[b], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (nx_item < n_items) issue(0);
+  }
+  __syncthreads();
+  int steps = 0;  // this CTA's total
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const int r = item / tiles;
+    steps += min(S, (r + 1) * run) - r * run;
+  }
+  uint32_t phase_bits = 0u;
+  for (int st = 0; st < steps; ++st) {
+    const int cur = st % 3, prv = (st + 2) % 3;
+    float *ci = reinterpret_cast<float *>(smem + G::O_BUF + cur * G::BUF);
+    const float *cp = reinterpret_cast<const float *>(smem + G::O_BUF + prv * G::BUF);
+    const int i0 = slot[cur * 2] >> 16, j0 = (slot[cur * 2] & 0xFFFF) * TW;
+    const int k = slot[cur * 2 + 1] & 0x3FFFFFFF;
+    const bool first = (slot[cur * 2 + 1] & 0x40000000) != 0;
+    // the buffer of step st-2 (read as `prv` by step st-1) is free again
+    if (tid == 0 && st + 1 < steps) issue((st + 1) % 3);
+    // ---- P0a: gentle bits of the window region (bit x of word w = gentle
+    // column 32w + x, gentle column 0 = c_init column -r); resets
+    const uint32_t *bk = bits_in + (int64_t)k * words;
+    for (int idx = tid; idx < G::GH * G::GWW; idx += NT) {
+      const int y = idx / G::GWW, w = idx - y * G::GWW;
+      const int gi = i0 - R - PR + y;
+      const int gj = j0 - R - PR + 32 * w;
+      uint32_t word = 0;
+      if (gi >= 0 && gi < rows && gj < cols && gj + 32 > 0) {
+        const int64_t bit = (int64_t)gi * cols + gj;
+        const int64_t wi = bit >> 5;
+        const int sh = (int)(bit & 31);
+        const uint32_t lo = (wi >= 0 && wi < words) ? __ldg(bk + wi) : 0u;
+        const uint32_t hi = (wi + 1 >= 0 && wi + 1 < words) ? __ldg(bk + wi + 1) : 0u;
+        word = (uint32_t)((((uint64_t)hi << 32) | lo) >> sh);
+        const int first_b = gj < 0 ? -gj : 0;
+        const int last = cols - gj < 32 ? cols - gj : 32;
+        const uint32_t mhi = last >= 32 ? 0xFFFFFFFFu : ((1u << last) - 1u);
+        const uint32_t mlo = first_b >= 32 ? 0u : (0xFFFFFFFFu << first_b);
+        word &= mhi & mlo;
+      }
+      if (32 * w >= G::GW) word = 0;
+      else if (G::GW - 32 * w < 32) word &= (1u << (G::GW - 32 * w)) - 1u;
+      bits[idx] = word;
+    }
+    for (int idx = tid; idx < G::NBY * G::NBX; idx += NT) bm[idx] = 0u;
+    for (int idx = tid; idx < G::CBY * G::CBX; idx += NT) chg[idx] = first ? 1 : 0;
+    __syncthreads();
+    // ---- P0b: foothold test of every c_init cell, 32 cells per word:
+    // vertical counts of the (2r+1)-row window (bit-sliced, this word and the
+    // next), then the horizontal (2r+1)-column sum, then count >= ps_min
+    for (int idx = tid; idx < G::CH * G::CWW; idx += NT) {
+      const int y = idx / G::CWW, w = idx - y * G::CWW;
+      uint32_t x0[G::SIDE], x1[G::SIDE], v0[G::NVP], v1[G::NVP];
+#pragma unroll
+      for (int d = 0; d < G::SIDE; ++d) {
+        x0[d] = bits[(y + d) * G::GWW + w];
+        x1[d] = bits[(y + d) * G::GWW + w + 1];
+      }
+      column_count<G::SIDE, G::NVP>(x0, v0);
+      column_count<G::SIDE, G::NVP>(x1, v1);
+      uint32_t sum[G::NSB];
+#pragma unroll
+      for (int p = 0; p < G::NSB; ++p) sum[p] = 0u;
+#pragma unroll
+      for (int p = 0; p < G::NVP; ++p) {
+        uint32_t sh[G::SIDE], h[G::NVP];
+#pragma unroll
+        for (int d = 0; d < G::SIDE; ++d) sh[d] = __funnelshift_r(v0[p], v1[p], d);
+        column_count<G::SIDE, G::NVP>(sh, h);
+        bs_add<G::NSB, G::NVP>(sum, h, p);
+      }
+      okb[idx] = bs_ge<G::NSB>(sum, c_K.ps_min_count);
+    }
+    mbar_wait(&bar[cur], (phase_bits >> cur) & 1u);
+    phase_bits ^= 1u << cur;
+    __syncthreads();
+    // ---- P0c: resolve the foothold-branch cells in place; maxima of the
+    // aligned R x R blocks (c_init >= 0: float order = uint order); 4 x 4
+    // blocks that differ from the previous slice
+    constexpr int CW4 = G::CW / 4;
+    for (int q = tid; q < G::CH * CW4; q += NT) {
+      float4 v = lds4(ci + 4 * q);
+      const int y = q / CW4, x = 4 * (q - y * CW4);
+      const uint32_t sgn = (f32_bits(v.x) | f32_bits(v.y) | f32_bits(v.z) | f32_bits(v.w));
+      if (sgn & 0x80000000u) {
+        const uint32_t ok = okb[y * G::CWW + (x >> 5)] >> (x & 31);  // 4 cells, one word
+        v.x = cinit_resolve_ok(v.x, ok & 1u, c_K);
+        v.y = cinit_resolve_ok(v.y, ok & 2u, c_K);
+        v.z = cinit_resolve_ok(v.z, ok & 4u, c_K);
+        v.w = cinit_resolve_ok(v.w, ok & 8u, c_K);
+        *reinterpret_cast<float4 *>(ci + 4 * q) = v;
+      }
+      const float m4 = fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w));
+      if (m4 > 0.0f) atomicMax(&bm[(y / R) * G::NBX + x / R], f32_bits(m4));
+      if (!first) {
+        const float4 u = lds4(cp + 4 * q);
+        if (f32_bits(u.x) != f32_bits(v.x) || f32_bits(u.y) != f32_bits(v.y) ||
+            f32_bits(u.z) != f32_bits(v.z) || f32_bits(u.w) != f32_bits(v.w))
+          chg[(y >> 2) * G::CBX + (x >> 2)] = 1;
+      }
+    }
+    __syncthreads();
+    // ---- P1: dirty output blocks; horizontal maxima planes; upper bound per
+    // output block (3 x 3 c_init blocks cover every tap of its outputs' windows)
+    {
+      constexpr int NG = TW / 4;
+      constexpr int NQ = G::QY * G::QX;
+      constexpr int ND = G::DBY * G::DBX;
+      for (int q = tid; q < ND + NQ + G::CH * NG; q += NT) {
+        if (q < ND) {
+          const int dy = q / G::DBX, dx = q - dy * G::DBX;
+          bool d = false;
+#pragma unroll
+          for (int a = 0; a < G::SPAN; ++a)
+#pragma unroll
+            for (int b = 0; b < G::SPAN; ++b) d |= chg[(dy + a) * G::CBX + dx + b] != 0;
+          dirty[q] = d;
+        } else if (q < ND + NQ) {
+          const int e = q - ND;
+          const int qy = e / G::QX, qx = e - qy * G::QX;
+          const uint32_t *p = bm + qy * G::NBX + qx;
+          const uint32_t m = max(max(max(p[0], p[1]), max(p[2], p[G::NBX])),
+                                 max(max(p[G::NBX + 1], p[G::NBX + 2]),
+                                     max(max(p[2 * G::NBX], p[2 * G::NBX + 1]), p[2 * G::NBX + 2])));
+          ub[e] = bits_f32(m);
+        } else {
+          const int e = q - ND - NQ;
+          const int y = e / NG, g = e - y * NG;
+          // c_init columns 4g + R - 4 .. 4g + R + 7 (12 values, 16-byte aligned)
+          const float *p = ci + y * G::CW + 4 * g + R - 4;
+          const float4 a = lds4(p), b = lds4(p + 4), c = lds4(p + 8);
+          const float v[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
+          // output column 4g + t has its centre at v[4 + t]
+          if constexpr (R == 4) {
+            float4 h1;
+            h1.x = fmax3(v[3], v[4], v[5]);
+            h1.y = fmax3(v[4], v[5], v[6]);
+            h1.z = fmax3(v[5], v[6], v[7]);
+            h1.w = fmax3(v[6], v[7], v[8]);
+            *reinterpret_cast<float4 *>(planes + y * TW + 4 * g) = h1;
+          } else {
+            float h2[4], h3[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              h2[t] = fmax3(fmax3(v[t + 2], v[t + 3], v[t + 4]), v[t + 5], v[t + 6]);
+              h3[t] = fmax3(h2[t], v[t + 1], v[t + 7]);
+            }
+            *reinterpret_cast<float4 *>(planes + y * TW + 4 * g) = make_float4(h3[0], h3[1], h3[2], h3[3]);
+            *reinterpret_cast<float4 *>(planes + G::PLANE + y * TW + 4 * g) =
+                make_float4(h2[0], h2[1], h2[2], h2[3]);
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // ---- P2: dirty outputs: disk max, bound test; the rest to this warp's list
+    int nlist = 0;  // warp-uniform
+    {
+      constexpr int NG = TW / 4;
+      for (int q = tid; q < TH * NG; q += NT) {
+        const int i = q / NG, g = q - i * NG;
+        const bool dq = dirty[(i >> 2) * G::DBX + g] != 0;
+        if (!__any_sync(0xFFFFFFFFu, dq)) continue;
+        const int yc = i + R;  // centre row in c_init / plane coordinates
+        float d1[4];
+        if constexpr (R == 4) {
+          const float4 a = lds4(planes + (yc - 1) * TW + 4 * g);
+          const float4 b = lds4(planes + yc * TW + 4 * g);
+          const float4 c = lds4(planes + (yc + 1) * TW + 4 * g);
+          const float *cr = ci + yc * G::CW + 4 * g;  // c_init cols 4g .. 4g+11
+          const float4 r0 = lds4(cr), r1 = lds4(cr + 4), r2 = lds4(cr + 8);
+          const float rv[12] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w, r2.x, r2.y, r2.z, r2.w};
+          const float4 u2 = lds4(ci + (yc - 2) * G::CW + 4 * g + 4);
+          const float4 d2 = lds4(ci + (yc + 2) * G::CW + 4 * g + 4);
+          d1[0] = fmax3(fmax3(a.x, b.x, c.x), fmax3(rv[2], rv[6], u2.x), d2.x);
+          d1[1] = fmax3(fmax3(a.y, b.y, c.y), fmax3(rv[3], rv[7], u2.y), d2.y);
+          d1[2] = fmax3(fmax3(a.z, b.z, c.z), fmax3(rv[4], rv[8], u2.z), d2.z);
+          d1[3] = fmax3(fmax3(a.w, b.w, c.w), fmax3(rv[5], rv[9], u2.w), d2.w);
+        } else {
+          const float *h3 = planes + 4 * g, *h2 = planes + G::PLANE + 4 * g;
+          const float4 a0 = lds4(h3 + (yc - 2) * TW), a1 = lds4(h3 + (yc - 1) * TW),
+                       a2 = lds4(h3 + yc * TW), a3 = lds4(h3 + (yc + 1) * TW),
+                       a4 = lds4(h3 + (yc + 2) * TW);
+          const float4 b0 = lds4(h2 + (yc - 3) * TW), b1 = lds4(h2 + (yc + 3) * TW);
+          const float *cr = ci + yc * G::CW + 4 * g;  // centre of output 4g: col 4g + 8
+          const float4 l4 = lds4(cr + 4), r4 = lds4(cr + 12);
+          const float4 u4 = lds4(ci + (yc - 4) * G::CW + 4 * g + 8);
+          const float4 d4 = lds4(ci + (yc + 4) * G::CW + 4 * g + 8);
+          d1[0] = fmax3(fmax3(a0.x, a1.x, a2.x), fmax3(a3.x, a4.x, b0.x),
+                        fmax3(fmax3(b1.x, l4.x, r4.x), u4.x, d4.x));
+          d1[1] = fmax3(fmax3(a0.y, a1.y, a2.y), fmax3(a3.y, a4.y, b0.y),
+                        fmax3(fmax3(b1.y, l4.y, r4.y), u4.y, d4.y));
+          d1[2] = fmax3(fmax3(a0.z, a1.z, a2.z), fmax3(a3.z, a4.z, b0.z),
+                        fmax3(fmax3(b1.z, l4.z, r4.z), u4.z, d4.z));
+          d1[3] = fmax3(fmax3(a0.w, a1.w, a2.w), fmax3(a3.w, a4.w, b0.w),
+                        fmax3(fmax3(b1.w, l4.w, r4.w), u4.w, d4.w));
+        }
+        const float bound = w1 * ub[(i / R) * G::QX + (4 * g) / R];
+        float v[4];
+        unsigned m = 0;  // outputs of this thread that need the class walk
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          v[t] = w0 * d1[t];
+          if (dq && v[t] < bound) m |= 1u << t;
+        }
+        if (dq) *reinterpret_cast<float4 *>(ot + i * TW + 4 * g) = make_float4(v[0], v[1], v[2], v[3]);
+        if (__any_sync(0xFFFFFFFFu, m != 0u)) {
+          const unsigned lt = (1u << lane) - 1u;
+          int pos = nlist;
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const unsigned b = __ballot_sync(0xFFFFFFFFu, m & (1u << t));
+            if (m & (1u << t)) wlist[pos + __popc(b & lt)] = (uint16_t)(i * TW + 4 * g + t);
+            pos += __popc(b);
+          }
+          nlist = pos;
+        }
+      }
+    }
+    if (lane == 0) wcnt[warp] = nlist;
+    __syncthreads();
+    // ---- P3: the listed outputs (all warps' lists, shared out evenly) walk
+    // the remaining classes under the bound
+    {
+      int pre[NWARP + 1];
+      pre[0] = 0;
+#pragma unroll
+      for (int w = 0; w < NWARP; ++w) pre[w + 1] = pre[w] + wcnt[w];
+      const int ns = pre[NWARP];
+      for (int base = tid - lane; base < ns; base += NT) {
+        const int s = base + lane;
+        const bool in_list = s < ns;
+        int at = s;  // position in the segmented list: skip the unused tails
+#pragma unroll
+        for (int w = 1; w < NWARP; ++w)
+          if (s >= pre[w]) at += WSEG - (pre[w] - pre[w - 1]);
+        const int idx = in_list ? slist[at] : 0;
+        const int i = idx / TW, x = idx - i * TW;
+        const int yc = i + R;
+        float d1;  // the disk max again, from the planes (as P2)
+        if constexpr (R == 4) {
+          const float *cc = ci + yc * G::CW + x + R;
+          d1 = fmax3(fmax3(planes[(yc - 1) * TW + x], planes[yc * TW + x], planes[(yc + 1) * TW + x]),
+                     fmax3(cc[-2], cc[2], cc[-2 * G::CW]), cc[2 * G::CW]);
+        } else {
+          const float *h3 = planes + x, *h2 = planes + G::PLANE + x;
+          const float *cc = ci + yc * G::CW + x + R;
+          d1 = fmax3(fmax3(h3[(yc - 2) * TW], h3[(yc - 1) * TW], h3[yc * TW]),
+                     fmax3(h3[(yc + 1) * TW], h3[(yc + 2) * TW], h2[(yc - 3) * TW]),
+                     fmax3(fmax3(h2[(yc + 3) * TW], cc[-4], cc[4]), cc[-4 * G::CW], cc[4 * G::CW]));
+        }
+        float acc = w0 * d1;
+        const float U = ub[(i / R) * G::QX + x / R];
+        slow_classes<R, G::CW, 1>(ci + yc * G::CW + (x + R), U, in_list, acc);
+        if (in_list) ot[idx] = acc;
+      }
+    }
+    __syncthreads();
+    // ---- P4: store the output tile (every output, every slice)
+    {
+      float *out = cost + (int64_t)k * cells;
+      for (int idx = tid; idx < TH * TW; idx += NT) {
+        const int i = idx / TW, x = idx - i * TW;
+        if (i0 + i < rows && j0 + x < cols) out[(int64_t)(i0 + i) * cols + (j0 + x)] = ot[idx];
+      }
+    }
+    // the next step's first barrier orders P4's reads of `ot` before its P2
+  }
+}
+
+// Host: the caller's kernel must have exactly the compiled class structure
+// (class 0 = DiskShape<R>, classes 1.. = BnbRings<R>, strictly decreasing
+// weights); on success cw = the class weights + a trailing 0.
+template <int R>
+bool bnb_tables(const float *w, int kside, std::vector<float> &cw) {
+  using RG = BnbRings<R>;
+  using D = DiskShape<R>;
+  if (kside != 2 * R + 1) return false;
+  std::vector<float> vals;
+  for (int t = 0; t < kside * kside; ++t)
+    if (w[t] > 0.0f) vals.push_back(w[t]);
+  std::sort(vals.begin(), vals.end(), [](float a, float b) { return a > b; });
+  vals.erase(std::unique(vals.begin(), vals.end()), vals.end());
+  if ((int)vals.size() != RG::NCLS || RG::NCLS > kBnbMaxClasses) return false;
+  std::vector<int> cls(kside * kside, -1);  // compiled class of every tap
+  for (int m = 0; m < kside; ++m)
+    for (int n = 0; n < kside; ++n) {
+      const int a = std::abs(m - R), b = std::abs(n - R);
+      if (a <= D::A && D::h[a] >= b) cls[m * kside + n] = 0;
+    }
+  for (int c = 1; c < RG::NCLS; ++c)
+    for (int t = RG::start(c); t < RG::start(c + 1); ++t)
+      cls[(RG::dy(t) + R) * kside + (RG::dx(t) + R)] = c;
+  for (int t = 0; t < kside * kside; ++t) {
+    const int want = w[t] > 0.0f ? (int)(std::find(vals.begin(), vals.end(), w[t]) - vals.begin()) : -1;
+    if (cls[t] != want) return false;
+  }
+  cw.assign(vals.begin(), vals.end());
+  cw.push_back(0.0f);
+  return true;
+}

@@ -372,6 +372,7 @@ __global__ void __launch_bounds__(NT, MINB) eval_fast_kernel(const float *__rest
 
 #include "k_eval_incr.cuh"
 #include "k_eval_split.cuh"
+#include "k_eval_bnb.cuh"
 
 // ---------------------------------------------------------- generic kernel
 struct TileGeom {
@@ -606,13 +607,22 @@ int launch_incr_t(pct_ctx *ctx, const float *ground, const float *ceiling, int S
 }
 
 // two-kernel evaluation (k_eval_split.cuh): per-cell slice walk, then tiled
-// foothold resolution + inflation; intermediates in the context scratch
-template <int R, int PR>
+// foothold resolution + inflation; intermediates in the context scratch.
+// Inflation: the branch-and-bound kernel (k_eval_bnb.cuh) when the kernel's
+// weight classes fit its compiled disk (PCT_INFL=sym keeps the full-tap TMA
+// kernel for R <= 4), else the full-tap TMA kernel (R <= 4 only).
+template <int R, int PR, int TH, int TW, int BNT = 256>
 int launch_split(pct_ctx *ctx, const float *ground, const float *ceiling, int S, int rows,
-                 int cols, float *cost) {
-  constexpr int TH = 64, TW = 64;
+                 int cols, const float *kernel_w, int kside, float *cost, bool bnb) {
   const int64_t cells = (int64_t)rows * cols;
   const int64_t words = (cells + 31) / 32 + 1;
+  std::vector<float> bw;
+  if constexpr (R == 4 || R == 8) {
+    if (bnb && !bnb_tables<R>(kernel_w, kside, bw)) bnb = false;
+  } else {
+    bnb = false;
+  }
+  if (!bnb && R > 4) return fail(ctx, PCT_E_INVALID, "split evaluation needs the bnb tables for R > 4");
   EncLayout L;
   L.padr = R;
   L.padc = R;
@@ -634,11 +644,11 @@ int launch_split(pct_ctx *ctx, const float *ground, const float *ceiling, int S,
     ctx->enc_tag[0] = -1;
   }
   float *enc = static_cast<float *>(ctx->enc);
-  const int64_t tag[4] = {S, rows, cols, R};
-  if (!std::equal(tag, tag + 4, ctx->enc_tag)) {  // new layout: clear its padding once
+  const int64_t tag[6] = {S, rows, cols, R, TH, TW};
+  if (!std::equal(tag, tag + 6, ctx->enc_tag)) {  // new layout: clear its padding once
     zero_pads_kernel<<<dim3((unsigned)L.prows, S), 128, 0, ctx->stream>>>(enc, L, rows, cols);
     if (int rc = check_launch(ctx, "zero_pads_kernel")) return rc;
-    std::copy(tag, tag + 4, ctx->enc_tag);
+    std::copy(tag, tag + 6, ctx->enc_tag);
   }
   const unsigned g1 = (unsigned)((cells + kWalkNT - 1) / kWalkNT);
   const char *pf = getenv("PCT_WALK_PF");
@@ -654,7 +664,7 @@ int launch_split(pct_ctx *ctx, const float *ground, const float *ceiling, int S,
                                                            L, bits, words);
   if (int rc = check_launch(ctx, "terrain_walk_kernel")) return rc;
   const char *tma = getenv("PCT_TMA");
-  if (!(tma && tma[0] == '0') && R % 4 == 0) {
+  if (bnb || (!(tma && tma[0] == '0') && R % 4 == 0)) {
     // persistent TMA-pipelined resolve + inflate: a 3-D tensor map over the
     // padded stacks, box = one c_init tile + halo
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
@@ -666,49 +676,101 @@ int launch_split(pct_ctx *ctx, const float *ground, const float *ceiling, int S,
         return fail(ctx, PCT_E_CUDA, "cuTensorMapEncodeTiled unavailable");
       encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
     }
-    using TG = TmaGeom<R, PR, TH, TW>;
+    constexpr int CH = TH + 2 * R, CW = TW + 2 * R;
     CUtensorMap map;
     const cuuint64_t dims[3] = {(cuuint64_t)L.pitch, (cuuint64_t)L.prows, (cuuint64_t)S};
     const cuuint64_t strides[2] = {(cuuint64_t)L.pitch * 4, (cuuint64_t)L.sstride * 4};
-    const cuuint32_t box[3] = {(cuuint32_t)TG::CW, (cuuint32_t)TG::CH, 1};
+    const cuuint32_t box[3] = {(cuuint32_t)CW, (cuuint32_t)CH, 1};
     const cuuint32_t estr[3] = {1, 1, 1};
     if (encode(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, enc, dims, strides, box, estr,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return fail(ctx, PCT_E_CUDA, "cuTensorMapEncodeTiled failed");
-    auto kt = resolve_inflate_tma_kernel<R, PR, TH, TW, kNT, 3>;
-    constexpr int tsmem = TG::SMEM;
-    PCT_CUDA(ctx, cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, tsmem));
-    int per_sm = 0;
-    PCT_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kt, kNT, tsmem));
     const int64_t items = (int64_t)((cols + TW - 1) / TW) * ((rows + TH - 1) / TH) * S;
-    const unsigned grid = (unsigned)std::max<int64_t>(
-        1, std::min<int64_t>(items, (int64_t)std::max(1, per_sm) * ctx->num_sms));
-    kt<<<grid, kNT, tsmem, ctx->stream>>>(map, bits, rows, cols, S, words, cost);
-    return check_launch(ctx, "resolve_inflate_tma_kernel");
+    if (items > INT32_MAX) return fail(ctx, PCT_E_INVALID, "grid too large");
+    if constexpr (R == 4 || R == 8) {
+     if (bnb) {
+      PCT_CUDA(ctx, cudaMemcpyToSymbolAsync(c_bw, bw.data(), bw.size() * sizeof(float), 0,
+                                            cudaMemcpyHostToDevice, ctx->stream));
+      auto kb = resolve_inflate_bnb_kernel<R, PR, TH, TW, BNT, 1>;
+      constexpr int bsmem = BnbGeom<R, PR, TH, TW>::SMEM;
+      PCT_CUDA(ctx, cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, bsmem));
+      int per_sm = 0;
+      PCT_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kb, BNT, bsmem));
+      const int64_t slots = (int64_t)std::max(1, per_sm) * ctx->num_sms;
+      // slices per work item: long runs reuse the previous slice (only the
+      // first slice of a run is computed in full); shorter when the grid
+      // would otherwise not get ~2 items per resident CTA
+      const int64_t tiles = (int64_t)((cols + TW - 1) / TW) * ((rows + TH - 1) / TH);
+      int run = S;
+      while (run > 4 && tiles * ((S + run - 1) / run) < 2 * slots) run = (run + 1) / 2;
+      if (const char *e = getenv("PCT_INFL_RUN")) run = std::max(1, atoi(e));
+      run = std::min(run, S);
+      const int64_t nitems = tiles * ((S + run - 1) / run);
+      if (nitems > INT32_MAX) return fail(ctx, PCT_E_INVALID, "grid too large");
+      const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nitems, slots));
+      kb<<<grid, BNT, bsmem, ctx->stream>>>(map, bits, rows, cols, S, run, words, cost);
+      return check_launch(ctx, "resolve_inflate_bnb_kernel");
+     }
+    }
+    if constexpr (R <= 4 && R % 4 == 0) {
+      using TG = TmaGeom<R, PR, TH, TW>;
+      auto kt = resolve_inflate_tma_kernel<R, PR, TH, TW, kNT, 3>;
+      constexpr int tsmem = TG::SMEM;
+      PCT_CUDA(ctx, cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, tsmem));
+      int per_sm = 0;
+      PCT_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kt, kNT, tsmem));
+      const unsigned grid = (unsigned)std::max<int64_t>(
+          1, std::min<int64_t>(items, (int64_t)std::max(1, per_sm) * ctx->num_sms));
+      kt<<<grid, kNT, tsmem, ctx->stream>>>(map, bits, rows, cols, S, words, cost);
+      return check_launch(ctx, "resolve_inflate_tma_kernel");
+    }
   }
-  auto kern = resolve_inflate_kernel<R, PR, TH, TW, kNT, 3>;
-  constexpr int smem = SplitGeom<R, PR, TH, TW>::SMEM;
-  PCT_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  dim3 grid((cols + TW - 1) / TW, (rows + TH - 1) / TH, S);
-  kern<<<grid, kNT, smem, ctx->stream>>>(enc, L, bits, rows, cols, words, cost);
-  return check_launch(ctx, "resolve_inflate_kernel");
+  if constexpr (R <= 4) {
+    auto kern = resolve_inflate_kernel<R, PR, TH, TW, kNT, 3>;
+    constexpr int smem = SplitGeom<R, PR, TH, TW>::SMEM;
+    PCT_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    dim3 grid((cols + TW - 1) / TW, (rows + TH - 1) / TH, S);
+    kern<<<grid, kNT, smem, ctx->stream>>>(enc, L, bits, rows, cols, words, cost);
+    return check_launch(ctx, "resolve_inflate_kernel");
+  }
+  return fail(ctx, PCT_E_INVALID, "no resolve/inflate kernel for this radius");
 }
 
-// Kernel choice for symmetric kernels with compiled geometry: R <= 4 uses
-// the two-kernel split by default; PCT_EVAL_KERNEL=fast selects the fused
-// per-slice kernel and =incr the slice-incremental CTA kernel (kept as
-// measured alternatives; PCT_EVAL_TILE / PCT_EVAL_RUN tune
-// it).  R = 8 uses the fused per-slice kernel with split inflation roles.
+// Kernel choice for symmetric kernels with compiled geometry: the two-kernel
+// split by default (R = 8 only when the bnb tables fit); PCT_EVAL_KERNEL=fast
+// selects the fused per-slice kernel and =incr (R <= 4) the slice-incremental
+// CTA kernel (kept as measured alternatives; PCT_EVAL_TILE /
+// PCT_EVAL_RUN tune it).
 template <int R, int PR>
 int launch_fast(pct_ctx *ctx, const float *ground, const float *ceiling, int S, int rows,
-                int cols, float *cost) {
+                int cols, const float *kernel_w, int kside, float *cost) {
+  const char *m = getenv("PCT_EVAL_KERNEL");
+  const char *infl = getenv("PCT_INFL");
+  const char *tile = getenv("PCT_BNB_TILE");
+  const bool alt = tile && tile[0] == '1';
+  std::vector<float> bw;
+  bool bnb = false;
+  if constexpr (R == 4 || R == 8) bnb = !(infl && infl[0] == 's') && bnb_tables<R>(kernel_w, kside, bw);
+  if (!m || m[0] == 's') {
+    // default: the two-kernel split (terrain walk + resolve/inflate)
+    if constexpr (R == 4) {
+      if (bnb && alt)
+        return launch_split<R, PR, 32, 64, 128>(ctx, ground, ceiling, S, rows, cols, kernel_w, kside, cost, true);
+      if (bnb)
+        return launch_split<R, PR, 32, 32, 128>(ctx, ground, ceiling, S, rows, cols, kernel_w, kside, cost, true);
+    }
+    if constexpr (R == 8) {
+      if (bnb && alt)
+        return launch_split<R, PR, 64, 32, 256>(ctx, ground, ceiling, S, rows, cols, kernel_w, kside, cost, true);
+      if (bnb)
+        return launch_split<R, PR, 32, 32, 128>(ctx, ground, ceiling, S, rows, cols, kernel_w, kside, cost, true);
+    }
+    if constexpr (R <= 4)
+      return launch_split<R, PR, 64, 64>(ctx, ground, ceiling, S, rows, cols, kernel_w, kside, cost, false);
+  }
   if constexpr (R <= 4) {
-    // default: the two-kernel split (cfg1: 258 us vs 296 incremental vs 386
-    // per-slice; cfg0: 43 vs 52 us)
-    const char *m = getenv("PCT_EVAL_KERNEL");
-    if (!m || m[0] == 's') return launch_split<R, PR>(ctx, ground, ceiling, S, rows, cols, cost);
-    if (m[0] == 'i' && S > 1) {
+    if (m && m[0] == 'i' && S > 1) {
       const char *t = getenv("PCT_EVAL_TILE");
       if (t && atoi(t) == 64)
         return launch_incr_t<R, PR, 64, 64, 256, 2>(ctx, ground, ceiling, S, rows, cols, cost);
@@ -776,15 +838,15 @@ int launch_evaluate(pct_ctx *ctx, const float *ground, const float *ceiling, int
                                             cudaMemcpyHostToDevice, ctx->stream));
   }
   if (sym && R == 4 && p.patch_radius == 3)  // r_g = 0.1 with the Table-I radii
-    return launch_fast<4, 3>(ctx, ground, ceiling, S, rows, cols, cost);
+    return launch_fast<4, 3>(ctx, ground, ceiling, S, rows, cols, kernel_w, kside, cost);
   if (sym && R == 2 && p.patch_radius == 2)  // r_g = 0.2
-    return launch_fast<2, 2>(ctx, ground, ceiling, S, rows, cols, cost);
+    return launch_fast<2, 2>(ctx, ground, ceiling, S, rows, cols, kernel_w, kside, cost);
   if (sym && R == 3 && p.patch_radius == 3)
-    return launch_fast<3, 3>(ctx, ground, ceiling, S, rows, cols, cost);
+    return launch_fast<3, 3>(ctx, ground, ceiling, S, rows, cols, kernel_w, kside, cost);
   if (sym && R == 4 && p.patch_radius == 4)
-    return launch_fast<4, 4>(ctx, ground, ceiling, S, rows, cols, cost);
+    return launch_fast<4, 4>(ctx, ground, ceiling, S, rows, cols, kernel_w, kside, cost);
   if (sym && R == 8 && p.patch_radius == 6)  // r_g = 0.05 with the Table-I radii
-    return launch_fast<8, 6>(ctx, ground, ceiling, S, rows, cols, cost);
+    return launch_fast<8, 6>(ctx, ground, ceiling, S, rows, cols, kernel_w, kside, cost);
   // generic path: pick the largest square-ish tile that fits in shared memory
   int TH = 64, TW = 64;
   TileGeom G = make_geom(R, p.patch_radius, TH, TW);

@@ -32,7 +32,7 @@ struct pct_ctx {
   // is cleared only when the layout changes (the interior is rewritten)
   void *enc = nullptr;
   size_t enc_bytes = 0;
-  int64_t enc_tag[4] = {-1, -1, -1, -1};  // S, rows, cols, R of the cleared layout
+  int64_t enc_tag[6] = {-1, -1, -1, -1, -1, -1};  // S, rows, cols, R, tile h, w of the cleared layout
   // optional stage events of pct_tomo_run (pct_set_timing)
   bool timing = false;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};

@@ -80,6 +80,43 @@ def test_incremental_runs_match_full_kernel(golden, monkeypatch, run):
         assert digest(inc[k]) == case["cost_slice_sha256"][k]
 
 
+@pytest.mark.parametrize("name,env", [("synth_cfg0", {"PCT_INFL": "sym"}),
+                                      ("synth_cfg0", {}),
+                                      ("ref_random_multilayer_s9", {}),
+                                      ("synth_cfg2_n2000000", {})])
+def test_split_paths_match_fused_kernel(golden, monkeypatch, name, env):
+    """The two-kernel split (terrain walk + branch-and-bound or full-tap
+    inflation) gives the same bytes as the fused per-slice kernel."""
+    case = golden["cases"][name]
+    tom = pct.build_tomogram(pct.PointCloud(case_input(name, case)), case["d_s"], case["r_g"])
+    monkeypatch.setenv("PCT_EVAL_KERNEL", "fast")
+    full = pct.evaluate_tomogram(tom, pct.TravParams()).cost_stack()
+    monkeypatch.setenv("PCT_EVAL_KERNEL", "split")
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    got = pct.evaluate_tomogram(tom, pct.TravParams()).cost_stack()
+    assert np.array_equal(full.view(np.uint32), got.view(np.uint32))
+
+
+@pytest.mark.parametrize("r_g,d_inf,d_sm,patch", [(0.1, 0.2, 0.4, None), (0.05, 0.2, 0.4, None),
+                                                  (0.1, 0.25, 0.4, None), (0.05, 0.25, 0.4, None),
+                                                  (0.1, 0.2, 0.4, 4)])
+def test_inflation_kernels_vs_oracle_random_costs(r_g, d_inf, d_sm, patch):
+    """Branch-and-bound inflation (and its full-tap fallback for kernels
+    whose weight-1 disk differs from the compiled one) on random scenes with
+    non-default inflation radii, against the oracle."""
+    rng = np.random.default_rng(int(r_g * 1000 + d_inf * 100))
+    n = 80_000
+    xyz = np.column_stack([rng.uniform(0, 9, n), rng.uniform(0, 7, n),
+                           rng.uniform(0, 2.5, n)])
+    params = pct.TravParams(d_inf=d_inf, d_sm=d_sm, step_patch_radius=patch)
+    ref = oracle.build(xyz, 0.5, r_g)
+    tom = pct.build_tomogram(pct.PointCloud(xyz), 0.5, r_g)
+    got = pct.evaluate_tomogram(tom, params).cost_stack()
+    want = oracle.evaluate(ref["ground"], ref["ceiling"], r_g, params)
+    _assert_layers_equal(got, want, "cost")
+
+
 def test_f32_and_f64_inputs_agree(golden):
     case = golden["cases"]["synth_cfg0"]
     xyz = case_input("synth_cfg0", case)
