@@ -271,24 +271,12 @@ __global__ void __launch_bounds__(NT, MINB) resolve_inflate_bnb_kernel(
     // ---- P0a: gentle bits of the window region (bit x of word w = gentle
     // column 32w + x, gentle column 0 = c_init column -r); resets
     const uint32_t *bk = bits_in + (int64_t)k * words;
+    const int wpr = (cols + 31) / 32;
     for (int idx = tid; idx < G::GH * G::GWW; idx += NT) {
       const int y = idx / G::GWW, w = idx - y * G::GWW;
       const int gi = i0 - R - PR + y;
       const int gj = j0 - R - PR + 32 * w;
-      uint32_t word = 0;
-      if (gi >= 0 && gi < rows && gj < cols && gj + 32 > 0) {
-        const int64_t bit = (int64_t)gi * cols + gj;
-        const int64_t wi = bit >> 5;
-        const int sh = (int)(bit & 31);
-        const uint32_t lo = (wi >= 0 && wi < words) ? __ldg(bk + wi) : 0u;
-        const uint32_t hi = (wi + 1 >= 0 && wi + 1 < words) ? __ldg(bk + wi + 1) : 0u;
-        word = (uint32_t)((((uint64_t)hi << 32) | lo) >> sh);
-        const int first_b = gj < 0 ? -gj : 0;
-        const int last = cols - gj < 32 ? cols - gj : 32;
-        const uint32_t mhi = last >= 32 ? 0xFFFFFFFFu : ((1u << last) - 1u);
-        const uint32_t mlo = first_b >= 32 ? 0u : (0xFFFFFFFFu << first_b);
-        word &= mhi & mlo;
-      }
+      uint32_t word = gentle_word(bk, wpr, gi, gj, rows, cols);
       if (32 * w >= G::GW) word = 0;
       else if (G::GW - 32 * w < 32) word &= (1u << (G::GW - 32 * w)) - 1u;
       bits[idx] = word;

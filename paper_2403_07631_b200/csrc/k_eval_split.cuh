@@ -49,83 +49,119 @@ __global__ void __launch_bounds__(128) zero_pads_kernel(float *__restrict__ enc,
   }
 }
 
+// Gentle bitmap layout: per slice, rows of wpr = ceil(cols / 32) words; bit
+// b of word w of row i = cell (i, 32 w + b).  gentle_word returns the 32 bits
+// of row gi starting at column gj (any gj; 0 outside the map).
+__device__ __forceinline__ uint32_t gentle_word(const uint32_t *__restrict__ bk, int wpr, int gi,
+                                                int gj, int rows, int cols) {
+  if (gi < 0 || gi >= rows || gj >= cols || gj + 32 <= 0) return 0u;
+  const uint32_t *row = bk + (int64_t)gi * wpr;
+  const int w = gj >> 5, sh = gj & 31;  // floor division: w >= -1
+  const uint32_t lo = w >= 0 ? __ldg(row + w) : 0u;
+  const uint32_t hi = (sh != 0 && w + 1 < wpr) ? __ldg(row + w + 1) : 0u;
+  return sh ? __funnelshift_r(lo, hi, sh) : lo;  // bits past cols are 0 in the map
+}
+
+// Terrain walk: one thread per cell (flat row-major index, so a warp is 32
+// consecutive cells) walks the slices bottom-up.  The float64 terrain
+// arithmetic runs only when the cell's 5-point cross changed since the slice
+// below, the interval / fuse step only when the cross or the ceiling did.
+// Loads run PF slices ahead; left / right neighbours come from the adjacent
+// lanes (lanes 0 and 31 load the cell beyond), grid borders read NaN.
 template <int PF>
 __global__ void __launch_bounds__(kWalkNT) terrain_walk_kernel(
     const float *__restrict__ ground, const float *__restrict__ ceiling, int S, int rows,
     int cols, float *__restrict__ enc_out, EncLayout L, uint32_t *__restrict__ bits_out,
-    int64_t words) {
+    int wpr) {
   const int64_t cells = (int64_t)rows * cols;
-  const int64_t cell = (int64_t)blockIdx.x * kWalkNT + threadIdx.x;  // warps = aligned 32-cell words
-  const bool live = cell < cells;
-  const int i = live ? (int)(cell / cols) : 0;
-  const int j = live ? (int)(cell - (int64_t)i * cols) : 0;
+  // threads index row-padded columns: warp = one gentle-bitmap word of one row
+  const int64_t pidx = (int64_t)blockIdx.x * kWalkNT + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int pcols = wpr * 32;
+  const int i0_ = (int)(pidx / pcols), j0_ = (int)(pidx - (int64_t)i0_ * pcols);
+  const bool live = i0_ < rows && j0_ < cols;
+  const int i = i0_ < rows ? i0_ : rows - 1;
+  const int j = j0_ < cols ? j0_ : cols - 1;  // clamped: address formation only
+  const bool wlead = lane == 0 && i0_ < rows;
   const bool hl = live && j > 0, hr = live && j + 1 < cols, hu = live && i > 0,
              hd = live && i + 1 < rows;
+  const bool edge_l = lane == 0 && hl, edge_r = lane == 31 && hr;
   const float nanf_ = bits_f32(kNaNBits);
   const float cb32 = (float)c_K.c_barrier;
+  const int64_t base = (int64_t)i * cols + j;
+  const float *pg = ground + base;
+  const float *pc = ceiling + base;
+  float *pe = enc_out + L.at(0, i, j);
+  uint32_t *pb = bits_out + (int64_t)i * wpr + (j0_ >> 5);
 
-  // prefetch ring: the 5-point cross and the ceiling of the next PF slices
-  float pe[PF], pl[PF], pr[PF], pu[PF], pd[PF], pc[PF];
-  auto fetch = [&](int k, int s) {
-    const float *gk = ground + (int64_t)k * cells;
-    pe[s] = live ? __ldg(gk + cell) : nanf_;
-    pl[s] = hl ? __ldg(gk + cell - 1) : nanf_;
-    pr[s] = hr ? __ldg(gk + cell + 1) : nanf_;
-    pu[s] = hu ? __ldg(gk + cell - cols) : nanf_;
-    pd[s] = hd ? __ldg(gk + cell + cols) : nanf_;
-    pc[s] = live ? __ldg(ceiling + (int64_t)k * cells + cell) : nanf_;
+  float qe[PF], qu[PF], qd[PF], qc[PF], ql[PF], qr[PF];
+  auto fetch = [&](const float *g, const float *c, int s) {
+    qe[s] = live ? __ldg(g) : nanf_;
+    qu[s] = hu ? __ldg(g - cols) : nanf_;
+    qd[s] = hd ? __ldg(g + cols) : nanf_;
+    qc[s] = live ? __ldg(c) : nanf_;
+    ql[s] = edge_l ? __ldg(g - 1) : nanf_;
+    qr[s] = edge_r ? __ldg(g + 1) : nanf_;
   };
 #pragma unroll
   for (int s = 0; s < PF; ++s)
-    if (s < S) fetch(s, s);
+    if (s < S) fetch(pg + s * cells, pc + s * cells, s);
+  const float *ng = pg + PF * cells, *nc = pc + PF * cells;
 
   uint32_t xe = 0, xl = 0, xr = 0, xu = 0, xd = 0, xc = 0;  // previous slice's input bits
   float tenc = nanf_;  // terrain part: NaN = no ground, sign bit = foothold branch
   bool gentle = false;
   float enc = 0.0f;
-  for (int k = 0; k < S; ++k) {
-    const int s = k % PF;
-    float e, l, r, u, d, c;
+  for (int k0 = 0; k0 < S; k0 += PF) {
 #pragma unroll
-    for (int q = 0; q < PF; ++q)
-      if (q == s) {
-        e = pe[q]; l = pl[q]; r = pr[q]; u = pu[q]; d = pd[q]; c = pc[q];
+    for (int s = 0; s < PF; ++s) {
+      const int k = k0 + s;
+      if (k >= S) break;
+      const float e = qe[s], u = qu[s], d = qd[s], c = qc[s];
+      float l = __shfl_up_sync(0xFFFFFFFFu, e, 1);
+      float r = __shfl_down_sync(0xFFFFFFFFu, e, 1);
+      if (lane == 0) l = ql[s];
+      if (lane == 31) r = qr[s];
+      if (!hl) l = nanf_;
+      if (!hr) r = nanf_;
+      if (k + PF < S) {
+        fetch(ng, nc, s);
+        ng += cells;
+        nc += cells;
       }
-    if (k + PF < S) {
-#pragma unroll
-      for (int q = 0; q < PF; ++q)
-        if (q == s) fetch(k + PF, q);
-    }
-    const bool xch = k == 0 || f32_bits(e) != xe || f32_bits(l) != xl || f32_bits(r) != xr ||
-                     f32_bits(u) != xu || f32_bits(d) != xd;
-    if (xch && live) {
-      const FastCell t = fast_terrain(Cross{e, l, r, u, d}, c_K);
-      gentle = t.gentle;
-      if (!t.valid) {
-        tenc = nanf_;
-      } else if (t.isolated || t.m_xy > c_K.theta_b) {
-        tenc = cb32;
-      } else if (t.gentle) {
-        tenc = gentle_cost32(t.gx, t.gy, t.s, c_K);
-      } else {
-        const double q = div_const(t.m_xy, c_K.theta_b, c_K.inv_theta_b);
-        tenc = bits_f32(f32_bits((float)(c_K.alpha_b * (q * q))) | 0x80000000u);
+      const bool xch = k == 0 || f32_bits(e) != xe || f32_bits(l) != xl || f32_bits(r) != xr ||
+                       f32_bits(u) != xu || f32_bits(d) != xd;
+      if (xch && live) {
+        const FastCell t = fast_terrain(Cross{e, l, r, u, d}, c_K);
+        gentle = t.gentle;
+        if (!t.valid) {
+          tenc = nanf_;
+        } else if (t.isolated || t.m_xy > c_K.theta_b) {
+          tenc = cb32;
+        } else if (t.gentle) {
+          tenc = gentle_cost32(t.gx, t.gy, t.s, c_K);
+        } else {
+          const double q = div_const(t.m_xy, c_K.theta_b, c_K.inv_theta_b);
+          tenc = bits_f32(f32_bits((float)(c_K.alpha_b * (q * q))) | 0x80000000u);
+        }
       }
-    }
-    if ((xch || f32_bits(c) != xc) && live) {
-      if (!finite32(tenc)) {
-        enc = cb32;  // no ground: barrier (fuse_costs :169)
-      } else {
-        const uint32_t tb = f32_bits(tenc);
-        enc = fuse_value(interval_value(e, c, c_K), bits_f32(tb & 0x7FFFFFFFu), c_K);
-        if (tb & 0x80000000u) enc = bits_f32(f32_bits(enc) | 0x80000000u);
+      if ((xch || f32_bits(c) != xc) && live) {
+        if (!finite32(tenc)) {
+          enc = cb32;  // no ground: barrier (fuse_costs :169)
+        } else {
+          const uint32_t tb = f32_bits(tenc);
+          enc = fuse_value(interval_value(e, c, c_K), bits_f32(tb & 0x7FFFFFFFu), c_K);
+          if (tb & 0x80000000u) enc = bits_f32(f32_bits(enc) | 0x80000000u);
+        }
       }
+      xe = f32_bits(e); xl = f32_bits(l); xr = f32_bits(r); xu = f32_bits(u); xd = f32_bits(d);
+      xc = f32_bits(c);
+      if (live) *pe = enc;
+      pe += L.sstride;
+      const unsigned word = __ballot_sync(0xFFFFFFFFu, live && gentle);
+      if (wlead) *pb = word;
+      pb += (int64_t)rows * wpr;
     }
-    xe = f32_bits(e); xl = f32_bits(l); xr = f32_bits(r); xu = f32_bits(u); xd = f32_bits(d);
-    xc = f32_bits(c);
-    if (live) enc_out[L.at(k, i, j)] = enc;
-    const unsigned b = __ballot_sync(0xFFFFFFFFu, live && gentle);
-    if ((threadIdx.x & 31) == 0 && (cell >> 5) < words) bits_out[(int64_t)k * words + (cell >> 5)] = b;
   }
 }
 
@@ -155,6 +191,7 @@ __global__ void __launch_bounds__(NT, MINB) resolve_inflate_kernel(
   const int k = blockIdx.z;
   const int i0 = blockIdx.y * TH, j0 = blockIdx.x * TW;
   const uint32_t *bk = bits_in + (int64_t)k * words;
+  const int wpr = (cols + 31) / 32;
   if (tid == 0) n_flagged = 0;
   __syncthreads();
 
@@ -202,20 +239,7 @@ __global__ void __launch_bounds__(NT, MINB) resolve_inflate_kernel(
     const int y = idx / G::GWW, w = idx - y * G::GWW;
     const int gi = i0 - R - PR + y;
     const int gj = j0 - R - PR + 32 * w;  // column of bit 0 of this word
-    uint32_t word = 0;
-    if (gi >= 0 && gi < rows && gj < cols && gj + 32 > 0) {
-      const int64_t bit = (int64_t)gi * cols + gj;  // may be < row start; masked below
-      const int64_t wi = bit >> 5;
-      const int sh = (int)(bit & 31);
-      const uint32_t lo = (wi >= 0 && wi < words) ? __ldg(bk + wi) : 0u;
-      const uint32_t hi = (wi + 1 >= 0 && wi + 1 < words) ? __ldg(bk + wi + 1) : 0u;
-      word = (uint32_t)((((uint64_t)hi << 32) | lo) >> sh);
-      const int first = gj < 0 ? -gj : 0;                // bits left of column 0
-      const int last = cols - gj < 32 ? cols - gj : 32;  // bits up to the last column
-      const uint32_t mhi = last >= 32 ? 0xFFFFFFFFu : ((1u << last) - 1u);
-      const uint32_t mlo = first >= 32 ? 0u : (0xFFFFFFFFu << first);
-      word &= mhi & mlo;
-    }
+    uint32_t word = gentle_word(bk, wpr, gi, gj, rows, cols);
     if (32 * w >= G::GW) word = 0;
     else if (G::GW - 32 * w < 32) word &= (1u << (G::GW - 32 * w)) - 1u;
     bits[idx] = word;
@@ -361,24 +385,12 @@ __global__ void __launch_bounds__(NT, MINB) resolve_inflate_tma_kernel(
     if (tid == 0) n_flagged = 0;
     // gentle bits of the window region (global bitmap -> smem), overlapping the TMA
     const uint32_t *bk = bits_in + (int64_t)k * words;
+    const int wpr = (cols + 31) / 32;
     for (int idx = tid; idx < G::GH * G::GWW; idx += NT) {
       const int y = idx / G::GWW, w = idx - y * G::GWW;
       const int gi = i0 - R - PR + y;
       const int gj = j0 - R - PR + 32 * w;
-      uint32_t word = 0;
-      if (gi >= 0 && gi < rows && gj < cols && gj + 32 > 0) {
-        const int64_t bit = (int64_t)gi * cols + gj;
-        const int64_t wi = bit >> 5;
-        const int sh = (int)(bit & 31);
-        const uint32_t lo = (wi >= 0 && wi < words) ? __ldg(bk + wi) : 0u;
-        const uint32_t hi = (wi + 1 >= 0 && wi + 1 < words) ? __ldg(bk + wi + 1) : 0u;
-        word = (uint32_t)((((uint64_t)hi << 32) | lo) >> sh);
-        const int first = gj < 0 ? -gj : 0;
-        const int last = cols - gj < 32 ? cols - gj : 32;
-        const uint32_t mhi = last >= 32 ? 0xFFFFFFFFu : ((1u << last) - 1u);
-        const uint32_t mlo = first >= 32 ? 0u : (0xFFFFFFFFu << first);
-        word &= mhi & mlo;
-      }
+      uint32_t word = gentle_word(bk, wpr, gi, gj, rows, cols);
       if (32 * w >= G::GW) word = 0;
       else if (G::GW - 32 * w < 32) word &= (1u << (G::GW - 32 * w)) - 1u;
       bits[idx] = word;
