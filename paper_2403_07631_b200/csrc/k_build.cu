@@ -173,6 +173,214 @@ __global__ void __launch_bounds__(256) scatter_kernel(const T *__restrict__ xyz,
   }
 }
 
+// -------------------------------------------- tile-partitioned build (T1-T4)
+// Alternative build for S <= kTileMaxS (PCT_BUILD=tiled).  Instead of S x cells scratch planes
+// per reduction (memset, scattered global atomics, a full scan pass), points
+// are partitioned by 16 x 16-cell tile and each tile is reduced in shared
+// memory:
+//   T1 tile_count: points per tile (warp-aggregated atomics)
+//   T2 tile_offsets: exclusive prefix sum (one block)
+//   T3 tile_scatter: one 8-byte record per point into its tile's range:
+//      key(f32 z) << 32 | bin << 8 | cell within the tile
+// Tiles are 8 rows x 32 columns (a warp stores whole 128-byte row segments);
+// T1 / T3 give each block a contiguous range of points, so that spatially
+// coherent inputs (scanner order) spread the tile counters over many tiles
+// at any moment instead of serialising all blocks on a few.
+//   T4 tile_reduce: one CTA per tile: shared-memory max / min per (bin, cell),
+//      then the per-cell bin scan writes the tile's ground / ceiling columns
+constexpr int kTBH = 8, kTBW = 32;  // tile rows x columns
+constexpr int kTB2 = kTBH * kTBW;    // cells per tile (8-bit local index)
+constexpr int kTileMaxS = 96;     // 2 x S x 256 x 4 B of shared memory
+constexpr int kTileNT = 256;
+
+// cell and bin of one point (tomogram.py:147-157): false when outside the band
+__device__ __forceinline__ bool point_cell_bin(double x, double y, double z, const BinArgs &a,
+                                               const double *hts, int &fi_out, int &fj_out,
+                                               int &b_out) {
+  const double fi = floor(div_const(y - a.y0, a.r_g, a.inv_rg) + 0.5) - (double)a.row0;
+  const double fj = floor(div_const(x - a.x0, a.r_g, a.inv_rg) + 0.5);
+  if (!(fi >= 0.0 && fi < (double)a.rows && fj >= 0.0 && fj < (double)a.cols)) return false;
+  double est = floor((z - a.z0) * a.inv_ds);  // estimate only; fixed up exactly below
+  int b = est < 0.0 ? 0 : (est > (double)a.S ? a.S : (int)est);
+  while (b > 0 && hts[b - 1] >= z) --b;
+  while (b < a.S && hts[b] < z) ++b;
+  fi_out = (int)fi;
+  fj_out = (int)fj;
+  b_out = b;
+  return true;
+}
+
+// T1 / T3: every batch of 256 points (one per thread) is merged per tile in
+// a shared-memory hash table, so a tile costs one global atomic per batch
+// however many of the batch's points it holds (scanner-ordered inputs put
+// whole batches into one tile: pillars, walls).
+constexpr int kPPT = 1;      // points per thread per batch (4 measured slower)
+constexpr int kHash = 512;   // slots (power of 2, >= 2 x batch)
+constexpr int kCtrPad = 32;  // tile counters / cursors: one per 128-byte line
+template <typename T, bool SCATTER>
+__global__ void __launch_bounds__(256) tile_pass_kernel(const T *__restrict__ xyz, int64_t n,
+                                                        BinArgs a, int ntx,
+                                                        unsigned *__restrict__ counter,
+                                                        unsigned long long *__restrict__ recs,
+                                                        unsigned long long *outside) {
+  extern __shared__ double hsm[];
+  __shared__ int h_tile[kHash];
+  __shared__ unsigned h_cnt[kHash];
+  const bool staged = a.S <= kMaxStagedHeights;
+  if (staged)
+    for (int k = threadIdx.x; k < a.S; k += blockDim.x) hsm[k] = a.heights[k];
+  for (int h = threadIdx.x; h < kHash; h += blockDim.x) {
+    h_tile[h] = -1;
+    h_cnt[h] = 0u;
+  }
+  __syncthreads();
+  const double *hts = staged ? hsm : a.heights;
+  constexpr int BATCH = 256 * kPPT;
+  const int64_t chunk = ((n + gridDim.x - 1) / gridDim.x + BATCH - 1) / BATCH * BATCH;
+  const int64_t p0 = (int64_t)blockIdx.x * chunk;
+  const int64_t p1 = p0 + chunk < n ? p0 + chunk : n;
+  for (int64_t pb = p0; pb < p1; pb += BATCH) {  // block-uniform trip count
+    int slot[kPPT], fi[kPPT], fj[kPPT], bin[kPPT];
+    unsigned rank[kPPT];
+    float z32[kPPT];
+#pragma unroll
+    for (int u = 0; u < kPPT; ++u) {
+      const int64_t p = pb + u * 256 + threadIdx.x;  // coalesced per u
+      bool in = false;
+      slot[u] = -1;
+      if (p < p1) {
+        const double x = (double)__ldg(xyz + 3 * p);
+        const double y = (double)__ldg(xyz + 3 * p + 1);
+        const double z = (double)__ldg(xyz + 3 * p + 2);
+        in = point_cell_bin(x, y, z, a, hts, fi[u], fj[u], bin[u]);
+        z32[u] = __double2float_rn(z);
+        if (!in && !SCATTER) atomicAdd(outside, 1ull);
+      }
+      if (in) {
+        const int tile = (fi[u] / kTBH) * ntx + fj[u] / kTBW;
+        int sl = (int)(((unsigned)tile * 2654435761u) >> 20) & (kHash - 1);
+        while (true) {
+          const int prev = atomicCAS(&h_tile[sl], -1, tile);
+          if (prev == -1 || prev == tile) break;
+          sl = (sl + 1) & (kHash - 1);
+        }
+        slot[u] = sl;
+        rank[u] = atomicAdd(&h_cnt[sl], 1u);
+      }
+    }
+    __syncthreads();
+    // one global atomic per occupied slot; the slot count becomes its base
+    for (int h = threadIdx.x; h < kHash; h += blockDim.x) {
+      const int tl = h_tile[h];
+      if (tl >= 0) {
+        // one counter per 128-byte line: atomics on neighbouring tiles do not
+        // serialise in one L2 line
+        if (SCATTER) h_cnt[h] = atomicAdd(counter + (int64_t)tl * kCtrPad, h_cnt[h]);
+        else atomicAdd(counter + (int64_t)tl * kCtrPad, h_cnt[h]);  // RED
+      }
+    }
+    __syncthreads();
+    if (SCATTER) {
+#pragma unroll
+      for (int u = 0; u < kPPT; ++u)
+        if (slot[u] >= 0) {
+          const unsigned pos = h_cnt[slot[u]] + rank[u];
+          const unsigned local = (unsigned)((fi[u] % kTBH) * kTBW + fj[u] % kTBW);
+          recs[pos] = ((unsigned long long)f32_key(z32[u]) << 32) |
+                      ((unsigned long long)bin[u] << 8) | local;
+        }
+    }
+    __syncthreads();
+    for (int h = threadIdx.x; h < kHash; h += blockDim.x) {
+      h_tile[h] = -1;
+      h_cnt[h] = 0u;
+    }
+    __syncthreads();
+  }
+}
+
+// exclusive prefix sum of the n (padded) tile counts in one block, 1024
+// tiles per step (coalesced); offs[n] = total.  The cursors (padded) are the
+// copy T3 advances.
+__global__ void __launch_bounds__(1024) tile_offsets_kernel(const unsigned *__restrict__ cnt,
+                                                            int n, unsigned *__restrict__ offs,
+                                                            unsigned *__restrict__ cursor) {
+  __shared__ unsigned wsum[32];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  unsigned carry = 0;
+  for (int c0 = 0; c0 < n; c0 += 1024) {
+    const int i = c0 + t;
+    const unsigned v = i < n ? cnt[(int64_t)i * kCtrPad] : 0u;
+    unsigned x = v;  // inclusive warp scan
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const unsigned y = __shfl_up_sync(0xFFFFFFFFu, x, d);
+      if (lane >= d) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      unsigned w = wsum[lane];
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const unsigned y = __shfl_up_sync(0xFFFFFFFFu, w, d);
+        if (lane >= d) w += y;
+      }
+      wsum[lane] = w;  // inclusive over warps
+    }
+    __syncthreads();
+    const unsigned excl = carry + (warp ? wsum[warp - 1] : 0u) + x - v;
+    if (i < n) {
+      offs[i] = excl;
+      cursor[(int64_t)i * kCtrPad] = excl;
+    }
+    carry += wsum[31];
+    __syncthreads();
+  }
+  if (t == 0) offs[n] = carry;
+}
+
+__global__ void __launch_bounds__(kTileNT) tile_reduce_kernel(
+    const unsigned long long *__restrict__ recs, const unsigned *__restrict__ offs, int ntx,
+    int rows, int cols, int S, int64_t out_stride, float *__restrict__ ground,
+    float *__restrict__ ceiling) {
+  extern __shared__ uint32_t tk[];  // [S][256] max keys, then [S][256] min keys
+  uint32_t *gk = tk, *ck = tk + S * kTB2;
+  const int tile = blockIdx.x;
+  const int t = threadIdx.x;
+  for (int q = t; q < S * kTB2; q += kTileNT) {
+    gk[q] = kKeyEmptyMax;
+    ck[q] = kKeyEmptyMin;
+  }
+  __syncthreads();
+  const unsigned r0 = offs[tile], r1 = offs[tile + 1];
+  for (unsigned r = r0 + t; r < r1; r += kTileNT) {
+    const unsigned long long rec = __ldcs(recs + r);
+    const unsigned local = (unsigned)(rec & 0xFFu);
+    const int b = (int)((rec >> 8) & 0xFFFFFFu);
+    const uint32_t key = (uint32_t)(rec >> 32);
+    if (b < S) atomicMax(gk + b * kTB2 + local, key);
+    if (b > 0) atomicMin(ck + (b - 1) * kTB2 + local, key);
+  }
+  __syncthreads();
+  const int ti = tile / ntx, tj = tile - ti * ntx;
+  const int i = ti * kTBH + t / kTBW, j = tj * kTBW + t % kTBW;
+  if (i >= rows || j >= cols) return;
+  const int64_t cell = (int64_t)i * cols + j;
+  uint32_t run = kKeyEmptyMax;
+  for (int k = 0; k < S; ++k) {
+    const uint32_t v = gk[k * kTB2 + t];
+    run = v > run ? v : run;
+    __stcs(ground + (int64_t)k * out_stride + cell, decode_ground(run));
+  }
+  run = kKeyEmptyMin;
+  for (int k = S - 1; k >= 0; --k) {
+    const uint32_t v = ck[k * kTB2 + t];
+    run = v < run ? v : run;
+    __stcs(ceiling + (int64_t)k * out_stride + cell, decode_ceiling(run));
+  }
+}
+
 // ------------------------------------------------------------- K3 bin scan
 // ground[k] = max(bins 0..k), ceiling[k] = min(bins k+1..S); scratch bin
 // plane k of ckey holds bin k+1.
@@ -276,6 +484,55 @@ int launch_build(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, const pct_
   const size_t plane = (size_t)cells * sizeof(uint32_t);
   // scratch: gkey (S planes) | ckey (S planes) | heights (S doubles) | outside counter
   const size_t hbytes = ((size_t)S * sizeof(double) + 255) & ~(size_t)255;
+  const char *bmode = getenv("PCT_BUILD");
+  // the tile-partitioned build is the measured alternative (PCT_BUILD=tiled):
+  // cfg1 211 us vs 141 us for the atomic build incl. its memsets, cfg2 781 vs
+  // ~800 us (profiles/r01d_build_variants.txt)
+  if (S <= kTileMaxS && n > 0 && n < (int64_t)UINT32_MAX && bmode && bmode[0] == 't') {
+    // tile-partitioned build: scratch = heights | outside | counts | offsets |
+    // cursors | records (the key planes above are not used)
+    const int ntx = (fr.cols + kTBW - 1) / kTBW, nty = (nrows + kTBH - 1) / kTBH;
+    const int64_t ntiles = (int64_t)ntx * nty;
+    const size_t cbytes = ((size_t)(ntiles + 1) * 4 * kCtrPad + 255) & ~(size_t)255;
+    if (int rc = ensure_scratch(ctx, hbytes + 256 + 3 * cbytes + (size_t)n * 8)) return rc;
+    char *b0 = static_cast<char *>(ctx->scratch);
+    double *hd = reinterpret_cast<double *>(b0);
+    unsigned long long *outs = reinterpret_cast<unsigned long long *>(b0 + hbytes);
+    unsigned *cnt = reinterpret_cast<unsigned *>(b0 + hbytes + 256);
+    unsigned *offs = reinterpret_cast<unsigned *>(b0 + hbytes + 256 + cbytes);
+    unsigned *cur = reinterpret_cast<unsigned *>(b0 + hbytes + 256 + 2 * cbytes);
+    unsigned long long *recs = reinterpret_cast<unsigned long long *>(b0 + hbytes + 256 + 3 * cbytes);
+    PCT_CUDA(ctx, cudaMemcpyAsync(hd, heights_host, (size_t)S * sizeof(double),
+                                  cudaMemcpyHostToDevice, ctx->stream));
+    PCT_CUDA(ctx, cudaMemsetAsync(outs, 0, 8, ctx->stream));
+    PCT_CUDA(ctx, cudaMemsetAsync(cnt, 0, (size_t)ntiles * 4 * kCtrPad, ctx->stream));
+    BinArgs a{fr.origin_x, fr.origin_y, fr.z_min, fr.r_g, fr.d_s, 1.0 / fr.r_g, 1.0 / fr.d_s,
+              hd, cells, nrows, fr.cols, S, row0};
+    const size_t hsm = S <= kMaxStagedHeights ? (size_t)S * sizeof(double) : 0;
+    const int g = grid_for(ctx, n, 256, 16);
+    if (dtype == PCT_F32)
+      tile_pass_kernel<float, false><<<g, 256, hsm, ctx->stream>>>(
+          static_cast<const float *>(xyz), n, a, ntx, cnt, nullptr, outs);
+    else
+      tile_pass_kernel<double, false><<<g, 256, hsm, ctx->stream>>>(
+          static_cast<const double *>(xyz), n, a, ntx, cnt, nullptr, outs);
+    if (int rc = check_launch(ctx, "tile_count_kernel")) return rc;
+    tile_offsets_kernel<<<1, 1024, 0, ctx->stream>>>(cnt, (int)ntiles, offs, cur);
+    if (int rc = check_launch(ctx, "tile_offsets_kernel")) return rc;
+    if (dtype == PCT_F32)
+      tile_pass_kernel<float, true><<<g, 256, hsm, ctx->stream>>>(
+          static_cast<const float *>(xyz), n, a, ntx, cur, recs, outs);
+    else
+      tile_pass_kernel<double, true><<<g, 256, hsm, ctx->stream>>>(
+          static_cast<const double *>(xyz), n, a, ntx, cur, recs, outs);
+    if (int rc = check_launch(ctx, "tile_scatter_kernel")) return rc;
+    const size_t tsm = (size_t)2 * S * kTB2 * 4;
+    PCT_CUDA(ctx, cudaFuncSetAttribute(tile_reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)tsm));
+    tile_reduce_kernel<<<(unsigned)ntiles, kTileNT, tsm, ctx->stream>>>(
+        recs, offs, ntx, nrows, fr.cols, S, out_stride, ground, ceiling);
+    return check_launch(ctx, "tile_reduce_kernel");
+  }
   if (int rc = ensure_scratch(ctx, 2 * plane * S + hbytes + 256)) return rc;
   char *base = static_cast<char *>(ctx->scratch);
   uint32_t *gkey = reinterpret_cast<uint32_t *>(base);

@@ -117,6 +117,22 @@ def test_inflation_kernels_vs_oracle_random_costs(r_g, d_inf, d_sm, patch):
     _assert_layers_equal(got, want, "cost")
 
 
+@pytest.mark.parametrize("name", ["synth_cfg0", "ref_random_multilayer_s9", "ref_spiral_s3",
+                                  "synth_cfg2_n2000000"])
+def test_tiled_build_matches_reference_golden(golden, monkeypatch, name):
+    """The tile-partitioned build (PCT_BUILD=tiled: bucket by 8x32-cell tile,
+    shared-memory segmented max / min) gives the reference's layers too."""
+    monkeypatch.setenv("PCT_BUILD", "tiled")
+    case = golden["cases"][name]
+    xyz = case_input(name, case)
+    for arr in (xyz, xyz.astype(np.float64)):
+        tom = pct.build_tomogram(pct.PointCloud(arr), case["d_s"], case["r_g"])
+        g, c = tom.ground_stack(), tom.ceiling_stack()
+        for k in range(g.shape[0]):
+            assert digest(g[k]) == case["ground_slice_sha256"][k], f"ground slice {k}"
+            assert digest(c[k]) == case["ceiling_slice_sha256"][k], f"ceiling slice {k}"
+
+
 def test_f32_and_f64_inputs_agree(golden):
     case = golden["cases"]["synth_cfg0"]
     xyz = case_input("synth_cfg0", case)
