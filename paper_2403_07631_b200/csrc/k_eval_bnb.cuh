@@ -228,6 +228,7 @@ __global__ void __launch_bounds__(NT, MINB) resolve_inflate_bnb_kernel(
   const int64_t cells = (int64_t)rows * cols;
   constexpr uint32_t BOX_BYTES = G::CH * G::CW * 4;
   const float w0 = c_bw[0], w1 = c_bw[1];
+  const uint32_t cb_bits = f32_bits((float)c_K.c_barrier);
   // thread 0 walks the CTA's step sequence one step ahead of the others:
   // step = (item, slice); it records the tile origin and slice of each step
   // in the slot of the buffer it loads
@@ -281,7 +282,6 @@ __global__ void __launch_bounds__(NT, MINB) resolve_inflate_bnb_kernel(
       else if (G::GW - 32 * w < 32) word &= (1u << (G::GW - 32 * w)) - 1u;
       bits[idx] = word;
     }
-    for (int idx = tid; idx < G::NBY * G::NBX; idx += NT) bm[idx] = 0u;
     for (int idx = tid; idx < G::CBY * G::CBX; idx += NT) chg[idx] = first ? 1 : 0;
     __syncthreads();
     // ---- P0b: foothold test of every c_init cell, 32 cells per word:
@@ -317,35 +317,44 @@ __global__ void __launch_bounds__(NT, MINB) resolve_inflate_bnb_kernel(
     // aligned R x R blocks (c_init >= 0: float order = uint order); 4 x 4
     // blocks that differ from the previous slice
     constexpr int CW4 = G::CW / 4;
+    bool changed = first;
     for (int q = tid; q < G::CH * CW4; q += NT) {
       float4 v = lds4(ci + 4 * q);
       const int y = q / CW4, x = 4 * (q - y * CW4);
       const uint32_t sgn = (f32_bits(v.x) | f32_bits(v.y) | f32_bits(v.z) | f32_bits(v.w));
-      if (sgn & 0x80000000u) {
+      if (sgn & 0x80000000u) {  // branch-free cinit_resolve of the 4 cells
         const uint32_t ok = okb[y * G::CWW + (x >> 5)] >> (x & 31);  // 4 cells, one word
-        v.x = cinit_resolve_ok(v.x, ok & 1u, c_K);
-        v.y = cinit_resolve_ok(v.y, ok & 2u, c_K);
-        v.z = cinit_resolve_ok(v.z, ok & 4u, c_K);
-        v.w = cinit_resolve_ok(v.w, ok & 8u, c_K);
+        auto res = [&](float f, uint32_t okbit) {
+          const uint32_t u = f32_bits(f);
+          const uint32_t r = okbit ? (u & 0x7FFFFFFFu) : cb_bits;
+          return bits_f32((u & 0x80000000u) ? r : u);
+        };
+        v.x = res(v.x, ok & 1u);
+        v.y = res(v.y, ok & 2u);
+        v.z = res(v.z, ok & 4u);
+        v.w = res(v.w, ok & 8u);
         *reinterpret_cast<float4 *>(ci + 4 * q) = v;
       }
-      const float m4 = fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w));
-      if (m4 > 0.0f) atomicMax(&bm[(y / R) * G::NBX + x / R], f32_bits(m4));
       if (!first) {
         const float4 u = lds4(cp + 4 * q);
         if (f32_bits(u.x) != f32_bits(v.x) || f32_bits(u.y) != f32_bits(v.y) ||
-            f32_bits(u.z) != f32_bits(v.z) || f32_bits(u.w) != f32_bits(v.w))
+            f32_bits(u.z) != f32_bits(v.z) || f32_bits(u.w) != f32_bits(v.w)) {
           chg[(y >> 2) * G::CBX + (x >> 2)] = 1;
+          changed = true;
+        }
       }
     }
-    __syncthreads();
+    // a tile whose resolved c_init equals the previous slice's keeps every
+    // output: straight to the store
+    if (__syncthreads_or(changed)) {
     // ---- P1: dirty output blocks; horizontal maxima planes; upper bound per
     // output block (3 x 3 c_init blocks cover every tap of its outputs' windows)
     {
       constexpr int NG = TW / 4;
       constexpr int NQ = G::QY * G::QX;
       constexpr int ND = G::DBY * G::DBX;
-      for (int q = tid; q < ND + NQ + G::CH * NG; q += NT) {
+      constexpr int NB = G::NBY * G::NBX;
+      for (int q = tid; q < ND + NB + G::CH * NG; q += NT) {
         if (q < ND) {
           const int dy = q / G::DBX, dx = q - dy * G::DBX;
           bool d = false;
@@ -354,16 +363,21 @@ __global__ void __launch_bounds__(NT, MINB) resolve_inflate_bnb_kernel(
 #pragma unroll
             for (int b = 0; b < G::SPAN; ++b) d |= chg[(dy + a) * G::CBX + dx + b] != 0;
           dirty[q] = d;
-        } else if (q < ND + NQ) {
+        } else if (q < ND + NB) {  // maxima of the aligned R x R c_init blocks
           const int e = q - ND;
-          const int qy = e / G::QX, qx = e - qy * G::QX;
-          const uint32_t *p = bm + qy * G::NBX + qx;
-          const uint32_t m = max(max(max(p[0], p[1]), max(p[2], p[G::NBX])),
-                                 max(max(p[G::NBX + 1], p[G::NBX + 2]),
-                                     max(max(p[2 * G::NBX], p[2 * G::NBX + 1]), p[2 * G::NBX + 2])));
-          ub[e] = bits_f32(m);
+          const int by = e / G::NBX, bx = e - by * G::NBX;
+          const float *p = ci + by * R * G::CW + bx * R;
+          float m = 0.0f;
+#pragma unroll
+          for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int c4 = 0; c4 < R; c4 += 4) {
+              const float4 v = lds4(p + r * G::CW + c4);
+              m = fmax3(m, fmaxf(v.x, v.y), fmaxf(v.z, v.w));
+            }
+          bm[e] = f32_bits(m);
         } else {
-          const int e = q - ND - NQ;
+          const int e = q - ND - NB;
           const int y = e / NG, g = e - y * NG;
           // c_init columns 4g + R - 4 .. 4g + R + 7 (12 values, 16-byte aligned)
           const float *p = ci + y * G::CW + 4 * g + R - 4;
@@ -434,7 +448,12 @@ __global__ void __launch_bounds__(NT, MINB) resolve_inflate_bnb_kernel(
           d1[3] = fmax3(fmax3(a0.w, a1.w, a2.w), fmax3(a3.w, a4.w, b0.w),
                         fmax3(fmax3(b1.w, l4.w, r4.w), u4.w, d4.w));
         }
-        const float bound = w1 * ub[(i / R) * G::QX + (4 * g) / R];
+        const uint32_t *pq = bm + (i / R) * G::NBX + (4 * g) / R;  // 3 x 3 blocks under the window
+        const float U = bits_f32(max(max(max(pq[0], pq[1]), max(pq[2], pq[G::NBX])),
+                                     max(max(pq[G::NBX + 1], pq[G::NBX + 2]),
+                                         max(max(pq[2 * G::NBX], pq[2 * G::NBX + 1]),
+                                             pq[2 * G::NBX + 2]))));
+        const float bound = w1 * U;
         float v[4];
         unsigned m = 0;  // outputs of this thread that need the class walk
 #pragma unroll
@@ -489,18 +508,26 @@ __global__ void __launch_bounds__(NT, MINB) resolve_inflate_bnb_kernel(
                      fmax3(fmax3(h2[(yc + 3) * TW], cc[-4], cc[4]), cc[-4 * G::CW], cc[4 * G::CW]));
         }
         float acc = w0 * d1;
-        const float U = ub[(i / R) * G::QX + x / R];
+        const uint32_t *pq = bm + (i / R) * G::NBX + x / R;
+        const float U = bits_f32(max(max(max(pq[0], pq[1]), max(pq[2], pq[G::NBX])),
+                                     max(max(pq[G::NBX + 1], pq[G::NBX + 2]),
+                                         max(max(pq[2 * G::NBX], pq[2 * G::NBX + 1]),
+                                             pq[2 * G::NBX + 2]))));
         slow_classes<R, G::CW, 1>(ci + yc * G::CW + (x + R), U, in_list, acc);
         if (in_list) ot[idx] = acc;
       }
     }
     __syncthreads();
+    }  // tile changed
     // ---- P4: store the output tile (every output, every slice)
     {
-      float *out = cost + (int64_t)k * cells;
-      for (int idx = tid; idx < TH * TW; idx += NT) {
-        const int i = idx / TW, x = idx - i * TW;
-        if (i0 + i < rows && j0 + x < cols) out[(int64_t)(i0 + i) * cols + (j0 + x)] = ot[idx];
+      static_assert(NT % TW == 0, "store layout");
+      constexpr int RPS = NT / TW;  // rows per pass
+      const int x = tid % TW, r0 = tid / TW;
+      const int imax = min(TH, rows - i0);
+      if (j0 + x < cols) {
+        float *o = cost + (int64_t)k * cells + (int64_t)(i0 + r0) * cols + (j0 + x);
+        for (int i = r0; i < imax; i += RPS, o += (int64_t)RPS * cols) *o = ot[i * TW + x];
       }
     }
     // the next step's first barrier orders P4's reads of `ot` before its P2
