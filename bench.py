@@ -401,7 +401,10 @@ def run_b200(args):
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    launches0 = ctx.launches
+    def all_launches():  # the batch runner's worker contexts launch the batch's kernels
+        return ctx.launches + (sum(c.launches for c in runner.ctxs) if runner is not None else 0)
+
+    launches0 = all_launches()
     recs = []
     with ClockSampler(local) as clk:
         t_start = time.perf_counter()
@@ -412,7 +415,7 @@ def run_b200(args):
         t_wall = time.perf_counter() - t_start
     if world > 1:
         torch.distributed.barrier()
-    launches = ctx.launches - launches0
+    launches = all_launches() - launches0
     per = {}
     for r in recs:
         for k, pairs in r.items():

@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstring>
 #include <map>
 #include <tuple>
 #include <vector>
@@ -230,8 +231,18 @@ int run_simplify(pct_ctx *ctx, const float *ground, const float *cost, int S, in
     window_kernel<<<grid, kWinNT, tab_smem, ctx->stream>>>(A, table);
   }
   if (int rc = check_launch(ctx, "window_kernel")) return rc;
-  PCT_CUDA(ctx, cudaMemcpyAsync(htable.data(), table, tbytes, cudaMemcpyDeviceToHost, ctx->stream));
-  PCT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  // host round trips through the context's pinned buffer (pageable copies
+  // are staged and cost latency)
+  const bool pinned = tbytes + (size_t)S * (sizeof(Triple) + sizeof(int)) + 64 <= 65536;
+  char *hbase = static_cast<char *>(ctx->hsmall);
+  if (pinned) {
+    PCT_CUDA(ctx, cudaMemcpyAsync(hbase, table, tbytes, cudaMemcpyDeviceToHost, ctx->stream));
+    PCT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    std::memcpy(htable.data(), hbase, tbytes);
+  } else {
+    PCT_CUDA(ctx, cudaMemcpyAsync(htable.data(), table, tbytes, cudaMemcpyDeviceToHost, ctx->stream));
+    PCT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  }
 
   std::map<std::tuple<int, int, int>, bool> cache;
   auto from_window = [&](int below, int k, int above, bool *hit) -> bool {
@@ -249,17 +260,21 @@ int run_simplify(pct_ctx *ctx, const float *ground, const float *cost, int S, in
   auto batch = [&](const std::vector<Triple> &ts) -> int {
     if (ts.empty()) return PCT_OK;
     const int T = (int)ts.size();
-    PCT_CUDA(ctx, cudaMemcpyAsync(dtr, ts.data(), sizeof(Triple) * T, cudaMemcpyHostToDevice,
-                                  ctx->stream));
+    Triple *htr = reinterpret_cast<Triple *>(hbase + tbytes);
+    int *hfl = reinterpret_cast<int *>(hbase + tbytes + (size_t)S * sizeof(Triple));
+    if (pinned) std::memcpy(htr, ts.data(), sizeof(Triple) * T);
+    PCT_CUDA(ctx, cudaMemcpyAsync(dtr, pinned ? htr : ts.data(), sizeof(Triple) * T,
+                                  cudaMemcpyHostToDevice, ctx->stream));
     PCT_CUDA(ctx, cudaMemsetAsync(dflags, 0, sizeof(int) * T, ctx->stream));
     int64_t bx = (A.cells + 255) / 256;
     if (bx > blocks_x) bx = blocks_x;
     triples_kernel<<<dim3((unsigned)bx, T), 256, 0, ctx->stream>>>(A, dtr, dflags);
     if (int rc = check_launch(ctx, "triples_kernel")) return rc;
     std::vector<int> hf(T);
-    PCT_CUDA(ctx, cudaMemcpyAsync(hf.data(), dflags, sizeof(int) * T, cudaMemcpyDeviceToHost,
-                                  ctx->stream));
+    PCT_CUDA(ctx, cudaMemcpyAsync(pinned ? hfl : hf.data(), dflags, sizeof(int) * T,
+                                  cudaMemcpyDeviceToHost, ctx->stream));
     PCT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    if (pinned) std::memcpy(hf.data(), hfl, sizeof(int) * T);
     for (int i = 0; i < T; ++i) cache[{ts[i].below, ts[i].k, ts[i].above}] = hf[i] != 0;
     return PCT_OK;
   };
