@@ -149,6 +149,7 @@ int pct_ctx_destroy(pct_ctx *ctx) {
   if (ctx->staging) cudaFree(ctx->staging);
   if (ctx->dsmall) cudaFree(ctx->dsmall);
   if (ctx->enc) cudaFree(ctx->enc);
+  if (ctx->keys) cudaFree(ctx->keys);
   for (auto e : ctx->ev)
     if (e) cudaEventDestroy(e);
   if (ctx->hsmall) cudaFreeHost(ctx->hsmall);

@@ -384,8 +384,8 @@ __global__ void __launch_bounds__(kTileNT) tile_reduce_kernel(
 // ------------------------------------------------------------- K3 bin scan
 // ground[k] = max(bins 0..k), ceiling[k] = min(bins k+1..S); scratch bin
 // plane k of ckey holds bin k+1.
-__global__ void __launch_bounds__(256) scan_kernel(const uint32_t *__restrict__ gkey,
-                                                   const uint32_t *__restrict__ ckey,
+__global__ void __launch_bounds__(256) scan_kernel(uint32_t *__restrict__ gkey,
+                                                   uint32_t *__restrict__ ckey,
                                                    int64_t cells, int S, int64_t out_stride,
                                                    float *__restrict__ ground,
                                                    float *__restrict__ ceiling) {
@@ -405,6 +405,9 @@ __global__ void __launch_bounds__(256) scan_kernel(const uint32_t *__restrict__ 
 #pragma unroll
     for (int u = 0; u < U; ++u) v[u] = __ldcs(gkey + (int64_t)(k + u) * cells + c);
 #pragma unroll
+    for (int u = 0; u < U; ++u)  // reset the (few) non-empty keys for the next build
+      if (v[u] != kKeyEmptyMax) gkey[(int64_t)(k + u) * cells + c] = kKeyEmptyMax;
+#pragma unroll
     for (int u = 0; u < U; ++u) {
       run = v[u] > run ? v[u] : run;
       __stcs(ground + (int64_t)(k + u) * out_stride + c, decode_ground(run));
@@ -412,6 +415,7 @@ __global__ void __launch_bounds__(256) scan_kernel(const uint32_t *__restrict__ 
   }
   for (; k < S; ++k) {
     const uint32_t v = __ldcs(gkey + (int64_t)k * cells + c);
+    if (v != kKeyEmptyMax) gkey[(int64_t)k * cells + c] = kKeyEmptyMax;
     run = v > run ? v : run;
     __stcs(ground + (int64_t)k * out_stride + c, decode_ground(run));
   }
@@ -424,6 +428,9 @@ __global__ void __launch_bounds__(256) scan_kernel(const uint32_t *__restrict__ 
 #pragma unroll
     for (int u = 0; u < U; ++u) v[u] = __ldcs(ckey + (int64_t)(k - u) * cells + c);
 #pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (v[u] != kKeyEmptyMin) ckey[(int64_t)(k - u) * cells + c] = kKeyEmptyMin;
+#pragma unroll
     for (int u = 0; u < U; ++u) {
       run = v[u] < run ? v[u] : run;
       __stcs(ceiling + (int64_t)(k - u) * out_stride + c, decode_ceiling(run));
@@ -431,6 +438,7 @@ __global__ void __launch_bounds__(256) scan_kernel(const uint32_t *__restrict__ 
   }
   for (; k >= 0; --k) {
     const uint32_t v = __ldcs(ckey + (int64_t)k * cells + c);
+    if (v != kKeyEmptyMin) ckey[(int64_t)k * cells + c] = kKeyEmptyMin;
     run = v < run ? v : run;
     __stcs(ceiling + (int64_t)k * out_stride + c, decode_ceiling(run));
   }
@@ -533,16 +541,33 @@ int launch_build(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, const pct_
         recs, offs, ntx, nrows, fr.cols, S, out_stride, ground, ceiling);
     return check_launch(ctx, "tile_reduce_kernel");
   }
-  if (int rc = ensure_scratch(ctx, 2 * plane * S + hbytes + 256)) return rc;
+  // key planes in their own grow-only buffer: the scan leaves them empty
+  // again, so only a new layout needs the memsets
+  const size_t kbytes = 2 * plane * S;
+  if (ctx->keys_bytes < kbytes) {
+    if (ctx->keys) {
+      cudaStreamSynchronize(ctx->stream);
+      cudaFree(ctx->keys);
+      ctx->keys = nullptr;
+      ctx->keys_bytes = 0;
+    }
+    PCT_CUDA(ctx, cudaMalloc(&ctx->keys, kbytes));
+    ctx->keys_bytes = kbytes;
+    ctx->keys_tag[0] = -1;
+  }
+  if (int rc = ensure_scratch(ctx, hbytes + 256)) return rc;
+  uint32_t *gkey = static_cast<uint32_t *>(ctx->keys);
+  uint32_t *ckey = reinterpret_cast<uint32_t *>(static_cast<char *>(ctx->keys) + plane * S);
   char *base = static_cast<char *>(ctx->scratch);
-  uint32_t *gkey = reinterpret_cast<uint32_t *>(base);
-  uint32_t *ckey = reinterpret_cast<uint32_t *>(base + plane * S);
-  double *hdev = reinterpret_cast<double *>(base + 2 * plane * S);
-  unsigned long long *outside = reinterpret_cast<unsigned long long *>(base + 2 * plane * S + hbytes);
+  double *hdev = reinterpret_cast<double *>(base);
+  unsigned long long *outside = reinterpret_cast<unsigned long long *>(base + hbytes);
   PCT_CUDA(ctx, cudaMemcpyAsync(hdev, heights_host, (size_t)S * sizeof(double),
                                 cudaMemcpyHostToDevice, ctx->stream));
-  PCT_CUDA(ctx, cudaMemsetAsync(gkey, 0x00, plane * S, ctx->stream));
-  PCT_CUDA(ctx, cudaMemsetAsync(ckey, 0xFF, plane * S, ctx->stream));
+  if (ctx->keys_tag[0] != S || ctx->keys_tag[1] != cells) {
+    PCT_CUDA(ctx, cudaMemsetAsync(gkey, 0x00, plane * S, ctx->stream));
+    PCT_CUDA(ctx, cudaMemsetAsync(ckey, 0xFF, plane * S, ctx->stream));
+  }
+  ctx->keys_tag[0] = -1;  // dirty until the scan below is launched
   PCT_CUDA(ctx, cudaMemsetAsync(outside, 0, 8, ctx->stream));
   BinArgs a{fr.origin_x, fr.origin_y, fr.z_min, fr.r_g, fr.d_s, 1.0 / fr.r_g, 1.0 / fr.d_s,
             hdev, cells, nrows, fr.cols, S, row0};
@@ -558,7 +583,10 @@ int launch_build(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, const pct_
   }
   scan_kernel<<<dim3((unsigned)((cells + 255) / 256), 2), 256, 0, ctx->stream>>>(
       gkey, ckey, cells, S, out_stride, ground, ceiling);
-  return check_launch(ctx, "scan_kernel");
+  if (int rc = check_launch(ctx, "scan_kernel")) return rc;
+  ctx->keys_tag[0] = S;  // the scan resets every key it reads
+  ctx->keys_tag[1] = cells;
+  return PCT_OK;
 }
 
 }  // namespace pct

@@ -28,6 +28,11 @@ struct pct_ctx {
   // small device/pinned buffers for reductions and flags
   void *dsmall = nullptr;   // 64 KiB device
   void *hsmall = nullptr;   // 64 KiB pinned host
+  // build key planes (gkey | ckey): the scan resets every key it reads, so a
+  // layout that was built once needs no memset (keys_tag = S, cells)
+  void *keys = nullptr;
+  size_t keys_bytes = 0;
+  int64_t keys_tag[2] = {-1, -1};
   // zero-padded encoded c_init stacks of the split evaluation; the padding
   // is cleared only when the layout changes (the interior is rewritten)
   void *enc = nullptr;
