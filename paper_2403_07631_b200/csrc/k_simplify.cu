@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <tuple>
@@ -79,17 +80,24 @@ __global__ void __launch_bounds__(kWinNT) window_kernel(SimpArgs A,
   for (int64_t cell = (int64_t)blockIdx.x * kWinNT + threadIdx.x; cell < span; cell += stride) {
     const bool live = cell < A.cells;
     float ce[KB + 1], cc[KB + 1];  // slices k0 .. k0+KB of this cell
-    auto load = [&](int k, float &e, float &c) {
-      const bool ok = live && k < A.S;
-      e = ok ? __ldg(A.ground + (int64_t)k * A.stride + cell) : nanf_;
-      c = ok ? __ldg(A.cost + (int64_t)k * A.stride + cell) : 0.f;
+    // running pointers to the next slice to load (no 64-bit multiply per load)
+    const float *pg = A.ground + (live ? cell : 0), *pc = A.cost + (live ? cell : 0);
+    int kn = 0;  // slice pg / pc point at
+    auto load = [&](float &e, float &c) {
+      const bool ok = live && kn < A.S;
+      e = ok ? __ldg(pg) : nanf_;
+      c = ok ? __ldg(pc) : 0.f;
+      pg += A.stride;
+      pc += A.stride;
+      ++kn;
     };
 #pragma unroll
-    for (int u = 0; u <= KB; ++u) load(u, ce[u], cc[u]);
+    for (int u = 0; u <= KB; ++u) load(ce[u], cc[u]);
     for (int k0 = 0; k0 < A.S; k0 += KB) {
       float ne[KB], nc[KB];  // slices k0+KB+1 .. k0+2KB, in flight while testing
 #pragma unroll
-      for (int u = 0; u < KB; ++u) load(k0 + KB + 1 + u, ne[u], nc[u]);
+      for (int u = 0; u < KB; ++u) load(ne[u], nc[u]);
+
 #pragma unroll
       for (int u = 0; u < KB; ++u) {
         const int k = k0 + u;
@@ -227,7 +235,9 @@ int run_simplify(pct_ctx *ctx, const float *ground, const float *cost, int S, in
     PCT_CUDA(ctx, cudaFuncSetAttribute(window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)tab_smem));
     const int64_t blocks_needed = (A.cells + kWinNT - 1) / kWinNT;
-    const unsigned grid = (unsigned)std::min<int64_t>(blocks_needed, 12LL * ctx->num_sms);
+    const char *wb = getenv("PCT_WIN_BLOCKS");
+    const int per_sm = wb ? atoi(wb) : 12;
+    const unsigned grid = (unsigned)std::min<int64_t>(blocks_needed, (int64_t)per_sm * ctx->num_sms);
     window_kernel<<<grid, kWinNT, tab_smem, ctx->stream>>>(A, table);
   }
   if (int rc = check_launch(ctx, "window_kernel")) return rc;
