@@ -493,10 +493,14 @@ int launch_build(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, const pct_
   // scratch: gkey (S planes) | ckey (S planes) | heights (S doubles) | outside counter
   const size_t hbytes = ((size_t)S * sizeof(double) + 255) & ~(size_t)255;
   const char *bmode = getenv("PCT_BUILD");
-  // the tile-partitioned build is the measured alternative (PCT_BUILD=tiled):
-  // cfg1 211 us vs 141 us for the atomic build incl. its memsets, cfg2 781 vs
-  // ~800 us (profiles/r01d_build_variants.txt)
-  if (S <= kTileMaxS && n > 0 && n < (int64_t)UINT32_MAX && bmode && bmode[0] == 't') {
+  // Atomic build while the key planes stay within reach of L2 / the TLB;
+  // beyond ~1.5 GB of keys every RED becomes a DRAM read-modify-write of a
+  // sector (cfg3, 5.6 GB of keys: atomic scatter 11.5 ms + scan 2.1 ms vs
+  // tiled 7.0 ms; cfg1 141 vs 211 us and cfg2 ~660 vs 781 us the other way,
+  // profiles/r01d_build_variants.txt).  PCT_BUILD=atomic / tiled forces one.
+  const bool big_keys = 2.0 * (double)S * (double)cells * 4.0 > 1.5e9;
+  const bool tiled = bmode ? bmode[0] == 't' : big_keys;
+  if (S <= kTileMaxS && n > 0 && n < (int64_t)UINT32_MAX && tiled) {
     // tile-partitioned build: scratch = heights | outside | counts | offsets |
     // cursors | records (the key planes above are not used)
     const int ntx = (fr.cols + kTBW - 1) / kTBW, nty = (nrows + kTBH - 1) / kTBH;

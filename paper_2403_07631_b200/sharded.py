@@ -194,15 +194,19 @@ def band_pipeline(xyz, d_s, r_g, params, rank, size, *, device=None, eps_e=1e-6,
     row0, row1 = starts[rank], starts[rank + 1]
     nrows = row1 - row0
 
-    # 2. partition by owner band, all-to-all
-    part = torch.empty_like(xyz)
-    counts = np.zeros(size, np.int64)
-    st = np.asarray(starts, np.int32)
-    if n > 0:
-        ctx.check(lib.pct_partition_rows(h, xyz.data_ptr(), n, code, C.byref(fr), st.ctypes.data,
-                                         size, part.data_ptr(), counts.ctypes.data), "partition")
-    mine = yield ("alltoallv", part, counts.tolist())
-    mine = mine.contiguous()
+    # 2. partition by owner band, all-to-all (one band owns every point)
+    if size == 1:
+        mine = xyz
+    else:
+        part = torch.empty_like(xyz)
+        counts = np.zeros(size, np.int64)
+        st = np.asarray(starts, np.int32)
+        if n > 0:
+            ctx.check(lib.pct_partition_rows(h, xyz.data_ptr(), n, code, C.byref(fr),
+                                             st.ctypes.data, size, part.data_ptr(),
+                                             counts.ctypes.data), "partition")
+        mine = yield ("alltoallv", part, counts.tolist())
+        mine = mine.contiguous()
 
     # 3. banded build into the extended stack
     from .traversability import build_kernel
