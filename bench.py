@@ -351,8 +351,9 @@ def run_b200(args):
     runner = None
     if args.mode == "batch":
         from paper_2403_07631_b200.batch import BatchRunner
-        wstreams = [torch.cuda.Stream(device=local) for _ in range(8)]
-        runner = BatchRunner(local, workers=8, streams=[s.cuda_stream for s in wstreams])
+        nw = int(os.environ.get("PCT_BATCH_WORKERS", "8"))
+        wstreams = [torch.cuda.Stream(device=local) for _ in range(nw)]
+        runner = BatchRunner(local, workers=nw, streams=[s.cuda_stream for s in wstreams])
         batch_maps = [(dm.ptr, len(m), _lib.PCT_F32, 0) for dm, m in zip(dmaps, maps)]
 
     def step():

@@ -216,6 +216,18 @@ int pct_tomo_run(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, int xyz_on
                  double d_s, double r_g, int64_t max_grid_side, const pct_trav_params *p,
                  const float *kernel_w, int32_t kside, double eps_e, double c_barrier,
                  pct_tomo **out, int32_t *keep_host, int32_t *n_keep);
+/* pct_tomo_run for n_maps independent maps (BASELINE config 4; the reference
+   runs one map per call, tomoplan/bench.py:50-57).  Maps are spread over the
+   n_ctx contexts (one stream + scratch each, same device) and issued phase by
+   phase with one synchronisation per phase.  xyz[m]: device points of map m
+   (n_points[m] x 3, dtype).  keep_host: n_maps x keep_stride slice indices,
+   n_keep[m] their count.  out (optional): per-map tomogram handles, else the
+   stacks are freed. */
+int pct_tomo_run_batch(pct_ctx **ctxs, int32_t n_ctx, int32_t n_maps, const void *const *xyz,
+                       const int64_t *n_points, int dtype, double d_s, double r_g,
+                       int64_t max_grid_side, const pct_trav_params *p, const float *kernel_w,
+                       int32_t kside, double eps_e, double c_barrier, pct_tomo **out,
+                       int32_t *keep_host, int32_t keep_stride, int32_t *n_keep);
 /* Stage timing of pct_tomo_run with CUDA events on the context stream:
    ms[0] = bounds + frame + build, ms[1] = evaluate, ms[2] = simplify. */
 int pct_set_timing(pct_ctx *ctx, int on);

@@ -90,6 +90,9 @@ _SIGS = {
     "pct_tomo_simplify": ([_vp, _vp, _d, _d, _vp, _vp], C.c_int),
     "pct_tomo_run": ([_vp, _vp, _i64, C.c_int, C.c_int, _d, _d, _i64, C.POINTER(TravParamsC), _vp,
                       _i32, _d, _d, C.POINTER(_vp), _vp, _vp], C.c_int),
+    "pct_tomo_run_batch": ([_vp, _i32, _i32, _vp, _vp, C.c_int, _d, _d, _i64,
+                            C.POINTER(TravParamsC), _vp, _i32, _d, _d, _vp, _vp, _i32, _vp],
+                           C.c_int),
     "pct_set_timing": ([_vp, C.c_int], C.c_int),
     "pct_last_stage_ms": ([_vp, _vp], C.c_int),
     "pct_tomo_frame": ([_vp, C.POINTER(FrameC), _vp, _i32], C.c_int),

@@ -1,12 +1,14 @@
 """Many independent maps on one GPU (BASELINE config 4: 256 two-storey maps).
 
 Small maps are latency-bound: one map's pipeline is a handful of short
-kernels separated by two host round trips (grid frame after the bounds,
-simplify sweep).  ``BatchRunner`` keeps ``workers`` maps in flight: each
-worker thread owns a libpct context with its own CUDA stream and scratch and
-runs the whole path with one native call (``pct_tomo_run``; ctypes releases
-the GIL for its duration), so the syncs of one map overlap the kernels of
-the others.  Maps never communicate ("batches of independent maps are
+kernels separated by host round trips (grid frame after the bounds, simplify
+sweep).  ``BatchRunner`` owns ``workers`` libpct contexts (a CUDA stream and
+scratch each).  Device-resident batches go through one native call,
+``pct_tomo_run_batch``, which issues the maps phase by phase over the
+contexts with one synchronisation per phase (bounds; build + evaluate +
+simplify table; triple rounds); host-resident ones run one ``pct_tomo_run``
+per map on a thread pool (ctypes releases the GIL), so the syncs of one map
+overlap the kernels of the others.  Maps never communicate ("batches of independent maps are
 distributed without communication"); across GPUs each rank takes its share.
 
 ``evaluate_maps`` is the public entry (an extension of the reference API):
@@ -58,13 +60,56 @@ class BatchRunner:
 
     def run(self, maps, d_s, r_g, params, eps_e=1e-6, c_barrier=50.0, keep_handles=True):
         """maps: list of (pointer, n_points, dtype code, on_host).  Returns, in
-        order, ((ctx, pct_tomo handle) or None, surviving slice indices)."""
+        order, ((ctx, pct_tomo handle) or None, surviving slice indices).
+
+        Device-resident maps go through pct_tomo_run_batch (one host thread,
+        phase by phase over the contexts, one synchronisation per phase);
+        host-resident ones through per-map pct_tomo_run calls on the pool."""
+        if maps and all(not on_host for _, _, _, on_host in maps) and \
+                len({code for _, _, code, _ in maps}) == 1:
+            return self._run_batch(maps, d_s, r_g, params, eps_e, c_barrier, keep_handles)
         w = np.ascontiguousarray(build_kernel(params.d_inf, params.d_sm, r_g).weights)
         pc = _lib.trav_params_c(params, r_g)
         futs = [self.pool.submit(self._one, int(p), int(n), code, int(on_host), float(d_s),
                                  float(r_g), pc, w, float(eps_e), float(c_barrier), keep_handles)
                 for p, n, code, on_host in maps]
         return [f.result() for f in futs]
+
+    def _run_batch(self, maps, d_s, r_g, params, eps_e, c_barrier, keep_handles):
+        """Map groups (map m -> worker m % workers), each driven phase by phase
+        by one pct_tomo_run_batch call on its own context from the pool."""
+        n = len(maps)
+        w = np.ascontiguousarray(build_kernel(params.d_inf, params.d_sm, r_g).weights)
+        pc = _lib.trav_params_c(params, r_g)
+        nw = len(self.ctxs)
+        code = maps[0][2]
+        stride = 4096
+
+        def group(g):
+            idx = list(range(g, n, nw))
+            if not idx:
+                return []
+            ctx = self.ctxs[g]
+            hs = (C.c_void_p * 1)(ctx.h)
+            ptrs = (C.c_void_p * len(idx))(*[int(maps[m][0]) for m in idx])
+            npts = np.asarray([int(maps[m][1]) for m in idx], np.int64)
+            keep = np.empty((len(idx), stride), np.int32)
+            nk = np.empty(len(idx), np.int32)
+            handles = (C.c_void_p * len(idx))() if keep_handles else None
+            rc = ctx.lib.pct_tomo_run_batch(hs, 1, len(idx), ptrs, npts.ctypes.data, code,
+                                            float(d_s), float(r_g), GRID_SIDE_LIMIT, C.byref(pc),
+                                            w.ctypes.data, w.shape[0], float(eps_e),
+                                            float(c_barrier), handles, keep.ctypes.data, stride,
+                                            nk.ctypes.data)
+            ctx.check(rc, "pct_tomo_run_batch")
+            return [(m, (ctx, C.c_void_p(handles[i])) if keep_handles else None,
+                     keep[i, :nk[i]].tolist()) for i, m in enumerate(idx)]
+
+        res = [None] * n
+        for part in self.pool.map(group, range(nw)):
+            for m, h, ks in part:
+                res[m] = (h, ks)
+        return res
 
     def close(self):
         self.pool.shutdown()
@@ -93,8 +138,17 @@ def evaluate_maps(clouds, d_s, r_g, params, *, workers=8, device=None, eps_e=1e-
     own = runner is None
     runner = runner or BatchRunner(device, workers)
     arrays = [np.ascontiguousarray(c.xyz if hasattr(c, "xyz") else c) for c in clouds]
-    maps = [(a.ctypes.data, a.shape[0], _lib.PCT_F32 if a.dtype == np.float32 else _lib.PCT_F64, 1)
-            for a in arrays]
+    codes = {a.dtype for a in arrays}
+    if len(codes) == 1:
+        # one upload per map, then the phase-batched native call
+        ctx0 = runner.ctxs[0]
+        bufs = [_lib.DeviceBuffer.from_host(ctx0, a) for a in arrays]
+        ctx0.check(ctx0.lib.pct_sync(ctx0.h), "sync")
+        maps = [(b.ptr, a.shape[0], _lib.PCT_F32 if a.dtype == np.float32 else _lib.PCT_F64, 0)
+                for a, b in zip(arrays, bufs)]
+    else:
+        maps = [(a.ctypes.data, a.shape[0],
+                 _lib.PCT_F32 if a.dtype == np.float32 else _lib.PCT_F64, 1) for a in arrays]
     try:
         res = runner.run(maps, d_s, r_g, params, eps_e, c_barrier)
     finally:

@@ -154,6 +154,7 @@ int pct_ctx_destroy(pct_ctx *ctx) {
     if (e) cudaEventDestroy(e);
   if (ctx->hsmall) cudaFreeHost(ctx->hsmall);
   if (ctx->pinned_io) cudaFreeHost(ctx->pinned_io);
+  if (ctx->pinned_batch) cudaFreeHost(ctx->pinned_batch);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
   return PCT_OK;
@@ -365,7 +366,7 @@ int pct_unique_mask(pct_ctx *ctx, const float *ground, const float *cost, int32_
 }
 
 // ------------------------------------------------------- device tomogram
-static int tomo_alloc(pct_ctx *ctx, const pct_frame &fr, pct_tomo **out) {
+int tomo_alloc(pct_ctx *ctx, const pct_frame &fr, pct_tomo **out) {
   pct_tomo *t = new (std::nothrow) pct_tomo();
   if (!t) return fail(ctx, PCT_E_NOMEM, "out of host memory");
   t->fr = fr;

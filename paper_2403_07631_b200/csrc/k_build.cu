@@ -12,8 +12,10 @@
 // numpy's NaN (0x7FC00000) where a cell is empty.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <vector>
 
 #include "pct_internal.h"
 
@@ -52,8 +54,8 @@ __device__ __forceinline__ void mm_point(MinMax3<T> &m, T x, T y, T z) {
 }
 
 template <typename T>
-__global__ void __launch_bounds__(256) bounds_kernel(const T *__restrict__ xyz, int64_t n,
-                                                     unsigned long long *keys) {
+__device__ __forceinline__ void bounds_body(const T *__restrict__ xyz, int64_t n,
+                                            unsigned long long *keys) {
   MinMax3<T> m;
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
@@ -123,6 +125,12 @@ __global__ void __launch_bounds__(256) bounds_kernel(const T *__restrict__ xyz, 
   }
 }
 
+template <typename T>
+__global__ void __launch_bounds__(256) bounds_kernel(const T *__restrict__ xyz, int64_t n,
+                                                     unsigned long long *keys) {
+  bounds_body(xyz, n, keys);
+}
+
 // ------------------------------------------------------- K1+K2 bin/scatter
 constexpr int kMaxStagedHeights = 4096;
 
@@ -135,10 +143,10 @@ struct BinArgs {
 };
 
 template <typename T>
-__global__ void __launch_bounds__(256) scatter_kernel(const T *__restrict__ xyz, int64_t n,
-                                                      BinArgs a, uint32_t *__restrict__ gkey,
-                                                      uint32_t *__restrict__ ckey,
-                                                      unsigned long long *outside) {
+__device__ __forceinline__ void scatter_body(const T *__restrict__ xyz, int64_t n, const BinArgs &a,
+                                             uint32_t *__restrict__ gkey,
+                                             uint32_t *__restrict__ ckey,
+                                             unsigned long long *outside) {
   // plane heights staged in shared memory for the bin fix-ups (dynamic
   // shared size is 0 when S is too large; then they are read from global)
   extern __shared__ double hsm[];
@@ -171,6 +179,14 @@ __global__ void __launch_bounds__(256) scatter_kernel(const T *__restrict__ xyz,
     if (b < a.S) atomicMax(gkey + (int64_t)b * a.cells + cell, key);
     if (b > 0) atomicMin(ckey + (int64_t)(b - 1) * a.cells + cell, key);
   }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) scatter_kernel(const T *__restrict__ xyz, int64_t n,
+                                                      BinArgs a, uint32_t *__restrict__ gkey,
+                                                      uint32_t *__restrict__ ckey,
+                                                      unsigned long long *outside) {
+  scatter_body(xyz, n, a, gkey, ckey, outside);
 }
 
 // -------------------------------------------- tile-partitioned build (T1-T4)
@@ -384,11 +400,10 @@ __global__ void __launch_bounds__(kTileNT) tile_reduce_kernel(
 // ------------------------------------------------------------- K3 bin scan
 // ground[k] = max(bins 0..k), ceiling[k] = min(bins k+1..S); scratch bin
 // plane k of ckey holds bin k+1.
-__global__ void __launch_bounds__(256) scan_kernel(uint32_t *__restrict__ gkey,
-                                                   uint32_t *__restrict__ ckey,
-                                                   int64_t cells, int S, int64_t out_stride,
-                                                   float *__restrict__ ground,
-                                                   float *__restrict__ ceiling) {
+__device__ __forceinline__ void scan_body(uint32_t *__restrict__ gkey, uint32_t *__restrict__ ckey,
+                                          int64_t cells, int S, int64_t out_stride,
+                                          float *__restrict__ ground, float *__restrict__ ceiling,
+                                          bool ground_side) {
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= cells) return;
   // scratch planes are dense (stride cells); output slice k of the band lives
@@ -399,7 +414,7 @@ __global__ void __launch_bounds__(256) scan_kernel(uint32_t *__restrict__ gkey,
   constexpr int U = 8;
   uint32_t run = kKeyEmptyMax;
   int k = 0;
-  if (blockIdx.y == 0) {
+  if (ground_side) {
   for (; k + U <= S; k += U) {
     uint32_t v[U];
 #pragma unroll
@@ -444,6 +459,44 @@ __global__ void __launch_bounds__(256) scan_kernel(uint32_t *__restrict__ gkey,
   }
 }
 
+__global__ void __launch_bounds__(256) scan_kernel(uint32_t *__restrict__ gkey,
+                                                   uint32_t *__restrict__ ckey,
+                                                   int64_t cells, int S, int64_t out_stride,
+                                                   float *__restrict__ ground,
+                                                   float *__restrict__ ceiling) {
+  scan_body(gkey, ckey, cells, S, out_stride, ground, ceiling, blockIdx.y == 0);
+}
+
+// ------------------------------------------------ batched maps (config 4)
+// One launch per stage for a whole batch of independent maps; blockIdx.y
+// (bounds, scatter, scan: z) selects the map's descriptor.
+struct BuildMap {
+  const void *xyz;
+  int64_t n;
+  BinArgs a;  // a.heights: device, per map
+  uint32_t *gkey, *ckey;
+  float *ground, *ceiling;
+  unsigned long long *bkeys;  // 7 bounds keys
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) bounds_batch_kernel(const BuildMap *__restrict__ maps) {
+  const BuildMap &m = maps[blockIdx.y];
+  bounds_body(static_cast<const T *>(m.xyz), m.n, m.bkeys);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) scatter_batch_kernel(const BuildMap *__restrict__ maps,
+                                                            unsigned long long *outside) {
+  const BuildMap &m = maps[blockIdx.y];
+  scatter_body(static_cast<const T *>(m.xyz), m.n, m.a, m.gkey, m.ckey, outside);
+}
+
+__global__ void __launch_bounds__(256) scan_batch_kernel(const BuildMap *__restrict__ maps) {
+  const BuildMap &m = maps[blockIdx.z];
+  scan_body(m.gkey, m.ckey, m.a.cells, m.a.S, m.a.cells, m.ground, m.ceiling, blockIdx.y == 0);
+}
+
 int grid_for(pct_ctx *ctx, int64_t work, int block, int per_sm = 8) {
   int64_t g = (work + block - 1) / block;
   int64_t cap = (int64_t)ctx->num_sms * per_sm;
@@ -477,6 +530,157 @@ int launch_bounds(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, double lo
     hi[c] = dkey_inv(hk[3 + c]);
   }
   return PCT_OK;
+}
+
+// ------------------------------------------------ batched maps (host side)
+// descriptors + per-map scratch live in the context buffers; the caller keeps
+// the batch's inputs / outputs alive until the stream is synchronised
+int launch_bounds_batch(pct_ctx *ctx, int n_maps, const void *const *xyz, const int64_t *n,
+                        int dtype, unsigned long long *keys_host) {
+  // keys (7 per map, padded to 8) in dsmall; descriptors in the scratch
+  if ((size_t)n_maps * 64 > 65536) return fail(ctx, PCT_E_INVALID, "batch too large for bounds");
+  std::vector<BuildMap> d(n_maps);
+  unsigned long long *dk = static_cast<unsigned long long *>(ctx->dsmall);
+  int64_t nmax = 1;
+  for (int m = 0; m < n_maps; ++m) {
+    d[m] = BuildMap{};
+    d[m].xyz = xyz[m];
+    d[m].n = n[m];
+    d[m].bkeys = dk + 8 * (size_t)m;
+    nmax = std::max<int64_t>(nmax, n[m]);
+    const unsigned long long init[8] = {~0ull, ~0ull, ~0ull, 0ull, 0ull, 0ull, 0ull, 0ull};
+    std::memcpy(keys_host + 8 * (size_t)m, init, sizeof(init));
+  }
+  if (int rc = ensure_scratch(ctx, sizeof(BuildMap) * (size_t)n_maps)) return rc;
+  BuildMap *dd = static_cast<BuildMap *>(ctx->scratch);
+  PCT_CUDA(ctx, cudaMemcpyAsync(dd, d.data(), sizeof(BuildMap) * n_maps, cudaMemcpyHostToDevice,
+                                ctx->stream));
+  PCT_CUDA(ctx, cudaMemcpyAsync(dk, keys_host, 64 * (size_t)n_maps, cudaMemcpyHostToDevice,
+                                ctx->stream));
+  const int per_map = std::max(1, std::min(grid_for(ctx, (nmax + 3) / 4, 256), 64));
+  if (dtype == PCT_F32)
+    bounds_batch_kernel<float><<<dim3(per_map, n_maps), 256, 0, ctx->stream>>>(dd);
+  else
+    bounds_batch_kernel<double><<<dim3(per_map, n_maps), 256, 0, ctx->stream>>>(dd);
+  if (int rc = check_launch(ctx, "bounds_batch_kernel")) return rc;
+  PCT_CUDA(ctx, cudaMemcpyAsync(keys_host, dk, 64 * (size_t)n_maps, cudaMemcpyDeviceToHost,
+                                ctx->stream));
+  return PCT_OK;
+}
+
+int launch_build_batch(pct_ctx *ctx, int n_maps, const void *const *xyz, const int64_t *n,
+                       int dtype, const pct_frame *frames, const double *const *heights,
+                       float *const *ground, float *const *ceiling) {
+  // scratch: descriptors | heights (all maps) | outside counter
+  int64_t key_words = 0, hcount = 0, nmax = 1;
+  int smax = 1;
+  uint64_t tag = 1469598103934665603ull;  // FNV-1a over the batch layout
+  for (int m = 0; m < n_maps; ++m) {
+    const int64_t cells = (int64_t)frames[m].rows * frames[m].cols;
+    key_words += 2 * (int64_t)frames[m].n_slices * cells;
+    hcount += frames[m].n_slices;
+    nmax = std::max<int64_t>(nmax, n[m]);
+    smax = std::max(smax, frames[m].n_slices);
+    for (uint64_t v : {(uint64_t)frames[m].n_slices, (uint64_t)cells}) tag = (tag ^ v) * 1099511628211ull;
+  }
+  const size_t dbytes = ((sizeof(BuildMap) * (size_t)n_maps + 255) / 256) * 256;
+  const size_t hbytes = (((size_t)hcount * 8 + 255) / 256) * 256;
+  if (int rc = ensure_scratch(ctx, dbytes + hbytes + 256)) return rc;
+  char *base = static_cast<char *>(ctx->scratch);
+  BuildMap *dd = reinterpret_cast<BuildMap *>(base);
+  double *hd = reinterpret_cast<double *>(base + dbytes);
+  unsigned long long *outside = reinterpret_cast<unsigned long long *>(base + dbytes + hbytes);
+  // keys of every map in the context's key buffer; the scans reset them, so
+  // the same batch layout needs no memset next time
+  const size_t kbytes = (size_t)key_words * 4;
+  if (ctx->keys_bytes < kbytes) {
+    if (ctx->keys) {
+      cudaStreamSynchronize(ctx->stream);
+      cudaFree(ctx->keys);
+      ctx->keys = nullptr;
+      ctx->keys_bytes = 0;
+    }
+    PCT_CUDA(ctx, cudaMalloc(&ctx->keys, kbytes));
+    ctx->keys_bytes = kbytes;
+    ctx->keys_tag[0] = -1;
+  }
+  std::vector<BuildMap> d(n_maps);
+  std::vector<double> hh((size_t)hcount);
+  int64_t koff = 0, hoff = 0;
+  uint32_t *kb = static_cast<uint32_t *>(ctx->keys);
+  for (int m = 0; m < n_maps; ++m) {
+    const pct_frame &fr = frames[m];
+    const int64_t cells = (int64_t)fr.rows * fr.cols;
+    std::memcpy(hh.data() + hoff, heights[m], sizeof(double) * fr.n_slices);
+    d[m] = BuildMap{};
+    d[m].xyz = xyz[m];
+    d[m].n = n[m];
+    d[m].a = BinArgs{fr.origin_x, fr.origin_y, fr.z_min, fr.r_g, fr.d_s, 1.0 / fr.r_g,
+                     1.0 / fr.d_s, hd + hoff, cells, fr.rows, fr.cols, fr.n_slices, 0};
+    d[m].gkey = kb + koff;
+    d[m].ckey = kb + koff + (int64_t)fr.n_slices * cells;
+    d[m].ground = ground[m];
+    d[m].ceiling = ceiling[m];
+    koff += 2 * (int64_t)fr.n_slices * cells;
+    hoff += fr.n_slices;
+  }
+  PCT_CUDA(ctx, cudaMemcpyAsync(dd, d.data(), sizeof(BuildMap) * n_maps, cudaMemcpyHostToDevice,
+                                ctx->stream));
+  PCT_CUDA(ctx, cudaMemcpyAsync(hd, hh.data(), sizeof(double) * hcount, cudaMemcpyHostToDevice,
+                                ctx->stream));
+  const int64_t tagi = (int64_t)(tag >> 1);
+  if (ctx->keys_tag[0] != -2 || ctx->keys_tag[1] != tagi) {  // -2: a batch layout
+    int64_t off = 0;
+    for (int m = 0; m < n_maps; ++m) {  // gkey -> 0x00, ckey -> 0xFF per map
+      const int64_t sc = (int64_t)frames[m].n_slices * frames[m].rows * frames[m].cols;
+      PCT_CUDA(ctx, cudaMemsetAsync(kb + off, 0x00, sc * 4, ctx->stream));
+      PCT_CUDA(ctx, cudaMemsetAsync(kb + off + sc, 0xFF, sc * 4, ctx->stream));
+      off += 2 * sc;
+    }
+  }
+  ctx->keys_tag[0] = -1;  // dirty until the scans are launched
+  PCT_CUDA(ctx, cudaMemsetAsync(outside, 0, 8, ctx->stream));
+  const size_t hsm = smax <= kMaxStagedHeights ? (size_t)smax * sizeof(double) : 0;
+  const int gx = std::max(1, std::min(grid_for(ctx, nmax, 256, 16), 64));
+  if (dtype == PCT_F32)
+    scatter_batch_kernel<float><<<dim3(gx, n_maps), 256, hsm, ctx->stream>>>(dd, outside);
+  else
+    scatter_batch_kernel<double><<<dim3(gx, n_maps), 256, hsm, ctx->stream>>>(dd, outside);
+  if (int rc = check_launch(ctx, "scatter_batch_kernel")) return rc;
+  int64_t cmax = 1;
+  for (int m = 0; m < n_maps; ++m) cmax = std::max<int64_t>(cmax, (int64_t)frames[m].rows * frames[m].cols);
+  scan_batch_kernel<<<dim3((unsigned)((cmax + 255) / 256), 2, n_maps), 256, 0, ctx->stream>>>(dd);
+  if (int rc = check_launch(ctx, "scan_batch_kernel")) return rc;
+  ctx->keys_tag[0] = -2;
+  ctx->keys_tag[1] = tagi;
+  return PCT_OK;
+}
+
+// bounds without the host synchronisation: the 7 keys land in keys_host
+// (pinned; decode with bounds_from_keys after the stream is synchronised)
+int launch_bounds_async(pct_ctx *ctx, const void *xyz, int64_t n, int dtype,
+                        unsigned long long *keys_host, const unsigned long long *init_host) {
+  unsigned long long *keys = static_cast<unsigned long long *>(ctx->dsmall);
+  PCT_CUDA(ctx, cudaMemcpyAsync(keys, init_host, 7 * sizeof(unsigned long long),
+                                cudaMemcpyHostToDevice, ctx->stream));
+  if (dtype == PCT_F32)
+    bounds_kernel<float><<<grid_for(ctx, (n + 3) / 4, 256), 256, 0, ctx->stream>>>(
+        static_cast<const float *>(xyz), n, keys);
+  else
+    bounds_kernel<double><<<grid_for(ctx, n, 256), 256, 0, ctx->stream>>>(
+        static_cast<const double *>(xyz), n, keys);
+  if (int rc = check_launch(ctx, "bounds_kernel")) return rc;
+  PCT_CUDA(ctx, cudaMemcpyAsync(keys_host, keys, 7 * sizeof(unsigned long long),
+                                cudaMemcpyDeviceToHost, ctx->stream));
+  return PCT_OK;
+}
+
+bool bounds_from_keys(const unsigned long long *k, double lo[3], double hi[3]) {
+  for (int c = 0; c < 3; ++c) {
+    lo[c] = dkey_inv(k[c]);
+    hi[c] = dkey_inv(k[3 + c]);
+  }
+  return k[6] == 0;  // no non-finite coordinate
 }
 
 int launch_build(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, const pct_frame &fr,

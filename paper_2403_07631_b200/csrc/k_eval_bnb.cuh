@@ -198,8 +198,7 @@ __device__ __forceinline__ void slow_classes(const float *__restrict__ ctr, floa
 // (the output tile lives in shared memory and is stored every slice).
 template <int R, int PR, int TH, int TW, int NT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) resolve_inflate_bnb_kernel(
-    const __grid_constant__ CUtensorMap enc_map, const uint32_t *__restrict__ bits_in, int rows,
-    int cols, int S, int run, int64_t words, float *__restrict__ cost) {
+    const EvalMap *__restrict__ maps, const int *__restrict__ item_off, int n_maps) {
   using G = BnbGeom<R, PR, TH, TW>;
   constexpr int NWARP = NT / 32;
   constexpr int WSEG = TH * TW / NWARP;  // list entries per warp (its P2 outputs)
@@ -215,36 +214,57 @@ __global__ void __launch_bounds__(NT, MINB) resolve_inflate_bnb_kernel(
   unsigned char *chg = smem + G::O_CB;
   unsigned char *dirty = smem + G::O_DB;
   uint64_t *bar = reinterpret_cast<uint64_t *>(smem + G::O_BAR);  // [3]
-  int *slot = reinterpret_cast<int *>(smem + G::O_BAR + 32);      // [3][2]
-  int *wcnt = reinterpret_cast<int *>(smem + G::O_BAR + 64);      // [NWARP]
+  int *slot = reinterpret_cast<int *>(smem + G::O_BAR + 32);      // [3][3]
+  int *wcnt = reinterpret_cast<int *>(smem + G::O_BAR + 72);      // [NWARP]
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   uint16_t *wlist = slist + warp * WSEG;
   if (tid == 0 && (smem_u32(smem) & 127u) != 0u) __trap();
-  const int tx = (cols + TW - 1) / TW, ty = (rows + TH - 1) / TH;
-  const int tiles = tx * ty;
-  const int nruns = (S + run - 1) / run;
-  const int n_items = tiles * nruns;
-  const int64_t cells = (int64_t)rows * cols;
+  // work items: (map, run of slices, tile), maps concatenated (item_off:
+  // first item of each map); a single map is a batch of one
+  const int n_items = item_off[n_maps];
+  auto decode = [&](int g, int &m, int &r, int &t) {
+    int lo = 0, hi = n_maps - 1;  // last m with item_off[m] <= g
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (item_off[mid] <= g) lo = mid;
+      else hi = mid - 1;
+    }
+    m = lo;
+    const EvalMap &M = maps[m];
+    const int tiles = ((M.cols + TW - 1) / TW) * ((M.rows + TH - 1) / TH);
+    const int local = g - item_off[m];
+    r = local / tiles;
+    t = local - r * tiles;
+  };
   constexpr uint32_t BOX_BYTES = G::CH * G::CW * 4;
   const float w0 = c_bw[0], w1 = c_bw[1];
   const uint32_t cb_bits = f32_bits((float)c_K.c_barrier);
   // thread 0 walks the CTA's step sequence one step ahead of the others:
-  // step = (item, slice); it records the tile origin and slice of each step
-  // in the slot of the buffer it loads
-  int nx_item = blockIdx.x, nx_k = (blockIdx.x / tiles) * run;
+  // step = (item, slice); it records the map, tile origin and slice of each
+  // step in the slot of the buffer it loads
+  int nx_item = blockIdx.x, nx_k = 0, nx_m = 0, nx_r = 0, nx_t = 0;
+  if (nx_item < n_items) {
+    decode(nx_item, nx_m, nx_r, nx_t);
+    nx_k = nx_r * maps[nx_m].run;
+  }
   auto issue = [&](int buf) {
-    const int r = nx_item / tiles, t = nx_item - r * tiles;
-    const int ti = t / tx;
-    const int i0 = ti * TH, j0 = (t - ti * tx) * TW;
-    slot[buf * 2] = i0 * 65536 + j0 / TW;  // rows < 2^15, tiles of >= 32 columns
-    slot[buf * 2 + 1] = nx_k | ((nx_k == r * run) ? 0x40000000 : 0);  // first slice of its run
+    const EvalMap &M = maps[nx_m];
+    const int tx = (M.cols + TW - 1) / TW;
+    const int ti = nx_t / tx;
+    const int i0 = ti * TH, j0 = (nx_t - ti * tx) * TW;
+    slot[buf * 3] = i0 * 65536 + j0 / TW;  // rows < 2^15, tiles of >= 32 columns
+    slot[buf * 3 + 1] = nx_k | ((nx_k == nx_r * M.run) ? 0x40000000 : 0);  // first of its run
+    slot[buf * 3 + 2] = nx_m;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     mbar_expect_tx(&bar[buf], BOX_BYTES);
-    tma_load_3d(smem + G::O_BUF + buf * G::BUF, &enc_map, &bar[buf], j0, i0, nx_k);
-    if (++nx_k >= min(S, (r + 1) * run)) {
+    tma_load_3d(smem + G::O_BUF + buf * G::BUF, &M.tmap, &bar[buf], j0, i0, nx_k);
+    if (++nx_k >= min(M.S, (nx_r + 1) * M.run)) {
       nx_item += gridDim.x;
-      nx_k = (nx_item / tiles) * run;
+      if (nx_item < n_items) {
+        decode(nx_item, nx_m, nx_r, nx_t);
+        nx_k = nx_r * maps[nx_m].run;
+      }
     }
   };
   if (tid == 0) {
@@ -256,23 +276,29 @@ __global__ void __launch_bounds__(NT, MINB) resolve_inflate_bnb_kernel(
   __syncthreads();
   int steps = 0;  // this CTA's total
   for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-    const int r = item / tiles;
-    steps += min(S, (r + 1) * run) - r * run;
+    int m, r, t;
+    decode(item, m, r, t);
+    steps += min(maps[m].S, (r + 1) * maps[m].run) - r * maps[m].run;
   }
   uint32_t phase_bits = 0u;
   for (int st = 0; st < steps; ++st) {
     const int cur = st % 3, prv = (st + 2) % 3;
     float *ci = reinterpret_cast<float *>(smem + G::O_BUF + cur * G::BUF);
     const float *cp = reinterpret_cast<const float *>(smem + G::O_BUF + prv * G::BUF);
-    const int i0 = slot[cur * 2] >> 16, j0 = (slot[cur * 2] & 0xFFFF) * TW;
-    const int k = slot[cur * 2 + 1] & 0x3FFFFFFF;
-    const bool first = (slot[cur * 2 + 1] & 0x40000000) != 0;
+    const int i0 = slot[cur * 3] >> 16, j0 = (slot[cur * 3] & 0xFFFF) * TW;
+    const int k = slot[cur * 3 + 1] & 0x3FFFFFFF;
+    const bool first = (slot[cur * 3 + 1] & 0x40000000) != 0;
+    const EvalMap &M = maps[slot[cur * 3 + 2]];
+    const int rows = M.rows, cols = M.cols;
+    const int64_t cells = (int64_t)rows * cols, words = M.words;
+    const uint32_t *bits_in = M.bits;
+    float *cost = M.cost;
     // the buffer of step st-2 (read as `prv` by step st-1) is free again
     if (tid == 0 && st + 1 < steps) issue((st + 1) % 3);
     // ---- P0a: gentle bits of the window region (bit x of word w = gentle
     // column 32w + x, gentle column 0 = c_init column -r); resets
     const uint32_t *bk = bits_in + (int64_t)k * words;
-    const int wpr = (cols + 31) / 32;
+    const int wpr = M.wpr;
     for (int idx = tid; idx < G::GH * G::GWW; idx += NT) {
       const int y = idx / G::GWW, w = idx - y * G::GWW;
       const int gi = i0 - R - PR + y;

@@ -69,10 +69,11 @@ __device__ __forceinline__ uint32_t gentle_word(const uint32_t *__restrict__ bk,
 // Loads run PF slices ahead; left / right neighbours come from the adjacent
 // lanes (lanes 0 and 31 load the cell beyond), grid borders read NaN.
 template <int PF>
-__global__ void __launch_bounds__(kWalkNT) terrain_walk_kernel(
-    const float *__restrict__ ground, const float *__restrict__ ceiling, int S, int rows,
-    int cols, float *__restrict__ enc_out, EncLayout L, uint32_t *__restrict__ bits_out,
-    int wpr) {
+__device__ __forceinline__ void walk_body(const float *__restrict__ ground,
+                                          const float *__restrict__ ceiling, int S, int rows,
+                                          int cols, float *__restrict__ enc_out,
+                                          const EncLayout &L, uint32_t *__restrict__ bits_out,
+                                          int wpr) {
   const int64_t cells = (int64_t)rows * cols;
   // threads index row-padded columns: warp = one gentle-bitmap word of one row
   const int64_t pidx = (int64_t)blockIdx.x * kWalkNT + threadIdx.x;
@@ -163,6 +164,33 @@ __global__ void __launch_bounds__(kWalkNT) terrain_walk_kernel(
       pb += (int64_t)rows * wpr;
     }
   }
+}
+
+template <int PF>
+__global__ void __launch_bounds__(kWalkNT) terrain_walk_kernel(
+    const float *__restrict__ ground, const float *__restrict__ ceiling, int S, int rows,
+    int cols, float *__restrict__ enc_out, EncLayout L, uint32_t *__restrict__ bits_out,
+    int wpr) {
+  walk_body<PF>(ground, ceiling, S, rows, cols, enc_out, L, bits_out, wpr);
+}
+
+// per-map arguments of the split evaluation (a single map is a batch of one)
+struct EvalMap {
+  CUtensorMap tmap;  // encoded c_init stack (TMA), 64-byte aligned first member
+  const float *ground, *ceiling;
+  float *enc, *cost;
+  uint32_t *bits;
+  EncLayout L;
+  int S, rows, cols, wpr, run;
+  int64_t words;  // gentle bitmap words per slice
+};
+
+// walk over a batch: blockIdx.y = map; blocks past the map's extent leave
+template <int PF>
+__global__ void __launch_bounds__(kWalkNT) terrain_walk_batch_kernel(const EvalMap *__restrict__ maps) {
+  const EvalMap &m = maps[blockIdx.y];
+  if ((int64_t)blockIdx.x * kWalkNT >= (int64_t)m.rows * m.wpr * 32) return;  // whole block
+  walk_body<PF>(m.ground, m.ceiling, m.S, m.rows, m.cols, m.enc, m.L, m.bits, m.wpr);
 }
 
 template <int R, int PR, int TH, int TW>

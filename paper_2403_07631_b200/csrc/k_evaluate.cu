@@ -631,7 +631,9 @@ int launch_split(pct_ctx *ctx, const float *ground, const float *ceiling, int S,
   L.pitch = ((int64_t)((cols + TW - 1) / TW * TW + 2 * R) + 3) / 4 * 4;
   L.sstride = (int64_t)L.prows * L.pitch;
   const size_t enc_bytes = (size_t)S * L.sstride * 4;
-  if (int rc = ensure_scratch(ctx, (size_t)S * words * 4)) return rc;
+  // gentle bitmap | (bnb) descriptor of a batch of one, 256-byte aligned
+  if (int rc = ensure_scratch(ctx, (((size_t)S * words * 4 + 255) / 256) * 256 + sizeof(EvalMap) + 128))
+    return rc;
   uint32_t *bits = static_cast<uint32_t *>(ctx->scratch);
   if (ctx->enc_bytes < enc_bytes) {
     if (ctx->enc) {
@@ -709,7 +711,37 @@ int launch_split(pct_ctx *ctx, const float *ground, const float *ceiling, int S,
       const int64_t nitems = tiles * ((S + run - 1) / run);
       if (nitems > INT32_MAX) return fail(ctx, PCT_E_INVALID, "grid too large");
       const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nitems, slots));
-      kb<<<grid, BNT, bsmem, ctx->stream>>>(map, bits, rows, cols, S, run, words, cost);
+      // a batch of one: the descriptor (with its tensor map) and the item
+      // offsets behind the gentle bitmap in the scratch (64-byte aligned)
+      const size_t boff = (((size_t)S * words * 4 + 255) / 256) * 256;
+      EvalMap hm;
+      std::memset(&hm, 0, sizeof(hm));
+      hm.tmap = map;
+      hm.ground = ground;
+      hm.ceiling = ceiling;
+      hm.enc = enc;
+      hm.cost = cost;
+      hm.bits = bits;
+      hm.L = L;
+      hm.S = S;
+      hm.rows = rows;
+      hm.cols = cols;
+      hm.wpr = wpr;
+      hm.run = run;
+      hm.words = words;
+      struct {
+        EvalMap m;
+        int off[2];
+      } desc;
+      static_assert(offsetof(decltype(desc), m) == 0, "descriptor layout");
+      desc.m = hm;
+      desc.off[0] = 0;
+      desc.off[1] = (int)nitems;
+      char *dptr = static_cast<char *>(ctx->scratch) + boff;
+      PCT_CUDA(ctx, cudaMemcpyAsync(dptr, &desc, sizeof(desc), cudaMemcpyHostToDevice, ctx->stream));
+      const EvalMap *dm = reinterpret_cast<const EvalMap *>(dptr);
+      const int *doff = reinterpret_cast<const int *>(dptr + offsetof(decltype(desc), off));
+      kb<<<grid, BNT, bsmem, ctx->stream>>>(dm, doff, 1);
       return check_launch(ctx, "resolve_inflate_bnb_kernel");
      }
     }

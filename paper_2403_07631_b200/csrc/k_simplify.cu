@@ -358,6 +358,52 @@ int simplify_window_table(pct_ctx *ctx, const float *ground, const float *cost, 
   return PCT_OK;
 }
 
+// no host synchronisation: the table / flags land in pinned host memory
+int simplify_window_async(pct_ctx *ctx, const float *ground, const float *cost, int S,
+                          int64_t cells, double eps_e, double c_barrier, uint64_t *table_host) {
+  if (S <= 0) return PCT_OK;
+  SimpArgs A{ground, cost, cells, cells, S, eps_e, (float)c_barrier};
+  const size_t tbytes = (size_t)S * 8;
+  if (tbytes > 65536 - 128) return fail(ctx, PCT_E_INVALID, "too many slices");
+  unsigned long long *table = static_cast<unsigned long long *>(ctx->dsmall);
+  PCT_CUDA(ctx, cudaMemsetAsync(table, 0, tbytes, ctx->stream));
+  if (cells > 0) {
+    PCT_CUDA(ctx, cudaFuncSetAttribute(window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)tbytes));
+    const int64_t blocks_needed = (cells + kWinNT - 1) / kWinNT;
+    const unsigned grid = (unsigned)std::min<int64_t>(blocks_needed, 12LL * ctx->num_sms);
+    window_kernel<<<grid, kWinNT, tbytes, ctx->stream>>>(A, table);
+    if (int rc = check_launch(ctx, "window_kernel")) return rc;
+  }
+  PCT_CUDA(ctx, cudaMemcpyAsync(table_host, table, tbytes, cudaMemcpyDeviceToHost, ctx->stream));
+  return PCT_OK;
+}
+
+int simplify_triples_async(pct_ctx *ctx, const float *ground, const float *cost, int S,
+                           int64_t cells, double eps_e, double c_barrier, const int32_t *tri_host,
+                           int n, int32_t *flags_host) {
+  if (n <= 0) return PCT_OK;
+  SimpArgs A{ground, cost, cells, cells, S, eps_e, (float)c_barrier};
+  const size_t need = (size_t)n * (sizeof(Triple) + sizeof(int)) + 64;
+  if (need > 65536 - 128) return fail(ctx, PCT_E_INVALID, "too many triples in one batch");
+  char *dbase = static_cast<char *>(ctx->dsmall);
+  Triple *dtr = reinterpret_cast<Triple *>(dbase);
+  int *dflags = reinterpret_cast<int *>(dbase + (size_t)n * sizeof(Triple));
+  static_assert(sizeof(Triple) == 3 * sizeof(int32_t), "triple layout");
+  PCT_CUDA(ctx, cudaMemcpyAsync(dtr, tri_host, sizeof(Triple) * n, cudaMemcpyHostToDevice,
+                                ctx->stream));
+  PCT_CUDA(ctx, cudaMemsetAsync(dflags, 0, sizeof(int) * n, ctx->stream));
+  if (cells > 0) {
+    int64_t bx = (cells + 255) / 256;
+    if (bx > 2LL * ctx->num_sms) bx = 2LL * ctx->num_sms;
+    triples_kernel<<<dim3((unsigned)bx, n), 256, 0, ctx->stream>>>(A, dtr, dflags);
+    if (int rc = check_launch(ctx, "triples_kernel")) return rc;
+  }
+  PCT_CUDA(ctx, cudaMemcpyAsync(flags_host, dflags, sizeof(int) * n, cudaMemcpyDeviceToHost,
+                                ctx->stream));
+  return PCT_OK;
+}
+
 int simplify_triple_flags(pct_ctx *ctx, const float *ground, const float *cost, int S,
                           int64_t cells, int64_t stride, double eps_e, double c_barrier,
                           const int32_t *triples, int n, int32_t *flags_host) {

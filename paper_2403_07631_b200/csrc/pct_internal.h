@@ -25,6 +25,8 @@ struct pct_ctx {
   size_t staging_bytes = 0;
   void *pinned_io = nullptr;  // pinned double buffer of the PCD file reader
   size_t pinned_io_bytes = 0;
+  void *pinned_batch = nullptr;  // per-map result slots of pct_tomo_run_batch
+  size_t pinned_batch_bytes = 0;
   // small device/pinned buffers for reductions and flags
   void *dsmall = nullptr;   // 64 KiB device
   void *hsmall = nullptr;   // 64 KiB pinned host
@@ -85,6 +87,23 @@ int launch_unique_mask(pct_ctx *ctx, const float *ground, const float *cost, int
                        uint8_t *mask);
 
 EvalConsts make_consts(const pct_trav_params &p, double r_g);
+
+// asynchronous pieces of the whole-pipeline call (results land in pinned
+// host memory; the caller synchronises the stream) used by pct_tomo_run_batch
+int launch_bounds_async(pct_ctx *ctx, const void *xyz, int64_t n, int dtype,
+                        unsigned long long *keys_host, const unsigned long long *init_host);
+bool bounds_from_keys(const unsigned long long *keys, double lo[3], double hi[3]);
+// batched maps: one launch per stage (keys_host: 8 u64 per map, pinned)
+int launch_bounds_batch(pct_ctx *ctx, int n_maps, const void *const *xyz, const int64_t *n,
+                        int dtype, unsigned long long *keys_host);
+int launch_build_batch(pct_ctx *ctx, int n_maps, const void *const *xyz, const int64_t *n,
+                       int dtype, const pct_frame *frames, const double *const *heights,
+                       float *const *ground, float *const *ceiling);
+int simplify_window_async(pct_ctx *ctx, const float *ground, const float *cost, int S,
+                          int64_t cells, double eps_e, double c_barrier, uint64_t *table_host);
+int simplify_triples_async(pct_ctx *ctx, const float *ground, const float *cost, int S,
+                           int64_t cells, double eps_e, double c_barrier, const int32_t *tri_host,
+                           int n, int32_t *flags_host);
 
 // evaluate modes for the per-op entry points
 enum EvalMode { kEvalFull = 0, kEvalGroundCost = 1, kEvalInterval = 2, kEvalCinit = 3 };
