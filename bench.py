@@ -355,6 +355,8 @@ def run_b200(args):
         wstreams = [torch.cuda.Stream(device=local) for _ in range(nw)]
         runner = BatchRunner(local, workers=nw, streams=[s.cuda_stream for s in wstreams])
         batch_maps = [(dm.ptr, len(m), _lib.PCT_F32, 0) for dm, m in zip(dmaps, maps)]
+        bctx = runner.ctxs[0]  # the batched native call runs on the first context
+        bctx.check(bctx.lib.pct_set_timing(bctx.h, 1), "set_timing")
 
     def step():
         """One pass of the path over this rank's data; returns per-stage (start, end) events."""
@@ -368,7 +370,10 @@ def run_b200(args):
                 ew.record(s)
                 stream.wait_event(ew)
             e1 = pipe.ev()
-            return {"total": [(e0, e1)]}
+            st = (C.c_float * 3)()  # the batch's own stage events (one launch per stage)
+            bctx.check(bctx.lib.pct_last_stage_ms(bctx.h, st), "stage_ms")
+            return {"total": [(e0, e1)], "bounds+build": [float(st[0])],
+                    "evaluate": [float(st[1])], "simplify": [float(st[2])]}
         if args.mode == "sharded":
             with torch.cuda.stream(stream):
                 e0 = pipe.ev()
@@ -434,14 +439,9 @@ def run_b200(args):
     ms = step_ms / args.steps
     value = total_pts * args.steps / (step_ms * 1e3)  # Mpts/s, whole job
 
-    if args.mode == "batch":  # per-kernel numbers from single-map passes (first map)
-        per_ev = []
-        for _ in range(3):
-            flush_l2()
-            _, ms = pipe.run_native(dmaps[0], len(maps[0]))
-            per_ev.append(ms[1])
-        per["evaluate"] = [min(per_ev) * len(maps)]
+    if args.mode == "batch":
         runner.close()
+        pipe.run_native(dmaps[0], len(maps[0]))  # grid of map 0 for the line (untimed)
     info = band_info if args.mode == "sharded" else pipe.info
     S, R, Cc = info["S"], info["R"], info["C"]
     cs = S * R * Cc

@@ -4,10 +4,10 @@ Small maps are latency-bound: one map's pipeline is a handful of short
 kernels separated by host round trips (grid frame after the bounds, simplify
 sweep).  ``BatchRunner`` owns ``workers`` libpct contexts (a CUDA stream and
 scratch each).  Device-resident batches go through one native call,
-``pct_tomo_run_batch``, which issues the maps phase by phase over the
-contexts with one synchronisation per phase (bounds; build + evaluate +
-simplify table; triple rounds); host-resident ones run one ``pct_tomo_run``
-per map on a thread pool (ctypes releases the GIL), so the syncs of one map
+``pct_tomo_run_batch``, that runs every stage as ONE launch over all maps
+(bounds; build; evaluate; simplify tables; triple rounds) with one host
+synchronisation per phase; host-resident ones run one ``pct_tomo_run`` per
+map on a thread pool (ctypes releases the GIL), so the syncs of one map
 overlap the kernels of the others.  Maps never communicate ("batches of independent maps are
 distributed without communication"); across GPUs each rank takes its share.
 
@@ -76,40 +76,25 @@ class BatchRunner:
         return [f.result() for f in futs]
 
     def _run_batch(self, maps, d_s, r_g, params, eps_e, c_barrier, keep_handles):
-        """Map groups (map m -> worker m % workers), each driven phase by phase
-        by one pct_tomo_run_batch call on its own context from the pool."""
+        """One pct_tomo_run_batch call: one launch per stage for every map."""
         n = len(maps)
         w = np.ascontiguousarray(build_kernel(params.d_inf, params.d_sm, r_g).weights)
         pc = _lib.trav_params_c(params, r_g)
-        nw = len(self.ctxs)
-        code = maps[0][2]
+        ctx = self.ctxs[0]
+        hs = (C.c_void_p * 1)(ctx.h)
+        ptrs = (C.c_void_p * n)(*[int(m[0]) for m in maps])
+        npts = np.asarray([int(m[1]) for m in maps], np.int64)
         stride = 4096
-
-        def group(g):
-            idx = list(range(g, n, nw))
-            if not idx:
-                return []
-            ctx = self.ctxs[g]
-            hs = (C.c_void_p * 1)(ctx.h)
-            ptrs = (C.c_void_p * len(idx))(*[int(maps[m][0]) for m in idx])
-            npts = np.asarray([int(maps[m][1]) for m in idx], np.int64)
-            keep = np.empty((len(idx), stride), np.int32)
-            nk = np.empty(len(idx), np.int32)
-            handles = (C.c_void_p * len(idx))() if keep_handles else None
-            rc = ctx.lib.pct_tomo_run_batch(hs, 1, len(idx), ptrs, npts.ctypes.data, code,
-                                            float(d_s), float(r_g), GRID_SIDE_LIMIT, C.byref(pc),
-                                            w.ctypes.data, w.shape[0], float(eps_e),
-                                            float(c_barrier), handles, keep.ctypes.data, stride,
-                                            nk.ctypes.data)
-            ctx.check(rc, "pct_tomo_run_batch")
-            return [(m, (ctx, C.c_void_p(handles[i])) if keep_handles else None,
-                     keep[i, :nk[i]].tolist()) for i, m in enumerate(idx)]
-
-        res = [None] * n
-        for part in self.pool.map(group, range(nw)):
-            for m, h, ks in part:
-                res[m] = (h, ks)
-        return res
+        keep = np.empty((n, stride), np.int32)
+        nk = np.empty(n, np.int32)
+        handles = (C.c_void_p * n)() if keep_handles else None
+        rc = ctx.lib.pct_tomo_run_batch(hs, 1, n, ptrs, npts.ctypes.data, maps[0][2], float(d_s),
+                                        float(r_g), GRID_SIDE_LIMIT, C.byref(pc), w.ctypes.data,
+                                        w.shape[0], float(eps_e), float(c_barrier), handles,
+                                        keep.ctypes.data, stride, nk.ctypes.data)
+        ctx.check(rc, "pct_tomo_run_batch")
+        return [((ctx, C.c_void_p(handles[m])) if keep_handles else None,
+                 keep[m, :nk[m]].tolist()) for m in range(n)]
 
     def close(self):
         self.pool.shutdown()

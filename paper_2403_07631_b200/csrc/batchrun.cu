@@ -1,19 +1,17 @@
 // batchrun.cu — pct_tomo_run_batch: the whole hot path for many independent
-// maps (BASELINE config 4) from one host thread.
+// maps (BASELINE config 4) with one launch per stage for the whole batch.
 //
-// pct_tomo_run synchronises three times per map (bounds -> grid frame, the
-// simplify table, triple batches).  Here the maps are spread over several
-// contexts (one CUDA stream and one set of scratch buffers each; map m goes
-// to context m % n_ctx) and the work is issued phase by phase, so each phase
-// costs one synchronisation for the whole batch:
-//   1  bounds of every map (keys into pinned per-map slots)       -> sync
-//   2  frames on the host; build + evaluate + simplify window table of every
-//      map (tables into pinned slots)                             -> sync
-//   3  rounds of the simplify replay: every map whose sweep needs triples the
-//      table cannot answer posts them; one triples launch per such map,
-//      one sync per round (SweepState replays simplify.py:59-70 exactly as
-//      run_simplify does)
-// Within a context, stream order protects its scratch buffers between maps.
+// A small map (config 0/4: 250k points, 203 x 204 x 13) fills a fraction of
+// the GPU per kernel and pct_tomo_run adds three host synchronisations per
+// map.  Here each stage runs once over every map of a group (descriptor
+// arrays in device memory; blockIdx.y or flattened work items pick the map):
+//   1  bounds (one launch)                                          -> sync
+//   2  frames on the host; build (scatter + scan), evaluate (walk +
+//      branch-and-bound resolve/inflate), simplify window tables, one launch
+//      each                                                         -> sync
+//   3  simplify replays on the host (SweepState, exactly as run_simplify);
+//      each round's triples of every map in one launch              -> sync
+// Results equal pct_tomo_run map by map (tests/test_gpu_parity.py).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -130,47 +128,28 @@ int ensure_pinned(pct_ctx *ctx, size_t bytes) {
 
 using namespace pct;
 
-extern "C" int pct_tomo_run_batch(pct_ctx **ctxs, int32_t n_ctx, int32_t n_maps,
-                                  const void *const *xyz, const int64_t *n_points, int dtype,
-                                  double d_s, double r_g, int64_t max_grid_side,
-                                  const pct_trav_params *p, const float *kernel_w, int32_t kside,
-                                  double eps_e, double c_barrier, pct_tomo **out,
-                                  int32_t *keep_host, int32_t keep_stride, int32_t *n_keep) {
-  if (!ctxs || n_ctx <= 0 || !ctxs[0]) return PCT_E_INVALID;
-  pct_ctx *c0 = ctxs[0];
-  if (n_maps < 0 || !xyz || !n_points || !p || !kernel_w || !keep_host || !n_keep ||
-      keep_stride <= 0 || (dtype != PCT_F32 && dtype != PCT_F64))
-    return fail(c0, PCT_E_INVALID, "bad arguments to pct_tomo_run_batch");
-  if (!(d_s > 0) || !(r_g > 0)) return fail(c0, PCT_E_INVALID, "d_s and r_g must be positive");
-  for (int c = 0; c < n_ctx; ++c)
-    if (!ctxs[c] || ctxs[c]->device != c0->device)
-      return fail(c0, PCT_E_INVALID, "batch contexts must share one device");
-  PCT_CUDA(c0, cudaSetDevice(c0->device));
-  for (int m = 0; m < n_maps; ++m)
-    if (n_points[m] <= 0) return fail(c0, PCT_E_EMPTY, "zero valid points");
-  auto ctx_of = [&](int m) { return ctxs[m % n_ctx]; };
+namespace {
 
-  // pinned slots: init keys | bounds keys (8 u64 per map) | tables | triples
-  // | flags (tables / triples sized once the frames are known)
-  const size_t bounds_bytes = 64 + (size_t)n_maps * 64;
-  if (int rc = ensure_pinned(c0, bounds_bytes)) return rc;
-  unsigned long long *init = static_cast<unsigned long long *>(c0->pinned_batch);
-  const unsigned long long init_v[7] = {~0ull, ~0ull, ~0ull, 0ull, 0ull, 0ull, 0ull};
-  std::memcpy(init, init_v, sizeof(init_v));
-  // 1. bounds
-  for (int m = 0; m < n_maps; ++m) {
-    unsigned long long *slot = init + 8 + 8 * (size_t)m;
-    if (int rc = launch_bounds_async(ctx_of(m), xyz[m], n_points[m], dtype, slot, init))
-      return rc;
-  }
-  if (int rc = sync_all(ctxs, n_ctx)) return rc;
-  // 2. frames, build, evaluate, simplify window table
+// one group of <= kGroup maps: every stage is one launch for the whole group
+constexpr int kGroup = 512;
+
+int run_group(pct_ctx *c0, int n_maps, const void *const *xyz, const int64_t *n_points,
+              int dtype, double d_s, double r_g, int64_t max_grid_side, const pct_trav_params *p,
+              const float *kernel_w, int32_t kside, double eps_e, double c_barrier,
+              pct_tomo **out, int32_t *keep_host, int32_t keep_stride, int32_t *n_keep) {
+  // 1. bounds (one launch, keys into pinned slots)
+  if (c0->timing) cudaEventRecord(c0->ev[0], c0->stream);  // stage events as pct_tomo_run
+  if (int rc = ensure_pinned(c0, (size_t)n_maps * 64 + 64)) return rc;
+  unsigned long long *bk = static_cast<unsigned long long *>(c0->pinned_batch);
+  if (int rc = launch_bounds_batch(c0, n_maps, xyz, n_points, dtype, bk)) return rc;
+  PCT_CUDA(c0, cudaStreamSynchronize(c0->stream));
+  // 2. frames; build, evaluate, simplify tables: one launch per stage
   std::vector<pct_frame> frames(n_maps);
   std::vector<std::vector<double>> heights(n_maps);
   int max_S = 1;
   for (int m = 0; m < n_maps; ++m) {
     double lo[3], hi[3];
-    if (!bounds_from_keys(init + 8 + 8 * (size_t)m, lo, hi))
+    if (!bounds_from_keys(bk + 8 * (size_t)m, lo, hi))
       return fail(c0, PCT_E_NONFINITE, "point cloud contains non-finite coordinates");
     const int rc = pct_frame_compute(lo, hi, d_s, r_g, max_grid_side, &frames[m], nullptr, 0);
     if (rc == PCT_E_GRID)
@@ -184,52 +163,61 @@ extern "C" int pct_tomo_run_batch(pct_ctx **ctxs, int32_t n_ctx, int32_t n_maps,
     max_S = std::max(max_S, frames[m].n_slices);
   }
   if (max_S > keep_stride) return fail(c0, PCT_E_INVALID, "keep_stride below the slice count");
-  // tables (S u64 per map) | triples (3 S i32 per map) | flags (S i32 per map);
-  // the bounds slots are no longer needed
-  const size_t tab_b = (size_t)n_maps * max_S * 8, tri_b = (size_t)n_maps * max_S * 12,
-               flg_b = (size_t)n_maps * max_S * 4;
-  if (int rc = ensure_pinned(c0, tab_b + tri_b + flg_b + 256)) return rc;
-  char *pb = static_cast<char *>(c0->pinned_batch);
-  uint64_t *tables = reinterpret_cast<uint64_t *>(pb);
-  int32_t *tris = reinterpret_cast<int32_t *>(pb + tab_b);
-  int32_t *flags = reinterpret_cast<int32_t *>(pb + tab_b + tri_b);
   std::vector<pct_tomo *> toms(n_maps, nullptr);
   auto free_all = [&]() {
     for (int m = 0; m < n_maps; ++m)
-      if (toms[m]) pct_tomo_free(ctx_of(m), toms[m]);
+      if (toms[m]) pct_tomo_free(c0, toms[m]);
   };
+  std::vector<float *> g(n_maps), c(n_maps), co(n_maps);
+  std::vector<const double *> hp(n_maps);
+  std::vector<int> Sv(n_maps);
+  std::vector<int64_t> cells(n_maps);
   for (int m = 0; m < n_maps; ++m) {
-    pct_ctx *ctx = ctx_of(m);
     const pct_frame &fr = frames[m];
-    int rc = tomo_alloc(ctx, fr, &toms[m]);
-    if (rc) {
+    if (int rc = tomo_alloc(c0, fr, &toms[m])) {
       free_all();
       return rc;
     }
     pct_tomo *t = toms[m];
     t->heights = heights[m];
     const size_t bytes = (size_t)fr.n_slices * fr.rows * fr.cols * sizeof(float);
-    if (cudaMallocAsync(reinterpret_cast<void **>(&t->cost), bytes, ctx->stream) != cudaSuccess) {
+    if (cudaMallocAsync(reinterpret_cast<void **>(&t->cost), bytes, c0->stream) != cudaSuccess) {
       free_all();
       return fail(c0, PCT_E_NOMEM, "cudaMallocAsync(cost)");
     }
-    if ((rc = launch_build(ctx, xyz[m], n_points[m], dtype, fr, t->heights.data(), t->ground,
-                           t->ceiling)) ||
-        (rc = launch_evaluate(ctx, t->ground, t->ceiling, fr.n_slices, fr.rows, fr.cols, fr.r_g,
-                              *p, kernel_w, kside, t->cost, kEvalFull)) ||
-        (rc = simplify_window_async(ctx, t->ground, t->cost, fr.n_slices,
-                                    (int64_t)fr.rows * fr.cols, eps_e, c_barrier,
-                                    tables + (size_t)m * max_S))) {
-      if (ctx != c0) c0->err = ctx->err;
-      free_all();
-      return rc;
-    }
+    g[m] = t->ground;
+    c[m] = t->ceiling;
+    co[m] = t->cost;
+    hp[m] = t->heights.data();
+    Sv[m] = fr.n_slices;
+    cells[m] = (int64_t)fr.rows * fr.cols;
   }
-  if (int rc = sync_all(ctxs, n_ctx)) {
+  // pinned: tables (S_max u64 per map) | triples (4 x S_max i32 per map) |
+  // flags (S_max i32 per map); the bounds keys are consumed
+  const size_t tab_b = (size_t)n_maps * max_S * 8, tri_b = (size_t)n_maps * max_S * 16,
+               flg_b = (size_t)n_maps * max_S * 4;
+  if (int rc = ensure_pinned(c0, tab_b + tri_b + flg_b + 256)) {
     free_all();
     return rc;
   }
-  // 3. simplify replays, triple batches in rounds
+  char *pb = static_cast<char *>(c0->pinned_batch);
+  uint64_t *tables = reinterpret_cast<uint64_t *>(pb);
+  int32_t *tris = reinterpret_cast<int32_t *>(pb + tab_b);
+  int32_t *flags = reinterpret_cast<int32_t *>(pb + tab_b + tri_b);
+  int rc = launch_build_batch(c0, n_maps, xyz, n_points, dtype, frames.data(), hp.data(), g.data(),
+                              c.data());
+  if (!rc && c0->timing) cudaEventRecord(c0->ev[1], c0->stream);
+  if (!rc) rc = launch_evaluate_batch(c0, n_maps, g.data(), c.data(), frames.data(), *p, kernel_w,
+                                      kside, co.data());
+  if (!rc && c0->timing) cudaEventRecord(c0->ev[2], c0->stream);
+  if (!rc) rc = simplify_window_batch(c0, n_maps, g.data(), co.data(), Sv.data(), cells.data(),
+                                     max_S, eps_e, c_barrier, tables);
+  if (!rc && cudaStreamSynchronize(c0->stream) != cudaSuccess) rc = fail(c0, PCT_E_CUDA, "sync");
+  if (rc) {
+    free_all();
+    return rc;
+  }
+  // 3. simplify replays; each round's triples of every map in one launch
   std::vector<SweepState> sw(n_maps);
   for (int m = 0; m < n_maps; ++m) {
     sw[m].S = frames[m].n_slices;
@@ -237,43 +225,67 @@ extern "C" int pct_tomo_run_batch(pct_ctx **ctxs, int32_t n_ctx, int32_t n_maps,
     for (int k = 0; k < sw[m].S; ++k) sw[m].keep.push_back(k);
   }
   std::vector<std::vector<int32_t>> need(n_maps);
+  std::vector<int> first(n_maps);
   for (;;) {
-    bool any = false;
+    int total = 0;
     for (int m = 0; m < n_maps; ++m) {
-      if (sw[m].done) continue;
-      if (sw[m].run(need[m])) continue;
-      const int n = (int)(need[m].size() / 3);
-      if (n == 0) continue;  // cannot happen: a miss always yields its own triple
-      std::memcpy(tris + (size_t)m * max_S * 3, need[m].data(), need[m].size() * 4);
-      pct_ctx *ctx = ctx_of(m);
-      const pct_frame &fr = frames[m];
-      if (int rc = simplify_triples_async(ctx, toms[m]->ground, toms[m]->cost, fr.n_slices,
-                                          (int64_t)fr.rows * fr.cols, eps_e, c_barrier,
-                                          tris + (size_t)m * max_S * 3, n,
-                                          flags + (size_t)m * max_S)) {
-        free_all();
-        return rc;
+      first[m] = total;
+      if (sw[m].done || sw[m].run(need[m])) {
+        need[m].clear();
+        continue;
       }
-      any = true;
+      for (size_t i = 0; i < need[m].size() / 3; ++i) {
+        int32_t *t = tris + 4 * (size_t)(total++);
+        t[0] = need[m][3 * i];
+        t[1] = need[m][3 * i + 1];
+        t[2] = need[m][3 * i + 2];
+        t[3] = m;
+      }
     }
-    if (!any) break;
-    if (int rc = sync_all(ctxs, n_ctx)) {
+    if (total == 0) break;
+    if ((rc = simplify_triples_batch(c0, n_maps, total, tris, flags)) ||
+        cudaStreamSynchronize(c0->stream) != cudaSuccess) {
       free_all();
-      return rc;
+      return rc ? rc : fail(c0, PCT_E_CUDA, "sync");
     }
     for (int m = 0; m < n_maps; ++m)
-      if (!sw[m].done && !need[m].empty()) sw[m].feed(need[m], flags + (size_t)m * max_S);
+      if (!need[m].empty()) sw[m].feed(need[m], flags + first[m]);
   }
+  if (c0->timing) cudaEventRecord(c0->ev[3], c0->stream);
   for (int m = 0; m < n_maps; ++m) {
     n_keep[m] = (int32_t)sw[m].keep.size();
     for (size_t i = 0; i < sw[m].keep.size(); ++i)
       keep_host[(size_t)m * keep_stride + i] = sw[m].keep[i];
-    if (out) {
-      out[m] = toms[m];
-    } else {
-      pct_tomo_free(ctx_of(m), toms[m]);
-    }
+    if (out) out[m] = toms[m];
+    else pct_tomo_free(c0, toms[m]);
     toms[m] = nullptr;
+  }
+  return PCT_OK;
+}
+
+}  // namespace
+
+extern "C" int pct_tomo_run_batch(pct_ctx **ctxs, int32_t n_ctx, int32_t n_maps,
+                                  const void *const *xyz, const int64_t *n_points, int dtype,
+                                  double d_s, double r_g, int64_t max_grid_side,
+                                  const pct_trav_params *p, const float *kernel_w, int32_t kside,
+                                  double eps_e, double c_barrier, pct_tomo **out,
+                                  int32_t *keep_host, int32_t keep_stride, int32_t *n_keep) {
+  if (!ctxs || n_ctx <= 0 || !ctxs[0]) return PCT_E_INVALID;
+  pct_ctx *c0 = ctxs[0];
+  if (n_maps < 0 || !xyz || !n_points || !p || !kernel_w || !keep_host || !n_keep ||
+      keep_stride <= 0 || (dtype != PCT_F32 && dtype != PCT_F64))
+    return fail(c0, PCT_E_INVALID, "bad arguments to pct_tomo_run_batch");
+  if (!(d_s > 0) || !(r_g > 0)) return fail(c0, PCT_E_INVALID, "d_s and r_g must be positive");
+  PCT_CUDA(c0, cudaSetDevice(c0->device));
+  for (int m = 0; m < n_maps; ++m)
+    if (n_points[m] <= 0) return fail(c0, PCT_E_EMPTY, "zero valid points");
+  for (int m0 = 0; m0 < n_maps; m0 += kGroup) {
+    const int nm = std::min(kGroup, n_maps - m0);
+    if (int rc = run_group(c0, nm, xyz + m0, n_points + m0, dtype, d_s, r_g, max_grid_side, p,
+                           kernel_w, kside, eps_e, c_barrier, out ? out + m0 : nullptr,
+                           keep_host + (size_t)m0 * keep_stride, keep_stride, n_keep + m0))
+      return rc;
   }
   return PCT_OK;
 }

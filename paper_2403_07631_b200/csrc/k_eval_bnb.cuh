@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(NT, MINB) resolve_inflate_bnb_kernel(
   // thread 0 walks the CTA's step sequence one step ahead of the others:
   // step = (item, slice); it records the map, tile origin and slice of each
   // step in the slot of the buffer it loads
-  int nx_item = blockIdx.x, nx_k = 0, nx_m = 0, nx_r = 0, nx_t = 0;
+  int nx_item = blockIdx.x, nx_k = 0, nx_m = 0, nx_r = 0, nx_t = 0, acq_m = -1;
   if (nx_item < n_items) {
     decode(nx_item, nx_m, nx_r, nx_t);
     nx_k = nx_r * maps[nx_m].run;
@@ -257,6 +257,14 @@ __global__ void __launch_bounds__(NT, MINB) resolve_inflate_bnb_kernel(
     slot[buf * 3 + 1] = nx_k | ((nx_k == nx_r * M.run) ? 0x40000000 : 0);  // first of its run
     slot[buf * 3 + 2] = nx_m;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    // the tensor map lives in global memory and is rewritten between launches
+    // (possibly at the same address): acquire it for the tensor-map proxy once
+    // per map, so a stale descriptor-cache copy is not used
+    if (nx_m != acq_m) {
+      asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(&M.tmap)
+                   : "memory");
+      acq_m = nx_m;
+    }
     mbar_expect_tx(&bar[buf], BOX_BYTES);
     tma_load_3d(smem + G::O_BUF + buf * G::BUF, &M.tmap, &bar[buf], j0, i0, nx_k);
     if (++nx_k >= min(M.S, (nx_r + 1) * M.run)) {

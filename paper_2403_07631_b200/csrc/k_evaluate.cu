@@ -894,6 +894,149 @@ int launch_evaluate(pct_ctx *ctx, const float *ground, const float *ceiling, int
   return check_launch(ctx, "eval_generic_kernel");
 }
 
+// Batched maps (config 4): one walk launch and one resolve/inflate launch for
+// every map (blockIdx.y / flattened work items select the map's descriptor).
+// Kernels whose weight classes the compiled tables cover (R = 4, r = 3: r_g
+// 0.1 with the Table-I parameters); anything else evaluates map by map.
+int launch_evaluate_batch(pct_ctx *ctx, int n_maps, float *const *ground, float *const *ceiling,
+                          const pct_frame *frames, const pct_trav_params &p,
+                          const float *kernel_w, int kside, float *const *cost) {
+  if (n_maps <= 0) return PCT_OK;
+  constexpr int R = 4, PR = 3, TH = 32, TW = 32, BNT = 128;
+  std::vector<float> bw;
+  const double r_g = frames[0].r_g;
+  bool same_rg = true;
+  for (int m = 1; m < n_maps; ++m) same_rg = same_rg && frames[m].r_g == r_g;
+  if (!(kside == 2 * R + 1 && p.patch_radius == PR && same_rg && bnb_tables<R>(kernel_w, kside, bw))) {
+    for (int m = 0; m < n_maps; ++m)
+      if (int rc = launch_evaluate(ctx, ground[m], ceiling[m], frames[m].n_slices, frames[m].rows,
+                                   frames[m].cols, frames[m].r_g, p, kernel_w, kside, cost[m],
+                                   kEvalFull))
+        return rc;
+    return PCT_OK;
+  }
+  EvalConsts K = make_consts(p, r_g);
+  PCT_CUDA(ctx, cudaMemcpyToSymbolAsync(c_K, &K, sizeof(K), 0, cudaMemcpyHostToDevice, ctx->stream));
+  PCT_CUDA(ctx, cudaMemcpyToSymbolAsync(c_bw, bw.data(), bw.size() * sizeof(float), 0,
+                                        cudaMemcpyHostToDevice, ctx->stream));
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    PCT_CUDA(ctx, cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess)
+      return fail(ctx, PCT_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  auto kb = resolve_inflate_bnb_kernel<R, PR, TH, TW, BNT, 1>;
+  constexpr int bsmem = BnbGeom<R, PR, TH, TW>::SMEM;
+  PCT_CUDA(ctx, cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, bsmem));
+  int per_sm = 0;
+  PCT_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kb, BNT, bsmem));
+  const int64_t slots = (int64_t)std::max(1, per_sm) * ctx->num_sms;
+  // layouts, offsets, run length
+  std::vector<EvalMap> hm(n_maps);
+  std::vector<int> off(n_maps + 1, 0);
+  int64_t enc_floats = 0, bit_words = 0, total_tiles = 0, walk_blocks = 1;
+  uint64_t tag = 1469598103934665603ull;
+  for (int m = 0; m < n_maps; ++m) {
+    const pct_frame &fr = frames[m];
+    EvalMap &e = hm[m];
+    std::memset(&e, 0, sizeof(EvalMap));
+    e.S = fr.n_slices;
+    e.rows = fr.rows;
+    e.cols = fr.cols;
+    e.wpr = (fr.cols + 31) / 32;
+    e.words = (int64_t)fr.rows * e.wpr;
+    e.L.padr = R;
+    e.L.padc = R;
+    e.L.prows = (fr.rows + TH - 1) / TH * TH + 2 * R;
+    e.L.pitch = ((int64_t)((fr.cols + TW - 1) / TW * TW + 2 * R) + 3) / 4 * 4;
+    e.L.sstride = (int64_t)e.L.prows * e.L.pitch;
+    enc_floats += (int64_t)e.S * e.L.sstride;
+    bit_words += (int64_t)e.S * e.words;
+    total_tiles += (int64_t)((fr.cols + TW - 1) / TW) * ((fr.rows + TH - 1) / TH);
+    walk_blocks = std::max<int64_t>(walk_blocks, (e.words * 32 + kWalkNT - 1) / kWalkNT);
+    for (uint64_t v : {(uint64_t)e.S, (uint64_t)e.rows, (uint64_t)e.cols})
+      tag = (tag ^ v) * 1099511628211ull;
+  }
+  // encoded c_init stacks of every map in the context's buffer; zeroed once
+  // per batch layout (the walk rewrites the interiors, the pads stay 0)
+  const size_t enc_bytes = (size_t)enc_floats * 4;
+  if (ctx->enc_bytes < enc_bytes) {
+    if (ctx->enc) {
+      cudaStreamSynchronize(ctx->stream);
+      cudaFree(ctx->enc);
+      ctx->enc = nullptr;
+      ctx->enc_bytes = 0;
+    }
+    PCT_CUDA(ctx, cudaMalloc(&ctx->enc, enc_bytes));
+    ctx->enc_bytes = enc_bytes;
+    ctx->enc_tag[0] = -1;
+  }
+  const int64_t tagi = (int64_t)(tag >> 1);
+  if (ctx->enc_tag[0] != -2 || ctx->enc_tag[1] != tagi) {
+    PCT_CUDA(ctx, cudaMemsetAsync(ctx->enc, 0, enc_bytes, ctx->stream));
+    ctx->enc_tag[0] = -2;
+    ctx->enc_tag[1] = tagi;
+  }
+  // scratch: gentle bitmaps | descriptors (64-byte aligned) | item offsets
+  const size_t bbytes = (((size_t)bit_words * 4 + 255) / 256) * 256;
+  const size_t dbytes = (((size_t)n_maps * sizeof(EvalMap) + 255) / 256) * 256;
+  if (int rc = ensure_scratch(ctx, bbytes + dbytes + (size_t)(n_maps + 1) * 4 + 64)) return rc;
+  char *sb = static_cast<char *>(ctx->scratch);
+  int run_all = 0;
+  {
+    int smax = 1;
+    for (auto &e : hm) smax = std::max(smax, e.S);
+    run_all = smax;
+    auto items_for = [&](int run) {
+      int64_t n = 0;
+      for (auto &e : hm) {
+        const int rr = std::min(run, e.S);
+        n += (int64_t)((e.cols + TW - 1) / TW) * ((e.rows + TH - 1) / TH) * ((e.S + rr - 1) / rr);
+      }
+      return n;
+    };
+    while (run_all > 4 && items_for(run_all) < 2 * slots) run_all = (run_all + 1) / 2;
+    if (const char *e = getenv("PCT_INFL_RUN")) run_all = std::max(1, atoi(e));
+  }
+  float *encb = static_cast<float *>(ctx->enc);
+  int64_t eoff = 0, boffw = 0;
+  for (int m = 0; m < n_maps; ++m) {
+    EvalMap &e = hm[m];
+    e.ground = ground[m];
+    e.ceiling = ceiling[m];
+    e.cost = cost[m];
+    e.enc = encb + eoff;
+    e.bits = reinterpret_cast<uint32_t *>(sb) + boffw;
+    e.run = std::min(run_all, e.S);
+    const cuuint64_t dims[3] = {(cuuint64_t)e.L.pitch, (cuuint64_t)e.L.prows, (cuuint64_t)e.S};
+    const cuuint64_t strides[2] = {(cuuint64_t)e.L.pitch * 4, (cuuint64_t)e.L.sstride * 4};
+    const cuuint32_t box[3] = {(cuuint32_t)(TW + 2 * R), (cuuint32_t)(TH + 2 * R), 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    if (encode(&e.tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, e.enc, dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return fail(ctx, PCT_E_CUDA, "cuTensorMapEncodeTiled failed");
+    const int tiles = ((e.cols + TW - 1) / TW) * ((e.rows + TH - 1) / TH);
+    off[m + 1] = off[m] + tiles * ((e.S + e.run - 1) / e.run);
+    eoff += (int64_t)e.S * e.L.sstride;
+    boffw += (int64_t)e.S * e.words;
+  }
+  EvalMap *dm = reinterpret_cast<EvalMap *>(sb + bbytes);
+  int *doff = reinterpret_cast<int *>(sb + bbytes + dbytes);
+  PCT_CUDA(ctx, cudaMemcpyAsync(dm, hm.data(), sizeof(EvalMap) * n_maps, cudaMemcpyHostToDevice,
+                                ctx->stream));
+  PCT_CUDA(ctx, cudaMemcpyAsync(doff, off.data(), sizeof(int) * (n_maps + 1),
+                                cudaMemcpyHostToDevice, ctx->stream));
+  terrain_walk_batch_kernel<1><<<dim3((unsigned)walk_blocks, n_maps), kWalkNT, 0, ctx->stream>>>(dm);
+  if (int rc = check_launch(ctx, "terrain_walk_batch_kernel")) return rc;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(off[n_maps], slots));
+  kb<<<grid, BNT, bsmem, ctx->stream>>>(dm, doff, n_maps);
+  return check_launch(ctx, "resolve_inflate_bnb_kernel");
+}
+
 int launch_inflate(pct_ctx *ctx, const float *in, int rows, int cols, const float *kernel_w,
                    int kside, float *out) {
   if (rows <= 0 || cols <= 0) return PCT_OK;

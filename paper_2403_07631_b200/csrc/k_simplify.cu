@@ -66,8 +66,8 @@ __device__ __forceinline__ bool higher_than(float hi, float lo, double eps) {
 // shared memory (no block barrier per slice), flushed once at the end.
 // Warps with no traversable, upper-uncovered cell at slice k skip the
 // lower-neighbour tests and the reductions.
-__global__ void __launch_bounds__(kWinNT) window_kernel(SimpArgs A,
-                                                        unsigned long long *__restrict__ table) {
+__device__ __forceinline__ void window_phase(const SimpArgs &A,
+                                             unsigned long long *__restrict__ table) {
   __shared__ float ring_e[kWin][kWinNT];
   __shared__ float ring_c[kWin][kWinNT];
   extern __shared__ unsigned long long btab[];  // [S]
@@ -149,6 +149,11 @@ __global__ void __launch_bounds__(kWinNT) window_kernel(SimpArgs A,
     if (btab[k]) atomicOr(table + k, btab[k]);
 }
 
+__global__ void __launch_bounds__(kWinNT) window_kernel(SimpArgs A,
+                                                        unsigned long long *__restrict__ table) {
+  window_phase(A, table);
+}
+
 struct Triple {
   int below, k, above;
 };
@@ -161,6 +166,48 @@ __global__ void __launch_bounds__(256) triples_kernel(SimpArgs A, const Triple *
   __syncthreads();
   if (skip) return;
   const Triple T = tr[t];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  bool any = false;
+  for (int64_t cell = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; cell < A.cells && !any;
+       cell += stride) {
+    const float e = __ldg(A.ground + (int64_t)T.k * A.stride + cell);
+    const float c = __ldg(A.cost + (int64_t)T.k * A.stride + cell);
+    if (!(finite32(e) && c < A.c_barrier32)) continue;
+    bool u = true;
+    if (T.below >= 0)
+      u = not_covered(e, c, __ldg(A.ground + (int64_t)T.below * A.stride + cell),
+                      __ldg(A.cost + (int64_t)T.below * A.stride + cell), A.eps_e, true);
+    if (u && T.above >= 0)
+      u = not_covered(e, c, __ldg(A.ground + (int64_t)T.above * A.stride + cell),
+                      __ldg(A.cost + (int64_t)T.above * A.stride + cell), A.eps_e, false);
+    any = u;
+  }
+  if (__syncthreads_or(any) && threadIdx.x == 0) atomicOr(flags + t, 1);
+}
+
+// batched maps: blockIdx.y = map (window tables); triples carry their map
+struct SimpMap {
+  SimpArgs A;
+  unsigned long long *table;
+};
+struct TripleM {
+  int below, k, above, map;
+};
+
+__global__ void __launch_bounds__(kWinNT) window_batch_kernel(const SimpMap *__restrict__ maps) {
+  window_phase(maps[blockIdx.y].A, maps[blockIdx.y].table);
+}
+
+__global__ void __launch_bounds__(256) triples_batch_kernel(const SimpMap *__restrict__ maps,
+                                                            const TripleM *__restrict__ tr,
+                                                            int *__restrict__ flags) {
+  const int t = blockIdx.y;
+  __shared__ int skip;
+  if (threadIdx.x == 0) skip = *((volatile int *)(flags + t));
+  __syncthreads();
+  if (skip) return;
+  const TripleM T = tr[t];
+  const SimpArgs &A = maps[T.map].A;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   bool any = false;
   for (int64_t cell = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; cell < A.cells && !any;
@@ -399,6 +446,62 @@ int simplify_triples_async(pct_ctx *ctx, const float *ground, const float *cost,
     triples_kernel<<<dim3((unsigned)bx, n), 256, 0, ctx->stream>>>(A, dtr, dflags);
     if (int rc = check_launch(ctx, "triples_kernel")) return rc;
   }
+  PCT_CUDA(ctx, cudaMemcpyAsync(flags_host, dflags, sizeof(int) * n, cudaMemcpyDeviceToHost,
+                                ctx->stream));
+  return PCT_OK;
+}
+
+// batched maps: one window launch for every map's table (tables_host: S_max
+// u64 per map, pinned), one triples launch for a round of every map's
+// triples (tri_host: (below, k, above, map) int32 x n, flags_host: n)
+int simplify_window_batch(pct_ctx *ctx, int n_maps, const float *const *ground,
+                          const float *const *cost, const int *S, const int64_t *cells,
+                          int S_max, double eps_e, double c_barrier, uint64_t *tables_host) {
+  const size_t tbytes = (size_t)n_maps * S_max * 8;
+  const size_t dbytes = ((sizeof(SimpMap) * (size_t)n_maps + 255) / 256) * 256;
+  if ((size_t)S_max * 8 > 160 * 1024) return fail(ctx, PCT_E_INVALID, "too many slices for simplify");
+  if (int rc = ensure_staging(ctx, dbytes + tbytes)) return rc;
+  SimpMap *dd = static_cast<SimpMap *>(ctx->staging);
+  unsigned long long *dt = reinterpret_cast<unsigned long long *>(static_cast<char *>(ctx->staging) + dbytes);
+  std::vector<SimpMap> h(n_maps);
+  int64_t cmax = 1;
+  for (int m = 0; m < n_maps; ++m) {
+    h[m].A = SimpArgs{ground[m], cost[m], cells[m], cells[m], S[m], eps_e, (float)c_barrier};
+    h[m].table = dt + (size_t)m * S_max;
+    cmax = std::max<int64_t>(cmax, cells[m]);
+  }
+  PCT_CUDA(ctx, cudaMemcpyAsync(dd, h.data(), sizeof(SimpMap) * n_maps, cudaMemcpyHostToDevice,
+                                ctx->stream));
+  PCT_CUDA(ctx, cudaMemsetAsync(dt, 0, tbytes, ctx->stream));
+  const size_t smem = (size_t)S_max * 8;
+  PCT_CUDA(ctx, cudaFuncSetAttribute(window_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+  // per map about as many blocks as its cells need, the whole launch <= 12
+  // resident blocks per SM
+  const int64_t per_map = std::max<int64_t>(
+      1, std::min<int64_t>((cmax + kWinNT - 1) / kWinNT, 12LL * ctx->num_sms / std::max(1, n_maps)));
+  window_batch_kernel<<<dim3((unsigned)per_map, n_maps), kWinNT, smem, ctx->stream>>>(dd);
+  if (int rc = check_launch(ctx, "window_batch_kernel")) return rc;
+  PCT_CUDA(ctx, cudaMemcpyAsync(tables_host, dt, tbytes, cudaMemcpyDeviceToHost, ctx->stream));
+  return PCT_OK;
+}
+
+int simplify_triples_batch(pct_ctx *ctx, int n_maps, int n, const int32_t *tri_host,
+                           int32_t *flags_host) {
+  if (n <= 0) return PCT_OK;
+  // descriptors stay in the staging buffer from simplify_window_batch
+  const size_t dbytes = ((sizeof(SimpMap) * (size_t)n_maps + 255) / 256) * 256;
+  SimpMap *dd = static_cast<SimpMap *>(ctx->staging);
+  const size_t need = (size_t)n * (sizeof(TripleM) + sizeof(int)) + 64;
+  if (int rc = ensure_scratch(ctx, need)) return rc;
+  TripleM *dtr = static_cast<TripleM *>(ctx->scratch);
+  int *dflags = reinterpret_cast<int *>(dtr + n);
+  (void)dbytes;
+  PCT_CUDA(ctx, cudaMemcpyAsync(dtr, tri_host, sizeof(TripleM) * n, cudaMemcpyHostToDevice,
+                                ctx->stream));
+  PCT_CUDA(ctx, cudaMemsetAsync(dflags, 0, sizeof(int) * n, ctx->stream));
+  triples_batch_kernel<<<dim3(8, n), 256, 0, ctx->stream>>>(dd, dtr, dflags);
+  if (int rc = check_launch(ctx, "triples_batch_kernel")) return rc;
   PCT_CUDA(ctx, cudaMemcpyAsync(flags_host, dflags, sizeof(int) * n, cudaMemcpyDeviceToHost,
                                 ctx->stream));
   return PCT_OK;

@@ -96,6 +96,15 @@ bool bounds_from_keys(const unsigned long long *keys, double lo[3], double hi[3]
 // batched maps: one launch per stage (keys_host: 8 u64 per map, pinned)
 int launch_bounds_batch(pct_ctx *ctx, int n_maps, const void *const *xyz, const int64_t *n,
                         int dtype, unsigned long long *keys_host);
+int simplify_window_batch(pct_ctx *ctx, int n_maps, const float *const *ground,
+                          const float *const *cost, const int *S, const int64_t *cells,
+                          int S_max, double eps_e, double c_barrier, uint64_t *tables_host);
+int simplify_triples_batch(pct_ctx *ctx, int n_maps, int n, const int32_t *tri_host,
+                           int32_t *flags_host);
+int launch_evaluate_batch(pct_ctx *ctx, int n_maps, float *const *ground,
+                          float *const *ceiling, const pct_frame *frames,
+                          const pct_trav_params &p, const float *kernel_w, int kside,
+                          float *const *cost);
 int launch_build_batch(pct_ctx *ctx, int n_maps, const void *const *xyz, const int64_t *n,
                        int dtype, const pct_frame *frames, const double *const *heights,
                        float *const *ground, float *const *ceiling);
