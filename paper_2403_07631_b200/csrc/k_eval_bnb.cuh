@@ -237,72 +237,122 @@ __global__ void __launch_bounds__(NT, MINB) resolve_inflate_bnb_kernel(
     r = local / tiles;
     t = local - r * tiles;
   };
+  auto origin = [&](const EvalMap &M, int t, int &i0, int &j0) {
+    const int tx = (M.cols + TW - 1) / TW;
+    const int ti = t / tx;
+    i0 = ti * TH;
+    j0 = (t - ti * tx) * TW;
+  };
   constexpr uint32_t BOX_BYTES = G::CH * G::CW * 4;
   const float w0 = c_bw[0], w1 = c_bw[1];
   const uint32_t cb_bits = f32_bits((float)c_K.c_barrier);
-  // thread 0 walks the CTA's step sequence one step ahead of the others:
-  // step = (item, slice); it records the map, tile origin and slice of each
-  // step in the slot of the buffer it loads
-  int nx_item = blockIdx.x, nx_k = 0, nx_m = 0, nx_r = 0, nx_t = 0, acq_m = -1;
-  if (nx_item < n_items) {
-    decode(nx_item, nx_m, nx_r, nx_t);
-    nx_k = nx_r * maps[nx_m].run;
-  }
-  auto issue = [&](int buf) {
-    const EvalMap &M = maps[nx_m];
-    const int tx = (M.cols + TW - 1) / TW;
-    const int ti = nx_t / tx;
-    const int i0 = ti * TH, j0 = (nx_t - ti * tx) * TW;
-    slot[buf * 3] = i0 * 65536 + j0 / TW;  // rows < 2^15, tiles of >= 32 columns
-    slot[buf * 3 + 1] = nx_k | ((nx_k == nx_r * M.run) ? 0x40000000 : 0);  // first of its run
-    slot[buf * 3 + 2] = nx_m;
+  // Loads: only steps that are not skipped load their tile (TMA into buffer
+  // (#loads issued) % 3); a step consumes the loads in issue order, so its
+  // buffer is (#loads consumed) % 3 and the previous loaded tile is the one
+  // before.  Thread 0 keeps one load in flight, for the next step to load.
+  int acq_m = -1, ld = 0;  // thread 0
+  bool pending = false;    // thread 0
+  auto issue = [&](int m, int t, int k) {
+    const EvalMap &M = maps[m];
+    int i0, j0;
+    origin(M, t, i0, j0);
+    const int buf = ld % 3;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     // the tensor map lives in global memory and is rewritten between launches
     // (possibly at the same address): acquire it for the tensor-map proxy once
     // per map, so a stale descriptor-cache copy is not used
-    if (nx_m != acq_m) {
+    if (m != acq_m) {
       asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(&M.tmap)
                    : "memory");
-      acq_m = nx_m;
+      acq_m = m;
     }
     mbar_expect_tx(&bar[buf], BOX_BYTES);
-    tma_load_3d(smem + G::O_BUF + buf * G::BUF, &M.tmap, &bar[buf], j0, i0, nx_k);
-    if (++nx_k >= min(M.S, (nx_r + 1) * M.run)) {
-      nx_item += gridDim.x;
-      if (nx_item < n_items) {
-        decode(nx_item, nx_m, nx_r, nx_t);
-        nx_k = nx_r * maps[nx_m].run;
-      }
-    }
+    tma_load_3d(smem + G::O_BUF + buf * G::BUF, &M.tmap, &bar[buf], j0, i0, k);
+    ++ld;
+    pending = true;
   };
+  uint64_t *skipmask = reinterpret_cast<uint64_t *>(slot);  // per item: slice j skippable
   if (tid == 0) {
 #pragma unroll
     for (int b = 0; b < G::NBUF; ++b) mbar_init(&bar[b], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    if (nx_item < n_items) issue(0);
+    if (blockIdx.x < n_items) {
+      int m, r, t;
+      decode(blockIdx.x, m, r, t);
+      issue(m, t, r * maps[m].run);
+    }
   }
   __syncthreads();
-  int steps = 0;  // this CTA's total
+  uint32_t phase_bits = 0u;
+  int lc = 0;  // loads consumed
   for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
     int m, r, t;
     decode(item, m, r, t);
-    steps += min(maps[m].S, (r + 1) * maps[m].run) - r * maps[m].run;
-  }
-  uint32_t phase_bits = 0u;
-  for (int st = 0; st < steps; ++st) {
-    const int cur = st % 3, prv = (st + 2) % 3;
-    float *ci = reinterpret_cast<float *>(smem + G::O_BUF + cur * G::BUF);
-    const float *cp = reinterpret_cast<const float *>(smem + G::O_BUF + prv * G::BUF);
-    const int i0 = slot[cur * 3] >> 16, j0 = (slot[cur * 3] & 0xFFFF) * TW;
-    const int k = slot[cur * 3 + 1] & 0x3FFFFFFF;
-    const bool first = (slot[cur * 3 + 1] & 0x40000000) != 0;
-    const EvalMap &M = maps[slot[cur * 3 + 2]];
+    const EvalMap &M = maps[m];
+    int i0, j0;
+    origin(M, t, i0, j0);
+    const int k0 = r * M.run, k1 = min(M.S, k0 + M.run);  // run <= 64
     const int rows = M.rows, cols = M.cols;
     const int64_t cells = (int64_t)rows * cols, words = M.words;
     const uint32_t *bits_in = M.bits;
     float *cost = M.cost;
-    // the buffer of step st-2 (read as `prv` by step st-1) is free again
-    if (tid == 0 && st + 1 < steps) issue((st + 1) % 3);
+    // skippable slices of this item: no change of encoded c_init or gentle
+    // flag in the tile + R + r window since the slice below (walk change map);
+    // every thread checks a few (slice, block) bytes, changes are OR-ed into
+    // a shared mask
+    unsigned *chgw = reinterpret_cast<unsigned *>(skipmask);  // [2]: slices 0-31, 32-63
+    __syncthreads();  // every thread is done with the previous item's mask
+    if (tid < 2) chgw[tid] = M.chg ? 0u : 0xFFFFFFFFu;  // no change map: nothing skips
+    __syncthreads();
+    if (M.chg) {
+      const int nbr = (rows + 7) >> 3, wpr = M.wpr;
+      const int br0 = max(0, (i0 - R - PR) >> 3), br1 = min(nbr - 1, (i0 + TH + R + PR - 1) >> 3);
+      const int wc0 = max(0, (j0 - R - PR) >> 5), wc1 = min(wpr - 1, (j0 + TW + R + PR - 1) >> 5);
+      const int nb = br1 - br0 + 1, nw = wc1 - wc0 + 1;
+      const int per = nb * nw;
+      const int64_t cms = (int64_t)nbr * wpr;
+      for (int q = tid; q < (k1 - k0 - 1) * per; q += NT) {
+        const int j = 1 + q / per, e = q - (j - 1) * per;
+        const int br = br0 + e / nw, wc = wc0 + e - (e / nw) * nw;
+        if (M.chg[(int64_t)(k0 + j) * cms + (int64_t)br * wpr + wc])
+          atomicOr(&chgw[j >> 5], 1u << (j & 31));
+      }
+    }
+    __syncthreads();
+    const uint64_t changed = (uint64_t)chgw[0] | ((uint64_t)chgw[1] << 32);
+    const uint64_t skm = ~changed;  // bit j: slice k0 + j is skippable (bit 0 unused: first)
+    for (int k = k0; k < k1; ++k) {
+      const bool first = k == k0;
+      const bool skip = !first && ((skm >> (k - k0)) & 1ull);
+      if (tid == 0) {
+        if (!skip) pending = false;  // this step consumes the load in flight
+        if (!pending) {              // the next step that loads: this item, or the next one
+          int kn = k + 1;
+          while (kn < k1 && ((skm >> (kn - k0)) & 1ull)) ++kn;
+          if (kn < k1) {
+            issue(m, t, kn);
+          } else if (item + (int)gridDim.x < n_items) {
+            int m2, r2, t2;
+            decode(item + gridDim.x, m2, r2, t2);
+            issue(m2, t2, r2 * maps[m2].run);
+          }
+        }
+      }
+      if (skip) {  // outputs equal the previous slice's: store the kept tile
+        static_assert(NT % TW == 0, "store layout");
+        constexpr int RPS = NT / TW;
+        const int x = tid % TW, r0 = tid / TW;
+        const int imax = min(TH, rows - i0);
+        if (j0 + x < cols) {
+          float *o = cost + (int64_t)k * cells + (int64_t)(i0 + r0) * cols + (j0 + x);
+          for (int i = r0; i < imax; i += RPS, o += (int64_t)RPS * cols) *o = ot[i * TW + x];
+        }
+        continue;
+      }
+      const int cur = lc % 3, prv = (lc + 2) % 3;
+      ++lc;
+      float *ci = reinterpret_cast<float *>(smem + G::O_BUF + cur * G::BUF);
+      const float *cp = reinterpret_cast<const float *>(smem + G::O_BUF + prv * G::BUF);
     // ---- P0a: gentle bits of the window region (bit x of word w = gentle
     // column 32w + x, gentle column 0 = c_init column -r); resets
     const uint32_t *bk = bits_in + (int64_t)k * words;
@@ -565,6 +615,7 @@ __global__ void __launch_bounds__(NT, MINB) resolve_inflate_bnb_kernel(
       }
     }
     // the next step's first barrier orders P4's reads of `ot` before its P2
+    }
   }
 }
 

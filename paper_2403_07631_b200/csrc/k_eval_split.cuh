@@ -73,7 +73,7 @@ __device__ __forceinline__ void walk_body(const float *__restrict__ ground,
                                           const float *__restrict__ ceiling, int S, int rows,
                                           int cols, float *__restrict__ enc_out,
                                           const EncLayout &L, uint32_t *__restrict__ bits_out,
-                                          int wpr) {
+                                          int wpr, unsigned char *__restrict__ chgmap) {
   const int64_t cells = (int64_t)rows * cols;
   // threads index row-padded columns: warp = one gentle-bitmap word of one row
   const int64_t pidx = (int64_t)blockIdx.x * kWalkNT + threadIdx.x;
@@ -113,6 +113,13 @@ __device__ __forceinline__ void walk_body(const float *__restrict__ ground,
   float tenc = nanf_;  // terrain part: NaN = no ground, sign bit = foothold branch
   bool gentle = false;
   float enc = 0.0f;
+  // change map: one byte per (slice, 8-row block, bitmap word) set when any
+  // cell's encoded c_init or gentle flag differs from the slice below (the
+  // resolve/inflate kernel skips tiles whose window saw no change)
+  const int64_t cmstride = (int64_t)((rows + 7) >> 3) * wpr;
+  unsigned char *pcm = chgmap + (int64_t)(i >> 3) * wpr + (j0_ >> 5);
+  uint32_t prev_enc = 0u;
+  unsigned prev_word = 0u;
   for (int k0 = 0; k0 < S; k0 += PF) {
 #pragma unroll
     for (int s = 0; s < PF; ++s) {
@@ -160,8 +167,15 @@ __device__ __forceinline__ void walk_body(const float *__restrict__ ground,
       if (live) *pe = enc;
       pe += L.sstride;
       const unsigned word = __ballot_sync(0xFFFFFFFFu, live && gentle);
+      if (chgmap) {  // uniform
+        const bool enc_changed = __any_sync(0xFFFFFFFFu, live && f32_bits(enc) != prev_enc);
+        if (wlead && (k == 0 || word != prev_word || enc_changed)) *pcm = 1;
+        prev_word = word;
+        prev_enc = f32_bits(enc);
+      }
       if (wlead) *pb = word;
       pb += (int64_t)rows * wpr;
+      pcm += cmstride;
     }
   }
 }
@@ -170,8 +184,8 @@ template <int PF>
 __global__ void __launch_bounds__(kWalkNT) terrain_walk_kernel(
     const float *__restrict__ ground, const float *__restrict__ ceiling, int S, int rows,
     int cols, float *__restrict__ enc_out, EncLayout L, uint32_t *__restrict__ bits_out,
-    int wpr) {
-  walk_body<PF>(ground, ceiling, S, rows, cols, enc_out, L, bits_out, wpr);
+    int wpr, unsigned char *__restrict__ chgmap) {
+  walk_body<PF>(ground, ceiling, S, rows, cols, enc_out, L, bits_out, wpr, chgmap);
 }
 
 // per-map arguments of the split evaluation (a single map is a batch of one)
@@ -183,6 +197,7 @@ struct EvalMap {
   EncLayout L;
   int S, rows, cols, wpr, run;
   int64_t words;  // gentle bitmap words per slice
+  unsigned char *chg;  // change map of the walk ((rows + 7) / 8 x wpr bytes per slice)
 };
 
 // walk over a batch: blockIdx.y = map; blocks past the map's extent leave
@@ -190,7 +205,7 @@ template <int PF>
 __global__ void __launch_bounds__(kWalkNT) terrain_walk_batch_kernel(const EvalMap *__restrict__ maps) {
   const EvalMap &m = maps[blockIdx.y];
   if ((int64_t)blockIdx.x * kWalkNT >= (int64_t)m.rows * m.wpr * 32) return;  // whole block
-  walk_body<PF>(m.ground, m.ceiling, m.S, m.rows, m.cols, m.enc, m.L, m.bits, m.wpr);
+  walk_body<PF>(m.ground, m.ceiling, m.S, m.rows, m.cols, m.enc, m.L, m.bits, m.wpr, m.chg);
 }
 
 template <int R, int PR, int TH, int TW>

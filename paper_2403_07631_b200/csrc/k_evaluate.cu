@@ -611,6 +611,13 @@ int launch_incr_t(pct_ctx *ctx, const float *ground, const float *ceiling, int S
 // Inflation: the branch-and-bound kernel (k_eval_bnb.cuh) when the kernel's
 // weight classes fit its compiled disk (PCT_INFL=sym keeps the full-tap TMA
 // kernel for R <= 4), else the full-tap TMA kernel (R <= 4 only).
+// resident CTAs the bnb kernel is compiled for (caps its registers): R = 4
+// tiles need ~34 KB of shared memory (6 CTAs fit), R = 8 ~47 KB (4 fit)
+template <int R>
+constexpr int kBnbMinBlocks() {
+  return R <= 4 ? 6 : 4;
+}
+
 template <int R, int PR, int TH, int TW, int BNT = 256>
 int launch_split(pct_ctx *ctx, const float *ground, const float *ceiling, int S, int rows,
                  int cols, const float *kernel_w, int kside, float *cost, bool bnb) {
@@ -631,10 +638,19 @@ int launch_split(pct_ctx *ctx, const float *ground, const float *ceiling, int S,
   L.pitch = ((int64_t)((cols + TW - 1) / TW * TW + 2 * R) + 3) / 4 * 4;
   L.sstride = (int64_t)L.prows * L.pitch;
   const size_t enc_bytes = (size_t)S * L.sstride * 4;
-  // gentle bitmap | (bnb) descriptor of a batch of one, 256-byte aligned
-  if (int rc = ensure_scratch(ctx, (((size_t)S * words * 4 + 255) / 256) * 256 + sizeof(EvalMap) + 128))
-    return rc;
+  // gentle bitmap | (bnb) descriptor of a batch of one | walk change map
+  const size_t cm_off = (((size_t)S * words * 4 + 255) / 256) * 256 + ((sizeof(EvalMap) + 128 + 255) / 256) * 256;
+  const size_t cm_bytes = (size_t)S * ((rows + 7) / 8) * wpr;
+  if (int rc = ensure_scratch(ctx, cm_off + cm_bytes + 64)) return rc;
   uint32_t *bits = static_cast<uint32_t *>(ctx->scratch);
+  // tiles whose window saw no change skip the resolve/inflate work (R >= 8:
+  // cfg2 bnb 798 -> 473 us; at R = 4 the per-tile work is light and the
+  // change map costs the walk about what it saves, so it is off unless
+  // PCT_BNB_SKIP=1)
+  const char *skv = getenv("PCT_BNB_SKIP");
+  const bool use_skip = skv ? skv[0] == '1' : R >= 8;
+  unsigned char *chgmap = use_skip ? static_cast<unsigned char *>(ctx->scratch) + cm_off : nullptr;
+  if (chgmap) PCT_CUDA(ctx, cudaMemsetAsync(chgmap, 0, cm_bytes, ctx->stream));
   if (ctx->enc_bytes < enc_bytes) {
     if (ctx->enc) {
       cudaStreamSynchronize(ctx->stream);
@@ -660,10 +676,10 @@ int launch_split(pct_ctx *ctx, const float *ground, const float *ceiling, int S,
   // 2 / 4; deeper prefetch costs occupancy)
   if (pf && pf[0] == '2')
     terrain_walk_kernel<2><<<g1, kWalkNT, 0, ctx->stream>>>(ground, ceiling, S, rows, cols, enc, L,
-                                                           bits, wpr);
+                                                           bits, wpr, chgmap);
   else
     terrain_walk_kernel<1><<<g1, kWalkNT, 0, ctx->stream>>>(ground, ceiling, S, rows, cols, enc, L,
-                                                           bits, wpr);
+                                                           bits, wpr, chgmap);
   if (int rc = check_launch(ctx, "terrain_walk_kernel")) return rc;
   const char *tma = getenv("PCT_TMA");
   if (bnb || (!(tma && tma[0] == '0') && R % 4 == 0)) {
@@ -694,7 +710,7 @@ int launch_split(pct_ctx *ctx, const float *ground, const float *ceiling, int S,
      if (bnb) {
       PCT_CUDA(ctx, cudaMemcpyToSymbolAsync(c_bw, bw.data(), bw.size() * sizeof(float), 0,
                                             cudaMemcpyHostToDevice, ctx->stream));
-      auto kb = resolve_inflate_bnb_kernel<R, PR, TH, TW, BNT, 1>;
+      auto kb = resolve_inflate_bnb_kernel<R, PR, TH, TW, BNT, kBnbMinBlocks<R>()>;
       constexpr int bsmem = BnbGeom<R, PR, TH, TW>::SMEM;
       PCT_CUDA(ctx, cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, bsmem));
       int per_sm = 0;
@@ -707,7 +723,7 @@ int launch_split(pct_ctx *ctx, const float *ground, const float *ceiling, int S,
       int run = S;
       while (run > 4 && tiles * ((S + run - 1) / run) < 2 * slots) run = (run + 1) / 2;
       if (const char *e = getenv("PCT_INFL_RUN")) run = std::max(1, atoi(e));
-      run = std::min(run, S);
+      run = std::min(std::min(run, S), 64);  // per-item skip mask: 64 slices
       const int64_t nitems = tiles * ((S + run - 1) / run);
       if (nitems > INT32_MAX) return fail(ctx, PCT_E_INVALID, "grid too large");
       const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nitems, slots));
@@ -729,6 +745,7 @@ int launch_split(pct_ctx *ctx, const float *ground, const float *ceiling, int S,
       hm.wpr = wpr;
       hm.run = run;
       hm.words = words;
+      hm.chg = chgmap;
       struct {
         EvalMap m;
         int off[2];
@@ -928,7 +945,7 @@ int launch_evaluate_batch(pct_ctx *ctx, int n_maps, float *const *ground, float 
       return fail(ctx, PCT_E_CUDA, "cuTensorMapEncodeTiled unavailable");
     encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
-  auto kb = resolve_inflate_bnb_kernel<R, PR, TH, TW, BNT, 1>;
+  auto kb = resolve_inflate_bnb_kernel<R, PR, TH, TW, BNT, kBnbMinBlocks<R>()>;
   constexpr int bsmem = BnbGeom<R, PR, TH, TW>::SMEM;
   PCT_CUDA(ctx, cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, bsmem));
   int per_sm = 0;
@@ -980,11 +997,19 @@ int launch_evaluate_batch(pct_ctx *ctx, int n_maps, float *const *ground, float 
     ctx->enc_tag[0] = -2;
     ctx->enc_tag[1] = tagi;
   }
-  // scratch: gentle bitmaps | descriptors (64-byte aligned) | item offsets
+  // scratch: gentle bitmaps | descriptors (64-byte aligned) | item offsets |
+  // walk change maps
   const size_t bbytes = (((size_t)bit_words * 4 + 255) / 256) * 256;
   const size_t dbytes = (((size_t)n_maps * sizeof(EvalMap) + 255) / 256) * 256;
-  if (int rc = ensure_scratch(ctx, bbytes + dbytes + (size_t)(n_maps + 1) * 4 + 64)) return rc;
+  const size_t obytes = (((size_t)(n_maps + 1) * 4 + 255) / 256) * 256;
+  int64_t cm_total = 0;
+  for (auto &e : hm) cm_total += (int64_t)e.S * ((e.rows + 7) / 8) * e.wpr;
+  if (int rc = ensure_scratch(ctx, bbytes + dbytes + obytes + (size_t)cm_total + 64)) return rc;
   char *sb = static_cast<char *>(ctx->scratch);
+  unsigned char *cmb = reinterpret_cast<unsigned char *>(sb + bbytes + dbytes + obytes);
+  const char *skv = getenv("PCT_BNB_SKIP");  // R = 4: off by default (see launch_split)
+  const bool use_skip = skv && skv[0] == '1';
+  if (use_skip) PCT_CUDA(ctx, cudaMemsetAsync(cmb, 0, (size_t)cm_total, ctx->stream));
   int run_all = 0;
   {
     int smax = 1;
@@ -1000,6 +1025,7 @@ int launch_evaluate_batch(pct_ctx *ctx, int n_maps, float *const *ground, float 
     };
     while (run_all > 4 && items_for(run_all) < 2 * slots) run_all = (run_all + 1) / 2;
     if (const char *e = getenv("PCT_INFL_RUN")) run_all = std::max(1, atoi(e));
+    run_all = std::min(run_all, 64);  // per-item skip mask: 64 slices
   }
   float *encb = static_cast<float *>(ctx->enc);
   int64_t eoff = 0, boffw = 0;
@@ -1011,6 +1037,8 @@ int launch_evaluate_batch(pct_ctx *ctx, int n_maps, float *const *ground, float 
     e.enc = encb + eoff;
     e.bits = reinterpret_cast<uint32_t *>(sb) + boffw;
     e.run = std::min(run_all, e.S);
+    e.chg = use_skip ? cmb : nullptr;
+    cmb += (int64_t)e.S * ((e.rows + 7) / 8) * e.wpr;
     const cuuint64_t dims[3] = {(cuuint64_t)e.L.pitch, (cuuint64_t)e.L.prows, (cuuint64_t)e.S};
     const cuuint64_t strides[2] = {(cuuint64_t)e.L.pitch * 4, (cuuint64_t)e.L.sstride * 4};
     const cuuint32_t box[3] = {(cuuint32_t)(TW + 2 * R), (cuuint32_t)(TH + 2 * R), 1};

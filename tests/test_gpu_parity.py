@@ -398,3 +398,16 @@ def test_planner_context_matches_reference(golden, name):
         assert t._planner_ctx is pc and pc.eps_e == 1e-6 and pc.c_barrier == 50.0
         assert digest(pc.canon) == case["planner"][key]["canon_sha256"], key
         assert digest(pc.cn) == case["planner"][key]["cn_sha256"], key
+
+
+@pytest.mark.parametrize("name,skip", [("synth_cfg1", "1"), ("synth_cfg2_n2000000", "0"),
+                                       ("ref_random_multilayer_s9", "1")])
+def test_bnb_tile_skipping_is_exact(golden, monkeypatch, name, skip):
+    """Skipping unchanged tiles (walk change map; default for R >= 8) and not
+    skipping give the reference's cost bytes either way."""
+    monkeypatch.setenv("PCT_BNB_SKIP", skip)
+    case = golden["cases"][name]
+    tom = pct.build_tomogram(pct.PointCloud(case_input(name, case)), case["d_s"], case["r_g"])
+    cost = pct.evaluate_tomogram(tom, pct.TravParams()).cost_stack()
+    for k in range(cost.shape[0]):
+        assert digest(cost[k]) == case["cost_slice_sha256"][k], f"cost slice {k}"
