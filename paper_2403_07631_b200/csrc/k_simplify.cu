@@ -80,6 +80,11 @@ __device__ __forceinline__ void window_phase(const SimpArgs &A,
   for (int64_t cell = (int64_t)blockIdx.x * kWinNT + threadIdx.x; cell < span; cell += stride) {
     const bool live = cell < A.cells;
     float ce[KB + 1], cc[KB + 1];  // slices k0 .. k0+KB of this cell
+    // last slice whose ground dropped below the slice under it (or became
+    // invalid after being valid); the older-bits shortcut needs none within
+    // the window
+    int last_dec = -(1 << 20);
+    float e_prev = nanf_;
     // running pointers to the next slice to load (no 64-bit multiply per load)
     const float *pg = A.ground + (live ? cell : 0), *pc = A.cost + (live ? cell : 0);
     int kn = 0;  // slice pg / pc point at
@@ -103,6 +108,9 @@ __device__ __forceinline__ void window_phase(const SimpArgs &A,
         const int k = k0 + u;
         if (k >= A.S) break;  // uniform
         const float e_cur = ce[u], c_cur = cc[u], e_up = ce[u + 1], c_up = cc[u + 1];
+        if (finite32(e_prev) && !(e_cur >= e_prev)) last_dec = k;  // NaN fails >= too
+        e_prev = e_cur;
+        const bool mono = k - last_dec > kWin;
         const bool up_ok = k + 1 >= A.S || !finite32(e_up) || higher_than(e_up, e_cur, A.eps_e) ||
                            c_cur < c_up;
         const bool cand = live && finite32(e_cur) && c_cur < A.c_barrier32 && up_ok;
@@ -117,14 +125,25 @@ __device__ __forceinline__ void window_phase(const SimpArgs &A,
           if (cand && (known & want) != want) {
             m = 1ull << kBit;
             unsigned todo = (unsigned)(~known & want);
+            // when this cell's ground did not decrease within the window
+            // (always, for stacks built here: a prefix max over bins), once a
+            // lower neighbour a is invalid or lower by more than eps_e, every
+            // older one is too (double subtraction is monotone) -- the
+            // remaining, older bits are set at once
             while (todo) {
-              const int j = __ffs(todo) - 1;  // a = k-1-j
+              const int j = __ffs(todo) - 1;  // a = k-1-j, most recent first
               todo &= todo - 1;
               const int slot = (k - 1 - j) & (kWin - 1);
               const float ea = ring_e[slot][threadIdx.x];
-              if (!finite32(ea) || higher_than(e_cur, ea, A.eps_e) ||
-                  c_cur < ring_c[slot][threadIdx.x])
+              if (!finite32(ea) || higher_than(e_cur, ea, A.eps_e)) {
                 m |= 1ull << j;
+                if (mono) {
+                  m |= (unsigned long long)todo;
+                  break;
+                }
+              } else if (c_cur < ring_c[slot][threadIdx.x]) {
+                m |= 1ull << j;
+              }
             }
           }
           const unsigned lo = __reduce_or_sync(0xffffffffu, (unsigned)m);
@@ -157,6 +176,18 @@ __global__ void __launch_bounds__(kWinNT) window_kernel(SimpArgs A,
 struct Triple {
   int below, k, above;
 };
+
+// resident window blocks per SM (one wave; the kernel is persistent)
+int window_blocks_per_sm(pct_ctx *ctx, size_t smem) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, window_kernel, kWinNT, smem) !=
+          cudaSuccess ||
+      per_sm < 1) {
+    cudaGetLastError();
+    per_sm = 8;
+  }
+  return per_sm;
+}
 
 __global__ void __launch_bounds__(256) triples_kernel(SimpArgs A, const Triple *__restrict__ tr,
                                                       int *__restrict__ flags) {
@@ -283,7 +314,7 @@ int run_simplify(pct_ctx *ctx, const float *ground, const float *cost, int S, in
                                        (int)tab_smem));
     const int64_t blocks_needed = (A.cells + kWinNT - 1) / kWinNT;
     const char *wb = getenv("PCT_WIN_BLOCKS");
-    const int per_sm = wb ? atoi(wb) : 12;
+    const int per_sm = wb ? atoi(wb) : window_blocks_per_sm(ctx, tab_smem);
     const unsigned grid = (unsigned)std::min<int64_t>(blocks_needed, (int64_t)per_sm * ctx->num_sms);
     window_kernel<<<grid, kWinNT, tab_smem, ctx->stream>>>(A, table);
   }
@@ -396,7 +427,8 @@ int simplify_window_table(pct_ctx *ctx, const float *ground, const float *cost, 
     PCT_CUDA(ctx, cudaFuncSetAttribute(window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)tbytes));
     const int64_t blocks_needed = (cells + kWinNT - 1) / kWinNT;
-    const unsigned grid = (unsigned)std::min<int64_t>(blocks_needed, 12LL * ctx->num_sms);
+    const unsigned grid = (unsigned)std::min<int64_t>(
+        blocks_needed, (int64_t)window_blocks_per_sm(ctx, tbytes) * ctx->num_sms);
     window_kernel<<<grid, kWinNT, tbytes, ctx->stream>>>(A, table);
     if (int rc = check_launch(ctx, "window_kernel")) return rc;
   }
@@ -418,7 +450,8 @@ int simplify_window_async(pct_ctx *ctx, const float *ground, const float *cost, 
     PCT_CUDA(ctx, cudaFuncSetAttribute(window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)tbytes));
     const int64_t blocks_needed = (cells + kWinNT - 1) / kWinNT;
-    const unsigned grid = (unsigned)std::min<int64_t>(blocks_needed, 12LL * ctx->num_sms);
+    const unsigned grid = (unsigned)std::min<int64_t>(
+        blocks_needed, (int64_t)window_blocks_per_sm(ctx, tbytes) * ctx->num_sms);
     window_kernel<<<grid, kWinNT, tbytes, ctx->stream>>>(A, table);
     if (int rc = check_launch(ctx, "window_kernel")) return rc;
   }
@@ -479,7 +512,8 @@ int simplify_window_batch(pct_ctx *ctx, int n_maps, const float *const *ground,
   // per map about as many blocks as its cells need, the whole launch <= 12
   // resident blocks per SM
   const int64_t per_map = std::max<int64_t>(
-      1, std::min<int64_t>((cmax + kWinNT - 1) / kWinNT, 12LL * ctx->num_sms / std::max(1, n_maps)));
+      1, std::min<int64_t>((cmax + kWinNT - 1) / kWinNT,
+                           (int64_t)window_blocks_per_sm(ctx, smem) * ctx->num_sms / std::max(1, n_maps)));
   window_batch_kernel<<<dim3((unsigned)per_map, n_maps), kWinNT, smem, ctx->stream>>>(dd);
   if (int rc = check_launch(ctx, "window_batch_kernel")) return rc;
   PCT_CUDA(ctx, cudaMemcpyAsync(tables_host, dt, tbytes, cudaMemcpyDeviceToHost, ctx->stream));
