@@ -210,18 +210,20 @@ constexpr int kTileMaxS = 96;     // 2 x S x 256 x 4 B of shared memory
 constexpr int kTileNT = 256;
 
 // cell and bin of one point (tomogram.py:147-157): false when outside the band
+template <bool BIN = true>
 __device__ __forceinline__ bool point_cell_bin(double x, double y, double z, const BinArgs &a,
                                                const double *hts, int &fi_out, int &fj_out,
                                                int &b_out) {
   const double fi = floor(div_const(y - a.y0, a.r_g, a.inv_rg) + 0.5) - (double)a.row0;
   const double fj = floor(div_const(x - a.x0, a.r_g, a.inv_rg) + 0.5);
   if (!(fi >= 0.0 && fi < (double)a.rows && fj >= 0.0 && fj < (double)a.cols)) return false;
+  fi_out = (int)fi;
+  fj_out = (int)fj;
+  if (!BIN) return true;  // the tile count needs the cell only
   double est = floor((z - a.z0) * a.inv_ds);  // estimate only; fixed up exactly below
   int b = est < 0.0 ? 0 : (est > (double)a.S ? a.S : (int)est);
   while (b > 0 && hts[b - 1] >= z) --b;
   while (b < a.S && hts[b] < z) ++b;
-  fi_out = (int)fi;
-  fj_out = (int)fj;
   b_out = b;
   return true;
 }
@@ -267,8 +269,8 @@ __global__ void __launch_bounds__(256) tile_pass_kernel(const T *__restrict__ xy
       if (p < p1) {
         const double x = (double)__ldg(xyz + 3 * p);
         const double y = (double)__ldg(xyz + 3 * p + 1);
-        const double z = (double)__ldg(xyz + 3 * p + 2);
-        in = point_cell_bin(x, y, z, a, hts, fi[u], fj[u], bin[u]);
+        const double z = SCATTER ? (double)__ldg(xyz + 3 * p + 2) : 0.0;
+        in = point_cell_bin<SCATTER>(x, y, z, a, hts, fi[u], fj[u], bin[u]);
         z32[u] = __double2float_rn(z);
         if (!in && !SCATTER) atomicAdd(outside, 1ull);
       }
