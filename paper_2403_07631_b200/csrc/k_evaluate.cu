@@ -643,12 +643,12 @@ int launch_split(pct_ctx *ctx, const float *ground, const float *ceiling, int S,
   const size_t cm_bytes = (size_t)S * ((rows + 7) / 8) * wpr;
   if (int rc = ensure_scratch(ctx, cm_off + cm_bytes + 64)) return rc;
   uint32_t *bits = static_cast<uint32_t *>(ctx->scratch);
-  // tiles whose window saw no change skip the resolve/inflate work (R >= 8:
-  // cfg2 bnb 798 -> 473 us; at R = 4 the per-tile work is light and the
-  // change map costs the walk about what it saves, so it is off unless
-  // PCT_BNB_SKIP=1)
+  // tiles whose window saw no change skip the resolve/inflate work: cfg2
+  // (R = 8) bnb 798 -> 473 us, cfg3 (R = 4, open campus) 3.22 -> 2.00 ms;
+  // cfg1 about neutral (the change map costs the walk ~5 us).  PCT_BNB_SKIP=0
+  // turns it off.
   const char *skv = getenv("PCT_BNB_SKIP");
-  const bool use_skip = skv ? skv[0] == '1' : R >= 8;
+  const bool use_skip = skv ? skv[0] == '1' : true;
   unsigned char *chgmap = use_skip ? static_cast<unsigned char *>(ctx->scratch) + cm_off : nullptr;
   if (chgmap) PCT_CUDA(ctx, cudaMemsetAsync(chgmap, 0, cm_bytes, ctx->stream));
   if (ctx->enc_bytes < enc_bytes) {
@@ -1007,8 +1007,8 @@ int launch_evaluate_batch(pct_ctx *ctx, int n_maps, float *const *ground, float 
   if (int rc = ensure_scratch(ctx, bbytes + dbytes + obytes + (size_t)cm_total + 64)) return rc;
   char *sb = static_cast<char *>(ctx->scratch);
   unsigned char *cmb = reinterpret_cast<unsigned char *>(sb + bbytes + dbytes + obytes);
-  const char *skv = getenv("PCT_BNB_SKIP");  // R = 4: off by default (see launch_split)
-  const bool use_skip = skv && skv[0] == '1';
+  const char *skv = getenv("PCT_BNB_SKIP");  // on by default (see launch_split)
+  const bool use_skip = skv ? skv[0] == '1' : true;
   if (use_skip) PCT_CUDA(ctx, cudaMemsetAsync(cmb, 0, (size_t)cm_total, ctx->stream));
   int run_all = 0;
   {
