@@ -53,6 +53,21 @@ static int ensure_buffer(pct_ctx *ctx, void **buf, size_t *have, size_t bytes) {
   return PCT_OK;
 }
 
+constexpr size_t kUploadRing = 256 * 1024;
+
+const void *pin_upload(pct_ctx *ctx, const void *src, size_t n) {
+  if (!ctx->upload || n > kUploadRing / 4) return src;
+  size_t off = (ctx->upload_off + 15) & ~(size_t)15;
+  if (off + n > kUploadRing) {  // wrap: the oldest copies must have run
+    cudaStreamSynchronize(ctx->stream);
+    off = 0;
+  }
+  char *dst = static_cast<char *>(ctx->upload) + off;
+  std::memcpy(dst, src, n);
+  ctx->upload_off = off + n;
+  return dst;
+}
+
 int ensure_scratch(pct_ctx *ctx, size_t bytes) {
   return ensure_buffer(ctx, &ctx->scratch, &ctx->scratch_bytes, bytes);
 }
@@ -132,6 +147,7 @@ int pct_ctx_create(int device, pct_ctx **out) {
     }
     if (cudaMalloc(&ctx->dsmall, 65536) != cudaSuccess) { rc = PCT_E_NOMEM; break; }
     if (cudaMallocHost(&ctx->hsmall, 65536) != cudaSuccess) { rc = PCT_E_NOMEM; break; }
+    if (cudaMallocHost(&ctx->upload, kUploadRing) != cudaSuccess) { rc = PCT_E_NOMEM; break; }
   } while (0);
   if (rc) {
     pct_ctx_destroy(ctx);
@@ -155,6 +171,7 @@ int pct_ctx_destroy(pct_ctx *ctx) {
   if (ctx->hsmall) cudaFreeHost(ctx->hsmall);
   if (ctx->pinned_io) cudaFreeHost(ctx->pinned_io);
   if (ctx->pinned_batch) cudaFreeHost(ctx->pinned_batch);
+  if (ctx->upload) cudaFreeHost(ctx->upload);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
   return PCT_OK;

@@ -555,7 +555,7 @@ int launch_bounds_batch(pct_ctx *ctx, int n_maps, const void *const *xyz, const 
   }
   if (int rc = ensure_scratch(ctx, sizeof(BuildMap) * (size_t)n_maps)) return rc;
   BuildMap *dd = static_cast<BuildMap *>(ctx->scratch);
-  PCT_CUDA(ctx, cudaMemcpyAsync(dd, d.data(), sizeof(BuildMap) * n_maps, cudaMemcpyHostToDevice,
+  PCT_CUDA(ctx, cudaMemcpyAsync(dd, pin_upload(ctx, d.data(), sizeof(BuildMap) * n_maps), sizeof(BuildMap) * n_maps, cudaMemcpyHostToDevice,
                                 ctx->stream));
   PCT_CUDA(ctx, cudaMemcpyAsync(dk, keys_host, 64 * (size_t)n_maps, cudaMemcpyHostToDevice,
                                 ctx->stream));
@@ -626,9 +626,9 @@ int launch_build_batch(pct_ctx *ctx, int n_maps, const void *const *xyz, const i
     koff += 2 * (int64_t)fr.n_slices * cells;
     hoff += fr.n_slices;
   }
-  PCT_CUDA(ctx, cudaMemcpyAsync(dd, d.data(), sizeof(BuildMap) * n_maps, cudaMemcpyHostToDevice,
+  PCT_CUDA(ctx, cudaMemcpyAsync(dd, pin_upload(ctx, d.data(), sizeof(BuildMap) * n_maps), sizeof(BuildMap) * n_maps, cudaMemcpyHostToDevice,
                                 ctx->stream));
-  PCT_CUDA(ctx, cudaMemcpyAsync(hd, hh.data(), sizeof(double) * hcount, cudaMemcpyHostToDevice,
+  PCT_CUDA(ctx, cudaMemcpyAsync(hd, pin_upload(ctx, hh.data(), sizeof(double) * hcount), sizeof(double) * hcount, cudaMemcpyHostToDevice,
                                 ctx->stream));
   const int64_t tagi = (int64_t)(tag >> 1);
   if (ctx->keys_tag[0] != -2 || ctx->keys_tag[1] != tagi) {  // -2: a batch layout
@@ -720,7 +720,7 @@ int launch_build(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, const pct_
     unsigned *offs = reinterpret_cast<unsigned *>(b0 + hbytes + 256 + cbytes);
     unsigned *cur = reinterpret_cast<unsigned *>(b0 + hbytes + 256 + 2 * cbytes);
     unsigned long long *recs = reinterpret_cast<unsigned long long *>(b0 + hbytes + 256 + 3 * cbytes);
-    PCT_CUDA(ctx, cudaMemcpyAsync(hd, heights_host, (size_t)S * sizeof(double),
+    PCT_CUDA(ctx, cudaMemcpyAsync(hd, pin_upload(ctx, heights_host, (size_t)S * sizeof(double)), (size_t)S * sizeof(double),
                                   cudaMemcpyHostToDevice, ctx->stream));
     PCT_CUDA(ctx, cudaMemsetAsync(outs, 0, 8, ctx->stream));
     PCT_CUDA(ctx, cudaMemsetAsync(cnt, 0, (size_t)ntiles * 4 * kCtrPad, ctx->stream));
@@ -771,7 +771,7 @@ int launch_build(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, const pct_
   char *base = static_cast<char *>(ctx->scratch);
   double *hdev = reinterpret_cast<double *>(base);
   unsigned long long *outside = reinterpret_cast<unsigned long long *>(base + hbytes);
-  PCT_CUDA(ctx, cudaMemcpyAsync(hdev, heights_host, (size_t)S * sizeof(double),
+  PCT_CUDA(ctx, cudaMemcpyAsync(hdev, pin_upload(ctx, heights_host, (size_t)S * sizeof(double)), (size_t)S * sizeof(double),
                                 cudaMemcpyHostToDevice, ctx->stream));
   if (ctx->keys_tag[0] != S || ctx->keys_tag[1] != cells) {
     PCT_CUDA(ctx, cudaMemsetAsync(gkey, 0x00, plane * S, ctx->stream));

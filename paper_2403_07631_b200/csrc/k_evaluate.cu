@@ -708,7 +708,7 @@ int launch_split(pct_ctx *ctx, const float *ground, const float *ceiling, int S,
     if (items > INT32_MAX) return fail(ctx, PCT_E_INVALID, "grid too large");
     if constexpr (R == 4 || R == 8) {
      if (bnb) {
-      PCT_CUDA(ctx, cudaMemcpyToSymbolAsync(c_bw, bw.data(), bw.size() * sizeof(float), 0,
+      PCT_CUDA(ctx, cudaMemcpyToSymbolAsync(c_bw, pin_upload(ctx, bw.data(), bw.size() * sizeof(float)), bw.size() * sizeof(float), 0,
                                             cudaMemcpyHostToDevice, ctx->stream));
       auto kb = resolve_inflate_bnb_kernel<R, PR, TH, TW, BNT, kBnbMinBlocks<R>()>;
       constexpr int bsmem = BnbGeom<R, PR, TH, TW>::SMEM;
@@ -755,7 +755,7 @@ int launch_split(pct_ctx *ctx, const float *ground, const float *ceiling, int S,
       desc.off[0] = 0;
       desc.off[1] = (int)nitems;
       char *dptr = static_cast<char *>(ctx->scratch) + boff;
-      PCT_CUDA(ctx, cudaMemcpyAsync(dptr, &desc, sizeof(desc), cudaMemcpyHostToDevice, ctx->stream));
+      PCT_CUDA(ctx, cudaMemcpyAsync(dptr, pin_upload(ctx, &desc, sizeof(desc)), sizeof(desc), cudaMemcpyHostToDevice, ctx->stream));
       const EvalMap *dm = reinterpret_cast<const EvalMap *>(dptr);
       const int *doff = reinterpret_cast<const int *>(dptr + offsetof(decltype(desc), off));
       kb<<<grid, BNT, bsmem, ctx->stream>>>(dm, doff, 1);
@@ -875,12 +875,12 @@ int launch_evaluate(pct_ctx *ctx, const float *ground, const float *ceiling, int
     R = kside / 2;
   }
   EvalConsts K = make_consts(p, r_g);
-  PCT_CUDA(ctx, cudaMemcpyToSymbolAsync(c_K, &K, sizeof(K), 0, cudaMemcpyHostToDevice, ctx->stream));
+  PCT_CUDA(ctx, cudaMemcpyToSymbolAsync(c_K, pin_upload(ctx, &K, sizeof(K)), sizeof(K), 0, cudaMemcpyHostToDevice, ctx->stream));
   float wsym[81];
   const bool sym = mode == kEvalFull && symmetric_kernel(kernel_w, kside, R, wsym);
   if (mode == kEvalFull) {
     if (sym)
-      PCT_CUDA(ctx, cudaMemcpyToSymbolAsync(c_wsym, wsym, sizeof(wsym), 0, cudaMemcpyHostToDevice,
+      PCT_CUDA(ctx, cudaMemcpyToSymbolAsync(c_wsym, pin_upload(ctx, wsym, sizeof(wsym)), sizeof(wsym), 0, cudaMemcpyHostToDevice,
                                             ctx->stream));
     else
       PCT_CUDA(ctx, cudaMemcpyToSymbolAsync(c_wfull, kernel_w, sizeof(float) * kside * kside, 0,
@@ -933,8 +933,8 @@ int launch_evaluate_batch(pct_ctx *ctx, int n_maps, float *const *ground, float 
     return PCT_OK;
   }
   EvalConsts K = make_consts(p, r_g);
-  PCT_CUDA(ctx, cudaMemcpyToSymbolAsync(c_K, &K, sizeof(K), 0, cudaMemcpyHostToDevice, ctx->stream));
-  PCT_CUDA(ctx, cudaMemcpyToSymbolAsync(c_bw, bw.data(), bw.size() * sizeof(float), 0,
+  PCT_CUDA(ctx, cudaMemcpyToSymbolAsync(c_K, pin_upload(ctx, &K, sizeof(K)), sizeof(K), 0, cudaMemcpyHostToDevice, ctx->stream));
+  PCT_CUDA(ctx, cudaMemcpyToSymbolAsync(c_bw, pin_upload(ctx, bw.data(), bw.size() * sizeof(float)), bw.size() * sizeof(float), 0,
                                         cudaMemcpyHostToDevice, ctx->stream));
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
@@ -1054,9 +1054,9 @@ int launch_evaluate_batch(pct_ctx *ctx, int n_maps, float *const *ground, float 
   }
   EvalMap *dm = reinterpret_cast<EvalMap *>(sb + bbytes);
   int *doff = reinterpret_cast<int *>(sb + bbytes + dbytes);
-  PCT_CUDA(ctx, cudaMemcpyAsync(dm, hm.data(), sizeof(EvalMap) * n_maps, cudaMemcpyHostToDevice,
+  PCT_CUDA(ctx, cudaMemcpyAsync(dm, pin_upload(ctx, hm.data(), sizeof(EvalMap) * n_maps), sizeof(EvalMap) * n_maps, cudaMemcpyHostToDevice,
                                 ctx->stream));
-  PCT_CUDA(ctx, cudaMemcpyAsync(doff, off.data(), sizeof(int) * (n_maps + 1),
+  PCT_CUDA(ctx, cudaMemcpyAsync(doff, pin_upload(ctx, off.data(), sizeof(int) * (n_maps + 1)), sizeof(int) * (n_maps + 1),
                                 cudaMemcpyHostToDevice, ctx->stream));
   terrain_walk_batch_kernel<1><<<dim3((unsigned)walk_blocks, n_maps), kWalkNT, 0, ctx->stream>>>(dm);
   if (int rc = check_launch(ctx, "terrain_walk_batch_kernel")) return rc;

@@ -503,7 +503,7 @@ int simplify_window_batch(pct_ctx *ctx, int n_maps, const float *const *ground,
     h[m].table = dt + (size_t)m * S_max;
     cmax = std::max<int64_t>(cmax, cells[m]);
   }
-  PCT_CUDA(ctx, cudaMemcpyAsync(dd, h.data(), sizeof(SimpMap) * n_maps, cudaMemcpyHostToDevice,
+  PCT_CUDA(ctx, cudaMemcpyAsync(dd, pin_upload(ctx, h.data(), sizeof(SimpMap) * n_maps), sizeof(SimpMap) * n_maps, cudaMemcpyHostToDevice,
                                 ctx->stream));
   PCT_CUDA(ctx, cudaMemsetAsync(dt, 0, tbytes, ctx->stream));
   const size_t smem = (size_t)S_max * 8;

@@ -27,6 +27,10 @@ struct pct_ctx {
   size_t pinned_io_bytes = 0;
   void *pinned_batch = nullptr;  // per-map result slots of pct_tomo_run_batch
   size_t pinned_batch_bytes = 0;
+  // pinned ring for small host->device copies (constants, descriptors,
+  // heights): copies from pageable memory may synchronise with the stream
+  void *upload = nullptr;
+  size_t upload_off = 0;
   // small device/pinned buffers for reductions and flags
   void *dsmall = nullptr;   // 64 KiB device
   void *hsmall = nullptr;   // 64 KiB pinned host
@@ -60,6 +64,9 @@ int cuda_fail(pct_ctx *ctx, cudaError_t e, const char *what);
 int ensure_scratch(pct_ctx *ctx, size_t bytes);
 int ensure_staging(pct_ctx *ctx, size_t bytes);
 int check_launch(pct_ctx *ctx, const char *what);
+// copy n bytes of host data into the context's pinned upload ring and return
+// the pinned address (src itself if it does not fit)
+const void *pin_upload(pct_ctx *ctx, const void *src, size_t n);
 
 #define PCT_CUDA(ctx, call)                                  \
   do {                                                       \
