@@ -266,8 +266,9 @@ class PinnedPool:
     block goes back to the pool (not to the OS) when they are collected, so
     repeated pipelines do not pay for page locking again."""
 
-    def __init__(self, ctx: Context):
-        self.ctx = ctx
+    def __init__(self, device: int):
+        self.device = device
+        self.ctx = None  # the context page-locking new blocks (set per call)
         self.free: dict[int, list[int]] = {}
         self.lock = threading.Lock()
 
@@ -276,7 +277,7 @@ class PinnedPool:
         q = 1 << 20
         return max(q, (nbytes + q - 1) // q * q)
 
-    def array(self, shape, dtype) -> np.ndarray:
+    def array(self, shape, dtype, ctx: Context | None = None) -> np.ndarray:
         dt = np.dtype(dtype)
         count = int(np.prod(shape))
         size = self._class(count * dt.itemsize)
@@ -284,9 +285,9 @@ class PinnedPool:
             lst = self.free.get(size)
             ptr = lst.pop() if lst else None
         if ptr is None:
+            ctx = ctx or self.ctx
             p = C.c_void_p()
-            self.ctx.check(self.ctx.lib.pct_host_alloc(self.ctx.h, C.c_size_t(size), C.byref(p)),
-                           "host_alloc")
+            ctx.check(ctx.lib.pct_host_alloc(ctx.h, C.c_size_t(size), C.byref(p)), "host_alloc")
             ptr = p.value
         raw = (C.c_char * size).from_address(ptr)
         raw._pct_block = _PinnedBlock(self, ptr, size)
@@ -297,11 +298,29 @@ class PinnedPool:
             self.free.setdefault(block.nbytes, []).append(block.ptr)
 
 
+_POOLS: dict[int, PinnedPool] = {}
+_POOLS_LOCK = threading.Lock()
+
+
 def pinned_pool(ctx: Context) -> PinnedPool:
-    pool = getattr(ctx, "_pinned_pool", None)
-    if pool is None:
-        pool = ctx._pinned_pool = PinnedPool(ctx)
-    return pool
+    """The process-wide pool of ctx's device: contexts share page-locked
+    blocks (any stream can copy into them), so maps read back on alternating
+    contexts re-use each other's blocks instead of page-locking new ones."""
+    with _POOLS_LOCK:
+        pool = _POOLS.get(ctx.device)
+        if pool is None:
+            pool = _POOLS[ctx.device] = PinnedPool(ctx.device)
+    return _BoundPool(pool, ctx)
+
+
+class _BoundPool:
+    """A device pool with the context that page-locks its new blocks."""
+
+    def __init__(self, pool: PinnedPool, ctx: Context):
+        self.pool, self.ctx = pool, ctx
+
+    def array(self, shape, dtype) -> np.ndarray:
+        return self.pool.array(shape, dtype, self.ctx)
 
 
 def trav_params_c(params, r_g: float) -> TravParamsC:

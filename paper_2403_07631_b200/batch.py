@@ -140,3 +140,57 @@ def evaluate_maps(clouds, d_s, r_g, params, *, workers=8, device=None, eps_e=1e-
         if own:
             runner.close()
     return [_to_tomogram(h[0], h[1], keep, d_s, r_g) for h, keep in res]
+
+
+def stream_maps(clouds, d_s, r_g, params, *, workers=2, device=None, eps_e=1e-6,
+                c_barrier=50.0, runner: BatchRunner | None = None):
+    """Generator over ``clouds`` (host arrays or PointClouds, ideally in pinned
+    memory): yields, in input order, the simplified tomogram of each cloud
+    with every surviving layer already copied to host memory.
+
+    Each map is one native ``pct_tomo_run`` (upload, build, evaluate,
+    simplify) plus the read-back of its surviving layers, on one of
+    ``workers`` contexts; up to ``workers`` maps are in flight, so the
+    host->device upload of one map overlaps the device->host read-back of
+    the previous one (the PCIe link is full duplex) and its kernels."""
+    if d_s <= 0 or r_g <= 0:
+        raise ValueError("d_s and r_g must be positive")
+    own = runner is None
+    runner = runner or BatchRunner(device, workers)
+    w = np.ascontiguousarray(build_kernel(params.d_inf, params.d_sm, r_g).weights)
+    pc = _lib.trav_params_c(params, r_g)
+
+    def one(a):
+        code = _lib.PCT_F32 if a.dtype == np.float32 else _lib.PCT_F64
+        ctx = runner.free.get()  # held until the read-back is done
+        try:
+            with ctx.lock:
+                h = C.c_void_p()
+                keep = np.empty(65536, np.int32)
+                nk = C.c_int32()
+                ctx.check(ctx.lib.pct_tomo_run(ctx.h, a.ctypes.data, a.shape[0], code, 1,
+                                               float(d_s), float(r_g), GRID_SIDE_LIMIT,
+                                               C.byref(pc), w.ctypes.data, w.shape[0],
+                                               float(eps_e), float(c_barrier), C.byref(h),
+                                               keep.ctypes.data, C.byref(nk)), "pct_tomo_run")
+                return _to_tomogram(ctx, h, keep[:nk.value].tolist(), d_s, r_g).materialize()
+        finally:
+            runner.free.put(ctx)
+
+    depth = max(1, len(runner.ctxs))
+    pending = []
+    try:
+        for c in clouds:
+            a = np.ascontiguousarray(c.xyz if hasattr(c, "xyz") else c)
+            if a.dtype not in (np.float32, np.float64) or a.ndim != 2 or a.shape[1] != 3:
+                raise ValueError("clouds must be (N, 3) float32/float64 arrays")
+            pending.append(runner.pool.submit(one, a))
+            if len(pending) >= depth:
+                yield pending.pop(0).result()
+        while pending:
+            yield pending.pop(0).result()
+    finally:
+        for f in pending:
+            f.cancel()
+        if own:
+            runner.close()

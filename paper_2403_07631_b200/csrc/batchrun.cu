@@ -181,7 +181,7 @@ int run_group(pct_ctx *c0, int n_maps, const void *const *xyz, const int64_t *n_
     pct_tomo *t = toms[m];
     t->heights = heights[m];
     const size_t bytes = (size_t)fr.n_slices * fr.rows * fr.cols * sizeof(float);
-    if (cudaMallocAsync(reinterpret_cast<void **>(&t->cost), bytes, c0->stream) != cudaSuccess) {
+    if (cudaMallocFromPoolAsync(reinterpret_cast<void **>(&t->cost), bytes, c0->mempool, c0->stream) != cudaSuccess) {
       free_all();
       return fail(c0, PCT_E_NOMEM, "cudaMallocAsync(cost)");
     }

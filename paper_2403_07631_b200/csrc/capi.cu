@@ -68,6 +68,41 @@ const void *pin_upload(pct_ctx *ctx, const void *src, size_t n) {
   return dst;
 }
 
+namespace {
+__global__ void small_copy_kernel(uint32_t *__restrict__ dst, const uint32_t *__restrict__ src,
+                                  size_t words, unsigned char *__restrict__ dtail,
+                                  const unsigned char *__restrict__ stail, int ntail) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < words;
+       i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+  if (blockIdx.x == 0 && (int)threadIdx.x < ntail) dtail[threadIdx.x] = stail[threadIdx.x];
+}
+
+cudaError_t small_copy(pct_ctx *ctx, void *dst, const void *src, size_t n) {
+  if (n == 0) return cudaSuccess;
+  if ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 3)
+    return cudaMemcpyAsync(dst, src, n, cudaMemcpyDefault, ctx->stream);
+  const size_t words = n / 4;
+  const int ntail = (int)(n & 3);
+  const unsigned grid = (unsigned)std::max<size_t>(1, std::min<size_t>((words + 255) / 256, 64));
+  small_copy_kernel<<<grid, 256, 0, ctx->stream>>>(
+      static_cast<uint32_t *>(dst), static_cast<const uint32_t *>(src), words,
+      static_cast<unsigned char *>(dst) + 4 * words,
+      static_cast<const unsigned char *>(src) + 4 * words, ntail);
+  return cudaGetLastError();
+}
+}  // namespace
+
+cudaError_t upload_async(pct_ctx *ctx, void *ddst, const void *src, size_t n) {
+  const void *p = pin_upload(ctx, src, n);
+  if (p == src) return cudaMemcpyAsync(ddst, src, n, cudaMemcpyHostToDevice, ctx->stream);
+  return small_copy(ctx, ddst, p, n);  // pinned host memory is device-addressable (UVA)
+}
+
+cudaError_t readback_async(pct_ctx *ctx, void *hdst, const void *dsrc, size_t n) {
+  return small_copy(ctx, hdst, dsrc, n);
+}
+
 int ensure_scratch(pct_ctx *ctx, size_t bytes) {
   return ensure_buffer(ctx, &ctx->scratch, &ctx->scratch_bytes, bytes);
 }
@@ -139,11 +174,17 @@ int pct_ctx_create(int device, pct_ctx **out) {
       break;
     }
     ctx->stream = ctx->own_stream;
-    // keep freed stacks cached in the pool: repeated builds re-use memory
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    // a memory pool per context: stacks freed on this context's stream are
+    // re-used in stream order by its next map (no growth, no dependency on
+    // another context's queue); freed memory stays cached in the pool
+    {
+      cudaMemPoolProps props = {};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = device;
+      if (cudaMemPoolCreate(&ctx->mempool, &props) != cudaSuccess) { rc = PCT_E_CUDA; break; }
       uint64_t thr = UINT64_MAX;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      cudaMemPoolSetAttribute(ctx->mempool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
     if (cudaMalloc(&ctx->dsmall, 65536) != cudaSuccess) { rc = PCT_E_NOMEM; break; }
     if (cudaMallocHost(&ctx->hsmall, 65536) != cudaSuccess) { rc = PCT_E_NOMEM; break; }
@@ -173,6 +214,7 @@ int pct_ctx_destroy(pct_ctx *ctx) {
   if (ctx->pinned_batch) cudaFreeHost(ctx->pinned_batch);
   if (ctx->upload) cudaFreeHost(ctx->upload);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  if (ctx->mempool) cudaMemPoolDestroy(ctx->mempool);  // deferred while blocks are live
   delete ctx;
   return PCT_OK;
 }
@@ -198,7 +240,7 @@ int pct_malloc(pct_ctx *ctx, size_t bytes, void **dptr) {
   if (!dptr) return fail(ctx, PCT_E_INVALID, "dptr is NULL");
   *dptr = nullptr;
   if (bytes == 0) bytes = 1;
-  PCT_CUDA(ctx, cudaMallocAsync(dptr, bytes, ctx->stream));
+  PCT_CUDA(ctx, cudaMallocFromPoolAsync(dptr, bytes, ctx->mempool, ctx->stream));
   return PCT_OK;
 }
 
@@ -388,9 +430,9 @@ int tomo_alloc(pct_ctx *ctx, const pct_frame &fr, pct_tomo **out) {
   if (!t) return fail(ctx, PCT_E_NOMEM, "out of host memory");
   t->fr = fr;
   const size_t bytes = (size_t)fr.n_slices * fr.rows * fr.cols * sizeof(float);
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void **>(&t->ground), bytes, ctx->stream);
+  cudaError_t e = cudaMallocFromPoolAsync(reinterpret_cast<void **>(&t->ground), bytes, ctx->mempool, ctx->stream);
   if (e == cudaSuccess)
-    e = cudaMallocAsync(reinterpret_cast<void **>(&t->ceiling), bytes, ctx->stream);
+    e = cudaMallocFromPoolAsync(reinterpret_cast<void **>(&t->ceiling), bytes, ctx->mempool, ctx->stream);
   if (e != cudaSuccess) {
     pct_tomo_free(ctx, t);
     return cuda_fail(ctx, e, "cudaMallocAsync(tomogram)");
@@ -463,7 +505,7 @@ int pct_tomo_evaluate(pct_ctx *ctx, pct_tomo *t, const pct_trav_params *p, const
   if (!t) return fail(ctx, PCT_E_INVALID, "tomogram is NULL");
   if (int rc = check_params(ctx, p)) return rc;
   const size_t bytes = (size_t)t->fr.n_slices * t->fr.rows * t->fr.cols * sizeof(float);
-  if (!t->cost) PCT_CUDA(ctx, cudaMallocAsync(reinterpret_cast<void **>(&t->cost), bytes, ctx->stream));
+  if (!t->cost) PCT_CUDA(ctx, cudaMallocFromPoolAsync(reinterpret_cast<void **>(&t->cost), bytes, ctx->mempool, ctx->stream));
   return launch_evaluate(ctx, t->ground, t->ceiling, t->fr.n_slices, t->fr.rows, t->fr.cols,
                          t->fr.r_g, *p, kernel_w, kside, t->cost, kEvalFull);
 }

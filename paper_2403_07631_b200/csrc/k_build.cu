@@ -514,8 +514,7 @@ int launch_bounds(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, double lo
   unsigned long long *keys = static_cast<unsigned long long *>(ctx->dsmall);
   unsigned long long init[7] = {~0ull, ~0ull, ~0ull, 0ull, 0ull, 0ull, 0ull};
   unsigned long long *hk = static_cast<unsigned long long *>(ctx->hsmall);
-  std::memcpy(hk, init, sizeof(init));
-  PCT_CUDA(ctx, cudaMemcpyAsync(keys, hk, sizeof(init), cudaMemcpyHostToDevice, ctx->stream));
+  PCT_CUDA(ctx, upload_async(ctx, keys, init, sizeof(init)));
   if (dtype == PCT_F32) {  // float4 path when 16 B aligned, scalar otherwise
     bounds_kernel<float><<<grid_for(ctx, (n + 3) / 4, 256), 256, 0, ctx->stream>>>(
         static_cast<const float *>(xyz), n, keys);
@@ -524,7 +523,7 @@ int launch_bounds(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, double lo
         static_cast<const double *>(xyz), n, keys);
   }
   if (int rc = check_launch(ctx, "bounds_kernel")) return rc;
-  PCT_CUDA(ctx, cudaMemcpyAsync(hk, keys, sizeof(init), cudaMemcpyDeviceToHost, ctx->stream));
+  PCT_CUDA(ctx, readback_async(ctx, hk, keys, sizeof(init)));
   PCT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   if (hk[6]) return fail(ctx, PCT_E_NONFINITE, "point cloud contains non-finite coordinates");
   for (int c = 0; c < 3; ++c) {
@@ -555,8 +554,7 @@ int launch_bounds_batch(pct_ctx *ctx, int n_maps, const void *const *xyz, const 
   }
   if (int rc = ensure_scratch(ctx, sizeof(BuildMap) * (size_t)n_maps)) return rc;
   BuildMap *dd = static_cast<BuildMap *>(ctx->scratch);
-  PCT_CUDA(ctx, cudaMemcpyAsync(dd, pin_upload(ctx, d.data(), sizeof(BuildMap) * n_maps), sizeof(BuildMap) * n_maps, cudaMemcpyHostToDevice,
-                                ctx->stream));
+  PCT_CUDA(ctx, upload_async(ctx, dd, d.data(), sizeof(BuildMap) * n_maps));
   PCT_CUDA(ctx, cudaMemcpyAsync(dk, keys_host, 64 * (size_t)n_maps, cudaMemcpyHostToDevice,
                                 ctx->stream));
   const int per_map = std::max(1, std::min(grid_for(ctx, (nmax + 3) / 4, 256), 64));
@@ -626,10 +624,8 @@ int launch_build_batch(pct_ctx *ctx, int n_maps, const void *const *xyz, const i
     koff += 2 * (int64_t)fr.n_slices * cells;
     hoff += fr.n_slices;
   }
-  PCT_CUDA(ctx, cudaMemcpyAsync(dd, pin_upload(ctx, d.data(), sizeof(BuildMap) * n_maps), sizeof(BuildMap) * n_maps, cudaMemcpyHostToDevice,
-                                ctx->stream));
-  PCT_CUDA(ctx, cudaMemcpyAsync(hd, pin_upload(ctx, hh.data(), sizeof(double) * hcount), sizeof(double) * hcount, cudaMemcpyHostToDevice,
-                                ctx->stream));
+  PCT_CUDA(ctx, upload_async(ctx, dd, d.data(), sizeof(BuildMap) * n_maps));
+  PCT_CUDA(ctx, upload_async(ctx, hd, hh.data(), sizeof(double) * hcount));
   const int64_t tagi = (int64_t)(tag >> 1);
   if (ctx->keys_tag[0] != -2 || ctx->keys_tag[1] != tagi) {  // -2: a batch layout
     int64_t off = 0;
@@ -720,8 +716,7 @@ int launch_build(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, const pct_
     unsigned *offs = reinterpret_cast<unsigned *>(b0 + hbytes + 256 + cbytes);
     unsigned *cur = reinterpret_cast<unsigned *>(b0 + hbytes + 256 + 2 * cbytes);
     unsigned long long *recs = reinterpret_cast<unsigned long long *>(b0 + hbytes + 256 + 3 * cbytes);
-    PCT_CUDA(ctx, cudaMemcpyAsync(hd, pin_upload(ctx, heights_host, (size_t)S * sizeof(double)), (size_t)S * sizeof(double),
-                                  cudaMemcpyHostToDevice, ctx->stream));
+    PCT_CUDA(ctx, upload_async(ctx, hd, heights_host, (size_t)S * sizeof(double)));
     PCT_CUDA(ctx, cudaMemsetAsync(outs, 0, 8, ctx->stream));
     PCT_CUDA(ctx, cudaMemsetAsync(cnt, 0, (size_t)ntiles * 4 * kCtrPad, ctx->stream));
     BinArgs a{fr.origin_x, fr.origin_y, fr.z_min, fr.r_g, fr.d_s, 1.0 / fr.r_g, 1.0 / fr.d_s,
@@ -771,8 +766,7 @@ int launch_build(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, const pct_
   char *base = static_cast<char *>(ctx->scratch);
   double *hdev = reinterpret_cast<double *>(base);
   unsigned long long *outside = reinterpret_cast<unsigned long long *>(base + hbytes);
-  PCT_CUDA(ctx, cudaMemcpyAsync(hdev, pin_upload(ctx, heights_host, (size_t)S * sizeof(double)), (size_t)S * sizeof(double),
-                                cudaMemcpyHostToDevice, ctx->stream));
+  PCT_CUDA(ctx, upload_async(ctx, hdev, heights_host, (size_t)S * sizeof(double)));
   if (ctx->keys_tag[0] != S || ctx->keys_tag[1] != cells) {
     PCT_CUDA(ctx, cudaMemsetAsync(gkey, 0x00, plane * S, ctx->stream));
     PCT_CUDA(ctx, cudaMemsetAsync(ckey, 0xFF, plane * S, ctx->stream));

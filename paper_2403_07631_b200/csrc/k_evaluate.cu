@@ -755,7 +755,7 @@ int launch_split(pct_ctx *ctx, const float *ground, const float *ceiling, int S,
       desc.off[0] = 0;
       desc.off[1] = (int)nitems;
       char *dptr = static_cast<char *>(ctx->scratch) + boff;
-      PCT_CUDA(ctx, cudaMemcpyAsync(dptr, pin_upload(ctx, &desc, sizeof(desc)), sizeof(desc), cudaMemcpyHostToDevice, ctx->stream));
+      PCT_CUDA(ctx, upload_async(ctx, dptr, &desc, sizeof(desc)));
       const EvalMap *dm = reinterpret_cast<const EvalMap *>(dptr);
       const int *doff = reinterpret_cast<const int *>(dptr + offsetof(decltype(desc), off));
       kb<<<grid, BNT, bsmem, ctx->stream>>>(dm, doff, 1);
@@ -1054,10 +1054,8 @@ int launch_evaluate_batch(pct_ctx *ctx, int n_maps, float *const *ground, float 
   }
   EvalMap *dm = reinterpret_cast<EvalMap *>(sb + bbytes);
   int *doff = reinterpret_cast<int *>(sb + bbytes + dbytes);
-  PCT_CUDA(ctx, cudaMemcpyAsync(dm, pin_upload(ctx, hm.data(), sizeof(EvalMap) * n_maps), sizeof(EvalMap) * n_maps, cudaMemcpyHostToDevice,
-                                ctx->stream));
-  PCT_CUDA(ctx, cudaMemcpyAsync(doff, pin_upload(ctx, off.data(), sizeof(int) * (n_maps + 1)), sizeof(int) * (n_maps + 1),
-                                cudaMemcpyHostToDevice, ctx->stream));
+  PCT_CUDA(ctx, upload_async(ctx, dm, hm.data(), sizeof(EvalMap) * n_maps));
+  PCT_CUDA(ctx, upload_async(ctx, doff, off.data(), sizeof(int) * (n_maps + 1)));
   terrain_walk_batch_kernel<1><<<dim3((unsigned)walk_blocks, n_maps), kWalkNT, 0, ctx->stream>>>(dm);
   if (int rc = check_launch(ctx, "terrain_walk_batch_kernel")) return rc;
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(off[n_maps], slots));

@@ -324,7 +324,7 @@ int run_simplify(pct_ctx *ctx, const float *ground, const float *cost, int S, in
   const bool pinned = tbytes + (size_t)S * (sizeof(Triple) + sizeof(int)) + 64 <= 65536;
   char *hbase = static_cast<char *>(ctx->hsmall);
   if (pinned) {
-    PCT_CUDA(ctx, cudaMemcpyAsync(hbase, table, tbytes, cudaMemcpyDeviceToHost, ctx->stream));
+    PCT_CUDA(ctx, readback_async(ctx, hbase, table, tbytes));
     PCT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     std::memcpy(htable.data(), hbase, tbytes);
   } else {
@@ -350,17 +350,17 @@ int run_simplify(pct_ctx *ctx, const float *ground, const float *cost, int S, in
     const int T = (int)ts.size();
     Triple *htr = reinterpret_cast<Triple *>(hbase + tbytes);
     int *hfl = reinterpret_cast<int *>(hbase + tbytes + (size_t)S * sizeof(Triple));
-    if (pinned) std::memcpy(htr, ts.data(), sizeof(Triple) * T);
-    PCT_CUDA(ctx, cudaMemcpyAsync(dtr, pinned ? htr : ts.data(), sizeof(Triple) * T,
-                                  cudaMemcpyHostToDevice, ctx->stream));
+    (void)htr;
+    PCT_CUDA(ctx, upload_async(ctx, dtr, ts.data(), sizeof(Triple) * T));
     PCT_CUDA(ctx, cudaMemsetAsync(dflags, 0, sizeof(int) * T, ctx->stream));
     int64_t bx = (A.cells + 255) / 256;
     if (bx > blocks_x) bx = blocks_x;
     triples_kernel<<<dim3((unsigned)bx, T), 256, 0, ctx->stream>>>(A, dtr, dflags);
     if (int rc = check_launch(ctx, "triples_kernel")) return rc;
     std::vector<int> hf(T);
-    PCT_CUDA(ctx, cudaMemcpyAsync(pinned ? hfl : hf.data(), dflags, sizeof(int) * T,
-                                  cudaMemcpyDeviceToHost, ctx->stream));
+    if (pinned) PCT_CUDA(ctx, readback_async(ctx, hfl, dflags, sizeof(int) * T));
+    else PCT_CUDA(ctx, cudaMemcpyAsync(hf.data(), dflags, sizeof(int) * T, cudaMemcpyDeviceToHost,
+                                       ctx->stream));
     PCT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     if (pinned) std::memcpy(hf.data(), hfl, sizeof(int) * T);
     for (int i = 0; i < T; ++i) cache[{ts[i].below, ts[i].k, ts[i].above}] = hf[i] != 0;
@@ -503,8 +503,7 @@ int simplify_window_batch(pct_ctx *ctx, int n_maps, const float *const *ground,
     h[m].table = dt + (size_t)m * S_max;
     cmax = std::max<int64_t>(cmax, cells[m]);
   }
-  PCT_CUDA(ctx, cudaMemcpyAsync(dd, pin_upload(ctx, h.data(), sizeof(SimpMap) * n_maps), sizeof(SimpMap) * n_maps, cudaMemcpyHostToDevice,
-                                ctx->stream));
+  PCT_CUDA(ctx, upload_async(ctx, dd, h.data(), sizeof(SimpMap) * n_maps));
   PCT_CUDA(ctx, cudaMemsetAsync(dt, 0, tbytes, ctx->stream));
   const size_t smem = (size_t)S_max * 8;
   PCT_CUDA(ctx, cudaFuncSetAttribute(window_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -29,6 +29,7 @@ struct pct_ctx {
   size_t pinned_batch_bytes = 0;
   // pinned ring for small host->device copies (constants, descriptors,
   // heights): copies from pageable memory may synchronise with the stream
+  cudaMemPool_t mempool = nullptr;  // this context's stream-ordered allocations
   void *upload = nullptr;
   size_t upload_off = 0;
   // small device/pinned buffers for reductions and flags
@@ -67,6 +68,13 @@ int check_launch(pct_ctx *ctx, const char *what);
 // copy n bytes of host data into the context's pinned upload ring and return
 // the pinned address (src itself if it does not fit)
 const void *pin_upload(pct_ctx *ctx, const void *src, size_t n);
+// small transfers moved by a kernel through mapped pinned memory instead of
+// the copy engines, so they never queue behind another context's bulk copy:
+// upload_async stages src in the upload ring and copies it to ddst;
+// readback_async copies n bytes of device memory to pinned host memory hdst
+// (visible to the host after the stream synchronises)
+cudaError_t upload_async(pct_ctx *ctx, void *ddst, const void *src, size_t n);
+cudaError_t readback_async(pct_ctx *ctx, void *hdst, const void *dsrc, size_t n);
 
 #define PCT_CUDA(ctx, call)                                  \
   do {                                                       \

@@ -63,20 +63,28 @@ class DeviceStack:
             self._host[k] = a
         return a
 
-    def prefetch(self, ks) -> None:
-        """Copy several slices to (pinned) host memory with one synchronisation."""
-        todo = [k for k in dict.fromkeys(ks) if k not in self._host]
+    def prefetch(self, ks, sync: bool = True) -> None:
+        """Copy several slices to (pinned) host memory: one pinned block, one
+        copy per run of consecutive slices, one synchronisation (none with
+        ``sync=False``: the caller synchronises the context's stream)."""
+        todo = sorted(k for k in set(ks) if k not in self._host)
         if not todo:
             return
-        pool = _lib.pinned_pool(self.ctx)
+        block = _lib.pinned_pool(self.ctx).array((len(todo), self.rows, self.cols), np.float32)
         with self.ctx.lock:
-            for k in todo:
-                a = pool.array((self.rows, self.cols), np.float32)
-                self.ctx.check(self.ctx.lib.pct_memcpy_d2h_async(self.ctx.h, a.ctypes.data,
-                                                                 self.slice_ptr(k), a.nbytes),
-                               "d2h")
-                self._host[k] = a
-            self.ctx.check(self.ctx.lib.pct_sync(self.ctx.h), "sync")
+            i = 0
+            while i < len(todo):
+                j = i
+                while j + 1 < len(todo) and todo[j + 1] == todo[j] + 1:
+                    j += 1
+                self.ctx.check(self.ctx.lib.pct_memcpy_d2h_async(
+                    self.ctx.h, block[i].ctypes.data, self.slice_ptr(todo[i]),
+                    (j - i + 1) * self.plane_bytes), "d2h")
+                i = j + 1
+            if sync:
+                self.ctx.check(self.ctx.lib.pct_sync(self.ctx.h), "sync")
+        for n, k in enumerate(todo):
+            self._host[k] = block[n]
 
     def host_all(self) -> np.ndarray:
         out = np.empty((self.n_slices, self.rows, self.cols), np.float32)
@@ -234,8 +242,13 @@ class Tomogram:
             for l in (s.ground, s.ceiling, s.cost):
                 if isinstance(l, Layer) and l._values is None and l._stack is not None:
                     groups.setdefault(id(l._stack), (l._stack, []))[1].append(l._k)
+        ctxs = {}
         for stack, ks in groups.values():
-            stack.prefetch(ks)
+            stack.prefetch(ks, sync=False)
+            ctxs[id(stack.ctx)] = stack.ctx
+        for ctx in ctxs.values():
+            with ctx.lock:
+                ctx.check(ctx.lib.pct_sync(ctx.h), "sync")
         return self
 
     def _stack(self, attr):

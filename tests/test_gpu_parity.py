@@ -359,6 +359,28 @@ def test_batch_runner_matches_single_maps():
                                       getattr(b, attr).values.view(np.uint32))
 
 
+def test_stream_maps_matches_single_maps():
+    """stream_maps (maps in flight on two contexts, layers read back in the
+    worker) yields, in order, the per-map drop-in results."""
+    from paper_2403_07631_b200 import synth
+    from paper_2403_07631_b200.batch import stream_maps
+    clouds = [synth.generate(4, 60_000, 2000 + m) for m in range(7)]
+    clouds[3] = clouds[3].astype(np.float64)
+    outs = list(stream_maps(clouds, 0.5, 0.1, pct.TravParams(), workers=2))
+    assert len(outs) == len(clouds)
+    for xyz, got in zip(clouds, outs):
+        ev = pct.evaluate_tomogram(pct.build_tomogram(pct.PointCloud(xyz), 0.5, 0.1),
+                                   pct.TravParams())
+        want = pct.simplify_tomogram(ev)
+        assert [s.plane_height for s in got.slices] == [s.plane_height for s in want.slices]
+        for a, b in zip(got.slices, want.slices):
+            for attr in ("ground", "ceiling", "cost"):
+                la = getattr(a, attr)  # already on the host
+                assert la._values is not None or la._k in la._stack._host
+                assert np.array_equal(getattr(a, attr).values.view(np.uint32),
+                                      getattr(b, attr).values.view(np.uint32))
+
+
 @pytest.mark.parametrize("name", ["ref_random_multilayer_s9", "ref_spiral_s3", "synth_cfg0",
                                   "synth_cfg1"])
 def test_lga_archives_byte_identical(golden, tmp_path, name):
