@@ -8,6 +8,8 @@
 
 #include <cmath>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -101,6 +103,57 @@ cudaError_t upload_async(pct_ctx *ctx, void *ddst, const void *src, size_t n) {
 
 cudaError_t readback_async(pct_ctx *ctx, void *hdst, const void *dsrc, size_t n) {
   return small_copy(ctx, hdst, dsrc, n);
+}
+
+namespace {
+struct ResidentConst {
+  std::vector<char> bytes;
+  cudaEvent_t uploaded = nullptr;
+  const pct_ctx *uploader = nullptr;
+};
+std::recursive_mutex g_const_mu;
+std::map<void *, ResidentConst> g_const;     // symbol device address -> content
+std::map<pct_ctx *, cudaEvent_t> g_const_users;  // last launch reading constants
+}  // namespace
+
+ConstBank::ConstBank(pct_ctx *ctx) : ctx_(ctx) { g_const_mu.lock(); }
+
+ConstBank::~ConstBank() {
+  cudaEvent_t &ev = g_const_users[ctx_];
+  if (!ev) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  if (ev) cudaEventRecord(ev, ctx_->stream);
+  g_const_mu.unlock();
+}
+
+cudaError_t ConstBank::set(void *addr, const void *src, size_t n) {
+  ResidentConst &r = g_const[addr];
+  if (r.bytes.size() == n && std::memcmp(r.bytes.data(), src, n) == 0) {
+    if (r.uploaded && r.uploader != ctx_) return cudaStreamWaitEvent(ctx_->stream, r.uploaded, 0);
+    return cudaSuccess;
+  }
+  for (auto &u : g_const_users)
+    if (u.first != ctx_ && u.first->device == ctx_->device && u.second)
+      if (cudaError_t e = cudaStreamWaitEvent(ctx_->stream, u.second, 0)) return e;
+  if (cudaError_t e = cudaMemcpyAsync(addr, pin_upload(ctx_, src, n), n, cudaMemcpyHostToDevice,
+                                      ctx_->stream))
+    return e;
+  if (!r.uploaded)
+    if (cudaError_t e = cudaEventCreateWithFlags(&r.uploaded, cudaEventDisableTiming)) return e;
+  if (cudaError_t e = cudaEventRecord(r.uploaded, ctx_->stream)) return e;
+  r.uploader = ctx_;
+  r.bytes.assign(static_cast<const char *>(src), static_cast<const char *>(src) + n);
+  return cudaSuccess;
+}
+
+void const_bank_forget(pct_ctx *ctx) {
+  std::lock_guard<std::recursive_mutex> lk(g_const_mu);
+  auto it = g_const_users.find(ctx);
+  if (it != g_const_users.end()) {
+    if (it->second) cudaEventDestroy(it->second);
+    g_const_users.erase(it);
+  }
+  for (auto &r : g_const)
+    if (r.second.uploader == ctx) r.second.uploader = nullptr;
 }
 
 int ensure_scratch(pct_ctx *ctx, size_t bytes) {
@@ -202,6 +255,7 @@ int pct_ctx_destroy(pct_ctx *ctx) {
   if (!ctx) return PCT_OK;
   cudaSetDevice(ctx->device);
   if (ctx->own_stream) cudaStreamSynchronize(ctx->own_stream);
+  const_bank_forget(ctx);
   if (ctx->scratch) cudaFree(ctx->scratch);
   if (ctx->staging) cudaFree(ctx->staging);
   if (ctx->dsmall) cudaFree(ctx->dsmall);

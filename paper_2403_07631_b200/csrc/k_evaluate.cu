@@ -621,6 +621,7 @@ constexpr int kBnbMinBlocks() {
 template <int R, int PR, int TH, int TW, int BNT = 256>
 int launch_split(pct_ctx *ctx, const float *ground, const float *ceiling, int S, int rows,
                  int cols, const float *kernel_w, int kside, float *cost, bool bnb) {
+  ConstBank cb(ctx);  // nested in launch_evaluate's scope: c_bw joins its constants
   const int64_t cells = (int64_t)rows * cols;
   const int wpr = (cols + 31) / 32;
   const int64_t words = (int64_t)rows * wpr;  // gentle bitmap words per slice
@@ -708,8 +709,7 @@ int launch_split(pct_ctx *ctx, const float *ground, const float *ceiling, int S,
     if (items > INT32_MAX) return fail(ctx, PCT_E_INVALID, "grid too large");
     if constexpr (R == 4 || R == 8) {
      if (bnb) {
-      PCT_CUDA(ctx, cudaMemcpyToSymbolAsync(c_bw, pin_upload(ctx, bw.data(), bw.size() * sizeof(float)), bw.size() * sizeof(float), 0,
-                                            cudaMemcpyHostToDevice, ctx->stream));
+      PCT_CUDA(ctx, cb.set_symbol(c_bw, bw.data(), bw.size() * sizeof(float)));
       auto kb = resolve_inflate_bnb_kernel<R, PR, TH, TW, BNT, kBnbMinBlocks<R>()>;
       constexpr int bsmem = BnbGeom<R, PR, TH, TW>::SMEM;
       PCT_CUDA(ctx, cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, bsmem));
@@ -874,17 +874,16 @@ int launch_evaluate(pct_ctx *ctx, const float *ground, const float *ceiling, int
       return fail(ctx, PCT_E_INVALID, "inflation kernel side must be odd and <= 125");
     R = kside / 2;
   }
+  ConstBank cb(ctx);
   EvalConsts K = make_consts(p, r_g);
-  PCT_CUDA(ctx, cudaMemcpyToSymbolAsync(c_K, pin_upload(ctx, &K, sizeof(K)), sizeof(K), 0, cudaMemcpyHostToDevice, ctx->stream));
+  PCT_CUDA(ctx, cb.set_symbol(c_K, &K, sizeof(K)));
   float wsym[81];
   const bool sym = mode == kEvalFull && symmetric_kernel(kernel_w, kside, R, wsym);
   if (mode == kEvalFull) {
     if (sym)
-      PCT_CUDA(ctx, cudaMemcpyToSymbolAsync(c_wsym, pin_upload(ctx, wsym, sizeof(wsym)), sizeof(wsym), 0, cudaMemcpyHostToDevice,
-                                            ctx->stream));
+      PCT_CUDA(ctx, cb.set_symbol(c_wsym, wsym, sizeof(wsym)));
     else
-      PCT_CUDA(ctx, cudaMemcpyToSymbolAsync(c_wfull, kernel_w, sizeof(float) * kside * kside, 0,
-                                            cudaMemcpyHostToDevice, ctx->stream));
+      PCT_CUDA(ctx, cb.set_symbol(c_wfull, kernel_w, sizeof(float) * kside * kside));
   }
   if (sym && R == 4 && p.patch_radius == 3)  // r_g = 0.1 with the Table-I radii
     return launch_fast<4, 3>(ctx, ground, ceiling, S, rows, cols, kernel_w, kside, cost);
@@ -932,10 +931,10 @@ int launch_evaluate_batch(pct_ctx *ctx, int n_maps, float *const *ground, float 
         return rc;
     return PCT_OK;
   }
+  ConstBank cb(ctx);
   EvalConsts K = make_consts(p, r_g);
-  PCT_CUDA(ctx, cudaMemcpyToSymbolAsync(c_K, pin_upload(ctx, &K, sizeof(K)), sizeof(K), 0, cudaMemcpyHostToDevice, ctx->stream));
-  PCT_CUDA(ctx, cudaMemcpyToSymbolAsync(c_bw, pin_upload(ctx, bw.data(), bw.size() * sizeof(float)), bw.size() * sizeof(float), 0,
-                                        cudaMemcpyHostToDevice, ctx->stream));
+  PCT_CUDA(ctx, cb.set_symbol(c_K, &K, sizeof(K)));
+  PCT_CUDA(ctx, cb.set_symbol(c_bw, bw.data(), bw.size() * sizeof(float)));
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
     void *fn = nullptr;
@@ -1068,8 +1067,8 @@ int launch_inflate(pct_ctx *ctx, const float *in, int rows, int cols, const floa
   if (rows <= 0 || cols <= 0) return PCT_OK;
   if (kside <= 0 || (kside & 1) == 0 || kside * kside > kMaxTaps)
     return fail(ctx, PCT_E_INVALID, "inflation kernel side must be odd and <= 125");
-  PCT_CUDA(ctx, cudaMemcpyToSymbolAsync(c_wfull, kernel_w, sizeof(float) * kside * kside, 0,
-                                        cudaMemcpyHostToDevice, ctx->stream));
+  ConstBank cb(ctx);
+  PCT_CUDA(ctx, cb.set_symbol(c_wfull, kernel_w, sizeof(float) * kside * kside));
   int TH = 32, TW = 32;
   TileGeom G = make_geom(kside / 2, 0, TH, TW);
   while (G.smem > 200 * 1024 && (TH > 8 || TW > 8)) {

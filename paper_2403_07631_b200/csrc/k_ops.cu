@@ -83,7 +83,8 @@ int launch_slope(pct_ctx *ctx, const float *g, int rows, int cols, double r_g, d
   p.theta_p = 0.2;
   p.c_barrier = 50;
   EvalConsts K = make_consts(p, r_g);
-  PCT_CUDA(ctx, cudaMemcpyToSymbolAsync(c_Kops, &K, sizeof(K), 0, cudaMemcpyHostToDevice, ctx->stream));
+  ConstBank cb(ctx);
+  PCT_CUDA(ctx, cb.set_symbol(c_Kops, &K, sizeof(K)));
   const int64_t n = (int64_t)rows * cols;
   if (n == 0) return PCT_OK;
   slope_kernel<<<blocks(n), 256, 0, ctx->stream>>>(g, rows, cols, m_xy, m_grad, iso);
@@ -101,7 +102,8 @@ int launch_gentle_fraction(pct_ctx *ctx, const uint8_t *gentle, int rows, int co
 int launch_terrain_values(pct_ctx *ctx, const double *m_xy, const double *m_grad,
                           const double *p_s, int64_t n, const pct_trav_params &p, double *out) {
   EvalConsts K = make_consts(p, 1.0);
-  PCT_CUDA(ctx, cudaMemcpyToSymbolAsync(c_Kops, &K, sizeof(K), 0, cudaMemcpyHostToDevice, ctx->stream));
+  ConstBank cb(ctx);
+  PCT_CUDA(ctx, cb.set_symbol(c_Kops, &K, sizeof(K)));
   if (n == 0) return PCT_OK;
   terrain_values_kernel<<<blocks(n), 256, 0, ctx->stream>>>(m_xy, m_grad, p_s, n, p.theta_p, out);
   return check_launch(ctx, "terrain_values_kernel");
@@ -110,7 +112,8 @@ int launch_terrain_values(pct_ctx *ctx, const double *m_xy, const double *m_grad
 int launch_fuse(pct_ctx *ctx, const float *ci, const float *cg, const uint8_t *valid, int64_t n,
                 const pct_trav_params &p, float *out) {
   EvalConsts K = make_consts(p, 1.0);
-  PCT_CUDA(ctx, cudaMemcpyToSymbolAsync(c_Kops, &K, sizeof(K), 0, cudaMemcpyHostToDevice, ctx->stream));
+  ConstBank cb(ctx);
+  PCT_CUDA(ctx, cb.set_symbol(c_Kops, &K, sizeof(K)));
   if (n == 0) return PCT_OK;
   fuse_kernel<<<blocks(n), 256, 0, ctx->stream>>>(ci, cg, valid, n, out);
   return check_launch(ctx, "fuse_kernel");

@@ -140,8 +140,8 @@ extern "C" int pct_ceiling_inflate(pct_ctx *ctx, const float *ceiling, int32_t n
     while ((h + 1) * (h + 1) + di * di <= radius * radius) ++h;
     hw[di + radius] = h;
   }
-  PCT_CUDA(ctx, cudaMemcpyToSymbolAsync(c_half_width, hw, sizeof(int) * (2 * radius + 1), 0,
-                                        cudaMemcpyHostToDevice, ctx->stream));
+  ConstBank cb(ctx);
+  PCT_CUDA(ctx, cb.set_symbol(c_half_width, hw, sizeof(int) * (2 * radius + 1)));
   const int64_t cells = (int64_t)rows * cols;
   ceiling_flat_kernel<<<dim3((unsigned)((cells + 255) / 256), n_slices), 256, 0, ctx->stream>>>(
       ceiling, rows, cols, radius, flat);

@@ -74,6 +74,31 @@ const void *pin_upload(pct_ctx *ctx, const void *src, size_t n);
 // readback_async copies n bytes of device memory to pinned host memory hdst
 // (visible to the host after the stream synchronises)
 cudaError_t upload_async(pct_ctx *ctx, void *ddst, const void *src, size_t n);
+
+// __constant__ symbols (parameters, inflation weights) are shared by every
+// context on a device.  A ConstBank scope serialises their use: set() skips
+// the upload when the symbol already holds these bytes (waiting for the
+// upload that put them there), and before changing them waits for every
+// other context's last launch that read constants; the destructor records
+// this context's use after the launches made inside the scope.
+class ConstBank {
+ public:
+  explicit ConstBank(pct_ctx *ctx);
+  ~ConstBank();
+  ConstBank(const ConstBank &) = delete;
+  ConstBank &operator=(const ConstBank &) = delete;
+  cudaError_t set(void *symbol_addr, const void *src, size_t n);
+  template <class T>
+  cudaError_t set_symbol(const T &symbol, const void *src, size_t n) {
+    void *d = nullptr;
+    cudaError_t e = cudaGetSymbolAddress(&d, symbol);
+    return e == cudaSuccess ? set(d, src, n) : e;
+  }
+
+ private:
+  pct_ctx *ctx_;
+};
+void const_bank_forget(pct_ctx *ctx);  // context teardown
 cudaError_t readback_async(pct_ctx *ctx, void *hdst, const void *dsrc, size_t n);
 
 #define PCT_CUDA(ctx, call)                                  \

@@ -381,6 +381,44 @@ def test_stream_maps_matches_single_maps():
                                       getattr(b, attr).values.view(np.uint32))
 
 
+def test_concurrent_contexts_with_different_parameters():
+    """Contexts running at the same time with different TravParams / kernels
+    (the __constant__ banks are shared per device) each get their own
+    results."""
+    import threading
+    from paper_2403_07631_b200 import synth
+    from paper_2403_07631_b200.batch import BatchRunner, stream_maps
+    xyz = synth.generate(4, 80_000, 3000)
+    variants = [(pct.TravParams(), 0.1), (pct.TravParams(theta_b=0.9, d_inf=0.25), 0.1),
+                (pct.TravParams(c_barrier=30.0), 0.2)]
+
+    def want(params, r_g):
+        ev = pct.evaluate_tomogram(pct.build_tomogram(pct.PointCloud(xyz), 0.5, r_g), params)
+        return [s.cost.values.copy() for s in pct.simplify_tomogram(ev, c_barrier=params.c_barrier).slices]
+
+    expected = [want(p, r) for p, r in variants]
+    got = [[] for _ in variants]
+
+    def worker(i):
+        p, r = variants[i]
+        run = BatchRunner(0, workers=2)
+        for t in stream_maps([xyz] * 6, 0.5, r, p, runner=run, c_barrier=p.c_barrier):
+            got[i].append([s.cost.values.copy() for s in t.slices])
+        run.close()
+
+    ths = [threading.Thread(target=worker, args=(i,)) for i in range(len(variants))]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    for i in range(len(variants)):
+        assert len(got[i]) == 6
+        for res in got[i]:
+            assert len(res) == len(expected[i])
+            for a, b in zip(res, expected[i]):
+                assert np.array_equal(a.view(np.uint32), b.view(np.uint32)), i
+
+
 @pytest.mark.parametrize("name", ["ref_random_multilayer_s9", "ref_spiral_s3", "synth_cfg0",
                                   "synth_cfg1"])
 def test_lga_archives_byte_identical(golden, tmp_path, name):
