@@ -62,6 +62,48 @@ __device__ __forceinline__ uint32_t gentle_word(const uint32_t *__restrict__ bk,
   return sh ? __funnelshift_r(lo, hi, sh) : lo;  // bits past cols are 0 in the map
 }
 
+// Per-cell state of a terrain walk between slices, and one slice of it: the
+// terrain part runs only when the 5-point cross changed since the slice
+// below, the interval / fuse part only when the cross or the ceiling did.
+struct WalkState {
+  uint32_t xe = 0, xl = 0, xr = 0, xu = 0, xd = 0, xc = 0;  // previous slice's input bits
+  float tenc;  // terrain part: NaN = no ground, sign bit = foothold branch
+  float enc = 0.0f;
+  bool gentle = false;
+};
+
+__device__ __forceinline__ void walk_step(WalkState &st, int k, bool live, float e, float l,
+                                          float r, float u, float d, float c, float nanf_,
+                                          float cb32) {
+  const bool xch = k == 0 || f32_bits(e) != st.xe || f32_bits(l) != st.xl ||
+                   f32_bits(r) != st.xr || f32_bits(u) != st.xu || f32_bits(d) != st.xd;
+  if (xch && live) {
+    const FastCell t = fast_terrain(Cross{e, l, r, u, d}, c_K);
+    st.gentle = t.gentle;
+    if (!t.valid) {
+      st.tenc = nanf_;
+    } else if (t.isolated || t.m_xy > c_K.theta_b) {
+      st.tenc = cb32;
+    } else if (t.gentle) {
+      st.tenc = gentle_cost32(t.gx, t.gy, t.s, c_K);
+    } else {
+      const double q = div_const(t.m_xy, c_K.theta_b, c_K.inv_theta_b);
+      st.tenc = bits_f32(f32_bits((float)(c_K.alpha_b * (q * q))) | 0x80000000u);
+    }
+  }
+  if ((xch || f32_bits(c) != st.xc) && live) {
+    if (!finite32(st.tenc)) {
+      st.enc = cb32;  // no ground: barrier (fuse_costs :169)
+    } else {
+      const uint32_t tb = f32_bits(st.tenc);
+      st.enc = fuse_value(interval_value(e, c, c_K), bits_f32(tb & 0x7FFFFFFFu), c_K);
+      if (tb & 0x80000000u) st.enc = bits_f32(f32_bits(st.enc) | 0x80000000u);
+    }
+  }
+  st.xe = f32_bits(e); st.xl = f32_bits(l); st.xr = f32_bits(r); st.xu = f32_bits(u);
+  st.xd = f32_bits(d); st.xc = f32_bits(c);
+}
+
 // Terrain walk: one thread per cell (flat row-major index, so a warp is 32
 // consecutive cells) walks the slices bottom-up.  The float64 terrain
 // arithmetic runs only when the cell's 5-point cross changed since the slice
@@ -109,10 +151,8 @@ __device__ __forceinline__ void walk_body(const float *__restrict__ ground,
     if (s < S) fetch(pg + s * cells, pc + s * cells, s);
   const float *ng = pg + PF * cells, *nc = pc + PF * cells;
 
-  uint32_t xe = 0, xl = 0, xr = 0, xu = 0, xd = 0, xc = 0;  // previous slice's input bits
-  float tenc = nanf_;  // terrain part: NaN = no ground, sign bit = foothold branch
-  bool gentle = false;
-  float enc = 0.0f;
+  WalkState st;
+  st.tenc = nanf_;
   // change map: one byte per (slice, 8-row block, bitmap word) set when any
   // cell's encoded c_init or gentle flag differs from the slice below (the
   // resolve/inflate kernel skips tiles whose window saw no change)
@@ -137,33 +177,9 @@ __device__ __forceinline__ void walk_body(const float *__restrict__ ground,
         ng += cells;
         nc += cells;
       }
-      const bool xch = k == 0 || f32_bits(e) != xe || f32_bits(l) != xl || f32_bits(r) != xr ||
-                       f32_bits(u) != xu || f32_bits(d) != xd;
-      if (xch && live) {
-        const FastCell t = fast_terrain(Cross{e, l, r, u, d}, c_K);
-        gentle = t.gentle;
-        if (!t.valid) {
-          tenc = nanf_;
-        } else if (t.isolated || t.m_xy > c_K.theta_b) {
-          tenc = cb32;
-        } else if (t.gentle) {
-          tenc = gentle_cost32(t.gx, t.gy, t.s, c_K);
-        } else {
-          const double q = div_const(t.m_xy, c_K.theta_b, c_K.inv_theta_b);
-          tenc = bits_f32(f32_bits((float)(c_K.alpha_b * (q * q))) | 0x80000000u);
-        }
-      }
-      if ((xch || f32_bits(c) != xc) && live) {
-        if (!finite32(tenc)) {
-          enc = cb32;  // no ground: barrier (fuse_costs :169)
-        } else {
-          const uint32_t tb = f32_bits(tenc);
-          enc = fuse_value(interval_value(e, c, c_K), bits_f32(tb & 0x7FFFFFFFu), c_K);
-          if (tb & 0x80000000u) enc = bits_f32(f32_bits(enc) | 0x80000000u);
-        }
-      }
-      xe = f32_bits(e); xl = f32_bits(l); xr = f32_bits(r); xu = f32_bits(u); xd = f32_bits(d);
-      xc = f32_bits(c);
+      walk_step(st, k, live, e, l, r, u, d, c, nanf_, cb32);
+      const float enc = st.enc;
+      const bool gentle = st.gentle;
       if (live) *pe = enc;
       pe += L.sstride;
       const unsigned word = __ballot_sync(0xFFFFFFFFu, live && gentle);
