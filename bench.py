@@ -375,15 +375,20 @@ def run_b200(args):
             return {"total": [(e0, e1)], "bounds+build": [float(st[0])],
                     "evaluate": [float(st[1])], "simplify": [float(st[2])]}
         if args.mode == "sharded":
+            evs = {}
             with torch.cuda.stream(stream):
                 e0 = pipe.ev()
                 gen = sharded.band_pipeline(dmaps[0], d_s, r_g, pct.TravParams(), rank, world,
-                                            device=local)
+                                            device=local, events=evs)
                 res = sharded.run_torch(gen) if world > 1 else sharded.run_virtual([gen])[0]
                 e1 = pipe.ev()
             band_info.update(S=len(res.heights), R=res.rows, C=res.cols, keep=len(res.keep),
-                             nrows=res.nrows, res=res)
-            return {"total": [(e0, e1)]}
+                             nrows=res.nrows, res=res, cs_band=evs["cell_slices"])
+            ea, eb = evs["evaluate"]
+            # build = bounds .. evaluate start (incl. point exchange and halo
+            # exchange when sharded), simplify = evaluate end .. step end
+            return {"total": [(e0, e1)], "bounds+build": [(e0, ea)], "evaluate": [(ea, eb)],
+                    "simplify": [(eb, e1)]}
         out = {"bounds+build": [], "evaluate": [], "simplify": [], "total": []}
         for dm, m in zip(dmaps, maps):
             tot, ms = pipe.run_native(dm, len(m))
@@ -470,26 +475,29 @@ def run_b200(args):
     }
     if args.mode == "batch":
         line["maps_per_s"] = len(maps) * world * args.steps / (step_ms * 1e-3)
-    if args.mode != "sharded":
-        ev_ms = statistics.mean(per["evaluate"]) / len(maps)
-        n_map = n_local / len(maps)
-        achieved = 12.0 * cs / (ev_ms * 1e-3) / 1e9
-        traffic = None
-        prof = ROOT / "profiles" / "ncu_traffic.json"
-        if prof.exists():
-            try:
-                traffic = json.loads(prof.read_text()).get(f"cfg{args.config}", {}).get(
-                    "eval_dram_bytes")
-            except Exception:
-                traffic = None
-        line["algorithmic_bytes_per_map"] = 12 * n_map + 28 * cs
-        line["pipeline_gbs_per_gpu"] = (12 * n_map + 28 * cs) * len(maps) / (
-            step_ms / args.steps * 1e-3) / 1e9
-        line["roofline"] = {"kernel": "evaluate stage (terrain walk + resolve/inflate launches)", "bound": "hbm",
-                            "achieved": achieved, "peak": peak, "unit": "GB/s",
-                            "frac": achieved / peak, "traffic": traffic,
-                            "algorithmic": f"12 B per cell-slice x {cs} cell-slices per launch",
-                            "peak_source": peak_src}
+    ev_ms = statistics.mean(per["evaluate"]) / len(maps)
+    n_map = n_local / len(maps)
+    # sharded: this rank's band (own rows + halo rows it evaluates)
+    cs_eval = info["cs_band"] if args.mode == "sharded" else cs
+    achieved = 12.0 * cs_eval / (ev_ms * 1e-3) / 1e9
+    traffic = None
+    prof = ROOT / "profiles" / "ncu_traffic.json"
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get(f"cfg{args.config}", {}).get(
+                "eval_dram_bytes")
+        except Exception:
+            traffic = None
+    if args.mode == "sharded" and world > 1:
+        traffic = None  # the recorded capture is of the one-GPU band
+    line["algorithmic_bytes_per_map"] = 12 * n_map + 28 * cs
+    line["pipeline_gbs_per_gpu"] = (12 * n_map + 28 * cs_eval) * len(maps) / (
+        step_ms / args.steps * 1e-3) / 1e9
+    line["roofline"] = {"kernel": "evaluate stage (terrain walk + resolve/inflate launches)", "bound": "hbm",
+                        "achieved": achieved, "peak": peak, "unit": "GB/s",
+                        "frac": achieved / peak, "traffic": traffic,
+                        "algorithmic": f"12 B per cell-slice x {cs_eval} cell-slices per launch",
+                        "peak_source": peak_src}
 
     # ---- e2e through the public API with host buffers (replica mode)
     if args.mode == "replica" and not args.no_e2e and not args.profile:

@@ -91,6 +91,7 @@ cudaError_t small_copy(pct_ctx *ctx, void *dst, const void *src, size_t n) {
       static_cast<uint32_t *>(dst), static_cast<const uint32_t *>(src), words,
       static_cast<unsigned char *>(dst) + 4 * words,
       static_cast<const unsigned char *>(src) + 4 * words, ntail);
+  ctx->launches++;
   return cudaGetLastError();
 }
 }  // namespace

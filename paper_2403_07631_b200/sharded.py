@@ -151,11 +151,14 @@ def _ptr(t, offset_elems=0):
 
 
 def band_pipeline(xyz, d_s, r_g, params, rank, size, *, device=None, eps_e=1e-6,
-                  c_barrier=50.0, max_grid_side=16384):
+                  c_barrier=50.0, max_grid_side=16384, events=None):
     """Generator: the row-band pipeline of one rank.
 
     xyz: this rank's points, a CUDA torch tensor (n, 3) float32/float64.
-    Yields collective requests (tuples) and finally returns a BandResult."""
+    Yields collective requests (tuples) and finally returns a BandResult.
+    ``events`` (a dict) receives CUDA events recorded on the current stream
+    around the evaluate launch ("evaluate" -> (start, end)) and its extent
+    ("cell_slices")."""
     import torch
 
     ctx = _lib.context(device if device is not None else xyz.device.index)
@@ -245,9 +248,17 @@ def band_pipeline(xyz, d_s, r_g, params, rank, size, *, device=None, eps_e=1e-6,
     # 5. evaluate the extended band (own rows are exact)
     cost = torch.empty_like(g)
     pc = _lib.trav_params_c(params, r_g)
+    if events is not None:
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev0.record()
     ctx.check(lib.pct_evaluate(h, g.data_ptr(), c.data_ptr(), S, ext_rows, cols, float(r_g),
                                C.byref(pc), w.ctypes.data, w.shape[0], cost.data_ptr()),
               "evaluate")
+    if events is not None:
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev1.record()
+        events["evaluate"] = (ev0, ev1)
+        events["cell_slices"] = S * ext_rows * cols
 
     # 6. simplify: reduced any() tables, shared sweep
     cells = nrows * cols
