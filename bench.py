@@ -551,12 +551,16 @@ def run_b200(args):
             t = torch.tensor([st_s], device=f"cuda:{local}", dtype=torch.float64)
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             st_s = float(t.item())
-        line["e2e"] = {"value": total_pts / (st_s * 1e6), "unit": "Mpts/s",
-                       "ms_per_step": 1e3 * st_s, "h2d_bytes_per_step": 12 * len(xyz),
-                       "d2h_bytes_per_step": d2h_s // args.steps,
-                       "path": "stream_maps(pinned f32 clouds, 2 in flight) -> simplified "
-                               "tomograms with every surviving layer in host memory",
-                       "sequential": seq}
+        streamed = {"value": total_pts / (st_s * 1e6), "unit": "Mpts/s", "ms_per_step": 1e3 * st_s,
+                    "path": "stream_maps(pinned f32 clouds, 2 in flight) -> simplified "
+                            "tomograms with every surviving layer in host memory"}
+        # the faster of the two public entry points is the e2e number (small
+        # maps: the one-at-a-time path; large: the streamed one), the other
+        # is reported beside it
+        best, other = (streamed, seq) if streamed["value"] >= seq["value"] else (seq, streamed)
+        line["e2e"] = dict(best, h2d_bytes_per_step=12 * len(xyz),
+                           d2h_bytes_per_step=d2h_s // args.steps,
+                           alternative=other)
 
     # ---- CPU baseline (rank 0, N=1 only): the reference algorithm on host cores
     if rank == 0 and world == 1 and not args.no_cpu and not args.profile:
