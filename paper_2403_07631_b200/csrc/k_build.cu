@@ -207,7 +207,7 @@ __global__ void __launch_bounds__(256) scatter_kernel(const T *__restrict__ xyz,
 constexpr int kTBH = 8, kTBW = 32;  // tile rows x columns
 constexpr int kTB2 = kTBH * kTBW;    // cells per tile (8-bit local index)
 constexpr int kTileMaxS = 96;     // 2 x S x 256 x 4 B of shared memory
-constexpr int kTileNT = 256;
+constexpr int kTileNT = 2 * kTB2;  // reduce: two threads per cell (ground / ceiling side)
 
 // cell and bin of one point (tomogram.py:147-157): false when outside the band
 template <bool BIN = true>
@@ -317,45 +317,67 @@ __global__ void __launch_bounds__(256) tile_pass_kernel(const T *__restrict__ xy
   }
 }
 
-// exclusive prefix sum of the n (padded) tile counts in one block, 1024
-// tiles per step (coalesced); offs[n] = total.  The cursors (padded) are the
-// copy T3 advances.
-__global__ void __launch_bounds__(1024) tile_offsets_kernel(const unsigned *__restrict__ cnt,
-                                                            int n, unsigned *__restrict__ offs,
-                                                            unsigned *__restrict__ cursor) {
-  __shared__ unsigned wsum[32];
+// exclusive prefix sum of the n (padded) tile counts, reduce-then-scan over
+// blocks of 1024 tiles (the counters sit one per 128-byte line: a one-block
+// scan was load-latency bound, 140 us for cfg3's 62.6k tiles): T2a sums each
+// block's counts, T2b adds the sums of the blocks before it and scans its
+// own; offs[n] = total.  The cursors (padded) are the copy T3 advances.
+__device__ __forceinline__ unsigned block_incl_scan(unsigned x, unsigned *wsum, unsigned &total) {
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  unsigned carry = 0;
-  for (int c0 = 0; c0 < n; c0 += 1024) {
-    const int i = c0 + t;
-    const unsigned v = i < n ? cnt[(int64_t)i * kCtrPad] : 0u;
-    unsigned x = v;  // inclusive warp scan
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const unsigned y = __shfl_up_sync(0xFFFFFFFFu, x, d);
+    if (lane >= d) x += y;
+  }
+  if (lane == 31) wsum[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    unsigned w = wsum[lane];
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
-      const unsigned y = __shfl_up_sync(0xFFFFFFFFu, x, d);
-      if (lane >= d) x += y;
+      const unsigned y = __shfl_up_sync(0xFFFFFFFFu, w, d);
+      if (lane >= d) w += y;
     }
-    if (lane == 31) wsum[warp] = x;
-    __syncthreads();
-    if (warp == 0) {
-      unsigned w = wsum[lane];
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const unsigned y = __shfl_up_sync(0xFFFFFFFFu, w, d);
-        if (lane >= d) w += y;
-      }
-      wsum[lane] = w;  // inclusive over warps
-    }
-    __syncthreads();
-    const unsigned excl = carry + (warp ? wsum[warp - 1] : 0u) + x - v;
-    if (i < n) {
-      offs[i] = excl;
-      cursor[(int64_t)i * kCtrPad] = excl;
-    }
-    carry += wsum[31];
-    __syncthreads();
+    wsum[lane] = w;  // inclusive over warps
   }
-  if (t == 0) offs[n] = carry;
+  __syncthreads();
+  total = wsum[31];
+  return (warp ? wsum[warp - 1] : 0u) + x;
+}
+
+__global__ void __launch_bounds__(1024) tile_sums_kernel(const unsigned *__restrict__ cnt, int n,
+                                                         unsigned *__restrict__ bsum) {
+  __shared__ unsigned wsum[32];
+  const int i = blockIdx.x * 1024 + threadIdx.x;
+  unsigned total;
+  block_incl_scan(i < n ? __ldcg(cnt + (int64_t)i * kCtrPad) : 0u, wsum, total);
+  if (threadIdx.x == 0) bsum[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(1024) tile_offsets_kernel(const unsigned *__restrict__ cnt,
+                                                            int n, const unsigned *__restrict__ bsum,
+                                                            unsigned *__restrict__ offs,
+                                                            unsigned *__restrict__ cursor) {
+  __shared__ unsigned wsum[32];
+  __shared__ unsigned base;
+  const int t = threadIdx.x;
+  if (t < 32) {  // sum of the blocks before this one
+    unsigned s = 0;
+    for (int b = t; b < (int)blockIdx.x; b += 32) s += bsum[b];
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, d);
+    if (t == 0) base = s;
+  }
+  const int i = blockIdx.x * 1024 + t;
+  const unsigned v = i < n ? __ldcg(cnt + (int64_t)i * kCtrPad) : 0u;
+  unsigned total;
+  const unsigned incl = block_incl_scan(v, wsum, total);  // its barriers also publish `base`
+  const unsigned excl = base + incl - v;
+  if (i < n) {
+    offs[i] = excl;
+    cursor[(int64_t)i * kCtrPad] = excl;
+  }
+  if (blockIdx.x == gridDim.x - 1 && t == 0) offs[n] = base + total;
 }
 
 __global__ void __launch_bounds__(kTileNT) tile_reduce_kernel(
@@ -381,21 +403,26 @@ __global__ void __launch_bounds__(kTileNT) tile_reduce_kernel(
     if (b > 0) atomicMin(ck + (b - 1) * kTB2 + local, key);
   }
   __syncthreads();
+  // threads 0..255 walk a cell's ground bins up, 256..511 its ceiling bins down
+  const int c = t & (kTB2 - 1);
   const int ti = tile / ntx, tj = tile - ti * ntx;
-  const int i = ti * kTBH + t / kTBW, j = tj * kTBW + t % kTBW;
+  const int i = ti * kTBH + c / kTBW, j = tj * kTBW + c % kTBW;
   if (i >= rows || j >= cols) return;
   const int64_t cell = (int64_t)i * cols + j;
-  uint32_t run = kKeyEmptyMax;
-  for (int k = 0; k < S; ++k) {
-    const uint32_t v = gk[k * kTB2 + t];
-    run = v > run ? v : run;
-    __stcs(ground + (int64_t)k * out_stride + cell, decode_ground(run));
-  }
-  run = kKeyEmptyMin;
-  for (int k = S - 1; k >= 0; --k) {
-    const uint32_t v = ck[k * kTB2 + t];
-    run = v < run ? v : run;
-    __stcs(ceiling + (int64_t)k * out_stride + cell, decode_ceiling(run));
+  if (t < kTB2) {
+    uint32_t run = kKeyEmptyMax;
+    for (int k = 0; k < S; ++k) {
+      const uint32_t v = gk[k * kTB2 + c];
+      run = v > run ? v : run;
+      __stcs(ground + (int64_t)k * out_stride + cell, decode_ground(run));
+    }
+  } else {
+    uint32_t run = kKeyEmptyMin;
+    for (int k = S - 1; k >= 0; --k) {
+      const uint32_t v = ck[k * kTB2 + c];
+      run = v < run ? v : run;
+      __stcs(ceiling + (int64_t)k * out_stride + cell, decode_ceiling(run));
+    }
   }
 }
 
@@ -708,14 +735,17 @@ int launch_build(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, const pct_
     const int ntx = (fr.cols + kTBW - 1) / kTBW, nty = (nrows + kTBH - 1) / kTBH;
     const int64_t ntiles = (int64_t)ntx * nty;
     const size_t cbytes = ((size_t)(ntiles + 1) * 4 * kCtrPad + 255) & ~(size_t)255;
-    if (int rc = ensure_scratch(ctx, hbytes + 256 + 3 * cbytes + (size_t)n * 8)) return rc;
+    const size_t sbytes = ((size_t)((ntiles + 1023) / 1024) * 4 + 255) & ~(size_t)255;
+    if (int rc = ensure_scratch(ctx, hbytes + 256 + 3 * cbytes + sbytes + (size_t)n * 8)) return rc;
     char *b0 = static_cast<char *>(ctx->scratch);
     double *hd = reinterpret_cast<double *>(b0);
     unsigned long long *outs = reinterpret_cast<unsigned long long *>(b0 + hbytes);
     unsigned *cnt = reinterpret_cast<unsigned *>(b0 + hbytes + 256);
     unsigned *offs = reinterpret_cast<unsigned *>(b0 + hbytes + 256 + cbytes);
     unsigned *cur = reinterpret_cast<unsigned *>(b0 + hbytes + 256 + 2 * cbytes);
-    unsigned long long *recs = reinterpret_cast<unsigned long long *>(b0 + hbytes + 256 + 3 * cbytes);
+    unsigned *bsum = reinterpret_cast<unsigned *>(b0 + hbytes + 256 + 3 * cbytes);
+    unsigned long long *recs =
+        reinterpret_cast<unsigned long long *>(b0 + hbytes + 256 + 3 * cbytes + sbytes);
     PCT_CUDA(ctx, upload_async(ctx, hd, heights_host, (size_t)S * sizeof(double)));
     PCT_CUDA(ctx, cudaMemsetAsync(outs, 0, 8, ctx->stream));
     PCT_CUDA(ctx, cudaMemsetAsync(cnt, 0, (size_t)ntiles * 4 * kCtrPad, ctx->stream));
@@ -730,7 +760,10 @@ int launch_build(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, const pct_
       tile_pass_kernel<double, false><<<g, 256, hsm, ctx->stream>>>(
           static_cast<const double *>(xyz), n, a, ntx, cnt, nullptr, outs);
     if (int rc = check_launch(ctx, "tile_count_kernel")) return rc;
-    tile_offsets_kernel<<<1, 1024, 0, ctx->stream>>>(cnt, (int)ntiles, offs, cur);
+    const unsigned nb = (unsigned)((ntiles + 1023) / 1024);
+    tile_sums_kernel<<<nb, 1024, 0, ctx->stream>>>(cnt, (int)ntiles, bsum);
+    if (int rc = check_launch(ctx, "tile_sums_kernel")) return rc;
+    tile_offsets_kernel<<<nb, 1024, 0, ctx->stream>>>(cnt, (int)ntiles, bsum, offs, cur);
     if (int rc = check_launch(ctx, "tile_offsets_kernel")) return rc;
     if (dtype == PCT_F32)
       tile_pass_kernel<float, true><<<g, 256, hsm, ctx->stream>>>(
