@@ -140,7 +140,13 @@ struct BinArgs {
   int64_t cells;          // band_rows * cols
   int rows, cols, S;      // rows = band rows; the frame is global
   int row0;               // first global row of the band
+  int derive;             // heights[k] == z0 + d_s (k + 1): staged from the formula, not loaded
 };
+
+// the plane heights of pct_frame_compute, evaluated the same way (no contraction)
+__device__ __forceinline__ double plane_height(const BinArgs &a, int k) {
+  return __dadd_rn(a.z0, __dmul_rn(a.d_s, (double)k + 1.0));
+}
 
 template <typename T>
 __device__ __forceinline__ void scatter_body(const T *__restrict__ xyz, int64_t n, const BinArgs &a,
@@ -152,7 +158,8 @@ __device__ __forceinline__ void scatter_body(const T *__restrict__ xyz, int64_t 
   extern __shared__ double hsm[];
   const bool staged = a.S <= kMaxStagedHeights;
   if (staged)
-    for (int k = threadIdx.x; k < a.S; k += blockDim.x) hsm[k] = a.heights[k];
+    for (int k = threadIdx.x; k < a.S; k += blockDim.x)
+      hsm[k] = a.derive ? plane_height(a, k) : a.heights[k];
   __syncthreads();
   const double *hts = staged ? hsm : a.heights;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -165,7 +172,7 @@ __device__ __forceinline__ void scatter_body(const T *__restrict__ xyz, int64_t 
     const double fi = floor(div_const(y - a.y0, a.r_g, a.inv_rg) + 0.5) - (double)a.row0;
     const double fj = floor(div_const(x - a.x0, a.r_g, a.inv_rg) + 0.5);
     if (!(fi >= 0.0 && fi < (double)a.rows && fj >= 0.0 && fj < (double)a.cols)) {
-      atomicAdd(outside, 1ull);
+      if (outside) atomicAdd(outside, 1ull);
       continue;
     }
     const int64_t cell = (int64_t)fi * a.cols + (int64_t)fj;
@@ -246,7 +253,8 @@ __global__ void __launch_bounds__(256) tile_pass_kernel(const T *__restrict__ xy
   __shared__ unsigned h_cnt[kHash];
   const bool staged = a.S <= kMaxStagedHeights;
   if (staged)
-    for (int k = threadIdx.x; k < a.S; k += blockDim.x) hsm[k] = a.heights[k];
+    for (int k = threadIdx.x; k < a.S; k += blockDim.x)
+      hsm[k] = a.derive ? plane_height(a, k) : a.heights[k];
   for (int h = threadIdx.x; h < kHash; h += blockDim.x) {
     h_tile[h] = -1;
     h_cnt[h] = 0u;
@@ -272,7 +280,7 @@ __global__ void __launch_bounds__(256) tile_pass_kernel(const T *__restrict__ xy
         const double z = SCATTER ? (double)__ldg(xyz + 3 * p + 2) : 0.0;
         in = point_cell_bin<SCATTER>(x, y, z, a, hts, fi[u], fj[u], bin[u]);
         z32[u] = __double2float_rn(z);
-        if (!in && !SCATTER) atomicAdd(outside, 1ull);
+        if (!in && !SCATTER && outside) atomicAdd(outside, 1ull);
       }
       if (in) {
         const int tile = (fi[u] / kTBH) * ntx + fj[u] / kTBW;
@@ -728,6 +736,15 @@ int launch_build(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, const pct_
   // tiled 7.0 ms; cfg1 141 vs 211 us and cfg2 ~660 vs 781 us the other way,
   // profiles/r01d_build_variants.txt).  PCT_BUILD=atomic / tiled forces one.
   const bool big_keys = 2.0 * (double)S * (double)cells * 4.0 > 1.5e9;
+  // heights that follow the frame formula are derived in the kernels (no
+  // upload); points outside a whole-grid frame cannot occur, so the
+  // diagnostic outside-counter is only kept for bands
+  bool derive = S <= kMaxStagedHeights;
+  for (int k = 0; derive && k < S; ++k) {
+    volatile double t = fr.d_s * ((double)k + 1.0);
+    derive = heights_host[k] == fr.z_min + t;
+  }
+  const bool whole = row0 == 0 && nrows == fr.rows;
   const bool tiled = bmode ? bmode[0] == 't' : big_keys;
   if (S <= kTileMaxS && n > 0 && n < (int64_t)UINT32_MAX && tiled) {
     // tile-partitioned build: scratch = heights | outside | counts | offsets |
@@ -746,11 +763,12 @@ int launch_build(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, const pct_
     unsigned *bsum = reinterpret_cast<unsigned *>(b0 + hbytes + 256 + 3 * cbytes);
     unsigned long long *recs =
         reinterpret_cast<unsigned long long *>(b0 + hbytes + 256 + 3 * cbytes + sbytes);
-    PCT_CUDA(ctx, upload_async(ctx, hd, heights_host, (size_t)S * sizeof(double)));
-    PCT_CUDA(ctx, cudaMemsetAsync(outs, 0, 8, ctx->stream));
+    if (!derive) PCT_CUDA(ctx, upload_async(ctx, hd, heights_host, (size_t)S * sizeof(double)));
+    if (whole) outs = nullptr;
+    else PCT_CUDA(ctx, cudaMemsetAsync(outs, 0, 8, ctx->stream));
     PCT_CUDA(ctx, cudaMemsetAsync(cnt, 0, (size_t)ntiles * 4 * kCtrPad, ctx->stream));
     BinArgs a{fr.origin_x, fr.origin_y, fr.z_min, fr.r_g, fr.d_s, 1.0 / fr.r_g, 1.0 / fr.d_s,
-              hd, cells, nrows, fr.cols, S, row0};
+              hd, cells, nrows, fr.cols, S, row0, derive ? 1 : 0};
     const size_t hsm = S <= kMaxStagedHeights ? (size_t)S * sizeof(double) : 0;
     const int g = grid_for(ctx, n, 256, 16);
     if (dtype == PCT_F32)
@@ -799,15 +817,16 @@ int launch_build(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, const pct_
   char *base = static_cast<char *>(ctx->scratch);
   double *hdev = reinterpret_cast<double *>(base);
   unsigned long long *outside = reinterpret_cast<unsigned long long *>(base + hbytes);
-  PCT_CUDA(ctx, upload_async(ctx, hdev, heights_host, (size_t)S * sizeof(double)));
+  if (!derive) PCT_CUDA(ctx, upload_async(ctx, hdev, heights_host, (size_t)S * sizeof(double)));
   if (ctx->keys_tag[0] != S || ctx->keys_tag[1] != cells) {
     PCT_CUDA(ctx, cudaMemsetAsync(gkey, 0x00, plane * S, ctx->stream));
     PCT_CUDA(ctx, cudaMemsetAsync(ckey, 0xFF, plane * S, ctx->stream));
   }
   ctx->keys_tag[0] = -1;  // dirty until the scan below is launched
-  PCT_CUDA(ctx, cudaMemsetAsync(outside, 0, 8, ctx->stream));
+  if (whole) outside = nullptr;
+  else PCT_CUDA(ctx, cudaMemsetAsync(outside, 0, 8, ctx->stream));
   BinArgs a{fr.origin_x, fr.origin_y, fr.z_min, fr.r_g, fr.d_s, 1.0 / fr.r_g, 1.0 / fr.d_s,
-            hdev, cells, nrows, fr.cols, S, row0};
+            hdev, cells, nrows, fr.cols, S, row0, derive ? 1 : 0};
   const size_t hsm_bytes = S <= kMaxStagedHeights ? (size_t)S * sizeof(double) : 0;
   if (n > 0) {
     if (dtype == PCT_F32)
