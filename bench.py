@@ -194,6 +194,22 @@ def workload(args, rank, world):
     return cfg, [np.ascontiguousarray(xyz[rank::world])], f"seed {cfg['seed']}, 1/{world} points"
 
 
+def make_config(args, cfg, world, total_pts, R, Cc, S, keep, desc, maps_per_rank, step):
+    """The `config` object of a bench line (both arms print the same one)."""
+    r_g, d_s = cfg["r_g"], cfg["d_s"]
+    return {"workload": f"cfg{args.config} {cfg['name']} ({args.mode}): "
+                        f"{int(total_pts)} float32 pts, grid {R}x{Cc}, {S} slices, "
+                        f"r_g {r_g}, d_s {d_s}",
+            "mode": args.mode, "points_total": int(total_pts), "data_desc": desc,
+            "rows": R, "cols": Cc, "slices": S, "slices_kept": keep,
+            "r_g": r_g, "d_s": d_s, "step": step,
+            "l2": f"flushed between steps ({L2_FLUSH_BYTES >> 20} MiB write), "
+                  "flush excluded from step time",
+            "parallelism": {"replica": f"{world} independent maps (one per GPU)",
+                            "sharded": f"1 map in {world} row bands (NCCL)",
+                            "batch": f"{maps_per_rank} maps per GPU x {world}"}[args.mode]}
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -213,17 +229,28 @@ def run_reference(args):
         for xyz in maps:
             cpu_pipeline(xyz, cfg, threads)
     times, stages = [], []
+    kept = 0
     for _ in range(args.steps):
         t = 0.0
         st = {"build": 0.0, "evaluate": 0.0, "simplify": 0.0}
         for xyz in maps:
-            dt, s, _ = cpu_pipeline(xyz, cfg, threads)
+            dt, s, kept = cpu_pipeline(xyz, cfg, threads)
             t += dt
             for k in st:
                 st[k] += s[k]
         times.append(t)
         stages.append(st)
     pts = sum(len(x) for x in maps)
+    import oracle
+    fr = oracle.frame(*oracle.bounds(maps[-1]), cfg["d_s"], cfg["r_g"])
+    # the B200 arm's config for the same workload (one map per step here; a
+    # bounded sample of it when the map is too large for the host, noted)
+    ref_config = make_config(args, cfg, 1, len(maps[-1]), fr["rows"], fr["cols"],
+                             len(fr["heights"]), kept, f"seed {cfg['seed']}", len(maps),
+                             "bounds+build+evaluate+simplify, host-resident points (CPU)")
+    ref_config["l2"] = "not applicable (host caches)"
+    if desc != "full map":
+        ref_config["cpu_sample"] = desc
     ms = 1e3 * statistics.mean(times)
     mpts = pts / (ms * 1e3)
     line = {
@@ -231,8 +258,7 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": f"cfg{args.config} {cfg['name']}", "n_points": pts,
-                   "r_g": cfg["r_g"], "d_s": cfg["d_s"], "sample": desc},
+        "config": ref_config,
         "stages_ms": {k: 1e3 * statistics.mean(s[k] for s in stages) for k in stages[0]},
         "cpu_baseline": {"value": mpts, "unit": "Mpts/s", "cores": threads, "kind": "port",
                          "sample": f"{desc}; build+evaluate+simplify per step; {cpu_model()}"},
@@ -456,18 +482,8 @@ def run_b200(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "strong" if args.mode != "replica" else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"cfg{args.config} {cfg['name']} ({args.mode}): "
-                               f"{int(total_pts)} float32 pts, grid {R}x{Cc}, {S} slices, "
-                               f"r_g {r_g}, d_s {d_s}",
-                   "mode": args.mode, "points_total": int(total_pts), "data_desc": desc,
-                   "rows": R, "cols": Cc, "slices": S, "slices_kept": info["keep"],
-                   "r_g": r_g, "d_s": d_s,
-                   "step": "bounds+build+evaluate+simplify, device-resident points",
-                   "l2": f"flushed between steps ({L2_FLUSH_BYTES >> 20} MiB write), "
-                         "flush excluded from step time",
-                   "parallelism": {"replica": f"{world} independent maps (one per GPU)",
-                                   "sharded": f"1 map in {world} row bands (NCCL)",
-                                   "batch": f"{len(maps)} maps per GPU x {world}"}[args.mode]},
+        "config": make_config(args, cfg, world, total_pts, R, Cc, S, info["keep"], desc,
+                              len(maps), "bounds+build+evaluate+simplify, device-resident points"),
         "stages_ms": {k: statistics.mean(v) for k, v in per.items()},
         "wall_s_timed_region": t_wall,
         "gpu_launches": launches,
