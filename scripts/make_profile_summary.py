@@ -40,9 +40,13 @@ if rep.exists():
     by = collections.OrderedDict()
     for r in lines[1:]:
         by.setdefault(r[ii2], []).append(r)
+    seen = collections.Counter()
     for rid, rs in by.items():
         kname = rs[0][ki2]
         short = re.sub(r"[^a-z_]", "", kname.split("(")[0].split("::")[-1].split("<")[0])
+        seen[short] += 1
+        if seen[short] > 1:  # another instantiation of the same kernel
+            short = f"{short}{seen[short]}"
         body = [f"ncu --set full --clock-control none --import-source on, report {rep.name}, launch id {rid}",
                 f"kernel: {kname}", ""]
         for r in rs:
