@@ -159,6 +159,43 @@ def test_random_scenes_vs_oracle(seed):
     assert [s.plane_height for s in simp.slices] == [float(ref["heights"][k]) for k in keep]
 
 
+@pytest.mark.parametrize("shape", ["tall", "strip", "column", "wide"])
+def test_extreme_shapes_vs_oracle(monkeypatch, shape):
+    """Shapes at the kernels' limits: more slices than a bnb work item's
+    64-slice skip mask and the tiled build's shared-memory bins (tall), a
+    two-column strip (one partial bitmap word per row), a single cell column
+    with many slices, and a one-row-of-tiles map wider than the
+    32-column tiles; built both ways."""
+    rng = np.random.default_rng(11)
+    if shape == "tall":  # ~140 slices over a small footprint, stacked floors
+        n = 30_000
+        xyz = np.column_stack([rng.uniform(0, 3, n), rng.uniform(0, 2, n),
+                               np.floor(rng.uniform(0, 70, n)) + rng.normal(0, 0.02, n)])
+    elif shape == "strip":
+        n = 20_000
+        xyz = np.column_stack([rng.uniform(0, 0.1, n), rng.uniform(0, 50, n),
+                               rng.uniform(0, 3, n)])
+    elif shape == "column":
+        n = 5_000
+        xyz = np.column_stack([rng.uniform(0, 0.04, n), rng.uniform(0, 0.04, n),
+                               rng.uniform(0, 40, n)])
+    else:
+        n = 40_000
+        xyz = np.column_stack([rng.uniform(0, 80, n), rng.uniform(0, 0.5, n),
+                               rng.uniform(0, 2, n)])
+    d_s, r_g = 0.5, 0.1
+    ref = oracle.build(xyz, d_s, r_g)
+    cost = oracle.evaluate(ref["ground"], ref["ceiling"], r_g, TABLE_PARAMS)
+    keep = oracle.simplify(ref["ground"], cost)
+    for build in ("atomic", "tiled"):
+        monkeypatch.setenv("PCT_BUILD", build)
+        tom, ev, simp = _run(xyz, d_s, r_g)
+        _assert_layers_equal(ev.ground_stack(), ref["ground"], f"ground {build}")
+        _assert_layers_equal(ev.ceiling_stack(), ref["ceiling"], f"ceiling {build}")
+        _assert_layers_equal(ev.cost_stack(), cost, f"cost {build}")
+        assert [s.plane_height for s in simp.slices] == [float(ref["heights"][k]) for k in keep]
+
+
 def test_point_order_independence(golden):
     case = golden["cases"]["synth_cfg0"]
     xyz = case_input("synth_cfg0", case)
