@@ -396,6 +396,31 @@ def test_batch_runner_matches_single_maps():
                                       getattr(b, attr).values.view(np.uint32))
 
 
+def test_batch_of_heterogeneous_maps():
+    """One batched native call over maps of very different extents and slice
+    counts (a tiny map, a 100+-slice tower, a wide strip, a config-0 map):
+    each equals its own per-map drop-in result."""
+    from paper_2403_07631_b200 import synth
+    from paper_2403_07631_b200.batch import evaluate_maps
+    rng = np.random.default_rng(5)
+    tower = np.column_stack([rng.uniform(0, 2, 20_000), rng.uniform(0, 2, 20_000),
+                             np.floor(rng.uniform(0, 55, 20_000)) + rng.normal(0, 0.02, 20_000)])
+    strip = np.column_stack([rng.uniform(0, 60, 30_000), rng.uniform(0, 0.3, 30_000),
+                             rng.uniform(0, 2, 30_000)])
+    tiny = np.array([[0.0, 0.0, 0.0], [0.05, 0.02, 0.6], [0.1, 0.1, 1.3]])
+    clouds = [c.astype(np.float32) for c in (tiny, tower, strip, synth.generate(0, 100_000, 9))]
+    outs = evaluate_maps(clouds, 0.5, 0.1, pct.TravParams(), workers=2)
+    for xyz, got in zip(clouds, outs):
+        ev = pct.evaluate_tomogram(pct.build_tomogram(pct.PointCloud(xyz), 0.5, 0.1),
+                                   pct.TravParams())
+        want = pct.simplify_tomogram(ev)
+        assert [s.plane_height for s in got.slices] == [s.plane_height for s in want.slices]
+        for a, b in zip(got.slices, want.slices):
+            for attr in ("ground", "ceiling", "cost"):
+                assert np.array_equal(getattr(a, attr).values.view(np.uint32),
+                                      getattr(b, attr).values.view(np.uint32))
+
+
 def test_stream_maps_matches_single_maps():
     """stream_maps (maps in flight on two contexts, layers read back in the
     worker) yields, in order, the per-map drop-in results."""
