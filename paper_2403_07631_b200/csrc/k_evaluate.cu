@@ -370,6 +370,15 @@ __global__ void __launch_bounds__(NT, MINB) eval_fast_kernel(const float *__rest
   }
 }
 
+// slices of DRAM -> L2 prefetch ahead of the terrain walk's register loads
+// (prefetch.global.L2 holds no registers; the walk keeps one slice in
+// registers): 4 measured best (cfg1 walk 96 -> 90 us, cfg2 524 -> 481 us;
+// 2 and 8 close); PCT_WALK_L2PF=0 turns it off
+int walk_l2_ahead_host() {
+  const char *e = getenv("PCT_WALK_L2PF");
+  return e ? atoi(e) : 4;
+}
+
 #include "k_eval_incr.cuh"
 #include "k_eval_split.cuh"
 #include "k_eval_bnb.cuh"
@@ -673,14 +682,15 @@ int launch_split(pct_ctx *ctx, const float *ground, const float *ceiling, int S,
   const int64_t walk_threads = (int64_t)rows * wpr * 32;
   const unsigned g1 = (unsigned)((walk_threads + kWalkNT - 1) / kWalkNT);
   const char *pf = getenv("PCT_WALK_PF");
+  const int l2d = walk_l2_ahead_host();
   // one slice of look-ahead measured fastest (cfg1 85 us vs 105 / 132 for
   // 2 / 4; deeper prefetch costs occupancy)
   if (pf && pf[0] == '2')
     terrain_walk_kernel<2><<<g1, kWalkNT, 0, ctx->stream>>>(ground, ceiling, S, rows, cols, enc, L,
-                                                           bits, wpr, chgmap);
+                                                           bits, wpr, chgmap, l2d);
   else
     terrain_walk_kernel<1><<<g1, kWalkNT, 0, ctx->stream>>>(ground, ceiling, S, rows, cols, enc, L,
-                                                           bits, wpr, chgmap);
+                                                           bits, wpr, chgmap, l2d);
   if (int rc = check_launch(ctx, "terrain_walk_kernel")) return rc;
   const char *tma = getenv("PCT_TMA");
   if (bnb || (!(tma && tma[0] == '0') && R % 4 == 0)) {

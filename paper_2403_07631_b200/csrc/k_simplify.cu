@@ -348,9 +348,7 @@ int run_simplify(pct_ctx *ctx, const float *ground, const float *cost, int S, in
   auto batch = [&](const std::vector<Triple> &ts) -> int {
     if (ts.empty()) return PCT_OK;
     const int T = (int)ts.size();
-    Triple *htr = reinterpret_cast<Triple *>(hbase + tbytes);
     int *hfl = reinterpret_cast<int *>(hbase + tbytes + (size_t)S * sizeof(Triple));
-    (void)htr;
     PCT_CUDA(ctx, upload_async(ctx, dtr, ts.data(), sizeof(Triple) * T));
     PCT_CUDA(ctx, cudaMemsetAsync(dflags, 0, sizeof(int) * T, ctx->stream));
     int64_t bx = (A.cells + 255) / 256;
