@@ -396,12 +396,20 @@ __global__ void __launch_bounds__(kTileNT) tile_reduce_kernel(
   uint32_t *gk = tk, *ck = tk + S * kTB2;
   const int tile = blockIdx.x;
   const int t = threadIdx.x;
+  const unsigned r0 = offs[tile], r1 = offs[tile + 1];
+  if (t == 0 && r1 > r0) {  // the tile's records DRAM -> L2 while the keys are initialised
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(recs + r0) & ~(uintptr_t)15;
+    const uintptr_t a1 = (reinterpret_cast<uintptr_t>(recs + r1) + 15) & ~(uintptr_t)15;
+    for (uintptr_t a = a0; a < a1; a += 65536) {
+      const unsigned n = (unsigned)(a1 - a < 65536 ? a1 - a : 65536);
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(n) : "memory");
+    }
+  }
   for (int q = t; q < S * kTB2; q += kTileNT) {
     gk[q] = kKeyEmptyMax;
     ck[q] = kKeyEmptyMin;
   }
   __syncthreads();
-  const unsigned r0 = offs[tile], r1 = offs[tile + 1];
   for (unsigned r = r0 + t; r < r1; r += kTileNT) {
     const unsigned long long rec = __ldcs(recs + r);
     const unsigned local = (unsigned)(rec & 0xFFu);
