@@ -242,6 +242,10 @@ __device__ __forceinline__ bool point_cell_bin(double x, double y, double z, con
 constexpr int kPPT = 1;      // points per thread per batch (4 measured slower)
 constexpr int kHash = 512;   // slots (power of 2, >= 2 x batch)
 constexpr int kCtrPad = 32;  // tile counters / cursors: one per 128-byte line
+#ifndef PCT_TILE_L2
+#define PCT_TILE_L2 4
+#endif
+constexpr int kTileL2 = PCT_TILE_L2;  // batches of L2 prefetch ahead in the tile passes
 template <typename T, bool SCATTER>
 __global__ void __launch_bounds__(256) tile_pass_kernel(const T *__restrict__ xyz, int64_t n,
                                                         BinArgs a, int ntx,
@@ -266,6 +270,14 @@ __global__ void __launch_bounds__(256) tile_pass_kernel(const T *__restrict__ xy
   const int64_t p0 = (int64_t)blockIdx.x * chunk;
   const int64_t p1 = p0 + chunk < n ? p0 + chunk : n;
   for (int64_t pb = p0; pb < p1; pb += BATCH) {  // block-uniform trip count
+    if (threadIdx.x == 0 && pb + kTileL2 * BATCH < p1) {  // a later batch: DRAM -> L2
+      const int64_t q0 = pb + kTileL2 * BATCH;
+      const int64_t q1 = q0 + BATCH < p1 ? q0 + BATCH : p1;
+      const uintptr_t a0 = reinterpret_cast<uintptr_t>(xyz + 3 * q0) & ~(uintptr_t)15;
+      const uintptr_t a1 = (reinterpret_cast<uintptr_t>(xyz + 3 * q1) + 15) & ~(uintptr_t)15;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((unsigned)(a1 - a0))
+                   : "memory");
+    }
     int slot[kPPT], fi[kPPT], fj[kPPT], bin[kPPT];
     unsigned rank[kPPT];
     float z32[kPPT];
