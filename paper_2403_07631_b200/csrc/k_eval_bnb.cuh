@@ -244,6 +244,26 @@ __global__ void __launch_bounds__(NT, MINB) resolve_inflate_bnb_kernel(
     j0 = (t - ti * tx) * TW;
   };
   constexpr uint32_t BOX_BYTES = G::CH * G::CW * 4;
+  // the output tile of one slice from shared memory: float4 stores when the
+  // rows are 16-byte aligned (cols % 4 == 0) and the tile is whole in x
+  auto store_tile = [&](float *plane, int rows, int cols, int i0, int j0, int tid) {
+    static_assert(NT % TW == 0 && TW % 4 == 0 && NT % (TW / 4) == 0, "store layout");
+    const int imax = min(TH, rows - i0);
+    if ((cols & 3) == 0 && j0 + TW <= cols) {
+      constexpr int Q = TW / 4, RPS = NT / Q;
+      const int q = tid % Q, r0 = tid / Q;
+      for (int i = r0; i < imax; i += RPS)
+        reinterpret_cast<float4 *>(plane + (int64_t)(i0 + i) * cols + j0)[q] =
+            reinterpret_cast<const float4 *>(ot + i * TW)[q];
+    } else {
+      constexpr int RPS = NT / TW;  // rows per pass
+      const int x = tid % TW, r0 = tid / TW;
+      if (j0 + x < cols) {
+        float *o = plane + (int64_t)(i0 + r0) * cols + (j0 + x);
+        for (int i = r0; i < imax; i += RPS, o += (int64_t)RPS * cols) *o = ot[i * TW + x];
+      }
+    }
+  };
   const float w0 = c_bw[0], w1 = c_bw[1];
   const uint32_t cb_bits = f32_bits((float)c_K.c_barrier);
   // Loads: only steps that are not skipped load their tile (TMA into buffer
@@ -339,14 +359,7 @@ __global__ void __launch_bounds__(NT, MINB) resolve_inflate_bnb_kernel(
         }
       }
       if (skip) {  // outputs equal the previous slice's: store the kept tile
-        static_assert(NT % TW == 0, "store layout");
-        constexpr int RPS = NT / TW;
-        const int x = tid % TW, r0 = tid / TW;
-        const int imax = min(TH, rows - i0);
-        if (j0 + x < cols) {
-          float *o = cost + (int64_t)k * cells + (int64_t)(i0 + r0) * cols + (j0 + x);
-          for (int i = r0; i < imax; i += RPS, o += (int64_t)RPS * cols) *o = ot[i * TW + x];
-        }
+        store_tile(cost + (int64_t)k * cells, rows, cols, i0, j0, tid);
         continue;
       }
       const int cur = lc % 3, prv = (lc + 2) % 3;
@@ -604,16 +617,7 @@ __global__ void __launch_bounds__(NT, MINB) resolve_inflate_bnb_kernel(
     __syncthreads();
     }  // tile changed
     // ---- P4: store the output tile (every output, every slice)
-    {
-      static_assert(NT % TW == 0, "store layout");
-      constexpr int RPS = NT / TW;  // rows per pass
-      const int x = tid % TW, r0 = tid / TW;
-      const int imax = min(TH, rows - i0);
-      if (j0 + x < cols) {
-        float *o = cost + (int64_t)k * cells + (int64_t)(i0 + r0) * cols + (j0 + x);
-        for (int i = r0; i < imax; i += RPS, o += (int64_t)RPS * cols) *o = ot[i * TW + x];
-      }
-    }
+    store_tile(cost + (int64_t)k * cells, rows, cols, i0, j0, tid);
     // the next step's first barrier orders P4's reads of `ot` before its P2
     }
   }
