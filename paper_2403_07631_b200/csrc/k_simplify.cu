@@ -189,14 +189,12 @@ int window_blocks_per_sm(pct_ctx *ctx, size_t smem) {
   return per_sm;
 }
 
-__global__ void __launch_bounds__(256) triples_kernel(SimpArgs A, const Triple *__restrict__ tr,
-                                                      int *__restrict__ flags) {
-  const int t = blockIdx.y;
+__device__ __forceinline__ void triple_any(const SimpArgs &A, const Triple T, int *flag) {
   __shared__ int skip;
-  if (threadIdx.x == 0) skip = *((volatile int *)(flags + t));  // already known unique
+  __syncthreads();  // previous triple's readers of `skip` are done
+  if (threadIdx.x == 0) skip = *((volatile int *)flag);  // already known unique
   __syncthreads();
   if (skip) return;
-  const Triple T = tr[t];
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   bool any = false;
   for (int64_t cell = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; cell < A.cells && !any;
@@ -213,7 +211,79 @@ __global__ void __launch_bounds__(256) triples_kernel(SimpArgs A, const Triple *
                       __ldg(A.cost + (int64_t)T.above * A.stride + cell), A.eps_e, false);
     any = u;
   }
-  if (__syncthreads_or(any) && threadIdx.x == 0) atomicOr(flags + t, 1);
+  if (__syncthreads_or(any) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
+// blockIdx.y = triple (host lists); with a device count, blocks stride over
+// the device-built list instead (gridDim.y small, no empty blocks)
+__global__ void __launch_bounds__(256) triples_kernel(SimpArgs A, const Triple *__restrict__ tr,
+                                                      int *__restrict__ flags,
+                                                      const int *__restrict__ count = nullptr) {
+  if (!count) {
+    triple_any(A, tr[blockIdx.y], flags + blockIdx.y);
+    return;
+  }
+  const int n = *count;
+  for (int t = blockIdx.y; t < n; t += gridDim.y) triple_any(A, tr[t], flags + t);
+}
+
+// The host sweep's first pass, replayed on the device from the window table
+// (one thread; the keep list as a linked list), followed by the triples the
+// second pass would ask assuming it removes nothing -- the speculation the
+// host makes itself on a table miss.  Lets the triples kernel run without a
+// host round trip in between; the host replays the whole sweep afterwards
+// and only falls back to its own rounds on a miss.  count = 0: nothing to
+// speculate (the first pass removed nothing, or needed a triple itself).
+__device__ __forceinline__ int window_lookup(const unsigned long long *table, int S, int below,
+                                             int k, int above) {  // 1 / 0, or -1 = not in table
+  const bool above_ok = (above == k + 1) || (above < 0 && k == S - 1);
+  if (!above_ok) return -1;
+  int bit = -1;
+  if (below < 0) bit = kBit;
+  else if (k - 1 - below < kWin) bit = k - 1 - below;
+  if (bit < 0) return -1;
+  return (int)((table[k] >> bit) & 1ull);
+}
+
+__global__ void spec_sweep_kernel(const unsigned long long *__restrict__ table, int S,
+                                  int *__restrict__ prv, int *__restrict__ nxt,
+                                  Triple *__restrict__ tr, int *__restrict__ flags,
+                                  int *__restrict__ count) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  for (int k = 0; k < S; ++k) {
+    prv[k] = k - 1;
+    nxt[k] = k + 1 < S ? k + 1 : -1;
+  }
+  int head = 0, size = S, T = 0;
+  bool removed = false;
+  for (int k = head; k >= 0;) {  // pass 1
+    const int next = nxt[k];
+    if (size > 1) {
+      const int u = window_lookup(table, S, prv[k], k, next);
+      if (u < 0) {  // the host's own rounds take over
+        *count = 0;
+        return;
+      }
+      if (!u) {
+        if (prv[k] >= 0) nxt[prv[k]] = next;
+        else head = next;
+        if (next >= 0) prv[next] = prv[k];
+        --size;
+        removed = true;
+      }
+    }
+    k = next;
+  }
+  if (removed) {
+    for (int k = head; k >= 0; k = nxt[k]) {  // pass 2, assuming no removal
+      if (size <= 1) break;
+      if (window_lookup(table, S, prv[k], k, nxt[k]) >= 0) continue;
+      tr[T] = Triple{prv[k], k, nxt[k]};
+      flags[T] = 0;
+      ++T;
+    }
+  }
+  *count = T;
 }
 
 // batched maps: blockIdx.y = map (window tables); triples carry their map
@@ -294,9 +364,11 @@ int run_simplify(pct_ctx *ctx, const float *ground, const float *cost, int S, in
   if (S <= 1) return PCT_OK;
   SimpArgs A{ground, cost, (int64_t)rows * cols, (int64_t)rows * cols, S, eps_e,
              (float)c_barrier};
-  // device small buffer layout: table[S] u64 | triples | flags
+  // device small buffer layout: table[S] u64 | triples | flags | count |
+  // speculation's linked list (2 x S ints)
   const size_t tbytes = (size_t)S * 8;
-  const size_t need = tbytes + (size_t)S * sizeof(Triple) + (size_t)S * sizeof(int) + 64;
+  const size_t need = tbytes + (size_t)S * sizeof(Triple) + (size_t)S * sizeof(int) + 64 +
+                      (size_t)2 * S * sizeof(int);
   if (need > 65536) {
     if (int rc = ensure_scratch(ctx, need)) return rc;
   }
@@ -304,6 +376,9 @@ int run_simplify(pct_ctx *ctx, const float *ground, const float *cost, int S, in
   unsigned long long *table = reinterpret_cast<unsigned long long *>(dbase);
   Triple *dtr = reinterpret_cast<Triple *>(dbase + tbytes);
   int *dflags = reinterpret_cast<int *>(dbase + tbytes + (size_t)S * sizeof(Triple));
+  int *dcount = dflags + S;
+  int *dlinks = reinterpret_cast<int *>(dbase + tbytes + (size_t)S * sizeof(Triple) +
+                                        (size_t)S * sizeof(int) + 64);
 
   std::vector<unsigned long long> htable(S, 0);
   PCT_CUDA(ctx, cudaMemsetAsync(table, 0, tbytes, ctx->stream));
@@ -321,12 +396,32 @@ int run_simplify(pct_ctx *ctx, const float *ground, const float *cost, int S, in
   if (int rc = check_launch(ctx, "window_kernel")) return rc;
   // host round trips through the context's pinned buffer (pageable copies
   // are staged and cost latency)
-  const bool pinned = tbytes + (size_t)S * (sizeof(Triple) + sizeof(int)) + 64 <= 65536;
+  const size_t rbytes = tbytes + (size_t)S * (sizeof(Triple) + sizeof(int)) + sizeof(int);
+  const bool pinned = rbytes + 64 <= 65536;
   char *hbase = static_cast<char *>(ctx->hsmall);
+  int spec_n = 0;
   if (pinned) {
-    PCT_CUDA(ctx, readback_async(ctx, hbase, table, tbytes));
+    // first pass on the device + the second pass's triples evaluated
+    // speculatively, all read back with the table in one round trip
+    const char *sp = getenv("PCT_SIMPLIFY_SPEC");
+    const bool spec = !(sp && sp[0] == '0');
+    if (spec) {
+      spec_sweep_kernel<<<1, 32, 0, ctx->stream>>>(table, S, dlinks, dlinks + S, dtr, dflags,
+                                                   dcount);
+      if (int rc = check_launch(ctx, "spec_sweep_kernel")) return rc;
+      int64_t bx = (A.cells + 255) / 256;
+      if (bx > ctx->num_sms * 2) bx = ctx->num_sms * 2;
+      triples_kernel<<<dim3((unsigned)bx, (unsigned)std::min(S, 8)), 256, 0, ctx->stream>>>(
+          A, dtr, dflags, dcount);
+      if (int rc = check_launch(ctx, "triples_kernel")) return rc;
+      PCT_CUDA(ctx, readback_async(ctx, hbase, table, rbytes));
+    } else {
+      PCT_CUDA(ctx, readback_async(ctx, hbase, table, tbytes));
+    }
     PCT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     std::memcpy(htable.data(), hbase, tbytes);
+    if (spec) std::memcpy(&spec_n, hbase + tbytes + (size_t)S * (sizeof(Triple) + sizeof(int)),
+                          sizeof(int));
   } else {
     PCT_CUDA(ctx, cudaMemcpyAsync(htable.data(), table, tbytes, cudaMemcpyDeviceToHost, ctx->stream));
     PCT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
@@ -344,6 +439,11 @@ int run_simplify(pct_ctx *ctx, const float *ground, const float *cost, int S, in
     *hit = true;
     return (htable[k] >> bit) & 1ull;
   };
+  if (spec_n > 0) {  // the speculated triples' answers
+    const Triple *ht = reinterpret_cast<const Triple *>(hbase + tbytes);
+    const int *hf = reinterpret_cast<const int *>(hbase + tbytes + (size_t)S * sizeof(Triple));
+    for (int i = 0; i < spec_n; ++i) cache[{ht[i].below, ht[i].k, ht[i].above}] = hf[i] != 0;
+  }
   int blocks_x = ctx->num_sms * 2;
   auto batch = [&](const std::vector<Triple> &ts) -> int {
     if (ts.empty()) return PCT_OK;
