@@ -196,6 +196,35 @@ def test_extreme_shapes_vs_oracle(monkeypatch, shape):
         assert [s.plane_height for s in simp.slices] == [float(ref["heights"][k]) for k in keep]
 
 
+@pytest.mark.parametrize("scene", ["plane_tall", "stairs", "random"])
+def test_simplify_speculation_matches_host_sweep(monkeypatch, scene):
+    """The device-replayed first pass + speculative second-pass triples give
+    the same surviving slices as the host-only sweep and the oracle, including
+    removal chains longer than the 16-slice window (a plane under a tall
+    empty column) and second passes that remove again."""
+    rng = np.random.default_rng(3)
+    if scene == "plane_tall":
+        n = 20_000
+        xyz = np.column_stack([rng.uniform(0, 4, n), rng.uniform(0, 4, n), np.zeros(n)])
+        xyz = np.vstack([xyz, [[2.0, 2.0, 25.0]]])  # one point far above: ~50 slices
+    elif scene == "stairs":
+        n = 40_000
+        x = rng.uniform(0, 6, n)
+        xyz = np.column_stack([x, rng.uniform(0, 3, n), np.floor(x / 0.5) * 0.4])
+    else:
+        n = 30_000
+        xyz = np.column_stack([rng.uniform(0, 5, n), rng.uniform(0, 5, n),
+                               np.round(rng.uniform(0, 8, n) * 4) / 4])
+    d_s, r_g = 0.5, 0.1
+    ref = oracle.build(xyz, d_s, r_g)
+    cost = oracle.evaluate(ref["ground"], ref["ceiling"], r_g, TABLE_PARAMS)
+    want = [float(ref["heights"][k]) for k in oracle.simplify(ref["ground"], cost)]
+    for spec in ("1", "0"):
+        monkeypatch.setenv("PCT_SIMPLIFY_SPEC", spec)
+        _, _, simp = _run(xyz, d_s, r_g)
+        assert [s.plane_height for s in simp.slices] == want, spec
+
+
 def test_point_order_independence(golden):
     case = golden["cases"]["synth_cfg0"]
     xyz = case_input("synth_cfg0", case)
