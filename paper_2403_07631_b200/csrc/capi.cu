@@ -262,6 +262,7 @@ int pct_ctx_destroy(pct_ctx *ctx) {
   if (ctx->dsmall) cudaFree(ctx->dsmall);
   if (ctx->enc) cudaFree(ctx->enc);
   if (ctx->keys) cudaFree(ctx->keys);
+  if (ctx->spec_ev) cudaEventDestroy(ctx->spec_ev);
   for (auto e : ctx->ev)
     if (e) cudaEventDestroy(e);
   if (ctx->hsmall) cudaFreeHost(ctx->hsmall);
@@ -513,9 +514,20 @@ int pct_tomo_build(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, int xyz_
     dxyz = ctx->staging;
   }
   double lo[3], hi[3];
-  if (int rc = launch_bounds(ctx, dxyz, n, dtype, lo, hi)) return rc;
+  pct_frame dfr{};
+  bool scattered = false;
+  if (int rc = launch_bounds_spec(ctx, dxyz, n, dtype, d_s, r_g, max_grid_side, lo, hi, &dfr,
+                                  &scattered))
+    return rc;
   pct_frame fr;
   int rc = pct_frame_compute(lo, hi, d_s, r_g, max_grid_side, &fr, nullptr, 0);
+  // the device derived the frame the same way; should it ever differ, its
+  // keys are dropped (the key buffer is not clean, so the build below clears
+  // it and scatters again)
+  if (scattered && (rc || dfr.rows != fr.rows || dfr.cols != fr.cols ||
+                    dfr.n_slices != fr.n_slices || dfr.origin_x != fr.origin_x ||
+                    dfr.origin_y != fr.origin_y || dfr.z_min != fr.z_min))
+    scattered = false;
   if (rc == PCT_E_GRID)
     return fail(ctx, PCT_E_GRID, "grid " + std::to_string(fr.rows) + "x" + std::to_string(fr.cols) +
                                      " exceeds the " + std::to_string(max_grid_side) +
@@ -525,7 +537,8 @@ int pct_tomo_build(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, int xyz_
   if ((rc = tomo_alloc(ctx, fr, &t))) return rc;
   t->heights.resize(fr.n_slices);
   pct_frame_compute(lo, hi, d_s, r_g, max_grid_side, &fr, t->heights.data(), fr.n_slices);
-  if ((rc = launch_build(ctx, dxyz, n, dtype, fr, t->heights.data(), t->ground, t->ceiling))) {
+  if ((rc = launch_build(ctx, dxyz, n, dtype, fr, t->heights.data(), t->ground, t->ceiling, 0, -1,
+                         0, scattered))) {
     pct_tomo_free(ctx, t);
     return rc;
   }

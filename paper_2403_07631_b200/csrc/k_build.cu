@@ -32,6 +32,10 @@ __host__ inline double dkey_inv(unsigned long long k) {
   std::memcpy(&d, &u, 8);
   return d;
 }
+__device__ __forceinline__ double dkey_inv_dev(unsigned long long k) {
+  const unsigned long long u = (k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k;
+  return __longlong_as_double((long long)u);
+}
 
 // ---------------------------------------------------------------- K0 bounds
 // keys[0..2] = min (atomicMin), keys[3..5] = max (atomicMax), keys[6] = #non-finite
@@ -194,6 +198,56 @@ __global__ void __launch_bounds__(256) scatter_kernel(const T *__restrict__ xyz,
                                                       uint32_t *__restrict__ ckey,
                                                       unsigned long long *outside) {
   scatter_body(xyz, n, a, gkey, ckey, outside);
+}
+
+// Speculative scatter (single maps): the grid frame of pct_frame_compute
+// derived on the device from the bounds keys (same IEEE operations, no
+// contraction), so the scatter can run before the host has read the bounds.
+// ok = 0 when the frame would not take the atomic single-map path
+// (non-finite points, grid over the limit, too many slices to stage, keys
+// beyond the buffer half or the tiled-build threshold).
+struct SpecFrame {
+  BinArgs a;
+  int ok;
+};
+constexpr int kSpecMaxS = 512;  // the launch stages at most this many heights (4 KB)
+
+__global__ void spec_frame_kernel(const unsigned long long *__restrict__ keys, double d_s,
+                                  double r_g, int64_t max_side, double half_bytes,
+                                  double max_key_bytes, SpecFrame *__restrict__ f) {
+  if (threadIdx.x != 0) return;
+  f->ok = 0;
+  if (keys[6]) return;
+  double lo[3], hi[3];
+  for (int c = 0; c < 3; ++c) {
+    lo[c] = dkey_inv_dev(keys[c]);
+    hi[c] = dkey_inv_dev(keys[3 + c]);
+  }
+  const double qy = __ddiv_rn(__dsub_rn(hi[1], lo[1]), r_g);
+  const double qx = __ddiv_rn(__dsub_rn(hi[0], lo[0]), r_g);
+  const double qz = __ddiv_rn(__dsub_rn(hi[2], lo[2]), d_s);
+  const double rows_d = floor(__dadd_rn(qy, 0.5)) + 2.0;
+  const double cols_d = floor(__dadd_rn(qx, 0.5)) + 2.0;
+  double s = ceil(__dsub_rn(qz, 1e-9));
+  if (s < 1) s = 1;
+  if (rows_d > (double)max_side || cols_d > (double)max_side || s > (double)kSpecMaxS) return;
+  const int rows = (int)rows_d, cols = (int)cols_d, S = (int)s;
+  const int64_t cells = (int64_t)rows * cols;
+  const double kb = 4.0 * (double)S * (double)cells;
+  if (kb > half_bytes || 2.0 * (double)S * (double)cells * 4.0 > max_key_bytes) return;
+  f->a = BinArgs{lo[0], lo[1], lo[2], r_g, d_s, __ddiv_rn(1.0, r_g), __ddiv_rn(1.0, d_s),
+                 nullptr, cells, rows, cols, S, 0, 1};
+  f->ok = 1;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) spec_scatter_kernel(const T *__restrict__ xyz, int64_t n,
+                                                           const SpecFrame *__restrict__ f,
+                                                           uint32_t *__restrict__ keys,
+                                                           int64_t half_words) {
+  if (!f->ok) return;  // uniform
+  const BinArgs a = f->a;
+  scatter_body(xyz, n, a, keys, keys + half_words, nullptr);
 }
 
 // -------------------------------------------- tile-partitioned build (T1-T4)
@@ -588,6 +642,75 @@ int launch_bounds(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, double lo
   return PCT_OK;
 }
 
+int launch_bounds_spec(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, double d_s,
+                       double r_g, int64_t max_grid_side, double lo[3], double hi[3],
+                       pct_frame *dev_frame, bool *scattered) {
+  *scattered = false;
+  if (n <= 0) return fail(ctx, PCT_E_EMPTY, "zero valid points");
+  const char *bmode = getenv("PCT_BUILD");
+  const char *sv = getenv("PCT_BUILD_SPEC");
+  const bool spec = ctx->keys && ctx->keys_clean && !(sv && sv[0] == '0') &&
+                    !(bmode && bmode[0] == 't');
+  unsigned long long *keys = static_cast<unsigned long long *>(ctx->dsmall);
+  SpecFrame *df = reinterpret_cast<SpecFrame *>(static_cast<char *>(ctx->dsmall) + 64);
+  unsigned long long init[7] = {~0ull, ~0ull, ~0ull, 0ull, 0ull, 0ull, 0ull};
+  char *hb = static_cast<char *>(ctx->hsmall);
+  PCT_CUDA(ctx, upload_async(ctx, keys, init, sizeof(init)));
+  if (dtype == PCT_F32)
+    bounds_kernel<float><<<grid_for(ctx, (n + 3) / 4, 256), 256, 0, ctx->stream>>>(
+        static_cast<const float *>(xyz), n, keys);
+  else
+    bounds_kernel<double><<<grid_for(ctx, n, 256), 256, 0, ctx->stream>>>(
+        static_cast<const double *>(xyz), n, keys);
+  if (int rc = check_launch(ctx, "bounds_kernel")) return rc;
+  if (spec) {
+    const int64_t half = (int64_t)(ctx->keys_bytes / 2) / 4;  // words per half
+    const char *bm = getenv("PCT_BUILD");
+    const double max_key = (bm && bm[0] == 'a') ? 1e300 : 1.5e9;
+    spec_frame_kernel<<<1, 32, 0, ctx->stream>>>(keys, d_s, r_g, max_grid_side,
+                                                 4.0 * (double)half, max_key, df);
+    if (int rc = check_launch(ctx, "spec_frame_kernel")) return rc;
+    // bounds + frame come back while the scatter runs: the host waits on an
+    // event recorded before the scatter, not on the stream
+    PCT_CUDA(ctx, readback_async(ctx, hb, keys, 64 + sizeof(SpecFrame)));
+    if (!ctx->spec_ev) PCT_CUDA(ctx, cudaEventCreateWithFlags(&ctx->spec_ev, cudaEventDisableTiming));
+    PCT_CUDA(ctx, cudaEventRecord(ctx->spec_ev, ctx->stream));
+    uint32_t *kw = static_cast<uint32_t *>(ctx->keys);
+    const size_t hs = (size_t)kSpecMaxS * sizeof(double);
+    if (dtype == PCT_F32)
+      spec_scatter_kernel<float><<<grid_for(ctx, n, 256, 16), 256, hs, ctx->stream>>>(
+          static_cast<const float *>(xyz), n, df, kw, half);
+    else
+      spec_scatter_kernel<double><<<grid_for(ctx, n, 256, 16), 256, hs, ctx->stream>>>(
+          static_cast<const double *>(xyz), n, df, kw, half);
+    if (int rc = check_launch(ctx, "spec_scatter_kernel")) return rc;
+    PCT_CUDA(ctx, cudaEventSynchronize(ctx->spec_ev));
+  } else {
+    PCT_CUDA(ctx, readback_async(ctx, hb, keys, 56));
+    PCT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  }
+  const unsigned long long *hk = reinterpret_cast<const unsigned long long *>(hb);
+  if (spec) {
+    const SpecFrame *hf = reinterpret_cast<const SpecFrame *>(hb + 64);
+    if (hf->ok) {
+      *scattered = true;
+      ctx->keys_clean = false;  // until a scan of this frame consumes them
+      dev_frame->rows = hf->a.rows;
+      dev_frame->cols = hf->a.cols;
+      dev_frame->n_slices = hf->a.S;
+      dev_frame->origin_x = hf->a.x0;
+      dev_frame->origin_y = hf->a.y0;
+      dev_frame->z_min = hf->a.z0;
+    }
+  }
+  if (hk[6]) return fail(ctx, PCT_E_NONFINITE, "point cloud contains non-finite coordinates");
+  for (int c = 0; c < 3; ++c) {
+    lo[c] = dkey_inv(hk[c]);
+    hi[c] = dkey_inv(hk[3 + c]);
+  }
+  return PCT_OK;
+}
+
 // ------------------------------------------------ batched maps (host side)
 // descriptors + per-map scratch live in the context buffers; the caller keeps
 // the batch's inputs / outputs alive until the stream is synchronised
@@ -658,6 +781,7 @@ int launch_build_batch(pct_ctx *ctx, int n_maps, const void *const *xyz, const i
     PCT_CUDA(ctx, cudaMalloc(&ctx->keys, kbytes));
     ctx->keys_bytes = kbytes;
     ctx->keys_tag[0] = -1;
+    ctx->keys_clean = false;
   }
   std::vector<BuildMap> d(n_maps);
   std::vector<double> hh((size_t)hcount);
@@ -692,6 +816,7 @@ int launch_build_batch(pct_ctx *ctx, int n_maps, const void *const *xyz, const i
     }
   }
   ctx->keys_tag[0] = -1;  // dirty until the scans are launched
+  ctx->keys_clean = false;  // the single-map layout must be cleared again
   PCT_CUDA(ctx, cudaMemsetAsync(outside, 0, 8, ctx->stream));
   const size_t hsm = smax <= kMaxStagedHeights ? (size_t)smax * sizeof(double) : 0;
   const int gx = std::max(1, std::min(grid_for(ctx, nmax, 256, 16), 64));
@@ -738,7 +863,7 @@ bool bounds_from_keys(const unsigned long long *k, double lo[3], double hi[3]) {
 
 int launch_build(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, const pct_frame &fr,
                  const double *heights_host, float *ground, float *ceiling, int row0, int nrows,
-                 int64_t out_stride) {
+                 int64_t out_stride, bool keys_scattered) {
   const int S = fr.n_slices;
   if (nrows < 0) {  // whole grid
     row0 = 0;
@@ -817,38 +942,43 @@ int launch_build(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, const pct_
         recs, offs, ntx, nrows, fr.cols, S, out_stride, ground, ceiling);
     return check_launch(ctx, "tile_reduce_kernel");
   }
-  // key planes in their own grow-only buffer: the scan leaves them empty
-  // again, so only a new layout needs the memsets
-  const size_t kbytes = 2 * plane * S;
-  if (ctx->keys_bytes < kbytes) {
+  // key planes in their own grow-only buffer: ground keys in the first
+  // half, ceiling keys in the second (fixed offsets, so any layout that fits
+  // finds them empty: the scan leaves every key it reads empty again); a
+  // memset only after growth or a batch build (another layout)
+  if (keys_scattered && !(S <= kSpecMaxS && whole && derive && ctx->keys_bytes / 2 >= plane * S))
+    return fail(ctx, PCT_E_INVALID, "speculative scatter does not match the frame");
+  if (ctx->keys_bytes / 2 < plane * S) {
     if (ctx->keys) {
       cudaStreamSynchronize(ctx->stream);
       cudaFree(ctx->keys);
       ctx->keys = nullptr;
       ctx->keys_bytes = 0;
     }
-    PCT_CUDA(ctx, cudaMalloc(&ctx->keys, kbytes));
-    ctx->keys_bytes = kbytes;
-    ctx->keys_tag[0] = -1;
+    PCT_CUDA(ctx, cudaMalloc(&ctx->keys, 2 * plane * S));
+    ctx->keys_bytes = 2 * plane * S;
+    ctx->keys_clean = false;
   }
   if (int rc = ensure_scratch(ctx, hbytes + 256)) return rc;
+  const size_t half = ctx->keys_bytes / 2;
   uint32_t *gkey = static_cast<uint32_t *>(ctx->keys);
-  uint32_t *ckey = reinterpret_cast<uint32_t *>(static_cast<char *>(ctx->keys) + plane * S);
+  uint32_t *ckey = reinterpret_cast<uint32_t *>(static_cast<char *>(ctx->keys) + half);
   char *base = static_cast<char *>(ctx->scratch);
   double *hdev = reinterpret_cast<double *>(base);
   unsigned long long *outside = reinterpret_cast<unsigned long long *>(base + hbytes);
   if (!derive) PCT_CUDA(ctx, upload_async(ctx, hdev, heights_host, (size_t)S * sizeof(double)));
-  if (ctx->keys_tag[0] != S || ctx->keys_tag[1] != cells) {
-    PCT_CUDA(ctx, cudaMemsetAsync(gkey, 0x00, plane * S, ctx->stream));
-    PCT_CUDA(ctx, cudaMemsetAsync(ckey, 0xFF, plane * S, ctx->stream));
+  if (!keys_scattered && !ctx->keys_clean) {
+    PCT_CUDA(ctx, cudaMemsetAsync(gkey, 0x00, half, ctx->stream));
+    PCT_CUDA(ctx, cudaMemsetAsync(ckey, 0xFF, half, ctx->stream));
   }
-  ctx->keys_tag[0] = -1;  // dirty until the scan below is launched
+  ctx->keys_clean = false;  // until the scan below is launched
+  ctx->keys_tag[0] = -3;    // single-map layout (the batch layout memsets again)
   if (whole) outside = nullptr;
   else PCT_CUDA(ctx, cudaMemsetAsync(outside, 0, 8, ctx->stream));
   BinArgs a{fr.origin_x, fr.origin_y, fr.z_min, fr.r_g, fr.d_s, 1.0 / fr.r_g, 1.0 / fr.d_s,
             hdev, cells, nrows, fr.cols, S, row0, derive ? 1 : 0};
   const size_t hsm_bytes = S <= kMaxStagedHeights ? (size_t)S * sizeof(double) : 0;
-  if (n > 0) {
+  if (n > 0 && !keys_scattered) {
     if (dtype == PCT_F32)
       scatter_kernel<float><<<grid_for(ctx, n, 256, 16), 256, hsm_bytes, ctx->stream>>>(
           static_cast<const float *>(xyz), n, a, gkey, ckey, outside);
@@ -860,8 +990,7 @@ int launch_build(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, const pct_
   scan_kernel<<<dim3((unsigned)((cells + 255) / 256), 2), 256, 0, ctx->stream>>>(
       gkey, ckey, cells, S, out_stride, ground, ceiling);
   if (int rc = check_launch(ctx, "scan_kernel")) return rc;
-  ctx->keys_tag[0] = S;  // the scan resets every key it reads
-  ctx->keys_tag[1] = cells;
+  ctx->keys_clean = true;  // the scan resets every key it reads
   return PCT_OK;
 }
 

@@ -40,6 +40,10 @@ struct pct_ctx {
   void *keys = nullptr;
   size_t keys_bytes = 0;
   int64_t keys_tag[2] = {-1, -1};
+  // single-map layout: ground keys in the first half of the buffer, ceiling
+  // keys in the second; clean = every key empty (the scan restores that)
+  bool keys_clean = false;
+  cudaEvent_t spec_ev = nullptr;  // bounds read back ahead of the speculative scatter
   // zero-padded encoded c_init stacks of the split evaluation; the padding
   // is cleared only when the layout changes (the interior is rewritten)
   void *enc = nullptr;
@@ -114,7 +118,13 @@ int launch_bounds(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, double lo
 // slice k at k*out_stride floats (<= 0: dense)
 int launch_build(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, const pct_frame &fr,
                  const double *heights_host, float *ground, float *ceiling, int row0 = 0,
-                 int nrows = -1, int64_t out_stride = 0);
+                 int nrows = -1, int64_t out_stride = 0, bool keys_scattered = false);
+// bounds + (when the key buffer allows) the scatter of the frame the device
+// derives from them, before the host has the bounds: *scattered tells
+// whether the keys of that frame are already in place
+int launch_bounds_spec(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, double d_s,
+                       double r_g, int64_t max_grid_side, double lo[3], double hi[3],
+                       pct_frame *dev_frame, bool *scattered);
 int launch_evaluate(pct_ctx *ctx, const float *ground, const float *ceiling, int S, int rows,
                     int cols, double r_g, const pct_trav_params &p, const float *kernel_w,
                     int kside, float *cost, int mode);

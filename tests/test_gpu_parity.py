@@ -225,6 +225,27 @@ def test_simplify_speculation_matches_host_sweep(monkeypatch, scene):
         assert [s.plane_height for s in simp.slices] == want, spec
 
 
+def test_build_speculation_across_layouts(monkeypatch):
+    """Consecutive builds on one context with changing grid layouts (smaller,
+    larger -> key buffer growth, back, f64 input), with the speculative
+    scatter on and off, equal the oracle's stacks."""
+    rng = np.random.default_rng(21)
+
+    def cloud(w, h, zmax, n):
+        return np.column_stack([rng.uniform(0, w, n), rng.uniform(0, h, n),
+                                rng.uniform(0, zmax, n)]).astype(np.float32)
+
+    clouds = [cloud(3, 2, 2, 20_000), cloud(9, 7, 5, 60_000), cloud(3, 2, 2, 20_000),
+              cloud(5, 5, 9, 30_000).astype(np.float64), cloud(2, 9, 1, 10_000)]
+    for spec in ("1", "0", "1"):
+        monkeypatch.setenv("PCT_BUILD_SPEC", spec)
+        for xyz in clouds:
+            ref = oracle.build(xyz, 0.5, 0.1)
+            tom = pct.build_tomogram(pct.PointCloud(xyz), 0.5, 0.1)
+            _assert_layers_equal(tom.ground_stack(), ref["ground"], f"ground spec={spec}")
+            _assert_layers_equal(tom.ceiling_stack(), ref["ceiling"], f"ceiling spec={spec}")
+
+
 def test_point_order_independence(golden):
     case = golden["cases"]["synth_cfg0"]
     xyz = case_input("synth_cfg0", case)
