@@ -245,21 +245,30 @@ __device__ __forceinline__ int window_lookup(const unsigned long long *table, in
   return (int)((table[k] >> bit) & 1ull);
 }
 
-__global__ void spec_sweep_kernel(const unsigned long long *__restrict__ table, int S,
-                                  int *__restrict__ prv, int *__restrict__ nxt,
-                                  Triple *__restrict__ tr, int *__restrict__ flags,
-                                  int *__restrict__ count) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  for (int k = 0; k < S; ++k) {
+constexpr int kSpecSweepMaxS = 1024;  // table + links staged in shared memory (16 KB)
+
+__global__ void __launch_bounds__(32) spec_sweep_kernel(
+    const unsigned long long *__restrict__ table, int S, Triple *__restrict__ tr,
+    int *__restrict__ flags, int *__restrict__ count) {
+  __shared__ unsigned long long tb[kSpecSweepMaxS];
+  __shared__ int prv[kSpecSweepMaxS], nxt[kSpecSweepMaxS];
+  if (S > kSpecSweepMaxS) {
+    if (threadIdx.x == 0) *count = 0;
+    return;
+  }
+  for (int k = threadIdx.x; k < S; k += 32) {  // one global read per entry
+    tb[k] = table[k];
     prv[k] = k - 1;
     nxt[k] = k + 1 < S ? k + 1 : -1;
   }
+  __syncwarp();
+  if (threadIdx.x != 0) return;
   int head = 0, size = S, T = 0;
   bool removed = false;
   for (int k = head; k >= 0;) {  // pass 1
     const int next = nxt[k];
     if (size > 1) {
-      const int u = window_lookup(table, S, prv[k], k, next);
+      const int u = window_lookup(tb, S, prv[k], k, next);
       if (u < 0) {  // the host's own rounds take over
         *count = 0;
         return;
@@ -277,7 +286,7 @@ __global__ void spec_sweep_kernel(const unsigned long long *__restrict__ table, 
   if (removed) {
     for (int k = head; k >= 0; k = nxt[k]) {  // pass 2, assuming no removal
       if (size <= 1) break;
-      if (window_lookup(table, S, prv[k], k, nxt[k]) >= 0) continue;
+      if (window_lookup(tb, S, prv[k], k, nxt[k]) >= 0) continue;
       tr[T] = Triple{prv[k], k, nxt[k]};
       flags[T] = 0;
       ++T;
@@ -364,11 +373,9 @@ int run_simplify(pct_ctx *ctx, const float *ground, const float *cost, int S, in
   if (S <= 1) return PCT_OK;
   SimpArgs A{ground, cost, (int64_t)rows * cols, (int64_t)rows * cols, S, eps_e,
              (float)c_barrier};
-  // device small buffer layout: table[S] u64 | triples | flags | count |
-  // speculation's linked list (2 x S ints)
+  // device small buffer layout: table[S] u64 | triples | flags | count
   const size_t tbytes = (size_t)S * 8;
-  const size_t need = tbytes + (size_t)S * sizeof(Triple) + (size_t)S * sizeof(int) + 64 +
-                      (size_t)2 * S * sizeof(int);
+  const size_t need = tbytes + (size_t)S * sizeof(Triple) + (size_t)S * sizeof(int) + 64;
   if (need > 65536) {
     if (int rc = ensure_scratch(ctx, need)) return rc;
   }
@@ -377,8 +384,6 @@ int run_simplify(pct_ctx *ctx, const float *ground, const float *cost, int S, in
   Triple *dtr = reinterpret_cast<Triple *>(dbase + tbytes);
   int *dflags = reinterpret_cast<int *>(dbase + tbytes + (size_t)S * sizeof(Triple));
   int *dcount = dflags + S;
-  int *dlinks = reinterpret_cast<int *>(dbase + tbytes + (size_t)S * sizeof(Triple) +
-                                        (size_t)S * sizeof(int) + 64);
 
   std::vector<unsigned long long> htable(S, 0);
   PCT_CUDA(ctx, cudaMemsetAsync(table, 0, tbytes, ctx->stream));
@@ -406,8 +411,7 @@ int run_simplify(pct_ctx *ctx, const float *ground, const float *cost, int S, in
     const char *sp = getenv("PCT_SIMPLIFY_SPEC");
     const bool spec = !(sp && sp[0] == '0');
     if (spec) {
-      spec_sweep_kernel<<<1, 32, 0, ctx->stream>>>(table, S, dlinks, dlinks + S, dtr, dflags,
-                                                   dcount);
+      spec_sweep_kernel<<<1, 32, 0, ctx->stream>>>(table, S, dtr, dflags, dcount);
       if (int rc = check_launch(ctx, "spec_sweep_kernel")) return rc;
       int64_t bx = (A.cells + 255) / 256;
       if (bx > ctx->num_sms * 2) bx = ctx->num_sms * 2;
