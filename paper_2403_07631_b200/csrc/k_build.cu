@@ -665,8 +665,8 @@ int launch_bounds_spec(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, doub
   if (int rc = check_launch(ctx, "bounds_kernel")) return rc;
   if (spec) {
     const int64_t half = (int64_t)(ctx->keys_bytes / 2) / 4;  // words per half
-    const char *bm = getenv("PCT_BUILD");
-    const double max_key = (bm && bm[0] == 'a') ? 1e300 : 1.5e9;
+    // the atomic path's key-size limit (launch_build's big_keys), unless forced
+    const double max_key = (bmode && bmode[0] == 'a') ? 1e300 : 1.5e9;
     spec_frame_kernel<<<1, 32, 0, ctx->stream>>>(keys, d_s, r_g, max_grid_side,
                                                  4.0 * (double)half, max_key, df);
     if (int rc = check_launch(ctx, "spec_frame_kernel")) return rc;
