@@ -116,7 +116,8 @@ __device__ __forceinline__ void walk_body(const float *__restrict__ ground,
                                           int cols, float *__restrict__ enc_out,
                                           const EncLayout &L, uint32_t *__restrict__ bits_out,
                                           int wpr, unsigned char *__restrict__ chgmap,
-                                          int l2d) {
+                                          int l2d, int kb, int ke) {
+  // slices kb .. ke-1 (a chunk: its first slice is computed in full)
   const int64_t cells = (int64_t)rows * cols;
   // threads index row-padded columns: warp = one gentle-bitmap word of one row
   const int64_t pidx = (int64_t)blockIdx.x * kWalkNT + threadIdx.x;
@@ -133,10 +134,10 @@ __device__ __forceinline__ void walk_body(const float *__restrict__ ground,
   const float nanf_ = bits_f32(kNaNBits);
   const float cb32 = (float)c_K.c_barrier;
   const int64_t base = (int64_t)i * cols + j;
-  const float *pg = ground + base;
-  const float *pc = ceiling + base;
-  float *pe = enc_out + L.at(0, i, j);
-  uint32_t *pb = bits_out + (int64_t)i * wpr + (j0_ >> 5);
+  const float *pg = ground + base + (int64_t)kb * cells;
+  const float *pc = ceiling + base + (int64_t)kb * cells;
+  float *pe = enc_out + L.at(kb, i, j);
+  uint32_t *pb = bits_out + (int64_t)kb * rows * wpr + (int64_t)i * wpr + (j0_ >> 5);
 
   float qe[PF], qu[PF], qd[PF], qc[PF], ql[PF], qr[PF];
   auto fetch = [&](const float *g, const float *c, int s) {
@@ -149,7 +150,7 @@ __device__ __forceinline__ void walk_body(const float *__restrict__ ground,
   };
 #pragma unroll
   for (int s = 0; s < PF; ++s)
-    if (s < S) fetch(pg + s * cells, pc + s * cells, s);
+    if (kb + s < ke) fetch(pg + s * cells, pc + s * cells, s);
   const float *ng = pg + PF * cells, *nc = pc + PF * cells;
 
   WalkState st;
@@ -158,14 +159,14 @@ __device__ __forceinline__ void walk_body(const float *__restrict__ ground,
   // cell's encoded c_init or gentle flag differs from the slice below (the
   // resolve/inflate kernel skips tiles whose window saw no change)
   const int64_t cmstride = (int64_t)((rows + 7) >> 3) * wpr;
-  unsigned char *pcm = chgmap + (int64_t)(i >> 3) * wpr + (j0_ >> 5);
+  unsigned char *pcm = chgmap + (int64_t)kb * cmstride + (int64_t)(i >> 3) * wpr + (j0_ >> 5);
   uint32_t prev_enc = 0u;
   unsigned prev_word = 0u;
-  for (int k0 = 0; k0 < S; k0 += PF) {
+  for (int k0 = kb; k0 < ke; k0 += PF) {
 #pragma unroll
     for (int s = 0; s < PF; ++s) {
       const int k = k0 + s;
-      if (k >= S) break;
+      if (k >= ke) break;
       const float e = qe[s], u = qu[s], d = qd[s], c = qc[s];
       float l = __shfl_up_sync(0xFFFFFFFFu, e, 1);
       float r = __shfl_down_sync(0xFFFFFFFFu, e, 1);
@@ -173,16 +174,16 @@ __device__ __forceinline__ void walk_body(const float *__restrict__ ground,
       if (lane == 31) r = qr[s];
       if (!hl) l = nanf_;
       if (!hr) r = nanf_;
-      if (k + PF < S) {
+      if (k + PF < ke) {
         fetch(ng, nc, s);
-        if (l2d > 0 && live && k + PF + l2d < S) {  // DRAM -> L2 ahead, no registers held
+        if (l2d > 0 && live && k + PF + l2d < ke) {  // DRAM -> L2 ahead, no registers held
           asm volatile("prefetch.global.L2 [%0];" ::"l"(ng + (int64_t)l2d * cells));
           asm volatile("prefetch.global.L2 [%0];" ::"l"(nc + (int64_t)l2d * cells));
         }
         ng += cells;
         nc += cells;
       }
-      walk_step(st, k, live, e, l, r, u, d, c, nanf_, cb32);
+      walk_step(st, k - kb, live, e, l, r, u, d, c, nanf_, cb32);
       const float enc = st.enc;
       const bool gentle = st.gentle;
       if (live) *pe = enc;
@@ -190,7 +191,7 @@ __device__ __forceinline__ void walk_body(const float *__restrict__ ground,
       const unsigned word = __ballot_sync(0xFFFFFFFFu, live && gentle);
       if (chgmap) {  // uniform
         const bool enc_changed = __any_sync(0xFFFFFFFFu, live && f32_bits(enc) != prev_enc);
-        if (wlead && (k == 0 || word != prev_word || enc_changed)) *pcm = 1;
+        if (wlead && (k == kb || word != prev_word || enc_changed)) *pcm = 1;
         prev_word = word;
         prev_enc = f32_bits(enc);
       }
@@ -201,12 +202,18 @@ __device__ __forceinline__ void walk_body(const float *__restrict__ ground,
   }
 }
 
-template <int PF>
+template <int PF, bool CHUNKED = false>
 __global__ void __launch_bounds__(kWalkNT) terrain_walk_kernel(
     const float *__restrict__ ground, const float *__restrict__ ceiling, int S, int rows,
     int cols, float *__restrict__ enc_out, EncLayout L, uint32_t *__restrict__ bits_out,
     int wpr, unsigned char *__restrict__ chgmap, int l2d) {
-  walk_body<PF>(ground, ceiling, S, rows, cols, enc_out, L, bits_out, wpr, chgmap, l2d);
+  if constexpr (CHUNKED) {  // blockIdx.y = chunk of slices (small maps: more threads in flight)
+    const int kb = (int)((int64_t)S * blockIdx.y / gridDim.y);
+    const int ke = (int)((int64_t)S * (blockIdx.y + 1) / gridDim.y);
+    walk_body<PF>(ground, ceiling, S, rows, cols, enc_out, L, bits_out, wpr, chgmap, l2d, kb, ke);
+  } else {
+    walk_body<PF>(ground, ceiling, S, rows, cols, enc_out, L, bits_out, wpr, chgmap, l2d, 0, S);
+  }
 }
 
 // per-map arguments of the split evaluation (a single map is a batch of one)
@@ -228,7 +235,8 @@ __global__ void __launch_bounds__(kWalkNT) terrain_walk_batch_kernel(const EvalM
   if ((int64_t)blockIdx.x * kWalkNT >= (int64_t)m.rows * m.wpr * 32) return;  // whole block
   // no L2 look-ahead for batches of small maps (measured slower: cfg4
   // evaluate 1.97 -> 2.07 ms)
-  walk_body<PF>(m.ground, m.ceiling, m.S, m.rows, m.cols, m.enc, m.L, m.bits, m.wpr, m.chg, 0);
+  walk_body<PF>(m.ground, m.ceiling, m.S, m.rows, m.cols, m.enc, m.L, m.bits, m.wpr, m.chg, 0, 0,
+                m.S);
 }
 
 template <int R, int PR, int TH, int TW>

@@ -683,14 +683,28 @@ int launch_split(pct_ctx *ctx, const float *ground, const float *ceiling, int S,
   const unsigned g1 = (unsigned)((walk_threads + kWalkNT - 1) / kWalkNT);
   const char *pf = getenv("PCT_WALK_PF");
   const int l2d = walk_l2_ahead_host();
+  // slice chunks: a small map gets ~2 waves of threads by walking its slices
+  // in up to 4 independent chunks (each chunk's first slice in full); large
+  // maps fill the GPU with one chunk (PCT_WALK_CHUNKS overrides)
+  int chunks = 1;
+  {
+    const int64_t resident = (int64_t)ctx->num_sms * 2048;
+    const int64_t threads = (int64_t)g1 * kWalkNT;
+    while (chunks < 4 && threads * chunks * 2 <= 2 * resident && S >= 6 * (chunks * 2)) chunks *= 2;
+    if (const char *e = getenv("PCT_WALK_CHUNKS")) chunks = std::max(1, std::min(S, atoi(e)));
+  }
   // one slice of look-ahead measured fastest (cfg1 85 us vs 105 / 132 for
   // 2 / 4; deeper prefetch costs occupancy)
   if (pf && pf[0] == '2')
     terrain_walk_kernel<2><<<g1, kWalkNT, 0, ctx->stream>>>(ground, ceiling, S, rows, cols, enc, L,
                                                            bits, wpr, chgmap, l2d);
   else
-    terrain_walk_kernel<1><<<g1, kWalkNT, 0, ctx->stream>>>(ground, ceiling, S, rows, cols, enc, L,
-                                                           bits, wpr, chgmap, l2d);
+    if (chunks > 1)
+      terrain_walk_kernel<1, true><<<dim3(g1, chunks), kWalkNT, 0, ctx->stream>>>(
+          ground, ceiling, S, rows, cols, enc, L, bits, wpr, chgmap, l2d);
+    else
+      terrain_walk_kernel<1><<<g1, kWalkNT, 0, ctx->stream>>>(ground, ceiling, S, rows, cols, enc,
+                                                             L, bits, wpr, chgmap, l2d);
   if (int rc = check_launch(ctx, "terrain_walk_kernel")) return rc;
   const char *tma = getenv("PCT_TMA");
   if (bnb || (!(tma && tma[0] == '0') && R % 4 == 0)) {

@@ -246,6 +246,20 @@ def test_build_speculation_across_layouts(monkeypatch):
             _assert_layers_equal(tom.ceiling_stack(), ref["ceiling"], f"ceiling spec={spec}")
 
 
+@pytest.mark.parametrize("chunks", ["1", "3", "7"])
+def test_walk_slice_chunks_are_exact(golden, monkeypatch, chunks):
+    """The terrain walk split into independent slice chunks (each chunk's
+    first slice computed in full) gives the same costs."""
+    for name in ("synth_cfg0", "ref_spiral_s3"):
+        case = golden["cases"][name]
+        tom = pct.build_tomogram(pct.PointCloud(case_input(name, case)), case["d_s"], case["r_g"])
+        monkeypatch.delenv("PCT_WALK_CHUNKS", raising=False)
+        want = pct.evaluate_tomogram(tom, pct.TravParams()).cost_stack()
+        monkeypatch.setenv("PCT_WALK_CHUNKS", chunks)
+        got = pct.evaluate_tomogram(tom, pct.TravParams()).cost_stack()
+        assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), name
+
+
 def test_point_order_independence(golden):
     case = golden["cases"]["synth_cfg0"]
     xyz = case_input("synth_cfg0", case)
