@@ -404,6 +404,31 @@ def test_simplify_edge_cases():
         pct.simplify_tomogram(t)
 
 
+@pytest.mark.parametrize("eps_e", [1e-6, 0.0, -1e-6, 3e-5])
+def test_simplify_eps_boundary(eps_e):
+    """Elevation differences straddling eps_e at several magnitudes (the
+    window kernel's float32 pre-test must defer to the float64 subtraction in
+    exactly these cases): surviving slices equal the oracle's."""
+    from paper_2403_07631_b200.tomogram import Tomogram, TomogramSlice, Layer
+    rng = np.random.default_rng(17)
+    shape = (24, 24)
+    S = 12
+    base = rng.choice(np.array([0.0, 0.37, 3.1, 17.5, 250.0, 4097.0]), size=shape)
+    gs, cs = [], []
+    for k in range(S):
+        # per-cell offsets within a few ulps of +-eps, some exactly representable
+        off = eps_e * (1 + rng.integers(-3, 4, size=shape) * 2.0 ** -22) * (k % 3)
+        gs.append((base + off).astype(np.float32))
+        cs.append(np.ones(shape, np.float32))  # equal costs: elevations decide
+    G, Cst = np.stack(gs), np.stack(cs)
+    keep = oracle.simplify(G, Cst, eps_e=eps_e)
+    tom = Tomogram([TomogramSlice(Layer(g, 0.1, (0, 0)), Layer(g, 0.1, (0, 0)), 0.5 * (k + 1), k,
+                                  Layer(c, 0.1, (0, 0))) for k, (g, c) in enumerate(zip(gs, cs))],
+                   0.5, 0.0)
+    out = pct.simplify_tomogram(tom, eps_e=eps_e)
+    assert [s.plane_height for s in out.slices] == [0.5 * (k + 1) for k in keep]
+
+
 def test_build_errors_and_kats():
     with pytest.raises(ValueError):
         pct.build_tomogram(pct.PointCloud(np.ones((3, 3))), 0.0, 0.1)
