@@ -293,8 +293,21 @@ __device__ __forceinline__ bool point_cell_bin(double x, double y, double z, con
 // a shared-memory hash table, so a tile costs one global atomic per batch
 // however many of the batch's points it holds (scanner-ordered inputs put
 // whole batches into one tile: pillars, walls).
-constexpr int kPPT = 1;      // points per thread per batch (4 measured slower)
-constexpr int kHash = 512;   // slots (power of 2, >= 2 x batch)
+#ifndef PCT_PPT_COUNT
+#define PCT_PPT_COUNT 4
+#endif
+#ifndef PCT_PPT_SCATTER
+#define PCT_PPT_SCATTER 1
+#endif
+// points per thread per batch: the count pass merges 1024-point batches
+// (cfg3 1.44 ms at 256, 1.08 at 512, 1.00 at 1024: fewer barriers and
+// global atomics per point); the scatter pass keeps 256 (512: no gain);
+// slots = power of 2 >= 2 x batch
+template <bool SCATTER>
+struct TilePass {
+  static constexpr int PPT = SCATTER ? PCT_PPT_SCATTER : PCT_PPT_COUNT;
+  static constexpr int HASH = 512 * PPT;
+};
 constexpr int kCtrPad = 32;  // tile counters / cursors: one per 128-byte line
 #ifndef PCT_TILE_L2
 #define PCT_TILE_L2 4
@@ -307,6 +320,7 @@ __global__ void __launch_bounds__(256) tile_pass_kernel(const T *__restrict__ xy
                                                         unsigned long long *__restrict__ recs,
                                                         unsigned long long *outside) {
   extern __shared__ double hsm[];
+  constexpr int kPPT = TilePass<SCATTER>::PPT, kHash = TilePass<SCATTER>::HASH;
   __shared__ int h_tile[kHash];
   __shared__ unsigned h_cnt[kHash];
   const bool staged = a.S <= kMaxStagedHeights;
