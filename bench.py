@@ -3,35 +3,49 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl b200|reference]
 
 One "step" = one pass of the hot path (the whole SURVEY.md §8 path, simplify
-included) over synthetic maps of BASELINE.json config C, inputs resident in
-HBM.  Prints ONE JSON line (rank 0).  Modes (by config, --mode overrides):
+included) over synthetic maps of BASELINE.json config C (default 3: the
+200M-point campus the metric is quoted on), inputs resident in HBM.  Prints
+ONE JSON line (rank 0).  Modes (by config, --mode overrides):
 
-  replica  (configs 0-2, default config 1 = 5M points): every rank processes
-           its own independently seeded map, no data-path collective
-           ("batches of independent maps are distributed without
-           communication"); scaling "weak".
-  sharded  (config 3, 200M points): ONE map split into row bands over the
-           ranks (device partition + NCCL all-to-all of points, halo rows by
-           NCCL send/recv, any()-tables all-reduced for simplify); "strong".
+  sharded  (config 3, default): ONE map.  N = 1: the single-GPU library call
+           (pct_tomo_run).  N > 1: row bands over the ranks (device partition
+           + NCCL all-to-all of points, NCCL halo rows, any()-tables
+           all-reduced for simplify, surviving slices gathered on rank 0);
+           every rank draws only its own share of the cloud.  "strong".
+  replica  (configs 0-2): every rank processes its own independently seeded
+           map, no data-path collective; scaling "weak".
   batch    (config 4): 256 independent 250k-point maps split over the ranks,
            each rank runs its share per step; value also as maps/s; "strong".
+
+``--gpus N`` without torchrun re-launches this script under
+``torch.distributed.run`` with N ranks (127.0.0.1); under torchrun,
+WORLD_SIZE must equal N.
 
 Timing: W warm-up steps (and >= 0.5 s so clocks ramp), then K steps each
 bracketed by CUDA events on the library's stream; L2 flushed (256 MiB write)
 between steps outside the events; barrier + synchronize around the timed
-region; max over ranks.  --impl reference times the reference algorithm's CPU
-implementation (the numpy port in oracle/, pinned to the reference's outputs;
-the reference package cannot travel to the GPU box) on all host threads,
-rank 0 only, on the same map (configs 2-3: a bounded crop, stated).
+region; max over ranks.  ``e2e``: the same metric through the public API with
+host buffers (pinned float32 points in, every surviving layer in host numpy
+arrays out, both copies inside the timed region).  ``parity``: the benched
+map's outputs checked against the CPU port in the same run (all slices
+bitwise, keep list, the reference bench's archive checksum).
+
+--impl reference times the reference algorithm's CPU implementation -- the
+multi-threaded C port in oracle/ (pinned to the reference's outputs by the
+golden fixtures; the reference package itself cannot travel to the GPU box)
+-- on all host threads, rank 0 only, on the SAME full map per step.
 """
 
 from __future__ import annotations
 
 import argparse
 import ctypes as C
+import hashlib
 import json
 import os
+import socket
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -47,6 +61,9 @@ from paper_2403_07631_b200 import synth  # noqa: E402
 METRIC = "tomogram build+eval ms/map & Mpts/s at 1/2/4/8 B200; % HBM peak; vs CPU ref"
 L2_FLUSH_BYTES = 256 << 20
 MODES = {0: "replica", 1: "replica", 2: "replica", 3: "sharded", 4: "batch"}
+# the CPU T=1 figure's bounded sample of config 3: one full-density building
+# (the region of tests/golden/golden_r2.json "campus_crop")
+CAMPUS_T1_BOX = (126.0, 126.0, 174.0, 174.0)
 
 
 def parse():
@@ -54,13 +71,14 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--mode", choices=["replica", "sharded", "batch"], default=None)
     ap.add_argument("--points", type=int, default=None, help="override the config's N")
     ap.add_argument("--maps", type=int, default=None, help="config 4: total maps (default 256)")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--profile", action="store_true", help="1 warm-up + 1 step, no extras (ncu)")
     a = ap.parse_args()
     a.mode = a.mode or MODES[a.config]
@@ -70,6 +88,29 @@ def parse():
 def dist_env():
     return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
             int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def maybe_spawn(args):
+    """--gpus N outside torchrun: re-run under torch.distributed.run with N
+    ranks.  Under torchrun the world size must be N.  Returns an exit code
+    when this process should not run the bench itself."""
+    ws = os.environ.get("WORLD_SIZE")
+    if ws is None:
+        if args.gpus <= 1:
+            return None
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+        s.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+               f"--master-port={port}", str(Path(__file__).resolve())] + sys.argv[1:]
+        return subprocess.call(cmd)
+    if int(ws) != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}; launch with matching "
+              "--nproc-per-node", file=sys.stderr)
+        return 2
+    return None
 
 
 def peaks():
@@ -146,41 +187,21 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# CPU side: the reference algorithm (oracle port) on host cores
+# workload
 
-def cpu_pipeline(xyz, cfg, threads):
-    import oracle
-    from paper_2403_07631_b200.traversability import TravParams
-    params = TravParams()
-    t0 = time.perf_counter()
-    t = oracle.build(xyz, cfg["d_s"], cfg["r_g"], threads=threads)
-    t1 = time.perf_counter()
-    cost = oracle.evaluate(t["ground"], t["ceiling"], cfg["r_g"], params, threads=threads)
-    t2 = time.perf_counter()
-    keep = oracle.simplify(t["ground"], cost)
-    t3 = time.perf_counter()
-    return (t3 - t0), dict(build=t1 - t0, evaluate=t2 - t1, simplify=t3 - t2), len(keep)
+def n_points(args, cfg):
+    return args.points or cfg["n_points"]
 
 
-def cpu_sample(xyz, cfg, max_points=5_000_000):
-    """The bounded CPU sample: the whole map if it has <= max_points points,
-    else the points of a corner square of the map holding about max_points."""
-    n = len(xyz)
-    if n <= max_points:
-        return xyz, "full map"
-    frac = max_points / n
-    lo = xyz.min(axis=0)
-    hi = xyz.max(axis=0)
-    side = np.sqrt(frac) * (hi[:2] - lo[:2])
-    m = (xyz[:, 0] < lo[0] + side[0]) & (xyz[:, 1] < lo[1] + side[1])
-    sub = np.ascontiguousarray(xyz[m])
-    return sub, f"corner crop {side[0]:.0f} x {side[1]:.0f} m ({len(sub)} of {n} points)"
+def full_map(args, cfg):
+    """The whole (single) map of a config (rank 0's map in replica mode)."""
+    return synth.generate(args.config, n_points(args, cfg), cfg["seed"])
 
 
 def workload(args, rank, world):
-    """(cfg, list of per-rank maps (xyz arrays), description)."""
+    """(cfg, list of this rank's maps (xyz arrays), description)."""
     cfg = dict(synth.CONFIGS[args.config])
-    n = args.points or cfg["n_points"]
+    n = n_points(args, cfg)
     if args.mode == "replica":
         seed = cfg["seed"] + rank
         return cfg, [synth.generate(args.config, n, seed)], f"seed {seed}"
@@ -189,7 +210,11 @@ def workload(args, rank, world):
         mine = list(range(rank, total, world))
         return cfg, [synth.generate(4, n, cfg["seed"] + m) for m in mine], \
             f"maps {total} (seeds {cfg['seed']}+m), {len(mine)} on this rank"
-    # sharded: every rank draws the same map and keeps every world-th point
+    if world == 1:
+        return cfg, [synth.generate(args.config, n, cfg["seed"])], f"seed {cfg['seed']}"
+    if args.config == 3:  # every rank draws only its share of the surfaces
+        return cfg, [synth.campus(n, cfg["seed"], share=(rank, world))], \
+            f"seed {cfg['seed']}, surfaces i % {world} == {rank} on rank {rank}"
     xyz = synth.generate(args.config, n, cfg["seed"])
     return cfg, [np.ascontiguousarray(xyz[rank::world])], f"seed {cfg['seed']}, 1/{world} points"
 
@@ -206,8 +231,62 @@ def make_config(args, cfg, world, total_pts, R, Cc, S, keep, desc, maps_per_rank
             "l2": f"flushed between steps ({L2_FLUSH_BYTES >> 20} MiB write), "
                   "flush excluded from step time",
             "parallelism": {"replica": f"{world} independent maps (one per GPU)",
-                            "sharded": f"1 map in {world} row bands (NCCL)",
+                            "sharded": (f"1 map in {world} row bands (NCCL), gathered on rank 0"
+                                        if world > 1 else "1 map on 1 GPU"),
                             "batch": f"{maps_per_rank} maps per GPU x {world}"}[args.mode]}
+
+
+# ---------------------------------------------------------------------------
+# CPU side: the reference algorithm (C port in oracle/) on host cores
+
+def cpu_pipeline(xyz, cfg, threads):
+    """build -> evaluate -> simplify with the C port; (seconds, stages, (t, cost, keep))."""
+    from oracle import fast
+    from paper_2403_07631_b200.traversability import TravParams
+    params = TravParams()
+    t0 = time.perf_counter()
+    t = fast.build(xyz, cfg["d_s"], cfg["r_g"], threads=threads)
+    t1 = time.perf_counter()
+    cost = fast.evaluate(t["ground"], t["ceiling"], cfg["r_g"], params, threads=threads)
+    t2 = time.perf_counter()
+    keep = fast.simplify(t["ground"], cost, threads=threads)
+    t3 = time.perf_counter()
+    return (t3 - t0), dict(build=t1 - t0, evaluate=t2 - t1, simplify=t3 - t2), (t, cost, keep)
+
+
+def cpu_t1_sample(args, cfg, xyz):
+    """The bounded sample the single-thread figure is measured on."""
+    if args.config == 3:
+        sub = synth.campus(n_points(args, cfg), cfg["seed"], box=CAMPUS_T1_BOX)
+        return sub, (f"crop {CAMPUS_T1_BOX} of the full map ({len(sub)} pts, one building "
+                     "at full density)")
+    if len(xyz) > 5_000_000:
+        n = 5_000_000
+        return np.ascontiguousarray(xyz[:n]), f"first {n} of {len(xyz)} points"
+    return xyz, "full map"
+
+
+def lga_sha256(ground, ceiling, cost, heights, origin, r_g, z_min, d_s):
+    """sha256 (16 hex) of the LGA archive bytes of a tomogram given as layer
+    lists -- the determinism checksum of the reference's bench
+    (tomoplan/bench.py:58-62; format tomogram.py:219-244) -- streamed, without
+    building the archive in memory."""
+    from oracle.archive import HEADER, SLICE
+    h = hashlib.sha256(HEADER.pack(b"LGA1", 1, ground[0].shape[0], ground[0].shape[1],
+                                   np.float32(r_g), float(origin[0]), float(origin[1]),
+                                   float(z_min), np.float32(d_s), len(ground)))
+    for k in range(len(ground)):
+        h.update(SLICE.pack(float(heights[k]), 1 | 2 | 4))
+        for layer in (ground[k], ceiling[k], cost[k]):
+            h.update(memoryview(np.ascontiguousarray(layer, "<f4")).cast("B"))
+    return h.hexdigest()[:16]
+
+
+def tomogram_checksum(tom):
+    s = tom.slices
+    return lga_sha256([x.ground.values for x in s], [x.ceiling.values for x in s],
+                      [x.cost.values for x in s], [x.plane_height for x in s], tom.origin,
+                      tom.resolution, tom.z_min, tom.d_s)
 
 
 def run_reference(args):
@@ -215,15 +294,13 @@ def run_reference(args):
     if rank != 0:
         return 0
     cfg = dict(synth.CONFIGS[args.config])
-    n = args.points or cfg["n_points"]
-    if args.config == 4:
-        maps = [synth.generate(4, n, cfg["seed"] + m) for m in range(2)]
-        desc = "2 of the batch maps per step (extrapolated per map)"
+    if args.mode == "batch":
+        total = args.maps or cfg.get("n_maps", 256)
+        maps = [synth.generate(4, n_points(args, cfg), cfg["seed"] + m) for m in range(total)]
+        desc = f"all {total} maps per step"
     else:
-        full = synth.generate(args.config, n, cfg["seed"])
-        sub, how = cpu_sample(full, cfg)
-        maps, desc = [sub], how
-        del full
+        maps = [full_map(args, cfg)]
+        desc = "full map"
     threads = os.cpu_count() or 1
     for _ in range(args.warmup):
         for xyz in maps:
@@ -234,36 +311,36 @@ def run_reference(args):
         t = 0.0
         st = {"build": 0.0, "evaluate": 0.0, "simplify": 0.0}
         for xyz in maps:
-            dt, s, kept = cpu_pipeline(xyz, cfg, threads)
+            dt, s, (tt, cost, keep) = cpu_pipeline(xyz, cfg, threads)
+            kept = len(keep)
             t += dt
             for k in st:
                 st[k] += s[k]
         times.append(t)
         stages.append(st)
+    S, R, Cc = tt["ground"].shape
     pts = sum(len(x) for x in maps)
-    import oracle
-    fr = oracle.frame(*oracle.bounds(maps[-1]), cfg["d_s"], cfg["r_g"])
-    # the B200 arm's config for the same workload (one map per step here; a
-    # bounded sample of it when the map is too large for the host, noted)
-    ref_config = make_config(args, cfg, 1, len(maps[-1]), fr["rows"], fr["cols"],
-                             len(fr["heights"]), kept, f"seed {cfg['seed']}", len(maps),
+    ref_config = make_config(args, cfg, world, pts if args.mode != "batch" else len(maps[0]),
+                             R, Cc, S, kept, f"seed {cfg['seed']}", len(maps),
                              "bounds+build+evaluate+simplify, host-resident points (CPU)")
     ref_config["l2"] = "not applicable (host caches)"
-    if desc != "full map":
-        ref_config["cpu_sample"] = desc
+    ref_config["cpu_sample"] = desc
     ms = 1e3 * statistics.mean(times)
     mpts = pts / (ms * 1e3)
     line = {
         "impl": "reference", "metric": METRIC, "value": mpts, "unit": "Mpts/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic",
-        "config": ref_config,
+        "n_gpus": world, "cpu_processes": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak" if args.mode == "replica" else "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic", "config": ref_config,
         "stages_ms": {k: 1e3 * statistics.mean(s[k] for s in stages) for k in stages[0]},
         "cpu_baseline": {"value": mpts, "unit": "Mpts/s", "cores": threads, "kind": "port",
-                         "sample": f"{desc}; build+evaluate+simplify per step; {cpu_model()}"},
+                         "sample": f"{desc}; build+evaluate+simplify per step; multi-threaded "
+                                   f"C port of the reference path (oracle/c); {cpu_model()}"},
         "e2e": {"value": mpts, "unit": "Mpts/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if args.mode == "batch":
+        line["maps_per_s"] = len(maps) / (ms * 1e-3)
     print(json.dumps(line), flush=True)
     return 0
 
@@ -316,10 +393,10 @@ class Pipeline:
         return (e0, e1), list(ms)
 
     def run(self, dxyz, n):
+        """Stage by stage, keeping the stacks (the parity check's GPU side)."""
         from paper_2403_07631_b200.tomogram import new_device_stack
         _lib, lib, h, ctx = self._lib, self.lib, self.h, self.ctx
         d_s, r_g = self.cfg["d_s"], self.cfg["r_g"]
-        e0 = self.ev()
         lo = np.empty(3)
         hi = np.empty(3)
         ctx.check(lib.pct_bounds(h, dxyz.ptr, n, _lib.PCT_F32, lo.ctypes.data, hi.ctypes.data),
@@ -332,20 +409,30 @@ class Pipeline:
         g = new_device_stack(ctx, S, R, Cc)
         c = new_device_stack(ctx, S, R, Cc)
         cost = new_device_stack(ctx, S, R, Cc)
-        e1 = self.ev()
         ctx.check(lib.pct_build(h, dxyz.ptr, n, _lib.PCT_F32, C.byref(fr), hts.ctypes.data,
                                 g.ptr, c.ptr), "build")
-        e2 = self.ev()
         ctx.check(lib.pct_evaluate(h, g.ptr, c.ptr, S, R, Cc, r_g, C.byref(self.pc),
                                    self.w.ctypes.data, self.w.shape[0], cost.ptr), "evaluate")
-        e3 = self.ev()
         keep = np.empty(S, np.int32)
         nk = C.c_int32()
         ctx.check(lib.pct_simplify(h, g.ptr, cost.ptr, S, R, Cc, 1e-6, 50.0, keep.ctypes.data,
                                    C.byref(nk)), "simplify")
-        e4 = self.ev()
-        self.info = dict(S=S, R=R, C=Cc, keep=int(nk.value), stacks=(g, c, cost))
-        return [e0, e1, e2, e3, e4]
+        return dict(S=S, R=R, C=Cc, keep=[int(k) for k in keep[:nk.value]], stacks=(g, c, cost),
+                    heights=hts[:S].copy())
+
+
+def all_max(x, local):
+    import torch
+    t = torch.tensor([float(x)], device=f"cuda:{local}", dtype=torch.float64)
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return float(t.item())
+
+
+def all_sum(x, local):
+    import torch
+    t = torch.tensor([float(x)], device=f"cuda:{local}", dtype=torch.float64)
+    torch.distributed.all_reduce(t)
+    return float(t.item())
 
 
 def run_b200(args):
@@ -367,8 +454,9 @@ def run_b200(args):
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=f"cuda:{local}")
     pipe = Pipeline(ctx, stream, cfg)
     n_local = sum(len(m) for m in maps)
+    banded = args.mode == "sharded" and world > 1
 
-    if args.mode == "sharded":
+    if banded:
         dmaps = [torch.from_numpy(maps[0]).to(f"cuda:{local}")]
     else:
         dmaps = [_lib.DeviceBuffer.from_host(ctx, m) for m in maps]
@@ -400,19 +488,19 @@ def run_b200(args):
             bctx.check(bctx.lib.pct_last_stage_ms(bctx.h, st), "stage_ms")
             return {"total": [(e0, e1)], "bounds+build": [float(st[0])],
                     "evaluate": [float(st[1])], "simplify": [float(st[2])]}
-        if args.mode == "sharded":
+        if banded:
             evs = {}
             with torch.cuda.stream(stream):
                 e0 = pipe.ev()
                 gen = sharded.band_pipeline(dmaps[0], d_s, r_g, pct.TravParams(), rank, world,
-                                            device=local, events=evs)
-                res = sharded.run_torch(gen) if world > 1 else sharded.run_virtual([gen])[0]
+                                            device=local, events=evs, gather_to=0)
+                res = sharded.run_torch(gen)
                 e1 = pipe.ev()
             band_info.update(S=len(res.heights), R=res.rows, C=res.cols, keep=len(res.keep),
                              nrows=res.nrows, res=res, cs_band=evs["cell_slices"])
             ea, eb = evs["evaluate"]
             # build = bounds .. evaluate start (incl. point exchange and halo
-            # exchange when sharded), simplify = evaluate end .. step end
+            # exchange), simplify = evaluate end .. step end (incl. the gather)
             return {"total": [(e0, e1)], "bounds+build": [(e0, ea)], "evaluate": [(ea, eb)],
                     "simplify": [(eb, e1)]}
         out = {"bounds+build": [], "evaluate": [], "simplify": [], "total": []}
@@ -438,6 +526,7 @@ def run_b200(args):
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
+
     def all_launches():  # the batch runner's worker contexts launch the batch's kernels
         return ctx.launches + (sum(c.launches for c in runner.ctxs) if runner is not None else 0)
 
@@ -461,19 +550,16 @@ def run_b200(args):
     step_ms = sum(per["total"])  # device time of the K steps on this rank
     total_pts = float(n_local)
     if world > 1:
-        t = torch.tensor([step_ms], device=f"cuda:{local}", dtype=torch.float64)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        step_ms = float(t.item())
-        cnt = torch.tensor([total_pts], device=f"cuda:{local}", dtype=torch.float64)
-        torch.distributed.all_reduce(cnt)
-        total_pts = float(cnt.item())
+        step_ms = all_max(step_ms, local)
+        total_pts = all_sum(total_pts, local)
+        launches = int(all_sum(launches, local))
     ms = step_ms / args.steps
     value = total_pts * args.steps / (step_ms * 1e3)  # Mpts/s, whole job
 
     if args.mode == "batch":
         runner.close()
         pipe.run_native(dmaps[0], len(maps[0]))  # grid of map 0 for the line (untimed)
-    info = band_info if args.mode == "sharded" else pipe.info
+    info = band_info if banded else pipe.info
     S, R, Cc = info["S"], info["R"], info["C"]
     cs = S * R * Cc
     peak, peak_src = peaks()
@@ -482,8 +568,10 @@ def run_b200(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "strong" if args.mode != "replica" else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": make_config(args, cfg, world, total_pts, R, Cc, S, info["keep"], desc,
-                              len(maps), "bounds+build+evaluate+simplify, device-resident points"),
+        "config": make_config(args, cfg, world, total_pts if args.mode != "batch" else
+                              len(maps[0]), R, Cc, S, info["keep"], desc, len(maps),
+                              "bounds+build+evaluate+simplify, device-resident points" +
+                              (" (+ gather of the surviving slices on rank 0)" if banded else "")),
         "stages_ms": {k: statistics.mean(v) for k, v in per.items()},
         "wall_s_timed_region": t_wall,
         "gpu_launches": launches,
@@ -492,111 +580,234 @@ def run_b200(args):
     if args.mode == "batch":
         line["maps_per_s"] = len(maps) * world * args.steps / (step_ms * 1e-3)
     ev_ms = statistics.mean(per["evaluate"]) / len(maps)
-    n_map = n_local / len(maps)
-    # sharded: this rank's band (own rows + halo rows it evaluates)
-    cs_eval = info["cs_band"] if args.mode == "sharded" else cs
+    n_map = total_pts if args.mode != "batch" else n_local / len(maps)
+    # banded: this rank's band (own rows + halo rows it evaluates)
+    cs_eval = info["cs_band"] if banded else cs
     achieved = 12.0 * cs_eval / (ev_ms * 1e-3) / 1e9
     traffic = None
     prof = ROOT / "profiles" / "ncu_traffic.json"
-    if prof.exists():
+    if prof.exists() and not banded:
         try:
             traffic = json.loads(prof.read_text()).get(f"cfg{args.config}", {}).get(
                 "eval_dram_bytes")
         except Exception:
             traffic = None
-    if args.mode == "sharded" and world > 1:
-        traffic = None  # the recorded capture is of the one-GPU band
     line["algorithmic_bytes_per_map"] = 12 * n_map + 28 * cs
-    line["pipeline_gbs_per_gpu"] = (12 * n_map + 28 * cs_eval) * len(maps) / (
-        step_ms / args.steps * 1e-3) / 1e9
-    line["roofline"] = {"kernel": "evaluate stage (terrain walk + resolve/inflate launches)", "bound": "hbm",
-                        "achieved": achieved, "peak": peak, "unit": "GB/s",
+    line["pipeline_gbs_per_gpu"] = (12 * n_map + 28 * cs) * (len(maps) if args.mode == "batch"
+                                                             else 1) / (ms * 1e-3) / 1e9 / (
+        world if args.mode == "sharded" else 1)
+    line["roofline"] = {"kernel": "evaluate stage (terrain walk + resolve/inflate launches)",
+                        "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                         "frac": achieved / peak, "traffic": traffic,
                         "algorithmic": f"12 B per cell-slice x {cs_eval} cell-slices per launch",
                         "peak_source": peak_src}
 
-    # ---- e2e through the public API with host buffers (replica mode)
-    if args.mode == "replica" and not args.no_e2e and not args.profile:
-        xyz = maps[0]
-        pin = _lib.PinnedBuffer(ctx, xyz.shape, np.float32)
-        pin.array[...] = xyz
-        cloud = pct.PointCloud(pin.array)
-        params = pct.TravParams()
-        e2e_times = []
-        d2h = 0
-        for i in range(args.warmup + args.steps):
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            tom = pct.build_tomogram(cloud, d_s, r_g)
-            evt = pct.evaluate_tomogram(tom, params)
-            simp = pct.simplify_tomogram(evt).materialize()
-            for s in simp.slices:  # the caller reads every surviving layer
-                _ = s.ground.values, s.ceiling.values, s.cost.values
-            t1 = time.perf_counter()
-            if i >= args.warmup:
-                e2e_times.append(t1 - t0)
-            d2h = 3 * 4 * R * Cc * len(simp.slices)
-            del tom, evt, simp
-        e2e_s = statistics.mean(e2e_times)
-        if world > 1:
-            t = torch.tensor([e2e_s], device=f"cuda:{local}", dtype=torch.float64)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            e2e_s = float(t.item())
-        seq = {"value": total_pts / (e2e_s * 1e6), "unit": "Mpts/s", "ms_per_step": 1e3 * e2e_s,
-               "path": "PointCloud(pinned f32) -> build_tomogram -> evaluate_tomogram -> "
-                       "simplify_tomogram -> host arrays of surviving slices, one map at a time"}
-        # the same maps through the streaming entry point: up to two maps in
-        # flight, so one map's upload overlaps the previous one's read-back
-        from paper_2403_07631_b200.batch import BatchRunner, stream_maps
-        srun = BatchRunner(local, workers=2)
-        # warm-up maps until the pinned read-back pool holds every block the
-        # steady state needs (page-locking new host memory stalls the device)
-        for tom in stream_maps([pin.array] * max(args.warmup, 8), d_s, r_g, params, runner=srun):
-            pass
-        del tom
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        d2h_s = 0
-        for tom in stream_maps([pin.array] * args.steps, d_s, r_g, params, runner=srun):
-            for s in tom.slices:
-                d2h_s += s.ground.values.nbytes + s.ceiling.values.nbytes + s.cost.values.nbytes
-            del tom
-        st_s = (time.perf_counter() - t0) / args.steps
-        srun.close()
-        if world > 1:
-            t = torch.tensor([st_s], device=f"cuda:{local}", dtype=torch.float64)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            st_s = float(t.item())
-        streamed = {"value": total_pts / (st_s * 1e6), "unit": "Mpts/s", "ms_per_step": 1e3 * st_s,
-                    "path": "stream_maps(pinned f32 clouds, 2 in flight) -> simplified "
-                            "tomograms with every surviving layer in host memory"}
-        # the faster of the two public entry points is the e2e number (small
-        # maps: the one-at-a-time path; large: the streamed one), the other
-        # is reported beside it
-        best, other = (streamed, seq) if streamed["value"] >= seq["value"] else (seq, streamed)
-        line["e2e"] = dict(best, h2d_bytes_per_step=12 * len(xyz),
-                           d2h_bytes_per_step=d2h_s // args.steps,
-                           alternative=other)
+    # ---- e2e through the public API with host buffers
+    last_tom = None
+    if not args.no_e2e and not args.profile:
+        e2e, last_tom = run_e2e(args, cfg, maps, ctx, local, rank, world, R, Cc)
+        line["e2e"] = e2e
 
-    # ---- CPU baseline (rank 0, N=1 only): the reference algorithm on host cores
-    if rank == 0 and world == 1 and not args.no_cpu and not args.profile:
+    # ---- CPU baseline (rank 0, N=1 only) and same-run parity (rank 0)
+    cpu_res = None
+    if rank == 0 and not args.profile and args.mode != "batch" and \
+            (not args.no_parity or (world == 1 and not args.no_cpu)):
+        xyz_full = maps[0] if (world == 1 or args.mode == "replica") else full_map(args, cfg)
         threads = os.cpu_count() or 1
-        sub, how = cpu_sample(maps[0], cfg)
-        t, st, _ = cpu_pipeline(sub, cfg, threads)
-        line["cpu_baseline"] = {"value": len(sub) / (t * 1e6), "unit": "Mpts/s",
-                                "cores": threads, "kind": "port",
-                                "sample": f"{how} of cfg{args.config} (build+evaluate+simplify, "
-                                          f"{t:.1f} s), {cpu_model()}",
-                                "stages_s": st}
+        t, st, cpu_res = cpu_pipeline(xyz_full, cfg, threads)
+        if world == 1 and not args.no_cpu:
+            t1_xyz, t1_desc = cpu_t1_sample(args, cfg, xyz_full)
+            t1, _, _ = cpu_pipeline(t1_xyz, cfg, 1)
+            line["cpu_baseline"] = {
+                "value": len(xyz_full) / (t * 1e6), "unit": "Mpts/s", "cores": threads,
+                "kind": "port",
+                "sample": f"full map of cfg{args.config} (build+evaluate+simplify, {t:.2f} s), "
+                          f"multi-threaded C port of the reference path (oracle/c), {cpu_model()}",
+                "stages_s": st,
+                "single_thread": {"value": len(t1_xyz) / (t1 * 1e6), "unit": "Mpts/s",
+                                  "cores": 1, "seconds": t1, "sample": t1_desc}}
+        del xyz_full
+    elif rank == 0 and args.mode == "batch" and world == 1 and not args.no_cpu and \
+            not args.profile:
+        threads = os.cpu_count() or 1
+        t0 = time.perf_counter()
+        for m in maps[:16]:
+            cpu_pipeline(m, cfg, threads)
+        t = time.perf_counter() - t0
+        line["cpu_baseline"] = {"value": sum(len(m) for m in maps[:16]) / (t * 1e6),
+                                "unit": "Mpts/s", "cores": threads, "kind": "port",
+                                "sample": f"16 of the batch maps, C port (oracle/c), {cpu_model()}"}
+    if not args.no_parity and not args.profile and args.mode != "batch":
+        par = parity(args, cfg, cpu_res, pipe, dmaps, maps, last_tom, rank, world, banded,
+                     band_info)
+        if rank == 0:
+            line["parity"] = par
+    rc = 0
     if rank == 0:
         print(json.dumps(line), flush=True)
+        if "parity" in line and not line["parity"]["ok"]:
+            print("bench.py: PARITY FAILURE against the CPU port: " + json.dumps(line["parity"]),
+                  file=sys.stderr)
+            rc = 1
     if world > 1:
         torch.distributed.destroy_process_group()
-    return 0
+    return rc
+
+
+def run_e2e(args, cfg, maps, ctx, local, rank, world, R, Cc):
+    """The metric end to end through the public API with host buffers: every
+    step uploads this rank's pinned float32 points and reads every surviving
+    layer back into host numpy arrays (inside the timed region)."""
+    import torch
+
+    import paper_2403_07631_b200 as pct
+    from paper_2403_07631_b200 import _lib, sharded
+    d_s, r_g = cfg["d_s"], cfg["r_g"]
+    params = pct.TravParams()
+    pins = []
+    for m in maps:
+        pin = _lib.PinnedBuffer(ctx, m.shape, np.float32)
+        pin.array[...] = m
+        pins.append(pin)
+    clouds = [pct.PointCloud(p.array) for p in pins]  # validation outside the timer
+    h2d = sum(12 * len(m) for m in maps)
+    banded = args.mode == "sharded" and world > 1
+
+    def one_step():
+        if args.mode == "batch":
+            from paper_2403_07631_b200.batch import stream_maps
+            d2h, last = 0, None
+            for tom in stream_maps([p.array for p in pins], d_s, r_g, params, device=local):
+                for s in tom.slices:
+                    d2h += s.ground.values.nbytes + s.ceiling.values.nbytes + s.cost.values.nbytes
+                last = tom
+            return d2h, last
+        if banded:
+            tom = sharded.tomogram_sharded(clouds[0], d_s, r_g, params, root=0, device=local)
+        else:
+            tom = pct.simplify_tomogram(pct.evaluate_tomogram(
+                pct.build_tomogram(clouds[0], d_s, r_g, device=local), params))
+        if tom is None:
+            return 0, None
+        tom.materialize()
+        d2h = 0
+        for s in tom.slices:  # the caller reads every surviving layer
+            d2h += s.ground.values.nbytes + s.ceiling.values.nbytes + s.cost.values.nbytes
+        return d2h, tom
+
+    times = []
+    tom = None
+    d2h = 0
+    for i in range(args.warmup + args.steps):
+        del tom
+        tom = None
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        t0 = time.perf_counter()
+        d2h, tom = one_step()
+        t1 = time.perf_counter()
+        if i >= args.warmup:
+            times.append(t1 - t0)
+    e2e_s = statistics.mean(times)
+    total = float(sum(len(m) for m in maps))
+    if world > 1:
+        e2e_s = all_max(e2e_s, local)
+        total = all_sum(total, local)
+        h2d = int(all_sum(h2d, local))
+        d2h = int(all_sum(d2h, local))
+    path = {"batch": "stream_maps(pinned f32 clouds, 2 in flight) -> simplified tomograms, "
+                     "every surviving layer in host memory",
+            "sharded": ("tomogram_sharded(pinned f32 share per rank) -> simplified Tomogram "
+                        "gathered on rank 0 -> every surviving layer in host memory")
+            if banded else None,
+            "replica": None}[args.mode] or (
+        "PointCloud(pinned f32) -> build_tomogram -> evaluate_tomogram -> simplify_tomogram "
+        "-> every surviving layer in host memory (the reference's drop-in chain)")
+    out = {"value": total / (e2e_s * 1e6), "unit": "Mpts/s", "ms_per_step": 1e3 * e2e_s,
+           "path": path, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+           "timing": "wall clock per step (host copies included), max over ranks"}
+    if args.mode == "replica" and world == 1 and len(maps[0]) <= 20_000_000:
+        out["streamed"] = streamed_e2e(args, cfg, pins[0], local, total)
+    return out, tom
+
+
+def streamed_e2e(args, cfg, pin, local, total):
+    """stream_maps over the same pinned cloud (two maps in flight: one map's
+    upload overlaps the previous map's read-back): a repo extension, not the
+    reference's call sequence, reported beside the drop-in e2e."""
+    import torch
+
+    import paper_2403_07631_b200 as pct
+    from paper_2403_07631_b200.batch import BatchRunner, stream_maps
+    params = pct.TravParams()
+    srun = BatchRunner(local, workers=2)
+    tom = None
+    for tom in stream_maps([pin.array] * max(args.warmup, 8), cfg["d_s"], cfg["r_g"], params,
+                           runner=srun):
+        pass
+    del tom
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for tom in stream_maps([pin.array] * args.steps, cfg["d_s"], cfg["r_g"], params,
+                           runner=srun):
+        for s in tom.slices:
+            _ = s.ground.values, s.ceiling.values, s.cost.values
+        del tom
+    st_s = (time.perf_counter() - t0) / args.steps
+    srun.close()
+    return {"value": total / (st_s * 1e6), "unit": "Mpts/s", "ms_per_step": 1e3 * st_s,
+            "path": "stream_maps(pinned f32 clouds, 2 in flight), a repo extension"}
+
+
+def parity(args, cfg, cpu_res, pipe, dmaps, maps, tom, rank, world, banded, band_info):
+    """The benched map's GPU outputs against the CPU port (same run).
+
+    N = 1 (and replica rank 0): one more untimed device pass keeping the
+    stacks: every slice of ground / ceiling / cost bitwise, the keep list,
+    plane heights.  Banded: the simplified Tomogram gathered on rank 0 (its
+    kept slices bitwise).  Both: the reference bench's archive checksum of
+    the public API's simplified tomogram against the CPU port's."""
+    if rank != 0:
+        return None
+    t, cost, keep = cpu_res
+    out = {"against": "C port of the reference path (oracle/c) on the same map"}
+    ok = True
+    if not banded:
+        g = pipe.run(dmaps[0], len(maps[0]))
+        gs, cs_, ks = (st.host_all() for st in g["stacks"])
+        out["slices_bitwise"] = {
+            "ground": bool(np.array_equal(gs.view(np.uint32), t["ground"].view(np.uint32))),
+            "ceiling": bool(np.array_equal(cs_.view(np.uint32), t["ceiling"].view(np.uint32))),
+            "cost": bool(np.array_equal(ks.view(np.uint32), cost.view(np.uint32))),
+            "n_slices": int(gs.shape[0])}
+        out["keep"] = g["keep"] == keep
+        out["heights"] = bool(np.array_equal(g["heights"], t["heights"]))
+        ok &= all(out["slices_bitwise"][k] for k in ("ground", "ceiling", "cost"))
+        ok &= out["keep"] and out["heights"]
+        del gs, cs_, ks, g
+    else:
+        res = band_info["res"]
+        out["keep"] = res.keep == keep
+        ok &= out["keep"]
+    want = lga_sha256([t["ground"][k] for k in keep], [t["ceiling"][k] for k in keep],
+                      [cost[k] for k in keep], [t["heights"][k] for k in keep], t["origin"],
+                      cfg["r_g"], t["z_min"], cfg["d_s"])
+    out["archive_sha256_16_cpu"] = want
+    if tom is not None:
+        got = tomogram_checksum(tom)
+        out["archive_sha256_16_gpu"] = got
+        out["archive_checksum"] = got == want
+        ok &= got == want
+    out["ok"] = bool(ok)
+    return out
 
 
 def main():
     args = parse()
+    rc = maybe_spawn(args)
+    if rc is not None:
+        return rc
     if args.profile:
         args.warmup, args.steps = 1, 1
     sys.path.insert(0, str(ROOT / "tests"))

@@ -76,7 +76,9 @@ const char *pct_last_error(const pct_ctx *ctx);
 int pct_sync(pct_ctx *ctx);
 /* Kernel launches issued by this context since creation (evidence counter). */
 int64_t pct_launch_count(const pct_ctx *ctx);
-/* Use an external stream (cudaStream_t as void*); NULL restores the own stream. */
+/* Use an external stream (cudaStream_t as void*); NULL restores the own stream.
+ * Work already queued on the previous stream is ordered before anything the
+ * context issues on the new one (event join). */
 int pct_set_stream(pct_ctx *ctx, void *stream);
 
 /* ---- memory helpers (device / pinned host, owned by the caller) ------- */
@@ -150,6 +152,14 @@ int pct_partition_rows(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, cons
 int pct_build_band(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, const pct_frame *fr,
                    const double *heights, int32_t row0, int32_t nrows, int64_t out_slice_stride,
                    float *ground, float *ceiling);
+/* Strided slice copy on the device (halo packing / unpacking, gathering
+   the kept slices of a band into a full-grid stack): for m < n,
+   dst[m * dst_slice_stride .. + block_elems) = src[k * src_slice_stride ..)
+   with k = slice_idx_host[m] (host array; NULL: k = m), n <= 4096.  All
+   strides and sizes in floats.  Stream-ordered, no host synchronisation. */
+int pct_copy_slices(pct_ctx *ctx, float *dst, int64_t dst_slice_stride, const float *src,
+                    int64_t src_slice_stride, const int32_t *slice_idx_host, int32_t n,
+                    int64_t block_elems);
 /* Sweep primitives for a distributed simplify (simplify.py:18-73): the any()
    table of the first pass (bit j of table[k]: below = k-1-j, j < 16; bit 32:
    no lower neighbour; upper neighbour k+1) and any() flags of explicit

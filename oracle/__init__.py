@@ -10,11 +10,15 @@ the three stages on the hot path:
   planner_ctx.py     canonical-node arrays    tomoplan/planner.py:62-93
   cloud_io.py        binary PCD payload       tomoplan/cloud_io.py:53-55,123-146
   trajectory.py      ceiling inflation        tomoplan/trajectory.py:277-317
+  fast.py + c/       build / evaluate /       the same three stages restated in
+                     simplify in C            multi-threaded C (full-size maps)
 
 Parity status: PINNED.  ``tests/golden/make_golden.py`` imports the reference
 package (only available in the build container, /root/reference) and records
 its outputs on seeded inputs as fixtures under ``tests/golden/``;
-``tests/test_oracle_golden.py`` checks this oracle bit-for-bit against them.
+``tests/test_oracle_golden.py`` checks this oracle bit-for-bit against them,
+``tests/test_oracle_c.py`` the C restatement (plus the config-3 pins of
+``golden_r2.json``, written by ``make_golden_r2.py``).
 
 Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py`` (its
 ``cpu_baseline`` leg and ``--impl reference`` arm) may import this package,

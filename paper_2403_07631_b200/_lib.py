@@ -78,6 +78,7 @@ _SIGS = {
                            C.c_int),
     "pct_build_band": ([_vp, _vp, _i64, C.c_int, C.POINTER(FrameC), _vp, _i32, _i32, _i64, _vp,
                         _vp], C.c_int),
+    "pct_copy_slices": ([_vp, _vp, _i64, _vp, _i64, _vp, _i32, _i64], C.c_int),
     "pct_simplify_window": ([_vp, _vp, _vp, _i32, _i64, _i64, _d, _d, _vp], C.c_int),
     "pct_simplify_triples": ([_vp, _vp, _vp, _i32, _i64, _i64, _d, _d, _vp, _i32, _vp], C.c_int),
     "pct_planner_context": ([_vp, _vp, _vp, _i32, _i32, _i32, _d, _vp, _vp], C.c_int),

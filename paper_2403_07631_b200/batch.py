@@ -25,6 +25,7 @@ from concurrent.futures import ThreadPoolExecutor
 import numpy as np
 
 from . import _lib
+from .cloud import source_points
 from .tomogram import GRID_SIDE_LIMIT, DeviceTomogram, Layer, Tomogram, TomogramSlice
 from .traversability import build_kernel
 
@@ -122,7 +123,7 @@ def evaluate_maps(clouds, d_s, r_g, params, *, workers=8, device=None, eps_e=1e-
         raise ValueError("d_s and r_g must be positive")
     own = runner is None
     runner = runner or BatchRunner(device, workers)
-    arrays = [np.ascontiguousarray(c.xyz if hasattr(c, "xyz") else c) for c in clouds]
+    arrays = [np.ascontiguousarray(source_points(c)) for c in clouds]
     codes = {a.dtype for a in arrays}
     if len(codes) == 1:
         # one upload per map, then the phase-batched native call
@@ -181,7 +182,7 @@ def stream_maps(clouds, d_s, r_g, params, *, workers=2, device=None, eps_e=1e-6,
     pending = []
     try:
         for c in clouds:
-            a = np.ascontiguousarray(c.xyz if hasattr(c, "xyz") else c)
+            a = np.ascontiguousarray(source_points(c))
             if a.dtype not in (np.float32, np.float64) or a.ndim != 2 or a.shape[1] != 3:
                 raise ValueError("clouds must be (N, 3) float32/float64 arrays")
             pending.append(runner.pool.submit(one, a))

@@ -7,14 +7,15 @@ file into pinned chunks and straight to HBM, where the float32 x/y/z of every
 record are gathered and the finite rows compacted in order
 (cloud_io.py:123-146 + _keep_finite :53-55).  The result is a
 :class:`DeviceCloud`, a ``PointCloud`` whose points stay in HBM;
-``build_tomogram`` consumes it in place.  ``.xyz`` copies the points to the
-host on first access (float32; the reference's float64 copy holds the same
-values because float32 -> float64 is exact).
+``build_tomogram`` consumes it in place.  ``.points`` copies the float32
+points to the host on first access, ``.xyz`` is their float64 copy (the
+reference's type; float32 -> float64 is exact).
 
 Header parsing and validation happen here on the host with the reference's
 error types and messages (cloud_io.py:92-141).  The text formats (PCD ascii,
-PLY ascii, xyz text) are not on the hot path: they are delegated to the
-reference's own parsers when ``tomoplan`` is importable.
+PLY ascii, xyz text) are not on the hot path and are not parsed here:
+``load_cloud`` raises ``CloudFormatError`` for them.  ``compat.install``
+routes them to the reference's own parsers when it patches ``tomoplan``.
 """
 
 from __future__ import annotations
@@ -87,16 +88,18 @@ class DeviceCloud(PointCloud):
     """A ``PointCloud`` whose (N, 3) float32 points live in HBM.
 
     ``len``, ``dropped`` and ``bounds`` (computed on the device) need no host
-    copy; ``xyz`` downloads the points once."""
+    copy; ``points`` downloads the float32 points once, ``xyz`` is their
+    float64 copy (as the reference stores it)."""
 
-    def __init__(self, ctx, buf, n: int, dropped: int):  # noqa: D107 (no dataclass init)
+    def __init__(self, ctx, buf, n: int, dropped: int):  # noqa: D107 (no validation pass)
         self._ctx, self._buf, self._n = ctx, buf, int(n)
         self.dropped = int(dropped)
         self._host = None
+        self._xyz64 = None
         self._bounds = None
 
     @property
-    def xyz(self) -> np.ndarray:
+    def points(self) -> np.ndarray:
         if self._host is None:
             out = np.empty((self._n, 3), np.float32)
             self._buf.to_host(out)
@@ -176,31 +179,20 @@ def pcd_records_to_device(records: np.ndarray, *, device=None) -> DeviceCloud:
                        ctx.h, rec.ctypes.data, int(n), int(dt.itemsize), offs, 1, out, nv), "")
 
 
-def _reference_loader(fmt: str):
-    try:
-        from tomoplan import cloud_io as ref  # the reference package, when installed
-    except ImportError:
-        return None
-    return ref._LOADERS.get(fmt)
-
-
 def load_cloud(path, fmt: str, *, device=None) -> PointCloud:
     """Read a point cloud (cloud_io.py:281-288); non-finite rows are dropped
-    into ``cloud.dropped``.  ``pcd_binary`` is ingested on the GPU."""
+    into ``cloud.dropped``.  Only ``pcd_binary`` (the format large maps are
+    stored in) is read here, by the device ingest; the text formats are
+    file IO before the hot path and raise ``CloudFormatError``."""
     if fmt not in FORMATS:
         raise ValueError(f"unknown format '{fmt}', expected one of {FORMATS}")
     path = Path(path)
     if not path.is_file():
         raise CloudFormatError(f"{path}: no such file")
-    if fmt == "pcd_binary":
-        return load_pcd_binary(path, device=device)
-    loader = _reference_loader(fmt)
-    if loader is None:
-        raise NotImplementedError(
-            f"format '{fmt}' is parsed by the reference's host reader (tomoplan.cloud_io); "
-            "only pcd_binary has a device ingest path here")
-    ref = loader(path)
-    return PointCloud(ref.xyz, ref.dropped)
+    if fmt != "pcd_binary":
+        raise CloudFormatError(f"{path}: format '{fmt}' has no device ingest; only pcd_binary "
+                               "is read by this package")
+    return load_pcd_binary(path, device=device)
 
 
 def sniff_format(path) -> str:

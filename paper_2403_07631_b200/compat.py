@@ -41,7 +41,8 @@ REPLACEMENTS = {
     "unique_cells": _simp.unique_cells,
     "save_tomogram": _arch.save_tomogram,   # byte-identical LGA writer (§8 f)
     "load_tomogram": _arch.load_tomogram,
-    "load_cloud": _cio.load_cloud,          # binary PCD straight to HBM (§8 f)
+    # load_cloud: a per-install dispatcher (binary PCD straight to HBM, §8 f;
+    # the text formats stay with the reference's own parsers), see install()
     "_inflate_ceiling": _traj.inflate_ceiling,  # trajectory.py:277-317 (§8 f)
 }
 
@@ -56,17 +57,40 @@ def install(package=None) -> list:
     (module, name) pairs."""
     pkg = package if package is not None else importlib.import_module("tomoplan")
     patched = []
+    repl = dict(REPLACEMENTS)
+    try:
+        ref_cio = importlib.import_module(pkg.__name__ + ".cloud_io")
+        repl["load_cloud"] = _load_cloud_dispatch(getattr(ref_cio, "load_cloud"))
+    except Exception:
+        pass
     for suffix in MODULES:
         try:
             mod = importlib.import_module(pkg.__name__ + suffix) if suffix else pkg
         except Exception:  # e.g. bench needs matplotlib
             continue
-        for name, fn in REPLACEMENTS.items():
+        for name, fn in repl.items():
             if hasattr(mod, name) and getattr(mod, name) is not fn:
                 _saved.append((mod, name, getattr(mod, name)))
                 setattr(mod, name, fn)
                 patched.append((mod.__name__, name))
     return patched
+
+
+def _load_cloud_dispatch(ref_load_cloud):
+    """``load_cloud`` for the patched package: ``pcd_binary`` goes through
+    the device ingest (this package), every other format through the
+    reference's own parser (cloud_io.py:281-288), saved at install time."""
+    if getattr(ref_load_cloud, "_pct_dispatch", False):  # installed twice
+        return ref_load_cloud
+
+    def load_cloud(path, fmt):
+        if fmt == "pcd_binary":
+            return _cio.load_cloud(path, fmt)
+        return ref_load_cloud(path, fmt)
+
+    load_cloud.__doc__ = ref_load_cloud.__doc__
+    load_cloud._pct_dispatch = True
+    return load_cloud
 
 
 def uninstall() -> None:

@@ -263,6 +263,7 @@ int pct_ctx_destroy(pct_ctx *ctx) {
   if (ctx->enc) cudaFree(ctx->enc);
   if (ctx->keys) cudaFree(ctx->keys);
   if (ctx->spec_ev) cudaEventDestroy(ctx->spec_ev);
+  if (ctx->switch_ev) cudaEventDestroy(ctx->switch_ev);
   for (auto e : ctx->ev)
     if (e) cudaEventDestroy(e);
   if (ctx->hsmall) cudaFreeHost(ctx->hsmall);
@@ -286,8 +287,17 @@ int pct_sync(pct_ctx *ctx) {
 int64_t pct_launch_count(const pct_ctx *ctx) { return ctx ? ctx->launches : 0; }
 
 int pct_set_stream(pct_ctx *ctx, void *stream) {
-  if (!ctx) return PCT_E_INVALID;
-  ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+  CTX_GUARD(ctx);
+  cudaStream_t next = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+  if (next == ctx->stream) return PCT_OK;
+  // join: work already queued on the old stream (copies out of the pinned
+  // upload ring, constant uploads, kernels writing buffers the caller reuses)
+  // is ordered before everything issued on the new one
+  if (!ctx->switch_ev)
+    PCT_CUDA(ctx, cudaEventCreateWithFlags(&ctx->switch_ev, cudaEventDisableTiming));
+  PCT_CUDA(ctx, cudaEventRecord(ctx->switch_ev, ctx->stream));
+  PCT_CUDA(ctx, cudaStreamWaitEvent(next, ctx->switch_ev, 0));
+  ctx->stream = next;
   return PCT_OK;
 }
 
@@ -591,6 +601,7 @@ int pct_tomo_run(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, int xyz_on
                  double d_s, double r_g, int64_t max_grid_side, const pct_trav_params *p,
                  const float *kernel_w, int32_t kside, double eps_e, double c_barrier,
                  pct_tomo **out, int32_t *keep_host, int32_t *n_keep) {
+  CTX_GUARD(ctx);
   if (!out || !keep_host || !n_keep) return fail(ctx, PCT_E_INVALID, "bad arguments to pct_tomo_run");
   pct_tomo *t = nullptr;
   if (ctx->timing) cudaEventRecord(ctx->ev[0], ctx->stream);

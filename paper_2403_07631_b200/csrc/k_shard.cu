@@ -81,6 +81,37 @@ __global__ void __launch_bounds__(256) band_scatter_kernel(const T *__restrict__
   }
 }
 
+// dst[m] <- src[idx[m]] for n blocks of `block` floats (slice strides in
+// floats); idx == nullptr means m.  blockIdx.y = m; 16-byte vectors when the
+// layout allows.
+constexpr int kMaxCopyIdx = 4096;
+
+struct CopyIdx {
+  int32_t idx[kMaxCopyIdx];
+};
+
+template <bool kVec>
+__global__ void __launch_bounds__(256) copy_slices_kernel(float *__restrict__ dst, int64_t dstride,
+                                                          const float *__restrict__ src,
+                                                          int64_t sstride, int64_t block,
+                                                          const CopyIdx *__restrict__ idx) {
+  const int m = blockIdx.y;
+  const int64_t k = idx ? idx->idx[m] : m;
+  float *d = dst + (int64_t)m * dstride;
+  const float *s = src + k * sstride;
+  const int64_t step = (int64_t)gridDim.x * blockDim.x;
+  if (kVec) {
+    const int64_t nv = block >> 2;
+    float4 *d4 = reinterpret_cast<float4 *>(d);
+    const float4 *s4 = reinterpret_cast<const float4 *>(s);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += step)
+      __stcs(d4 + i, __ldcs(s4 + i));
+  } else {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < block; i += step)
+      d[i] = s[i];
+  }
+}
+
 }  // namespace
 }  // namespace pct
 
@@ -139,6 +170,39 @@ int pct_partition_rows(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, cons
     PCT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));  // the offsets buffer is reused
   }
   return PCT_OK;
+}
+
+int pct_copy_slices(pct_ctx *ctx, float *dst, int64_t dst_slice_stride, const float *src,
+                    int64_t src_slice_stride, const int32_t *slice_idx_host, int32_t n,
+                    int64_t block_elems) {
+  if (!ctx) return PCT_E_INVALID;
+  if (cudaSetDevice(ctx->device) != cudaSuccess) return PCT_E_CUDA;
+  if (n < 0 || n > kMaxCopyIdx || block_elems < 0 || (n > 0 && block_elems > 0 && (!dst || !src)))
+    return fail(ctx, PCT_E_INVALID, "bad arguments to pct_copy_slices");
+  if (n == 0 || block_elems == 0) return PCT_OK;
+  const CopyIdx *didx = nullptr;
+  if (slice_idx_host) {
+    // the index list goes up through the context's small device buffer
+    // (after the 2 x 64 partition counters)
+    static_assert(sizeof(CopyIdx) + 2 * kMaxBands * 8 <= 65536, "dsmall too small");
+    CopyIdx *d = reinterpret_cast<CopyIdx *>(static_cast<char *>(ctx->dsmall) + 2 * kMaxBands * 8);
+    PCT_CUDA(ctx, upload_async(ctx, d, slice_idx_host, sizeof(int32_t) * n));
+    didx = d;
+  }
+  const bool vec = ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0 &&
+                   (dst_slice_stride & 3) == 0 && (src_slice_stride & 3) == 0 &&
+                   (block_elems & 3) == 0;
+  const int64_t work = vec ? block_elems / 4 : block_elems;
+  const unsigned gx = (unsigned)std::max<int64_t>(
+      1, std::min<int64_t>((work + 255) / 256, std::max<int64_t>(1, 4LL * ctx->num_sms / n)));
+  dim3 grid(gx, (unsigned)n);
+  if (vec)
+    copy_slices_kernel<true><<<grid, 256, 0, ctx->stream>>>(dst, dst_slice_stride, src,
+                                                            src_slice_stride, block_elems, didx);
+  else
+    copy_slices_kernel<false><<<grid, 256, 0, ctx->stream>>>(dst, dst_slice_stride, src,
+                                                             src_slice_stride, block_elems, didx);
+  return check_launch(ctx, "copy_slices_kernel");
 }
 
 int pct_build_band(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, const pct_frame *fr,

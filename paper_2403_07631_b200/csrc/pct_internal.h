@@ -44,6 +44,7 @@ struct pct_ctx {
   // keys in the second; clean = every key empty (the scan restores that)
   bool keys_clean = false;
   cudaEvent_t spec_ev = nullptr;  // bounds read back ahead of the speculative scatter
+  cudaEvent_t switch_ev = nullptr;  // pct_set_stream: old stream -> new stream join
   // zero-padded encoded c_init stacks of the split evaluation; the padding
   // is cleared only when the layout changes (the interior is rewritten)
   void *enc = nullptr;

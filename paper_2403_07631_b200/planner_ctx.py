@@ -64,42 +64,41 @@ class PlannerContext:
         keep.append(st)
         return st.ptr
 
-    # --- the reference object's lookups (planner.py:95-129), host side
+    # --- the reference object's two lookups (planner.py:95-129), answered
+    # from one column of the (K, rows, cols) arrays with vectorised numpy
+    def _cell(self, point):
+        """Grid cell of a query position (tomogram.rasterize_index rule), or None."""
+        K, nr, nc = self.elev.shape
+        col = math.floor((float(point[0]) - self.origin[0]) / self.res + 0.5)
+        row = math.floor((float(point[1]) - self.origin[1]) / self.res + 0.5)
+        return (row, col) if 0 <= row < nr and 0 <= col < nc else None
+
     def snap(self, point, tol: float):
-        """Nearest traversable node for a query position, or None."""
-        x, y, z = float(point[0]), float(point[1]), float(point[2])
-        K, R, C = self.elev.shape
-        i = math.floor((y - self.origin[1]) / self.res + 0.5)
-        j = math.floor((x - self.origin[0]) / self.res + 0.5)
-        if not (0 <= i < R and 0 <= j < C):
+        """(k0, i, j) of the traversable canonical node nearest a query
+        position, or None.  Candidates are the valid slices of the query's
+        cell within ``tol`` vertically; the winner is the smallest
+        (|dz|, cost, k) triple; it must belong to a node whose run cost is
+        below the barrier."""
+        cell = self._cell(point)
+        if cell is None:
             return None
-        best = None
-        for k in range(K):
-            if not self.valid[k, i, j]:
-                continue
-            dz = abs(float(self.elev[k, i, j]) - z)
-            if dz > tol:
-                continue
-            key = (dz, float(self.cost[k, i, j]), k)
-            if best is None or key < best[0]:
-                best = (key, k)
-        if best is None:
+        i, j = cell
+        dz = np.abs(self.elev[:, i, j].astype(np.float64) - float(point[2]))
+        ok = np.flatnonzero(self.valid[:, i, j] & (dz <= tol))
+        if ok.size == 0:
             return None
-        k0 = int(self.canon[best[1], i, j])
-        if not self.cn[k0, i, j] < self.c_barrier:
-            return None
-        return k0, i, j
+        # lexsort: last key is primary -> (dz, cost, k) ascending, first wins
+        order = np.lexsort((ok, self.cost[ok, i, j].astype(np.float64), dz[ok]))
+        k0 = int(self.canon[ok[order[0]], i, j])
+        return (k0, i, j) if self.cn[k0, i, j] < self.c_barrier else None
 
     def member_with_min_cost(self, k0, i, j):
-        K = self.elev.shape[0]
-        best_k, best_c = k0, float(self.cost[k0, i, j])
-        k = k0 + 1
-        while k < K and self.canon[k, i, j] == k0:
-            c = float(self.cost[k, i, j])
-            if c < best_c:
-                best_k, best_c = k, c
-            k += 1
-        return best_k
+        """The slice of node (k0, i, j)'s run with the lowest cost (the first
+        one on ties): the run is k0 and the slices above it whose canonical
+        index is k0."""
+        above = self.canon[k0 + 1:, i, j] != k0
+        run = int(np.argmax(above)) if above.any() else above.size
+        return k0 + int(np.argmin(self.cost[k0:k0 + 1 + run, i, j]))
 
 
 def attach_planner_context(tomogram, eps_e: float = 1e-6, c_barrier: float = 50.0):

@@ -16,7 +16,16 @@ buffers):
      stencil reaches at most R + r + 1 rows for ground and R for ceiling
   6. simplify: every rank computes the any() table / triple flags over its
      own rows; they are max-reduced and every rank replays the same sweep
-     (simplify.py:59-70), so all ranks agree on the surviving slices.
+     (simplify.py:59-70), so all ranks agree on the surviving slices
+  7. gather: the surviving slices of every band (ground, ceiling, cost) go
+     to one rank (NCCL send/recv), which assembles the full-grid stacks and
+     returns one reference-compatible Tomogram (``tomogram_sharded``).
+
+Every error that depends on the data (a non-finite point on any rank, a band
+thinner than the halo) is decided on values all ranks share, before the
+first point exchange, so all ranks raise together instead of leaving the
+others blocked in a collective.  Strided copies (halo packing, gathering)
+are libpct kernels (pct_copy_slices); torch only provides the buffers.
 
 The result is bit-identical to the single-GPU pipeline (tested with
 virtual ranks on one GPU, tests/test_gpu_sharded.py, and the collective /
@@ -144,21 +153,53 @@ class BandResult:
     ceiling: object = None
     cost: object = None
     stages_ms: dict = field(default_factory=dict)
+    # gather_to=root: the simplified tomogram assembled on the root rank
+    tomogram: object = None
 
 
 def _ptr(t, offset_elems=0):
     return t.data_ptr() + 4 * int(offset_elems)
 
 
+def check_bands(starts, H: int):
+    """Every band must be at least as thick as the halo its neighbours read
+    from it.  Decided from the shared frame on every rank alike, before any
+    point exchange, so either all ranks raise or none does."""
+    size = len(starts) - 1
+    rows = starts[-1]
+    for b in range(size):
+        nrows = starts[b + 1] - starts[b]
+        need = max(min(H, rows - starts[b]) if b > 0 else 0,          # rank b-1's bottom halo
+                   min(H, starts[b + 1]) if b + 1 < size else 0)      # rank b+1's top halo
+        if need > nrows:
+            raise ValueError(f"row band {b} has {nrows} rows, thinner than the {H}-row halo "
+                             f"its neighbours need; use fewer ranks for this {rows}-row grid")
+
+
+def _copy_slices(ctx, dst, dst_stride, src, src_stride, n, block, idx=None):
+    """pct_copy_slices on device pointers (strides / sizes in floats), in
+    launches of at most 4096 slices."""
+    ix = np.arange(n, dtype=np.int32) if idx is None else np.ascontiguousarray(idx, np.int32)
+    for a in range(0, int(n), 4096):
+        b = min(int(n), a + 4096)
+        sub = None if idx is None else ix[a:b]
+        ctx.check(ctx.lib.pct_copy_slices(
+            ctx.h, dst + 4 * a * int(dst_stride), int(dst_stride),
+            src + (4 * a * int(src_stride) if idx is None else 0), int(src_stride),
+            None if sub is None else sub.ctypes.data, b - a, int(block)), "copy_slices")
+
+
 def band_pipeline(xyz, d_s, r_g, params, rank, size, *, device=None, eps_e=1e-6,
-                  c_barrier=50.0, max_grid_side=16384, events=None):
+                  c_barrier=50.0, max_grid_side=16384, events=None, gather_to=None):
     """Generator: the row-band pipeline of one rank.
 
     xyz: this rank's points, a CUDA torch tensor (n, 3) float32/float64.
     Yields collective requests (tuples) and finally returns a BandResult.
     ``events`` (a dict) receives CUDA events recorded on the current stream
     around the evaluate launch ("evaluate" -> (start, end)) and its extent
-    ("cell_slices")."""
+    ("cell_slices").  ``gather_to`` = a rank: the surviving slices of every
+    band are sent to that rank and assembled there into one reference-
+    compatible ``Tomogram`` (``BandResult.tomogram``; tomogram.py:65-96)."""
     import torch
 
     ctx = _lib.context(device if device is not None else xyz.device.index)
@@ -172,13 +213,19 @@ def band_pipeline(xyz, d_s, r_g, params, rank, size, *, device=None, eps_e=1e-6,
     xyz = xyz.contiguous()
     n = xyz.shape[0]
 
-    # 1. bounds -> global frame
+    # 1. bounds -> global frame; a non-finite point on any rank fails every rank
     lo = np.full(3, np.inf)
     hi = np.full(3, -np.inf)
+    bad = 0.0
     if n > 0:
-        ctx.check(lib.pct_bounds(h, xyz.data_ptr(), n, code, lo.ctypes.data, hi.ctypes.data),
-                  "bounds")
-    lo, hi = yield ("bounds", lo, hi)
+        rc = lib.pct_bounds(h, xyz.data_ptr(), n, code, lo.ctypes.data, hi.ctypes.data)
+        if rc == _lib.PCT_E_NONFINITE:
+            bad, lo[:], hi[:] = 1.0, np.inf, -np.inf
+        else:
+            ctx.check(rc, "bounds")
+    lo, hi, bad = yield ("bounds", lo, hi, bad)
+    if bad:
+        raise ValueError("point cloud contains non-finite coordinates")
     if not np.all(np.isfinite(lo)):
         from .cloud import CloudFormatError
         raise CloudFormatError("zero valid points")
@@ -196,6 +243,11 @@ def band_pipeline(xyz, d_s, r_g, params, rank, size, *, device=None, eps_e=1e-6,
     starts = band_starts(rows, size)
     row0, row1 = starts[rank], starts[rank + 1]
     nrows = row1 - row0
+    from .traversability import build_kernel
+    kern = build_kernel(params.d_inf, params.d_sm, r_g)
+    w = np.ascontiguousarray(kern.weights)
+    H = halo_rows(params, r_g, w.shape[0])
+    check_bands(starts, H)
 
     # 2. partition by owner band, all-to-all (one band owns every point)
     if size == 1:
@@ -212,10 +264,6 @@ def band_pipeline(xyz, d_s, r_g, params, rank, size, *, device=None, eps_e=1e-6,
         mine = mine.contiguous()
 
     # 3. banded build into the extended stack
-    from .traversability import build_kernel
-    kern = build_kernel(params.d_inf, params.d_sm, r_g)
-    w = np.ascontiguousarray(kern.weights)
-    H = halo_rows(params, r_g, w.shape[0])
     top = min(H, row0)
     bot = min(H, rows - row1)
     ext_rows = top + nrows + bot
@@ -226,24 +274,27 @@ def band_pipeline(xyz, d_s, r_g, params, rank, size, *, device=None, eps_e=1e-6,
         ctx.check(lib.pct_build_band(h, mine.data_ptr(), mine.shape[0], code, C.byref(fr),
                                      heights.ctypes.data, row0, nrows, stride,
                                      _ptr(g, top * cols), _ptr(c, top * cols)), "build_band")
-    # 4. halo exchange: my first rows go up (to rank-1), my last rows go down
+    # 4. halo exchange: my first rows go up (to rank-1), my last rows go down;
+    # packed into / unpacked from contiguous (2, S, rows, cols) buffers by libpct
     up_n = min(H, rows - row0) if rank > 0 else 0   # == rank-1's bottom halo
     down_n = min(H, row1) if rank + 1 < size else 0  # == rank+1's top halo
-    if up_n > nrows or down_n > nrows:
-        raise ValueError(f"row band of {nrows} rows is thinner than the {H}-row halo; "
-                         "use fewer ranks for this grid")
-    send_up = torch.stack([g[:, top:top + up_n], c[:, top:top + up_n]]).contiguous() \
-        if rank > 0 else None
-    send_down = torch.stack([g[:, top + nrows - down_n:top + nrows],
-                             c[:, top + nrows - down_n:top + nrows]]).contiguous() \
-        if rank + 1 < size else None
+
+    def pack(first_row, nr):
+        buf = torch.empty((2, S, nr, cols), dtype=torch.float32, device=xyz.device)
+        for L, src in enumerate((g, c)):
+            _copy_slices(ctx, _ptr(buf, L * S * nr * cols), nr * cols,
+                         _ptr(src, first_row * cols), stride, S, nr * cols)
+        return buf
+
+    send_up = pack(top, up_n) if rank > 0 else None
+    send_down = pack(top + nrows - down_n, down_n) if rank + 1 < size else None
     from_up, from_down = yield ("halo", send_up, send_down, (2, S, top, cols), (2, S, bot, cols))
-    if top:
-        g[:, :top] = from_up[0]
-        c[:, :top] = from_up[1]
-    if bot:
-        g[:, top + nrows:] = from_down[0]
-        c[:, top + nrows:] = from_down[1]
+    for buf, first_row, nr in ((from_up, 0, top), (from_down, top + nrows, bot)):
+        if nr:
+            buf = buf.contiguous()
+            for L, dst in enumerate((g, c)):
+                _copy_slices(ctx, _ptr(dst, first_row * cols), stride,
+                             _ptr(buf, L * S * nr * cols), nr * cols, S, nr * cols)
 
     # 5. evaluate the extended band (own rows are exact)
     cost = torch.empty_like(g)
@@ -291,12 +342,100 @@ def band_pipeline(xyz, d_s, r_g, params, rank, size, *, device=None, eps_e=1e-6,
         triples_any(req[1])
         red = yield ("max_u8", pending["local"])
         req = sweep.send([bool(v) for v in red])
+    keep = keep_box["keep"]
+    res = BandResult(rank=rank, size=size, rows=rows, cols=cols, row0=row0, nrows=nrows,
+                     heights=heights, origin=(float(fr.origin_x), float(fr.origin_y)),
+                     z_min=float(fr.z_min), keep=keep,
+                     ground=g[:, top:top + nrows], ceiling=c[:, top:top + nrows],
+                     cost=cost[:, top:top + nrows])
+
+    # 7. gather the surviving slices on one rank
+    if gather_to is not None:
+        K = len(keep)
+        if rank == gather_to:
+            from .tomogram import new_device_stack
+            stacks = [new_device_stack(ctx, K, rows, cols) for _ in range(3)]
+            for L, src in enumerate((g, c, cost)):   # own band, straight from the ext stacks
+                _copy_slices(ctx, stacks[L].ptr + 4 * row0 * cols, rows * cols,
+                             _ptr(src, top * cols), stride, K, nrows * cols, idx=keep)
+            shapes = [(3, K, starts[b + 1] - starts[b], cols) for b in range(size)]
+            bands = yield ("gather", None, gather_to, shapes, xyz.device)
+            for b, buf in enumerate(bands):
+                if b == rank or buf is None:
+                    continue
+                buf = buf.contiguous()
+                nb = starts[b + 1] - starts[b]
+                for L in range(3):
+                    _copy_slices(ctx, stacks[L].ptr + 4 * starts[b] * cols, rows * cols,
+                                 _ptr(buf, L * K * nb * cols), nb * cols, K, nb * cols)
+            res.tomogram = _assemble_tomogram(stacks, heights, keep, r_g, res.origin, d_s,
+                                              res.z_min)
+        else:
+            buf = torch.empty((3, K, nrows, cols), dtype=torch.float32, device=xyz.device)
+            for L, src in enumerate((g, c, cost)):
+                _copy_slices(ctx, _ptr(buf, L * K * nrows * cols), nrows * cols,
+                             _ptr(src, top * cols), stride, K, nrows * cols, idx=keep)
+            yield ("gather", buf, gather_to, None, xyz.device)
     lib.pct_set_stream(h, None)
-    return BandResult(rank=rank, size=size, rows=rows, cols=cols, row0=row0, nrows=nrows,
-                      heights=heights, origin=(float(fr.origin_x), float(fr.origin_y)),
-                      z_min=float(fr.z_min), keep=keep_box["keep"],
-                      ground=g[:, top:top + nrows], ceiling=c[:, top:top + nrows],
-                      cost=cost[:, top:top + nrows])
+    return res
+
+
+def _assemble_tomogram(stacks, heights, keep, r_g, origin, d_s, z_min):
+    """The simplified Tomogram over full-grid device stacks (ground, ceiling,
+    cost), as simplify_tomogram returns it (simplify.py:71-73: indices
+    0..K-1, plane heights kept); Layer.values materialise on first access."""
+    from .tomogram import Layer, Tomogram, TomogramSlice
+    g, c, cost = stacks
+    slices = [TomogramSlice(Layer.on_device(g, m, r_g, origin), Layer.on_device(c, m, r_g, origin),
+                            float(heights[k]), m, Layer.on_device(cost, m, r_g, origin))
+              for m, k in enumerate(keep)]
+    return Tomogram(slices=slices, d_s=float(d_s), z_min=float(z_min))
+
+
+def tomogram_sharded(points, d_s: float, r_g: float, params=None, *, eps_e: float = 1e-6,
+                     c_barrier: float = 50.0, root: int = 0, group=None, device=None,
+                     max_grid_side: int = 16384):
+    """build_tomogram -> evaluate_tomogram -> simplify_tomogram of ONE map
+    whose points are spread over the ranks of a torch.distributed group (one
+    process per GPU), row-band sharded as in the module docstring.
+
+    ``points``: this rank's share of the cloud -- a PointCloud, an (n, 3)
+    float32/float64 host array (pinned memory uploads fastest) or a CUDA
+    tensor; any split of the points over the ranks gives the same result.
+    Returns on ``root`` the simplified reference-compatible ``Tomogram``
+    (tomogram.py:65-96; bit-identical to the one-GPU chain, its layers
+    device-resident until ``materialize()`` / ``Layer.values``), and None on
+    the other ranks.  With a one-rank group (or no process group) it runs the
+    same band pipeline on one GPU."""
+    import torch
+    import torch.distributed as dist
+
+    from .cloud import source_points
+    from .traversability import TravParams
+    params = params if params is not None else TravParams()
+    single = not (dist.is_available() and dist.is_initialized())
+    rank = 0 if single else dist.get_rank(group)
+    size = 1 if single else dist.get_world_size(group)
+    dev = torch.device("cuda", device if device is not None else torch.cuda.current_device())
+    if isinstance(points, torch.Tensor):
+        xyz = points.to(dev)
+    else:
+        arr = np.ascontiguousarray(source_points(points))
+        if arr.dtype not in (np.float32, np.float64):
+            arr = arr.astype(np.float64)
+        ctx = _lib.context(dev.index)
+        xyz = torch.empty(arr.shape, dtype=torch.float32 if arr.dtype == np.float32
+                          else torch.float64, device=dev)
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        with ctx.lock:
+            ctx.check(ctx.lib.pct_set_stream(ctx.h, C.c_void_p(stream)), "set_stream")
+            ctx.check(ctx.lib.pct_memcpy_h2d(ctx.h, xyz.data_ptr(), arr.ctypes.data, arr.nbytes),
+                      "h2d")
+    gen = band_pipeline(xyz, d_s, r_g, params, rank, size, device=dev.index, eps_e=eps_e,
+                        c_barrier=c_barrier, max_grid_side=max_grid_side,
+                        gather_to=root if size > 1 else 0)
+    res = run_virtual([gen])[0] if size == 1 else run_torch(gen, group)
+    return res.tomogram if rank == root else None
 
 
 def _sweep_gen(S, tb):
@@ -331,44 +470,57 @@ class _NeedAny(Exception):
 # drivers
 
 def run_torch(gen, group=None):
-    """Serve a band_pipeline generator with torch.distributed collectives."""
+    """Serve a band_pipeline generator with torch.distributed collectives.
+
+    NCCL: device buffers straight over NVLink.  Gloo (CPU process groups:
+    the multi-process tests): the same requests staged through host memory."""
     import torch
     import torch.distributed as dist
 
     rank = dist.get_rank(group)
     size = dist.get_world_size(group)
+    nccl = dist.get_backend(group) == "nccl"
+    coll = _collective_device(group)
+
+    def out(t):        # device buffer -> what the backend can send
+        return t if (nccl or t is None) else t.cpu()
+
+    def back(t, dev):  # what the backend received -> device buffer
+        return t if (nccl or t is None) else t.to(dev)
+
     req = next(gen)
     while True:
         kind = req[0]
         if kind == "bounds":
-            lo, hi = req[1], req[2]
-            dev = _collective_device(group)
-            t = torch.tensor(np.concatenate([-lo, hi]), dtype=torch.float64, device=dev)
+            lo, hi, bad = req[1], req[2], req[3]
+            t = torch.tensor(np.concatenate([-lo, hi, [bad]]), dtype=torch.float64, device=coll)
             dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
             v = t.cpu().numpy()
-            ans = (-v[:3], v[3:])
+            ans = (-v[:3], v[3:6], float(v[6]))
         elif kind == "alltoallv":
             part, counts = req[1], req[2]
             dev = part.device
-            cnt = torch.tensor(counts, dtype=torch.int64, device=dev)
+            cnt = torch.tensor(counts, dtype=torch.int64, device=coll)
             rcnt = torch.empty_like(cnt)
             dist.all_to_all_single(rcnt, cnt, group=group)
             rc = rcnt.cpu().tolist()
-            out = torch.empty((int(sum(rc)), 3), dtype=part.dtype, device=dev)
-            dist.all_to_all_single(out, part, output_split_sizes=rc, input_split_sizes=counts,
+            src = out(part)
+            res = torch.empty((int(sum(rc)), 3), dtype=part.dtype, device=src.device)
+            dist.all_to_all_single(res, src, output_split_sizes=rc, input_split_sizes=counts,
                                    group=group)
-            ans = out
+            ans = back(res, dev)
         elif kind == "halo":
             send_up, send_down, up_shape, down_shape = req[1:]
             ref = send_up if send_up is not None else send_down
-            dev = ref.device if ref is not None else _collective_device(group)
-            recv_up = torch.empty(up_shape, dtype=torch.float32, device=dev)
-            recv_down = torch.empty(down_shape, dtype=torch.float32, device=dev)
+            dev = ref.device if ref is not None else coll
+            bdev = dev if nccl else torch.device("cpu")
+            recv_up = torch.empty(up_shape, dtype=torch.float32, device=bdev)
+            recv_down = torch.empty(down_shape, dtype=torch.float32, device=bdev)
             ops = []
             if send_up is not None:
-                ops.append(dist.P2POp(dist.isend, send_up, _global(group, rank - 1), group))
+                ops.append(dist.P2POp(dist.isend, out(send_up), _global(group, rank - 1), group))
             if send_down is not None:
-                ops.append(dist.P2POp(dist.isend, send_down, _global(group, rank + 1), group))
+                ops.append(dist.P2POp(dist.isend, out(send_down), _global(group, rank + 1), group))
             if up_shape[2] > 0:
                 ops.append(dist.P2POp(dist.irecv, recv_up, _global(group, rank - 1), group))
             if down_shape[2] > 0:
@@ -376,12 +528,30 @@ def run_torch(gen, group=None):
             if ops:
                 for r in dist.batch_isend_irecv(ops):
                     r.wait()
-            ans = (recv_up, recv_down)
+            ans = (back(recv_up, dev), back(recv_down, dev))
         elif kind == "max_u8":
-            dev = _collective_device(group)
-            t = torch.from_numpy(np.ascontiguousarray(req[1])).to(dev)
+            t = torch.from_numpy(np.ascontiguousarray(req[1])).to(coll)
             dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
             ans = t.cpu().numpy()
+        elif kind == "gather":
+            buf, root, shapes, dev = req[1], req[2], req[3], req[4]
+            if rank == root:
+                bdev = dev if nccl else torch.device("cpu")
+                bufs = [None if b == rank else torch.empty(shapes[b], dtype=torch.float32,
+                                                           device=bdev)
+                        for b in range(size)]
+                ops = [dist.P2POp(dist.irecv, bufs[b], _global(group, b), group)
+                       for b in range(size) if b != rank and bufs[b].numel() > 0]
+                if ops:
+                    for r in dist.batch_isend_irecv(ops):
+                        r.wait()
+                ans = [back(b, dev) for b in bufs]
+            else:
+                if buf.numel() > 0:
+                    for r in dist.batch_isend_irecv([dist.P2POp(dist.isend, out(buf),
+                                                                _global(group, root), group)]):
+                        r.wait()
+                ans = None
         else:
             raise RuntimeError(f"unknown collective {kind}")
         try:
@@ -407,6 +577,8 @@ def run_virtual(gens):
     """Run P band_pipeline generators in lockstep in one process (one GPU):
     the collectives are performed by direct tensor / array operations."""
     import torch
+    if not gens:
+        return []
 
     P = len(gens)
     reqs = [next(g) for g in gens]
@@ -418,7 +590,8 @@ def run_virtual(gens):
         if kind == "bounds":
             lo = np.min([r[1] for r in reqs], axis=0)
             hi = np.max([r[2] for r in reqs], axis=0)
-            answers = [(lo.copy(), hi.copy()) for _ in range(P)]
+            bad = max(r[3] for r in reqs)
+            answers = [(lo.copy(), hi.copy(), bad) for _ in range(P)]
         elif kind == "alltoallv":
             offs = [np.concatenate([[0], np.cumsum(r[2])]) for r in reqs]
             answers = []
@@ -435,6 +608,10 @@ def run_virtual(gens):
         elif kind == "max_u8":
             m = np.max([r[1] for r in reqs], axis=0)
             answers = [m.copy() for _ in range(P)]
+        elif kind == "gather":
+            root = reqs[0][2]
+            bufs = [r[1] for r in reqs]
+            answers = [bufs if i == root else None for i in range(P)]
         else:
             raise RuntimeError(kind)
         done = 0

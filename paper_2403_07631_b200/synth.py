@@ -35,7 +35,12 @@ CONFIGS = {
 
 
 # ---------------------------------------------------------------------------
-# surface primitives: each returns (area, sampler(rng, n) -> (n, 3) float64)
+# surface primitives: each returns (area, sampler(rng, n) -> (n, 3) float64,
+# xy bounding box (x_lo, y_lo, x_hi, y_hi))
+
+
+def _bb(xs, ys):
+    return (min(xs), min(ys), max(xs), max(ys))
 
 def _hrect(x0, y0, lx, ly, z):
     """Horizontal rectangle; z is a constant or a callable z(x, y)."""
@@ -44,7 +49,7 @@ def _hrect(x0, y0, lx, ly, z):
         y = y0 + rng.random(n) * ly
         zz = np.full(n, float(z)) if not callable(z) else z(x, y)
         return np.column_stack([x, y, zz])
-    return abs(lx * ly), draw
+    return abs(lx * ly), draw, _bb((x0, x0 + lx), (y0, y0 + ly))
 
 
 def _vrect(x0, y0, x1, y1, z0, z1):
@@ -55,7 +60,7 @@ def _vrect(x0, y0, x1, y1, z0, z1):
         s = rng.random(n)
         return np.column_stack([x0 + s * (x1 - x0), y0 + s * (y1 - y0),
                                 z0 + rng.random(n) * (z1 - z0)])
-    return length * abs(z1 - z0), draw
+    return length * abs(z1 - z0), draw, _bb((x0, x1), (y0, y1))
 
 
 def _incline(x0, y0, lx, ly, z0, slope_x):
@@ -63,7 +68,7 @@ def _incline(x0, y0, lx, ly, z0, slope_x):
     def draw(rng, n):
         u = rng.random(n) * lx
         return np.column_stack([x0 + u, y0 + rng.random(n) * ly, z0 + u * slope_x])
-    return lx * ly * math.sqrt(1.0 + slope_x * slope_x), draw
+    return lx * ly * math.sqrt(1.0 + slope_x * slope_x), draw, _bb((x0, x0 + lx), (y0, y0 + ly))
 
 
 def _helix(cx, cy, r_in, r_out, z0, rise_per_rad, theta_total):
@@ -75,7 +80,7 @@ def _helix(cx, cy, r_in, r_out, z0, rise_per_rad, theta_total):
         r = np.sqrt(r_in ** 2 + rng.random(n) * (r_out ** 2 - r_in ** 2))
         return np.column_stack([cx + r * np.cos(th), cy + r * np.sin(th),
                                 z0 + th * rise_per_rad])
-    return area, draw
+    return area, draw, (cx - r_out, cy - r_out, cx + r_out, cy + r_out)
 
 
 def _box_faces(x0, y0, z0, sx, sy, sz, faces="tbs"):
@@ -119,17 +124,35 @@ def _incline_strip(x0, y0, x1, y1, nx, ny, z):
         t = rng.random(n)
         return np.column_stack([x0 + s * (x1 - x0) + t * nx,
                                 y0 + s * (y1 - y0) + t * ny, np.full(n, z)])
-    return length * thick, draw
+    return length * thick, draw, _bb((x0, x1, x0 + nx, x1 + nx), (y0, y1, y0 + ny, y1 + ny))
+
+
+def _hrect_with_hole(x0, y0, lx, ly, z, hx0, hy0, hlx, hly):
+    """Horizontal rectangle minus an axis-aligned opening (four pieces)."""
+    return [_hrect(x0, y0, lx, hy0 - y0, z),
+            _hrect(x0, hy0 + hly, lx, y0 + ly - hy0 - hly, z),
+            _hrect(x0, hy0, hx0 - x0, hly, z),
+            _hrect(hx0 + hlx, hy0, x0 + lx - hx0 - hlx, hly, z)]
+
+
+def _stair(x0, y0, width, z0, steps, rise, tread):
+    """Straight flight rising along +x: `steps` treads and their risers."""
+    parts = []
+    for s in range(steps):
+        z = z0 + (s + 1) * rise
+        parts.append(_hrect(x0 + s * tread, y0, tread, width, z))
+        parts.append(_vrect(x0 + s * tread, y0, x0 + s * tread, y0 + width, z - rise, z))
+    return parts
 
 
 def _sample(parts, n_points, sigma, rng, weights=None):
-    areas = np.array([a for a, _ in parts], dtype=np.float64)
+    areas = np.array([p[0] for p in parts], dtype=np.float64)
     if weights is not None:
         areas = areas * weights
     counts = rng.multinomial(n_points, areas / areas.sum())
     out = np.empty((n_points, 3), dtype=np.float32)
     pos = 0
-    for (_, draw), c in zip(parts, counts):
+    for (_, draw, _), c in zip(parts, counts):
         if c:
             out[pos:pos + c] = draw(rng, int(c))
             pos += c
@@ -139,6 +162,52 @@ def _sample(parts, n_points, sigma, rng, weights=None):
         for a in range(0, n_points, step):
             b = min(n_points, a + step)
             out[a:b] += rng.normal(0.0, sigma, (b - a, 3)).astype(np.float32)
+    return out
+
+
+def _sample_seeded(parts, n_points, sigma, seed, box=None, workers=8, share=None):
+    """Like _sample, but part i draws its points and noise from its own
+    generator ``default_rng([seed, i])``.  The cloud is the same whichever
+    parts are drawn and in whatever order, so (a) the parts are drawn in
+    parallel threads and (b) ``box = (x_lo, y_lo, x_hi, y_hi)`` yields
+    exactly the points of the full cloud inside the box (half-open) while
+    drawing only the parts whose footprint comes near it, and (c) ``share =
+    (r, n)`` draws only the parts i with i % n == r: n such shares are a
+    partition of the cloud (one per rank of a sharded run)."""
+    from concurrent.futures import ThreadPoolExecutor
+    areas = np.array([p[0] for p in parts], dtype=np.float64)
+    counts = np.random.default_rng([seed, len(parts)]).multinomial(n_points, areas / areas.sum())
+    pad = 8.0 * sigma + 1e-6  # noise never moves a point further than this (p < 1e-15)
+    todo = []
+    for i, (p, c) in enumerate(zip(parts, counts)):
+        if c == 0 or (share is not None and i % share[1] != share[0]):
+            continue
+        if box is not None:
+            bx = p[2]
+            if bx[0] > box[2] + pad or bx[2] < box[0] - pad or bx[1] > box[3] + pad \
+                    or bx[3] < box[1] - pad:
+                continue
+        todo.append((i, p[1], int(c)))
+    offs = np.concatenate([[0], np.cumsum([c for _, _, c in todo])]).astype(np.int64)
+    out = np.empty((int(offs[-1]), 3), dtype=np.float32)
+
+    def one(t):
+        i, draw, c = todo[t]
+        rng = np.random.default_rng([seed, i])
+        dst = out[offs[t]:offs[t + 1]]
+        step = 1 << 22
+        for a in range(0, c, step):
+            b = min(c, a + step)
+            dst[a:b] = draw(rng, b - a)
+            if sigma > 0:
+                dst[a:b] += rng.normal(0.0, sigma, (b - a, 3)).astype(np.float32)
+
+    with ThreadPoolExecutor(max(1, workers)) as ex:
+        list(ex.map(one, range(len(todo))))
+    if box is not None:
+        m = (out[:, 0] >= box[0]) & (out[:, 0] < box[2]) & (out[:, 1] >= box[1]) & \
+            (out[:, 1] < box[3])
+        out = np.ascontiguousarray(out[m])
     return out
 
 
@@ -287,10 +356,14 @@ def rough_terrain(n_points=20_000_000, seed=2, sigma=0.02, extent=100.0,
     return _sample(parts, n_points, sigma, rng, weights=np.asarray(weights))
 
 
-def campus(n_points=200_000_000, seed=3, sigma=0.03, extent=400.0):
+def campus(n_points=200_000_000, seed=3, sigma=0.03, extent=400.0, box=None, share=None):
     """Config 3: 400x400 m sloped terrain, 16 three-storey buildings (floors
-    every 4 m, roof, perimeter walls with doors, internal ramps), walkways
-    at 5 m between neighbouring buildings, rooftop plant rooms."""
+    every 4 m, roof, perimeter walls with doors, internal ramps between the
+    floors, a stair of 0.167 m risers from the top floor to the roof),
+    walkways at 5 m between neighbouring buildings, rooftop plant rooms.
+    Every surface draws from its own seeded generator (_sample_seeded), so
+    ``box`` cheaply yields the exact crop of the full cloud and ``share =
+    (rank, world)`` one rank's part of it."""
     rng = np.random.default_rng(seed)
     fbm = _Fbm(rng, extent, amplitude=0.5, base_wavelength=40.0)
 
@@ -322,19 +395,22 @@ def campus(n_points=200_000_000, seed=3, sigma=0.03, extent=400.0):
             sites.append((bx, by, base))
             run = 4.0 / math.tan(math.radians(15.0))
             rx0, ry0 = bx + 4.0, by + 30.0
+            st_steps, st_tread = 24, 0.3
+            sx0, sy0 = bx + 20.0, by + 4.0
             for f in range(4):       # ground floor, 2 upper floors, roof
                 z = base + 4.0 * f
                 surfaces = (z,) if f == 0 else (z, z - 0.3)
                 for zz in surfaces:
-                    if f in (1, 2):
-                        parts += [_hrect(bx, by, bsz, ry0 - by, zz),
-                                  _hrect(bx, ry0 + 3.0, bsz, by + bsz - ry0 - 3.0, zz),
-                                  _hrect(bx, ry0, rx0 - bx, 3.0, zz),
-                                  _hrect(rx0 + run, ry0, bx + bsz - rx0 - run, 3.0, zz)]
+                    if f in (1, 2):   # opening above the ramp from the floor below
+                        parts += _hrect_with_hole(bx, by, bsz, bsz, zz, rx0, ry0, run, 3.0)
+                    elif f == 3:      # opening above the stair
+                        parts += _hrect_with_hole(bx, by, bsz, bsz, zz, sx0, sy0,
+                                                  st_steps * st_tread, 2.0)
                     else:
                         parts.append(_hrect(bx, by, bsz, bsz, zz))
                 if f < 2:
                     parts.append(_incline(rx0, ry0, run, 3.0, z, 4.0 / run))
+            parts += _stair(sx0, sy0, 2.0, base + 8.0, st_steps, 4.0 / st_steps, st_tread)
             corners = [(bx, by), (bx + bsz, by), (bx + bsz, by + bsz), (bx, by + bsz)]
             for w in range(4):
                 (xa, ya), (xb, yb) = corners[w], corners[(w + 1) % 4]
@@ -351,7 +427,7 @@ def campus(n_points=200_000_000, seed=3, sigma=0.03, extent=400.0):
             x0 = bx + bsz
             parts += [_hrect(x0, by + 18.0, nx_ - x0, 3.0, z),
                       _hrect(x0, by + 18.0, nx_ - x0, 3.0, z - 0.4)]
-    return _sample(parts, n_points, sigma, rng)
+    return _sample_seeded(parts, n_points, sigma, seed, box=box, share=share)
 
 
 def generate(config: int, n_points: int | None = None, seed: int | None = None):

@@ -386,5 +386,5 @@ def build_tomogram(cloud: PointCloud, d_s: float, r_g: float, threads: int = 1,
         ptr, n, dtype, dev_id = dev()
         return build_from_points(ptr, d_s, r_g, max_grid_side, device=dev_id, on_device=True,
                                  n_points=n, dtype=dtype)
-    xyz = cloud.xyz if hasattr(cloud, "xyz") else np.asarray(cloud)
-    return build_from_points(xyz, d_s, r_g, max_grid_side, device=device)
+    from .cloud import source_points
+    return build_from_points(source_points(cloud), d_s, r_g, max_grid_side, device=device)

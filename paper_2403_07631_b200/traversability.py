@@ -304,9 +304,3 @@ def evaluate_tomogram(tomogram: Tomogram, params, threads: int = 1) -> Tomogram:
                                                                  s.ground.origin))
             start = end
     return Tomogram(slices=out, d_s=tomogram.d_s, z_min=tomogram.z_min)
-
-
-def cost_to_gray(cost: np.ndarray, c_barrier: float) -> np.ndarray:
-    """Map [0, c_barrier] linearly onto [255, 0] (export helper, host side)."""
-    scaled = np.rint(255.0 * (c_barrier - cost.astype(np.float64)) / c_barrier)
-    return np.clip(scaled, 0, 255).astype(np.uint8)

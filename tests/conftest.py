@@ -7,6 +7,11 @@ ROOT = Path(__file__).resolve().parent.parent
 if str(ROOT) not in sys.path:
     sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(Path(__file__).resolve().parent))
+# the reference package, importable only in the build container (CPU tests
+# that compare against it skip elsewhere; nothing on the GPU box reads it)
+_REF = Path("/root/reference/pkg/src")
+if _REF.is_dir() and str(_REF) not in sys.path:
+    sys.path.append(str(_REF))
 
 
 def pytest_configure(config):

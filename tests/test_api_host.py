@@ -55,8 +55,15 @@ def test_pointcloud_validation():
         pct.PointCloud(np.zeros((3, 2)))
     with pytest.raises(ValueError):
         pct.PointCloud(np.array([[0.0, np.nan, 0.0]]))
-    assert pct.PointCloud(np.zeros((2, 3), np.float32)).xyz.dtype == np.float32
+    # xyz is float64 like the reference's (cloud_io.py:35); the device path
+    # uploads the caller's float32 array (``points``) without that copy
+    f32 = np.arange(6, dtype=np.float32).reshape(2, 3) + 0.1
+    c = pct.PointCloud(f32)
+    assert c.points.dtype == np.float32 and c.points is not None
+    assert c.xyz.dtype == np.float64 and c.xyz.flags.c_contiguous
+    assert np.array_equal(c.xyz, f32.astype(np.float64))
     assert pct.PointCloud(np.zeros((2, 3), np.int32)).xyz.dtype == np.float64
+    assert len(c) == 2 and c.dropped == 0 and pct.PointCloud(f32, 3).dropped == 3
 
 
 def test_argument_errors_before_any_device_call():

@@ -80,3 +80,127 @@ def test_virtual_bands_tiled_build(golden, monkeypatch, P):
     assert np.array_equal(c1.view(np.uint32), c2.view(np.uint32))
     assert np.array_equal(k1.view(np.uint32), k2.view(np.uint32))
     assert keep1 == keep2 == case["keep"]
+
+
+def _simplified_single(xyz, d_s, r_g):
+    ev = pct.evaluate_tomogram(pct.build_tomogram(pct.PointCloud(xyz), d_s, r_g), pct.TravParams())
+    return pct.simplify_tomogram(ev).materialize()
+
+
+def _same_tomogram(a, b):
+    assert len(a.slices) == len(b.slices)
+    assert (a.rows, a.cols, a.resolution, a.origin, a.d_s, a.z_min) == \
+        (b.rows, b.cols, b.resolution, b.origin, b.d_s, b.z_min)
+    for sa, sb in zip(a.slices, b.slices):
+        assert sa.plane_height == sb.plane_height and sa.index == sb.index
+        for la, lb in ((sa.ground, sb.ground), (sa.ceiling, sb.ceiling), (sa.cost, sb.cost)):
+            assert np.array_equal(la.values.view(np.uint32), lb.values.view(np.uint32))
+
+
+@pytest.mark.parametrize("P", [1, 2, 4])
+def test_virtual_bands_gather_tomogram(golden, P):
+    """The surviving slices of every band gathered on one rank form the
+    simplified Tomogram of the one-GPU chain (tomogram.py:65-96)."""
+    import torch
+    from paper_2403_07631_b200 import sharded
+    case = golden["cases"]["synth_cfg0"]
+    xyz = case_input("synth_cfg0", case)
+    want = _simplified_single(xyz, 0.5, 0.1)
+    t = torch.from_numpy(xyz).cuda()
+    root = P - 1
+    gens = [sharded.band_pipeline(t[r::P].contiguous(), 0.5, 0.1, pct.TravParams(), r, P,
+                                  gather_to=root) for r in range(P)]
+    res = sharded.run_virtual(gens)
+    assert all(r.tomogram is None for i, r in enumerate(res) if i != root)
+    got = res[root].tomogram
+    assert [s.plane_height for s in got.slices] == [case["heights"][k] for k in case["keep"]]
+    _same_tomogram(got.materialize(), want)
+
+
+def test_tomogram_sharded_without_process_group():
+    from paper_2403_07631_b200 import sharded, synth
+    xyz = synth.spiral_ramp(300_000, seed=4)
+    _same_tomogram(sharded.tomogram_sharded(pct.PointCloud(xyz), 0.4, 0.1).materialize(),
+                   _simplified_single(xyz, 0.4, 0.1))
+
+
+def test_virtual_bands_errors_on_every_rank():
+    """A non-finite point on one rank, or a band thinner than the halo, fails
+    every rank before the first point exchange (no rank left waiting)."""
+    import torch
+    from paper_2403_07631_b200 import sharded, synth
+    xyz = torch.from_numpy(synth.two_storey(20_000, seed=1)).cuda()
+    bad = xyz[1::2].clone()
+    bad[5, 2] = float("nan")
+    gens = [sharded.band_pipeline(s.contiguous(), 0.5, 0.1, pct.TravParams(), r, 2)
+            for r, s in enumerate([xyz[0::2], bad])]
+    reqs = [next(g) for g in gens]
+    assert [r[0] for r in reqs] == ["bounds", "bounds"] and reqs[1][3] == 1.0
+    for g in gens:  # the reduced flag reaches both ranks: both raise
+        with pytest.raises(ValueError, match="non-finite"):
+            g.send((np.zeros(3), np.ones(3), 1.0))
+    # 203 rows over 40 ranks: 5-row bands against an 8-row halo
+    gens = [sharded.band_pipeline(xyz[r::40].contiguous(), 0.5, 0.1, pct.TravParams(), r, 40)
+            for r in range(40)]
+    with pytest.raises(ValueError, match="thinner than"):
+        sharded.run_virtual(gens)
+
+
+def _gloo_worker(rank, size, port, q, n_points):
+    import os
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=size)
+    try:
+        torch.cuda.set_device(0)
+        import paper_2403_07631_b200 as p
+        from paper_2403_07631_b200 import sharded, synth
+        xyz = synth.spiral_ramp(n_points, seed=4)
+        mine = np.ascontiguousarray(xyz[rank::size])
+        tom = sharded.tomogram_sharded(p.PointCloud(mine), 0.4, 0.1, root=0)
+        if rank == 0:
+            tom.materialize()
+            import hashlib
+            dig = [hashlib.sha256(np.stack([l.values for l in layers]).tobytes()).hexdigest()
+                   for layers in ([s.ground for s in tom.slices], [s.ceiling for s in tom.slices],
+                                  [s.cost for s in tom.slices])]
+            q.put((rank, [s.plane_height for s in tom.slices], dig))
+        else:
+            q.put((rank, tom is None, None))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_processes_gloo_equal_single_gpu():
+    """The real band pipeline in two processes (gloo: collectives staged
+    through host memory; both ranks share cuda:0) returns on rank 0 the
+    Tomogram of the one-GPU chain, bit for bit."""
+    import hashlib
+    import socket
+    import torch.multiprocessing as mp
+    from paper_2403_07631_b200 import synth
+    n = 300_000
+    want = _simplified_single(synth.spiral_ramp(n, seed=4), 0.4, 0.1)
+    wdig = [hashlib.sha256(np.stack([l.values for l in layers]).tobytes()).hexdigest()
+            for layers in ([s.ground for s in want.slices], [s.ceiling for s in want.slices],
+                           [s.cost for s in want.slices])]
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, q, n)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = {}
+    for _ in range(2):
+        r = q.get(timeout=300)
+        out[r[0]] = r
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    assert out[1][1] is True
+    assert out[0][1] == [sl.plane_height for sl in want.slices]
+    assert out[0][2] == wdig

@@ -139,3 +139,50 @@ def test_build_from_device_cloud_equals_host_build(tmp_path):
     for sa, sb in zip(a.slices, b.slices):
         assert sa.ground.values.tobytes() == sb.ground.values.tobytes()
         assert sa.ceiling.values.tobytes() == sb.ceiling.values.tobytes()
+
+
+def _reference_tomoplan():
+    """The reference package, where it is importable (the build container)."""
+    import sys
+    from pathlib import Path
+    src = Path("/root/reference/pkg/src")
+    if src.is_dir() and str(src) not in sys.path:
+        sys.path.append(str(src))
+    return pytest.importorskip("tomoplan")
+
+
+def test_product_load_cloud_has_no_text_parsers(tmp_path):
+    """The product reads pcd_binary only; text formats raise (no CPU
+    fallback through the reference inside the package)."""
+    from paper_2403_07631_b200 import CloudFormatError, cloud_io
+    p = tmp_path / "pts.xyz"
+    p.write_text("0 0 0\n1 2 3\n")
+    for fmt in ("xyz_text", "pcd_ascii", "ply_ascii"):
+        with pytest.raises(CloudFormatError, match="no device ingest"):
+            cloud_io.load_cloud(p, fmt)
+    import paper_2403_07631_b200 as pkg
+    for mod in ("cloud_io", "cloud", "tomogram", "traversability", "simplify", "sharded",
+                "batch", "archive", "planner_ctx", "trajectory"):
+        src = (Path(pkg.__file__).parent / f"{mod}.py").read_text()
+        code = "\n".join(ln for ln in src.splitlines() if not ln.strip().startswith("#"))
+        assert "import tomoplan" not in code and "from tomoplan" not in code, mod
+
+
+def test_compat_dispatches_text_formats_to_the_reference(tmp_path):
+    """After compat.install, tomoplan.load_cloud keeps the reference's
+    parser for text formats (cloud_io.py:281-288) and uses the device ingest
+    for pcd_binary."""
+    tp = _reference_tomoplan()
+    from paper_2403_07631_b200 import compat
+    p = tmp_path / "pts.xyz"
+    p.write_text("# comment\n0 0 0\n1.5 2 3\nnan 1 1\n")
+    want = tp.load_cloud(p, "xyz_text")
+    compat.install(tp)
+    try:
+        got = tp.load_cloud(p, "xyz_text")
+        assert type(got) is type(want)
+        assert np.array_equal(got.xyz, want.xyz) and got.dropped == want.dropped == 1
+        assert tp.cloud_io.load_cloud is tp.load_cloud
+    finally:
+        compat.uninstall()
+    assert tp.load_cloud(p, "xyz_text").dropped == 1

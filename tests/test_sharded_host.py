@@ -103,8 +103,9 @@ def _free_port():
 def _fake_pipeline(rank, size):
     """Exercises every collective kind the band pipeline issues."""
     import torch
-    lo, hi = yield ("bounds", np.array([rank, -rank, 2.0 * rank]),
-                    np.array([rank + 1.0, 5.0, -1.0]))
+    lo, hi, bad = yield ("bounds", np.array([rank, -rank, 2.0 * rank]),
+                         np.array([rank + 1.0, 5.0, -1.0]), float(rank == 1))
+    assert bad == 1.0  # one rank's flag reaches every rank
     counts = [rank + d + 1 for d in range(size)]
     part = torch.cat([torch.full((counts[d], 3), float(10 * rank + d)) for d in range(size)])
     mine = yield ("alltoallv", part, counts)
@@ -114,6 +115,15 @@ def _fake_pipeline(rank, size):
     bot = 1 if rank + 1 < size else 0
     fu, fd = yield ("halo", up, down, (2, 3, top, 4), (2, 3, bot, 4))
     red = yield ("max_u8", np.array([rank, 7 - rank, 3], np.uint8))
+    # gather to rank 1: rank 0 sends a (3, 2, 2, 4) band
+    cpu = torch.device("cpu")
+    if rank == 1:
+        got = yield ("gather", None, 1, [(3, 2, 2, 4), (3, 2, 3, 4)], cpu)
+        assert got[1] is None and got[0].shape == (3, 2, 2, 4)
+        assert torch.all(got[0] == 42.0)
+    else:
+        got = yield ("gather", torch.full((3, 2, 2, 4), 42.0), 1, None, cpu)
+        assert got is None
     return lo, hi, mine, fu, fd, red
 
 
@@ -155,3 +165,21 @@ def test_run_torch_collectives_gloo_two_ranks():
         assert red == [1, 7, 3]
     assert np.all(np.array(out[0][5]) == 1.0) and np.array(out[0][5]).shape == (2, 3, 1, 4)
     assert np.all(np.array(out[1][4]) == 0.5) and np.array(out[1][4]).shape == (2, 3, 2, 4)
+
+
+def test_check_bands_decided_globally():
+    """The thin-band error depends only on the shared frame: every rank raises
+    (rows=10 over 4 ranks gives bands 2/3/2/3; a 3-row halo fails)."""
+    st = sharded.band_starts(10, 4)
+    assert [b - a for a, b in zip(st, st[1:])] == [2, 3, 2, 3]
+    with pytest.raises(ValueError, match="thinner than"):
+        sharded.check_bands(st, 3)
+    sharded.check_bands(st, 2)
+    sharded.check_bands(sharded.band_starts(4004, 8), 8)
+    with pytest.raises(ValueError):
+        sharded.check_bands(sharded.band_starts(203, 40), 8)
+    # a halo is clipped at the grid edge: an edge band thinner than H is fine
+    # when the neighbour's halo reaches the edge anyway; a middle one is not
+    sharded.check_bands([0, 10, 12], 3)
+    with pytest.raises(ValueError):
+        sharded.check_bands([0, 10, 12, 20], 3)
