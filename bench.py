@@ -254,6 +254,18 @@ def cpu_pipeline(xyz, cfg, threads):
     return (t3 - t0), dict(build=t1 - t0, evaluate=t2 - t1, simplify=t3 - t2), (t, cost, keep)
 
 
+def numpy_port_seconds(xyz, cfg, threads):
+    """build -> evaluate -> simplify with the numpy restatement of the
+    reference (oracle/*.py), for context beside the C port."""
+    import oracle
+    from paper_2403_07631_b200.traversability import TravParams
+    t0 = time.perf_counter()
+    t = oracle.build(xyz, cfg["d_s"], cfg["r_g"], threads=threads)
+    cost = oracle.evaluate(t["ground"], t["ceiling"], cfg["r_g"], TravParams(), threads=threads)
+    oracle.simplify(t["ground"], cost)
+    return time.perf_counter() - t0
+
+
 def cpu_t1_sample(args, cfg, xyz):
     """The bounded sample the single-thread figure is measured on."""
     if args.config == 3:
@@ -618,6 +630,7 @@ def run_b200(args):
         if world == 1 and not args.no_cpu:
             t1_xyz, t1_desc = cpu_t1_sample(args, cfg, xyz_full)
             t1, _, _ = cpu_pipeline(t1_xyz, cfg, 1)
+            tn = numpy_port_seconds(t1_xyz, cfg, threads)
             line["cpu_baseline"] = {
                 "value": len(xyz_full) / (t * 1e6), "unit": "Mpts/s", "cores": threads,
                 "kind": "port",
@@ -625,7 +638,13 @@ def run_b200(args):
                           f"multi-threaded C port of the reference path (oracle/c), {cpu_model()}",
                 "stages_s": st,
                 "single_thread": {"value": len(t1_xyz) / (t1 * 1e6), "unit": "Mpts/s",
-                                  "cores": 1, "seconds": t1, "sample": t1_desc}}
+                                  "cores": 1, "seconds": t1, "sample": t1_desc},
+                "numpy_port": {"value": len(t1_xyz) / (tn * 1e6), "unit": "Mpts/s",
+                               "cores": threads, "seconds": tn, "sample": t1_desc,
+                               "what": "oracle/*.py: the reference's own numpy operations "
+                                       "(stable argsort, ufunc.at, scipy maximum_filter) "
+                                       "restated op for op, its thread pools as in the "
+                                       "reference -- how fast the reference itself runs"}}
         del xyz_full
     elif rank == 0 and args.mode == "batch" and world == 1 and not args.no_cpu and \
             not args.profile:

@@ -85,9 +85,10 @@ def test_device_ingest_matches_reference(name, chunk, tmp_path):
     cloud = cloud_io.load_pcd_binary(path, chunk_bytes=chunk)
     g = GOLD[name]
     assert (len(cloud), cloud.dropped) == (g["n"], g["dropped"])
-    xyz = cloud.xyz
-    assert xyz.dtype == np.float32
-    assert _sha(xyz.astype(np.float64)) == g["xyz_sha256"]
+    assert cloud.points.dtype == np.float32         # what the device path keeps
+    xyz = cloud.xyz                                  # the reference's float64 view
+    assert xyz.dtype == np.float64
+    assert _sha(xyz) == g["xyz_sha256"]
 
 
 @pytest.mark.gpu
