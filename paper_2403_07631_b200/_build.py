@@ -46,8 +46,9 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     deps = cu + sorted(CSRC.glob("*.cuh")) + sorted(CSRC.glob("*.h")) + [INCLUDE / "pct.h"]
     out = LIB / "libpct.so"
     if force or _stale(out, deps):
-        objs = []
-        for src in cu:
+        from concurrent.futures import ThreadPoolExecutor
+
+        def compile_one(src):
             obj = LIB / (src.stem + ".o")
             cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
             r = subprocess.run(cmd, capture_output=True, text=True)
@@ -57,7 +58,11 @@ def build(force: bool = False, verbose: bool = False) -> Path:
             if verbose:
                 sys.stderr.write(r.stderr)
             (LIB / (src.stem + ".ptxas.txt")).write_text(r.stderr)
-            objs.append(str(obj))
+            return str(obj)
+
+        # one nvcc per translation unit, in parallel (k_evaluate.cu dominates)
+        with ThreadPoolExecutor(max(1, min(len(cu), os.cpu_count() or 1))) as ex:
+            objs = list(ex.map(compile_one, cu))
         cmd = [nvcc(), *ARCH, "-shared", "-o", str(out), *objs, "-lcudart"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:

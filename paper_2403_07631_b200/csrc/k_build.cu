@@ -434,18 +434,20 @@ __device__ __forceinline__ unsigned block_incl_scan(unsigned x, unsigned *wsum, 
 }
 
 __global__ void __launch_bounds__(1024) tile_sums_kernel(const unsigned *__restrict__ cnt, int n,
-                                                         unsigned *__restrict__ bsum) {
+                                                         unsigned *__restrict__ bsum,
+                                                         int stride) {
   __shared__ unsigned wsum[32];
   const int i = blockIdx.x * 1024 + threadIdx.x;
   unsigned total;
-  block_incl_scan(i < n ? __ldcg(cnt + (int64_t)i * kCtrPad) : 0u, wsum, total);
+  block_incl_scan(i < n ? __ldcg(cnt + (int64_t)i * stride) : 0u, wsum, total);
   if (threadIdx.x == 0) bsum[blockIdx.x] = total;
 }
 
 __global__ void __launch_bounds__(1024) tile_offsets_kernel(const unsigned *__restrict__ cnt,
                                                             int n, const unsigned *__restrict__ bsum,
                                                             unsigned *__restrict__ offs,
-                                                            unsigned *__restrict__ cursor) {
+                                                            unsigned *__restrict__ cursor,
+                                                            int stride) {
   __shared__ unsigned wsum[32];
   __shared__ unsigned base;
   const int t = threadIdx.x;
@@ -457,13 +459,13 @@ __global__ void __launch_bounds__(1024) tile_offsets_kernel(const unsigned *__re
     if (t == 0) base = s;
   }
   const int i = blockIdx.x * 1024 + t;
-  const unsigned v = i < n ? __ldcg(cnt + (int64_t)i * kCtrPad) : 0u;
+  const unsigned v = i < n ? __ldcg(cnt + (int64_t)i * stride) : 0u;
   unsigned total;
   const unsigned incl = block_incl_scan(v, wsum, total);  // its barriers also publish `base`
   const unsigned excl = base + incl - v;
   if (i < n) {
     offs[i] = excl;
-    cursor[(int64_t)i * kCtrPad] = excl;
+    if (cursor) cursor[(int64_t)i * stride] = excl;
   }
   if (blockIdx.x == gridDim.x - 1 && t == 0) offs[n] = base + total;
 }
@@ -516,6 +518,199 @@ __global__ void __launch_bounds__(kTileNT) tile_reduce_kernel(
     uint32_t run = kKeyEmptyMin;
     for (int k = S - 1; k >= 0; --k) {
       const uint32_t v = ck[k * kTB2 + c];
+      run = v < run ? v : run;
+      __stcs(ceiling + (int64_t)k * out_stride + cell, decode_ceiling(run));
+    }
+  }
+}
+
+// ---------------------------------------- histogram-partitioned build (H)
+// The tile build's hash-merged passes replaced by per-CTA histograms: the
+// grid is exactly one CTA per SM and CTA c always takes the same contiguous
+// chunk of points, so
+//   H1 hist_count: each CTA counts its points per bucket (16 x 32 cells) in a
+//      private shared-memory histogram (plain shared atomics, no hashing, no
+//      global atomics) and writes it out whole: cnt[c][b];
+//   H2 hist_colscan + block scans: per bucket the column prefix over the
+//      CTAs and the bucket totals, then the exclusive scan of the totals, so
+//      CTA c's records of bucket b start at offs[b] + cnt[c][b];
+//   H3 hist_scatter: the same chunk again, one 8-byte record per point
+//      (key(f32 z) << 32 | bin << 9 | cell within the bucket) written at a
+//      shared-memory cursor -- deterministic positions, no global atomics;
+//   H4 hist_reduce: one CTA per bucket reduces max keys per (bin, cell) in
+//      shared memory and writes the ground planes, then re-reads the
+//      bucket's records (L2 hits) for the min keys and the ceiling planes
+//      (half the shared memory of a two-sided reduce: two CTAs per SM).
+// Traffic: 2 reads of the points + 8 B records out and back + the planes.
+constexpr int kHBH = 16, kHBW = 32;
+constexpr int kHB2 = kHBH * kHBW;          // 512 cells per bucket (9-bit local index)
+constexpr int kHistNT = 1024;              // H1 / H3 threads per CTA
+constexpr int kHistMaxBuckets = 48 * 1024;  // 192 KB of shared histogram
+constexpr int kHistMaxS = 100;             // H4: S x 512 x 4 B <= 200 KB
+
+template <typename T>
+__device__ __forceinline__ void load_point(const T *__restrict__ xyz, int64_t p, double &x,
+                                           double &y, double &z) {
+  x = (double)__ldg(xyz + 3 * p);
+  y = (double)__ldg(xyz + 3 * p + 1);
+  z = (double)__ldg(xyz + 3 * p + 2);
+}
+
+template <typename T, bool SCATTER>
+__global__ void __launch_bounds__(kHistNT, 1) hist_pass_kernel(
+    const T *__restrict__ xyz, int64_t n, BinArgs a, int nbx, int nb,
+    unsigned *__restrict__ cnt, const unsigned *__restrict__ offs,
+    unsigned long long *__restrict__ recs, unsigned long long *outside) {
+  extern __shared__ __align__(16) unsigned char hsmem[];
+  unsigned *h = reinterpret_cast<unsigned *>(hsmem);
+  double *hsm = reinterpret_cast<double *>(hsmem + (((size_t)nb * 4 + 15) & ~(size_t)15));
+  const int c = blockIdx.x, G = gridDim.x;
+  unsigned *mine = cnt + (int64_t)c * nb;
+  for (int b = threadIdx.x; b < nb; b += kHistNT) h[b] = SCATTER ? offs[b] + mine[b] : 0u;
+  const bool staged = a.S <= kMaxStagedHeights;
+  if (SCATTER && staged)
+    for (int k = threadIdx.x; k < a.S; k += kHistNT)
+      hsm[k] = a.derive ? plane_height(a, k) : a.heights[k];
+  __syncthreads();
+  const double *hts = staged ? hsm : a.heights;
+  auto one = [&](double x, double y, double z) {
+    int fi, fj, bin = 0;
+    if (!point_cell_bin<SCATTER>(x, y, z, a, hts, fi, fj, bin)) {
+      if (!SCATTER && outside) atomicAdd(outside, 1ull);
+      return;
+    }
+    const int b = (fi / kHBH) * nbx + fj / kHBW;
+    if (SCATTER) {
+      const unsigned pos = atomicAdd(&h[b], 1u);
+      const unsigned local = (unsigned)((fi % kHBH) * kHBW + fj % kHBW);
+      recs[pos] = ((unsigned long long)f32_key(__double2float_rn(z)) << 32) |
+                  ((unsigned long long)bin << 9) | local;
+    } else {
+      atomicAdd(&h[b], 1u);
+    }
+  };
+  // CTA c's chunk (the same in both passes), quad-aligned: float32 points
+  // are read 4 at a time as three 16-byte vectors (every load of a quad is
+  // issued before its arithmetic)
+  const int64_t p0 = (n * c / G) & ~(int64_t)3;
+  const int64_t p1 = c + 1 == G ? n : (n * (c + 1) / G) & ~(int64_t)3;
+  int64_t pq = p0;
+  if (sizeof(T) == 4 && (reinterpret_cast<uintptr_t>(xyz) & 15) == 0) {
+    const float4 *v = reinterpret_cast<const float4 *>(xyz);
+    const int64_t q1 = p1 >> 2;  // whole quads
+    for (int64_t q = (p0 >> 2) + threadIdx.x; q < q1; q += kHistNT) {
+      const float4 A = __ldg(v + 3 * q), B = __ldg(v + 3 * q + 1), Cv = __ldg(v + 3 * q + 2);
+      one(A.x, A.y, A.z);
+      one(A.w, B.x, B.y);
+      one(B.z, B.w, Cv.x);
+      one(Cv.y, Cv.z, Cv.w);
+    }
+    pq = q1 << 2;
+  }
+  for (int64_t p = pq + threadIdx.x; p < p1; p += kHistNT) {
+    double x, y, z;
+    load_point(xyz, p, x, y, z);
+    one(x, y, z);
+  }
+  if (!SCATTER) {
+    __syncthreads();
+    for (int b = threadIdx.x; b < nb; b += kHistNT) mine[b] = h[b];
+  }
+}
+
+// per bucket: column prefix over the CTAs (in place) and the bucket total
+__global__ void __launch_bounds__(256) hist_colscan_kernel(unsigned *__restrict__ cnt, int G,
+                                                           int nb, unsigned *__restrict__ tot) {
+  const int b = blockIdx.x * 256 + threadIdx.x;
+  if (b >= nb) return;
+  unsigned run = 0;
+  constexpr int U = 8;  // independent loads in flight
+  int c = 0;
+  for (; c + U <= G; c += U) {
+    unsigned v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = cnt[(int64_t)(c + u) * nb + b];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      cnt[(int64_t)(c + u) * nb + b] = run;
+      run += v[u];
+    }
+  }
+  for (; c < G; ++c) {
+    const unsigned v = cnt[(int64_t)c * nb + b];
+    cnt[(int64_t)c * nb + b] = run;
+    run += v;
+  }
+  tot[b] = run;
+}
+
+__global__ void __launch_bounds__(kHB2) hist_reduce_kernel(
+    const unsigned long long *__restrict__ recs, const unsigned *__restrict__ offs, int nbx,
+    int rows, int cols, int S, int64_t out_stride, float *__restrict__ ground,
+    float *__restrict__ ceiling) {
+  extern __shared__ uint32_t hk[];  // [S][512] max keys, then min keys
+  const int b = blockIdx.x, t = threadIdx.x;
+  const unsigned r0 = offs[b], r1 = offs[b + 1];
+  if (t == 0 && r1 > r0) {  // the bucket's records DRAM -> L2 while the keys are initialised
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(recs + r0) & ~(uintptr_t)15;
+    const uintptr_t a1 = (reinterpret_cast<uintptr_t>(recs + r1) + 15) & ~(uintptr_t)15;
+    for (uintptr_t q = a0; q < a1; q += 65536) {
+      const unsigned nbytes = (unsigned)(a1 - q < 65536 ? a1 - q : 65536);
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(q), "r"(nbytes) : "memory");
+    }
+  }
+  const int bi = b / nbx, bj = b - bi * nbx;
+  const int i = bi * kHBH + t / kHBW, j = bj * kHBW + t % kHBW;
+  const bool live = i < rows && j < cols;
+  const int64_t cell = (int64_t)i * cols + j;
+  // ground: max key per (bin, cell), bins 0 .. S-1
+  for (int q = t; q < S * kHB2; q += kHB2) hk[q] = kKeyEmptyMax;
+  __syncthreads();
+  auto gmax = [&](unsigned long long rec) {
+    const int bin = (int)((rec >> 9) & 0x7FFFFFu);
+    if (bin < S) atomicMax(hk + bin * kHB2 + (unsigned)(rec & 511u), (uint32_t)(rec >> 32));
+  };
+  auto cmin = [&](unsigned long long rec) {
+    const int bin = (int)((rec >> 9) & 0x7FFFFFu);
+    if (bin > 0) atomicMin(hk + (bin - 1) * kHB2 + (unsigned)(rec & 511u), (uint32_t)(rec >> 32));
+  };
+  constexpr int U = 4;  // records in flight per thread
+  unsigned r = r0 + t;
+  for (; r + (U - 1) * kHB2 < r1; r += U * kHB2) {
+    unsigned long long v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = __ldg(recs + r + u * kHB2);  // kept in L2: read again
+#pragma unroll
+    for (int u = 0; u < U; ++u) gmax(v[u]);
+  }
+  for (; r < r1; r += kHB2) gmax(__ldg(recs + r));
+  __syncthreads();
+  if (live) {
+    uint32_t run = kKeyEmptyMax;
+    for (int k = 0; k < S; ++k) {
+      const uint32_t v = hk[k * kHB2 + t];
+      run = v > run ? v : run;
+      __stcs(ground + (int64_t)k * out_stride + cell, decode_ground(run));
+    }
+  }
+  __syncthreads();
+  // ceiling: min key per (bin, cell), bins 1 .. S stored at bin - 1
+  for (int q = t; q < S * kHB2; q += kHB2) hk[q] = kKeyEmptyMin;
+  __syncthreads();
+  r = r0 + t;
+  for (; r + (U - 1) * kHB2 < r1; r += U * kHB2) {
+    unsigned long long v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = __ldcs(recs + r + u * kHB2);
+#pragma unroll
+    for (int u = 0; u < U; ++u) cmin(v[u]);
+  }
+  for (; r < r1; r += kHB2) cmin(__ldcs(recs + r));
+  __syncthreads();
+  if (live) {
+    uint32_t run = kKeyEmptyMin;
+    for (int k = S - 1; k >= 0; --k) {
+      const uint32_t v = hk[k * kHB2 + t];
       run = v < run ? v : run;
       __stcs(ceiling + (int64_t)k * out_stride + cell, decode_ceiling(run));
     }
@@ -904,7 +1099,74 @@ int launch_build(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, const pct_
     derive = heights_host[k] == fr.z_min + t;
   }
   const bool whole = row0 == 0 && nrows == fr.rows;
-  const bool tiled = bmode ? bmode[0] == 't' : big_keys;
+  const bool tiled = bmode ? (bmode[0] == 't' || bmode[0] == 'h') : big_keys;
+  const int hbx = (fr.cols + kHBW - 1) / kHBW, hby = (nrows + kHBH - 1) / kHBH;
+  const int64_t hnb = (int64_t)hbx * hby;
+  if (tiled && !(bmode && bmode[0] == 't') && S <= kHistMaxS && hnb <= kHistMaxBuckets &&
+      n > 0 && n < (int64_t)UINT32_MAX) {
+    // histogram-partitioned build: scratch = heights | outside | cnt [G][nb] |
+    // totals | offsets | block sums | records
+    const int G = ctx->num_sms;
+    const size_t cbytes = ((size_t)G * hnb * 4 + 255) & ~(size_t)255;
+    const size_t tbytes = ((size_t)(hnb + 1) * 4 + 255) & ~(size_t)255;
+    const size_t sbytes = ((size_t)((hnb + 1023) / 1024) * 4 + 255) & ~(size_t)255;
+    if (int rc = ensure_scratch(ctx, hbytes + 256 + cbytes + 2 * tbytes + sbytes + (size_t)n * 8))
+      return rc;
+    char *b0 = static_cast<char *>(ctx->scratch);
+    double *hd = reinterpret_cast<double *>(b0);
+    unsigned long long *outs = reinterpret_cast<unsigned long long *>(b0 + hbytes);
+    unsigned *cnt = reinterpret_cast<unsigned *>(b0 + hbytes + 256);
+    unsigned *tot = reinterpret_cast<unsigned *>(b0 + hbytes + 256 + cbytes);
+    unsigned *offs = reinterpret_cast<unsigned *>(b0 + hbytes + 256 + cbytes + tbytes);
+    unsigned *bsum = reinterpret_cast<unsigned *>(b0 + hbytes + 256 + cbytes + 2 * tbytes);
+    unsigned long long *recs = reinterpret_cast<unsigned long long *>(
+        b0 + hbytes + 256 + cbytes + 2 * tbytes + sbytes);
+    if (!derive) PCT_CUDA(ctx, upload_async(ctx, hd, heights_host, (size_t)S * sizeof(double)));
+    if (whole) outs = nullptr;
+    else PCT_CUDA(ctx, cudaMemsetAsync(outs, 0, 8, ctx->stream));
+    BinArgs a{fr.origin_x, fr.origin_y, fr.z_min, fr.r_g, fr.d_s, 1.0 / fr.r_g, 1.0 / fr.d_s,
+              hd, cells, nrows, fr.cols, S, row0, derive ? 1 : 0};
+    const size_t hist = ((size_t)hnb * 4 + 15) & ~(size_t)15;
+    const size_t hsm = hist + (S <= kMaxStagedHeights ? (size_t)S * sizeof(double) : 0);
+    const int nbi = (int)hnb;
+    if (dtype == PCT_F32) {
+      PCT_CUDA(ctx, cudaFuncSetAttribute(hist_pass_kernel<float, false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
+      hist_pass_kernel<float, false><<<G, kHistNT, hist, ctx->stream>>>(
+          static_cast<const float *>(xyz), n, a, hbx, nbi, cnt, nullptr, nullptr, outs);
+    } else {
+      PCT_CUDA(ctx, cudaFuncSetAttribute(hist_pass_kernel<double, false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
+      hist_pass_kernel<double, false><<<G, kHistNT, hist, ctx->stream>>>(
+          static_cast<const double *>(xyz), n, a, hbx, nbi, cnt, nullptr, nullptr, outs);
+    }
+    if (int rc = check_launch(ctx, "hist_count_kernel")) return rc;
+    hist_colscan_kernel<<<(unsigned)((hnb + 255) / 256), 256, 0, ctx->stream>>>(cnt, G, nbi, tot);
+    if (int rc = check_launch(ctx, "hist_colscan_kernel")) return rc;
+    const unsigned nsb = (unsigned)((hnb + 1023) / 1024);
+    tile_sums_kernel<<<nsb, 1024, 0, ctx->stream>>>(tot, nbi, bsum, 1);
+    if (int rc = check_launch(ctx, "tile_sums_kernel")) return rc;
+    tile_offsets_kernel<<<nsb, 1024, 0, ctx->stream>>>(tot, nbi, bsum, offs, nullptr, 1);
+    if (int rc = check_launch(ctx, "tile_offsets_kernel")) return rc;
+    if (dtype == PCT_F32) {
+      PCT_CUDA(ctx, cudaFuncSetAttribute(hist_pass_kernel<float, true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
+      hist_pass_kernel<float, true><<<G, kHistNT, hsm, ctx->stream>>>(
+          static_cast<const float *>(xyz), n, a, hbx, nbi, cnt, offs, recs, outs);
+    } else {
+      PCT_CUDA(ctx, cudaFuncSetAttribute(hist_pass_kernel<double, true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
+      hist_pass_kernel<double, true><<<G, kHistNT, hsm, ctx->stream>>>(
+          static_cast<const double *>(xyz), n, a, hbx, nbi, cnt, offs, recs, outs);
+    }
+    if (int rc = check_launch(ctx, "hist_scatter_kernel")) return rc;
+    const size_t rsm = (size_t)S * kHB2 * 4;
+    PCT_CUDA(ctx, cudaFuncSetAttribute(hist_reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)rsm));
+    hist_reduce_kernel<<<(unsigned)hnb, kHB2, rsm, ctx->stream>>>(recs, offs, hbx, nrows, fr.cols,
+                                                                  S, out_stride, ground, ceiling);
+    return check_launch(ctx, "hist_reduce_kernel");
+  }
   if (S <= kTileMaxS && n > 0 && n < (int64_t)UINT32_MAX && tiled) {
     // tile-partitioned build: scratch = heights | outside | counts | offsets |
     // cursors | records (the key planes above are not used)
@@ -938,9 +1200,9 @@ int launch_build(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, const pct_
           static_cast<const double *>(xyz), n, a, ntx, cnt, nullptr, outs);
     if (int rc = check_launch(ctx, "tile_count_kernel")) return rc;
     const unsigned nb = (unsigned)((ntiles + 1023) / 1024);
-    tile_sums_kernel<<<nb, 1024, 0, ctx->stream>>>(cnt, (int)ntiles, bsum);
+    tile_sums_kernel<<<nb, 1024, 0, ctx->stream>>>(cnt, (int)ntiles, bsum, kCtrPad);
     if (int rc = check_launch(ctx, "tile_sums_kernel")) return rc;
-    tile_offsets_kernel<<<nb, 1024, 0, ctx->stream>>>(cnt, (int)ntiles, bsum, offs, cur);
+    tile_offsets_kernel<<<nb, 1024, 0, ctx->stream>>>(cnt, (int)ntiles, bsum, offs, cur, kCtrPad);
     if (int rc = check_launch(ctx, "tile_offsets_kernel")) return rc;
     if (dtype == PCT_F32)
       tile_pass_kernel<float, true><<<g, 256, hsm, ctx->stream>>>(

@@ -77,7 +77,7 @@ def test_costs_bounded_and_barrier_where_no_ground(gpu):
     assert (cost[~np.isfinite(g)] == np.float32(p.c_barrier)).all()
 
 
-@pytest.mark.parametrize("build", ["atomic", "tiled"])
+@pytest.mark.parametrize("build", ["atomic", "tiled", "hist"])
 def test_build_variants_agree(cloud, gpu, monkeypatch, build):
     monkeypatch.setenv("PCT_BUILD", build)
     tom = pct.build_tomogram(pct.PointCloud(cloud), D_S, R_G)

@@ -119,10 +119,13 @@ def test_inflation_kernels_vs_oracle_random_costs(r_g, d_inf, d_sm, patch):
 
 @pytest.mark.parametrize("name", ["synth_cfg0", "ref_random_multilayer_s9", "ref_spiral_s3",
                                   "synth_cfg2_n2000000"])
-def test_tiled_build_matches_reference_golden(golden, monkeypatch, name):
-    """The tile-partitioned build (PCT_BUILD=tiled: bucket by 8x32-cell tile,
-    shared-memory segmented max / min) gives the reference's layers too."""
-    monkeypatch.setenv("PCT_BUILD", "tiled")
+@pytest.mark.parametrize("mode", ["tiled", "hist"])
+def test_tiled_build_matches_reference_golden(golden, monkeypatch, name, mode):
+    """The partitioned builds (PCT_BUILD=tiled: bucket by 8x32-cell tile with
+    hash-merged passes; PCT_BUILD=hist: per-CTA histograms of 16x32-cell
+    buckets; both reduce max / min in shared memory) give the reference's
+    layers too."""
+    monkeypatch.setenv("PCT_BUILD", mode)
     case = golden["cases"][name]
     xyz = case_input(name, case)
     for arr in (xyz, xyz.astype(np.float64)):
@@ -187,7 +190,7 @@ def test_extreme_shapes_vs_oracle(monkeypatch, shape):
     ref = oracle.build(xyz, d_s, r_g)
     cost = oracle.evaluate(ref["ground"], ref["ceiling"], r_g, TABLE_PARAMS)
     keep = oracle.simplify(ref["ground"], cost)
-    for build in ("atomic", "tiled"):
+    for build in ("atomic", "tiled", "hist"):
         monkeypatch.setenv("PCT_BUILD", build)
         tom, ev, simp = _run(xyz, d_s, r_g)
         _assert_layers_equal(ev.ground_stack(), ref["ground"], f"ground {build}")

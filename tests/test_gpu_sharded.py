@@ -65,8 +65,9 @@ def test_virtual_bands_fine_grid():
     assert keep1 == keep2
 
 
+@pytest.mark.parametrize("mode", ["tiled", "hist"])
 @pytest.mark.parametrize("P", [1, 3])
-def test_virtual_bands_tiled_build(golden, monkeypatch, P):
+def test_virtual_bands_tiled_build(golden, monkeypatch, P, mode):
     """The tile-partitioned build (chosen automatically for maps whose key
     planes exceed ~1.5 GB, e.g. config 3) on row bands."""
     monkeypatch.setenv("PCT_BUILD", "tiled")
@@ -74,7 +75,7 @@ def test_virtual_bands_tiled_build(golden, monkeypatch, P):
     xyz = case_input("synth_cfg0", case)
     monkeypatch.setenv("PCT_BUILD", "atomic")
     g1, c1, k1, keep1 = _single(xyz, 0.5, 0.1)
-    monkeypatch.setenv("PCT_BUILD", "tiled")
+    monkeypatch.setenv("PCT_BUILD", mode)
     g2, c2, k2, keep2 = _sharded(xyz, 0.5, 0.1, P)
     assert np.array_equal(g1.view(np.uint32), g2.view(np.uint32))
     assert np.array_equal(c1.view(np.uint32), c2.view(np.uint32))
