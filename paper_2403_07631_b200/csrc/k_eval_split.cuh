@@ -216,201 +216,6 @@ __global__ void __launch_bounds__(kWalkNT) terrain_walk_kernel(
   }
 }
 
-// Quad walk: as terrain_walk_kernel, but one thread owns FOUR consecutive
-// cells of a row (a warp = 128 columns = 4 bitmap words), so the per-slice
-// bookkeeping (addresses, loop control, the change map, the stores) is paid
-// once per 4 cells and the loads / stores are 16-byte vectors when the rows
-// are 16-byte aligned (VEC: cols % 4 == 0).  Inner left / right neighbours
-// are the thread's own registers; the outer ones come from the adjacent
-// lanes (lanes 0 / 31 load them).  A gentle bitmap word is the OR of the
-// nibbles of 8 lanes; the change-map byte of a word, a ballot of the lanes'
-// "changed" flags.  Cells past the grid hold NaN (no ground), so they never
-// count as neighbours.
-template <bool VEC>
-__device__ __forceinline__ void walk4_body(const float *__restrict__ ground,
-                                           const float *__restrict__ ceiling, int S, int rows,
-                                           int cols, float *__restrict__ enc_out,
-                                           const EncLayout &L, uint32_t *__restrict__ bits_out,
-                                           int wpr, unsigned char *__restrict__ chgmap,
-                                           int l2d, int kb, int ke) {
-  const int64_t cells = (int64_t)rows * cols;
-  const int64_t tidx = (int64_t)blockIdx.x * kWalkNT + threadIdx.x;
-  const int lane = threadIdx.x & 31;
-  const int tpr = wpr * 8;  // threads per row (4 cells each)
-  const int i0_ = (int)(tidx / tpr);
-  const int t = (int)(tidx - (int64_t)i0_ * tpr);
-  const int j0 = 4 * t;
-  const bool row_ok = i0_ < rows;
-  const int i = row_ok ? i0_ : rows - 1;
-  const int nlive = row_ok ? min(4, max(0, cols - j0)) : 0;  // live cells of this thread
-  const int jc = nlive > 0 ? j0 : 0;  // address formation only
-  const bool hu = nlive > 0 && i > 0, hd = nlive > 0 && i + 1 < rows;
-  const bool hl = nlive > 0 && j0 > 0;           // left neighbour of cell 0 exists
-  const bool hr = nlive == 4 && j0 + 4 < cols;   // right neighbour of cell 3 exists
-  const bool edge_l = lane == 0 && hl, edge_r = lane == 31 && hr;
-  const float nanf_ = bits_f32(kNaNBits);
-  const float cb32 = (float)c_K.c_barrier;
-  const int64_t base = (int64_t)i * cols + jc;
-  const float *pg = ground + base + (int64_t)kb * cells;
-  const float *pc = ceiling + base + (int64_t)kb * cells;
-  float *pe = enc_out + L.at(kb, i, jc);
-  const int64_t bstride = (int64_t)rows * wpr;
-  uint32_t *pb = bits_out + (int64_t)kb * bstride + (int64_t)i * wpr + (j0 >> 5);
-  const int64_t cmstride = (int64_t)((rows + 7) >> 3) * wpr;
-  unsigned char *pcm = chgmap + (int64_t)kb * cmstride + (int64_t)(i >> 3) * wpr + (j0 >> 5);
-  const bool gleader = (lane & 7) == 0 && row_ok && j0 < wpr * 32;
-
-  auto load4 = [&](const float *p, bool ok, float (&v)[4]) {
-    if (VEC) {
-      if (ok && nlive == 4) {
-        const float4 q = __ldg(reinterpret_cast<const float4 *>(p));
-        v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
-      } else {
-        v[0] = v[1] = v[2] = v[3] = nanf_;
-      }
-    } else {
-#pragma unroll
-      for (int q = 0; q < 4; ++q) v[q] = (ok && q < nlive) ? __ldg(p + q) : nanf_;
-    }
-  };
-  // current slice inputs and the prefetched next slice
-  float e[4], u[4], d[4], c[4], el = nanf_, er = nanf_;
-  float ne[4], nu[4], nd[4], nc[4], nel = nanf_, ner = nanf_;
-  auto fetch = [&](const float *g, const float *cc) {
-    load4(g, nlive > 0, ne);
-    load4(g - cols, hu, nu);
-    load4(g + cols, hd, nd);
-    load4(cc, nlive > 0, nc);
-    nel = edge_l ? __ldg(g - 1) : nanf_;
-    ner = edge_r ? __ldg(g + 4) : nanf_;
-  };
-  if (kb < ke) fetch(pg, pc);
-  const float *ng = pg + cells, *nc_ = pc + cells;
-
-  // previous slice's inputs (bit patterns) and per-cell state
-  uint32_t pe_[4] = {0, 0, 0, 0}, pu[4] = {0, 0, 0, 0}, pd[4] = {0, 0, 0, 0},
-           pcv[4] = {0, 0, 0, 0};
-  uint32_t pl = 0, pr = 0;
-  float tenc[4] = {nanf_, nanf_, nanf_, nanf_};
-  float enc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-  unsigned gent = 0u;  // bit q: cell q gentle
-  uint32_t prev_enc[4] = {0, 0, 0, 0};
-  unsigned prev_gent = 0u;
-  for (int k = kb; k < ke; ++k) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      e[q] = ne[q]; u[q] = nu[q]; d[q] = nd[q]; c[q] = nc[q];
-    }
-    el = nel; er = ner;
-    if (k + 1 < ke) {
-      fetch(ng, nc_);
-      if (l2d > 0 && nlive > 0 && k + 1 + l2d < ke) {  // DRAM -> L2 ahead, no registers held
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(ng + (int64_t)l2d * cells));
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(nc_ + (int64_t)l2d * cells));
-      }
-      ng += cells;
-      nc_ += cells;
-    }
-    // outer neighbours: adjacent lanes' edge cells (lanes 0 / 31 loaded theirs)
-    float l = __shfl_up_sync(0xFFFFFFFFu, e[3], 1);
-    float r = __shfl_down_sync(0xFFFFFFFFu, e[0], 1);
-    if (lane == 0) l = el;
-    if (lane == 31) r = er;
-    if (!hl) l = nanf_;
-    if (!hr) r = nanf_;
-    // which inputs changed since the slice below (all, for the first slice)
-    const bool first = k == kb;
-    unsigned ce = 0u, cud = 0u, ccv = 0u;  // ce bit q+1: cell q (bit 0: left, bit 5: right)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      ce |= (unsigned)(f32_bits(e[q]) != pe_[q]) << (q + 1);
-      cud |= (unsigned)(f32_bits(u[q]) != pu[q] || f32_bits(d[q]) != pd[q]) << q;
-      ccv |= (unsigned)(f32_bits(c[q]) != pcv[q]) << q;
-    }
-    ce |= (unsigned)(f32_bits(l) != pl) | ((unsigned)(f32_bits(r) != pr) << 5);
-    if (first) ce = cud = ccv = 0xFFu;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const bool live = q < nlive;
-      const bool xch = (((ce >> q) & 7u) != 0u) || ((cud >> q) & 1u);
-      if (xch && live) {
-        const float lq = q == 0 ? l : e[q - 1];
-        const float rq = q == 3 ? r : e[q + 1];
-        const FastCell tc = fast_terrain(Cross{e[q], lq, rq, u[q], d[q]}, c_K);
-        gent = (gent & ~(1u << q)) | ((unsigned)tc.gentle << q);
-        if (!tc.valid) {
-          tenc[q] = nanf_;
-        } else if (tc.isolated || tc.m_xy > c_K.theta_b) {
-          tenc[q] = cb32;
-        } else if (tc.gentle) {
-          tenc[q] = gentle_cost32(tc.gx, tc.gy, tc.s, c_K);
-        } else {
-          const double qq = div_const(tc.m_xy, c_K.theta_b, c_K.inv_theta_b);
-          tenc[q] = bits_f32(f32_bits((float)(c_K.alpha_b * (qq * qq))) | 0x80000000u);
-        }
-      }
-      if ((xch || ((ccv >> q) & 1u)) && live) {
-        if (!finite32(tenc[q])) {
-          enc[q] = cb32;  // no ground: barrier (fuse_costs :169)
-        } else {
-          const uint32_t tb = f32_bits(tenc[q]);
-          enc[q] = fuse_value(interval_value(e[q], c[q], c_K), bits_f32(tb & 0x7FFFFFFFu), c_K);
-          if (tb & 0x80000000u) enc[q] = bits_f32(f32_bits(enc[q]) | 0x80000000u);
-        }
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      pe_[q] = f32_bits(e[q]); pu[q] = f32_bits(u[q]); pd[q] = f32_bits(d[q]);
-      pcv[q] = f32_bits(c[q]);
-    }
-    pl = f32_bits(l);
-    pr = f32_bits(r);
-    // stores: encoded c_init, gentle word, change-map byte
-    if (VEC) {
-      if (nlive == 4) *reinterpret_cast<float4 *>(pe) = make_float4(enc[0], enc[1], enc[2], enc[3]);
-    } else {
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (q < nlive) pe[q] = enc[q];
-    }
-    pe += L.sstride;
-    const unsigned nib = gent & ((1u << nlive) - 1u);
-    unsigned word = nib << (4 * (lane & 7));
-    word |= __shfl_xor_sync(0xFFFFFFFFu, word, 1);
-    word |= __shfl_xor_sync(0xFFFFFFFFu, word, 2);
-    word |= __shfl_xor_sync(0xFFFFFFFFu, word, 4);
-    if (gleader) *pb = word;
-    pb += bstride;
-    if (chgmap) {  // uniform
-      bool ch = first || nib != prev_gent;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) ch |= q < nlive && f32_bits(enc[q]) != prev_enc[q];
-      const unsigned bal = __ballot_sync(0xFFFFFFFFu, ch);
-      if (gleader && ((bal >> (lane & 24)) & 0xFFu)) *pcm = 1;
-      prev_gent = nib;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) prev_enc[q] = f32_bits(enc[q]);
-    }
-    pcm += cmstride;
-  }
-}
-
-template <bool VEC, bool CHUNKED = false>
-__global__ void __launch_bounds__(kWalkNT) terrain_walk4_kernel(
-    const float *__restrict__ ground, const float *__restrict__ ceiling, int S, int rows,
-    int cols, float *__restrict__ enc_out, EncLayout L, uint32_t *__restrict__ bits_out,
-    int wpr, unsigned char *__restrict__ chgmap, int l2d) {
-  if constexpr (CHUNKED) {  // blockIdx.y = chunk of slices (small maps: more threads in flight)
-    const int kb = (int)((int64_t)S * blockIdx.y / gridDim.y);
-    const int ke = (int)((int64_t)S * (blockIdx.y + 1) / gridDim.y);
-    walk4_body<VEC>(ground, ceiling, S, rows, cols, enc_out, L, bits_out, wpr, chgmap, l2d, kb,
-                    ke);
-  } else {
-    walk4_body<VEC>(ground, ceiling, S, rows, cols, enc_out, L, bits_out, wpr, chgmap, l2d, 0, S);
-  }
-}
-
 // per-map arguments of the split evaluation (a single map is a batch of one)
 struct EvalMap {
   CUtensorMap tmap;  // encoded c_init stack (TMA), 64-byte aligned first member

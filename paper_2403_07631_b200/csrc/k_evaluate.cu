@@ -693,36 +693,6 @@ int launch_split(pct_ctx *ctx, const float *ground, const float *ceiling, int S,
     while (chunks < 4 && threads * chunks * 2 <= 2 * resident && S >= 6 * (chunks * 2)) chunks *= 2;
     if (const char *e = getenv("PCT_WALK_CHUNKS")) chunks = std::max(1, std::min(S, atoi(e)));
   }
-  // the quad walk (4 cells per thread) unless PCT_WALK=1
-  const char *wk = getenv("PCT_WALK");
-  if (!(wk && wk[0] == '1')) {
-    const int64_t t4 = (int64_t)rows * wpr * 8;
-    const unsigned g4 = (unsigned)((t4 + kWalkNT - 1) / kWalkNT);
-    int ch4 = 1;
-    {
-      const int64_t resident = (int64_t)ctx->num_sms * 2048;
-      const int64_t threads = (int64_t)g4 * kWalkNT;
-      while (ch4 < 8 && threads * ch4 * 2 <= 2 * resident && S >= 6 * (ch4 * 2)) ch4 *= 2;
-      if (const char *e = getenv("PCT_WALK_CHUNKS")) ch4 = std::max(1, std::min(S, atoi(e)));
-    }
-    const bool vec = (cols & 3) == 0 && (reinterpret_cast<uintptr_t>(ground) & 15) == 0 &&
-                     (reinterpret_cast<uintptr_t>(ceiling) & 15) == 0;
-    if (vec) {
-      if (ch4 > 1)
-        terrain_walk4_kernel<true, true><<<dim3(g4, ch4), kWalkNT, 0, ctx->stream>>>(
-            ground, ceiling, S, rows, cols, enc, L, bits, wpr, chgmap, l2d);
-      else
-        terrain_walk4_kernel<true><<<g4, kWalkNT, 0, ctx->stream>>>(
-            ground, ceiling, S, rows, cols, enc, L, bits, wpr, chgmap, l2d);
-    } else {
-      if (ch4 > 1)
-        terrain_walk4_kernel<false, true><<<dim3(g4, ch4), kWalkNT, 0, ctx->stream>>>(
-            ground, ceiling, S, rows, cols, enc, L, bits, wpr, chgmap, l2d);
-      else
-        terrain_walk4_kernel<false><<<g4, kWalkNT, 0, ctx->stream>>>(
-            ground, ceiling, S, rows, cols, enc, L, bits, wpr, chgmap, l2d);
-    }
-  } else
   // one slice of look-ahead measured fastest (cfg1 85 us vs 105 / 132 for
   // 2 / 4; deeper prefetch costs occupancy)
   if (pf && pf[0] == '2')
