@@ -216,6 +216,185 @@ __global__ void __launch_bounds__(kWalkNT) terrain_walk_kernel(
   }
 }
 
+// ---------------------------------------------------------------------------
+// Change masks + skipping walk.  A cell's encoded c_init and gentle flag at
+// slice k are functions of its 5-point ground cross and its ceiling at k
+// (walk_step recomputes only when those inputs change), and a plane cuts a
+// surface in few cells: on the campus map 5.4 % of the cells' inputs change
+// from one slice to the next, and only 7.3 % of the 32-cell warps see any
+// change at a slice.  So:
+//   change_mask_kernel: one streaming pass over ground / ceiling -> per cell
+//     gm bit k = ground[k] differs (bitwise) from ground[k-1], cm the same
+//     for the ceiling (bit 0 set), S <= 64;
+//   terrain_walk_skip_kernel: as terrain_walk_kernel, but a warp ORs its
+//     cells' input-change masks (own ground and ceiling, the 4 neighbours'
+//     ground) and loads / computes only at the slices where some lane's
+//     inputs changed; at the other slices every lane's encoded c_init and
+//     gentle flag are the previous slice's, which are stored again (the
+//     resolve / inflate kernel reads whole slices) -- no loads, no arithmetic.
+// The per-lane "changed" tests are the masks themselves (no bit compares).
+constexpr int kMaskNT = 256;
+
+__global__ void __launch_bounds__(kMaskNT) change_mask_kernel(
+    const float *__restrict__ ground, const float *__restrict__ ceiling, int S, int64_t cells,
+    unsigned long long *__restrict__ gm, unsigned long long *__restrict__ cm) {
+  const int64_t c = (int64_t)blockIdx.x * kMaskNT + threadIdx.x;
+  if (c >= cells) return;
+  constexpr int U = 8;  // independent loads in flight per array
+  unsigned long long g = 1ull, m = 1ull;
+  uint32_t pg = f32_bits(__ldcs(ground + c)), pc = f32_bits(__ldcs(ceiling + c));
+  int k = 1;
+  for (; k + U <= S; k += U) {
+    uint32_t vg[U], vc[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      vg[u] = f32_bits(__ldcs(ground + (int64_t)(k + u) * cells + c));
+      vc[u] = f32_bits(__ldcs(ceiling + (int64_t)(k + u) * cells + c));
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      g |= (unsigned long long)(vg[u] != pg) << (k + u);
+      m |= (unsigned long long)(vc[u] != pc) << (k + u);
+      pg = vg[u];
+      pc = vc[u];
+    }
+  }
+  for (; k < S; ++k) {
+    const uint32_t vg = f32_bits(__ldcs(ground + (int64_t)k * cells + c));
+    const uint32_t vc = f32_bits(__ldcs(ceiling + (int64_t)k * cells + c));
+    g |= (unsigned long long)(vg != pg) << k;
+    m |= (unsigned long long)(vc != pc) << k;
+    pg = vg;
+    pc = vc;
+  }
+  gm[c] = g;
+  cm[c] = m;
+}
+
+__device__ __forceinline__ unsigned long long warp_or64(unsigned long long v) {
+  const unsigned lo = __reduce_or_sync(0xFFFFFFFFu, (unsigned)v);
+  const unsigned hi = __reduce_or_sync(0xFFFFFFFFu, (unsigned)(v >> 32));
+  return ((unsigned long long)hi << 32) | lo;
+}
+
+template <bool CHUNKED>
+__global__ void __launch_bounds__(kWalkNT) terrain_walk_skip_kernel(
+    const float *__restrict__ ground, const float *__restrict__ ceiling, int S, int rows,
+    int cols, float *__restrict__ enc_out, EncLayout L, uint32_t *__restrict__ bits_out,
+    int wpr, unsigned char *__restrict__ chgmap, const unsigned long long *__restrict__ gmask,
+    const unsigned long long *__restrict__ cmask) {
+  int kb = 0, ke = S;
+  if constexpr (CHUNKED) {  // blockIdx.y = chunk of slices (small maps: more threads in flight)
+    kb = (int)((int64_t)S * blockIdx.y / gridDim.y);
+    ke = (int)((int64_t)S * (blockIdx.y + 1) / gridDim.y);
+  }
+  const int64_t cells = (int64_t)rows * cols;
+  const int64_t pidx = (int64_t)blockIdx.x * kWalkNT + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int pcols = wpr * 32;
+  const int i0_ = (int)(pidx / pcols), j0_ = (int)(pidx - (int64_t)i0_ * pcols);
+  const bool live = i0_ < rows && j0_ < cols;
+  const int i = i0_ < rows ? i0_ : rows - 1;
+  const int j = j0_ < cols ? j0_ : cols - 1;  // clamped: address formation only
+  const bool wlead = lane == 0 && i0_ < rows;
+  const bool hl = live && j > 0, hr = live && j + 1 < cols, hu = live && i > 0,
+             hd = live && i + 1 < rows;
+  const bool edge_l = lane == 0 && hl, edge_r = lane == 31 && hr;
+  const float nanf_ = bits_f32(kNaNBits);
+  const float cb32 = (float)c_K.c_barrier;
+  const int64_t base = (int64_t)i * cols + j;
+  // input-change masks: cross (own + 4 neighbours' ground) and interval (+ ceiling)
+  unsigned long long g_own = live ? __ldg(gmask + base) : 0ull;
+  unsigned long long xm = g_own;
+  if (hu) xm |= __ldg(gmask + base - cols);
+  if (hd) xm |= __ldg(gmask + base + cols);
+  unsigned long long gl = __shfl_up_sync(0xFFFFFFFFu, g_own, 1);
+  unsigned long long gr = __shfl_down_sync(0xFFFFFFFFu, g_own, 1);
+  if (lane == 0) gl = edge_l ? __ldg(gmask + base - 1) : 0ull;
+  if (lane == 31) gr = edge_r ? __ldg(gmask + base + 1) : 0ull;
+  if (hl) xm |= gl;
+  if (hr) xm |= gr;
+  const unsigned long long first = 1ull << kb;  // a chunk's first slice is computed in full
+  xm |= first;
+  const unsigned long long im = xm | (live ? __ldg(cmask + base) : 0ull);
+  const unsigned long long W = warp_or64(live ? im : first);  // warp-uniform
+  const unsigned long long kmask = ke >= 64 ? ~0ull : ((1ull << ke) - 1ull);
+  unsigned long long todo = W & kmask & ~((1ull << kb) - 1ull);
+
+  float *pe = enc_out + L.at(kb, i, j);
+  const int64_t bstride = (int64_t)rows * wpr;
+  uint32_t *pb = bits_out + (int64_t)kb * bstride + (int64_t)i * wpr + (j0_ >> 5);
+  const int64_t cmstride = (int64_t)((rows + 7) >> 3) * wpr;
+  unsigned char *pcm = chgmap ? chgmap + (int64_t)(i >> 3) * wpr + (j0_ >> 5) : nullptr;
+
+  // loads of one slice (grid borders read NaN)
+  float qe, qu, qd, qc, ql, qr;
+  auto fetch = [&](int k) {
+    const float *g = ground + base + (int64_t)k * cells;
+    qe = live ? __ldg(g) : nanf_;
+    qu = hu ? __ldg(g - cols) : nanf_;
+    qd = hd ? __ldg(g + cols) : nanf_;
+    qc = live ? __ldg(ceiling + base + (int64_t)k * cells) : nanf_;
+    ql = edge_l ? __ldg(g - 1) : nanf_;
+    qr = edge_r ? __ldg(g + 1) : nanf_;
+  };
+  int knext = todo ? __ffsll((long long)todo) - 1 : ke;  // next slice with a change
+  if (knext < ke) fetch(knext);
+  WalkState st;
+  st.tenc = nanf_;
+  uint32_t prev_enc = 0u;
+  unsigned word = 0u, prev_word = 0u;
+  for (int k = kb; k < ke; ++k) {
+    if (k == knext) {  // uniform: some lane's inputs changed
+      const float e = qe, u = qu, d = qd, c = qc;
+      float l = __shfl_up_sync(0xFFFFFFFFu, e, 1);
+      float r = __shfl_down_sync(0xFFFFFFFFu, e, 1);
+      if (lane == 0) l = ql;
+      if (lane == 31) r = qr;
+      if (!hl) l = nanf_;
+      if (!hr) r = nanf_;
+      todo &= todo - 1ull;
+      knext = todo ? __ffsll((long long)todo) - 1 : ke;
+      if (knext < ke) fetch(knext);  // in flight while this slice computes
+      const bool xch = (xm >> k) & 1ull, ich = (im >> k) & 1ull;
+      if (xch && live) {
+        const FastCell t = fast_terrain(Cross{e, l, r, u, d}, c_K);
+        st.gentle = t.gentle;
+        if (!t.valid) {
+          st.tenc = nanf_;
+        } else if (t.isolated || t.m_xy > c_K.theta_b) {
+          st.tenc = cb32;
+        } else if (t.gentle) {
+          st.tenc = gentle_cost32(t.gx, t.gy, t.s, c_K);
+        } else {
+          const double q = div_const(t.m_xy, c_K.theta_b, c_K.inv_theta_b);
+          st.tenc = bits_f32(f32_bits((float)(c_K.alpha_b * (q * q))) | 0x80000000u);
+        }
+      }
+      if (ich && live) {
+        if (!finite32(st.tenc)) {
+          st.enc = cb32;  // no ground: barrier (fuse_costs :169)
+        } else {
+          const uint32_t tb = f32_bits(st.tenc);
+          st.enc = fuse_value(interval_value(e, c, c_K), bits_f32(tb & 0x7FFFFFFFu), c_K);
+          if (tb & 0x80000000u) st.enc = bits_f32(f32_bits(st.enc) | 0x80000000u);
+        }
+      }
+      word = __ballot_sync(0xFFFFFFFFu, live && st.gentle);
+      if (pcm) {
+        const bool enc_changed = __any_sync(0xFFFFFFFFu, live && f32_bits(st.enc) != prev_enc);
+        if (wlead && (k == kb || word != prev_word || enc_changed)) pcm[(int64_t)k * cmstride] = 1;
+      }
+      prev_word = word;
+      prev_enc = f32_bits(st.enc);
+    }
+    if (live) *pe = st.enc;
+    pe += L.sstride;
+    if (wlead) *pb = word;
+    pb += bstride;
+  }
+}
+
 // per-map arguments of the split evaluation (a single map is a batch of one)
 struct EvalMap {
   CUtensorMap tmap;  // encoded c_init stack (TMA), 64-byte aligned first member

@@ -651,7 +651,9 @@ int launch_split(pct_ctx *ctx, const float *ground, const float *ceiling, int S,
   // gentle bitmap | (bnb) descriptor of a batch of one | walk change map
   const size_t cm_off = (((size_t)S * words * 4 + 255) / 256) * 256 + ((sizeof(EvalMap) + 128 + 255) / 256) * 256;
   const size_t cm_bytes = (size_t)S * ((rows + 7) / 8) * wpr;
-  if (int rc = ensure_scratch(ctx, cm_off + cm_bytes + 64)) return rc;
+  // then the walk's input-change masks (2 x 8 B per cell, S <= 64)
+  const size_t m_off = ((cm_off + cm_bytes + 64 + 255) / 256) * 256;
+  if (int rc = ensure_scratch(ctx, m_off + (S <= 64 ? 2 * (size_t)cells * 8 : 0))) return rc;
   uint32_t *bits = static_cast<uint32_t *>(ctx->scratch);
   // tiles whose window saw no change skip the resolve/inflate work: cfg2
   // (R = 8) bnb 798 -> 473 us, cfg3 (R = 4, open campus) 3.22 -> 2.00 ms;
@@ -693,6 +695,23 @@ int launch_split(pct_ctx *ctx, const float *ground, const float *ceiling, int S,
     while (chunks < 4 && threads * chunks * 2 <= 2 * resident && S >= 6 * (chunks * 2)) chunks *= 2;
     if (const char *e = getenv("PCT_WALK_CHUNKS")) chunks = std::max(1, std::min(S, atoi(e)));
   }
+  const char *wk = getenv("PCT_WALK");
+  if (S <= 64 && !(wk && wk[0] == '1')) {
+    // input-change masks, then the walk that skips the slices where none of
+    // a warp's inputs changed
+    unsigned long long *gm = reinterpret_cast<unsigned long long *>(
+        static_cast<char *>(ctx->scratch) + m_off);
+    unsigned long long *cmk = gm + cells;
+    change_mask_kernel<<<(unsigned)((cells + kMaskNT - 1) / kMaskNT), kMaskNT, 0, ctx->stream>>>(
+        ground, ceiling, S, cells, gm, cmk);
+    if (int rc = check_launch(ctx, "change_mask_kernel")) return rc;
+    if (chunks > 1)
+      terrain_walk_skip_kernel<true><<<dim3(g1, chunks), kWalkNT, 0, ctx->stream>>>(
+          ground, ceiling, S, rows, cols, enc, L, bits, wpr, chgmap, gm, cmk);
+    else
+      terrain_walk_skip_kernel<false><<<g1, kWalkNT, 0, ctx->stream>>>(
+          ground, ceiling, S, rows, cols, enc, L, bits, wpr, chgmap, gm, cmk);
+  } else
   // one slice of look-ahead measured fastest (cfg1 85 us vs 105 / 132 for
   // 2 / 4; deeper prefetch costs occupancy)
   if (pf && pf[0] == '2')
