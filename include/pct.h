@@ -110,6 +110,15 @@ int pct_build(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, const pct_fra
 int pct_evaluate(pct_ctx *ctx, const float *ground, const float *ceiling, int32_t n_slices,
                  int32_t rows, int32_t cols, double r_g, const pct_trav_params *p,
                  const float *kernel_w, int32_t kside, float *cost);
+/* pct_evaluate with the slice-change masks of the stacks (the ones the
+   build wrote, pct_tomo_masks): the terrain walk then skips deriving them
+   (one pass over ground + ceiling).  masks: device [2][rows*cols] uint64,
+   bit k = ground / ceiling of slice k differs from slice k-1, bit 0 set;
+   NULL (or n_slices > 64) behaves as pct_evaluate. */
+int pct_evaluate_masked(pct_ctx *ctx, const float *ground, const float *ceiling, int32_t n_slices,
+                        int32_t rows, int32_t cols, double r_g, const pct_trav_params *p,
+                        const float *kernel_w, int32_t kside, const uint64_t *masks,
+                        float *cost);
 /* per-op entry points on one (rows, cols) layer, device pointers */
 int pct_interval_cost(pct_ctx *ctx, const float *ground, const float *ceiling, int32_t rows,
                       int32_t cols, const pct_trav_params *p, float *out);      /* :59-73 */
@@ -243,6 +252,9 @@ int pct_tomo_run_batch(pct_ctx **ctxs, int32_t n_ctx, int32_t n_maps, const void
 int pct_set_timing(pct_ctx *ctx, int on);
 int pct_last_stage_ms(pct_ctx *ctx, float ms[3]);
 int pct_tomo_frame(const pct_tomo *t, pct_frame *fr, double *heights, int32_t heights_cap);
+/* the build's slice-change masks of a tomogram (device; NULL if none), see
+   pct_evaluate_masked */
+const uint64_t *pct_tomo_masks(const pct_tomo *t);
 /* device pointer of a layer stack (NULL if absent), e.g. for zero-copy consumers */
 const float *pct_tomo_layer(const pct_tomo *t, int layer);
 /* copy slice k of a layer (or all slices if k < 0) to host memory; syncs */

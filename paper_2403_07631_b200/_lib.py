@@ -65,6 +65,9 @@ _SIGS = {
     "pct_build": ([_vp, _vp, _i64, C.c_int, C.POINTER(FrameC), _vp, _vp, _vp], C.c_int),
     "pct_evaluate": ([_vp, _vp, _vp, _i32, _i32, _i32, _d, C.POINTER(TravParamsC), _vp, _i32,
                       _vp], C.c_int),
+    "pct_evaluate_masked": ([_vp, _vp, _vp, _i32, _i32, _i32, _d, C.POINTER(TravParamsC), _vp,
+                             _i32, _vp, _vp], C.c_int),
+    "pct_tomo_masks": ([_vp], _vp),
     "pct_interval_cost": ([_vp, _vp, _vp, _i32, _i32, C.POINTER(TravParamsC), _vp], C.c_int),
     "pct_ground_cost": ([_vp, _vp, _i32, _i32, _d, C.POINTER(TravParamsC), _vp], C.c_int),
     "pct_slope_magnitudes": ([_vp, _vp, _i32, _i32, _d, _vp, _vp, _vp], C.c_int),

@@ -413,6 +413,22 @@ int pct_evaluate(pct_ctx *ctx, const float *ground, const float *ceiling, int32_
                          cost, kEvalFull);
 }
 
+int pct_evaluate_masked(pct_ctx *ctx, const float *ground, const float *ceiling, int32_t n_slices,
+                        int32_t rows, int32_t cols, double r_g, const pct_trav_params *p,
+                        const float *kernel_w, int32_t kside, const uint64_t *masks,
+                        float *cost) {
+  CTX_GUARD(ctx);
+  ctx->eval_masks = n_slices <= 64 ? reinterpret_cast<const unsigned long long *>(masks) : nullptr;
+  const int rc = pct_evaluate(ctx, ground, ceiling, n_slices, rows, cols, r_g, p, kernel_w, kside,
+                              cost);
+  ctx->eval_masks = nullptr;
+  return rc;
+}
+
+const uint64_t *pct_tomo_masks(const pct_tomo *t) {
+  return t ? reinterpret_cast<const uint64_t *>(t->masks) : nullptr;
+}
+
 int pct_interval_cost(pct_ctx *ctx, const float *ground, const float *ceiling, int32_t rows,
                       int32_t cols, const pct_trav_params *p, float *out) {
   CTX_GUARD(ctx);
@@ -503,6 +519,7 @@ int tomo_alloc(pct_ctx *ctx, const pct_frame &fr, pct_tomo **out) {
     pct_tomo_free(ctx, t);
     return cuda_fail(ctx, e, "cudaMallocAsync(tomogram)");
   }
+
   *out = t;
   return PCT_OK;
 }
@@ -547,8 +564,24 @@ int pct_tomo_build(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, int xyz_
   if ((rc = tomo_alloc(ctx, fr, &t))) return rc;
   t->heights.resize(fr.n_slices);
   pct_frame_compute(lo, hi, d_s, r_g, max_grid_side, &fr, t->heights.data(), fr.n_slices);
-  if ((rc = launch_build(ctx, dxyz, n, dtype, fr, t->heights.data(), t->ground, t->ceiling, 0, -1,
-                         0, scattered))) {
+  if (fr.n_slices <= 64) {  // slice-change masks for the evaluation (16 B per cell)
+    const size_t mb = 2 * (size_t)fr.rows * fr.cols * sizeof(unsigned long long);
+    if (cudaMallocFromPoolAsync(reinterpret_cast<void **>(&t->masks), mb, ctx->mempool,
+                                ctx->stream) != cudaSuccess) {
+      cudaGetLastError();
+      t->masks = nullptr;  // optional: the walk derives them
+    }
+  }
+  ctx->build_masks = t->masks;
+  ctx->build_masks_written = false;
+  rc = launch_build(ctx, dxyz, n, dtype, fr, t->heights.data(), t->ground, t->ceiling, 0, -1, 0,
+                    scattered);
+  ctx->build_masks = nullptr;
+  if (t->masks && !ctx->build_masks_written) {  // a build path that does not emit them
+    cudaFreeAsync(t->masks, ctx->stream);
+    t->masks = nullptr;
+  }
+  if (rc) {
     pct_tomo_free(ctx, t);
     return rc;
   }
@@ -584,8 +617,11 @@ int pct_tomo_evaluate(pct_ctx *ctx, pct_tomo *t, const pct_trav_params *p, const
   if (int rc = check_params(ctx, p)) return rc;
   const size_t bytes = (size_t)t->fr.n_slices * t->fr.rows * t->fr.cols * sizeof(float);
   if (!t->cost) PCT_CUDA(ctx, cudaMallocFromPoolAsync(reinterpret_cast<void **>(&t->cost), bytes, ctx->mempool, ctx->stream));
-  return launch_evaluate(ctx, t->ground, t->ceiling, t->fr.n_slices, t->fr.rows, t->fr.cols,
-                         t->fr.r_g, *p, kernel_w, kside, t->cost, kEvalFull);
+  ctx->eval_masks = t->masks;  // written by this tomogram's build (NULL: derived again)
+  const int rc = launch_evaluate(ctx, t->ground, t->ceiling, t->fr.n_slices, t->fr.rows,
+                                 t->fr.cols, t->fr.r_g, *p, kernel_w, kside, t->cost, kEvalFull);
+  ctx->eval_masks = nullptr;
+  return rc;
 }
 
 int pct_tomo_simplify(pct_ctx *ctx, pct_tomo *t, double eps_e, double c_barrier,
@@ -677,6 +713,7 @@ int pct_tomo_free(pct_ctx *ctx, pct_tomo *t) {
   if (t->ground) cudaFreeAsync(t->ground, s);
   if (t->ceiling) cudaFreeAsync(t->ceiling, s);
   if (t->cost) cudaFreeAsync(t->cost, s);
+  if (t->masks) cudaFreeAsync(t->masks, s);
   delete t;
   return PCT_OK;
 }

@@ -647,7 +647,7 @@ __global__ void __launch_bounds__(256) hist_colscan_kernel(unsigned *__restrict_
 __global__ void __launch_bounds__(kHB2) hist_reduce_kernel(
     const unsigned long long *__restrict__ recs, const unsigned *__restrict__ offs, int nbx,
     int rows, int cols, int S, int64_t out_stride, float *__restrict__ ground,
-    float *__restrict__ ceiling) {
+    float *__restrict__ ceiling, unsigned long long *__restrict__ masks) {
   extern __shared__ uint32_t hk[];  // [S][512] max keys, then min keys
   const int b = blockIdx.x, t = threadIdx.x;
   const unsigned r0 = offs[b], r1 = offs[b + 1];
@@ -686,12 +686,17 @@ __global__ void __launch_bounds__(kHB2) hist_reduce_kernel(
   for (; r < r1; r += kHB2) gmax(__ldg(recs + r));
   __syncthreads();
   if (live) {
-    uint32_t run = kKeyEmptyMax;
+    uint32_t run = kKeyEmptyMax, prev = 0u;
+    unsigned long long m = 1ull;  // slice-change mask (bit k: differs from slice k-1)
     for (int k = 0; k < S; ++k) {
       const uint32_t v = hk[k * kHB2 + t];
       run = v > run ? v : run;
-      __stcs(ground + (int64_t)k * out_stride + cell, decode_ground(run));
+      const float o = decode_ground(run);
+      if (k > 0 && f32_bits(o) != prev) m |= 1ull << (k & 63);
+      prev = f32_bits(o);
+      __stcs(ground + (int64_t)k * out_stride + cell, o);
     }
+    if (masks) masks[(int64_t)i * cols + j] = m;
   }
   __syncthreads();
   // ceiling: min key per (bin, cell), bins 1 .. S stored at bin - 1
@@ -708,12 +713,17 @@ __global__ void __launch_bounds__(kHB2) hist_reduce_kernel(
   for (; r < r1; r += kHB2) cmin(__ldcs(recs + r));
   __syncthreads();
   if (live) {
-    uint32_t run = kKeyEmptyMin;
+    uint32_t run = kKeyEmptyMin, prev = 0u;
+    unsigned long long m = 1ull;
     for (int k = S - 1; k >= 0; --k) {
       const uint32_t v = hk[k * kHB2 + t];
       run = v < run ? v : run;
-      __stcs(ceiling + (int64_t)k * out_stride + cell, decode_ceiling(run));
+      const float o = decode_ceiling(run);
+      if (k < S - 1 && f32_bits(o) != prev) m |= 1ull << ((k + 1) & 63);
+      prev = f32_bits(o);
+      __stcs(ceiling + (int64_t)k * out_stride + cell, o);
     }
+    if (masks) masks[(int64_t)rows * cols + (int64_t)i * cols + j] = m;
   }
 }
 
@@ -723,7 +733,8 @@ __global__ void __launch_bounds__(kHB2) hist_reduce_kernel(
 __device__ __forceinline__ void scan_body(uint32_t *__restrict__ gkey, uint32_t *__restrict__ ckey,
                                           int64_t cells, int S, int64_t out_stride,
                                           float *__restrict__ ground, float *__restrict__ ceiling,
-                                          bool ground_side) {
+                                          bool ground_side,
+                                          unsigned long long *__restrict__ masks = nullptr) {
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= cells) return;
   // scratch planes are dense (stride cells); output slice k of the band lives
@@ -734,6 +745,15 @@ __device__ __forceinline__ void scan_body(uint32_t *__restrict__ gkey, uint32_t 
   constexpr int U = 8;
   uint32_t run = kKeyEmptyMax;
   int k = 0;
+  // slice-change mask of the layer written (bit k: differs from slice k-1)
+  unsigned long long m = 1ull;
+  uint32_t prev = 0u;
+  auto note = [&](int kk, float o, bool ascending) {
+    if (ascending ? kk > 0 : kk < S - 1) {
+      if (f32_bits(o) != prev) m |= 1ull << ((ascending ? kk : kk + 1) & 63);
+    }
+    prev = f32_bits(o);
+  };
   if (ground_side) {
   for (; k + U <= S; k += U) {
     uint32_t v[U];
@@ -745,15 +765,20 @@ __device__ __forceinline__ void scan_body(uint32_t *__restrict__ gkey, uint32_t 
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       run = v[u] > run ? v[u] : run;
-      __stcs(ground + (int64_t)(k + u) * out_stride + c, decode_ground(run));
+      const float o = decode_ground(run);
+      note(k + u, o, true);
+      __stcs(ground + (int64_t)(k + u) * out_stride + c, o);
     }
   }
   for (; k < S; ++k) {
     const uint32_t v = __ldcs(gkey + (int64_t)k * cells + c);
     if (v != kKeyEmptyMax) gkey[(int64_t)k * cells + c] = kKeyEmptyMax;
     run = v > run ? v : run;
-    __stcs(ground + (int64_t)k * out_stride + c, decode_ground(run));
+    const float o = decode_ground(run);
+    note(k, o, true);
+    __stcs(ground + (int64_t)k * out_stride + c, o);
   }
+  if (masks) masks[c] = m;
   return;
   }
   run = kKeyEmptyMin;
@@ -768,23 +793,29 @@ __device__ __forceinline__ void scan_body(uint32_t *__restrict__ gkey, uint32_t 
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       run = v[u] < run ? v[u] : run;
-      __stcs(ceiling + (int64_t)(k - u) * out_stride + c, decode_ceiling(run));
+      const float o = decode_ceiling(run);
+      note(k - u, o, false);
+      __stcs(ceiling + (int64_t)(k - u) * out_stride + c, o);
     }
   }
   for (; k >= 0; --k) {
     const uint32_t v = __ldcs(ckey + (int64_t)k * cells + c);
     if (v != kKeyEmptyMin) ckey[(int64_t)k * cells + c] = kKeyEmptyMin;
     run = v < run ? v : run;
-    __stcs(ceiling + (int64_t)k * out_stride + c, decode_ceiling(run));
+    const float o = decode_ceiling(run);
+    note(k, o, false);
+    __stcs(ceiling + (int64_t)k * out_stride + c, o);
   }
+  if (masks) masks[cells + c] = m;
 }
 
 __global__ void __launch_bounds__(256) scan_kernel(uint32_t *__restrict__ gkey,
                                                    uint32_t *__restrict__ ckey,
                                                    int64_t cells, int S, int64_t out_stride,
                                                    float *__restrict__ ground,
-                                                   float *__restrict__ ceiling) {
-  scan_body(gkey, ckey, cells, S, out_stride, ground, ceiling, blockIdx.y == 0);
+                                                   float *__restrict__ ceiling,
+                                                   unsigned long long *__restrict__ masks) {
+  scan_body(gkey, ckey, cells, S, out_stride, ground, ceiling, blockIdx.y == 0, masks);
 }
 
 // ------------------------------------------------ batched maps (config 4)
@@ -1163,8 +1194,10 @@ int launch_build(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, const pct_
     const size_t rsm = (size_t)S * kHB2 * 4;
     PCT_CUDA(ctx, cudaFuncSetAttribute(hist_reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)rsm));
+    unsigned long long *mk = (whole && S <= 64) ? ctx->build_masks : nullptr;
     hist_reduce_kernel<<<(unsigned)hnb, kHB2, rsm, ctx->stream>>>(recs, offs, hbx, nrows, fr.cols,
-                                                                  S, out_stride, ground, ceiling);
+                                                                  S, out_stride, ground, ceiling, mk);
+    if (mk) ctx->build_masks_written = true;
     return check_launch(ctx, "hist_reduce_kernel");
   }
   if (S <= kTileMaxS && n > 0 && n < (int64_t)UINT32_MAX && tiled) {
@@ -1263,8 +1296,10 @@ int launch_build(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, const pct_
           static_cast<const double *>(xyz), n, a, gkey, ckey, outside);
     if (int rc = check_launch(ctx, "scatter_kernel")) return rc;
   }
+  unsigned long long *mk = (whole && S <= 64) ? ctx->build_masks : nullptr;
   scan_kernel<<<dim3((unsigned)((cells + 255) / 256), 2), 256, 0, ctx->stream>>>(
-      gkey, ckey, cells, S, out_stride, ground, ceiling);
+      gkey, ckey, cells, S, out_stride, ground, ceiling, mk);
+  if (mk) ctx->build_masks_written = true;
   if (int rc = check_launch(ctx, "scan_kernel")) return rc;
   ctx->keys_clean = true;  // the scan resets every key it reads
   return PCT_OK;

@@ -699,12 +699,18 @@ int launch_split(pct_ctx *ctx, const float *ground, const float *ceiling, int S,
   if (S <= 64 && !(wk && wk[0] == '1')) {
     // input-change masks, then the walk that skips the slices where none of
     // a warp's inputs changed
-    unsigned long long *gm = reinterpret_cast<unsigned long long *>(
-        static_cast<char *>(ctx->scratch) + m_off);
-    unsigned long long *cmk = gm + cells;
-    change_mask_kernel<<<(unsigned)((cells + kMaskNT - 1) / kMaskNT), kMaskNT, 0, ctx->stream>>>(
-        ground, ceiling, S, cells, gm, cmk);
-    if (int rc = check_launch(ctx, "change_mask_kernel")) return rc;
+    const unsigned long long *gm = ctx->eval_masks, *cmk = nullptr;
+    if (gm) {  // written by the build of these stacks
+      cmk = gm + cells;
+    } else {
+      unsigned long long *m = reinterpret_cast<unsigned long long *>(
+          static_cast<char *>(ctx->scratch) + m_off);
+      change_mask_kernel<<<(unsigned)((cells + kMaskNT - 1) / kMaskNT), kMaskNT, 0, ctx->stream>>>(
+          ground, ceiling, S, cells, m, m + cells);
+      if (int rc = check_launch(ctx, "change_mask_kernel")) return rc;
+      gm = m;
+      cmk = m + cells;
+    }
     if (chunks > 1)
       terrain_walk_skip_kernel<true><<<dim3(g1, chunks), kWalkNT, 0, ctx->stream>>>(
           ground, ceiling, S, rows, cols, enc, L, bits, wpr, chgmap, gm, cmk);

@@ -45,6 +45,13 @@ struct pct_ctx {
   bool keys_clean = false;
   cudaEvent_t spec_ev = nullptr;  // bounds read back ahead of the speculative scatter
   cudaEvent_t switch_ev = nullptr;  // pct_set_stream: old stream -> new stream join
+  // per-cell slice-change masks ([2][cells] uint64: ground, ceiling; bit k =
+  // the layer differs from slice k-1, bit 0 set; S <= 64): build_masks, when
+  // set, is where the whole-grid build writes them; eval_masks, when set,
+  // the evaluation's walk reads them instead of deriving them again
+  unsigned long long *build_masks = nullptr;
+  bool build_masks_written = false;
+  const unsigned long long *eval_masks = nullptr;
   // zero-padded encoded c_init stacks of the split evaluation; the padding
   // is cleared only when the layout changes (the interior is rewritten)
   void *enc = nullptr;
@@ -61,6 +68,8 @@ struct pct_tomo {
   float *ground = nullptr;   // (S, rows, cols)
   float *ceiling = nullptr;
   float *cost = nullptr;     // nullptr until evaluated
+  // slice-change masks written by the build (S <= 64), read by the walk
+  unsigned long long *masks = nullptr;
 };
 
 namespace pct {

@@ -17,7 +17,8 @@ from dataclasses import dataclass, replace
 import numpy as np
 
 from . import _lib
-from .tomogram import Layer, Tomogram, TomogramSlice, device_run, new_device_stack, upload_stack
+from .tomogram import (DeviceTomogram, Layer, Tomogram, TomogramSlice, device_run,
+                       new_device_stack, upload_stack)
 
 
 @dataclass(frozen=True)
@@ -260,9 +261,17 @@ def _evaluate_layers(ctx, grounds, ceilings, r_g, params, w):
         keep.append(st)
         cptr = st.ptr
     out = new_device_stack(ctx, S, rows, cols)
-    ctx.check(ctx.lib.pct_evaluate(ctx.h, gptr, cptr, S, rows, cols, float(r_g),
-                                   C.byref(_lib.trav_params_c(params, r_g)), w.ctypes.data,
-                                   w.shape[0], out.ptr), "pct_evaluate")
+    # the whole stacks of one device build: its slice-change masks spare the
+    # walk a pass over ground + ceiling
+    masks = None
+    if gsrc is not None and csrc is not None and gsrc[1] == 0 and csrc[1] == 0 and \
+            gsrc[0].owner is csrc[0].owner and gsrc[0].n_slices == S and \
+            isinstance(gsrc[0].owner, DeviceTomogram) and gsrc[0].ctx is ctx:
+        masks = ctx.lib.pct_tomo_masks(gsrc[0].owner.handle)
+    ctx.check(ctx.lib.pct_evaluate_masked(ctx.h, gptr, cptr, S, rows, cols, float(r_g),
+                                          C.byref(_lib.trav_params_c(params, r_g)),
+                                          w.ctypes.data, w.shape[0], masks, out.ptr),
+              "pct_evaluate")
     return out
 
 

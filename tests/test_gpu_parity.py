@@ -625,3 +625,42 @@ def test_bnb_tile_skipping_is_exact(golden, monkeypatch, name, skip):
     cost = pct.evaluate_tomogram(tom, pct.TravParams()).cost_stack()
     for k in range(cost.shape[0]):
         assert digest(cost[k]) == case["cost_slice_sha256"][k], f"cost slice {k}"
+
+
+def _np_masks(stack):
+    """bit k: slice k differs (bitwise) from slice k-1; bit 0 set."""
+    u = np.ascontiguousarray(stack).view(np.uint32)
+    m = np.ones(u.shape[1:], np.uint64)
+    for k in range(1, u.shape[0]):
+        m |= (u[k] != u[k - 1]).astype(np.uint64) << np.uint64(k)
+    return m
+
+
+@pytest.mark.parametrize("mode", ["atomic", "hist", "tiled"])
+def test_build_slice_change_masks(monkeypatch, mode):
+    """The build's per-cell slice-change masks (read by the terrain walk in
+    place of a pass over the stacks) equal the masks of its own layers."""
+    from paper_2403_07631_b200 import _lib, synth
+    monkeypatch.setenv("PCT_BUILD", mode)
+    xyz = synth.two_storey(120_000, seed=3)
+    tom = pct.build_tomogram(pct.PointCloud(xyz), 0.5, 0.1)
+    g, c = tom.ground_stack(), tom.ceiling_stack()
+    owner = tom.slices[0].ground.device[0].owner
+    ptr = owner.ctx.lib.pct_tomo_masks(owner.handle)
+    if mode == "tiled":  # the hash-merged tile build does not emit them
+        assert not ptr
+        return
+    assert ptr
+    cells = g.shape[1] * g.shape[2]
+    host = np.empty(2 * cells, np.uint64)
+    owner.ctx.check(owner.ctx.lib.pct_memcpy_d2h(owner.ctx.h, host.ctypes.data, ptr, host.nbytes))
+    assert np.array_equal(host[:cells].reshape(g.shape[1:]), _np_masks(g))
+    assert np.array_equal(host[cells:].reshape(g.shape[1:]), _np_masks(c))
+    # the evaluation with and without them is identical
+    ev = pct.evaluate_tomogram(tom, pct.TravParams())
+    from paper_2403_07631_b200.tomogram import Layer, Tomogram, TomogramSlice
+    host_tom = Tomogram([TomogramSlice(Layer(g[k], 0.1, tom.origin), Layer(c[k], 0.1, tom.origin),
+                                       s.plane_height, k) for k, s in enumerate(tom.slices)],
+                        tom.d_s, tom.z_min)
+    ev2 = pct.evaluate_tomogram(host_tom, pct.TravParams())
+    assert np.array_equal(ev.cost_stack().view(np.uint32), ev2.cost_stack().view(np.uint32))
