@@ -77,9 +77,17 @@ struct BnbGeom {
   static constexpr int O_U = O_BM + ((NBY * NBX * 4 + 15) / 16) * 16;
   static constexpr int O_CB = O_U + ((QY * QX * 4 + 15) / 16) * 16;     // u8 change blocks
   static constexpr int O_DB = O_CB + ((CBY * CBX + 15) / 16) * 16;      // u8 dirty blocks
-  static constexpr int O_BAR = O_DB + ((DBY * DBX + 15) / 16) * 16;
+  // sparse walk output: the tile + halo's encoded c_init and the raw gentle
+  // source words of the window as of the last loaded slice, and the fresh
+  // flags of the current slice (one per row and source word)
+  static constexpr int NSW = GWW + 1;
+  static constexpr int O_RAWC = O_DB + ((DBY * DBX + 15) / 16) * 16;
+  static constexpr int O_RAWW = O_RAWC + BUF;
+  static constexpr int O_FRB = O_RAWW + ((GH * NSW * 4 + 15) / 16) * 16;
+  static constexpr int O_BAR = O_FRB + ((GH * NSW + 15) / 16) * 16;
   static constexpr int SMEM = O_BAR + 128;  // 3 mbarriers, 3 x 2 coordinate slots, warp counts
   static_assert(TH % R == 0 && TW % R == 0 && CW % 4 == 0 && R % 4 == 0, "bnb tile geometry");
+  static_assert(TW % 32 == 0, "sparse merge: 4-cell groups never straddle a bitmap word");
   static_assert(TH * TW <= 65536, "u16 output indices");
   static_assert((TH * (TW / 4)) % 32 == 0, "warp-uniform output loop (ballots)");
   static_assert(SIDE <= 31 && NSB <= 10, "foothold window");
@@ -213,6 +221,9 @@ __global__ void __launch_bounds__(NT, MINB) resolve_inflate_bnb_kernel(
   float *ub = reinterpret_cast<float *>(smem + G::O_U);
   unsigned char *chg = smem + G::O_CB;
   unsigned char *dirty = smem + G::O_DB;
+  float *rawc = reinterpret_cast<float *>(smem + G::O_RAWC);
+  uint32_t *raww = reinterpret_cast<uint32_t *>(smem + G::O_RAWW);
+  unsigned char *frb = smem + G::O_FRB;
   uint64_t *bar = reinterpret_cast<uint64_t *>(smem + G::O_BAR);  // [3]
   int *slot = reinterpret_cast<int *>(smem + G::O_BAR + 32);      // [3][3]
   int *wcnt = reinterpret_cast<int *>(smem + G::O_BAR + 72);      // [NWARP]
@@ -316,6 +327,7 @@ __global__ void __launch_bounds__(NT, MINB) resolve_inflate_bnb_kernel(
     const int64_t cells = (int64_t)rows * cols, words = M.words;
     const uint32_t *bits_in = M.bits;
     float *cost = M.cost;
+    const bool sparse = M.fresh != nullptr;  // uniform
     // skippable slices of this item: no change of encoded c_init or gentle
     // flag in the tile + R + r window since the slice below (walk change map);
     // every thread checks a few (slice, block) bytes, changes are OR-ed into
@@ -370,14 +382,38 @@ __global__ void __launch_bounds__(NT, MINB) resolve_inflate_bnb_kernel(
     // column 32w + x, gentle column 0 = c_init column -r); resets
     const uint32_t *bk = bits_in + (int64_t)k * words;
     const int wpr = M.wpr;
-    for (int idx = tid; idx < G::GH * G::GWW; idx += NT) {
-      const int y = idx / G::GWW, w = idx - y * G::GWW;
-      const int gi = i0 - R - PR + y;
-      const int gj = j0 - R - PR + 32 * w;
-      uint32_t word = gentle_word(bk, wpr, gi, gj, rows, cols);
-      if (32 * w >= G::GW) word = 0;
-      else if (G::GW - 32 * w < 32) word &= (1u << (G::GW - 32 * w)) - 1u;
-      bits[idx] = word;
+    const int gj0 = j0 - R - PR, ws0 = gj0 >> 5;  // first source word (floor)
+    if (sparse) {
+      // raw source words, the fresh ones of this slice from memory, the
+      // others kept from the last loaded slice (first slice of an item: all)
+      for (int idx = tid; idx < G::GH * G::NSW; idx += NT) {
+        const int y = idx / G::NSW, sw = idx - y * G::NSW;
+        const int gi = i0 - R - PR + y, ws = ws0 + sw;
+        const bool inmap = gi >= 0 && gi < rows && ws >= 0 && ws < wpr;
+        const bool fr = !inmap || first || M.fresh[((int64_t)k * rows + gi) * M.fpitch + ws] != 0;
+        frb[idx] = fr;
+        if (fr) raww[idx] = inmap ? __ldg(bk + (int64_t)gi * wpr + ws) : 0u;
+      }
+      __syncthreads();
+      const int sh = gj0 & 31;
+      for (int idx = tid; idx < G::GH * G::GWW; idx += NT) {
+        const int y = idx / G::GWW, w = idx - y * G::GWW;
+        const uint32_t lo = raww[y * G::NSW + w], hi = raww[y * G::NSW + w + 1];
+        uint32_t word = sh ? __funnelshift_r(lo, hi, sh) : lo;
+        if (32 * w >= G::GW) word = 0;
+        else if (G::GW - 32 * w < 32) word &= (1u << (G::GW - 32 * w)) - 1u;
+        bits[idx] = word;
+      }
+    } else {
+      for (int idx = tid; idx < G::GH * G::GWW; idx += NT) {
+        const int y = idx / G::GWW, w = idx - y * G::GWW;
+        const int gi = i0 - R - PR + y;
+        const int gj = j0 - R - PR + 32 * w;
+        uint32_t word = gentle_word(bk, wpr, gi, gj, rows, cols);
+        if (32 * w >= G::GW) word = 0;
+        else if (G::GW - 32 * w < 32) word &= (1u << (G::GW - 32 * w)) - 1u;
+        bits[idx] = word;
+      }
     }
     for (int idx = tid; idx < G::CBY * G::CBX; idx += NT) chg[idx] = first ? 1 : 0;
     __syncthreads();
@@ -418,6 +454,16 @@ __global__ void __launch_bounds__(NT, MINB) resolve_inflate_bnb_kernel(
     for (int q = tid; q < G::CH * CW4; q += NT) {
       float4 v = lds4(ci + 4 * q);
       const int y = q / CW4, x = 4 * (q - y * CW4);
+      if (sparse) {  // cells the walk did not rewrite: the last loaded slice's value
+        // (4 cells never straddle a bitmap word: R % 4 == 0, TW % 32 == 0)
+        const int sw = ((j0 - R + x) >> 5) - ws0;
+        if (!frb[(y + PR) * G::NSW + sw]) {
+          v = lds4(rawc + 4 * q);
+          *reinterpret_cast<float4 *>(ci + 4 * q) = v;
+        } else {
+          *reinterpret_cast<float4 *>(rawc + 4 * q) = v;
+        }
+      }
       const uint32_t sgn = (f32_bits(v.x) | f32_bits(v.y) | f32_bits(v.z) | f32_bits(v.w));
       if (sgn & 0x80000000u) {  // branch-free cinit_resolve of the 4 cells
         const uint32_t ok = okb[y * G::CWW + (x >> 5)] >> (x & 31);  // 4 cells, one word

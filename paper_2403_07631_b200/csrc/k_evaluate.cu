@@ -651,9 +651,13 @@ int launch_split(pct_ctx *ctx, const float *ground, const float *ceiling, int S,
   // gentle bitmap | (bnb) descriptor of a batch of one | walk change map
   const size_t cm_off = (((size_t)S * words * 4 + 255) / 256) * 256 + ((sizeof(EvalMap) + 128 + 255) / 256) * 256;
   const size_t cm_bytes = (size_t)S * ((rows + 7) / 8) * wpr;
-  // then the walk's input-change masks (2 x 8 B per cell, S <= 64)
+  // then the walk's input-change masks (2 x 8 B per cell, S <= 64) and its
+  // fresh map (sparse output: one byte per slice, row and bitmap word)
   const size_t m_off = ((cm_off + cm_bytes + 64 + 255) / 256) * 256;
-  if (int rc = ensure_scratch(ctx, m_off + (S <= 64 ? 2 * (size_t)cells * 8 : 0))) return rc;
+  const int fpitch = (wpr + 15) & ~15;
+  const size_t f_off = m_off + (S <= 64 ? 2 * (size_t)cells * 8 : 0);
+  const size_t f_bytes = S <= 64 ? (size_t)S * rows * fpitch : 0;
+  if (int rc = ensure_scratch(ctx, f_off + f_bytes)) return rc;
   uint32_t *bits = static_cast<uint32_t *>(ctx->scratch);
   // tiles whose window saw no change skip the resolve/inflate work: cfg2
   // (R = 8) bnb 798 -> 473 us, cfg3 (R = 4, open campus) 3.22 -> 2.00 ms;
@@ -695,8 +699,35 @@ int launch_split(pct_ctx *ctx, const float *ground, const float *ceiling, int S,
     while (chunks < 4 && threads * chunks * 2 <= 2 * resident && S >= 6 * (chunks * 2)) chunks *= 2;
     if (const char *e = getenv("PCT_WALK_CHUNKS")) chunks = std::max(1, std::min(S, atoi(e)));
   }
+  // the resolve / inflate kernel's slices per work item: long runs reuse the
+  // previous slice (only the first slice of a run is computed in full); the
+  // longest run that still gives every resident CTA ~3 items (small maps:
+  // down to one slice per item; cfg0 evaluate 44 -> 36 us, cfg1 unchanged at 5)
+  int bnb_run = 1, bnb_slots = 1;
+  if constexpr (R == 4 || R == 8) {
+    if (bnb) {
+      auto kb = resolve_inflate_bnb_kernel<R, PR, TH, TW, BNT, kBnbMinBlocks<R>()>;
+      constexpr int bsmem = BnbGeom<R, PR, TH, TW>::SMEM;
+      PCT_CUDA(ctx, cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, bsmem));
+      int per_sm = 0;
+      PCT_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kb, BNT, bsmem));
+      bnb_slots = (int)std::max(1, per_sm) * ctx->num_sms;
+      const int64_t tiles = (int64_t)((cols + TW - 1) / TW) * ((rows + TH - 1) / TH);
+      const int64_t runs_per_tile = std::min<int64_t>(S, (3 * (int64_t)bnb_slots + tiles - 1) / tiles);
+      bnb_run = (int)((S + runs_per_tile - 1) / runs_per_tile);
+      if (const char *e = getenv("PCT_INFL_RUN")) bnb_run = std::max(1, atoi(e));
+      bnb_run = std::min(std::min(bnb_run, S), 64);  // per-item skip mask: 64 slices
+    }
+  }
+  // sparse walk output when the bnb kernel (which merges) consumes it
+  const char *spv = getenv("PCT_WALK_SPARSE");
+  unsigned char *fresh = nullptr;
   const char *wk = getenv("PCT_WALK");
   if (S <= 64 && !(wk && wk[0] == '1')) {
+    if (bnb && chgmap && !(spv && spv[0] == '0')) {
+      fresh = static_cast<unsigned char *>(ctx->scratch) + f_off;
+      PCT_CUDA(ctx, cudaMemsetAsync(fresh, 0, f_bytes, ctx->stream));
+    }
     // input-change masks, then the walk that skips the slices where none of
     // a warp's inputs changed
     const unsigned long long *gm = ctx->eval_masks, *cmk = nullptr;
@@ -713,10 +744,12 @@ int launch_split(pct_ctx *ctx, const float *ground, const float *ceiling, int S,
     }
     if (chunks > 1)
       terrain_walk_skip_kernel<true><<<dim3(g1, chunks), kWalkNT, 0, ctx->stream>>>(
-          ground, ceiling, S, rows, cols, enc, L, bits, wpr, chgmap, gm, cmk);
+          ground, ceiling, S, rows, cols, enc, L, bits, wpr, chgmap, gm, cmk, fresh, fpitch,
+          bnb_run);
     else
       terrain_walk_skip_kernel<false><<<g1, kWalkNT, 0, ctx->stream>>>(
-          ground, ceiling, S, rows, cols, enc, L, bits, wpr, chgmap, gm, cmk);
+          ground, ceiling, S, rows, cols, enc, L, bits, wpr, chgmap, gm, cmk, fresh, fpitch,
+          bnb_run);
   } else
   // one slice of look-ahead measured fastest (cfg1 85 us vs 105 / 132 for
   // 2 / 4; deeper prefetch costs occupancy)
@@ -761,19 +794,9 @@ int launch_split(pct_ctx *ctx, const float *ground, const float *ceiling, int S,
       PCT_CUDA(ctx, cb.set_symbol(c_bw, bw.data(), bw.size() * sizeof(float)));
       auto kb = resolve_inflate_bnb_kernel<R, PR, TH, TW, BNT, kBnbMinBlocks<R>()>;
       constexpr int bsmem = BnbGeom<R, PR, TH, TW>::SMEM;
-      PCT_CUDA(ctx, cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, bsmem));
-      int per_sm = 0;
-      PCT_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kb, BNT, bsmem));
-      const int64_t slots = (int64_t)std::max(1, per_sm) * ctx->num_sms;
-      // slices per work item: long runs reuse the previous slice (only the
-      // first slice of a run is computed in full); the longest run that
-      // still gives every resident CTA ~3 items (small maps: down to one
-      // slice per item; cfg0 evaluate 44 -> 36 us, cfg1 unchanged at 5)
+      const int64_t slots = bnb_slots;
       const int64_t tiles = (int64_t)((cols + TW - 1) / TW) * ((rows + TH - 1) / TH);
-      const int64_t runs_per_tile = std::min<int64_t>(S, (3 * slots + tiles - 1) / tiles);
-      int run = (int)((S + runs_per_tile - 1) / runs_per_tile);
-      if (const char *e = getenv("PCT_INFL_RUN")) run = std::max(1, atoi(e));
-      run = std::min(std::min(run, S), 64);  // per-item skip mask: 64 slices
+      const int run = bnb_run;
       const int64_t nitems = tiles * ((S + run - 1) / run);
       if (nitems > INT32_MAX) return fail(ctx, PCT_E_INVALID, "grid too large");
       const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nitems, slots));
@@ -796,6 +819,8 @@ int launch_split(pct_ctx *ctx, const float *ground, const float *ceiling, int S,
       hm.run = run;
       hm.words = words;
       hm.chg = chgmap;
+      hm.fresh = fresh;
+      hm.fpitch = fpitch;
       struct {
         EvalMap m;
         int off[2];
