@@ -71,7 +71,7 @@ struct BnbGeom {
   static constexpr int O_PL = NBUF * BUF;
   static constexpr int O_BITS = O_PL + NPL * PLANE * 4;
   static constexpr int O_OK = O_BITS + ((GH * GWW * 4 + 15) / 16) * 16;
-  static constexpr int O_OT = O_OK + ((CH * CWW * 4 + 15) / 16) * 16;  // output tile
+  static constexpr int O_OT = O_OK + ((CH * CWW * 4 + 127) / 128) * 128;  // output tile (TMA store source)
   static constexpr int O_SL = O_OT + TH * TW * 4;                      // u16 list
   static constexpr int O_BM = O_SL + ((TH * TW * 2 + 15) / 16) * 16;
   static constexpr int O_U = O_BM + ((NBY * NBX * 4 + 15) / 16) * 16;
@@ -328,6 +328,16 @@ __global__ void __launch_bounds__(NT, MINB) resolve_inflate_bnb_kernel(
     const uint32_t *bits_in = M.bits;
     float *cost = M.cost;
     const bool sparse = M.fresh != nullptr;  // uniform
+    const bool tstore = M.ostore != 0;       // uniform
+    // the output tile of slice k to global memory: one TMA bulk tensor store
+    // issued by thread 0 (the copy engine reads `ot`), else the threads' stores
+    auto put_tile = [&](int k, int i0, int j0) {
+      if (tstore) {
+        if (tid == 0) tma_store_3d(&M.omap, ot, j0, i0, k);
+      } else {
+        store_tile(cost + (int64_t)k * cells, rows, cols, i0, j0, tid);
+      }
+    };
     // skippable slices of this item: no change of encoded c_init or gentle
     // flag in the tile + R + r window since the slice below (walk change map);
     // every thread checks a few (slice, block) bytes, changes are OR-ed into
@@ -371,13 +381,15 @@ __global__ void __launch_bounds__(NT, MINB) resolve_inflate_bnb_kernel(
         }
       }
       if (skip) {  // outputs equal the previous slice's: store the kept tile
-        store_tile(cost + (int64_t)k * cells, rows, cols, i0, j0, tid);
+        put_tile(k, i0, j0);
         continue;
       }
       const int cur = lc % 3, prv = (lc + 2) % 3;
       ++lc;
       float *ci = reinterpret_cast<float *>(smem + G::O_BUF + cur * G::BUF);
       const float *cp = reinterpret_cast<const float *>(smem + G::O_BUF + prv * G::BUF);
+    // the output tile is rewritten below: bulk stores still reading it first
+    if (tstore && tid == 0) tma_store_wait_read();
     // ---- P0a: gentle bits of the window region (bit x of word w = gentle
     // column 32w + x, gentle column 0 = c_init column -r); resets
     const uint32_t *bk = bits_in + (int64_t)k * words;
@@ -660,13 +672,15 @@ __global__ void __launch_bounds__(NT, MINB) resolve_inflate_bnb_kernel(
         if (in_list) ot[idx] = acc;
       }
     }
+    if (tstore) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // ot -> TMA store
     __syncthreads();
     }  // tile changed
     // ---- P4: store the output tile (every output, every slice)
-    store_tile(cost + (int64_t)k * cells, rows, cols, i0, j0, tid);
+    put_tile(k, i0, j0);
     // the next step's first barrier orders P4's reads of `ot` before its P2
     }
   }
+  if (tid == 0) tma_store_wait_all();  // bulk stores done before the CTA leaves
 }
 
 // Host: the caller's kernel must have exactly the compiled class structure

@@ -351,76 +351,84 @@ __global__ void __launch_bounds__(kWalkNT) terrain_walk_skip_kernel(
   st.tenc = nanf_;
   uint32_t prev_enc = 0u;
   unsigned word = 0u, prev_word = 0u;
-  for (int k = kb; k < ke; ++k) {
-    const bool computed = k == knext;
-    if (computed) {  // uniform: some lane's inputs changed
-      const float e = qe, u = qu, d = qd, c = qc;
-      float l = __shfl_up_sync(0xFFFFFFFFu, e, 1);
-      float r = __shfl_down_sync(0xFFFFFFFFu, e, 1);
-      if (lane == 0) l = ql;
-      if (lane == 31) r = qr;
-      if (!hl) l = nanf_;
-      if (!hr) r = nanf_;
-      todo &= todo - 1ull;
-      knext = todo ? __ffsll((long long)todo) - 1 : ke;
-      if (knext < ke) fetch(knext);  // in flight while this slice computes
-      const bool xch = (xm >> k) & 1ull, ich = (im >> k) & 1ull;
-      if (xch && live) {
-        const FastCell t = fast_terrain(Cross{e, l, r, u, d}, c_K);
-        st.gentle = t.gentle;
-        if (!t.valid) {
-          st.tenc = nanf_;
-        } else if (t.isolated || t.m_xy > c_K.theta_b) {
-          st.tenc = cb32;
-        } else if (t.gentle) {
-          st.tenc = gentle_cost32(t.gx, t.gy, t.s, c_K);
-        } else {
-          const double q = div_const(t.m_xy, c_K.theta_b, c_K.inv_theta_b);
-          st.tenc = bits_f32(f32_bits((float)(c_K.alpha_b * (q * q))) | 0x80000000u);
-        }
-      }
-      if (ich && live) {
-        if (!finite32(st.tenc)) {
-          st.enc = cb32;  // no ground: barrier (fuse_costs :169)
-        } else {
-          const uint32_t tb = f32_bits(st.tenc);
-          st.enc = fuse_value(interval_value(e, c, c_K), bits_f32(tb & 0x7FFFFFFFu), c_K);
-          if (tb & 0x80000000u) st.enc = bits_f32(f32_bits(st.enc) | 0x80000000u);
-        }
-      }
-      word = __ballot_sync(0xFFFFFFFFu, live && st.gentle);
-      if (pcm) {
-        const bool enc_changed = __any_sync(0xFFFFFFFFu, live && f32_bits(st.enc) != prev_enc);
-        if (wlead && (k == kb || word != prev_word || enc_changed)) pcm[(int64_t)k * cmstride] = 1;
-      }
-      prev_word = word;
-      prev_enc = f32_bits(st.enc);
-      if (fresh) {
-        if (live) *pe = st.enc;
-        if (wlead) {
-          *pb = word;
-          fresh[((int64_t)k * rows + i) * fpitch + (j0_ >> 5)] = 1;
-        }
+  // one slice where some lane's inputs changed: loads (the next such slice's
+  // issued before the arithmetic), walk_step, gentle word, change-map byte
+  auto compute = [&](int k) {
+    const float e = qe, u = qu, d = qd, c = qc;
+    float l = __shfl_up_sync(0xFFFFFFFFu, e, 1);
+    float r = __shfl_down_sync(0xFFFFFFFFu, e, 1);
+    if (lane == 0) l = ql;
+    if (lane == 31) r = qr;
+    if (!hl) l = nanf_;
+    if (!hr) r = nanf_;
+    todo &= todo - 1ull;
+    knext = todo ? __ffsll((long long)todo) - 1 : ke;
+    if (knext < ke) fetch(knext);  // in flight while this slice computes
+    const bool xch = (xm >> k) & 1ull, ich = (im >> k) & 1ull;
+    if (xch && live) {
+      const FastCell t = fast_terrain(Cross{e, l, r, u, d}, c_K);
+      st.gentle = t.gentle;
+      if (!t.valid) {
+        st.tenc = nanf_;
+      } else if (t.isolated || t.m_xy > c_K.theta_b) {
+        st.tenc = cb32;
+      } else if (t.gentle) {
+        st.tenc = gentle_cost32(t.gx, t.gy, t.s, c_K);
+      } else {
+        const double q = div_const(t.m_xy, c_K.theta_b, c_K.inv_theta_b);
+        st.tenc = bits_f32(f32_bits((float)(c_K.alpha_b * (q * q))) | 0x80000000u);
       }
     }
-    if (!fresh) {
+    if (ich && live) {
+      if (!finite32(st.tenc)) {
+        st.enc = cb32;  // no ground: barrier (fuse_costs :169)
+      } else {
+        const uint32_t tb = f32_bits(st.tenc);
+        st.enc = fuse_value(interval_value(e, c, c_K), bits_f32(tb & 0x7FFFFFFFu), c_K);
+        if (tb & 0x80000000u) st.enc = bits_f32(f32_bits(st.enc) | 0x80000000u);
+      }
+    }
+    word = __ballot_sync(0xFFFFFFFFu, live && st.gentle);
+    if (pcm) {
+      const bool enc_changed = __any_sync(0xFFFFFFFFu, live && f32_bits(st.enc) != prev_enc);
+      if (wlead && (k == kb || word != prev_word || enc_changed)) pcm[(int64_t)k * cmstride] = 1;
+    }
+    prev_word = word;
+    prev_enc = f32_bits(st.enc);
+  };
+  if (!fresh) {  // dense output: every slice written
+    for (int k = kb; k < ke; ++k) {
+      if (k == knext) compute(k);  // uniform
       if (live) *pe = st.enc;
+      pe += L.sstride;
       if (wlead) *pb = word;
-    } else if (!computed && k % run == 0) {  // run start: whole slice in memory
-      if (live) *pe = st.enc;
-      if (wlead) {
-        *pb = word;
-        fresh[((int64_t)k * rows + i) * fpitch + (j0_ >> 5)] = 1;
-      }
+      pb += bstride;
     }
-    pe += L.sstride;
-    pb += bstride;
+    return;
+  }
+  // sparse output: only the slices this warp recomputed, and the run starts
+  // of the resolve / inflate kernel (loaded whole, without a previous slice)
+  unsigned long long ev = todo;
+  for (int k = (kb + run - 1) / run * run; k < ke; k += run) ev |= 1ull << k;
+  float *pe0 = enc_out + L.at(0, i, j);
+  uint32_t *pb0 = bits_out + (int64_t)i * wpr + (j0_ >> 5);
+  unsigned char *pf0 = fresh + (int64_t)i * fpitch + (j0_ >> 5);
+  while (ev) {
+    const int k = __ffsll((long long)ev) - 1;
+    ev &= ev - 1ull;
+    if (k == knext) compute(k);  // uniform
+    if (live) pe0[(int64_t)k * L.sstride] = st.enc;
+    if (wlead) {
+      pb0[(int64_t)k * bstride] = word;
+      pf0[(int64_t)k * rows * fpitch] = 1;
+    }
   }
 }
 
 // per-map arguments of the split evaluation (a single map is a batch of one)
 struct EvalMap {
   CUtensorMap tmap;  // encoded c_init stack (TMA), 64-byte aligned first member
+  CUtensorMap omap;  // cost stack (TMA store of output tiles), valid when ostore
   const float *ground, *ceiling;
   float *enc, *cost;
   uint32_t *bits;
@@ -432,6 +440,7 @@ struct EvalMap {
   // wrote slice k's c_init / gentle word w of row i (NULL: every slice written)
   const unsigned char *fresh;
   int fpitch;
+  int ostore;  // output tiles leave by TMA bulk tensor stores (omap)
 };
 
 // walk over a batch: blockIdx.y = map; blocks past the map's extent leave
@@ -592,6 +601,23 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, u
       " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
       "l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
       : "memory");
+}
+
+// shared -> global bulk tensor store (async proxy; the caller fences the
+// shared-memory writes it covers and waits before overwriting the source)
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap *map, const void *src, int x, int y,
+                                             int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(map),
+      "r"(x), "r"(y), "r"(z), "r"(smem_u32(src))
+      : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 template <int R, int PR, int TH, int TW>

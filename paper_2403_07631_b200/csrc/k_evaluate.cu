@@ -821,6 +821,18 @@ int launch_split(pct_ctx *ctx, const float *ground, const float *ceiling, int S,
       hm.chg = chgmap;
       hm.fresh = fresh;
       hm.fpitch = fpitch;
+      // output tiles by TMA bulk stores when the cost rows are 16-byte pitched
+      const char *tsv = getenv("PCT_BNB_TMA_STORE");
+      if ((cols & 3) == 0 && (reinterpret_cast<uintptr_t>(cost) & 15) == 0 &&
+          !(tsv && tsv[0] == '0')) {
+        const cuuint64_t odims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)S};
+        const cuuint64_t ostr[2] = {(cuuint64_t)cols * 4, (cuuint64_t)cols * rows * 4};
+        const cuuint32_t obox[3] = {(cuuint32_t)TW, (cuuint32_t)TH, 1};
+        if (encode(&hm.omap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, cost, odims, ostr, obox, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+          hm.ostore = 1;
+      }
       struct {
         EvalMap m;
         int off[2];

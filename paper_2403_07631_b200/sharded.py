@@ -161,6 +161,15 @@ def _ptr(t, offset_elems=0):
     return t.data_ptr() + 4 * int(offset_elems)
 
 
+def _torch_stream(device) -> int:
+    """torch's current stream as a cudaStream_t for libpct.  torch's default
+    stream is the legacy NULL stream, which pct_set_stream(NULL) would read
+    as "the context's own stream" (non-blocking: no ordering with torch's
+    work); it is passed as cudaStreamLegacy (0x1) instead."""
+    import torch
+    return torch.cuda.current_stream(device).cuda_stream or 1
+
+
 def check_bands(starts, H: int):
     """Every band must be at least as thick as the halo its neighbours read
     from it.  Decided from the shared frame on every rank alike, before any
@@ -206,8 +215,7 @@ def band_pipeline(xyz, d_s, r_g, params, rank, size, *, device=None, eps_e=1e-6,
     lib, h = ctx.lib, ctx.h
     # libpct and torch share one stream for the whole pipeline (ordering of
     # the NCCL buffers against the kernels); restored at the end
-    ctx.check(lib.pct_set_stream(h, C.c_void_p(torch.cuda.current_stream(xyz.device).cuda_stream)),
-              "set_stream")
+    ctx.check(lib.pct_set_stream(h, C.c_void_p(_torch_stream(xyz.device))), "set_stream")
     dt = torch.float32 if xyz.dtype == torch.float32 else torch.float64
     code = _lib.PCT_F32 if dt == torch.float32 else _lib.PCT_F64
     xyz = xyz.contiguous()
@@ -426,7 +434,7 @@ def tomogram_sharded(points, d_s: float, r_g: float, params=None, *, eps_e: floa
         ctx = _lib.context(dev.index)
         xyz = torch.empty(arr.shape, dtype=torch.float32 if arr.dtype == np.float32
                           else torch.float64, device=dev)
-        stream = torch.cuda.current_stream(dev).cuda_stream
+        stream = _torch_stream(dev)
         with ctx.lock:
             ctx.check(ctx.lib.pct_set_stream(ctx.h, C.c_void_p(stream)), "set_stream")
             ctx.check(ctx.lib.pct_memcpy_h2d(ctx.h, xyz.data_ptr(), arr.ctypes.data, arr.nbytes),
