@@ -618,9 +618,28 @@ int pct_tomo_evaluate(pct_ctx *ctx, pct_tomo *t, const pct_trav_params *p, const
   const size_t bytes = (size_t)t->fr.n_slices * t->fr.rows * t->fr.cols * sizeof(float);
   if (!t->cost) PCT_CUDA(ctx, cudaMallocFromPoolAsync(reinterpret_cast<void **>(&t->cost), bytes, ctx->mempool, ctx->stream));
   ctx->eval_masks = t->masks;  // written by this tomogram's build (NULL: derived again)
+  // per-tile cost-change masks for the simplify window (room for 32 x 32 tiles)
+  if (t->masks && t->fr.n_slices <= 64 && !t->tcm) {
+    const size_t tb = (size_t)((t->fr.rows + 31) / 32) * ((t->fr.cols + 31) / 32) * 8;
+    if (cudaMallocFromPoolAsync(reinterpret_cast<void **>(&t->tcm), tb, ctx->mempool,
+                                ctx->stream) != cudaSuccess) {
+      cudaGetLastError();
+      t->tcm = nullptr;
+    }
+  }
+  ctx->eval_tcm = t->tcm;
+  ctx->eval_tcm_written = false;
   const int rc = launch_evaluate(ctx, t->ground, t->ceiling, t->fr.n_slices, t->fr.rows,
                                  t->fr.cols, t->fr.r_g, *p, kernel_w, kside, t->cost, kEvalFull);
   ctx->eval_masks = nullptr;
+  ctx->eval_tcm = nullptr;
+  if (t->tcm && !ctx->eval_tcm_written) {  // an evaluation path that does not record them
+    cudaFreeAsync(t->tcm, ctx->stream);
+    t->tcm = nullptr;
+  } else if (t->tcm) {
+    t->tcm_th = ctx->tcm_th;
+    t->tcm_tw = ctx->tcm_tw;
+  }
   return rc;
 }
 
@@ -629,8 +648,16 @@ int pct_tomo_simplify(pct_ctx *ctx, pct_tomo *t, double eps_e, double c_barrier,
   CTX_GUARD(ctx);
   if (!t) return fail(ctx, PCT_E_INVALID, "tomogram is NULL");
   if (!t->cost) return fail(ctx, PCT_E_NOCOST, "slice has no cost layer; evaluate the tomogram first");
-  return pct_simplify(ctx, t->ground, t->cost, t->fr.n_slices, t->fr.rows, t->fr.cols, eps_e,
-                      c_barrier, keep_host, n_keep);
+  if (t->masks && t->tcm) {  // slice-change information of its build and evaluation
+    ctx->simp_gm = t->masks;
+    ctx->simp_tcm = t->tcm;
+    ctx->simp_th = t->tcm_th;
+    ctx->simp_tw = t->tcm_tw;
+  }
+  const int rc = pct_simplify(ctx, t->ground, t->cost, t->fr.n_slices, t->fr.rows, t->fr.cols,
+                              eps_e, c_barrier, keep_host, n_keep);
+  ctx->simp_gm = ctx->simp_tcm = nullptr;
+  return rc;
 }
 
 int pct_tomo_run(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, int xyz_on_host,
@@ -714,6 +741,7 @@ int pct_tomo_free(pct_ctx *ctx, pct_tomo *t) {
   if (t->ceiling) cudaFreeAsync(t->ceiling, s);
   if (t->cost) cudaFreeAsync(t->cost, s);
   if (t->masks) cudaFreeAsync(t->masks, s);
+  if (t->tcm) cudaFreeAsync(t->tcm, s);
   delete t;
   return PCT_OK;
 }

@@ -71,7 +71,7 @@ struct BnbGeom {
   static constexpr int O_PL = NBUF * BUF;
   static constexpr int O_BITS = O_PL + NPL * PLANE * 4;
   static constexpr int O_OK = O_BITS + ((GH * GWW * 4 + 15) / 16) * 16;
-  static constexpr int O_OT = O_OK + ((CH * CWW * 4 + 127) / 128) * 128;  // output tile (TMA store source)
+  static constexpr int O_OT = ((O_OK + CH * CWW * 4 + 127) / 128) * 128;  // output tile (TMA store source)
   static constexpr int O_SL = O_OT + TH * TW * 4;                      // u16 list
   static constexpr int O_BM = O_SL + ((TH * TW * 2 + 15) / 16) * 16;
   static constexpr int O_U = O_BM + ((NBY * NBX * 4 + 15) / 16) * 16;
@@ -88,6 +88,7 @@ struct BnbGeom {
   static constexpr int SMEM = O_BAR + 128;  // 3 mbarriers, 3 x 2 coordinate slots, warp counts
   static_assert(TH % R == 0 && TW % R == 0 && CW % 4 == 0 && R % 4 == 0, "bnb tile geometry");
   static_assert(TW % 32 == 0, "sparse merge: 4-cell groups never straddle a bitmap word");
+  static_assert(O_OT % 128 == 0, "TMA store source alignment");
   static_assert(TH * TW <= 65536, "u16 output indices");
   static_assert((TH * (TW / 4)) % 32 == 0, "warp-uniform output loop (ballots)");
   static_assert(SIDE <= 31 && NSB <= 10, "foothold window");
@@ -363,6 +364,7 @@ __global__ void __launch_bounds__(NT, MINB) resolve_inflate_bnb_kernel(
     __syncthreads();
     const uint64_t changed = (uint64_t)chgw[0] | ((uint64_t)chgw[1] << 32);
     const uint64_t skm = ~changed;  // bit j: slice k0 + j is skippable (bit 0 unused: first)
+    unsigned long long touched = 0ull;  // slices whose outputs may have changed (thread 0)
     for (int k = k0; k < k1; ++k) {
       const bool first = k == k0;
       const bool skip = !first && ((skm >> (k - k0)) & 1ull);
@@ -501,7 +503,9 @@ __global__ void __launch_bounds__(NT, MINB) resolve_inflate_bnb_kernel(
     }
     // a tile whose resolved c_init equals the previous slice's keeps every
     // output: straight to the store
-    if (__syncthreads_or(changed)) {
+    const bool tile_changed = __syncthreads_or(changed);
+    if (tile_changed) touched |= 1ull << (k & 63);
+    if (tile_changed) {
     // ---- P1: dirty output blocks; horizontal maxima planes; upper bound per
     // output block (3 x 3 c_init blocks cover every tap of its outputs' windows)
     {
@@ -679,6 +683,9 @@ __global__ void __launch_bounds__(NT, MINB) resolve_inflate_bnb_kernel(
     put_tile(k, i0, j0);
     // the next step's first barrier orders P4's reads of `ot` before its P2
     }
+    // per tile: the slices whose outputs may differ from the slice below
+    // (the first slice of a run counts as changed), for the simplify window
+    if (M.tcm && tid == 0 && touched) atomicOr(M.tcm + t, touched | (1ull << (k0 & 63)));
   }
   if (tid == 0) tma_store_wait_all();  // bulk stores done before the CTA leaves
 }

@@ -441,6 +441,9 @@ struct EvalMap {
   const unsigned char *fresh;
   int fpitch;
   int ostore;  // output tiles leave by TMA bulk tensor stores (omap)
+  // per output tile (S <= 64): bit k = the tile's outputs may differ from
+  // slice k-1 (NULL: not recorded); read by the simplify window
+  unsigned long long *tcm;
 };
 
 // walk over a batch: blockIdx.y = map; blocks past the map's extent leave

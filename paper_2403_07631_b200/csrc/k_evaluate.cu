@@ -821,6 +821,13 @@ int launch_split(pct_ctx *ctx, const float *ground, const float *ceiling, int S,
       hm.chg = chgmap;
       hm.fresh = fresh;
       hm.fpitch = fpitch;
+      if (ctx->eval_tcm && S <= 64) {  // per-tile cost-change masks for the simplify window
+        PCT_CUDA(ctx, cudaMemsetAsync(ctx->eval_tcm, 0, (size_t)tiles * 8, ctx->stream));
+        hm.tcm = ctx->eval_tcm;
+        ctx->eval_tcm_written = true;
+        ctx->tcm_th = TH;
+        ctx->tcm_tw = TW;
+      }
       // output tiles by TMA bulk stores when the cost rows are 16-byte pitched
       const char *tsv = getenv("PCT_BNB_TMA_STORE");
       if ((cols & 3) == 0 && (reinterpret_cast<uintptr_t>(cost) & 15) == 0 &&

@@ -173,6 +173,98 @@ __global__ void __launch_bounds__(kWinNT) window_kernel(SimpArgs A,
   window_phase(A, table);
 }
 
+// The same table from slice-change information, reading only where values
+// change.  A cell's (ground, cost) pair is constant between the slices where
+// its build mask (ground changed) or its evaluation tile's mask (some output
+// of the tile may have changed) has a bit: segments.  A cell can only be a
+// candidate (traversable and not covered from above) at the last slice of a
+// segment -- inside a segment the slice above holds equal values, which
+// cover it for eps_e >= 0 -- and a lower neighbour in its own segment covers
+// it too; the lower neighbours in older segments share one test per segment.
+// Warps load (coalesced) only at the union of their lanes' segment starts;
+// each lane keeps its last 16 segments in shared memory.
+struct SimpMasks {
+  const unsigned long long *gm;   // per cell: ground slice-change mask (bit 0 set)
+  const unsigned long long *tcm;  // per evaluation tile: outputs may have changed
+  int cols, th, tw, tx;           // cell -> tile of tcm
+};
+
+__global__ void __launch_bounds__(kWinNT) window_skip_kernel(SimpArgs A, SimpMasks M,
+                                                             unsigned long long *__restrict__ table) {
+  __shared__ float seg_e[kWin][kWinNT];
+  __shared__ float seg_c[kWin][kWinNT];
+  __shared__ unsigned char seg_s[kWin][kWinNT];
+  extern __shared__ unsigned long long btab[];  // [S]
+  for (int k = threadIdx.x; k < A.S; k += kWinNT) btab[k] = 0ull;
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * kWinNT;
+  const int64_t span = (A.cells + kWinNT - 1) / kWinNT * kWinNT;  // whole warps iterate together
+  const int tid = threadIdx.x;
+  for (int64_t cell = (int64_t)blockIdx.x * kWinNT + tid; cell < span; cell += stride) {
+    const bool live = cell < A.cells;
+    const int64_t c0 = live ? cell : 0;
+    unsigned long long vm = 1ull;
+    if (live) {
+      const int i = (int)(c0 / M.cols), j = (int)(c0 - (int64_t)i * M.cols);
+      vm |= __ldg(M.gm + c0) | __ldg(M.tcm + (int64_t)(i / M.th) * M.tx + j / M.tw);
+    }
+    const unsigned lo = __reduce_or_sync(0xFFFFFFFFu, (unsigned)vm);
+    const unsigned hi = __reduce_or_sync(0xFFFFFFFFu, (unsigned)(vm >> 32));
+    unsigned long long ev = (((unsigned long long)hi << 32) | lo) & ~1ull;
+    if (A.S < 64) ev &= (1ull << A.S) - 1ull;
+    const float *pg = A.ground + c0, *pc = A.cost + c0;
+    float cur_e = live ? __ldg(pg) : bits_f32(kNaNBits), cur_c = live ? __ldg(pc) : 0.f;
+    int cur_s = 0, nseg = 0;
+    // candidate test at slice k for the current segment (values e, c, start
+    // s) with the slice above (eu, cu) or none
+    auto candidate = [&](int k, bool has_up, float eu, float cu) {
+      const float e = cur_e, c = cur_c;
+      const bool up_ok = !has_up || !finite32(eu) || higher_than(eu, e, A.eps_e) || c < cu;
+      if (!(live && finite32(e) && c < A.c_barrier32 && up_ok)) return;
+      const int depth = k < kWin ? k : kWin;
+      const unsigned long long want = (1ull << kBit) | ((1ull << depth) - 1ull);
+      const unsigned long long known = *((volatile unsigned long long *)&btab[k]);
+      if ((known & want) == want) return;
+      unsigned long long m = 1ull << kBit;
+      int end = cur_s;  // older segments, newest first: [st, end)
+      for (int q = 1; q <= kWin && q <= nseg && end > k - depth; ++q) {
+        const int slot = (nseg - q) & (kWin - 1);
+        const int st = seg_s[slot][tid];
+        const float se = seg_e[slot][tid], sc = seg_c[slot][tid];
+        if (!finite32(se) || higher_than(e, se, A.eps_e) || c < sc) {
+          // lower neighbours a in [max(st, k - depth), end): bits j = k-1-a
+          const int a0 = st > k - depth ? st : k - depth;
+          const int jlo = k - end, jhi = k - 1 - a0;  // inclusive
+          m |= (((2ull << jhi) - 1ull) >> jlo) << jlo;
+        }
+        end = st;
+      }
+      if ((m & want & ~known) != 0ull) atomicOr(&btab[k], m & want);
+    };
+    while (ev) {
+      const int k = __ffsll((long long)ev) - 1;
+      ev &= ev - 1ull;
+      const float e = live ? __ldg(pg + (int64_t)k * A.stride) : bits_f32(kNaNBits);
+      const float c = live ? __ldg(pc + (int64_t)k * A.stride) : 0.f;
+      if ((vm >> k) & 1ull) {  // this lane's segment ends at k - 1
+        candidate(k - 1, true, e, c);
+        const int slot = nseg & (kWin - 1);
+        seg_s[slot][tid] = (unsigned char)cur_s;
+        seg_e[slot][tid] = cur_e;
+        seg_c[slot][tid] = cur_c;
+        ++nseg;
+        cur_s = k;
+        cur_e = e;
+        cur_c = c;
+      }
+    }
+    candidate(A.S - 1, false, 0.f, 0.f);
+  }
+  __syncthreads();
+  for (int k = tid; k < A.S; k += kWinNT)
+    if (btab[k]) atomicOr(table + k, btab[k]);
+}
+
 struct Triple {
   int below, k, above;
 };
@@ -396,7 +488,16 @@ int run_simplify(pct_ctx *ctx, const float *ground, const float *cost, int S, in
     const char *wb = getenv("PCT_WIN_BLOCKS");
     const int per_sm = wb ? atoi(wb) : window_blocks_per_sm(ctx, tab_smem);
     const unsigned grid = (unsigned)std::min<int64_t>(blocks_needed, (int64_t)per_sm * ctx->num_sms);
-    window_kernel<<<grid, kWinNT, tab_smem, ctx->stream>>>(A, table);
+    const char *ws = getenv("PCT_WIN_SKIP");
+    if (ctx->simp_gm && ctx->simp_tcm && S <= 64 && eps_e >= 0.0 && !(ws && ws[0] == '0')) {
+      SimpMasks M{ctx->simp_gm, ctx->simp_tcm, cols, ctx->simp_th, ctx->simp_tw,
+                  (cols + ctx->simp_tw - 1) / ctx->simp_tw};
+      PCT_CUDA(ctx, cudaFuncSetAttribute(window_skip_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tab_smem));
+      window_skip_kernel<<<grid, kWinNT, tab_smem, ctx->stream>>>(A, M, table);
+    } else {
+      window_kernel<<<grid, kWinNT, tab_smem, ctx->stream>>>(A, table);
+    }
   }
   if (int rc = check_launch(ctx, "window_kernel")) return rc;
   // host round trips through the context's pinned buffer (pageable copies

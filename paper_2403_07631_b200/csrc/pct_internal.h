@@ -52,6 +52,15 @@ struct pct_ctx {
   unsigned long long *build_masks = nullptr;
   bool build_masks_written = false;
   const unsigned long long *eval_masks = nullptr;
+  // per evaluation tile (th x tw cells): bit k = the tile's costs may differ
+  // from slice k-1.  eval_tcm, when set, is where the bnb evaluation writes
+  // them (eval_tcm_written, geometry in tcm_th / tcm_tw); simp_gm / simp_tcm,
+  // when set, let the simplify window read only where values change
+  unsigned long long *eval_tcm = nullptr;
+  bool eval_tcm_written = false;
+  int tcm_th = 0, tcm_tw = 0;
+  const unsigned long long *simp_gm = nullptr, *simp_tcm = nullptr;
+  int simp_th = 0, simp_tw = 0;
   // zero-padded encoded c_init stacks of the split evaluation; the padding
   // is cleared only when the layout changes (the interior is rewritten)
   void *enc = nullptr;
@@ -70,6 +79,9 @@ struct pct_tomo {
   float *cost = nullptr;     // nullptr until evaluated
   // slice-change masks written by the build (S <= 64), read by the walk
   unsigned long long *masks = nullptr;
+  // per evaluation tile cost-change masks written by the evaluation (S <= 64)
+  unsigned long long *tcm = nullptr;
+  int tcm_th = 0, tcm_tw = 0;
 };
 
 namespace pct {

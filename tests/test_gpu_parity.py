@@ -664,3 +664,32 @@ def test_build_slice_change_masks(monkeypatch, mode):
                         tom.d_s, tom.z_min)
     ev2 = pct.evaluate_tomogram(host_tom, pct.TravParams())
     assert np.array_equal(ev.cost_stack().view(np.uint32), ev2.cost_stack().view(np.uint32))
+
+
+@pytest.mark.parametrize("win_skip", ["1", "0"])
+def test_fused_run_simplify_matches_oracle(monkeypatch, win_skip):
+    """pct_tomo_run (build -> evaluate -> simplify on one device tomogram):
+    its simplify window reads only where the build's ground masks and the
+    evaluation's per-tile cost masks say values change (PCT_WIN_SKIP=1, the
+    default) -- the surviving slices equal the oracle's, as with the full
+    window (PCT_WIN_SKIP=0)."""
+    from paper_2403_07631_b200 import synth
+    from paper_2403_07631_b200.batch import stream_maps
+    monkeypatch.setenv("PCT_WIN_SKIP", win_skip)
+    rng = np.random.default_rng(17)
+    clouds = [synth.generate(4, 80_000, 3000 + m) for m in range(3)]
+    clouds.append(synth.spiral_ramp(400_000, seed=9))
+    # stacked floors with small height differences around eps_e and equal costs
+    n = 60_000
+    pts = []
+    for lvl, dz in enumerate((0.0, 2.0, 2.0 + 5e-7, 4.0, 4.0 + 2e-6)):
+        x, y = rng.uniform(0, 15, n), rng.uniform(0, 12, n)
+        pts.append(np.column_stack([x, y, np.full(n, dz) + (x > 7) * 0.3]))
+    clouds.append(np.concatenate(pts).astype(np.float32))
+    d_s = [0.5, 0.5, 0.5, 0.4, 0.25]
+    for xyz, ds in zip(clouds, d_s):
+        got = next(stream_maps([xyz], ds, 0.1, pct.TravParams(), workers=1))
+        ref = oracle.build(xyz, ds, 0.1)
+        cost = oracle.evaluate(ref["ground"], ref["ceiling"], 0.1, TABLE_PARAMS)
+        keep = oracle.simplify(ref["ground"], cost)
+        assert [s.plane_height for s in got.slices] == [float(ref["heights"][k]) for k in keep]
