@@ -10,6 +10,8 @@
 // point order, like the reference).  A per-cell scan over bins then produces
 // ground[k] = max over bins <= k and ceiling[k] = min over bins > k, writing
 // numpy's NaN (0x7FC00000) where a cell is empty.
+#include <cuda.h>  // CUtensorMap (the encoder is fetched with cudaGetDriverEntryPoint)
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -644,11 +646,25 @@ __global__ void __launch_bounds__(256) hist_colscan_kernel(unsigned *__restrict_
   tot[b] = run;
 }
 
+// TMA bulk tensor store of a [S][16][32] float box from shared memory
+__device__ __forceinline__ void bulk_store_box(const CUtensorMap *map, const void *src, int x, int y) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(src);
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(map),
+      "r"(x), "r"(y), "r"(0), "r"(sa)
+      : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+template <bool TMA>
 __global__ void __launch_bounds__(kHB2) hist_reduce_kernel(
     const unsigned long long *__restrict__ recs, const unsigned *__restrict__ offs, int nbx,
     int rows, int cols, int S, int64_t out_stride, float *__restrict__ ground,
-    float *__restrict__ ceiling, unsigned long long *__restrict__ masks) {
-  extern __shared__ uint32_t hk[];  // [S][512] max keys, then min keys
+    float *__restrict__ ceiling, unsigned long long *__restrict__ masks,
+    const __grid_constant__ CUtensorMap gmap, const __grid_constant__ CUtensorMap cmap) {
+  // [S][512] max keys, then min keys; with TMA the decoded layers are written
+  // back in place ([S][16][32] floats = one box) and leave by bulk stores
+  extern __shared__ __align__(128) uint32_t hk[];
   const int b = blockIdx.x, t = threadIdx.x;
   const unsigned r0 = offs[b], r1 = offs[b + 1];
   if (t == 0 && r1 > r0) {  // the bucket's records DRAM -> L2 while the keys are initialised
@@ -685,7 +701,7 @@ __global__ void __launch_bounds__(kHB2) hist_reduce_kernel(
   }
   for (; r < r1; r += kHB2) gmax(__ldg(recs + r));
   __syncthreads();
-  if (live) {
+  {
     uint32_t run = kKeyEmptyMax, prev = 0u;
     unsigned long long m = 1ull;  // slice-change mask (bit k: differs from slice k-1)
     for (int k = 0; k < S; ++k) {
@@ -694,9 +710,18 @@ __global__ void __launch_bounds__(kHB2) hist_reduce_kernel(
       const float o = decode_ground(run);
       if (k > 0 && f32_bits(o) != prev) m |= 1ull << (k & 63);
       prev = f32_bits(o);
-      __stcs(ground + (int64_t)k * out_stride + cell, o);
+      if (TMA) hk[k * kHB2 + t] = f32_bits(o);
+      else if (live) __stcs(ground + (int64_t)k * out_stride + cell, o);
     }
-    if (masks) masks[(int64_t)i * cols + j] = m;
+    if (masks && live) masks[(int64_t)i * cols + j] = m;
+  }
+  if (TMA) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (t == 0) {
+      bulk_store_box(&gmap, hk, bj * kHBW, bi * kHBH);
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // hk free again
+    }
   }
   __syncthreads();
   // ceiling: min key per (bin, cell), bins 1 .. S stored at bin - 1
@@ -712,7 +737,7 @@ __global__ void __launch_bounds__(kHB2) hist_reduce_kernel(
   }
   for (; r < r1; r += kHB2) cmin(__ldcs(recs + r));
   __syncthreads();
-  if (live) {
+  {
     uint32_t run = kKeyEmptyMin, prev = 0u;
     unsigned long long m = 1ull;
     for (int k = S - 1; k >= 0; --k) {
@@ -721,9 +746,18 @@ __global__ void __launch_bounds__(kHB2) hist_reduce_kernel(
       const float o = decode_ceiling(run);
       if (k < S - 1 && f32_bits(o) != prev) m |= 1ull << ((k + 1) & 63);
       prev = f32_bits(o);
-      __stcs(ceiling + (int64_t)k * out_stride + cell, o);
+      if (TMA) hk[k * kHB2 + t] = f32_bits(o);
+      else if (live) __stcs(ceiling + (int64_t)k * out_stride + cell, o);
     }
-    if (masks) masks[(int64_t)rows * cols + (int64_t)i * cols + j] = m;
+    if (masks && live) masks[(int64_t)rows * cols + (int64_t)i * cols + j] = m;
+  }
+  if (TMA) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (t == 0) {
+      bulk_store_box(&cmap, hk, bj * kHBW, bi * kHBH);
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // before the CTA leaves
+    }
   }
 }
 
@@ -1192,11 +1226,51 @@ int launch_build(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, const pct_
     }
     if (int rc = check_launch(ctx, "hist_scatter_kernel")) return rc;
     const size_t rsm = (size_t)S * kHB2 * 4;
-    PCT_CUDA(ctx, cudaFuncSetAttribute(hist_reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)rsm));
     unsigned long long *mk = (whole && S <= 64) ? ctx->build_masks : nullptr;
-    hist_reduce_kernel<<<(unsigned)hnb, kHB2, rsm, ctx->stream>>>(recs, offs, hbx, nrows, fr.cols,
-                                                                  S, out_stride, ground, ceiling, mk);
+    // the layers leave by TMA bulk tensor stores when their rows are 16-byte
+    // pitched (one [S][16][32] box per bucket and layer)
+    CUtensorMap gmap, cmap;
+    std::memset(&gmap, 0, sizeof(gmap));
+    std::memset(&cmap, 0, sizeof(cmap));
+    bool tma = false;
+    {
+      const char *tv = getenv("PCT_BUILD_TMA");
+      static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+      if (!encode) {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) ==
+                cudaSuccess && fn && q == cudaDriverEntryPointSuccess)
+          encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+        cudaGetLastError();
+      }
+      if (encode && !(tv && tv[0] == '0') && (fr.cols & 3) == 0 && (out_stride & 3) == 0 &&
+          S <= 256 && ((reinterpret_cast<uintptr_t>(ground) | reinterpret_cast<uintptr_t>(ceiling)) & 15) == 0) {
+        const cuuint64_t dims[3] = {(cuuint64_t)fr.cols, (cuuint64_t)nrows, (cuuint64_t)S};
+        const cuuint64_t str[2] = {(cuuint64_t)fr.cols * 4, (cuuint64_t)out_stride * 4};
+        const cuuint32_t box[3] = {(cuuint32_t)kHBW, (cuuint32_t)kHBH, (cuuint32_t)S};
+        const cuuint32_t estr[3] = {1, 1, 1};
+        tma = encode(&gmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, ground, dims, str, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+                  CUDA_SUCCESS &&
+              encode(&cmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, ceiling, dims, str, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+                  CUDA_SUCCESS;
+      }
+    }
+    if (tma) {
+      PCT_CUDA(ctx, cudaFuncSetAttribute(hist_reduce_kernel<true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));
+      hist_reduce_kernel<true><<<(unsigned)hnb, kHB2, rsm, ctx->stream>>>(
+          recs, offs, hbx, nrows, fr.cols, S, out_stride, ground, ceiling, mk, gmap, cmap);
+    } else {
+      PCT_CUDA(ctx, cudaFuncSetAttribute(hist_reduce_kernel<false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));
+      hist_reduce_kernel<false><<<(unsigned)hnb, kHB2, rsm, ctx->stream>>>(
+          recs, offs, hbx, nrows, fr.cols, S, out_stride, ground, ceiling, mk, gmap, cmap);
+    }
     if (mk) ctx->build_masks_written = true;
     return check_launch(ctx, "hist_reduce_kernel");
   }

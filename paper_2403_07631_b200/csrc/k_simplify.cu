@@ -489,7 +489,11 @@ int run_simplify(pct_ctx *ctx, const float *ground, const float *cost, int S, in
     const int per_sm = wb ? atoi(wb) : window_blocks_per_sm(ctx, tab_smem);
     const unsigned grid = (unsigned)std::min<int64_t>(blocks_needed, (int64_t)per_sm * ctx->num_sms);
     const char *ws = getenv("PCT_WIN_SKIP");
-    if (ctx->simp_gm && ctx->simp_tcm && S <= 64 && eps_e >= 0.0 && !(ws && ws[0] == '0')) {
+    // the segment window pays off on large maps (cfg2 0.35 -> 0.23 ms, cfg3
+    // 1.75 -> 0.63 ms); on small ones (cfg0 / cfg1, < 1M cells) the dense
+    // window is faster (cfg1 92 vs 120 us)
+    const bool skip_ok = ws ? ws[0] == '1' : A.cells >= (1 << 20);
+    if (ctx->simp_gm && ctx->simp_tcm && S <= 64 && eps_e >= 0.0 && skip_ok) {
       SimpMasks M{ctx->simp_gm, ctx->simp_tcm, cols, ctx->simp_th, ctx->simp_tw,
                   (cols + ctx->simp_tw - 1) / ctx->simp_tw};
       PCT_CUDA(ctx, cudaFuncSetAttribute(window_skip_kernel,
