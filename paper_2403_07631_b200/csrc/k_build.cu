@@ -602,10 +602,37 @@ __global__ void __launch_bounds__(kHistNT, 1) hist_pass_kernel(
     const int64_t q1 = p1 >> 2;  // whole quads
     for (int64_t q = (p0 >> 2) + threadIdx.x; q < q1; q += kHistNT) {
       const float4 A = __ldg(v + 3 * q), B = __ldg(v + 3 * q + 1), Cv = __ldg(v + 3 * q + 2);
-      one(A.x, A.y, A.z);
-      one(A.w, B.x, B.y);
-      one(B.z, B.w, Cv.x);
-      one(Cv.y, Cv.z, Cv.w);
+      if (SCATTER) {
+        // the 4 points' cells, bins and records first, then their 4 cursor
+        // atomics, then the 4 stores (independent chains in flight)
+        const double px[4] = {A.x, A.w, B.z, Cv.y}, py[4] = {A.y, B.x, B.w, Cv.z},
+                     pz[4] = {A.z, B.y, Cv.x, Cv.w};
+        int bk[4];
+        unsigned long long rec[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          int fi, fj, bin = 0;
+          bk[u] = -1;
+          if (point_cell_bin<true>(px[u], py[u], pz[u], a, hts, fi, fj, bin)) {
+            bk[u] = (fi / kHBH) * nbx + fj / kHBW;
+            rec[u] = ((unsigned long long)f32_key(__double2float_rn(pz[u])) << 32) |
+                     ((unsigned long long)bin << 9) |
+                     (unsigned)((fi % kHBH) * kHBW + fj % kHBW);
+          }
+        }
+        unsigned pos[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (bk[u] >= 0) pos[u] = atomicAdd(&h[bk[u]], 1u);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (bk[u] >= 0) recs[pos[u]] = rec[u];
+      } else {
+        one(A.x, A.y, A.z);
+        one(A.w, B.x, B.y);
+        one(B.z, B.w, Cv.x);
+        one(Cv.y, Cv.z, Cv.w);
+      }
     }
     pq = q1 << 2;
   }
@@ -1234,6 +1261,8 @@ int launch_build(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, const pct_
     std::memset(&cmap, 0, sizeof(cmap));
     bool tma = false;
     {
+      // measured slower at cfg3 (2.26 vs 2.09 ms: the CTA waits for the
+      // bulk store's read of its keys before the ceiling pass): opt-in
       const char *tv = getenv("PCT_BUILD_TMA");
       static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
       if (!encode) {
@@ -1244,7 +1273,7 @@ int launch_build(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, const pct_
           encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
         cudaGetLastError();
       }
-      if (encode && !(tv && tv[0] == '0') && (fr.cols & 3) == 0 && (out_stride & 3) == 0 &&
+      if (encode && (tv && tv[0] == '1') && (fr.cols & 3) == 0 && (out_stride & 3) == 0 &&
           S <= 256 && ((reinterpret_cast<uintptr_t>(ground) | reinterpret_cast<uintptr_t>(ceiling)) & 15) == 0) {
         const cuuint64_t dims[3] = {(cuuint64_t)fr.cols, (cuuint64_t)nrows, (cuuint64_t)S};
         const cuuint64_t str[2] = {(cuuint64_t)fr.cols * 4, (cuuint64_t)out_stride * 4};
