@@ -365,6 +365,16 @@ __global__ void __launch_bounds__(NT, MINB) resolve_inflate_bnb_kernel(
     const uint64_t changed = (uint64_t)chgw[0] | ((uint64_t)chgw[1] << 32);
     const uint64_t skm = ~changed;  // bit j: slice k0 + j is skippable (bit 0 unused: first)
     unsigned long long touched = 0ull;  // slices whose outputs may have changed (thread 0)
+    // sparse P0a prefetch registers: fresh byte + bitmap word of this
+    // thread's window entries for slice pf_k
+    constexpr int kPfEnt = (G::GH * G::NSW + NT - 1) / NT;
+    uint32_t pf_w[kPfEnt];
+    unsigned char pf_f[kPfEnt];
+    int pf_k = -1;
+    auto pf_load = [&](int e, int kk, int gi, int ws) {
+      pf_f[e] = M.fresh[((int64_t)kk * rows + gi) * M.fpitch + ws];
+      pf_w[e] = __ldg(M.bits + (int64_t)kk * words + (int64_t)gi * M.wpr + ws);
+    };
     for (int k = k0; k < k1; ++k) {
       const bool first = k == k0;
       const bool skip = !first && ((skm >> (k - k0)) & 1ull);
@@ -399,14 +409,41 @@ __global__ void __launch_bounds__(NT, MINB) resolve_inflate_bnb_kernel(
     const int gj0 = j0 - R - PR, ws0 = gj0 >> 5;  // first source word (floor)
     if (sparse) {
       // raw source words, the fresh ones of this slice from memory, the
-      // others kept from the last loaded slice (first slice of an item: all)
-      for (int idx = tid; idx < G::GH * G::NSW; idx += NT) {
+      // others kept from the last loaded slice (first slice of an item: all).
+      // This thread's entries (fresh byte + word) for this slice were
+      // usually loaded into registers during the previous loaded slice of
+      // the item (pf_k == k); the next loaded slice's are issued below.
+#pragma unroll
+      for (int e = 0; e < kPfEnt; ++e) {
+        const int idx = tid + e * NT;
+        if (idx >= G::GH * G::NSW) break;
         const int y = idx / G::NSW, sw = idx - y * G::NSW;
         const int gi = i0 - R - PR + y, ws = ws0 + sw;
         const bool inmap = gi >= 0 && gi < rows && ws >= 0 && ws < wpr;
-        const bool fr = !inmap || first || M.fresh[((int64_t)k * rows + gi) * M.fpitch + ws] != 0;
+        if (pf_k != k && inmap && !first) pf_load(e, k, gi, ws);
+        const bool fr = !inmap || first || pf_f[e] != 0;
         frb[idx] = fr;
-        if (fr) raww[idx] = inmap ? __ldg(bk + (int64_t)gi * wpr + ws) : 0u;
+        if (fr) raww[idx] = inmap ? (first ? __ldg(bk + (int64_t)gi * wpr + ws) : pf_w[e]) : 0u;
+      }
+      // prefetch: the next loaded slice of this item (registers held across
+      // the rest of this step and any skipped steps)
+      {
+        pf_k = -1;
+        uint64_t rest = (k + 1 < k1) ? (~skm >> (k + 1 - k0)) : 0ull;
+        if (k + 1 - k0 < 64 && rest) {
+          const int kn = k + 1 + __ffsll((long long)rest) - 1;
+          if (kn < k1) {
+            pf_k = kn;
+#pragma unroll
+            for (int e = 0; e < kPfEnt; ++e) {
+              const int idx = tid + e * NT;
+              if (idx >= G::GH * G::NSW) break;
+              const int y = idx / G::NSW, sw = idx - y * G::NSW;
+              const int gi = i0 - R - PR + y, ws = ws0 + sw;
+              if (gi >= 0 && gi < rows && ws >= 0 && ws < wpr) pf_load(e, kn, gi, ws);
+            }
+          }
+        }
       }
       __syncthreads();
       const int sh = gj0 & 31;
