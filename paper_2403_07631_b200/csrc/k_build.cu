@@ -729,16 +729,20 @@ __global__ void __launch_bounds__(kHB2) hist_reduce_kernel(
   for (; r < r1; r += kHB2) gmax(__ldg(recs + r));
   __syncthreads();
   {
-    uint32_t run = kKeyEmptyMax, prev = 0u;
-    unsigned long long m = 1ull;  // slice-change mask (bit k: differs from slice k-1)
-    for (int k = 0; k < S; ++k) {
+    // slice-change mask: bit k set when the running max (and so the decoded
+    // layer, a bijection of it) grows at slice k; bit 0 always
+    uint32_t run = kKeyEmptyMax;
+    unsigned long long m = 1ull;
+    float *out = ground + cell;
+    for (int k = 0; k < S; ++k, out += out_stride) {
       const uint32_t v = hk[k * kHB2 + t];
-      run = v > run ? v : run;
+      if (v > run) {
+        run = v;
+        m |= 1ull << (k & 63);
+      }
       const float o = decode_ground(run);
-      if (k > 0 && f32_bits(o) != prev) m |= 1ull << (k & 63);
-      prev = f32_bits(o);
       if (TMA) hk[k * kHB2 + t] = f32_bits(o);
-      else if (live) __stcs(ground + (int64_t)k * out_stride + cell, o);
+      else if (live) __stcs(out, o);
     }
     if (masks && live) masks[(int64_t)i * cols + j] = m;
   }
@@ -765,16 +769,20 @@ __global__ void __launch_bounds__(kHB2) hist_reduce_kernel(
   for (; r < r1; r += kHB2) cmin(__ldcs(recs + r));
   __syncthreads();
   {
-    uint32_t run = kKeyEmptyMin, prev = 0u;
+    // bit k+1 set when the running min (walking down) shrinks at slice k:
+    // ceiling[k] differs from ceiling[k+1]
+    uint32_t run = kKeyEmptyMin;
     unsigned long long m = 1ull;
-    for (int k = S - 1; k >= 0; --k) {
+    float *out = ceiling + cell + (int64_t)(S - 1) * out_stride;
+    for (int k = S - 1; k >= 0; --k, out -= out_stride) {
       const uint32_t v = hk[k * kHB2 + t];
-      run = v < run ? v : run;
+      if (v < run) {
+        run = v;
+        if (k < S - 1) m |= 1ull << ((k + 1) & 63);
+      }
       const float o = decode_ceiling(run);
-      if (k < S - 1 && f32_bits(o) != prev) m |= 1ull << ((k + 1) & 63);
-      prev = f32_bits(o);
       if (TMA) hk[k * kHB2 + t] = f32_bits(o);
-      else if (live) __stcs(ceiling + (int64_t)k * out_stride + cell, o);
+      else if (live) __stcs(out, o);
     }
     if (masks && live) masks[(int64_t)rows * cols + (int64_t)i * cols + j] = m;
   }
