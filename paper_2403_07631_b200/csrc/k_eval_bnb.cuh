@@ -47,7 +47,7 @@ struct DiskShape<8> {  // a^2 + b^2 <= 16: 49 taps
 
 constexpr int count_bits(int n) { return n < 2 ? 1 : 1 + count_bits(n / 2); }
 
-template <int R, int PR, int TH, int TW>
+template <int R, int PR, int TH, int TW, bool SP = false>
 struct BnbGeom {
   static constexpr int CH = TH + 2 * R, CW = TW + 2 * R;  // c_init tile + halo
   static constexpr int GH = CH + 2 * PR, GW = CW + 2 * PR;
@@ -80,11 +80,13 @@ struct BnbGeom {
   // sparse walk output: the tile + halo's encoded c_init and the raw gentle
   // source words of the window as of the last loaded slice, and the fresh
   // flags of the current slice (one per row and source word)
+  // (only the sparse instantiation, SP, has them: the others keep the
+  // occupancy of the plain kernel)
   static constexpr int NSW = GWW + 1;
   static constexpr int O_RAWC = O_DB + ((DBY * DBX + 15) / 16) * 16;
-  static constexpr int O_RAWW = O_RAWC + BUF;
-  static constexpr int O_FRB = O_RAWW + ((GH * NSW * 4 + 15) / 16) * 16;
-  static constexpr int O_BAR = O_FRB + ((GH * NSW + 15) / 16) * 16;
+  static constexpr int O_RAWW = O_RAWC + (SP ? BUF : 0);
+  static constexpr int O_FRB = O_RAWW + (SP ? ((GH * NSW * 4 + 15) / 16) * 16 : 0);
+  static constexpr int O_BAR = O_FRB + (SP ? ((GH * NSW + 15) / 16) * 16 : 0);
   static constexpr int SMEM = O_BAR + 128;  // 3 mbarriers, 3 x 2 coordinate slots, warp counts
   static_assert(TH % R == 0 && TW % R == 0 && CW % 4 == 0 && R % 4 == 0, "bnb tile geometry");
   static_assert(TW % 32 == 0, "sparse merge: 4-cell groups never straddle a bitmap word");
@@ -205,10 +207,10 @@ __device__ __forceinline__ void slow_classes(const float *__restrict__ ctr, floa
 // whose (2R+1)^2 windows touch a changed block: an output is a function of
 // the resolved c_init in its window alone, so the others keep their values
 // (the output tile lives in shared memory and is stored every slice).
-template <int R, int PR, int TH, int TW, int NT, int MINB>
+template <int R, int PR, int TH, int TW, int NT, int MINB, bool SP = false>
 __global__ void __launch_bounds__(NT, MINB) resolve_inflate_bnb_kernel(
     const EvalMap *__restrict__ maps, const int *__restrict__ item_off, int n_maps) {
-  using G = BnbGeom<R, PR, TH, TW>;
+  using G = BnbGeom<R, PR, TH, TW, SP>;
   constexpr int NWARP = NT / 32;
   constexpr int WSEG = TH * TW / NWARP;  // list entries per warp (its P2 outputs)
   static_assert((TH * TW) % NWARP == 0 && NWARP <= 32, "warp list segments");
@@ -328,7 +330,7 @@ __global__ void __launch_bounds__(NT, MINB) resolve_inflate_bnb_kernel(
     const int64_t cells = (int64_t)rows * cols, words = M.words;
     const uint32_t *bits_in = M.bits;
     float *cost = M.cost;
-    const bool sparse = M.fresh != nullptr;  // uniform
+    const bool sparse = SP && M.fresh != nullptr;  // uniform (compile-time false without SP)
     const bool tstore = M.ostore != 0;       // uniform
     // the output tile of slice k to global memory: one TMA bulk tensor store
     // issued by thread 0 (the copy engine reads `ot`), else the threads' stores

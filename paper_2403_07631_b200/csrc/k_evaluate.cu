@@ -704,27 +704,42 @@ int launch_split(pct_ctx *ctx, const float *ground, const float *ceiling, int S,
   // longest run that still gives every resident CTA ~3 items (small maps:
   // down to one slice per item; cfg0 evaluate 44 -> 36 us, cfg1 unchanged at 5)
   int bnb_run = 1, bnb_slots = 1;
+  bool sparse = false;
+  const char *wk = getenv("PCT_WALK");
+  const bool skip_walk = S <= 64 && !(wk && wk[0] == '1');
   if constexpr (R == 4 || R == 8) {
     if (bnb) {
-      auto kb = resolve_inflate_bnb_kernel<R, PR, TH, TW, BNT, kBnbMinBlocks<R>()>;
-      constexpr int bsmem = BnbGeom<R, PR, TH, TW>::SMEM;
-      PCT_CUDA(ctx, cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, bsmem));
-      int per_sm = 0;
-      PCT_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kb, BNT, bsmem));
-      bnb_slots = (int)std::max(1, per_sm) * ctx->num_sms;
-      const int64_t tiles = (int64_t)((cols + TW - 1) / TW) * ((rows + TH - 1) / TH);
-      const int64_t runs_per_tile = std::min<int64_t>(S, (3 * (int64_t)bnb_slots + tiles - 1) / tiles);
-      bnb_run = (int)((S + runs_per_tile - 1) / runs_per_tile);
-      if (const char *e = getenv("PCT_INFL_RUN")) bnb_run = std::max(1, atoi(e));
-      bnb_run = std::min(std::min(bnb_run, S), 64);  // per-item skip mask: 64 slices
+      auto plan = [&](auto kb, int bsmem) -> int {
+        PCT_CUDA(ctx, cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, bsmem));
+        int per_sm = 0;
+        PCT_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kb, BNT, bsmem));
+        bnb_slots = (int)std::max(1, per_sm) * ctx->num_sms;
+        const int64_t tiles = (int64_t)((cols + TW - 1) / TW) * ((rows + TH - 1) / TH);
+        const int64_t runs_per_tile =
+            std::min<int64_t>(S, (3 * (int64_t)bnb_slots + tiles - 1) / tiles);
+        bnb_run = (int)((S + runs_per_tile - 1) / runs_per_tile);
+        if (const char *e = getenv("PCT_INFL_RUN")) bnb_run = std::max(1, atoi(e));
+        bnb_run = std::min(std::min(bnb_run, S), 64);  // per-item skip mask: 64 slices
+        return PCT_OK;
+      };
+      if (int rc = plan(resolve_inflate_bnb_kernel<R, PR, TH, TW, BNT, kBnbMinBlocks<R>()>,
+                        BnbGeom<R, PR, TH, TW>::SMEM))
+        return rc;
+      // sparse walk output (merged by the bnb kernel) pays off when the
+      // kernel's items are long runs of slices (large maps: cfg3 evaluate
+      // 3.27 -> 2.87 ms, cfg2 0.87 -> 0.84); short runs re-write every run
+      // start anyway (cfg1: 0.179 dense vs 0.193 ms)
+      const char *spv = getenv("PCT_WALK_SPARSE");
+      sparse = skip_walk && chgmap && (spv ? spv[0] == '1' : bnb_run >= 16);
+      if (sparse)
+        if (int rc = plan(resolve_inflate_bnb_kernel<R, PR, TH, TW, BNT, kBnbMinBlocks<R>(), true>,
+                          BnbGeom<R, PR, TH, TW, true>::SMEM))
+          return rc;
     }
   }
-  // sparse walk output when the bnb kernel (which merges) consumes it
-  const char *spv = getenv("PCT_WALK_SPARSE");
   unsigned char *fresh = nullptr;
-  const char *wk = getenv("PCT_WALK");
-  if (S <= 64 && !(wk && wk[0] == '1')) {
-    if (bnb && chgmap && !(spv && spv[0] == '0')) {
+  if (skip_walk) {
+    if (sparse) {
       fresh = static_cast<unsigned char *>(ctx->scratch) + f_off;
       PCT_CUDA(ctx, cudaMemsetAsync(fresh, 0, f_bytes, ctx->stream));
     }
@@ -792,8 +807,9 @@ int launch_split(pct_ctx *ctx, const float *ground, const float *ceiling, int S,
     if constexpr (R == 4 || R == 8) {
      if (bnb) {
       PCT_CUDA(ctx, cb.set_symbol(c_bw, bw.data(), bw.size() * sizeof(float)));
-      auto kb = resolve_inflate_bnb_kernel<R, PR, TH, TW, BNT, kBnbMinBlocks<R>()>;
-      constexpr int bsmem = BnbGeom<R, PR, TH, TW>::SMEM;
+      auto kb = sparse ? resolve_inflate_bnb_kernel<R, PR, TH, TW, BNT, kBnbMinBlocks<R>(), true>
+                       : resolve_inflate_bnb_kernel<R, PR, TH, TW, BNT, kBnbMinBlocks<R>()>;
+      const int bsmem = sparse ? BnbGeom<R, PR, TH, TW, true>::SMEM : BnbGeom<R, PR, TH, TW>::SMEM;
       const int64_t slots = bnb_slots;
       const int64_t tiles = (int64_t)((cols + TW - 1) / TW) * ((rows + TH - 1) / TH);
       const int run = bnb_run;

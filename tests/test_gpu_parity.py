@@ -693,3 +693,24 @@ def test_fused_run_simplify_matches_oracle(monkeypatch, win_skip):
         cost = oracle.evaluate(ref["ground"], ref["ceiling"], 0.1, TABLE_PARAMS)
         keep = oracle.simplify(ref["ground"], cost)
         assert [s.plane_height for s in got.slices] == [float(ref["heights"][k]) for k in keep]
+
+
+@pytest.mark.parametrize("sparse,run", [("1", "1"), ("1", "3"), ("1", "64"), ("0", "7")])
+@pytest.mark.parametrize("name", ["synth_cfg0", "ref_spiral_s3", "synth_two_storey_small"])
+def test_sparse_walk_and_bnb_runs(golden, monkeypatch, name, sparse, run):
+    """The walk's sparse output (only recomputed slices + run starts written,
+    the inflation kernel merging the rest) at several item run lengths,
+    through the fused path and the per-stack path: costs equal the
+    reference's."""
+    monkeypatch.setenv("PCT_WALK_SPARSE", sparse)
+    monkeypatch.setenv("PCT_INFL_RUN", run)
+    case = golden["cases"][name]
+    xyz = case_input(name, case)
+    ev = pct.evaluate_tomogram(pct.build_tomogram(pct.PointCloud(xyz), case["d_s"], case["r_g"]),
+                               pct.TravParams())
+    assert [digest(s.cost.values) for s in ev.slices] == case["cost_slice_sha256"]
+    from paper_2403_07631_b200.batch import stream_maps
+    got = next(stream_maps([xyz], case["d_s"], case["r_g"], pct.TravParams(), workers=1))
+    assert [s.plane_height for s in got.slices] == [case["heights"][k] for k in case["keep"]]
+    assert [digest(s.cost.values) for s in got.slices] == \
+        [case["cost_slice_sha256"][k] for k in case["keep"]]
