@@ -1468,8 +1468,10 @@ int launch_build(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, const pct_
                   CUDA_SUCCESS;
       }
     }
+    // the split-scan reduce measured slower at cfg3 (2.42 vs 2.18 ms):
+    // opt-in (PCT_BUILD_REDUCE=2)
     const char *rv = getenv("PCT_BUILD_REDUCE");
-    if (!tma && !(rv && rv[0] == '1')) {  // default: the split-scan reduce
+    if (!tma && rv && rv[0] == '2') {
       const size_t ssm = rsm + 4 * 128 * 16 + 2 * kHB2 * 8;
       PCT_CUDA(ctx, cudaFuncSetAttribute(hist_reduce_split_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm));
