@@ -726,11 +726,13 @@ int launch_split(pct_ctx *ctx, const float *ground, const float *ceiling, int S,
                         BnbGeom<R, PR, TH, TW>::SMEM))
         return rc;
       // sparse walk output (merged by the bnb kernel) pays off when the
-      // kernel's items are long runs of slices (large maps: cfg3 evaluate
-      // 3.27 -> 2.87 ms, cfg2 0.87 -> 0.84); short runs re-write every run
-      // start anyway (cfg1: 0.179 dense vs 0.193 ms)
+      // kernel's items are long runs of slices and its merge buffers cost no
+      // more than one resident CTA: R = 4 (cfg3 evaluate 3.32 -> 2.88 ms);
+      // short runs re-write every run start anyway (cfg1: 0.179 dense vs
+      // 0.193 ms); at R = 8 the buffers drop the kernel from 4 to 3 CTAs per
+      // SM (cfg2: 0.74 dense vs 0.84 ms)
       const char *spv = getenv("PCT_WALK_SPARSE");
-      sparse = skip_walk && chgmap && (spv ? spv[0] == '1' : bnb_run >= 16);
+      sparse = skip_walk && chgmap && (spv ? spv[0] == '1' : (R == 4 && bnb_run >= 16));
       if (sparse)
         if (int rc = plan(resolve_inflate_bnb_kernel<R, PR, TH, TW, BNT, kBnbMinBlocks<R>(), true>,
                           BnbGeom<R, PR, TH, TW, true>::SMEM))
