@@ -433,16 +433,26 @@ class Pipeline:
                     heights=hts[:S].copy())
 
 
+# PCT_BENCH_GLOO=1: a functional test of the multi-rank bench on ONE GPU
+# (gloo collectives staged through host memory, every rank on cuda:0); its
+# numbers are not measurements and the line says so
+GLOO_TEST = os.environ.get("PCT_BENCH_GLOO") == "1"
+
+
+def _coll_dev(local):
+    return "cpu" if GLOO_TEST else f"cuda:{local}"
+
+
 def all_max(x, local):
     import torch
-    t = torch.tensor([float(x)], device=f"cuda:{local}", dtype=torch.float64)
+    t = torch.tensor([float(x)], device=_coll_dev(local), dtype=torch.float64)
     torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     return float(t.item())
 
 
 def all_sum(x, local):
     import torch
-    t = torch.tensor([float(x)], device=f"cuda:{local}", dtype=torch.float64)
+    t = torch.tensor([float(x)], device=_coll_dev(local), dtype=torch.float64)
     torch.distributed.all_reduce(t)
     return float(t.item())
 
@@ -451,10 +461,15 @@ def run_b200(args):
     import torch
 
     rank, world, local = dist_env()
+    if GLOO_TEST:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if GLOO_TEST:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2403_07631_b200 as pct
     from paper_2403_07631_b200 import _lib, sharded
 
@@ -591,6 +606,8 @@ def run_b200(args):
     }
     if args.mode == "batch":
         line["maps_per_s"] = len(maps) * world * args.steps / (step_ms * 1e-3)
+    if GLOO_TEST:
+        line["functional_test"] = "PCT_BENCH_GLOO: gloo, every rank on cuda:0 -- not a measurement"
     ev_ms = statistics.mean(per["evaluate"]) / len(maps)
     n_map = total_pts if args.mode != "batch" else n_local / len(maps)
     # banded: this rank's band (own rows + halo rows it evaluates)
