@@ -718,8 +718,9 @@ def run_e2e(args, cfg, maps, ctx, local, rank, world, R, Cc):
                     d2h += s.ground.values.nbytes + s.ceiling.values.nbytes + s.cost.values.nbytes
                 last = tom
             return d2h, last
-        if banded:
-            tom = sharded.tomogram_sharded(clouds[0], d_s, r_g, params, root=0, device=local)
+        if banded:  # every rank reads its band back over its own PCIe link
+            tom = sharded.tomogram_sharded(clouds[0], d_s, r_g, params, root=0, device=local,
+                                           gather="host")
         else:
             tom = pct.simplify_tomogram(pct.evaluate_tomogram(
                 pct.build_tomogram(clouds[0], d_s, r_g, device=local), params))
@@ -754,8 +755,9 @@ def run_e2e(args, cfg, maps, ctx, local, rank, world, R, Cc):
         d2h = int(all_sum(d2h, local))
     path = {"batch": "stream_maps(pinned f32 clouds, 2 in flight) -> simplified tomograms, "
                      "every surviving layer in host memory",
-            "sharded": ("tomogram_sharded(pinned f32 share per rank) -> simplified Tomogram "
-                        "gathered on rank 0 -> every surviving layer in host memory")
+            "sharded": ("tomogram_sharded(pinned f32 share per rank, gather='host') -> each "
+                        "rank DMAs its band of every surviving layer into one shared host "
+                        "segment -> the simplified Tomogram on rank 0, all layers host-resident")
             if banded else None,
             "replica": None}[args.mode] or (
         "PointCloud(pinned f32) -> build_tomogram -> evaluate_tomogram -> simplify_tomogram "

@@ -86,6 +86,10 @@ int pct_malloc(pct_ctx *ctx, size_t bytes, void **dptr);
 int pct_free(pct_ctx *ctx, void *dptr);
 int pct_host_alloc(pct_ctx *ctx, size_t bytes, void **hptr);
 int pct_host_free(pct_ctx *ctx, void *hptr);
+/* Page-lock existing host memory (e.g. a shared-memory segment several
+   processes write their bands into) for DMA; unregister before unmapping. */
+int pct_host_register(pct_ctx *ctx, void *hptr, size_t bytes);
+int pct_host_unregister(pct_ctx *ctx, void *hptr);
 int pct_memcpy_h2d(pct_ctx *ctx, void *dst, const void *src, size_t bytes);
 int pct_memcpy_d2h(pct_ctx *ctx, void *dst, const void *src, size_t bytes); /* syncs */
 int pct_memcpy_d2h_async(pct_ctx *ctx, void *dst, const void *src, size_t bytes);

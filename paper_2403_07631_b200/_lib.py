@@ -57,6 +57,8 @@ _SIGS = {
     "pct_free": ([_vp, _vp], C.c_int),
     "pct_host_alloc": ([_vp, C.c_size_t, C.POINTER(_vp)], C.c_int),
     "pct_host_free": ([_vp, _vp], C.c_int),
+    "pct_host_register": ([_vp, _vp, C.c_size_t], C.c_int),
+    "pct_host_unregister": ([_vp, _vp], C.c_int),
     "pct_memcpy_h2d": ([_vp, _vp, _vp, C.c_size_t], C.c_int),
     "pct_memcpy_d2h": ([_vp, _vp, _vp, C.c_size_t], C.c_int),
     "pct_memcpy_d2h_async": ([_vp, _vp, _vp, C.c_size_t], C.c_int),

@@ -329,6 +329,19 @@ int pct_host_free(pct_ctx *ctx, void *hptr) {
   return PCT_OK;
 }
 
+int pct_host_register(pct_ctx *ctx, void *hptr, size_t bytes) {
+  CTX_GUARD(ctx);
+  if (!hptr || !bytes) return fail(ctx, PCT_E_INVALID, "bad arguments to pct_host_register");
+  PCT_CUDA(ctx, cudaHostRegister(hptr, bytes, cudaHostRegisterPortable));
+  return PCT_OK;
+}
+
+int pct_host_unregister(pct_ctx *ctx, void *hptr) {
+  CTX_GUARD(ctx);
+  if (hptr) PCT_CUDA(ctx, cudaHostUnregister(hptr));
+  return PCT_OK;
+}
+
 int pct_memcpy_h2d(pct_ctx *ctx, void *dst, const void *src, size_t bytes) {
   CTX_GUARD(ctx);
   if (bytes) PCT_CUDA(ctx, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));

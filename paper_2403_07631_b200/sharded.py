@@ -400,9 +400,140 @@ def _assemble_tomogram(stacks, heights, keep, r_g, origin, d_s, z_min):
     return Tomogram(slices=slices, d_s=float(d_s), z_min=float(z_min))
 
 
+# ---------------------------------------------------------------------------
+# host gather: every rank DMAs its band of the surviving layers into one
+# shared-memory segment on the node (its own PCIe link), the root wraps it
+
+class _Segment:
+    """One /dev/shm segment mapped (and page-locked for DMA) in this process."""
+
+    def __init__(self, ctx, name, nbytes, create):
+        import mmap
+        import os
+        path = "/dev/shm/" + name
+        fd = os.open(path, (os.O_CREAT | os.O_EXCL | os.O_RDWR) if create else os.O_RDWR, 0o600)
+        try:
+            if create:
+                os.ftruncate(fd, nbytes)
+            self.mm = mmap.mmap(fd, nbytes)
+        finally:
+            os.close(fd)
+        self.ctx, self.name, self.nbytes, self.path = ctx, name, nbytes, path
+        self._anchor = C.c_char.from_buffer(self.mm)  # exported: the mapping stays put
+        self.ptr = C.addressof(self._anchor)
+        ctx.check(ctx.lib.pct_host_register(ctx.h, C.c_void_p(self.ptr), C.c_size_t(nbytes)),
+                  "host_register")
+        self.view = None  # root: weakref to the array handed out
+
+    def free(self):
+        return self.view is None or self.view() is None
+
+    def release(self, unlink=False):
+        try:
+            self.ctx.lib.pct_host_unregister(self.ctx.h, C.c_void_p(self.ptr))
+        except Exception:
+            pass
+        if unlink:
+            _unlink(self.path)
+
+
+def _unlink(path):
+    import os
+    try:
+        os.unlink(path)
+    except OSError:
+        pass
+
+
+def _unlink_root_segments():
+    for seg in _ROOT_SEGS:
+        _unlink(seg.path)
+
+
+_ROOT_SEGS: list = []   # root: segments it created (reused while free)
+_ATTACHED: dict = {}    # other ranks: name -> _Segment (the last few)
+
+
+def _root_segment(ctx, nbytes):
+    import os
+    import uuid
+    for seg in _ROOT_SEGS:
+        if seg.nbytes == nbytes and seg.free() and seg.ctx is ctx:
+            return seg, False
+    while len(_ROOT_SEGS) >= 2 and any(sg.free() for sg in _ROOT_SEGS):  # drop an idle one
+        old = next(sg for sg in _ROOT_SEGS if sg.free())
+        _ROOT_SEGS.remove(old)
+        old.release(unlink=True)
+    if not _ROOT_SEGS:
+        import atexit
+        atexit.register(_unlink_root_segments)
+    seg = _Segment(ctx, f"pct-{os.getpid()}-{uuid.uuid4().hex[:12]}", nbytes, create=True)
+    _ROOT_SEGS.append(seg)
+    return seg, True
+
+
+def _attached_segment(ctx, name, nbytes):
+    seg = _ATTACHED.get(name)
+    if seg is None:
+        seg = _Segment(ctx, name, nbytes, create=False)
+        _ATTACHED[name] = seg
+        while len(_ATTACHED) > 3:  # oldest attachments go (no views on this side)
+            old = _ATTACHED.pop(next(iter(_ATTACHED)))
+            old.release()
+    return seg
+
+
+def _host_gather(res, ctx, root, group, d_s, r_g):
+    """The surviving slices of every band written by their own rank straight
+    into one pinned shared-memory segment of the node, wrapped on the root as
+    host-resident reference Layers (every rank's D2H runs on its own PCIe
+    link; nothing crosses NVLink)."""
+    import weakref
+
+    import torch.distributed as dist
+    rank = dist.get_rank(group)
+    K, R, Cc = len(res.keep), res.rows, res.cols
+    nbytes = 3 * K * R * Cc * 4
+    box = [None, None]
+    if rank == root:
+        seg, _ = _root_segment(ctx, nbytes)
+        box = [seg.name, nbytes]
+    dist.broadcast_object_list(box, src=_global(group, root), group=group)
+    name, nb = box
+    seg = seg if rank == root else _attached_segment(ctx, name, nb)
+    # this rank's rows of every kept slice of the three layers
+    plane = R * Cc * 4
+    band = res.nrows * Cc * 4
+    with ctx.lock:
+        for L, t in enumerate((res.ground, res.ceiling, res.cost)):
+            sstride = t.stride(0) * 4
+            for m, k in enumerate(res.keep):
+                if band == 0:
+                    continue
+                dst = seg.ptr + (L * K + m) * plane + res.row0 * Cc * 4
+                ctx.check(ctx.lib.pct_memcpy_d2h_async(ctx.h, C.c_void_p(dst),
+                                                       C.c_void_p(t.data_ptr() + k * sstride),
+                                                       C.c_size_t(band)), "d2h")
+        ctx.check(ctx.lib.pct_sync(ctx.h), "sync")
+    dist.barrier(group=group)  # every band landed; every rank attached the segment
+    if rank != root:
+        return None
+    # (the segment's file stays in /dev/shm while the root may hand it out
+    # again -- other ranks re-attach by name -- and is unlinked when dropped
+    # from the pool or at exit)
+    from .tomogram import Layer, Tomogram, TomogramSlice
+    arr = np.frombuffer(seg.mm, np.float32, count=3 * K * R * Cc).reshape(3, K, R, Cc)
+    seg.view = weakref.ref(arr)
+    origin = res.origin
+    slices = [TomogramSlice(Layer(arr[0, m], r_g, origin), Layer(arr[1, m], r_g, origin),
+                            float(res.heights[k]), m, Layer(arr[2, m], r_g, origin))
+              for m, k in enumerate(res.keep)]
+    return Tomogram(slices=slices, d_s=float(d_s), z_min=float(res.z_min))
+
+
 def tomogram_sharded(points, d_s: float, r_g: float, params=None, *, eps_e: float = 1e-6,
                      c_barrier: float = 50.0, root: int = 0, group=None, device=None,
-                     max_grid_side: int = 16384):
+                     max_grid_side: int = 16384, gather: str = "device"):
     """build_tomogram -> evaluate_tomogram -> simplify_tomogram of ONE map
     whose points are spread over the ranks of a torch.distributed group (one
     process per GPU), row-band sharded as in the module docstring.
@@ -411,10 +542,15 @@ def tomogram_sharded(points, d_s: float, r_g: float, params=None, *, eps_e: floa
     float32/float64 host array (pinned memory uploads fastest) or a CUDA
     tensor; any split of the points over the ranks gives the same result.
     Returns on ``root`` the simplified reference-compatible ``Tomogram``
-    (tomogram.py:65-96; bit-identical to the one-GPU chain, its layers
-    device-resident until ``materialize()`` / ``Layer.values``), and None on
-    the other ranks.  With a one-rank group (or no process group) it runs the
-    same band pipeline on one GPU."""
+    (tomogram.py:65-96; bit-identical to the one-GPU chain), and None on the
+    other ranks.  ``gather="device"``: the bands' surviving slices are sent to
+    the root's GPU (NCCL) and its layers stay device-resident until
+    ``materialize()`` / ``Layer.values``.  ``gather="host"`` (ranks on one
+    node): every rank writes its band straight into one page-locked
+    shared-memory segment over its own PCIe link and the root's layers are
+    host numpy arrays on return -- the read-back of a large map spreads over
+    all the GPUs' links.  With a one-rank group (or no process group) it runs
+    the same band pipeline on one GPU."""
     import torch
     import torch.distributed as dist
 
@@ -439,11 +575,18 @@ def tomogram_sharded(points, d_s: float, r_g: float, params=None, *, eps_e: floa
             ctx.check(ctx.lib.pct_set_stream(ctx.h, C.c_void_p(stream)), "set_stream")
             ctx.check(ctx.lib.pct_memcpy_h2d(ctx.h, xyz.data_ptr(), arr.ctypes.data, arr.nbytes),
                       "h2d")
+    if gather not in ("device", "host"):
+        raise ValueError("gather must be 'device' or 'host'")
+    host = gather == "host" and size > 1
     gen = band_pipeline(xyz, d_s, r_g, params, rank, size, device=dev.index, eps_e=eps_e,
                         c_barrier=c_barrier, max_grid_side=max_grid_side,
-                        gather_to=root if size > 1 else 0)
+                        gather_to=None if host else (root if size > 1 else 0))
     res = run_virtual([gen])[0] if size == 1 else run_torch(gen, group)
-    return res.tomogram if rank == root else None
+    if host:
+        return _host_gather(res, _lib.context(dev.index), root, group, d_s, r_g)
+    if rank != root:
+        return None
+    return res.tomogram.materialize() if gather == "host" else res.tomogram
 
 
 def _sweep_gen(S, tb):

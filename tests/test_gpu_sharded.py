@@ -147,7 +147,7 @@ def test_virtual_bands_errors_on_every_rank():
         sharded.run_virtual(gens)
 
 
-def _gloo_worker(rank, size, port, q, n_points):
+def _gloo_worker(rank, size, port, q, n_points, gather="device"):
     import os
     import torch
     import torch.distributed as dist
@@ -159,7 +159,14 @@ def _gloo_worker(rank, size, port, q, n_points):
         from paper_2403_07631_b200 import sharded, synth
         xyz = synth.spiral_ramp(n_points, seed=4)
         mine = np.ascontiguousarray(xyz[rank::size])
-        tom = sharded.tomogram_sharded(p.PointCloud(mine), 0.4, 0.1, root=0)
+        tom = sharded.tomogram_sharded(p.PointCloud(mine), 0.4, 0.1, root=0, gather=gather)
+        if gather == "host" and rank == 0:  # a second call re-uses the segment
+            again = sharded.tomogram_sharded(p.PointCloud(mine), 0.4, 0.1, root=0, gather=gather)
+            assert all(np.array_equal(a.cost.values, b.cost.values)
+                       for a, b in zip(tom.slices, again.slices))
+            assert all(s.ground._values is not None for s in tom.slices)  # host-resident
+        elif gather == "host":
+            sharded.tomogram_sharded(p.PointCloud(mine), 0.4, 0.1, root=0, gather=gather)
         if rank == 0:
             tom.materialize()
             import hashlib
@@ -173,10 +180,12 @@ def _gloo_worker(rank, size, port, q, n_points):
         dist.destroy_process_group()
 
 
-def test_two_processes_gloo_equal_single_gpu():
+@pytest.mark.parametrize("gather", ["device", "host"])
+def test_two_processes_gloo_equal_single_gpu(gather):
     """The real band pipeline in two processes (gloo: collectives staged
     through host memory; both ranks share cuda:0) returns on rank 0 the
-    Tomogram of the one-GPU chain, bit for bit."""
+    Tomogram of the one-GPU chain, bit for bit -- gathered on the root's GPU,
+    or written by each rank into one shared host segment."""
     import hashlib
     import socket
     import torch.multiprocessing as mp
@@ -192,7 +201,7 @@ def test_two_processes_gloo_equal_single_gpu():
     s.close()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, q, n)) for r in range(2)]
+    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, q, n, gather)) for r in range(2)]
     for p in procs:
         p.start()
     out = {}
