@@ -12,7 +12,8 @@ for tag in sys.argv[1:]:
     for r in rows[1:]:
         per.setdefault(r[ii], {"kernel": r[ki]})[r[mi]] = float(r[vi].replace(",", ""))
     launches = list(per.values())
-    half = [v for v in launches[len(launches) // 2:] if "pct::" in v["kernel"]]
+    half = [v for v in launches[len(launches) // 2:]
+            if "pct::" in v["kernel"] or "unnamed>::" in v["kernel"]]
     tot = sum(v.get("gpu__time_duration.sum", 0) for v in half)
     print(f"== {tag}: {len(half)} launches, {tot / 1e3:.1f} us")
     for v in half:

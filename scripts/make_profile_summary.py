@@ -21,7 +21,8 @@ for r in rows[1:]:
     per.setdefault(r[ii], {"kernel": r[ki]})[r[mi]] = float(r[vi].replace(",", ""))
 launches = list(per.values())
 half = launches[len(launches) // 2:]  # the timed step (after the warm-up step)
-half = [v for v in half if "pct::" in v["kernel"]]  # the L2 flush between steps is not in the step
+# the library's kernels (the L2 flush between steps is not in the step)
+half = [v for v in half if "pct::" in v["kernel"] or "unnamed>::" in v["kernel"]]
 tot = sum(v.get("gpu__time_duration.sum", 0) for v in half)
 with open(out / f"{rnd}_launches.csv", "w") as f:
     f.write("kernel,time_us,share,dram_read_MB,dram_write_MB\n")
@@ -57,7 +58,8 @@ if rep.exists():
 tr_path = out / "ncu_traffic.json"
 tr = json.loads(tr_path.read_text()) if tr_path.exists() else {}
 # the evaluate stage = every launch between the build scan and the simplify window
-ev = [v for v in half if any(x in v["kernel"] for x in ("eval", "terrain_walk", "resolve_inflate", "zero_pads"))]
+ev = [v for v in half if any(x in v["kernel"] for x in ("eval", "terrain_walk", "resolve_inflate",
+                                                          "zero_pads", "change_mask"))]
 if ev:
     tr[cfg] = {"kernels": sorted({v["kernel"][:80] for v in ev}),
                "eval_dram_bytes": sum(v.get("dram__bytes_read.sum", 0) + v.get("dram__bytes_write.sum", 0) for v in ev),
