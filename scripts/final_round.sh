@@ -14,10 +14,10 @@ for c in 0 1 2 3; do
   echo "ncu list cfg$c rc=$?"
 done
 timeout 1200 ncu --set full --clock-control none --import-source on \
-  -k regex:"hist_pass|hist_reduce|terrain_walk|resolve_inflate_bnb|window" -s 9 -c 7 \
+  -k regex:"hist_pass|hist_reduce|terrain_walk|resolve_inflate_bnb|window" -s 6 -c 6 \
   -o gpurun_out/prof_f3 python bench.py --config 3 --profile --no-e2e --no-cpu --no-parity > gpurun_out/ncu_full3.log 2>&1
 echo "ncu full cfg3 rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on \
-  -k regex:"terrain_walk|resolve_inflate_bnb|scatter_kernel|scan_kernel|window_kernel" -s 6 -c 6 \
+  -k regex:"terrain_walk|resolve_inflate_bnb|scatter_kernel|scan_kernel|window_kernel" -s 5 -c 5 \
   -o gpurun_out/prof_f1 python bench.py --config 1 --profile --no-e2e --no-cpu --no-parity > gpurun_out/ncu_full1.log 2>&1
 echo "ncu full cfg1 rc=$?"
