@@ -365,7 +365,10 @@ __global__ void __launch_bounds__(kWalkNT) terrain_walk_skip_kernel(
     knext = todo ? __ffsll((long long)todo) - 1 : ke;
     if (knext < ke) fetch(knext);  // in flight while this slice computes
     const bool xch = (xm >> k) & 1ull, ich = (im >> k) & 1ull;
-    if (xch && live) {
+    if (xch && live && !finite32(e)) {  // no ground: nothing to grade (fast_terrain's result)
+      st.gentle = false;
+      st.tenc = nanf_;
+    } else if (xch && live) {
       const FastCell t = fast_terrain(Cross{e, l, r, u, d}, c_K);
       st.gentle = t.gentle;
       if (!t.valid) {
