@@ -706,8 +706,10 @@ __global__ void __launch_bounds__(kHB2) hist_reduce_kernel(
   const int i = bi * kHBH + t / kHBW, j = bj * kHBW + t % kHBW;
   const bool live = i < rows && j < cols;
   const int64_t cell = (int64_t)i * cols + j;
-  // ground: max key per (bin, cell), bins 0 .. S-1
-  for (int q = t; q < S * kHB2; q += kHB2) hk[q] = kKeyEmptyMax;
+  // ground: max key per (bin, cell), bins 0 .. S-1 (16-byte stores)
+  uint4 *hk4 = reinterpret_cast<uint4 *>(hk);
+  for (int q = t; q < S * (kHB2 / 4); q += kHB2)
+    hk4[q] = make_uint4(kKeyEmptyMax, kKeyEmptyMax, kKeyEmptyMax, kKeyEmptyMax);
   __syncthreads();
   auto gmax = [&](unsigned long long rec) {
     const int bin = (int)((rec >> 9) & 0x7FFFFFu);
@@ -734,6 +736,7 @@ __global__ void __launch_bounds__(kHB2) hist_reduce_kernel(
     uint32_t run = kKeyEmptyMax;
     unsigned long long m = 1ull;
     float *out = ground + cell;
+#pragma unroll 4
     for (int k = 0; k < S; ++k, out += out_stride) {
       const uint32_t v = hk[k * kHB2 + t];
       if (v > run) {
@@ -756,7 +759,8 @@ __global__ void __launch_bounds__(kHB2) hist_reduce_kernel(
   }
   __syncthreads();
   // ceiling: min key per (bin, cell), bins 1 .. S stored at bin - 1
-  for (int q = t; q < S * kHB2; q += kHB2) hk[q] = kKeyEmptyMin;
+  for (int q = t; q < S * (kHB2 / 4); q += kHB2)
+    hk4[q] = make_uint4(kKeyEmptyMin, kKeyEmptyMin, kKeyEmptyMin, kKeyEmptyMin);
   __syncthreads();
   r = r0 + t;
   for (; r + (U - 1) * kHB2 < r1; r += U * kHB2) {
@@ -774,6 +778,7 @@ __global__ void __launch_bounds__(kHB2) hist_reduce_kernel(
     uint32_t run = kKeyEmptyMin;
     unsigned long long m = 1ull;
     float *out = ceiling + cell + (int64_t)(S - 1) * out_stride;
+#pragma unroll 4
     for (int k = S - 1; k >= 0; --k, out -= out_stride) {
       const uint32_t v = hk[k * kHB2 + t];
       if (v < run) {
