@@ -24,6 +24,8 @@
 namespace pct {
 namespace {
 
+#include "bulk.cuh"
+
 __device__ __forceinline__ unsigned long long dkey(double d) {
   unsigned long long u = (unsigned long long)__double_as_longlong(d);
   return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
@@ -544,7 +546,10 @@ __global__ void __launch_bounds__(kTileNT) tile_reduce_kernel(
 //      bucket's records (L2 hits) for the min keys and the ceiling planes
 //      (half the shared memory of a two-sided reduce: two CTAs per SM).
 // Traffic: 2 reads of the points + 8 B records out and back + the planes.
-constexpr int kHBH = 16, kHBW = 32;
+#ifndef PCT_HBW
+#define PCT_HBW 64
+#endif
+constexpr int kHBW = PCT_HBW, kHBH = 512 / PCT_HBW;  // bucket: kHBH rows x kHBW columns
 constexpr int kHB2 = kHBH * kHBW;          // 512 cells per bucket (9-bit local index)
 constexpr int kHistNT = 1024;              // H1 / H3 threads per CTA
 constexpr int kHistMaxBuckets = 48 * 1024;  // 192 KB of shared histogram
@@ -556,6 +561,48 @@ __device__ __forceinline__ void load_point(const T *__restrict__ xyz, int64_t p,
   x = (double)__ldg(xyz + 3 * p);
   y = (double)__ldg(xyz + 3 * p + 1);
   z = (double)__ldg(xyz + 3 * p + 2);
+}
+
+// one quad of float32 points (three 16-byte vectors): count its buckets, or
+// (SCATTER) place its records -- the 4 cells, bins and records first, then
+// the 4 cursor atomics, then the 4 stores (independent chains in flight)
+template <bool SCATTER>
+__device__ __forceinline__ void hist_quad(const float4 A, const float4 B, const float4 Cv,
+                                          const BinArgs &a, const double *hts, int nbx,
+                                          unsigned *h, unsigned long long *__restrict__ recs,
+                                          unsigned long long *outside) {
+  const double px[4] = {A.x, A.w, B.z, Cv.y}, py[4] = {A.y, B.x, B.w, Cv.z},
+               pz[4] = {A.z, B.y, Cv.x, Cv.w};
+  if (SCATTER) {
+    int bk[4];
+    unsigned long long rec[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      int fi, fj, bin = 0;
+      bk[u] = -1;
+      if (point_cell_bin<true>(px[u], py[u], pz[u], a, hts, fi, fj, bin)) {
+        bk[u] = (fi / kHBH) * nbx + fj / kHBW;
+        rec[u] = ((unsigned long long)f32_key(__double2float_rn(pz[u])) << 32) |
+                 ((unsigned long long)bin << 9) | (unsigned)((fi % kHBH) * kHBW + fj % kHBW);
+      }
+    }
+    unsigned pos[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (bk[u] >= 0) pos[u] = atomicAdd(&h[bk[u]], 1u);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (bk[u] >= 0) recs[pos[u]] = rec[u];
+  } else {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      int fi, fj, bin = 0;
+      if (point_cell_bin<false>(px[u], py[u], pz[u], a, hts, fi, fj, bin))
+        atomicAdd(&h[(fi / kHBH) * nbx + fj / kHBW], 1u);
+      else if (outside)
+        atomicAdd(outside, 1ull);
+    }
+  }
 }
 
 template <typename T, bool SCATTER>
@@ -600,40 +647,9 @@ __global__ void __launch_bounds__(kHistNT, 1) hist_pass_kernel(
   if (sizeof(T) == 4 && (reinterpret_cast<uintptr_t>(xyz) & 15) == 0) {
     const float4 *v = reinterpret_cast<const float4 *>(xyz);
     const int64_t q1 = p1 >> 2;  // whole quads
-    for (int64_t q = (p0 >> 2) + threadIdx.x; q < q1; q += kHistNT) {
-      const float4 A = __ldg(v + 3 * q), B = __ldg(v + 3 * q + 1), Cv = __ldg(v + 3 * q + 2);
-      if (SCATTER) {
-        // the 4 points' cells, bins and records first, then their 4 cursor
-        // atomics, then the 4 stores (independent chains in flight)
-        const double px[4] = {A.x, A.w, B.z, Cv.y}, py[4] = {A.y, B.x, B.w, Cv.z},
-                     pz[4] = {A.z, B.y, Cv.x, Cv.w};
-        int bk[4];
-        unsigned long long rec[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          int fi, fj, bin = 0;
-          bk[u] = -1;
-          if (point_cell_bin<true>(px[u], py[u], pz[u], a, hts, fi, fj, bin)) {
-            bk[u] = (fi / kHBH) * nbx + fj / kHBW;
-            rec[u] = ((unsigned long long)f32_key(__double2float_rn(pz[u])) << 32) |
-                     ((unsigned long long)bin << 9) |
-                     (unsigned)((fi % kHBH) * kHBW + fj % kHBW);
-          }
-        }
-        unsigned pos[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (bk[u] >= 0) pos[u] = atomicAdd(&h[bk[u]], 1u);
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (bk[u] >= 0) recs[pos[u]] = rec[u];
-      } else {
-        one(A.x, A.y, A.z);
-        one(A.w, B.x, B.y);
-        one(B.z, B.w, Cv.x);
-        one(Cv.y, Cv.z, Cv.w);
-      }
-    }
+    for (int64_t q = (p0 >> 2) + threadIdx.x; q < q1; q += kHistNT)
+      hist_quad<SCATTER>(__ldg(v + 3 * q), __ldg(v + 3 * q + 1), __ldg(v + 3 * q + 2), a, hts,
+                         nbx, h, recs, outside);
     pq = q1 << 2;
   }
   for (int64_t p = pq + threadIdx.x; p < p1; p += kHistNT) {
@@ -645,6 +661,103 @@ __global__ void __launch_bounds__(kHistNT, 1) hist_pass_kernel(
     __syncthreads();
     for (int b = threadIdx.x; b < nb; b += kHistNT) mine[b] = h[b];
   }
+}
+
+// H1 / H3 with the points staged through shared memory: the CTA's chunk
+// (16-byte aligned float32 quads) arrives in kBulkQ-quad stages by 1-D bulk
+// copies (cp.async.bulk, completion on a `full` mbarrier), kBulkStages
+// stages in flight, so the loads never stall the arithmetic; a stage is
+// refilled once all warps have arrived on its `empty` mbarrier.  Thread t
+// takes quad t of every stage.  Same chunks, counts and records as
+// hist_pass_kernel.
+constexpr int kBulkQ = kHistNT;        // quads per stage
+constexpr int kBulkBytes = kBulkQ * 48;  // 48 KB
+constexpr int kBulkStages = 2;
+template <bool SCATTER>
+__global__ void __launch_bounds__(kHistNT, 1) hist_pass_bulk_kernel(
+    const float *__restrict__ xyz, int64_t n, BinArgs a, int nbx, int nb,
+    unsigned *__restrict__ cnt, const unsigned *__restrict__ offs,
+    unsigned long long *__restrict__ recs, unsigned long long *outside) {
+  extern __shared__ __align__(128) unsigned char hsmem[];
+  const size_t hist_b = ((size_t)nb * 4 + 127) & ~(size_t)127;
+  const bool staged = a.S <= kMaxStagedHeights;
+  const size_t hts_b = SCATTER && staged ? (((size_t)a.S * 8 + 127) & ~(size_t)127) : 0;
+  unsigned *h = reinterpret_cast<unsigned *>(hsmem);
+  double *hsm = reinterpret_cast<double *>(hsmem + hist_b);
+  float4 *stage = reinterpret_cast<float4 *>(hsmem + hist_b + hts_b);
+  uint64_t *full = reinterpret_cast<uint64_t *>(hsmem + hist_b + hts_b +
+                                                (size_t)kBulkStages * kBulkBytes);
+  uint64_t *empty = full + kBulkStages;
+  const int c = blockIdx.x, G = gridDim.x, tid = threadIdx.x;
+  unsigned *mine = cnt + (int64_t)c * nb;
+  const int64_t p0 = (n * c / G) & ~(int64_t)3;
+  const int64_t p1 = c + 1 == G ? n : (n * (c + 1) / G) & ~(int64_t)3;
+  const int64_t q0 = p0 >> 2, q1 = p1 >> 2;
+  const int64_t nst = (q1 - q0 + kBulkQ - 1) / kBulkQ;
+  const float4 *v = reinterpret_cast<const float4 *>(xyz);
+  auto issue = [&](int64_t i) {  // stage i -> buffer i % kBulkStages
+    const int s = (int)(i % kBulkStages);
+    const int64_t qa = q0 + i * kBulkQ;
+    const int64_t qn = q1 - qa < kBulkQ ? q1 - qa : kBulkQ;
+    mbar_expect_tx(&full[s], (uint32_t)(qn * 48));
+    bulk_load_1d(stage + (size_t)s * kBulkQ * 3, v + 3 * qa, (uint32_t)(qn * 48), &full[s]);
+  };
+  if (tid == 0) {
+    for (int s = 0; s < kBulkStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kHistNT / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int64_t i = 0; i < kBulkStages && i < nst; ++i) issue(i);
+  }
+  for (int b = tid; b < nb; b += kHistNT) h[b] = SCATTER ? offs[b] + mine[b] : 0u;
+  if (hts_b)
+    for (int k = tid; k < a.S; k += kHistNT) hsm[k] = a.derive ? plane_height(a, k) : a.heights[k];
+  __syncthreads();
+  const double *hts = SCATTER && staged ? hsm : a.heights;
+  for (int64_t i = 0; i < nst; ++i) {
+    const int s = (int)(i % kBulkStages);
+    const uint32_t ph = (uint32_t)((i / kBulkStages) & 1);
+    mbar_wait(&full[s], ph);
+    const int64_t qn = q1 - (q0 + i * kBulkQ);
+    if (tid < qn) {
+      const float4 *sq = stage + (size_t)s * kBulkQ * 3 + 3 * tid;
+      hist_quad<SCATTER>(sq[0], sq[1], sq[2], a, hts, nbx, h, recs, outside);
+    }
+    __syncwarp();
+    if ((tid & 31) == 0) mbar_arrive(&empty[s]);
+    if (tid == 0 && i + kBulkStages < nst) {
+      mbar_wait(&empty[s], ph);
+      issue(i + kBulkStages);
+    }
+  }
+  for (int64_t p = (q1 << 2) + tid; p < p1; p += kHistNT) {  // the tail (< 4 points)
+    const float4 A = make_float4(xyz[3 * p], xyz[3 * p + 1], xyz[3 * p + 2], 0.f);
+    int fi, fj, bin = 0;
+    if (point_cell_bin<SCATTER>((double)A.x, (double)A.y, (double)A.z, a, hts, fi, fj, bin)) {
+      const int b = (fi / kHBH) * nbx + fj / kHBW;
+      if (SCATTER) {
+        const unsigned pos = atomicAdd(&h[b], 1u);
+        recs[pos] = ((unsigned long long)f32_key(A.z) << 32) | ((unsigned long long)bin << 9) |
+                    (unsigned)((fi % kHBH) * kHBW + fj % kHBW);
+      } else {
+        atomicAdd(&h[b], 1u);
+      }
+    } else if (!SCATTER && outside) {
+      atomicAdd(outside, 1ull);
+    }
+  }
+  if (!SCATTER) {
+    __syncthreads();
+    for (int b = tid; b < nb; b += kHistNT) mine[b] = h[b];
+  }
+}
+// shared memory of hist_pass_bulk_kernel (0 if it does not fit one CTA)
+inline size_t hist_bulk_smem(int nb, int S, bool scatter) {
+  const size_t hist_b = ((size_t)nb * 4 + 127) & ~(size_t)127;
+  const size_t hts_b = scatter && S <= kMaxStagedHeights ? (((size_t)S * 8 + 127) & ~(size_t)127) : 0;
+  const size_t tot = hist_b + hts_b + (size_t)kBulkStages * kBulkBytes + 2 * kBulkStages * 8;
+  return tot <= 226 * 1024 ? tot : 0;
 }
 
 // per bucket: column prefix over the CTAs (in place) and the bucket total
@@ -683,43 +796,90 @@ __device__ __forceinline__ void bulk_store_box(const CUtensorMap *map, const voi
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
 
+// One slice of a reduce scan: v beats the running key (max for ground, min
+// for ceiling) -> take it, its decoded float bits (shift + one LOP3) and
+// the slice's change bit, all under one predicate.
+template <bool MAX>
+__device__ __forceinline__ void scan_update(uint32_t v, uint32_t &run, uint32_t &o, uint32_t &m,
+                                            uint32_t bit) {
+  if (MAX)
+    asm("{\n\t.reg .pred p;\n\t.reg .b32 s;\n\t"
+        "setp.gt.u32 p, %3, %0;\n\t"
+        "shr.s32 s, %3, 31;\n\t"
+        "@p mov.b32 %0, %3;\n\t"
+        "@p lop3.b32 %1, %3, s, 0x80000000, 0x4B;\n\t"
+        "@p or.b32 %2, %2, %4;\n\t}"
+        : "+r"(run), "+r"(o), "+r"(m)
+        : "r"(v), "r"(bit));
+  else
+    asm("{\n\t.reg .pred p;\n\t.reg .b32 s;\n\t"
+        "setp.lt.u32 p, %3, %0;\n\t"
+        "shr.s32 s, %3, 31;\n\t"
+        "@p mov.b32 %0, %3;\n\t"
+        "@p lop3.b32 %1, %3, s, 0x80000000, 0x4B;\n\t"
+        "@p or.b32 %2, %2, %4;\n\t}"
+        : "+r"(run), "+r"(o), "+r"(m)
+        : "r"(v), "r"(bit));
+}
+
+// streaming store, then step the pointer by a run-time stride (kept as one
+// 64-bit add per slice)
+__device__ __forceinline__ void store_step(float *&out, uint32_t o, int64_t step) {
+  asm volatile("st.global.cs.b32 [%0], %1;" ::"l"(out), "r"(o) : "memory");
+  asm("add.s64 %0, %0, %1;" : "+l"(out) : "l"(step));
+}
+
 template <bool TMA>
 __global__ void __launch_bounds__(kHB2) hist_reduce_kernel(
     const unsigned long long *__restrict__ recs, const unsigned *__restrict__ offs, int nbx,
     int rows, int cols, int S, int64_t out_stride, float *__restrict__ ground,
-    float *__restrict__ ceiling, unsigned long long *__restrict__ masks,
+    float *__restrict__ ceiling, unsigned long long *__restrict__ masks, float *sink, int ahead,
     const __grid_constant__ CUtensorMap gmap, const __grid_constant__ CUtensorMap cmap) {
   // [S][512] max keys, then min keys; with TMA the decoded layers are written
   // back in place ([S][16][32] floats = one box) and leave by bulk stores
   extern __shared__ __align__(128) uint32_t hk[];
   const int b = blockIdx.x, t = threadIdx.x;
   const unsigned r0 = offs[b], r1 = offs[b + 1];
-  if (t == 0 && r1 > r0) {  // the bucket's records DRAM -> L2 while the keys are initialised
-    const uintptr_t a0 = reinterpret_cast<uintptr_t>(recs + r0) & ~(uintptr_t)15;
-    const uintptr_t a1 = (reinterpret_cast<uintptr_t>(recs + r1) + 15) & ~(uintptr_t)15;
+  // records DRAM -> L2 ahead of use: the first `ahead` CTAs fetch their own
+  // bucket, every CTA the bucket `ahead` places on (about one wave of
+  // resident CTAs later), so a CTA's first pass finds its records in L2
+  auto prefetch = [&](unsigned q0, unsigned q1) {
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(recs + q0) & ~(uintptr_t)15;
+    const uintptr_t a1 = (reinterpret_cast<uintptr_t>(recs + q1) + 15) & ~(uintptr_t)15;
     for (uintptr_t q = a0; q < a1; q += 65536) {
       const unsigned nbytes = (unsigned)(a1 - q < 65536 ? a1 - q : 65536);
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(q), "r"(nbytes) : "memory");
+    }
+  };
+  if (t == 0) {
+    if (b < ahead && r1 > r0) prefetch(r0, r1);
+    if (b + ahead < (int)gridDim.x) {
+      const unsigned f0 = offs[b + ahead], f1 = offs[b + ahead + 1];
+      if (f1 > f0) prefetch(f0, f1);
     }
   }
   const int bi = b / nbx, bj = b - bi * nbx;
   const int i = bi * kHBH + t / kHBW, j = bj * kHBW + t % kHBW;
   const bool live = i < rows && j < cols;
   const int64_t cell = (int64_t)i * cols + j;
+  // The low 32 bits of a record are bin * 512 + cell-in-bucket, the key
+  // slot itself; records outside the stack's bins go to a per-thread dummy
+  // word past the keys (no branch around the atomic).
+  const uint32_t lim = (uint32_t)S * kHB2, dummy = lim + (uint32_t)t;
   // ground: max key per (bin, cell), bins 0 .. S-1 (16-byte stores)
   uint4 *hk4 = reinterpret_cast<uint4 *>(hk);
   for (int q = t; q < S * (kHB2 / 4); q += kHB2)
     hk4[q] = make_uint4(kKeyEmptyMax, kKeyEmptyMax, kKeyEmptyMax, kKeyEmptyMax);
   __syncthreads();
   auto gmax = [&](unsigned long long rec) {
-    const int bin = (int)((rec >> 9) & 0x7FFFFFu);
-    if (bin < S) atomicMax(hk + bin * kHB2 + (unsigned)(rec & 511u), (uint32_t)(rec >> 32));
+    const uint32_t lo = (uint32_t)rec;
+    atomicMax(hk + (lo < lim ? lo : dummy), (uint32_t)(rec >> 32));
   };
-  auto cmin = [&](unsigned long long rec) {
-    const int bin = (int)((rec >> 9) & 0x7FFFFFu);
-    if (bin > 0) atomicMin(hk + (bin - 1) * kHB2 + (unsigned)(rec & 511u), (uint32_t)(rec >> 32));
+  auto cmin = [&](unsigned long long rec) {  // bins 1 .. S stored at bin - 1
+    const uint32_t lo = (uint32_t)rec - (uint32_t)kHB2;
+    atomicMin(hk + (lo < lim ? lo : dummy), (uint32_t)(rec >> 32));
   };
-  constexpr int U = 4;  // records in flight per thread
+  constexpr int U = 8;  // records in flight per thread
   unsigned r = r0 + t;
   for (; r + (U - 1) * kHB2 < r1; r += U * kHB2) {
     unsigned long long v[U];
@@ -730,24 +890,34 @@ __global__ void __launch_bounds__(kHB2) hist_reduce_kernel(
   }
   for (; r < r1; r += kHB2) gmax(__ldg(recs + r));
   __syncthreads();
+  // Scans: the running max (min) and its decoded float change only where a
+  // slice's key beats it, so the decode and the slice-change bit sit under
+  // that one predicate; the 64-bit mask is kept as two 32-bit words.
+  const uint32_t *col = hk + t;
   {
     // slice-change mask: bit k set when the running max (and so the decoded
     // layer, a bijection of it) grows at slice k; bit 0 always
-    uint32_t run = kKeyEmptyMax;
-    unsigned long long m = 1ull;
-    float *out = ground + cell;
+    uint32_t run = col[0];
+    uint32_t o = run == kKeyEmptyMax ? kNaNBits : f32_bits(key_f32(run));
+    uint32_t mw[2] = {1u, 0u};
+    // cells outside the map store into one scratch word instead (no predicate)
+    float *out = live ? ground + cell : sink;
+    const int64_t step_b = live ? out_stride * 4 : 0;
+    auto step = [&](int k, uint32_t bit, uint32_t &m) {
+      scan_update<true>(col[k * kHB2], run, o, m, bit);
+      if (TMA) hk[k * kHB2 + t] = o;
+      else store_step(out, o, step_b);
+    };
+    if (TMA) hk[t] = o;
+    else store_step(out, o, step_b);
+    const int k1 = S < 32 ? S : 32;
+    uint32_t bit = 2u;
 #pragma unroll 4
-    for (int k = 0; k < S; ++k, out += out_stride) {
-      const uint32_t v = hk[k * kHB2 + t];
-      if (v > run) {
-        run = v;
-        m |= 1ull << (k & 63);
-      }
-      const float o = decode_ground(run);
-      if (TMA) hk[k * kHB2 + t] = f32_bits(o);
-      else if (live) __stcs(out, o);
-    }
-    if (masks && live) masks[(int64_t)i * cols + j] = m;
+    for (int k = 1; k < k1; ++k, bit <<= 1) step(k, bit, mw[0]);
+    bit = 1u;
+#pragma unroll 4
+    for (int k = 32; k < S; ++k, bit <<= 1) step(k, bit, mw[1]);
+    if (masks && live) masks[(int64_t)i * cols + j] = (unsigned long long)mw[1] << 32 | mw[0];
   }
   if (TMA) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -775,21 +945,27 @@ __global__ void __launch_bounds__(kHB2) hist_reduce_kernel(
   {
     // bit k+1 set when the running min (walking down) shrinks at slice k:
     // ceiling[k] differs from ceiling[k+1]
-    uint32_t run = kKeyEmptyMin;
-    unsigned long long m = 1ull;
-    float *out = ceiling + cell + (int64_t)(S - 1) * out_stride;
+    uint32_t run = col[(S - 1) * kHB2];
+    uint32_t o = run == kKeyEmptyMin ? kNaNBits : f32_bits(key_f32(run));
+    uint32_t mw[2] = {1u, 0u};
+    float *out = live ? ceiling + cell + (int64_t)(S - 1) * out_stride : sink;
+    const int64_t step_b = live ? -out_stride * 4 : 0;
+    auto step = [&](int k, uint32_t bit, uint32_t &m) {
+      scan_update<false>(col[k * kHB2], run, o, m, bit);
+      if (TMA) hk[k * kHB2 + t] = o;
+      else store_step(out, o, step_b);
+    };
+    if (TMA) hk[(S - 1) * kHB2 + t] = o;
+    else store_step(out, o, step_b);
+    // slices S-2 .. 31 set bits S-1 .. 32 (word 1), slices 30 .. 0 bits 31 .. 1
+    int k = S - 2;
+    uint32_t bit = (S >= 33 && S <= 64) ? 1u << (S - 33) : 0u;
 #pragma unroll 4
-    for (int k = S - 1; k >= 0; --k, out -= out_stride) {
-      const uint32_t v = hk[k * kHB2 + t];
-      if (v < run) {
-        run = v;
-        if (k < S - 1) m |= 1ull << ((k + 1) & 63);
-      }
-      const float o = decode_ceiling(run);
-      if (TMA) hk[k * kHB2 + t] = f32_bits(o);
-      else if (live) __stcs(out, o);
-    }
-    if (masks && live) masks[(int64_t)rows * cols + (int64_t)i * cols + j] = m;
+    for (; k >= 31; --k, bit >>= 1) step(k, bit, mw[1]);
+    bit = 1u << (k + 1 < 31 ? k + 1 : 31);
+#pragma unroll 4
+    for (; k >= 0; --k, bit >>= 1) step(k, bit, mw[0]);
+    if (masks && live) masks[(int64_t)rows * cols + (int64_t)i * cols + j] = (unsigned long long)mw[1] << 32 | mw[0];
   }
   if (TMA) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -811,7 +987,7 @@ __global__ void __launch_bounds__(kHB2) hist_reduce_split_kernel(
     const unsigned long long *__restrict__ recs, const unsigned *__restrict__ offs, int nbx,
     int rows, int cols, int S, int64_t out_stride, float *__restrict__ ground,
     float *__restrict__ ceiling, unsigned long long *__restrict__ masks) {
-  extern __shared__ __align__(16) uint32_t hk[];      // [S][512] keys
+  extern __shared__ __align__(128) uint32_t hk[];     // [S][512] keys
   uint4 *xfer = reinterpret_cast<uint4 *>(hk + (size_t)S * kHB2);            // [4][128]
   unsigned long long *msk = reinterpret_cast<unsigned long long *>(xfer + 4 * 128);  // [2][512]
   const int b = blockIdx.x, t = threadIdx.x;
@@ -1397,6 +1573,7 @@ int launch_build(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, const pct_
     unsigned *bsum = reinterpret_cast<unsigned *>(b0 + hbytes + 256 + cbytes + 2 * tbytes);
     unsigned long long *recs = reinterpret_cast<unsigned long long *>(
         b0 + hbytes + 256 + cbytes + 2 * tbytes + sbytes);
+    float *sink = reinterpret_cast<float *>(b0 + hbytes + 128);  // unused bytes of `outs`
     if (!derive) PCT_CUDA(ctx, upload_async(ctx, hd, heights_host, (size_t)S * sizeof(double)));
     if (whole) outs = nullptr;
     else PCT_CUDA(ctx, cudaMemsetAsync(outs, 0, 8, ctx->stream));
@@ -1405,7 +1582,19 @@ int launch_build(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, const pct_
     const size_t hist = ((size_t)hnb * 4 + 15) & ~(size_t)15;
     const size_t hsm = hist + (S <= kMaxStagedHeights ? (size_t)S * sizeof(double) : 0);
     const int nbi = (int)hnb;
-    if (dtype == PCT_F32) {
+    // points staged through shared memory by bulk copies when the histogram
+    // leaves room for the stages (PCT_HIST_BULK=0: direct loads)
+    const char *hb = getenv("PCT_HIST_BULK");
+    const bool bulk_ok = dtype == PCT_F32 && (reinterpret_cast<uintptr_t>(xyz) & 15) == 0 &&
+                         !(hb && hb[0] == '0');
+    const size_t bsm_c = bulk_ok ? hist_bulk_smem(nbi, S, false) : 0;
+    const size_t bsm_s = bulk_ok ? hist_bulk_smem(nbi, S, true) : 0;
+    if (bsm_c) {
+      PCT_CUDA(ctx, cudaFuncSetAttribute(hist_pass_bulk_kernel<false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm_c));
+      hist_pass_bulk_kernel<false><<<G, kHistNT, bsm_c, ctx->stream>>>(
+          static_cast<const float *>(xyz), n, a, hbx, nbi, cnt, nullptr, nullptr, outs);
+    } else if (dtype == PCT_F32) {
       PCT_CUDA(ctx, cudaFuncSetAttribute(hist_pass_kernel<float, false>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
       hist_pass_kernel<float, false><<<G, kHistNT, hist, ctx->stream>>>(
@@ -1424,7 +1613,12 @@ int launch_build(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, const pct_
     if (int rc = check_launch(ctx, "tile_sums_kernel")) return rc;
     tile_offsets_kernel<<<nsb, 1024, 0, ctx->stream>>>(tot, nbi, bsum, offs, nullptr, 1);
     if (int rc = check_launch(ctx, "tile_offsets_kernel")) return rc;
-    if (dtype == PCT_F32) {
+    if (bsm_s) {
+      PCT_CUDA(ctx, cudaFuncSetAttribute(hist_pass_bulk_kernel<true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm_s));
+      hist_pass_bulk_kernel<true><<<G, kHistNT, bsm_s, ctx->stream>>>(
+          static_cast<const float *>(xyz), n, a, hbx, nbi, cnt, offs, recs, outs);
+    } else if (dtype == PCT_F32) {
       PCT_CUDA(ctx, cudaFuncSetAttribute(hist_pass_kernel<float, true>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
       hist_pass_kernel<float, true><<<G, kHistNT, hsm, ctx->stream>>>(
@@ -1437,6 +1631,12 @@ int launch_build(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, const pct_
     }
     if (int rc = check_launch(ctx, "hist_scatter_kernel")) return rc;
     const size_t rsm = (size_t)S * kHB2 * 4;
+    const size_t rsm1 = rsm + kHB2 * 4;  // + one dummy word per thread
+    // records prefetched one wave of resident CTAs ahead (PCT_REDUCE_AHEAD)
+    // (0: each CTA its own bucket; one wave ahead measured slower at cfg3,
+    // 4.32 vs 4.22 ms build)
+    int ahead = 0;
+    if (const char *av = getenv("PCT_REDUCE_AHEAD")) ahead = atoi(av);
     unsigned long long *mk = (whole && S <= 64) ? ctx->build_masks : nullptr;
     // the layers leave by TMA bulk tensor stores when their rows are 16-byte
     // pitched (one [S][16][32] box per bucket and layer)
@@ -1484,14 +1684,14 @@ int launch_build(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, const pct_
           recs, offs, hbx, nrows, fr.cols, S, out_stride, ground, ceiling, mk);
     } else if (tma) {
       PCT_CUDA(ctx, cudaFuncSetAttribute(hist_reduce_kernel<true>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));
-      hist_reduce_kernel<true><<<(unsigned)hnb, kHB2, rsm, ctx->stream>>>(
-          recs, offs, hbx, nrows, fr.cols, S, out_stride, ground, ceiling, mk, gmap, cmap);
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm1));
+      hist_reduce_kernel<true><<<(unsigned)hnb, kHB2, rsm1, ctx->stream>>>(
+          recs, offs, hbx, nrows, fr.cols, S, out_stride, ground, ceiling, mk, sink, ahead, gmap, cmap);
     } else {
       PCT_CUDA(ctx, cudaFuncSetAttribute(hist_reduce_kernel<false>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));
-      hist_reduce_kernel<false><<<(unsigned)hnb, kHB2, rsm, ctx->stream>>>(
-          recs, offs, hbx, nrows, fr.cols, S, out_stride, ground, ceiling, mk, gmap, cmap);
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm1));
+      hist_reduce_kernel<false><<<(unsigned)hnb, kHB2, rsm1, ctx->stream>>>(
+          recs, offs, hbx, nrows, fr.cols, S, out_stride, ground, ceiling, mk, sink, ahead, gmap, cmap);
     }
     if (mk) ctx->build_masks_written = true;
     return check_launch(ctx, "hist_reduce_kernel");

@@ -573,33 +573,7 @@ __global__ void __launch_bounds__(NT, MINB) resolve_inflate_kernel(
 // work item is fetched by the Tensor Memory Accelerator
 // (cp.async.bulk.tensor.3d, completion on an mbarrier) into the second of
 // two shared-memory buffers while the current item is resolved and inflated.
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-// bounded spin: a transfer that never lands (bad tensor map) traps instead of
-// hanging the device
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-  for (uint32_t spins = 0;; ++spins) {
-    uint32_t done;
-    asm volatile(
-        "{\n .reg .pred p;\n"
-        " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-        " selp.u32 %0, 1, 0, p;\n}"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-    if (done) return;
-    if (spins > (1u << 24)) __trap();
-  }
-}
+#include "bulk.cuh"  // smem_u32, mbarrier helpers
 __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, uint64_t *bar, int x,
                                             int y, int z) {
   asm volatile(

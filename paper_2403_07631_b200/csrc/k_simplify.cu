@@ -241,11 +241,28 @@ __global__ void __launch_bounds__(kWinNT) window_skip_kernel(SimpArgs A, SimpMas
       }
       if ((m & want & ~known) != 0ull) atomicOr(&btab[k], m & want);
     };
-    while (ev) {
-      const int k = __ffsll((long long)ev) - 1;
+    // event slices in order; the next event's two loads are issued before
+    // this one is processed (one event of latency hidden per lane)
+    auto fetch = [&](int k, float &e, float &c) {
+      e = live ? __ldg(pg + (int64_t)k * A.stride) : bits_f32(kNaNBits);
+      c = live ? __ldg(pc + (int64_t)k * A.stride) : 0.f;
+    };
+    int kn = -1;
+    float en = 0.f, cn = 0.f;
+    if (ev) {
+      kn = __ffsll((long long)ev) - 1;
       ev &= ev - 1ull;
-      const float e = live ? __ldg(pg + (int64_t)k * A.stride) : bits_f32(kNaNBits);
-      const float c = live ? __ldg(pc + (int64_t)k * A.stride) : 0.f;
+      fetch(kn, en, cn);
+    }
+    while (kn >= 0) {
+      const int k = kn;
+      const float e = en, c = cn;
+      kn = -1;
+      if (ev) {
+        kn = __ffsll((long long)ev) - 1;
+        ev &= ev - 1ull;
+        fetch(kn, en, cn);
+      }
       if ((vm >> k) & 1ull) {  // this lane's segment ends at k - 1
         candidate(k - 1, true, e, c);
         const int slot = nseg & (kWin - 1);
