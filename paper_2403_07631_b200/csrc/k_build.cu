@@ -680,8 +680,9 @@ __global__ void __launch_bounds__(kHistNT, 1) hist_pass_bulk_kernel(
     unsigned long long *__restrict__ recs, unsigned long long *outside) {
   extern __shared__ __align__(128) unsigned char hsmem[];
   const size_t hist_b = ((size_t)nb * 4 + 127) & ~(size_t)127;
-  const bool staged = a.S <= kMaxStagedHeights;
-  const size_t hts_b = SCATTER && staged ? (((size_t)a.S * 8 + 127) & ~(size_t)127) : 0;
+  // (launched only with S <= kMaxStagedHeights: the heights are always in
+  // shared memory, so the bin search reads them with LDS, not generic loads)
+  const size_t hts_b = SCATTER ? (((size_t)a.S * 8 + 127) & ~(size_t)127) : 0;
   unsigned *h = reinterpret_cast<unsigned *>(hsmem);
   double *hsm = reinterpret_cast<double *>(hsmem + hist_b);
   float4 *stage = reinterpret_cast<float4 *>(hsmem + hist_b + hts_b);
@@ -711,10 +712,10 @@ __global__ void __launch_bounds__(kHistNT, 1) hist_pass_bulk_kernel(
     for (int64_t i = 0; i < kBulkStages && i < nst; ++i) issue(i);
   }
   for (int b = tid; b < nb; b += kHistNT) h[b] = SCATTER ? offs[b] + mine[b] : 0u;
-  if (hts_b)
+  if (SCATTER)
     for (int k = tid; k < a.S; k += kHistNT) hsm[k] = a.derive ? plane_height(a, k) : a.heights[k];
   __syncthreads();
-  const double *hts = SCATTER && staged ? hsm : a.heights;
+  const double *hts = hsm;
   for (int64_t i = 0; i < nst; ++i) {
     const int s = (int)(i % kBulkStages);
     const uint32_t ph = (uint32_t)((i / kBulkStages) & 1);
@@ -755,7 +756,8 @@ __global__ void __launch_bounds__(kHistNT, 1) hist_pass_bulk_kernel(
 // shared memory of hist_pass_bulk_kernel (0 if it does not fit one CTA)
 inline size_t hist_bulk_smem(int nb, int S, bool scatter) {
   const size_t hist_b = ((size_t)nb * 4 + 127) & ~(size_t)127;
-  const size_t hts_b = scatter && S <= kMaxStagedHeights ? (((size_t)S * 8 + 127) & ~(size_t)127) : 0;
+  if (S > kMaxStagedHeights) return 0;
+  const size_t hts_b = scatter ? (((size_t)S * 8 + 127) & ~(size_t)127) : 0;
   const size_t tot = hist_b + hts_b + (size_t)kBulkStages * kBulkBytes + 2 * kBulkStages * 8;
   return tot <= 226 * 1024 ? tot : 0;
 }

@@ -298,42 +298,78 @@ int window_blocks_per_sm(pct_ctx *ctx, size_t smem) {
   return per_sm;
 }
 
-__device__ __forceinline__ void triple_any(const SimpArgs &A, const Triple T, int *flag) {
+// Is any cell of [lo, hi) a traversable cell of slice T.k not covered by
+// T.below / T.above?  Block-strided, 4 cells per thread per step: the 8
+// loads of the 4 cells are issued together, then the neighbour slices' loads
+// of the candidates among them (early exit once any thread of the block has
+// found one, or another block already has).
+__device__ __forceinline__ void triple_any(const SimpArgs &A, const Triple T, int *flag,
+                                           int64_t lo, int64_t hi, int64_t start, int64_t step) {
   __shared__ int skip;
   __syncthreads();  // previous triple's readers of `skip` are done
   if (threadIdx.x == 0) skip = *((volatile int *)flag);  // already known unique
   __syncthreads();
   if (skip) return;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  constexpr int U = 4;
+  const float *gk = A.ground + (int64_t)T.k * A.stride, *ck = A.cost + (int64_t)T.k * A.stride;
+  const float *gb = A.ground + (int64_t)T.below * A.stride, *cb = A.cost + (int64_t)T.below * A.stride;
+  const float *ga = A.ground + (int64_t)T.above * A.stride, *ca = A.cost + (int64_t)T.above * A.stride;
   bool any = false;
-  for (int64_t cell = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; cell < A.cells && !any;
-       cell += stride) {
-    const float e = __ldg(A.ground + (int64_t)T.k * A.stride + cell);
-    const float c = __ldg(A.cost + (int64_t)T.k * A.stride + cell);
-    if (!(finite32(e) && c < A.c_barrier32)) continue;
-    bool u = true;
-    if (T.below >= 0)
-      u = not_covered(e, c, __ldg(A.ground + (int64_t)T.below * A.stride + cell),
-                      __ldg(A.cost + (int64_t)T.below * A.stride + cell), A.eps_e, true);
-    if (u && T.above >= 0)
-      u = not_covered(e, c, __ldg(A.ground + (int64_t)T.above * A.stride + cell),
-                      __ldg(A.cost + (int64_t)T.above * A.stride + cell), A.eps_e, false);
-    any = u;
+  for (int64_t c0 = lo + start; c0 < hi && !any; c0 += U * step) {
+    float e[U], c[U];
+    bool cand[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t cell = c0 + u * step;
+      const bool in = cell < hi;
+      e[u] = in ? __ldg(gk + cell) : bits_f32(kNaNBits);
+      c[u] = in ? __ldg(ck + cell) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) cand[u] = finite32(e[u]) && c[u] < A.c_barrier32;
+    float eb[U], cbv[U], ea[U], cav[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t cell = c0 + u * step;
+      const bool lb = cand[u] && T.below >= 0, la = cand[u] && T.above >= 0;
+      eb[u] = lb ? __ldg(gb + cell) : 0.f;
+      cbv[u] = lb ? __ldg(cb + cell) : 0.f;
+      ea[u] = la ? __ldg(ga + cell) : 0.f;
+      cav[u] = la ? __ldg(ca + cell) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (!cand[u]) continue;
+      bool un = true;
+      if (T.below >= 0) un = not_covered(e[u], c[u], eb[u], cbv[u], A.eps_e, true);
+      if (un && T.above >= 0) un = not_covered(e[u], c[u], ea[u], cav[u], A.eps_e, false);
+      any = any || un;
+    }
   }
   if (__syncthreads_or(any) && threadIdx.x == 0) atomicOr(flag, 1);
 }
 
-// blockIdx.y = triple (host lists); with a device count, blocks stride over
-// the device-built list instead (gridDim.y small, no empty blocks)
+// blockIdx.y = triple (host lists), blocks stride over all cells; with a
+// device count, the blocks split (triple, cell range) items instead: each
+// of the n triples gets about G / n ranges, so a single triple still has the
+// whole grid (G blocks)
 __global__ void __launch_bounds__(256) triples_kernel(SimpArgs A, const Triple *__restrict__ tr,
                                                       int *__restrict__ flags,
                                                       const int *__restrict__ count = nullptr) {
   if (!count) {
-    triple_any(A, tr[blockIdx.y], flags + blockIdx.y);
+    triple_any(A, tr[blockIdx.y], flags + blockIdx.y, 0, A.cells,
+               (int64_t)blockIdx.x * blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x);
     return;
   }
   const int n = *count;
-  for (int t = blockIdx.y; t < n; t += gridDim.y) triple_any(A, tr[t], flags + t);
+  if (n <= 0) return;
+  const int G = (int)(gridDim.x * gridDim.y), b = (int)(blockIdx.y * gridDim.x + blockIdx.x);
+  const int X = G / n > 1 ? G / n : 1;
+  for (int w = b; w < n * X; w += G) {
+    const int t = w / X, x = w - t * X;
+    const int64_t lo = A.cells * x / X, hi = A.cells * (x + 1) / X;
+    triple_any(A, tr[t], flags + t, lo, hi, threadIdx.x, blockDim.x);
+  }
 }
 
 // The host sweep's first pass, replayed on the device from the window table
@@ -535,10 +571,9 @@ int run_simplify(pct_ctx *ctx, const float *ground, const float *cost, int S, in
     if (spec) {
       spec_sweep_kernel<<<1, 32, 0, ctx->stream>>>(table, S, dtr, dflags, dcount);
       if (int rc = check_launch(ctx, "spec_sweep_kernel")) return rc;
-      int64_t bx = (A.cells + 255) / 256;
-      if (bx > ctx->num_sms * 2) bx = ctx->num_sms * 2;
-      triples_kernel<<<dim3((unsigned)bx, (unsigned)std::min(S, 8)), 256, 0, ctx->stream>>>(
-          A, dtr, dflags, dcount);
+      int64_t bx = (A.cells + 1023) / 1024;
+      if (bx > ctx->num_sms) bx = ctx->num_sms;
+      triples_kernel<<<dim3((unsigned)bx, 8u), 256, 0, ctx->stream>>>(A, dtr, dflags, dcount);
       if (int rc = check_launch(ctx, "triples_kernel")) return rc;
       PCT_CUDA(ctx, readback_async(ctx, hbase, table, rbytes));
     } else {
