@@ -979,6 +979,113 @@ __global__ void __launch_bounds__(kHB2) hist_reduce_kernel(
   }
 }
 
+// Per-cell slice scans of the reduce (plain stores): ground walks up with the
+// running max key, ceiling walks down with the running min key; `col` is
+// the cell's key column ([S] keys kHB2 apart).  Returns the slice-change
+// mask (bits as hist_reduce_kernel's).
+__device__ __forceinline__ unsigned long long scan_ground_col(const uint32_t *col, int S,
+                                                              float *out, int64_t step_b) {
+  uint32_t run = col[0];
+  uint32_t o = run == kKeyEmptyMax ? kNaNBits : key_bits(run);
+  uint32_t mw0 = 1u, mw1 = 0u;
+  store_step(out, o, step_b);
+  const int k1 = S < 32 ? S : 32;
+  uint32_t bit = 2u;
+#pragma unroll 4
+  for (int k = 1; k < k1; ++k, bit <<= 1) {
+    scan_update<true>(col[k * kHB2], run, o, mw0, bit);
+    store_step(out, o, step_b);
+  }
+  bit = 1u;
+#pragma unroll 4
+  for (int k = 32; k < S; ++k, bit <<= 1) {
+    scan_update<true>(col[k * kHB2], run, o, mw1, bit);
+    store_step(out, o, step_b);
+  }
+  return (unsigned long long)mw1 << 32 | mw0;
+}
+__device__ __forceinline__ unsigned long long scan_ceiling_col(const uint32_t *col, int S,
+                                                               float *out, int64_t step_b) {
+  uint32_t run = col[(S - 1) * kHB2];
+  uint32_t o = run == kKeyEmptyMin ? kNaNBits : key_bits(run);
+  uint32_t mw0 = 1u, mw1 = 0u;
+  store_step(out, o, step_b);
+  int k = S - 2;
+  uint32_t bit = (S >= 33 && S <= 64) ? 1u << (S - 33) : 0u;
+#pragma unroll 4
+  for (; k >= 31; --k, bit >>= 1) {
+    scan_update<false>(col[k * kHB2], run, o, mw1, bit);
+    store_step(out, o, step_b);
+  }
+  bit = 1u << (k + 1 < 31 ? k + 1 : 31);
+#pragma unroll 4
+  for (; k >= 0; --k, bit >>= 1) {
+    scan_update<false>(col[k * kHB2], run, o, mw0, bit);
+    store_step(out, o, step_b);
+  }
+  return (unsigned long long)mw1 << 32 | mw0;
+}
+
+// H4, one pass: 1024 threads, both key planes in shared memory ([S][512]
+// max keys, [S][512] min keys, 1024 dummy words: 2 x S x 2 KB + 4 KB), each
+// record read once for both atomics; then threads 0-511 scan the ground
+// columns and 512-1023 the ceiling columns at the same time.  One CTA per SM.
+__global__ void __launch_bounds__(2 * kHB2, 1) hist_reduce_both_kernel(
+    const unsigned long long *__restrict__ recs, const unsigned *__restrict__ offs, int nbx,
+    int rows, int cols, int S, int64_t out_stride, float *__restrict__ ground,
+    float *__restrict__ ceiling, unsigned long long *__restrict__ masks, float *sink) {
+  extern __shared__ __align__(128) uint32_t hk[];
+  const int b = blockIdx.x, t = threadIdx.x;
+  const unsigned r0 = offs[b], r1 = offs[b + 1];
+  if (t == 0 && r1 > r0) {
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(recs + r0) & ~(uintptr_t)15;
+    const uintptr_t a1 = (reinterpret_cast<uintptr_t>(recs + r1) + 15) & ~(uintptr_t)15;
+    for (uintptr_t q = a0; q < a1; q += 65536) {
+      const unsigned nbytes = (unsigned)(a1 - q < 65536 ? a1 - q : 65536);
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(q), "r"(nbytes) : "memory");
+    }
+  }
+  const uint32_t lim = (uint32_t)S * kHB2, dummy = 2 * lim + (uint32_t)t;
+  uint4 *hk4 = reinterpret_cast<uint4 *>(hk);
+  const int nq = S * (kHB2 / 4);
+  for (int q = t; q < 2 * nq; q += 2 * kHB2) {
+    const uint32_t e = q < nq ? kKeyEmptyMax : kKeyEmptyMin;
+    hk4[q] = make_uint4(e, e, e, e);
+  }
+  __syncthreads();
+  auto both = [&](unsigned long long rec) {
+    const uint32_t lo = (uint32_t)rec, key = (uint32_t)(rec >> 32);
+    const uint32_t lc = lo - (uint32_t)kHB2;  // ceiling: bins 1 .. S at bin - 1
+    atomicMax(hk + (lo < lim ? lo : dummy), key);
+    atomicMin(hk + (lc < lim ? lim + lc : dummy), key);
+  };
+  constexpr int U = 8;
+  unsigned r = r0 + t;
+  for (; r + (U - 1) * 2 * kHB2 < r1; r += U * 2 * kHB2) {
+    unsigned long long v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = __ldcs(recs + r + u * 2 * kHB2);
+#pragma unroll
+    for (int u = 0; u < U; ++u) both(v[u]);
+  }
+  for (; r < r1; r += 2 * kHB2) both(__ldcs(recs + r));
+  __syncthreads();
+  const int side = t / kHB2, c = t - side * kHB2;  // warp-uniform side
+  const int bi = b / nbx, bj = b - bi * nbx;
+  const int i = bi * kHBH + c / kHBW, j = bj * kHBW + c % kHBW;
+  const bool live = i < rows && j < cols;
+  const int64_t cell = (int64_t)i * cols + j;
+  unsigned long long m;
+  if (side == 0) {
+    m = scan_ground_col(hk + c, S, live ? ground + cell : sink, live ? out_stride * 4 : 0);
+  } else {
+    m = scan_ceiling_col(hk + lim + c, S,
+                         live ? ceiling + cell + (int64_t)(S - 1) * out_stride : sink,
+                         live ? -out_stride * 4 : 0);
+  }
+  if (masks && live) masks[(int64_t)side * rows * cols + cell] = m;
+}
+
 // H4, split scan: the same reduction, with the per-cell slice scans shared by
 // all 512 threads: thread t takes 4 adjacent cells (one 16-byte vector of
 // keys per slice) and a quarter of the slices; each quarter first reduces its
@@ -1678,7 +1785,13 @@ int launch_build(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, const pct_
     // the split-scan reduce measured slower at cfg3 (2.42 vs 2.18 ms):
     // opt-in (PCT_BUILD_REDUCE=2)
     const char *rv = getenv("PCT_BUILD_REDUCE");
-    if (!tma && rv && rv[0] == '2') {
+    const size_t bsm = (size_t)2 * S * kHB2 * 4 + 2 * kHB2 * 4;
+    if (!tma && rv && rv[0] == '3' && bsm <= 226 * 1024) {
+      PCT_CUDA(ctx, cudaFuncSetAttribute(hist_reduce_both_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
+      hist_reduce_both_kernel<<<(unsigned)hnb, 2 * kHB2, bsm, ctx->stream>>>(
+          recs, offs, hbx, nrows, fr.cols, S, out_stride, ground, ceiling, mk, sink);
+    } else if (!tma && rv && rv[0] == '2') {
       const size_t ssm = rsm + 4 * 128 * 16 + 2 * kHB2 * 8;
       PCT_CUDA(ctx, cudaFuncSetAttribute(hist_reduce_split_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm));
