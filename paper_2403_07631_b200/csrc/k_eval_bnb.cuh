@@ -316,7 +316,22 @@ __global__ void __launch_bounds__(NT, MINB) resolve_inflate_bnb_kernel(
       issue(m, t, r * maps[m].run);
     }
   }
+  if (tid < 2) {  // the first item's mask words (parity 0)
+    unsigned *w = reinterpret_cast<unsigned *>(skipmask);
+    bool c0 = false;
+    if (blockIdx.x < n_items) {
+      int m, r, t;
+      decode(blockIdx.x, m, r, t);
+      c0 = maps[m].chg != nullptr;
+    }
+    w[tid] = c0 ? 0u : 0xFFFFFFFFu;
+  }
   __syncthreads();
+  int ip = 0;  // parity of the item's mask words
+  // change-map bytes of the next item, prefetched into registers
+  constexpr int kChgPf = 8;
+  unsigned char cpf[kChgPf];
+  int cpf_item = -1, cpf_j0 = 0, cpf_js = 1;
   uint32_t phase_bits = 0u;
   int lc = 0;  // loads consumed
   for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
@@ -342,30 +357,93 @@ __global__ void __launch_bounds__(NT, MINB) resolve_inflate_bnb_kernel(
       }
     };
     // skippable slices of this item: no change of encoded c_init or gentle
-    // flag in the tile + R + r window since the slice below (walk change map);
-    // every thread checks a few (slice, block) bytes, changes are OR-ed into
-    // a shared mask
-    unsigned *chgw = reinterpret_cast<unsigned *>(skipmask);  // [2]: slices 0-31, 32-63
-    __syncthreads();  // every thread is done with the previous item's mask
-    if (tid < 2) chgw[tid] = M.chg ? 0u : 0xFFFFFFFFu;  // no change map: nothing skips
-    __syncthreads();
+    // flag in the tile + R + r window since the slice below (walk change map).
+    // Each thread ORs the bytes it checks into a register mask (its loads
+    // batched, no atomic per byte), one shared atomic per warp; the shared
+    // words alternate between items (parity ip), the pair of the next item
+    // is cleared here, before this item's slice barriers, so one barrier per
+    // item suffices.
+    unsigned *chgw = reinterpret_cast<unsigned *>(skipmask) + 2 * ip;  // [2]: slices 0-31, 32-63
     if (M.chg) {
-      const int nbr = (rows + 7) >> 3, wpr = M.wpr;
-      const int br0 = max(0, (i0 - R - PR) >> 3), br1 = min(nbr - 1, (i0 + TH + R + PR - 1) >> 3);
-      const int wc0 = max(0, (j0 - R - PR) >> 5), wc1 = min(wpr - 1, (j0 + TW + R + PR - 1) >> 5);
-      const int nb = br1 - br0 + 1, nw = wc1 - wc0 + 1;
-      const int per = nb * nw;
-      const int64_t cms = (int64_t)nbr * wpr;
-      for (int q = tid; q < (k1 - k0 - 1) * per; q += NT) {
-        const int j = 1 + q / per, e = q - (j - 1) * per;
-        const int br = br0 + e / nw, wc = wc0 + e - (e / nw) * nw;
-        if (M.chg[(int64_t)(k0 + j) * cms + (int64_t)br * wpr + wc])
-          atomicOr(&chgw[j >> 5], 1u << (j & 31));
+      uint64_t loc = 0ull;
+      if (cpf_item == item) {  // this thread's bytes were loaded during the previous item
+#pragma unroll
+        for (int u = 0; u < kChgPf; ++u) {
+          const int j = cpf_j0 + u * cpf_js;
+          if (j < 64) loc |= (uint64_t)(cpf[u] != 0) << j;  // 0 beyond the item's slices
+        }
+      } else {
+        const int nbr = (rows + 7) >> 3, wpr = M.wpr;
+        const int br0 = max(0, (i0 - R - PR) >> 3), br1 = min(nbr - 1, (i0 + TH + R + PR - 1) >> 3);
+        const int wc0 = max(0, (j0 - R - PR) >> 5), wc1 = min(wpr - 1, (j0 + TW + R + PR - 1) >> 5);
+        const int nb = br1 - br0 + 1, nw = wc1 - wc0 + 1;
+        const int per = nb * nw;
+        const int64_t cms = (int64_t)nbr * wpr;
+        for (int q = tid; q < (k1 - k0 - 1) * per; q += NT) {
+          const int j = 1 + q / per, e = q - (j - 1) * per;
+          const int br = br0 + e / nw, wc = wc0 + e - (e / nw) * nw;
+          loc |= (uint64_t)(M.chg[(int64_t)(k0 + j) * cms + (int64_t)br * wpr + wc] != 0) << j;
+        }
+      }
+      const unsigned lo = __reduce_or_sync(0xFFFFFFFFu, (unsigned)loc);
+      const unsigned hi = __reduce_or_sync(0xFFFFFFFFu, (unsigned)(loc >> 32));
+      if (lane == 0) {
+        if (lo) atomicOr(&chgw[0], lo);
+        if (hi) atomicOr(&chgw[1], hi);
       }
     }
     __syncthreads();
     const uint64_t changed = (uint64_t)chgw[0] | ((uint64_t)chgw[1] << 32);
     const uint64_t skm = ~changed;  // bit j: slice k0 + j is skippable (bit 0 unused: first)
+    // the next item's change-map bytes: loads issued now, consumed at its start
+    // (thread: one (block, word) entry of the window, every jstep-th slice;
+    // only when the entries fit kChgPf registers, else that item loads them
+    // itself)
+    cpf_item = -1;
+    if (item + (int)gridDim.x < n_items) {
+      const int it2 = item + (int)gridDim.x;
+      int m2, r2, t2;
+      decode(it2, m2, r2, t2);
+      const EvalMap &M2 = maps[m2];
+      if (M2.chg) {
+        int a0, b0;
+        origin(M2, t2, a0, b0);
+        const int q0 = r2 * M2.run, q1 = min(M2.S, q0 + M2.run);
+        const int nbr = (M2.rows + 7) >> 3, wpr = M2.wpr;
+        const int br0 = max(0, (a0 - R - PR) >> 3), br1 = min(nbr - 1, (a0 + TH + R + PR - 1) >> 3);
+        const int wc0 = max(0, (b0 - R - PR) >> 5), wc1 = min(wpr - 1, (b0 + TW + R + PR - 1) >> 5);
+        const int nb = br1 - br0 + 1, nw = wc1 - wc0 + 1;
+        const int per = nb * nw;
+        const int js = per <= NT ? NT / per : 1;
+        if (per <= NT && (q1 - q0 - 1 + js - 1) / js <= kChgPf) {  // uniform
+          const int64_t cms = (int64_t)nbr * wpr;
+          const bool mine = tid < js * per;
+          const int e = tid % per;
+          const int br = br0 + e / nw, wc = wc0 + e - (e / nw) * nw;
+          const unsigned char *pc = M2.chg + (int64_t)q0 * cms + (int64_t)br * wpr + wc;
+          cpf_j0 = 1 + tid / per;
+          cpf_js = js;
+#pragma unroll
+          for (int u = 0; u < kChgPf; ++u) {
+            const int j = cpf_j0 + u * js;
+            cpf[u] = (mine && j < q1 - q0) ? pc[(int64_t)j * cms] : (unsigned char)0;
+          }
+          cpf_item = it2;
+        }
+      }
+    }
+    if (tid < 2) {  // the next item's pair (its last readers finished an item ago)
+      unsigned *nx = reinterpret_cast<unsigned *>(skipmask) + 2 * (ip ^ 1);
+      const int item2 = item + (int)gridDim.x;
+      bool nchg = false;
+      if (item2 < n_items) {
+        int m2, r2, t2;
+        decode(item2, m2, r2, t2);
+        nchg = maps[m2].chg != nullptr;
+      }
+      nx[tid] = nchg ? 0u : 0xFFFFFFFFu;  // no change map: nothing skips
+    }
+    ip ^= 1;
     unsigned long long touched = 0ull;  // slices whose outputs may have changed (thread 0)
     // sparse P0a prefetch registers: fresh byte + bitmap word of this
     // thread's window entries for slice pf_k

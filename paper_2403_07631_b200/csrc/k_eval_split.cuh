@@ -289,7 +289,7 @@ __global__ void __launch_bounds__(kWalkNT) terrain_walk_skip_kernel(
     int cols, float *__restrict__ enc_out, EncLayout L, uint32_t *__restrict__ bits_out,
     int wpr, unsigned char *__restrict__ chgmap, const unsigned long long *__restrict__ gmask,
     const unsigned long long *__restrict__ cmask, unsigned char *__restrict__ fresh, int fpitch,
-    int run) {
+    unsigned long long runmask) {
   int kb = 0, ke = S;
   if constexpr (CHUNKED) {  // blockIdx.y = chunk of slices (small maps: more threads in flight)
     kb = (int)((int64_t)S * blockIdx.y / gridDim.y);
@@ -412,7 +412,7 @@ __global__ void __launch_bounds__(kWalkNT) terrain_walk_skip_kernel(
   // sparse output: only the slices this warp recomputed, and the run starts
   // of the resolve / inflate kernel (loaded whole, without a previous slice)
   unsigned long long ev = todo;
-  for (int k = (kb + run - 1) / run * run; k < ke; k += run) ev |= 1ull << k;
+  ev |= runmask & kmask & ~((1ull << kb) - 1ull);  // run starts (host-built bits k % run == 0)
   float *pe0 = enc_out + L.at(0, i, j);
   uint32_t *pb0 = bits_out + (int64_t)i * wpr + (j0_ >> 5);
   unsigned char *pf0 = fresh + (int64_t)i * fpitch + (j0_ >> 5);

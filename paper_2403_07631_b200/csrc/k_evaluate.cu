@@ -626,6 +626,13 @@ template <int R>
 constexpr int kBnbMinBlocks() {
   return R <= 4 ? 6 : 4;
 }
+// the sparse-merge instantiation: its shared memory allows 5 CTAs per SM at
+// R = 4, so it may use the registers of 5 (the change-map prefetch lives in
+// them)
+template <int R>
+constexpr int kBnbMinBlocksSp() {
+  return R <= 4 ? 5 : 4;
+}
 
 template <int R, int PR, int TH, int TW, int BNT = 256>
 int launch_split(pct_ctx *ctx, const float *ground, const float *ceiling, int S, int rows,
@@ -734,7 +741,7 @@ int launch_split(pct_ctx *ctx, const float *ground, const float *ceiling, int S,
       const char *spv = getenv("PCT_WALK_SPARSE");
       sparse = skip_walk && chgmap && (spv ? spv[0] == '1' : (R == 4 && bnb_run >= 16));
       if (sparse)
-        if (int rc = plan(resolve_inflate_bnb_kernel<R, PR, TH, TW, BNT, kBnbMinBlocks<R>(), true>,
+        if (int rc = plan(resolve_inflate_bnb_kernel<R, PR, TH, TW, BNT, kBnbMinBlocksSp<R>(), true>,
                           BnbGeom<R, PR, TH, TW, true>::SMEM))
           return rc;
     }
@@ -759,14 +766,17 @@ int launch_split(pct_ctx *ctx, const float *ground, const float *ceiling, int S,
       gm = m;
       cmk = m + cells;
     }
+    unsigned long long runmask = 0ull;  // slices k with k % bnb_run == 0 (S <= 64 here)
+    if (bnb_run > 0)
+      for (int k = 0; k < S && k < 64; k += bnb_run) runmask |= 1ull << k;
     if (chunks > 1)
       terrain_walk_skip_kernel<true><<<dim3(g1, chunks), kWalkNT, 0, ctx->stream>>>(
           ground, ceiling, S, rows, cols, enc, L, bits, wpr, chgmap, gm, cmk, fresh, fpitch,
-          bnb_run);
+          runmask);
     else
       terrain_walk_skip_kernel<false><<<g1, kWalkNT, 0, ctx->stream>>>(
           ground, ceiling, S, rows, cols, enc, L, bits, wpr, chgmap, gm, cmk, fresh, fpitch,
-          bnb_run);
+          runmask);
   } else
   // one slice of look-ahead measured fastest (cfg1 85 us vs 105 / 132 for
   // 2 / 4; deeper prefetch costs occupancy)
@@ -809,7 +819,7 @@ int launch_split(pct_ctx *ctx, const float *ground, const float *ceiling, int S,
     if constexpr (R == 4 || R == 8) {
      if (bnb) {
       PCT_CUDA(ctx, cb.set_symbol(c_bw, bw.data(), bw.size() * sizeof(float)));
-      auto kb = sparse ? resolve_inflate_bnb_kernel<R, PR, TH, TW, BNT, kBnbMinBlocks<R>(), true>
+      auto kb = sparse ? resolve_inflate_bnb_kernel<R, PR, TH, TW, BNT, kBnbMinBlocksSp<R>(), true>
                        : resolve_inflate_bnb_kernel<R, PR, TH, TW, BNT, kBnbMinBlocks<R>()>;
       const int bsmem = sparse ? BnbGeom<R, PR, TH, TW, true>::SMEM : BnbGeom<R, PR, TH, TW>::SMEM;
       const int64_t slots = bnb_slots;
