@@ -563,13 +563,21 @@ __device__ __forceinline__ void load_point(const T *__restrict__ xyz, int64_t p,
   z = (double)__ldg(xyz + 3 * p + 2);
 }
 
+// warp-aggregated scatter cursors (__match_any_sync): measured much slower
+// at cfg3 (build 6.36 vs 3.83 ms), compile-time opt-in only
+#ifndef PCT_SCATTER_MATCH
+#define PCT_SCATTER_MATCH 0
+#endif
 // one quad of float32 points (three 16-byte vectors): count its buckets, or
 // (SCATTER) place its records -- the 4 cells, bins and records first, then
 // the 4 cursor atomics, then the 4 stores (independent chains in flight)
 template <bool SCATTER>
+// Called by every lane of the warp (the cursor aggregation is warp-wide);
+// lanes without a quad pass valid = false.
 __device__ __forceinline__ void hist_quad(const float4 A, const float4 B, const float4 Cv,
-                                          const BinArgs &a, const double *hts, int nbx,
-                                          unsigned *h, unsigned long long *__restrict__ recs,
+                                          bool valid, const BinArgs &a, const double *hts,
+                                          int nbx, unsigned *h,
+                                          unsigned long long *__restrict__ recs,
                                           unsigned long long *outside) {
   const double px[4] = {A.x, A.w, B.z, Cv.y}, py[4] = {A.y, B.x, B.w, Cv.z},
                pz[4] = {A.z, B.y, Cv.x, Cv.w};
@@ -580,20 +588,42 @@ __device__ __forceinline__ void hist_quad(const float4 A, const float4 B, const 
     for (int u = 0; u < 4; ++u) {
       int fi, fj, bin = 0;
       bk[u] = -1;
-      if (point_cell_bin<true>(px[u], py[u], pz[u], a, hts, fi, fj, bin)) {
+      if (valid && point_cell_bin<true>(px[u], py[u], pz[u], a, hts, fi, fj, bin)) {
         bk[u] = (fi / kHBH) * nbx + fj / kHBW;
         rec[u] = ((unsigned long long)f32_key(__double2float_rn(pz[u])) << 32) |
                  ((unsigned long long)bin << 9) | (unsigned)((fi % kHBH) * kHBW + fj % kHBW);
       }
     }
     unsigned pos[4];
+#if PCT_SCATTER_MATCH
+    // warp-aggregated cursors: lanes placing into one bucket take one atomic
+    // (the leader's) and consecutive slots by lane order, so scanner-ordered
+    // inputs (walls, pillars: many lanes per bucket) do not serialise on a
+    // shared-memory address.  Record order inside a bucket does not change
+    // any layer (max / min).
+    const unsigned lane = threadIdx.x & 31u;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const unsigned act = __ballot_sync(0xFFFFFFFFu, bk[u] >= 0);
+      if (bk[u] >= 0) {
+        const unsigned peers = __match_any_sync(act, bk[u]);
+        const int leader = __ffs(peers) - 1;
+        unsigned base = 0u;
+        if ((int)lane == leader) base = atomicAdd(&h[bk[u]], (unsigned)__popc(peers));
+        base = __shfl_sync(peers, base, leader);
+        pos[u] = base + (unsigned)__popc(peers & ((1u << lane) - 1u));
+      }
+    }
+#else
 #pragma unroll
     for (int u = 0; u < 4; ++u)
       if (bk[u] >= 0) pos[u] = atomicAdd(&h[bk[u]], 1u);
+#endif
 #pragma unroll
     for (int u = 0; u < 4; ++u)
       if (bk[u] >= 0) recs[pos[u]] = rec[u];
   } else {
+    if (!valid) return;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       int fi, fj, bin = 0;
@@ -610,7 +640,7 @@ __global__ void __launch_bounds__(kHistNT, 1) hist_pass_kernel(
     const T *__restrict__ xyz, int64_t n, BinArgs a, int nbx, int nb,
     unsigned *__restrict__ cnt, const unsigned *__restrict__ offs,
     unsigned long long *__restrict__ recs, unsigned long long *outside) {
-  extern __shared__ __align__(16) unsigned char hsmem[];
+  extern __shared__ __align__(128) unsigned char hsmem[];
   unsigned *h = reinterpret_cast<unsigned *>(hsmem);
   double *hsm = reinterpret_cast<double *>(hsmem + (((size_t)nb * 4 + 15) & ~(size_t)15));
   const int c = blockIdx.x, G = gridDim.x;
@@ -647,9 +677,15 @@ __global__ void __launch_bounds__(kHistNT, 1) hist_pass_kernel(
   if (sizeof(T) == 4 && (reinterpret_cast<uintptr_t>(xyz) & 15) == 0) {
     const float4 *v = reinterpret_cast<const float4 *>(xyz);
     const int64_t q1 = p1 >> 2;  // whole quads
-    for (int64_t q = (p0 >> 2) + threadIdx.x; q < q1; q += kHistNT)
-      hist_quad<SCATTER>(__ldg(v + 3 * q), __ldg(v + 3 * q + 1), __ldg(v + 3 * q + 2), a, hts,
-                         nbx, h, recs, outside);
+    // warp-uniform trip count: lanes past the end run with valid = false
+    const int64_t lane0 = (p0 >> 2) + (threadIdx.x & ~31);
+    for (int64_t qw = lane0; qw < q1; qw += kHistNT) {
+      const int64_t q = qw + (threadIdx.x & 31);
+      const bool ok = q < q1;
+      const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+      hist_quad<SCATTER>(ok ? __ldg(v + 3 * q) : z4, ok ? __ldg(v + 3 * q + 1) : z4,
+                         ok ? __ldg(v + 3 * q + 2) : z4, ok, a, hts, nbx, h, recs, outside);
+    }
     pq = q1 << 2;
   }
   for (int64_t p = pq + threadIdx.x; p < p1; p += kHistNT) {
@@ -721,9 +757,10 @@ __global__ void __launch_bounds__(kHistNT, 1) hist_pass_bulk_kernel(
     const uint32_t ph = (uint32_t)((i / kBulkStages) & 1);
     mbar_wait(&full[s], ph);
     const int64_t qn = q1 - (q0 + i * kBulkQ);
-    if (tid < qn) {
+    {  // every lane calls (warp-wide cursor aggregation); lanes past the
+       // stage's end read a stale (valid) slot and pass valid = false
       const float4 *sq = stage + (size_t)s * kBulkQ * 3 + 3 * tid;
-      hist_quad<SCATTER>(sq[0], sq[1], sq[2], a, hts, nbx, h, recs, outside);
+      hist_quad<SCATTER>(sq[0], sq[1], sq[2], tid < qn, a, hts, nbx, h, recs, outside);
     }
     __syncwarp();
     if ((tid & 31) == 0) mbar_arrive(&empty[s]);

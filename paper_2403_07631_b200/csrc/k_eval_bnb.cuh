@@ -209,7 +209,8 @@ __device__ __forceinline__ void slow_classes(const float *__restrict__ ctr, floa
 // (the output tile lives in shared memory and is stored every slice).
 template <int R, int PR, int TH, int TW, int NT, int MINB, bool SP = false>
 __global__ void __launch_bounds__(NT, MINB) resolve_inflate_bnb_kernel(
-    const EvalMap *__restrict__ maps, const int *__restrict__ item_off, int n_maps) {
+    const EvalMap *__restrict__ maps, const int *__restrict__ item_off, int n_maps,
+    int *__restrict__ work = nullptr) {
   using G = BnbGeom<R, PR, TH, TW, SP>;
   constexpr int NWARP = NT / 32;
   constexpr int WSEG = TH * TW / NWARP;  // list entries per warp (its P2 outputs)
@@ -334,7 +335,14 @@ __global__ void __launch_bounds__(NT, MINB) resolve_inflate_bnb_kernel(
   int cpf_item = -1, cpf_j0 = 0, cpf_js = 1;
   uint32_t phase_bits = 0u;
   int lc = 0;  // loads consumed
-  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+  // Items: the CTA's first is blockIdx.x; with a work counter the next one
+  // is claimed dynamically at each item's start (thread 0, published through
+  // shared memory at the item's mask barrier), else item + gridDim.x.  Any
+  // assignment gives the same outputs (items are independent).
+  int *nxt_s = slot + 5;
+  int nxt = 0;  // the item after this one (every thread, after the mask barrier)
+  for (int item = blockIdx.x; item < n_items; item = nxt) {
+    if (tid == 0) *nxt_s = work ? atomicAdd(work, 1) + (int)gridDim.x : item + (int)gridDim.x;
     int m, r, t;
     decode(item, m, r, t);
     const EvalMap &M = maps[m];
@@ -395,13 +403,14 @@ __global__ void __launch_bounds__(NT, MINB) resolve_inflate_bnb_kernel(
     __syncthreads();
     const uint64_t changed = (uint64_t)chgw[0] | ((uint64_t)chgw[1] << 32);
     const uint64_t skm = ~changed;  // bit j: slice k0 + j is skippable (bit 0 unused: first)
+    nxt = *nxt_s;
     // the next item's change-map bytes: loads issued now, consumed at its start
     // (thread: one (block, word) entry of the window, every jstep-th slice;
     // only when the entries fit kChgPf registers, else that item loads them
     // itself)
     cpf_item = -1;
-    if (item + (int)gridDim.x < n_items) {
-      const int it2 = item + (int)gridDim.x;
+    if (nxt < n_items) {
+      const int it2 = nxt;
       int m2, r2, t2;
       decode(it2, m2, r2, t2);
       const EvalMap &M2 = maps[m2];
@@ -434,7 +443,7 @@ __global__ void __launch_bounds__(NT, MINB) resolve_inflate_bnb_kernel(
     }
     if (tid < 2) {  // the next item's pair (its last readers finished an item ago)
       unsigned *nx = reinterpret_cast<unsigned *>(skipmask) + 2 * (ip ^ 1);
-      const int item2 = item + (int)gridDim.x;
+      const int item2 = nxt;
       bool nchg = false;
       if (item2 < n_items) {
         int m2, r2, t2;
@@ -465,9 +474,9 @@ __global__ void __launch_bounds__(NT, MINB) resolve_inflate_bnb_kernel(
           while (kn < k1 && ((skm >> (kn - k0)) & 1ull)) ++kn;
           if (kn < k1) {
             issue(m, t, kn);
-          } else if (item + (int)gridDim.x < n_items) {
+          } else if (nxt < n_items) {
             int m2, r2, t2;
-            decode(item + gridDim.x, m2, r2, t2);
+            decode(nxt, m2, r2, t2);
             issue(m2, t2, r2 * maps[m2].run);
           }
         }

@@ -871,16 +871,21 @@ int launch_split(pct_ctx *ctx, const float *ground, const float *ceiling, int S,
       struct {
         EvalMap m;
         int off[2];
+        int work;  // dynamic item counter (PCT_BNB_DYNAMIC=0: static round robin)
       } desc;
       static_assert(offsetof(decltype(desc), m) == 0, "descriptor layout");
       desc.m = hm;
       desc.off[0] = 0;
       desc.off[1] = (int)nitems;
+      desc.work = 0;
+      const char *dyv = getenv("PCT_BNB_DYNAMIC");
+      const bool dyn = !(dyv && dyv[0] == '0');
       char *dptr = static_cast<char *>(ctx->scratch) + boff;
       PCT_CUDA(ctx, upload_async(ctx, dptr, &desc, sizeof(desc)));
       const EvalMap *dm = reinterpret_cast<const EvalMap *>(dptr);
       const int *doff = reinterpret_cast<const int *>(dptr + offsetof(decltype(desc), off));
-      kb<<<grid, BNT, bsmem, ctx->stream>>>(dm, doff, 1);
+      int *dwork = reinterpret_cast<int *>(dptr + offsetof(decltype(desc), work));
+      kb<<<grid, BNT, bsmem, ctx->stream>>>(dm, doff, 1, dyn ? dwork : nullptr);
       return check_launch(ctx, "resolve_inflate_bnb_kernel");
      }
     }
@@ -1074,7 +1079,7 @@ int launch_evaluate_batch(pct_ctx *ctx, int n_maps, float *const *ground, float 
   const int64_t slots = (int64_t)std::max(1, per_sm) * ctx->num_sms;
   // layouts, offsets, run length
   std::vector<EvalMap> hm(n_maps);
-  std::vector<int> off(n_maps + 1, 0);
+  std::vector<int> off(n_maps + 2, 0);  // item offsets, then the dynamic item counter (0)
   int64_t enc_floats = 0, bit_words = 0, total_tiles = 0, walk_blocks = 1;
   uint64_t tag = 1469598103934665603ull;
   for (int m = 0; m < n_maps; ++m) {
@@ -1122,7 +1127,7 @@ int launch_evaluate_batch(pct_ctx *ctx, int n_maps, float *const *ground, float 
   // walk change maps
   const size_t bbytes = (((size_t)bit_words * 4 + 255) / 256) * 256;
   const size_t dbytes = (((size_t)n_maps * sizeof(EvalMap) + 255) / 256) * 256;
-  const size_t obytes = (((size_t)(n_maps + 1) * 4 + 255) / 256) * 256;
+  const size_t obytes = (((size_t)(n_maps + 2) * 4 + 255) / 256) * 256;  // + work counter
   int64_t cm_total = 0;
   for (auto &e : hm) cm_total += (int64_t)e.S * ((e.rows + 7) / 8) * e.wpr;
   if (int rc = ensure_scratch(ctx, bbytes + dbytes + obytes + (size_t)cm_total + 64)) return rc;
@@ -1171,11 +1176,13 @@ int launch_evaluate_batch(pct_ctx *ctx, int n_maps, float *const *ground, float 
   EvalMap *dm = reinterpret_cast<EvalMap *>(sb + bbytes);
   int *doff = reinterpret_cast<int *>(sb + bbytes + dbytes);
   PCT_CUDA(ctx, upload_async(ctx, dm, hm.data(), sizeof(EvalMap) * n_maps));
-  PCT_CUDA(ctx, upload_async(ctx, doff, off.data(), sizeof(int) * (n_maps + 1)));
+  PCT_CUDA(ctx, upload_async(ctx, doff, off.data(), sizeof(int) * (n_maps + 2)));
   terrain_walk_batch_kernel<1><<<dim3((unsigned)walk_blocks, n_maps), kWalkNT, 0, ctx->stream>>>(dm);
   if (int rc = check_launch(ctx, "terrain_walk_batch_kernel")) return rc;
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(off[n_maps], slots));
-  kb<<<grid, BNT, bsmem, ctx->stream>>>(dm, doff, n_maps);
+  const char *dyv = getenv("PCT_BNB_DYNAMIC");
+  const bool dyn = !(dyv && dyv[0] == '0');
+  kb<<<grid, BNT, bsmem, ctx->stream>>>(dm, doff, n_maps, dyn ? doff + n_maps + 1 : nullptr);
   return check_launch(ctx, "resolve_inflate_bnb_kernel");
 }
 

@@ -190,17 +190,41 @@ struct SimpMasks {
 };
 
 __global__ void __launch_bounds__(kWinNT) window_skip_kernel(SimpArgs A, SimpMasks M,
-                                                             unsigned long long *__restrict__ table) {
+                                                             unsigned long long *__restrict__ table,
+                                                             unsigned long long *__restrict__ work) {
   __shared__ float seg_e[kWin][kWinNT];
   __shared__ float seg_c[kWin][kWinNT];
   __shared__ unsigned char seg_s[kWin][kWinNT];
   extern __shared__ unsigned long long btab[];  // [S]
   for (int k = threadIdx.x; k < A.S; k += kWinNT) btab[k] = 0ull;
   __syncthreads();
-  const int64_t stride = (int64_t)gridDim.x * kWinNT;
-  const int64_t span = (A.cells + kWinNT - 1) / kWinNT * kWinNT;  // whole warps iterate together
   const int tid = threadIdx.x;
-  for (int64_t cell = (int64_t)blockIdx.x * kWinNT + tid; cell < span; cell += stride) {
+  // Warps take groups of 32 cells (whole warps iterate together), kClaim
+  // groups per claim: claimed from a global counter when `work` is given
+  // (dynamic: warps in event-dense regions take fewer), else round robin.
+  constexpr int kClaim = 4;
+  const int lane = tid & 31;
+  const int64_t groups = (A.cells + 31) / 32;
+  const int64_t wid = (int64_t)blockIdx.x * (kWinNT / 32) + (tid >> 5);
+  const int64_t nwarps = (int64_t)gridDim.x * (kWinNT / 32);
+  int64_t g = 0, gend = 0, nclaim = 0;
+  for (;;) {
+    if (g == gend) {
+      long long c;
+      if (work) {
+        unsigned long long v = 0ull;
+        if (lane == 0) v = atomicAdd(work, 1ull);
+        c = (long long)__shfl_sync(0xFFFFFFFFu, v, 0);
+      } else {
+        c = wid + nclaim * nwarps;
+        ++nclaim;
+      }
+      g = c * kClaim;
+      if (g >= groups) break;
+      gend = g + kClaim < groups ? g + kClaim : groups;
+    }
+    const int64_t cell = g * 32 + lane;
+    ++g;
     const bool live = cell < A.cells;
     const int64_t c0 = live ? cell : 0;
     unsigned long long vm = 1ull;
@@ -551,7 +575,16 @@ int run_simplify(pct_ctx *ctx, const float *ground, const float *cost, int S, in
                   (cols + ctx->simp_tw - 1) / ctx->simp_tw};
       PCT_CUDA(ctx, cudaFuncSetAttribute(window_skip_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tab_smem));
-      window_skip_kernel<<<grid, kWinNT, tab_smem, ctx->stream>>>(A, M, table);
+      // dynamic claims (PCT_WIN_DYNAMIC=0: round robin); the counter sits in
+      // the small buffer's slack after `count`
+      const char *wd = getenv("PCT_WIN_DYNAMIC");
+      unsigned long long *wctr = nullptr;
+      if (!(wd && wd[0] == '0')) {
+        wctr = reinterpret_cast<unsigned long long *>(
+            (reinterpret_cast<uintptr_t>(dcount + 1) + 7) & ~(uintptr_t)7);
+        PCT_CUDA(ctx, cudaMemsetAsync(wctr, 0, 8, ctx->stream));
+      }
+      window_skip_kernel<<<grid, kWinNT, tab_smem, ctx->stream>>>(A, M, table, wctr);
     } else {
       window_kernel<<<grid, kWinNT, tab_smem, ctx->stream>>>(A, table);
     }
