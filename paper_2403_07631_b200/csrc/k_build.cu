@@ -799,15 +799,40 @@ inline size_t hist_bulk_smem(int nb, int S, bool scatter) {
   return tot <= 226 * 1024 ? tot : 0;
 }
 
-// per bucket: column prefix over the CTAs (in place) and the bucket total
-__global__ void __launch_bounds__(256) hist_colscan_kernel(unsigned *__restrict__ cnt, int G,
-                                                           int nb, unsigned *__restrict__ tot) {
-  const int b = blockIdx.x * 256 + threadIdx.x;
+// per bucket: column prefix over the CTAs (in place) and the bucket total.
+// A block takes 64 buckets x 4 segments of the G CTA rows: each thread sums
+// its segment (independent loads), the segment sums are exchanged in shared
+// memory, then each thread rewrites its segment from its base (the rows are
+// still in L2).
+constexpr int kColSeg = 4, kColB = 64;
+__global__ void __launch_bounds__(kColSeg * kColB) hist_colscan_kernel(unsigned *__restrict__ cnt,
+                                                                      int G, int nb,
+                                                                      unsigned *__restrict__ tot) {
+  __shared__ unsigned part[kColSeg][kColB];
+  const int x = threadIdx.x % kColB, sg = threadIdx.x / kColB;
+  const int b = blockIdx.x * kColB + x;
+  const int c0 = G * sg / kColSeg, c1 = G * (sg + 1) / kColSeg;
+  constexpr int U = 8;  // independent loads in flight
+  unsigned sum = 0;
+  if (b < nb) {
+    int c = c0;
+    for (; c + U <= c1; c += U) {
+      unsigned v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = cnt[(int64_t)(c + u) * nb + b];
+#pragma unroll
+      for (int u = 0; u < U; ++u) sum += v[u];
+    }
+    for (; c < c1; ++c) sum += cnt[(int64_t)c * nb + b];
+  }
+  part[sg][x] = sum;
+  __syncthreads();
   if (b >= nb) return;
   unsigned run = 0;
-  constexpr int U = 8;  // independent loads in flight
-  int c = 0;
-  for (; c + U <= G; c += U) {
+  for (int k = 0; k < sg; ++k) run += part[k][x];
+  if (sg == kColSeg - 1) tot[b] = run + sum;
+  int c = c0;
+  for (; c + U <= c1; c += U) {
     unsigned v[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) v[u] = cnt[(int64_t)(c + u) * nb + b];
@@ -817,15 +842,14 @@ __global__ void __launch_bounds__(256) hist_colscan_kernel(unsigned *__restrict_
       run += v[u];
     }
   }
-  for (; c < G; ++c) {
+  for (; c < c1; ++c) {
     const unsigned v = cnt[(int64_t)c * nb + b];
     cnt[(int64_t)c * nb + b] = run;
     run += v;
   }
-  tot[b] = run;
 }
 
-// TMA bulk tensor store of a [S][16][32] float box from shared memory
+// TMA bulk tensor store of a [S][kHBH][kHBW] float box from shared memory
 __device__ __forceinline__ void bulk_store_box(const CUtensorMap *map, const void *src, int x, int y) {
   const uint32_t sa = (uint32_t)__cvta_generic_to_shared(src);
   asm volatile(
@@ -1752,7 +1776,8 @@ int launch_build(pct_ctx *ctx, const void *xyz, int64_t n, int dtype, const pct_
           static_cast<const double *>(xyz), n, a, hbx, nbi, cnt, nullptr, nullptr, outs);
     }
     if (int rc = check_launch(ctx, "hist_count_kernel")) return rc;
-    hist_colscan_kernel<<<(unsigned)((hnb + 255) / 256), 256, 0, ctx->stream>>>(cnt, G, nbi, tot);
+    hist_colscan_kernel<<<(unsigned)((hnb + kColB - 1) / kColB), kColSeg * kColB, 0, ctx->stream>>>(
+        cnt, G, nbi, tot);
     if (int rc = check_launch(ctx, "hist_colscan_kernel")) return rc;
     const unsigned nsb = (unsigned)((hnb + 1023) / 1024);
     tile_sums_kernel<<<nsb, 1024, 0, ctx->stream>>>(tot, nbi, bsum, 1);
