@@ -122,7 +122,7 @@ def test_inflation_kernels_vs_oracle_random_costs(r_g, d_inf, d_sm, patch):
 @pytest.mark.parametrize("mode", ["tiled", "hist"])
 def test_tiled_build_matches_reference_golden(golden, monkeypatch, name, mode):
     """The partitioned builds (PCT_BUILD=tiled: bucket by 8x32-cell tile with
-    hash-merged passes; PCT_BUILD=hist: per-CTA histograms of 16x32-cell
+    hash-merged passes; PCT_BUILD=hist: per-CTA histograms of 8x64-cell
     buckets; both reduce max / min in shared memory) give the reference's
     layers too."""
     monkeypatch.setenv("PCT_BUILD", mode)
@@ -714,3 +714,59 @@ def test_sparse_walk_and_bnb_runs(golden, monkeypatch, name, sparse, run):
     assert [s.plane_height for s in got.slices] == [case["heights"][k] for k in case["keep"]]
     assert [digest(s.cost.values) for s in got.slices] == \
         [case["cost_slice_sha256"][k] for k in case["keep"]]
+
+
+@pytest.mark.parametrize("env", [{"PCT_BUILD_REDUCE": "2"}, {"PCT_BUILD_REDUCE": "3"},
+                                 {"PCT_BUILD_TMA": "1"}, {"PCT_HIST_BULK": "0"}])
+@pytest.mark.parametrize("name", ["synth_cfg0", "ref_random_multilayer_s9", "synth_cfg2_n2000000"])
+def test_hist_build_variants_match_reference_golden(golden, monkeypatch, name, env):
+    """The opt-in histogram-build variants (split-scan reduce, one-pass
+    1024-thread reduce, TMA box stores of the layers, direct point loads
+    instead of bulk-copy staging) give the reference's layers and the same
+    slice-change masks as the default reduce."""
+    monkeypatch.setenv("PCT_BUILD", "hist")
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    case = golden["cases"][name]
+    xyz = case_input(name, case)
+    tom = pct.build_tomogram(pct.PointCloud(xyz), case["d_s"], case["r_g"])
+    g, c = tom.ground_stack(), tom.ceiling_stack()
+    for k in range(g.shape[0]):
+        assert digest(g[k]) == case["ground_slice_sha256"][k], f"ground slice {k}"
+        assert digest(c[k]) == case["ceiling_slice_sha256"][k], f"ceiling slice {k}"
+    owner = tom.slices[0].ground.device[0].owner
+    ptr = owner.ctx.lib.pct_tomo_masks(owner.handle)
+    if ptr and g.shape[0] <= 64:  # the variants emit the same slice-change masks
+        cells = g.shape[1] * g.shape[2]
+        host = np.empty(2 * cells, np.uint64)
+        owner.ctx.check(owner.ctx.lib.pct_memcpy_d2h(owner.ctx.h, host.ctypes.data, ptr,
+                                                     host.nbytes))
+        assert np.array_equal(host[:cells].reshape(g.shape[1:]), _np_masks(g))
+        assert np.array_equal(host[cells:].reshape(g.shape[1:]), _np_masks(c))
+
+
+@pytest.mark.parametrize("env", [{"PCT_BNB_DYNAMIC": "0"}, {"PCT_WIN_DYNAMIC": "0"},
+                                 {"PCT_BNB_DYNAMIC": "0", "PCT_WIN_DYNAMIC": "0"}])
+def test_dynamic_work_claims_match_static(golden, monkeypatch, env):
+    """The inflation kernel's dynamic item claims and the simplify window's
+    dynamic cell-group claims (the defaults) against their static round-robin
+    schedules: the same costs (the reference's) and the same surviving slices,
+    on a map large enough for the segment window (> 1M cells)."""
+    from paper_2403_07631_b200.batch import stream_maps
+    name = "synth_cfg2_n2000000"
+    case = golden["cases"][name]
+    xyz = case_input(name, case)
+
+    def run():
+        ev = pct.evaluate_tomogram(
+            pct.build_tomogram(pct.PointCloud(xyz), case["d_s"], case["r_g"]), pct.TravParams())
+        got = next(stream_maps([xyz], case["d_s"], case["r_g"], pct.TravParams(), workers=1))
+        return ([digest(s.cost.values) for s in ev.slices], [s.plane_height for s in got.slices],
+                [digest(s.cost.values) for s in got.slices])
+
+    dyn = run()
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    assert run() == dyn
+    assert dyn[0] == case["cost_slice_sha256"]
+    assert dyn[1] == [case["heights"][k] for k in case["keep"]]
