@@ -942,8 +942,23 @@ __global__ void __launch_bounds__(kHB2) hist_reduce_kernel(
     const uint32_t lo = (uint32_t)rec - (uint32_t)kHB2;
     atomicMin(hk + (lo < lim ? lo : dummy), (uint32_t)(rec >> 32));
   };
-  constexpr int U = 8;  // records in flight per thread
-  unsigned r = r0 + t;
+  // The first kKeep records of each thread stay in registers from the ground
+  // pass to the ceiling pass (all their loads issued at once; buckets of up
+  // to kKeep x 512 records are read once); the rest, if any, stream from
+  // memory in both passes.  An absent record is all ones: both atomics then
+  // land on the dummy word.
+  constexpr int kKeep = 16;
+  unsigned long long keep[kKeep];
+#pragma unroll
+  for (int u = 0; u < kKeep; ++u) {
+    const unsigned idx = r0 + t + u * kHB2;
+    keep[u] = idx < r1 ? __ldg(recs + idx) : ~0ull;
+  }
+#pragma unroll
+  for (int u = 0; u < kKeep; ++u) gmax(keep[u]);
+  constexpr int U = 8;  // records in flight per thread (beyond the kept ones)
+  const unsigned rs = r0 + t + kKeep * kHB2;
+  unsigned r = rs;
   for (; r + (U - 1) * kHB2 < r1; r += U * kHB2) {
     unsigned long long v[U];
 #pragma unroll
@@ -995,7 +1010,9 @@ __global__ void __launch_bounds__(kHB2) hist_reduce_kernel(
   for (int q = t; q < S * (kHB2 / 4); q += kHB2)
     hk4[q] = make_uint4(kKeyEmptyMin, kKeyEmptyMin, kKeyEmptyMin, kKeyEmptyMin);
   __syncthreads();
-  r = r0 + t;
+#pragma unroll
+  for (int u = 0; u < kKeep; ++u) cmin(keep[u]);
+  r = rs;
   for (; r + (U - 1) * kHB2 < r1; r += U * kHB2) {
     unsigned long long v[U];
 #pragma unroll
