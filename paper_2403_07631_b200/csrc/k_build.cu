@@ -981,13 +981,23 @@ __global__ void __launch_bounds__(kHB2) hist_reduce_kernel(
     // cells outside the map store into one scratch word instead (no predicate)
     float *out = live ? ground + cell : sink;
     const int64_t step_b = live ? out_stride * 4 : 0;
+    // (plain stores: each slot this thread read is reset to the ceiling
+    // pass's empty key on the way, in place of an init pass and a barrier)
     auto step = [&](int k, uint32_t bit, uint32_t &m) {
       scan_update<true>(col[k * kHB2], run, o, m, bit);
-      if (TMA) hk[k * kHB2 + t] = o;
-      else store_step(out, o, step_b);
+      if (TMA) {
+        hk[k * kHB2 + t] = o;
+      } else {
+        hk[k * kHB2 + t] = kKeyEmptyMin;
+        store_step(out, o, step_b);
+      }
     };
-    if (TMA) hk[t] = o;
-    else store_step(out, o, step_b);
+    if (TMA) {
+      hk[t] = o;
+    } else {
+      hk[t] = kKeyEmptyMin;
+      store_step(out, o, step_b);
+    }
     const int k1 = S < 32 ? S : 32;
     uint32_t bit = 2u;
 #pragma unroll 4
@@ -1007,9 +1017,11 @@ __global__ void __launch_bounds__(kHB2) hist_reduce_kernel(
   }
   __syncthreads();
   // ceiling: min key per (bin, cell), bins 1 .. S stored at bin - 1
-  for (int q = t; q < S * (kHB2 / 4); q += kHB2)
-    hk4[q] = make_uint4(kKeyEmptyMin, kKeyEmptyMin, kKeyEmptyMin, kKeyEmptyMin);
-  __syncthreads();
+  if (TMA) {  // (the plain-store scan has reset the keys already)
+    for (int q = t; q < S * (kHB2 / 4); q += kHB2)
+      hk4[q] = make_uint4(kKeyEmptyMin, kKeyEmptyMin, kKeyEmptyMin, kKeyEmptyMin);
+    __syncthreads();
+  }
 #pragma unroll
   for (int u = 0; u < kKeep; ++u) cmin(keep[u]);
   r = rs;
