@@ -730,7 +730,8 @@ def run_e2e(args, cfg, maps, ctx, local, rank, world, R, Cc):
         d2h = 0
         for s in tom.slices:  # the caller reads every surviving layer
             d2h += s.ground.values.nbytes + s.ceiling.values.nbytes + s.cost.values.nbytes
-        return d2h, tom
+        # bytes that crossed PCIe (mostly-empty layers travel compacted)
+        return getattr(tom, "xfer_bytes", None) or d2h, tom
 
     times = []
     tom = None
@@ -761,9 +762,15 @@ def run_e2e(args, cfg, maps, ctx, local, rank, world, R, Cc):
             if banded else None,
             "replica": None}[args.mode] or (
         "PointCloud(pinned f32) -> build_tomogram -> evaluate_tomogram -> simplify_tomogram "
-        "-> every surviving layer in host memory (the reference's drop-in chain)")
+        "-> every surviving layer in host memory (the reference's drop-in chain; mostly-empty "
+        "layers cross PCIe as a bitmap + their values and are expanded by host threads)")
+    layer_bytes = 0
+    if tom is not None and hasattr(tom, "slices"):
+        layer_bytes = sum(s.ground.values.nbytes + s.ceiling.values.nbytes + s.cost.values.nbytes
+                          for s in tom.slices)
     out = {"value": total / (e2e_s * 1e6), "unit": "Mpts/s", "ms_per_step": 1e3 * e2e_s,
            "path": path, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+           "host_layer_bytes_per_step": layer_bytes,
            "timing": "wall clock per step (host copies included), max over ranks"}
     if args.mode == "replica" and world == 1 and len(maps[0]) <= 20_000_000:
         out["streamed"] = streamed_e2e(args, cfg, pins[0], local, total)

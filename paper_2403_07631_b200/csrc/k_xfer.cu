@@ -1,0 +1,316 @@
+// k_xfer.cu — NaN-compacted read-back of layer slices (the layer transfer
+// behind Layer.values / Tomogram.materialize, SURVEY.md §8 b).
+//
+// A ceiling slice is mostly the empty-cell NaN (tomogram.py:203-204: numpy's
+// 0x7FC00000) -- 75 % of the cells of cfg3's kept ceilings -- and the drop-in
+// chain is bound by PCIe (every surviving layer goes to host memory).  A
+// compacted slice crosses PCIe as a bitmap (bit = cell is not the empty NaN)
+// plus its non-empty values in cell order; host threads expand it into the
+// caller's array while the dense slices are still in flight.  Lossless: a
+// cell is "empty" only when its bits are exactly 0x7FC00000, every other
+// value (any other NaN payload too) travels as it is.
+//
+// Device layout of one call over n slices (slice m = src + k_m * stride):
+//   bitmaps [n][W] u32 (W = ceil(cells / 32)),
+//   packed  values of slice m at packed + off[m] (off chosen by the caller),
+//   chunk   [n][nchunk] i64: absolute packed index of each chunk's first
+//           value (a chunk = kXChunk cells = 8 warps x 32 words).
+// A warp takes 32 words (1024 cells): lane l loads cell 32 i + l of word i
+// (coalesced), __ballot_sync forms word i, the lane's rank is a popcount.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <thread>
+#include <vector>
+#if defined(__SSE2__)
+#include <emmintrin.h>  // non-temporal stores of the host expansion
+#endif
+
+#include "pct_internal.h"
+
+namespace pct {
+namespace {
+
+constexpr int kXThreads = 256;
+constexpr int kXWarpCells = 1024;                            // 32 words of 32 cells
+constexpr int kXChunk = kXWarpCells * (kXThreads / 32);      // 8192 cells
+constexpr int kXMaxSlices = 4096;
+
+struct XferSlices {
+  const float *src;
+  int64_t stride;  // floats between slices
+  int64_t cells;
+  int n;
+  int32_t k[kXMaxSlices];
+};
+
+__device__ __forceinline__ bool not_empty(float v) { return f32_bits(v) != kNaNBits; }
+
+// blockIdx.x = chunk, blockIdx.y = slice: non-empty cells of the chunk
+__global__ void __launch_bounds__(kXThreads) xfer_count_kernel(const XferSlices *__restrict__ a,
+                                                               unsigned *__restrict__ cnt,
+                                                               int nchunk) {
+  __shared__ unsigned part[kXThreads / 32];
+  const int m = blockIdx.y, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t cells = a->cells;
+  const float *s = a->src + (int64_t)a->k[m] * a->stride;
+  const int64_t base = (int64_t)blockIdx.x * kXChunk + (int64_t)warp * kXWarpCells;
+  unsigned c = 0;
+#pragma unroll 8
+  for (int i = 0; i < 32; ++i) {
+    const int64_t cell = base + i * 32 + lane;
+    const bool v = cell < cells && not_empty(__ldg(s + cell));
+    c += __popc(__ballot_sync(0xFFFFFFFFu, v));
+  }
+  if (lane == 0) part[warp] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned t = 0;
+    for (int w = 0; w < kXThreads / 32; ++w) t += part[w];
+    cnt[(int64_t)m * nchunk + blockIdx.x] = t;
+  }
+}
+
+// one block per slice: exclusive prefix of its chunk counts (absolute, from
+// the slice's packed offset) and the slice total
+__global__ void __launch_bounds__(1024) xfer_scan_kernel(const unsigned *__restrict__ cnt,
+                                                         int nchunk,
+                                                         const int64_t *__restrict__ off,
+                                                         int64_t *__restrict__ chunk_off,
+                                                         int64_t *__restrict__ totals) {
+  __shared__ int64_t wsum[32];
+  __shared__ int64_t carry;
+  const int m = blockIdx.x, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  if (t == 0) carry = off ? off[m] : 0;
+  __syncthreads();
+  for (int c0 = 0; c0 < nchunk; c0 += 1024) {
+    const int c = c0 + t;
+    int64_t v = c < nchunk ? cnt[(int64_t)m * nchunk + c] : 0;
+    int64_t x = v;  // inclusive warp scan
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int64_t y = __shfl_up_sync(0xFFFFFFFFu, x, d);
+      if (lane >= d) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      int64_t w = wsum[lane];
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int64_t y = __shfl_up_sync(0xFFFFFFFFu, w, d);
+        if (lane >= d) w += y;
+      }
+      wsum[lane] = w;  // inclusive over warps
+    }
+    __syncthreads();
+    const int64_t before = carry + (warp ? wsum[warp - 1] : 0) + x - v;
+    if (c < nchunk) chunk_off[(int64_t)m * nchunk + c] = before;
+    __syncthreads();
+    if (t == 0) carry += wsum[31];
+    __syncthreads();
+  }
+  if (t == 0 && totals) totals[m] = carry - (off ? off[m] : 0);
+}
+
+// blockIdx.x = chunk, blockIdx.y = slice: bitmap words and packed values
+__global__ void __launch_bounds__(kXThreads) xfer_pack_kernel(const XferSlices *__restrict__ a,
+                                                              const int64_t *__restrict__ chunk_off,
+                                                              int nchunk,
+                                                              uint32_t *__restrict__ bitmaps,
+                                                              float *__restrict__ packed) {
+  __shared__ unsigned part[kXThreads / 32];
+  const int m = blockIdx.y, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t cells = a->cells, W = (cells + 31) / 32;
+  const float *s = a->src + (int64_t)a->k[m] * a->stride;
+  const int64_t base = (int64_t)blockIdx.x * kXChunk + (int64_t)warp * kXWarpCells;
+  // the warp's count first (its offset inside the chunk), then the writes
+  float v[32];
+  unsigned bal[32];
+  unsigned c = 0;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const int64_t cell = base + i * 32 + lane;
+    v[i] = cell < cells ? __ldg(s + cell) : bits_f32(kNaNBits);
+    bal[i] = __ballot_sync(0xFFFFFFFFu, not_empty(v[i]));
+    c += __popc(bal[i]);
+  }
+  if (lane == 0) part[warp] = c;
+  __syncthreads();
+  int64_t pos = chunk_off[(int64_t)m * nchunk + blockIdx.x];
+  for (int w = 0; w < warp; ++w) pos += part[w];
+  const unsigned lt = (1u << lane) - 1u;
+  const int64_t w0 = base / 32;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    if (bal[i] >> lane & 1u) packed[pos + __popc(bal[i] & lt)] = v[i];
+    pos += __popc(bal[i]);
+    if (lane == i && w0 + i < W) bitmaps[(int64_t)m * W + w0 + i] = bal[i];
+  }
+}
+
+int setup(pct_ctx *ctx, const float *src, int64_t stride, const int32_t *idx, int32_t n,
+          int64_t cells, XferSlices **dargs, int *nchunk) {
+  if (!ctx) return PCT_E_INVALID;
+  if (cudaSetDevice(ctx->device) != cudaSuccess) return PCT_E_CUDA;
+  if (!src || !idx || n <= 0 || n > kXMaxSlices || cells <= 0 || stride < cells)
+    return fail(ctx, PCT_E_INVALID, "bad arguments to the compacted read-back");
+  const int64_t nc = (cells + kXChunk - 1) / kXChunk;
+  if (nc > (int64_t)1 << 30) return fail(ctx, PCT_E_INVALID, "slice too large");
+  *nchunk = (int)nc;
+  // scratch: args | chunk counts [n][nchunk] u32 | chunk offsets [n][nchunk] i64 | totals [n]
+  const size_t abytes = (sizeof(XferSlices) + 255) & ~(size_t)255;
+  const size_t cbytes = ((size_t)n * nc * 4 + 255) & ~(size_t)255;
+  const size_t obytes = ((size_t)n * nc * 8 + 255) & ~(size_t)255;
+  if (int rc = ensure_scratch(ctx, abytes + cbytes + obytes + (size_t)n * 8 + 256)) return rc;
+  XferSlices h;
+  h.src = src;
+  h.stride = stride;
+  h.cells = cells;
+  h.n = n;
+  std::memcpy(h.k, idx, sizeof(int32_t) * (size_t)n);
+  *dargs = static_cast<XferSlices *>(ctx->scratch);
+  const size_t used = offsetof(XferSlices, k) + sizeof(int32_t) * (size_t)n;
+  PCT_CUDA(ctx, upload_async(ctx, *dargs, &h, used));
+  return PCT_OK;
+}
+
+}  // namespace
+}  // namespace pct
+
+using namespace pct;
+
+extern "C" int pct_xfer_count(pct_ctx *ctx, const float *src, int64_t slice_stride,
+                              const int32_t *slice_idx_host, int32_t n, int64_t cells,
+                              int64_t *totals_host) {
+  XferSlices *da = nullptr;
+  int nchunk = 0;
+  if (int rc = setup(ctx, src, slice_stride, slice_idx_host, n, cells, &da, &nchunk)) return rc;
+  if (!totals_host) return fail(ctx, PCT_E_INVALID, "pct_xfer_count: totals_host is NULL");
+  char *b = static_cast<char *>(ctx->scratch);
+  const size_t abytes = (sizeof(XferSlices) + 255) & ~(size_t)255;
+  const size_t cbytes = ((size_t)n * nchunk * 4 + 255) & ~(size_t)255;
+  const size_t obytes = ((size_t)n * nchunk * 8 + 255) & ~(size_t)255;
+  unsigned *cnt = reinterpret_cast<unsigned *>(b + abytes);
+  int64_t *coff = reinterpret_cast<int64_t *>(b + abytes + cbytes);
+  int64_t *tot = reinterpret_cast<int64_t *>(b + abytes + cbytes + obytes);
+  xfer_count_kernel<<<dim3((unsigned)nchunk, (unsigned)n), kXThreads, 0, ctx->stream>>>(da, cnt,
+                                                                                     nchunk);
+  if (int rc = check_launch(ctx, "xfer_count_kernel")) return rc;
+  xfer_scan_kernel<<<(unsigned)n, 1024, 0, ctx->stream>>>(cnt, nchunk, nullptr, coff, tot);
+  if (int rc = check_launch(ctx, "xfer_scan_kernel")) return rc;
+  PCT_CUDA(ctx, cudaMemcpyAsync(totals_host, tot, (size_t)n * 8, cudaMemcpyDeviceToHost,
+                                ctx->stream));
+  PCT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return PCT_OK;
+}
+
+extern "C" int pct_xfer_pack(pct_ctx *ctx, const float *src, int64_t slice_stride,
+                             const int32_t *slice_idx_host, int32_t n, int64_t cells,
+                             const int64_t *packed_off_host, uint32_t *bitmaps, float *packed,
+                             int64_t *chunk_off) {
+  XferSlices *da = nullptr;
+  int nchunk = 0;
+  if (int rc = setup(ctx, src, slice_stride, slice_idx_host, n, cells, &da, &nchunk)) return rc;
+  if (!packed_off_host || !bitmaps || !packed || !chunk_off)
+    return fail(ctx, PCT_E_INVALID, "pct_xfer_pack: NULL buffer");
+  char *b = static_cast<char *>(ctx->scratch);
+  const size_t abytes = (sizeof(XferSlices) + 255) & ~(size_t)255;
+  const size_t cbytes = ((size_t)n * nchunk * 4 + 255) & ~(size_t)255;
+  const size_t obytes = ((size_t)n * nchunk * 8 + 255) & ~(size_t)255;
+  unsigned *cnt = reinterpret_cast<unsigned *>(b + abytes);
+  int64_t *doff = reinterpret_cast<int64_t *>(b + abytes + cbytes + obytes);
+  PCT_CUDA(ctx, upload_async(ctx, doff, packed_off_host, (size_t)n * 8));
+  xfer_count_kernel<<<dim3((unsigned)nchunk, (unsigned)n), kXThreads, 0, ctx->stream>>>(da, cnt,
+                                                                                     nchunk);
+  if (int rc = check_launch(ctx, "xfer_count_kernel")) return rc;
+  xfer_scan_kernel<<<(unsigned)n, 1024, 0, ctx->stream>>>(cnt, nchunk, doff, chunk_off, nullptr);
+  if (int rc = check_launch(ctx, "xfer_scan_kernel")) return rc;
+  xfer_pack_kernel<<<dim3((unsigned)nchunk, (unsigned)n), kXThreads, 0, ctx->stream>>>(
+      da, chunk_off, nchunk, bitmaps, packed);
+  return check_launch(ctx, "xfer_pack_kernel");
+}
+
+extern "C" int64_t pct_xfer_chunk_cells(void) { return kXChunk; }
+
+extern "C" int pct_xfer_fence(pct_ctx *ctx) {
+  if (!ctx) return PCT_E_INVALID;
+  if (cudaSetDevice(ctx->device) != cudaSuccess) return PCT_E_CUDA;
+  if (!ctx->xfer_ev)
+    PCT_CUDA(ctx, cudaEventCreateWithFlags(&ctx->xfer_ev, cudaEventDisableTiming));
+  PCT_CUDA(ctx, cudaEventRecord(ctx->xfer_ev, ctx->stream));
+  return PCT_OK;
+}
+
+extern "C" int pct_xfer_wait(pct_ctx *ctx) {
+  if (!ctx) return PCT_E_INVALID;
+  if (!ctx->xfer_ev) return PCT_OK;
+  PCT_CUDA(ctx, cudaEventSynchronize(ctx->xfer_ev));
+  return PCT_OK;
+}
+
+// Host side: expand n compacted slices into their output arrays.  The work
+// is split into (slice, chunk) items over nthreads threads; item (m, c)
+// rebuilds cells [c * chunk, (c+1) * chunk) of slice m from its bitmap words
+// and the packed values from chunk_off[m][c] on.
+extern "C" int pct_xfer_expand(const uint32_t *bitmaps, const float *packed,
+                               const int64_t *chunk_off, int32_t n, int64_t cells,
+                               float *const *outs, int32_t nthreads) {
+  if (n <= 0) return PCT_OK;
+  if (!bitmaps || !packed || !chunk_off || !outs || cells <= 0) return PCT_E_INVALID;
+  const int64_t W = (cells + 31) / 32;
+  const int64_t nchunk = (cells + kXChunk - 1) / kXChunk;
+  const int64_t items = (int64_t)n * nchunk;
+  uint32_t nan_bits = kNaNBits;
+  float nanv;
+  std::memcpy(&nanv, &nan_bits, 4);
+  // One 32-cell word at a time into a 128-byte staging line, written with
+  // non-temporal stores where the output line is 16-byte aligned (no
+  // read-for-ownership of the output: the host's memory bandwidth is shared
+  // with the dense copies landing at the same time).
+  auto work = [&](int64_t i0, int64_t i1) {
+    alignas(16) float line[32];
+    for (int64_t it = i0; it < i1; ++it) {
+      const int64_t m = it / nchunk, c = it - m * nchunk;
+      const uint32_t *bm = bitmaps + m * W;
+      const float *p = packed + chunk_off[m * nchunk + c];
+      float *o = outs[m];
+      const int64_t w0 = c * (kXChunk / 32), w1 = std::min(W, w0 + kXChunk / 32);
+      for (int64_t w = w0; w < w1; ++w) {
+        const uint32_t bits = bm[w];
+        float *ow = o + w * 32;
+        const int nc = (int)std::min<int64_t>(32, cells - w * 32);
+        if (bits == 0xFFFFFFFFu && nc == 32) {
+          std::memcpy(line, p, 128);
+          p += 32;
+        } else {
+          for (int j = 0; j < 32; ++j) line[j] = (bits >> j & 1u) ? *p++ : nanv;
+        }
+#if defined(__SSE2__)
+        if (nc == 32 && (reinterpret_cast<uintptr_t>(ow) & 15) == 0) {
+          const __m128i *src = reinterpret_cast<const __m128i *>(line);
+          __m128i *dst = reinterpret_cast<__m128i *>(ow);
+          for (int q = 0; q < 8; ++q) _mm_stream_si128(dst + q, _mm_load_si128(src + q));
+          continue;
+        }
+#endif
+        std::memcpy(ow, line, sizeof(float) * (size_t)nc);
+      }
+    }
+#if defined(__SSE2__)
+    _mm_sfence();
+#endif
+  };
+  int nt = std::max(1, std::min<int>(nthreads, (int)std::min<int64_t>(items, 256)));
+  if (nt == 1) {
+    work(0, items);
+    return PCT_OK;
+  }
+  std::vector<std::thread> th;
+  th.reserve((size_t)nt);
+  for (int t = 0; t < nt; ++t)
+    th.emplace_back(work, items * t / nt, items * (t + 1) / nt);
+  for (auto &x : th) x.join();
+  return PCT_OK;
+}

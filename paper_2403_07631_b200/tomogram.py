@@ -12,6 +12,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 import weakref
 from dataclasses import dataclass
 
@@ -21,6 +22,11 @@ from . import _lib
 from .cloud import PointCloud
 
 GRID_SIDE_LIMIT = 16384
+
+# compacted read-back (Tomogram.materialize): slices with at least this share
+# of empty-NaN cells, in stacks of at least XFER_MIN_CELLS cells per slice
+XFER_MIN_EMPTY = 0.5
+XFER_MIN_CELLS = 1 << 20
 
 
 class GridSizeError(ValueError):
@@ -85,6 +91,60 @@ class DeviceStack:
                 self.ctx.check(self.ctx.lib.pct_sync(self.ctx.h), "sync")
         for n, k in enumerate(todo):
             self._host[k] = block[n]
+
+    def count_nonempty(self, ks) -> np.ndarray:
+        """Non-empty cells (not the empty-cell NaN 0x7FC00000) of slices ks."""
+        idx = np.ascontiguousarray(ks, dtype=np.int32)
+        tot = np.empty(len(idx), np.int64)
+        with self.ctx.lock:
+            self.ctx.check(self.ctx.lib.pct_xfer_count(
+                self.ctx.h, self.ptr, self.rows * self.cols, idx.ctypes.data, len(idx),
+                self.rows * self.cols, tot.ctypes.data), "xfer_count")
+        return tot
+
+    def compact_start(self, ks, totals):
+        """Queue the compacted read-back of slices ks (pct_xfer_pack, then
+        bitmaps, packed values and chunk offsets to pinned host memory);
+        finish with :meth:`compact_finish` once the copies have landed."""
+        cells = self.rows * self.cols
+        n = len(ks)
+        idx = np.ascontiguousarray(ks, dtype=np.int32)
+        off = np.zeros(n, np.int64)
+        off[1:] = np.cumsum(np.asarray(totals, np.int64))[:-1]
+        n_packed = int(np.sum(totals))
+        chunk = int(self.ctx.lib.pct_xfer_chunk_cells())
+        nchunk = (cells + chunk - 1) // chunk
+        words = (cells + 31) // 32
+        pool = _lib.pinned_pool(self.ctx)
+        block = pool.array((n, self.rows, self.cols), np.float32)
+        h_bm = pool.array((n, words), np.uint32)
+        h_pk = pool.array((max(n_packed, 1),), np.float32)
+        h_co = pool.array((n, nchunk), np.int64)
+        d_bm = _lib.DeviceBuffer(self.ctx, h_bm.nbytes)
+        d_pk = _lib.DeviceBuffer(self.ctx, h_pk.nbytes)
+        d_co = _lib.DeviceBuffer(self.ctx, h_co.nbytes)
+        lib, h = self.ctx.lib, self.ctx.h
+        with self.ctx.lock:
+            self.ctx.check(lib.pct_xfer_pack(h, self.ptr, cells, idx.ctypes.data, n, cells,
+                                             off.ctypes.data, d_bm.ptr, d_pk.ptr, d_co.ptr),
+                           "xfer_pack")
+            for dst, src in ((h_bm, d_bm), (h_co, d_co)):
+                self.ctx.check(lib.pct_memcpy_d2h_async(h, dst.ctypes.data, src.ptr, dst.nbytes),
+                               "d2h")
+            if n_packed:
+                self.ctx.check(lib.pct_memcpy_d2h_async(h, h_pk.ctypes.data, d_pk.ptr,
+                                                        n_packed * 4), "d2h")
+        return (list(ks), block, h_bm, h_pk, h_co, (d_bm, d_pk, d_co))
+
+    def compact_finish(self, pending, threads: int) -> None:
+        """Expand the landed compacted slices into their host arrays."""
+        ks, block, h_bm, h_pk, h_co, _dev = pending
+        outs = (C.c_void_p * len(ks))(*[block[i].ctypes.data for i in range(len(ks))])
+        self.ctx.check(self.ctx.lib.pct_xfer_expand(
+            h_bm.ctypes.data, h_pk.ctypes.data, h_co.ctypes.data, len(ks),
+            self.rows * self.cols, outs, int(threads)), "xfer_expand")
+        for i, k in enumerate(ks):
+            self._host[k] = block[i]
 
     def host_all(self) -> np.ndarray:
         out = np.empty((self.n_slices, self.rows, self.cols), np.float32)
@@ -236,16 +296,54 @@ class Tomogram:
 
     def materialize(self) -> "Tomogram":
         """Copy every device-resident layer to host memory with one
-        synchronisation per stack (``Layer.values`` then costs nothing)."""
+        synchronisation per stack (``Layer.values`` then costs nothing).
+
+        Slices that are mostly the empty-cell NaN (at least XFER_MIN_EMPTY of
+        their cells; cfg3's kept ceilings: 75 %) cross PCIe compacted (a
+        bitmap + the non-empty values, k_xfer.cu) ahead of the dense ones,
+        and host threads expand them while the dense copies are in flight
+        (PCT_XFER_COMPACT=0: every slice dense)."""
         groups = {}
         for s in self.slices:
             for l in (s.ground, s.ceiling, s.cost):
                 if isinstance(l, Layer) and l._values is None and l._stack is not None:
                     groups.setdefault(id(l._stack), (l._stack, []))[1].append(l._k)
         ctxs = {}
-        for stack, ks in groups.values():
-            stack.prefetch(ks, sync=False)
+        for stack, _ in groups.values():
             ctxs[id(stack.ctx)] = stack.ctx
+        compact = os.environ.get("PCT_XFER_COMPACT", "1") != "0"
+        plan = []  # (stack, dense slices, compacted slices, their non-empty counts)
+        for stack, ks in groups.values():
+            ks = sorted(k for k in set(ks) if k not in stack._host)
+            if not ks:
+                continue
+            cells = stack.rows * stack.cols
+            ck, ct = [], []
+            if compact and cells >= XFER_MIN_CELLS:
+                for k, t in zip(ks, stack.count_nonempty(ks)):
+                    if t <= (1.0 - XFER_MIN_EMPTY) * cells:
+                        ck.append(k)
+                        ct.append(int(t))
+            plan.append((stack, [k for k in ks if k not in set(ck)], ck, ct))
+        pending = [(stack, stack.compact_start(ck, ct)) for stack, _, ck, ct in plan if ck]
+        dense = [(stack, ks) for stack, ks, _, _ in plan]
+        # bytes that cross PCIe in this call (dense slices + compacted payloads)
+        self.xfer_bytes = sum(len(ks) * st.plane_bytes for st, ks in dense) + \
+            sum(p[2].nbytes + 4 * int(sum(ct)) + p[4].nbytes
+                for (st, p), (_, _, _, ct) in zip(pending, [q for q in plan if q[2]]))
+        if pending:
+            for ctx in ctxs.values():
+                with ctx.lock:
+                    ctx.check(ctx.lib.pct_xfer_fence(ctx.h), "xfer_fence")
+        for stack, ks in dense:
+            if ks:
+                stack.prefetch(ks, sync=False)
+        if pending:
+            for ctx in ctxs.values():
+                ctx.check(ctx.lib.pct_xfer_wait(ctx.h), "xfer_wait")
+            threads = max(1, (os.cpu_count() or 1))
+            for stack, p in pending:
+                stack.compact_finish(p, threads)
         for ctx in ctxs.values():
             with ctx.lock:
                 ctx.check(ctx.lib.pct_sync(ctx.h), "sync")
