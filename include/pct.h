@@ -180,7 +180,10 @@ int pct_copy_slices(pct_ctx *ctx, float *dst, int64_t dst_slice_stride, const fl
    numpy's NaN the reference writes for empty cells, tomogram.py:203-204) and
    those cells' values in cell order; pct_xfer_expand rebuilds it on the
    host.  Lossless for every bit pattern.  Slices m < n are
-   src + slice_idx_host[m] * slice_stride (floats), n <= 4096.
+   src + slice_idx_host[m] * slice_stride (floats), n <= 4096.  delta = 1:
+   a delta chain -- slice m > 0 is compared with (and rebuilt from) slice
+   m - 1 of the list instead of the empty NaN (consecutive kept slices share
+   most cells).
    pct_xfer_count: the number of non-empty cells of each slice (synchronous).
    pct_xfer_pack: device buffers bitmaps [n][ceil(cells/32)] u32, packed
    (slice m's values at packed_off_host[m]), chunk_off [n][ceil(cells /
@@ -190,16 +193,18 @@ int pct_copy_slices(pct_ctx *ctx, float *dst, int64_t dst_slice_stride, const fl
    while dense copies queued after them are still in flight).
    pct_xfer_expand: host function (no context), nthreads host threads. */
 int pct_xfer_count(pct_ctx *ctx, const float *src, int64_t slice_stride,
-                   const int32_t *slice_idx_host, int32_t n, int64_t cells, int64_t *totals_host);
+                   const int32_t *slice_idx_host, int32_t n, int64_t cells, int32_t delta,
+                   int64_t *totals_host);
 int pct_xfer_pack(pct_ctx *ctx, const float *src, int64_t slice_stride,
-                  const int32_t *slice_idx_host, int32_t n, int64_t cells,
+                  const int32_t *slice_idx_host, int32_t n, int64_t cells, int32_t delta,
                   const int64_t *packed_off_host, uint32_t *bitmaps, float *packed,
                   int64_t *chunk_off);
 int64_t pct_xfer_chunk_cells(void);
 int pct_xfer_fence(pct_ctx *ctx);
 int pct_xfer_wait(pct_ctx *ctx);
 int pct_xfer_expand(const uint32_t *bitmaps, const float *packed, const int64_t *chunk_off,
-                    int32_t n, int64_t cells, float *const *outs, int32_t nthreads);
+                    int32_t n, int64_t cells, int32_t delta, float *const *outs,
+                    int32_t nthreads);
 /* Sweep primitives for a distributed simplify (simplify.py:18-73): the any()
    table of the first pass (bit j of table[k]: below = k-1-j, j < 16; bit 32:
    no lower neighbour; upper neighbour k+1) and any() flags of explicit

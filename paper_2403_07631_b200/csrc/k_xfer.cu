@@ -42,10 +42,18 @@ struct XferSlices {
   int64_t stride;  // floats between slices
   int64_t cells;
   int n;
+  int delta;  // slice m > 0 against slice m - 1 of the list (else every slice against NaN)
   int32_t k[kXMaxSlices];
 };
 
-__device__ __forceinline__ bool not_empty(float v) { return f32_bits(v) != kNaNBits; }
+// the value slice m's cell is compared with: the empty NaN, or in a delta
+// chain the previous listed slice's value
+__device__ __forceinline__ const float *base_slice(const XferSlices *a, int m) {
+  return (a->delta && m > 0) ? a->src + (int64_t)a->k[m - 1] * a->stride : nullptr;
+}
+__device__ __forceinline__ bool differs(float v, const float *b, int64_t cell) {
+  return f32_bits(v) != (b ? f32_bits(__ldg(b + cell)) : kNaNBits);
+}
 
 // blockIdx.x = chunk, blockIdx.y = slice: non-empty cells of the chunk
 __global__ void __launch_bounds__(kXThreads) xfer_count_kernel(const XferSlices *__restrict__ a,
@@ -54,13 +62,13 @@ __global__ void __launch_bounds__(kXThreads) xfer_count_kernel(const XferSlices 
   __shared__ unsigned part[kXThreads / 32];
   const int m = blockIdx.y, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t cells = a->cells;
-  const float *s = a->src + (int64_t)a->k[m] * a->stride;
+  const float *s = a->src + (int64_t)a->k[m] * a->stride, *bs = base_slice(a, m);
   const int64_t base = (int64_t)blockIdx.x * kXChunk + (int64_t)warp * kXWarpCells;
   unsigned c = 0;
 #pragma unroll 8
   for (int i = 0; i < 32; ++i) {
     const int64_t cell = base + i * 32 + lane;
-    const bool v = cell < cells && not_empty(__ldg(s + cell));
+    const bool v = cell < cells && differs(__ldg(s + cell), bs, cell);
     c += __popc(__ballot_sync(0xFFFFFFFFu, v));
   }
   if (lane == 0) part[warp] = c;
@@ -123,7 +131,7 @@ __global__ void __launch_bounds__(kXThreads) xfer_pack_kernel(const XferSlices *
   __shared__ unsigned part[kXThreads / 32];
   const int m = blockIdx.y, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t cells = a->cells, W = (cells + 31) / 32;
-  const float *s = a->src + (int64_t)a->k[m] * a->stride;
+  const float *s = a->src + (int64_t)a->k[m] * a->stride, *bs = base_slice(a, m);
   const int64_t base = (int64_t)blockIdx.x * kXChunk + (int64_t)warp * kXWarpCells;
   // the warp's count first (its offset inside the chunk), then the writes
   float v[32];
@@ -132,8 +140,9 @@ __global__ void __launch_bounds__(kXThreads) xfer_pack_kernel(const XferSlices *
 #pragma unroll
   for (int i = 0; i < 32; ++i) {
     const int64_t cell = base + i * 32 + lane;
-    v[i] = cell < cells ? __ldg(s + cell) : bits_f32(kNaNBits);
-    bal[i] = __ballot_sync(0xFFFFFFFFu, not_empty(v[i]));
+    const bool in = cell < cells;
+    v[i] = in ? __ldg(s + cell) : bits_f32(kNaNBits);
+    bal[i] = __ballot_sync(0xFFFFFFFFu, in && differs(v[i], bs, cell));
     c += __popc(bal[i]);
   }
   if (lane == 0) part[warp] = c;
@@ -151,7 +160,7 @@ __global__ void __launch_bounds__(kXThreads) xfer_pack_kernel(const XferSlices *
 }
 
 int setup(pct_ctx *ctx, const float *src, int64_t stride, const int32_t *idx, int32_t n,
-          int64_t cells, XferSlices **dargs, int *nchunk) {
+          int64_t cells, int delta, XferSlices **dargs, int *nchunk) {
   if (!ctx) return PCT_E_INVALID;
   if (cudaSetDevice(ctx->device) != cudaSuccess) return PCT_E_CUDA;
   if (!src || !idx || n <= 0 || n > kXMaxSlices || cells <= 0 || stride < cells)
@@ -169,6 +178,7 @@ int setup(pct_ctx *ctx, const float *src, int64_t stride, const int32_t *idx, in
   h.stride = stride;
   h.cells = cells;
   h.n = n;
+  h.delta = delta ? 1 : 0;
   std::memcpy(h.k, idx, sizeof(int32_t) * (size_t)n);
   *dargs = static_cast<XferSlices *>(ctx->scratch);
   const size_t used = offsetof(XferSlices, k) + sizeof(int32_t) * (size_t)n;
@@ -183,10 +193,11 @@ using namespace pct;
 
 extern "C" int pct_xfer_count(pct_ctx *ctx, const float *src, int64_t slice_stride,
                               const int32_t *slice_idx_host, int32_t n, int64_t cells,
-                              int64_t *totals_host) {
+                              int32_t delta, int64_t *totals_host) {
   XferSlices *da = nullptr;
   int nchunk = 0;
-  if (int rc = setup(ctx, src, slice_stride, slice_idx_host, n, cells, &da, &nchunk)) return rc;
+  if (int rc = setup(ctx, src, slice_stride, slice_idx_host, n, cells, delta, &da, &nchunk))
+    return rc;
   if (!totals_host) return fail(ctx, PCT_E_INVALID, "pct_xfer_count: totals_host is NULL");
   char *b = static_cast<char *>(ctx->scratch);
   const size_t abytes = (sizeof(XferSlices) + 255) & ~(size_t)255;
@@ -208,11 +219,12 @@ extern "C" int pct_xfer_count(pct_ctx *ctx, const float *src, int64_t slice_stri
 
 extern "C" int pct_xfer_pack(pct_ctx *ctx, const float *src, int64_t slice_stride,
                              const int32_t *slice_idx_host, int32_t n, int64_t cells,
-                             const int64_t *packed_off_host, uint32_t *bitmaps, float *packed,
-                             int64_t *chunk_off) {
+                             int32_t delta, const int64_t *packed_off_host, uint32_t *bitmaps,
+                             float *packed, int64_t *chunk_off) {
   XferSlices *da = nullptr;
   int nchunk = 0;
-  if (int rc = setup(ctx, src, slice_stride, slice_idx_host, n, cells, &da, &nchunk)) return rc;
+  if (int rc = setup(ctx, src, slice_stride, slice_idx_host, n, cells, delta, &da, &nchunk))
+    return rc;
   if (!packed_off_host || !bitmaps || !packed || !chunk_off)
     return fail(ctx, PCT_E_INVALID, "pct_xfer_pack: NULL buffer");
   char *b = static_cast<char *>(ctx->scratch);
@@ -250,53 +262,92 @@ extern "C" int pct_xfer_wait(pct_ctx *ctx) {
   return PCT_OK;
 }
 
-// Host side: expand n compacted slices into their output arrays.  The work
-// is split into (slice, chunk) items over nthreads threads; item (m, c)
+// Host side: expand n compacted slices into their output arrays.  NaN mode
+// (delta = 0): the work is split into (slice, chunk) items; item (m, c)
 // rebuilds cells [c * chunk, (c+1) * chunk) of slice m from its bitmap words
-// and the packed values from chunk_off[m][c] on.
+// and the packed values from chunk_off[m][c] on (a clear bit = the empty
+// NaN).  Delta chains (delta = 1): the items are chunks; a thread rebuilds
+// the chunk of slice 0 against NaN in a cache-resident buffer, then patches
+// it slice after slice (a clear bit = the previous slice's value), streaming
+// each state out.  Output lines leave with non-temporal stores where they
+// are 16-byte aligned (no read-for-ownership: the host's memory bandwidth is
+// shared with the dense copies landing at the same time).
+namespace {
+inline void put_line(float *dst, const float *line, int nc) {
+#if defined(__SSE2__)
+  if (nc == 32 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+    const __m128i *s = reinterpret_cast<const __m128i *>(line);
+    __m128i *d = reinterpret_cast<__m128i *>(dst);
+    for (int q = 0; q < 8; ++q) _mm_stream_si128(d + q, _mm_load_si128(s + q));
+    return;
+  }
+#endif
+  std::memcpy(dst, line, sizeof(float) * (size_t)nc);
+}
+}  // namespace
+
 extern "C" int pct_xfer_expand(const uint32_t *bitmaps, const float *packed,
                                const int64_t *chunk_off, int32_t n, int64_t cells,
-                               float *const *outs, int32_t nthreads) {
+                               int32_t delta, float *const *outs, int32_t nthreads) {
   if (n <= 0) return PCT_OK;
   if (!bitmaps || !packed || !chunk_off || !outs || cells <= 0) return PCT_E_INVALID;
   const int64_t W = (cells + 31) / 32;
   const int64_t nchunk = (cells + kXChunk - 1) / kXChunk;
-  const int64_t items = (int64_t)n * nchunk;
+  const int64_t items = delta ? nchunk : (int64_t)n * nchunk;
   uint32_t nan_bits = kNaNBits;
   float nanv;
   std::memcpy(&nanv, &nan_bits, 4);
-  // One 32-cell word at a time into a 128-byte staging line, written with
-  // non-temporal stores where the output line is 16-byte aligned (no
-  // read-for-ownership of the output: the host's memory bandwidth is shared
-  // with the dense copies landing at the same time).
-  auto work = [&](int64_t i0, int64_t i1) {
+  auto nan_item = [&](int64_t it) {
     alignas(16) float line[32];
-    for (int64_t it = i0; it < i1; ++it) {
-      const int64_t m = it / nchunk, c = it - m * nchunk;
+    const int64_t m = it / nchunk, c = it - m * nchunk;
+    const uint32_t *bm = bitmaps + m * W;
+    const float *p = packed + chunk_off[m * nchunk + c];
+    float *o = outs[m];
+    const int64_t w0 = c * (kXChunk / 32), w1 = std::min(W, w0 + kXChunk / 32);
+    for (int64_t w = w0; w < w1; ++w) {
+      const uint32_t bits = bm[w];
+      const int nc = (int)std::min<int64_t>(32, cells - w * 32);
+      if (bits == 0xFFFFFFFFu && nc == 32) {
+        std::memcpy(line, p, 128);
+        p += 32;
+      } else {
+        for (int j = 0; j < 32; ++j) line[j] = (bits >> j & 1u) ? *p++ : nanv;
+      }
+      put_line(o + w * 32, line, nc);
+    }
+  };
+  auto delta_item = [&](int64_t c, float *buf) {
+    const int64_t w0 = c * (kXChunk / 32), w1 = std::min(W, w0 + kXChunk / 32);
+    for (int32_t m = 0; m < n; ++m) {
       const uint32_t *bm = bitmaps + m * W;
       const float *p = packed + chunk_off[m * nchunk + c];
       float *o = outs[m];
-      const int64_t w0 = c * (kXChunk / 32), w1 = std::min(W, w0 + kXChunk / 32);
       for (int64_t w = w0; w < w1; ++w) {
-        const uint32_t bits = bm[w];
-        float *ow = o + w * 32;
+        uint32_t bits = bm[w];
+        float *line = buf + (w - w0) * 32;
         const int nc = (int)std::min<int64_t>(32, cells - w * 32);
-        if (bits == 0xFFFFFFFFu && nc == 32) {
-          std::memcpy(line, p, 128);
-          p += 32;
-        } else {
+        if (m == 0) {
           for (int j = 0; j < 32; ++j) line[j] = (bits >> j & 1u) ? *p++ : nanv;
+        } else {
+          while (bits) {
+            const int j = __builtin_ctz(bits);
+            bits &= bits - 1u;
+            line[j] = *p++;
+          }
         }
-#if defined(__SSE2__)
-        if (nc == 32 && (reinterpret_cast<uintptr_t>(ow) & 15) == 0) {
-          const __m128i *src = reinterpret_cast<const __m128i *>(line);
-          __m128i *dst = reinterpret_cast<__m128i *>(ow);
-          for (int q = 0; q < 8; ++q) _mm_stream_si128(dst + q, _mm_load_si128(src + q));
-          continue;
-        }
-#endif
-        std::memcpy(ow, line, sizeof(float) * (size_t)nc);
+        put_line(o + w * 32, line, nc);
       }
+    }
+  };
+  auto work = [&](int64_t i0, int64_t i1) {
+    std::vector<float> dbuf;
+    if (delta) dbuf.resize(kXChunk + 4);
+    float *buf = dbuf.empty() ? nullptr
+                              : reinterpret_cast<float *>(
+                                    (reinterpret_cast<uintptr_t>(dbuf.data()) + 15) & ~(uintptr_t)15);
+    for (int64_t it = i0; it < i1; ++it) {
+      if (delta) delta_item(it, buf);
+      else nan_item(it);
     }
 #if defined(__SSE2__)
     _mm_sfence();

@@ -10,10 +10,9 @@ from golden_util import case_input, digest
 pytestmark = pytest.mark.gpu
 
 
-def _roundtrip(stack, ks):
-    from paper_2403_07631_b200.tomogram import DeviceStack  # noqa: F401
-    tot = stack.count_nonempty(ks)
-    p = stack.compact_start(list(ks), [int(t) for t in tot])
+def _roundtrip(stack, ks, delta=False):
+    tot = stack.count_nonempty(ks, delta=delta)
+    p = stack.compact_start(list(ks), [int(t) for t in tot], delta)
     with stack.ctx.lock:
         stack.ctx.check(stack.ctx.lib.pct_sync(stack.ctx.h), "sync")
     stack.compact_finish(p, 8)
@@ -51,6 +50,33 @@ def test_compacted_slices_are_bit_exact(rows, cols):
     _, got = _roundtrip(stack2, [4, 2])
     assert np.array_equal(got[0].view(np.uint32), u[4])
     assert np.array_equal(got[1].view(np.uint32), u[2])
+    # delta chains: each slice against the previous listed one
+    for ks in ([0, 1, 2, 3, 4, 5], [5, 3, 1], [2]):
+        st = DeviceStack(ctx, buf.ptr, n, rows, cols, buf)
+        tot, got = _roundtrip(st, ks, delta=True)
+        prev = np.full(u[0].shape, 0x7FC00000, np.uint32)
+        for k, t, g in zip(ks, tot, got):
+            assert int(t) == int((u[k] != prev).sum())
+            assert np.array_equal(g.view(np.uint32), u[k]), f"delta slice {k}"
+            prev = u[k]
+
+
+@pytest.mark.parametrize("mode", ["1", "nan", "0"])
+def test_materialize_modes_match_dense(golden, monkeypatch, mode):
+    """The default read-back (delta chains where consecutive slices share
+    most cells), NaN compaction only, and dense copies: the reference's
+    layers, every slice."""
+    name = "synth_cfg2_n2000000"
+    case = golden["cases"][name]
+    xyz = case_input(name, case)
+    monkeypatch.setenv("PCT_XFER_COMPACT", mode)
+    tom = pct.evaluate_tomogram(pct.build_tomogram(pct.PointCloud(xyz), case["d_s"], case["r_g"]),
+                                pct.TravParams())
+    tom.materialize()  # every slice (not only the kept ones): long chains
+    for k, s in enumerate(tom.slices):
+        assert digest(s.ground.values) == case["ground_slice_sha256"][k]
+        assert digest(s.ceiling.values) == case["ceiling_slice_sha256"][k]
+        assert digest(s.cost.values) == case["cost_slice_sha256"][k]
 
 
 def test_materialize_compacted_matches_dense(golden, monkeypatch):
