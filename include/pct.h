@@ -184,13 +184,15 @@ int pct_copy_slices(pct_ctx *ctx, float *dst, int64_t dst_slice_stride, const fl
    a delta chain -- slice m > 0 is compared with (and rebuilt from) slice
    m - 1 of the list instead of the empty NaN (consecutive kept slices share
    most cells).
-   pct_xfer_count: the number of non-empty cells of each slice (synchronous).
+   pct_xfer_count: the number of non-empty cells of each slice (synchronous);
+   pct_xfer_count_async: the same, stream-ordered (totals_host, page-locked,
+   is valid once the stream synchronises).
    pct_xfer_pack: device buffers bitmaps [n][ceil(cells/32)] u32, packed
    (slice m's values at packed_off_host[m]), chunk_off [n][ceil(cells /
    pct_xfer_chunk_cells())] i64 (absolute packed index of each chunk's first
-   value); stream-ordered.  pct_xfer_fence / pct_xfer_wait: record an event
-   on the stream / wait for it on the host (e.g. the packed copies landed
-   while dense copies queued after them are still in flight).
+   value); stream-ordered.  pct_xfer_fence / pct_xfer_wait: record event
+   slot (0..7) on the stream / wait for it on the host (e.g. one stack's
+   packed copies landed while later copies are still in flight).
    pct_xfer_expand: host function (no context), nthreads host threads. */
 int pct_xfer_count(pct_ctx *ctx, const float *src, int64_t slice_stride,
                    const int32_t *slice_idx_host, int32_t n, int64_t cells, int32_t delta,
@@ -199,9 +201,12 @@ int pct_xfer_pack(pct_ctx *ctx, const float *src, int64_t slice_stride,
                   const int32_t *slice_idx_host, int32_t n, int64_t cells, int32_t delta,
                   const int64_t *packed_off_host, uint32_t *bitmaps, float *packed,
                   int64_t *chunk_off);
+int pct_xfer_count_async(pct_ctx *ctx, const float *src, int64_t slice_stride,
+                         const int32_t *slice_idx_host, int32_t n, int64_t cells, int32_t delta,
+                         int64_t *totals_host);
 int64_t pct_xfer_chunk_cells(void);
-int pct_xfer_fence(pct_ctx *ctx);
-int pct_xfer_wait(pct_ctx *ctx);
+int pct_xfer_fence(pct_ctx *ctx, int32_t slot);
+int pct_xfer_wait(pct_ctx *ctx, int32_t slot);
 int pct_xfer_expand(const uint32_t *bitmaps, const float *packed, const int64_t *chunk_off,
                     int32_t n, int64_t cells, int32_t delta, float *const *outs,
                     int32_t nthreads);

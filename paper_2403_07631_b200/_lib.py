@@ -87,8 +87,9 @@ _SIGS = {
     "pct_xfer_count": ([_vp, _vp, _i64, _vp, _i32, _i64, _i32, _vp], C.c_int),
     "pct_xfer_pack": ([_vp, _vp, _i64, _vp, _i32, _i64, _i32, _vp, _vp, _vp, _vp], C.c_int),
     "pct_xfer_chunk_cells": ([], _i64),
-    "pct_xfer_fence": ([_vp], C.c_int),
-    "pct_xfer_wait": ([_vp], C.c_int),
+    "pct_xfer_count_async": ([_vp, _vp, _i64, _vp, _i32, _i64, _i32, _vp], C.c_int),
+    "pct_xfer_fence": ([_vp, _i32], C.c_int),
+    "pct_xfer_wait": ([_vp, _i32], C.c_int),
     "pct_xfer_expand": ([_vp, _vp, _vp, _i32, _i64, _i32, _vp, _i32], C.c_int),
     "pct_simplify_window": ([_vp, _vp, _vp, _i32, _i64, _i64, _d, _d, _vp], C.c_int),
     "pct_simplify_triples": ([_vp, _vp, _vp, _i32, _i64, _i64, _d, _d, _vp, _i32, _vp], C.c_int),

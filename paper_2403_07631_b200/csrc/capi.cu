@@ -264,7 +264,8 @@ int pct_ctx_destroy(pct_ctx *ctx) {
   if (ctx->keys) cudaFree(ctx->keys);
   if (ctx->spec_ev) cudaEventDestroy(ctx->spec_ev);
   if (ctx->switch_ev) cudaEventDestroy(ctx->switch_ev);
-  if (ctx->xfer_ev) cudaEventDestroy(ctx->xfer_ev);
+  for (auto &e : ctx->xfer_ev)
+    if (e) cudaEventDestroy(e);
   for (auto e : ctx->ev)
     if (e) cudaEventDestroy(e);
   if (ctx->hsmall) cudaFreeHost(ctx->hsmall);

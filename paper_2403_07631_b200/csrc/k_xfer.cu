@@ -191,9 +191,9 @@ int setup(pct_ctx *ctx, const float *src, int64_t stride, const int32_t *idx, in
 
 using namespace pct;
 
-extern "C" int pct_xfer_count(pct_ctx *ctx, const float *src, int64_t slice_stride,
-                              const int32_t *slice_idx_host, int32_t n, int64_t cells,
-                              int32_t delta, int64_t *totals_host) {
+static int xfer_count(pct_ctx *ctx, const float *src, int64_t slice_stride,
+                      const int32_t *slice_idx_host, int32_t n, int64_t cells, int32_t delta,
+                      int64_t *totals_host, bool sync) {
   XferSlices *da = nullptr;
   int nchunk = 0;
   if (int rc = setup(ctx, src, slice_stride, slice_idx_host, n, cells, delta, &da, &nchunk))
@@ -213,8 +213,20 @@ extern "C" int pct_xfer_count(pct_ctx *ctx, const float *src, int64_t slice_stri
   if (int rc = check_launch(ctx, "xfer_scan_kernel")) return rc;
   PCT_CUDA(ctx, cudaMemcpyAsync(totals_host, tot, (size_t)n * 8, cudaMemcpyDeviceToHost,
                                 ctx->stream));
-  PCT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  if (sync) PCT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   return PCT_OK;
+}
+
+extern "C" int pct_xfer_count(pct_ctx *ctx, const float *src, int64_t slice_stride,
+                              const int32_t *slice_idx_host, int32_t n, int64_t cells,
+                              int32_t delta, int64_t *totals_host) {
+  return xfer_count(ctx, src, slice_stride, slice_idx_host, n, cells, delta, totals_host, true);
+}
+
+extern "C" int pct_xfer_count_async(pct_ctx *ctx, const float *src, int64_t slice_stride,
+                                    const int32_t *slice_idx_host, int32_t n, int64_t cells,
+                                    int32_t delta, int64_t *totals_host) {
+  return xfer_count(ctx, src, slice_stride, slice_idx_host, n, cells, delta, totals_host, false);
 }
 
 extern "C" int pct_xfer_pack(pct_ctx *ctx, const float *src, int64_t slice_stride,
@@ -246,19 +258,21 @@ extern "C" int pct_xfer_pack(pct_ctx *ctx, const float *src, int64_t slice_strid
 
 extern "C" int64_t pct_xfer_chunk_cells(void) { return kXChunk; }
 
-extern "C" int pct_xfer_fence(pct_ctx *ctx) {
+extern "C" int pct_xfer_fence(pct_ctx *ctx, int32_t slot) {
   if (!ctx) return PCT_E_INVALID;
+  if (slot < 0 || slot >= kXferEvents) return fail(ctx, PCT_E_INVALID, "pct_xfer_fence: bad slot");
   if (cudaSetDevice(ctx->device) != cudaSuccess) return PCT_E_CUDA;
-  if (!ctx->xfer_ev)
-    PCT_CUDA(ctx, cudaEventCreateWithFlags(&ctx->xfer_ev, cudaEventDisableTiming));
-  PCT_CUDA(ctx, cudaEventRecord(ctx->xfer_ev, ctx->stream));
+  if (!ctx->xfer_ev[slot])
+    PCT_CUDA(ctx, cudaEventCreateWithFlags(&ctx->xfer_ev[slot], cudaEventDisableTiming));
+  PCT_CUDA(ctx, cudaEventRecord(ctx->xfer_ev[slot], ctx->stream));
   return PCT_OK;
 }
 
-extern "C" int pct_xfer_wait(pct_ctx *ctx) {
+extern "C" int pct_xfer_wait(pct_ctx *ctx, int32_t slot) {
   if (!ctx) return PCT_E_INVALID;
-  if (!ctx->xfer_ev) return PCT_OK;
-  PCT_CUDA(ctx, cudaEventSynchronize(ctx->xfer_ev));
+  if (slot < 0 || slot >= kXferEvents) return fail(ctx, PCT_E_INVALID, "pct_xfer_wait: bad slot");
+  if (!ctx->xfer_ev[slot]) return PCT_OK;
+  PCT_CUDA(ctx, cudaEventSynchronize(ctx->xfer_ev[slot]));
   return PCT_OK;
 }
 

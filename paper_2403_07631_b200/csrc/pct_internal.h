@@ -11,6 +11,8 @@
 #include "../../include/pct.h"
 #include "cellmath.cuh"
 
+constexpr int kXferEvents = 8;  // event slots of pct_xfer_fence / pct_xfer_wait
+
 struct pct_ctx {
   int device = 0;
   int num_sms = 148;
@@ -45,7 +47,7 @@ struct pct_ctx {
   bool keys_clean = false;
   cudaEvent_t spec_ev = nullptr;  // bounds read back ahead of the speculative scatter
   cudaEvent_t switch_ev = nullptr;  // pct_set_stream: old stream -> new stream join
-  cudaEvent_t xfer_ev = nullptr;    // pct_xfer_fence / pct_xfer_wait
+  cudaEvent_t xfer_ev[8] = {};      // pct_xfer_fence / pct_xfer_wait slots
   // per-cell slice-change masks ([2][cells] uint64: ground, ceiling; bit k =
   // the layer differs from slice k-1, bit 0 set; S <= 64): build_masks, when
   // set, is where the whole-grid build writes them; eval_masks, when set,

@@ -107,6 +107,15 @@ class DeviceStack:
                 self.rows * self.cols, int(bool(delta)), tot.ctypes.data), "xfer_count")
         return tot
 
+    def count_nonempty_async(self, ks, delta: bool, out: np.ndarray) -> None:
+        """count_nonempty into ``out`` (page-locked int64), stream-ordered:
+        valid once the context's stream has synchronised."""
+        idx = np.ascontiguousarray(ks, dtype=np.int32)
+        with self.ctx.lock:
+            self.ctx.check(self.ctx.lib.pct_xfer_count_async(
+                self.ctx.h, self.ptr, self.rows * self.cols, idx.ctypes.data, len(idx),
+                self.rows * self.cols, int(bool(delta)), out.ctypes.data), "xfer_count")
+
     def compact_start(self, ks, totals, delta: bool = False):
         """Queue the compacted read-back of slices ks (pct_xfer_pack, then
         bitmaps, packed values and chunk offsets to pinned host memory);
@@ -324,45 +333,64 @@ class Tomogram:
             ctxs[id(stack.ctx)] = stack.ctx
         mode = os.environ.get("PCT_XFER_COMPACT", "1")
         compact = mode != "0"
-        # plan: (stack, dense slices, compacted slices, their counts, delta chain)
-        plan = []
+        todo = []
         for stack, ks in groups.values():
             ks = sorted(k for k in set(ks) if k not in stack._host)
-            if not ks:
-                continue
-            cells = stack.rows * stack.cols
-            ck, ct, delta = [], [], False
-            if compact and cells >= XFER_MIN_CELLS:
-                if mode != "nan" and len(ks) > 1:
-                    dt = stack.count_nonempty(ks, delta=True)
-                    if int(dt[1:].sum()) <= XFER_DELTA_MAX * (len(ks) - 1) * cells:
-                        ck, ct, delta = list(ks), [int(t) for t in dt], True
-                if not ck:
-                    for k, t in zip(ks, stack.count_nonempty(ks)):
-                        if t <= (1.0 - XFER_MIN_EMPTY) * cells:
-                            ck.append(k)
-                            ct.append(int(t))
-            plan.append((stack, [k for k in ks if k not in set(ck)], ck, ct, delta))
-        pending = [(stack, stack.compact_start(ck, ct, delta))
-                   for stack, _, ck, ct, delta in plan if ck]
-        dense = [(stack, ks) for stack, ks, _, _, _ in plan]
+            if ks:
+                todo.append((stack, ks))
+
+        def counts(cands, delta):
+            # every candidate stack's counts queued, one synchronisation
+            outs = []
+            for stack, ks in cands:
+                out = _lib.pinned_pool(stack.ctx).array((len(ks),), np.int64)
+                stack.count_nonempty_async(ks, delta, out)
+                outs.append(out)
+            for ctx in {id(st.ctx): st.ctx for st, _ in cands}.values():
+                with ctx.lock:
+                    ctx.check(ctx.lib.pct_sync(ctx.h), "sync")
+            return outs
+
+        # plan: stack -> (compacted slices, their counts, delta chain)
+        chosen = {}
+        big = [(st, ks) for st, ks in todo if compact and st.rows * st.cols >= XFER_MIN_CELLS]
+        if mode != "nan":
+            cands = [(st, ks) for st, ks in big if len(ks) > 1]
+            for (st, ks), dt in zip(cands, counts(cands, True)):
+                if int(dt[1:].sum()) <= XFER_DELTA_MAX * (len(ks) - 1) * st.rows * st.cols:
+                    chosen[id(st)] = (list(ks), [int(t) for t in dt], True)
+        rest = [(st, ks) for st, ks in big if id(st) not in chosen]
+        for (st, ks), nt in zip(rest, counts(rest, False)):
+            lim = (1.0 - XFER_MIN_EMPTY) * st.rows * st.cols
+            ck = [k for k, t in zip(ks, nt) if t <= lim]
+            if ck:
+                chosen[id(st)] = (ck, [int(t) for t in nt if t <= lim], False)
+        # compacted copies first, stack by stack, each followed by an event
+        # (slot = its position, up to 8 per context), then the dense copies
+        pending, slot_of = [], {}
+        for st, ks in todo:
+            if id(st) in chosen:
+                ck, ct, delta = chosen[id(st)]
+                pending.append((st, st.compact_start(ck, ct, delta), ct))
+                slot = slot_of.get(id(st.ctx), 0) % 8
+                slot_of[id(st.ctx)] = slot + 1
+                with st.ctx.lock:
+                    st.ctx.check(st.ctx.lib.pct_xfer_fence(st.ctx.h, slot), "xfer_fence")
+                pending[-1] = pending[-1] + (slot,)
+        dense = [(st, [k for k in ks if id(st) not in chosen or k not in set(chosen[id(st)][0])])
+                 for st, ks in todo]
         # bytes that cross PCIe in this call (dense slices + compacted payloads)
         self.xfer_bytes = sum(len(ks) * st.plane_bytes for st, ks in dense) + \
-            sum(p[2].nbytes + 4 * int(sum(ct)) + p[4].nbytes
-                for (st, p), (_, _, _, ct, _) in zip(pending, [q for q in plan if q[2]]))
-        if pending:
-            for ctx in ctxs.values():
-                with ctx.lock:
-                    ctx.check(ctx.lib.pct_xfer_fence(ctx.h), "xfer_fence")
+            sum(p[2].nbytes + 4 * int(sum(ct)) + p[4].nbytes for _, p, ct, _ in pending)
         for stack, ks in dense:
             if ks:
                 stack.prefetch(ks, sync=False)
-        if pending:
-            for ctx in ctxs.values():
-                ctx.check(ctx.lib.pct_xfer_wait(ctx.h), "xfer_wait")
-            threads = max(1, (os.cpu_count() or 1))
-            for stack, p in pending:
-                stack.compact_finish(p, threads)
+        # expand each stack as soon as its compacted data has landed (the later
+        # stacks' copies and the dense ones still in flight)
+        threads = max(1, (os.cpu_count() or 1))
+        for stack, p, _, slot in pending:
+            stack.ctx.check(stack.ctx.lib.pct_xfer_wait(stack.ctx.h, slot), "xfer_wait")
+            stack.compact_finish(p, threads)
         for ctx in ctxs.values():
             with ctx.lock:
                 ctx.check(ctx.lib.pct_sync(ctx.h), "sync")

@@ -13,7 +13,7 @@ xyz = synth.generate(3)
 pin = _lib.PinnedBuffer(_lib.context(0), xyz.shape, np.float32)
 pin.array[...] = xyz
 cloud = pct.PointCloud(pin.array)
-for mode in ("0", "nan", "1", "1", "nan", "0"):
+for mode in ("1", "nan", "1", "0"):
     os.environ["PCT_XFER_COMPACT"] = mode
     ts = []
     for rep in range(3):
