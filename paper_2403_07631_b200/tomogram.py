@@ -321,8 +321,8 @@ class Tomogram:
         the empty NaN (at least XFER_MIN_EMPTY of their cells) go as a bitmap
         + their non-empty values, and the rest dense, copied while the
         compacted ones are expanded.  PCT_XFER_COMPACT=0: every slice dense;
-        =nan: no delta chains.  cfg3: 127 ms dense, 112 ms NaN-compacted,
-        89 ms with delta chains (host-memory bound: 6.7 GB written)."""
+        =nan: no delta chains.  cfg3: 127 ms dense, 110 ms NaN-compacted,
+        64 ms with delta chains (host-memory bound: 6.7 GB written)."""
         groups = {}
         for s in self.slices:
             for l in (s.ground, s.ceiling, s.cost):
