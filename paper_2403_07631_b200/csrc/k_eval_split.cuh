@@ -400,12 +400,25 @@ __global__ void __launch_bounds__(kWalkNT) terrain_walk_skip_kernel(
     prev_enc = f32_bits(st.enc);
   };
   if (!fresh) {  // dense output: every slice written
-    for (int k = kb; k < ke; ++k) {
-      if (k == knext) compute(k);  // uniform
+    // runs of slices without an event repeat the current values (a tight
+    // store loop); an event slice computes first
+    int k = kb;
+    while (true) {
+      const int kstop = knext < ke ? knext : ke;  // uniform
+#pragma unroll 2
+      for (; k < kstop; ++k) {
+        if (live) *pe = st.enc;
+        pe += L.sstride;
+        if (wlead) *pb = word;
+        pb += bstride;
+      }
+      if (k >= ke) break;
+      compute(k);
       if (live) *pe = st.enc;
       pe += L.sstride;
       if (wlead) *pb = word;
       pb += bstride;
+      ++k;
     }
     return;
   }
