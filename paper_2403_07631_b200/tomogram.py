@@ -387,7 +387,7 @@ class Tomogram:
                 stack.prefetch(ks, sync=False)
         # expand each stack as soon as its compacted data has landed (the later
         # stacks' copies and the dense ones still in flight)
-        threads = max(1, (os.cpu_count() or 1))
+        threads = int(os.environ.get("PCT_XFER_THREADS", 0)) or max(1, (os.cpu_count() or 1))
         for stack, p, _, slot in pending:
             stack.ctx.check(stack.ctx.lib.pct_xfer_wait(stack.ctx.h, slot), "xfer_wait")
             stack.compact_finish(p, threads)
