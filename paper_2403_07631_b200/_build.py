@@ -43,7 +43,9 @@ def _stale(target: Path, sources) -> bool:
 def build(force: bool = False, verbose: bool = False) -> Path:
     LIB.mkdir(exist_ok=True)
     cu = sorted(CSRC.glob("*.cu"))
-    deps = cu + sorted(CSRC.glob("*.cuh")) + sorted(CSRC.glob("*.h")) + [INCLUDE / "pct.h"]
+    # host-only C++ of libpct.so (g++; hostmath.cpp builds libpct_hostmath.so)
+    cpp = [p for p in sorted(CSRC.glob("*.cpp")) if p.name != "hostmath.cpp"]
+    deps = cu + cpp + sorted(CSRC.glob("*.cuh")) + sorted(CSRC.glob("*.h")) + [INCLUDE / "pct.h"]
     out = LIB / "libpct.so"
     if force or _stale(out, deps):
         from concurrent.futures import ThreadPoolExecutor
@@ -60,10 +62,22 @@ def build(force: bool = False, verbose: bool = False) -> Path:
             (LIB / (src.stem + ".ptxas.txt")).write_text(r.stderr)
             return str(obj)
 
-        # one nvcc per translation unit, in parallel (k_evaluate.cu dominates)
-        with ThreadPoolExecutor(max(1, min(len(cu), os.cpu_count() or 1))) as ex:
-            objs = list(ex.map(compile_one, cu))
-        cmd = [nvcc(), *ARCH, "-shared", "-o", str(out), *objs, "-lcudart"]
+        def compile_cpp(src):
+            obj = LIB / (src.stem + ".o")
+            cxx = shutil.which("g++") or "g++"
+            cmd = [cxx, "-O3", "-std=c++17", "-fPIC", "-pthread", "-I", str(INCLUDE), "-c",
+                   str(src), "-o", str(obj)]
+            r = subprocess.run(cmd, capture_output=True, text=True)
+            if r.returncode != 0:
+                sys.stderr.write(r.stdout + r.stderr)
+                raise RuntimeError(f"g++ failed on {src.name}")
+            return str(obj)
+
+        # one compiler per translation unit, in parallel (k_evaluate.cu dominates)
+        with ThreadPoolExecutor(max(1, min(len(cu) + len(cpp), os.cpu_count() or 1))) as ex:
+            objs = list(ex.map(compile_one, cu)) + list(ex.map(compile_cpp, cpp))
+        cmd = [nvcc(), *ARCH, "-shared", "-o", str(out), *objs, "-lcudart", "-Xcompiler",
+               "-pthread"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)

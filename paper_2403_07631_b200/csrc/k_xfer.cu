@@ -21,11 +21,7 @@
 
 #include <algorithm>
 #include <cstring>
-#include <thread>
 #include <vector>
-#if defined(__SSE2__)
-#include <emmintrin.h>  // non-temporal stores of the host expansion
-#endif
 
 #include "pct_internal.h"
 
@@ -276,106 +272,5 @@ extern "C" int pct_xfer_wait(pct_ctx *ctx, int32_t slot) {
   return PCT_OK;
 }
 
-// Host side: expand n compacted slices into their output arrays.  NaN mode
-// (delta = 0): the work is split into (slice, chunk) items; item (m, c)
-// rebuilds cells [c * chunk, (c+1) * chunk) of slice m from its bitmap words
-// and the packed values from chunk_off[m][c] on (a clear bit = the empty
-// NaN).  Delta chains (delta = 1): the items are chunks; a thread rebuilds
-// the chunk of slice 0 against NaN in a cache-resident buffer, then patches
-// it slice after slice (a clear bit = the previous slice's value), streaming
-// each state out.  Output lines leave with non-temporal stores where they
-// are 16-byte aligned (no read-for-ownership: the host's memory bandwidth is
-// shared with the dense copies landing at the same time).
-namespace {
-inline void put_line(float *dst, const float *line, int nc) {
-#if defined(__SSE2__)
-  if (nc == 32 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
-    const __m128i *s = reinterpret_cast<const __m128i *>(line);
-    __m128i *d = reinterpret_cast<__m128i *>(dst);
-    for (int q = 0; q < 8; ++q) _mm_stream_si128(d + q, _mm_load_si128(s + q));
-    return;
-  }
-#endif
-  std::memcpy(dst, line, sizeof(float) * (size_t)nc);
-}
-}  // namespace
-
-extern "C" int pct_xfer_expand(const uint32_t *bitmaps, const float *packed,
-                               const int64_t *chunk_off, int32_t n, int64_t cells,
-                               int32_t delta, float *const *outs, int32_t nthreads) {
-  if (n <= 0) return PCT_OK;
-  if (!bitmaps || !packed || !chunk_off || !outs || cells <= 0) return PCT_E_INVALID;
-  const int64_t W = (cells + 31) / 32;
-  const int64_t nchunk = (cells + kXChunk - 1) / kXChunk;
-  const int64_t items = delta ? nchunk : (int64_t)n * nchunk;
-  uint32_t nan_bits = kNaNBits;
-  float nanv;
-  std::memcpy(&nanv, &nan_bits, 4);
-  auto nan_item = [&](int64_t it) {
-    alignas(16) float line[32];
-    const int64_t m = it / nchunk, c = it - m * nchunk;
-    const uint32_t *bm = bitmaps + m * W;
-    const float *p = packed + chunk_off[m * nchunk + c];
-    float *o = outs[m];
-    const int64_t w0 = c * (kXChunk / 32), w1 = std::min(W, w0 + kXChunk / 32);
-    for (int64_t w = w0; w < w1; ++w) {
-      const uint32_t bits = bm[w];
-      const int nc = (int)std::min<int64_t>(32, cells - w * 32);
-      if (bits == 0xFFFFFFFFu && nc == 32) {
-        std::memcpy(line, p, 128);
-        p += 32;
-      } else {
-        for (int j = 0; j < 32; ++j) line[j] = (bits >> j & 1u) ? *p++ : nanv;
-      }
-      put_line(o + w * 32, line, nc);
-    }
-  };
-  auto delta_item = [&](int64_t c, float *buf) {
-    const int64_t w0 = c * (kXChunk / 32), w1 = std::min(W, w0 + kXChunk / 32);
-    for (int32_t m = 0; m < n; ++m) {
-      const uint32_t *bm = bitmaps + m * W;
-      const float *p = packed + chunk_off[m * nchunk + c];
-      float *o = outs[m];
-      for (int64_t w = w0; w < w1; ++w) {
-        uint32_t bits = bm[w];
-        float *line = buf + (w - w0) * 32;
-        const int nc = (int)std::min<int64_t>(32, cells - w * 32);
-        if (m == 0) {
-          for (int j = 0; j < 32; ++j) line[j] = (bits >> j & 1u) ? *p++ : nanv;
-        } else {
-          while (bits) {
-            const int j = __builtin_ctz(bits);
-            bits &= bits - 1u;
-            line[j] = *p++;
-          }
-        }
-        put_line(o + w * 32, line, nc);
-      }
-    }
-  };
-  auto work = [&](int64_t i0, int64_t i1) {
-    std::vector<float> dbuf;
-    if (delta) dbuf.resize(kXChunk + 4);
-    float *buf = dbuf.empty() ? nullptr
-                              : reinterpret_cast<float *>(
-                                    (reinterpret_cast<uintptr_t>(dbuf.data()) + 15) & ~(uintptr_t)15);
-    for (int64_t it = i0; it < i1; ++it) {
-      if (delta) delta_item(it, buf);
-      else nan_item(it);
-    }
-#if defined(__SSE2__)
-    _mm_sfence();
-#endif
-  };
-  int nt = std::max(1, std::min<int>(nthreads, (int)std::min<int64_t>(items, 256)));
-  if (nt == 1) {
-    work(0, items);
-    return PCT_OK;
-  }
-  std::vector<std::thread> th;
-  th.reserve((size_t)nt);
-  for (int t = 0; t < nt; ++t)
-    th.emplace_back(work, items * t / nt, items * (t + 1) / nt);
-  for (auto &x : th) x.join();
-  return PCT_OK;
-}
+// The host side, pct_xfer_expand, is in xfer_host.cpp (g++, AVX-512 when the
+// host has it).
