@@ -709,6 +709,9 @@ __global__ void __launch_bounds__(kHistNT, 1) hist_pass_kernel(
 constexpr int kBulkQ = kHistNT;        // quads per stage
 constexpr int kBulkBytes = kBulkQ * 48;  // 48 KB
 constexpr int kBulkStages = 2;
+#ifndef PCT_BULK_LASTWARP
+#define PCT_BULK_LASTWARP 1
+#endif
 template <bool SCATTER>
 __global__ void __launch_bounds__(kHistNT, 1) hist_pass_bulk_kernel(
     const float *__restrict__ xyz, int64_t n, BinArgs a, int nbx, int nb,
@@ -742,7 +745,11 @@ __global__ void __launch_bounds__(kHistNT, 1) hist_pass_bulk_kernel(
   if (tid == 0) {
     for (int s = 0; s < kBulkStages; ++s) {
       mbar_init(&full[s], 1);
+#if PCT_BULK_LASTWARP
+      reinterpret_cast<unsigned *>(empty)[s] = 0u;
+#else
       mbar_init(&empty[s], kHistNT / 32);
+#endif
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int64_t i = 0; i < kBulkStages && i < nst; ++i) issue(i);
@@ -763,11 +770,26 @@ __global__ void __launch_bounds__(kHistNT, 1) hist_pass_bulk_kernel(
       hist_quad<SCATTER>(sq[0], sq[1], sq[2], tid < qn, a, hts, nbx, h, recs, outside);
     }
     __syncwarp();
+#if PCT_BULK_LASTWARP
+    // the last warp done with the stage refills it (no thread waits for the
+    // others: warp 0 is not held back behind the slowest warp every stage)
+    if ((tid & 31) == 0) {
+      unsigned *done = reinterpret_cast<unsigned *>(empty) + s;
+      __threadfence_block();
+      if (atomicAdd(done, 1u) == kHistNT / 32 - 1) {
+        *done = 0u;  // next used after this refill lands
+        __threadfence_block();
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if (i + kBulkStages < nst) issue(i + kBulkStages);
+      }
+    }
+#else
     if ((tid & 31) == 0) mbar_arrive(&empty[s]);
     if (tid == 0 && i + kBulkStages < nst) {
       mbar_wait(&empty[s], ph);
       issue(i + kBulkStages);
     }
+#endif
   }
   for (int64_t p = (q1 << 2) + tid; p < p1; p += kHistNT) {  // the tail (< 4 points)
     const float4 A = make_float4(xyz[3 * p], xyz[3 * p + 1], xyz[3 * p + 2], 0.f);

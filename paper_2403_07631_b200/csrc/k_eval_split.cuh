@@ -284,7 +284,12 @@ __device__ __forceinline__ unsigned long long warp_or64(unsigned long long v) {
 // cells of a loaded tile from its previous slice.  At the campus map this
 // drops 93 % of the walk's stores.
 template <bool CHUNKED>
-__global__ void __launch_bounds__(kWalkNT) terrain_walk_skip_kernel(
+#ifdef PCT_WALK_MINB
+#define PCT_WALK_BOUNDS __launch_bounds__(kWalkNT, PCT_WALK_MINB)
+#else
+#define PCT_WALK_BOUNDS __launch_bounds__(kWalkNT)
+#endif
+__global__ void PCT_WALK_BOUNDS terrain_walk_skip_kernel(
     const float *__restrict__ ground, const float *__restrict__ ceiling, int S, int rows,
     int cols, float *__restrict__ enc_out, EncLayout L, uint32_t *__restrict__ bits_out,
     int wpr, unsigned char *__restrict__ chgmap, const unsigned long long *__restrict__ gmask,
