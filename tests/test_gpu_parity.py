@@ -770,3 +770,45 @@ def test_dynamic_work_claims_match_static(golden, monkeypatch, env):
     assert run() == dyn
     assert dyn[0] == case["cost_slice_sha256"]
     assert dyn[1] == [case["heights"][k] for k in case["keep"]]
+
+
+@pytest.mark.parametrize("offset", [0.0, 12.37, -731.9, 5.0e5])
+def test_partitioned_builds_at_cell_borders(monkeypatch, offset):
+    """Every build against the oracle on float32 points placed within a few
+    ulps of cell borders (v = v0 + (i + 0.5) r_g) and of the plane heights,
+    at small and large coordinates (5e5: the float32 grid is 3 cm).  (A
+    float32 cell path with a float64 fallback near borders was measured in
+    the histogram passes: correct here, but slower -- DESIGN 9.1.)"""
+    rng = np.random.default_rng(int(abs(offset)) + 7)
+    r_g, d_s = 0.1, 0.5
+    x0, y0, z0 = np.float32(offset), np.float32(offset * 0.5 - 3.3), np.float32(offset * 0.01)
+    n_i, n_j = 40, 60
+    pts = []
+    for i in range(n_i):
+        for j in range(0, n_j, 3):
+            for d in (-2, -1, 0, 1, 2):
+                bx = np.float32(np.float64(x0) + (j + 0.5) * r_g)
+                by = np.float32(np.float64(y0) + (i + 0.5) * r_g)
+                x = bx
+                y = by
+                for _ in range(abs(d)):
+                    x = np.nextafter(x, np.float32(np.inf if d > 0 else -np.inf))
+                    y = np.nextafter(y, np.float32(np.inf if d > 0 else -np.inf))
+                k = int(rng.integers(0, 6))
+                h = np.float32(np.float64(z0) + d_s * (k + 1))
+                for dz in (-1, 0, 1):
+                    z = h if dz == 0 else np.nextafter(h, np.float32(np.inf * dz))
+                    pts.append((x, y, z))
+    pts = np.array(pts, np.float32)
+    extra = np.column_stack([x0 + rng.uniform(0, n_j * r_g, 20_000),
+                             y0 + rng.uniform(0, n_i * r_g, 20_000),
+                             z0 + rng.uniform(0, 3.2, 20_000)]).astype(np.float32)
+    corner = np.array([[x0, y0, z0]], np.float32)
+    xyz = np.concatenate([corner, pts, extra])
+    xyz = xyz[rng.permutation(len(xyz))]
+    ref = oracle.build(xyz, d_s, r_g)
+    for build in ("atomic", "tiled", "hist"):
+        monkeypatch.setenv("PCT_BUILD", build)
+        tom = pct.build_tomogram(pct.PointCloud(xyz), d_s, r_g)
+        _assert_layers_equal(tom.ground_stack(), ref["ground"], f"ground {build}")
+        _assert_layers_equal(tom.ceiling_stack(), ref["ceiling"], f"ceiling {build}")
