@@ -633,9 +633,10 @@ int pct_tomo_evaluate(pct_ctx *ctx, pct_tomo *t, const pct_trav_params *p, const
   const size_t bytes = (size_t)t->fr.n_slices * t->fr.rows * t->fr.cols * sizeof(float);
   if (!t->cost) PCT_CUDA(ctx, cudaMallocFromPoolAsync(reinterpret_cast<void **>(&t->cost), bytes, ctx->mempool, ctx->stream));
   ctx->eval_masks = t->masks;  // written by this tomogram's build (NULL: derived again)
-  // per-tile cost-change masks for the simplify window (room for 32 x 32 tiles)
+  // per-tile cost-change masks for the simplify window (room for tiles of
+  // >= 16 rows x 32 columns)
   if (t->masks && t->fr.n_slices <= 64 && !t->tcm) {
-    const size_t tb = (size_t)((t->fr.rows + 31) / 32) * ((t->fr.cols + 31) / 32) * 8;
+    const size_t tb = (size_t)((t->fr.rows + 15) / 16) * ((t->fr.cols + 31) / 32) * 8;
     if (cudaMallocFromPoolAsync(reinterpret_cast<void **>(&t->tcm), tb, ctx->mempool,
                                 ctx->stream) != cudaSuccess) {
       cudaGetLastError();

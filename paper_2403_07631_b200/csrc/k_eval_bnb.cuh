@@ -73,7 +73,10 @@ struct BnbGeom {
   static constexpr int O_OK = O_BITS + ((GH * GWW * 4 + 15) / 16) * 16;
   static constexpr int O_OT = ((O_OK + CH * CWW * 4 + 127) / 128) * 128;  // output tile (TMA store source)
   static constexpr int O_SL = O_OT + TH * TW * 4;                      // u16 list
-  static constexpr int O_BM = O_SL + ((TH * TW * 2 + 15) / 16) * 16;
+  // list capacity: every warp's P2 outputs, i.e. TH x TW/4 groups rounded up
+  // to whole passes of the CTA (up to 256 threads) x 4 outputs
+  static constexpr int SLN = (TH * (TW / 4) + 255) / 256 * 256 * 4;
+  static constexpr int O_BM = O_SL + ((SLN * 2 + 15) / 16) * 16;
   static constexpr int O_U = O_BM + ((NBY * NBX * 4 + 15) / 16) * 16;
   static constexpr int O_CB = O_U + ((QY * QX * 4 + 15) / 16) * 16;     // u8 change blocks
   static constexpr int O_DB = O_CB + ((CBY * CBX + 15) / 16) * 16;      // u8 dirty blocks
@@ -213,7 +216,10 @@ __global__ void __launch_bounds__(NT, MINB) resolve_inflate_bnb_kernel(
     int *__restrict__ work = nullptr) {
   using G = BnbGeom<R, PR, TH, TW, SP>;
   constexpr int NWARP = NT / 32;
-  constexpr int WSEG = TH * TW / NWARP;  // list entries per warp (its P2 outputs)
+  // list entries per warp: its P2 outputs (4 per thread per pass over the
+  // TH x TW/4 output groups)
+  constexpr int WSEG = (TH * (TW / 4) + NT - 1) / NT * 32 * 4;
+  static_assert(NWARP * WSEG <= G::SLN, "bnb output list capacity");
   static_assert((TH * TW) % NWARP == 0 && NWARP <= 32, "warp list segments");
   extern __shared__ __align__(128) unsigned char smem[];
   uint32_t *bits = reinterpret_cast<uint32_t *>(smem + G::O_BITS);

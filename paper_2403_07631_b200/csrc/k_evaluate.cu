@@ -629,9 +629,15 @@ constexpr int kBnbMinBlocks() {
 // the sparse-merge instantiation: its shared memory allows 5 CTAs per SM at
 // R = 4, so it may use the registers of 5 (the change-map prefetch lives in
 // them)
+#ifndef PCT_BNB_TH
+#define PCT_BNB_TH 24  // output tile rows of the R = 4 bnb evaluation
+#endif
+#ifndef PCT_BNB_SP_MINB
+#define PCT_BNB_SP_MINB 5
+#endif
 template <int R>
 constexpr int kBnbMinBlocksSp() {
-  return R <= 4 ? 5 : 4;
+  return R <= 4 ? PCT_BNB_SP_MINB : 4;
 }
 
 template <int R, int PR, int TH, int TW, int BNT = 256>
@@ -933,8 +939,11 @@ int launch_fast(pct_ctx *ctx, const float *ground, const float *ceiling, int S, 
     if constexpr (R == 4) {
       if (bnb && alt)
         return launch_split<R, PR, 32, 64, 128>(ctx, ground, ceiling, S, rows, cols, kernel_w, kside, cost, true);
+      // 24 x 32 output tiles (measured against 32 x 32: cfg3 evaluate 2.525 ->
+      // 2.474 ms and simplify 0.682 -> 0.665 (finer tile change masks), cfg1
+      // evaluate 0.172 -> 0.167 ms; 16 x 32 with 6 CTAs per SM: 2.525 / 0.657)
       if (bnb)
-        return launch_split<R, PR, 32, 32, 128>(ctx, ground, ceiling, S, rows, cols, kernel_w, kside, cost, true);
+        return launch_split<R, PR, PCT_BNB_TH, 32, 128>(ctx, ground, ceiling, S, rows, cols, kernel_w, kside, cost, true);
     }
     if constexpr (R == 8) {
       if (bnb && alt)
