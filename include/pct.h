@@ -193,7 +193,12 @@ int pct_copy_slices(pct_ctx *ctx, float *dst, int64_t dst_slice_stride, const fl
    value); stream-ordered.  pct_xfer_fence / pct_xfer_wait: record event
    slot (0..7) on the stream / wait for it on the host (e.g. one stack's
    packed copies landed while later copies are still in flight).
-   pct_xfer_expand: host function (no context), nthreads host threads. */
+   pct_xfer_expand: host function (no context), nthreads host threads.
+   pct_xfer_expand_from: the same for a delta chain continued from `base`
+   (the already rebuilt slice before slice 0 of this call; its part of a
+   chain whose bitmaps / chunk offsets start at slice 0 of the call), so a
+   long chain can be rebuilt in parts while its later slices still cross
+   PCIe. */
 int pct_xfer_count(pct_ctx *ctx, const float *src, int64_t slice_stride,
                    const int32_t *slice_idx_host, int32_t n, int64_t cells, int32_t delta,
                    int64_t *totals_host);
@@ -210,6 +215,9 @@ int pct_xfer_wait(pct_ctx *ctx, int32_t slot);
 int pct_xfer_expand(const uint32_t *bitmaps, const float *packed, const int64_t *chunk_off,
                     int32_t n, int64_t cells, int32_t delta, float *const *outs,
                     int32_t nthreads);
+int pct_xfer_expand_from(const uint32_t *bitmaps, const float *packed, const int64_t *chunk_off,
+                         int32_t n, int64_t cells, int32_t delta, float *const *outs,
+                         int32_t nthreads, const float *base);
 /* Sweep primitives for a distributed simplify (simplify.py:18-73): the any()
    table of the first pass (bit j of table[k]: below = k-1-j, j < 16; bit 32:
    no lower neighbour; upper neighbour k+1) and any() flags of explicit

@@ -14,6 +14,7 @@
 #include <immintrin.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdint>
 #include <cstring>
 #include <thread>
@@ -33,6 +34,7 @@ struct Job {
   int32_t n;
   int64_t cells, W, nchunk, chunk;
   float *const *outs;
+  const float *base;  // delta chains: slice 0's predecessor (NULL: the empty NaN)
 };
 
 // ---- SSE2 path ------------------------------------------------------------
@@ -81,7 +83,9 @@ void delta_item_sse2(const Job &J, int64_t c, float *buf) {
       float *line = buf + (w - w0) * 32;
       const int nc = (int)std::min<int64_t>(32, J.cells - w * 32);
       if (m == 0) {
-        for (int j = 0; j < 32; ++j) line[j] = (bits >> j & 1u) ? *p++ : nanv;
+        const float *b0 = J.base ? J.base + w * 32 : nullptr;
+        for (int j = 0; j < 32; ++j)
+          line[j] = (bits >> j & 1u) ? *p++ : (b0 && j < nc ? b0[j] : nanv);
       } else {
         while (bits) {
           const int j = __builtin_ctz(bits);
@@ -143,7 +147,16 @@ __attribute__((target("avx512f"))) void delta_item_avx512(const Job &J, int64_t 
     for (int64_t w = w0; w < w1; ++w) {
       float *st = buf + (w - w0) * 32;
       const int nc = (int)std::min<int64_t>(32, J.cells - w * 32);
-      const __m512 lo = m ? _mm512_load_ps(st) : nanv, hi = m ? _mm512_load_ps(st + 16) : nanv;
+      __m512 lo = nanv, hi = nanv;
+      if (m) {
+        lo = _mm512_load_ps(st);
+        hi = _mm512_load_ps(st + 16);
+      } else if (J.base) {  // continuing a chain: the predecessor's cells (masked tail)
+        const __mmask16 ml = (__mmask16)(nc >= 16 ? 0xFFFFu : (1u << nc) - 1u);
+        const __mmask16 mh = (__mmask16)(nc >= 32 ? 0xFFFFu : nc > 16 ? (1u << (nc - 16)) - 1u : 0u);
+        lo = _mm512_mask_loadu_ps(nanv, ml, J.base + w * 32);
+        hi = _mm512_mask_loadu_ps(nanv, mh, J.base + w * 32 + 16);
+      }
       word_avx512(o + w * 32, st, p, bm[w], lo, hi, nc);
     }
   }
@@ -156,25 +169,38 @@ bool has_avx512() {
 
 }  // namespace
 
-extern "C" int pct_xfer_expand(const uint32_t *bitmaps, const float *packed,
-                               const int64_t *chunk_off, int32_t n, int64_t cells,
-                               int32_t delta, float *const *outs, int32_t nthreads) {
+extern "C" int pct_xfer_expand_from(const uint32_t *bitmaps, const float *packed,
+                                    const int64_t *chunk_off, int32_t n, int64_t cells,
+                                    int32_t delta, float *const *outs, int32_t nthreads,
+                                    const float *base) {
   if (n <= 0) return 0;
   if (!bitmaps || !packed || !chunk_off || !outs || cells <= 0) return kInvalid;
-  Job J{bitmaps, packed, chunk_off, n, cells, (cells + 31) / 32, 0, pct_xfer_chunk_cells(), outs};
+  if (base && !delta) return kInvalid;
+  Job J{bitmaps, packed, chunk_off, n, cells, (cells + 31) / 32, 0, pct_xfer_chunk_cells(), outs,
+        base};
   J.nchunk = (cells + J.chunk - 1) / J.chunk;
   const int64_t items = delta ? J.nchunk : (int64_t)n * J.nchunk;
   const bool avx = has_avx512();
-  auto work = [&](int64_t i0, int64_t i1) {
+  // items are claimed in small groups from a shared counter (chunks with
+  // many changed cells take longer: a static split left threads idle at the
+  // end of every stack)
+  std::atomic<int64_t> next{0};
+  constexpr int64_t kGrab = 2;
+  auto work = [&]() {
     float *buf = nullptr;
     if (delta) buf = static_cast<float *>(aligned_alloc(64, (size_t)J.chunk * 4 + 64));
-    for (int64_t it = i0; it < i1; ++it) {
-      if (delta) {
-        if (avx) delta_item_avx512(J, it, buf);
-        else delta_item_sse2(J, it, buf);
-      } else {
-        if (avx) nan_item_avx512(J, it);
-        else nan_item_sse2(J, it);
+    for (;;) {
+      const int64_t i0 = next.fetch_add(kGrab, std::memory_order_relaxed);
+      if (i0 >= items) break;
+      const int64_t i1 = std::min(items, i0 + kGrab);
+      for (int64_t it = i0; it < i1; ++it) {
+        if (delta) {
+          if (avx) delta_item_avx512(J, it, buf);
+          else delta_item_sse2(J, it, buf);
+        } else {
+          if (avx) nan_item_avx512(J, it);
+          else nan_item_sse2(J, it);
+        }
       }
     }
     _mm_sfence();
@@ -182,12 +208,20 @@ extern "C" int pct_xfer_expand(const uint32_t *bitmaps, const float *packed,
   };
   int nt = std::max(1, std::min<int>(nthreads, (int)std::min<int64_t>(items, 256)));
   if (nt == 1) {
-    work(0, items);
+    work();
     return 0;
   }
   std::vector<std::thread> th;
-  th.reserve((size_t)nt);
-  for (int t = 0; t < nt; ++t) th.emplace_back(work, items * t / nt, items * (t + 1) / nt);
+  th.reserve((size_t)nt - 1);
+  for (int t = 1; t < nt; ++t) th.emplace_back(work);
+  work();  // the calling thread takes items too
   for (auto &x : th) x.join();
   return 0;
+}
+
+extern "C" int pct_xfer_expand(const uint32_t *bitmaps, const float *packed,
+                               const int64_t *chunk_off, int32_t n, int64_t cells,
+                               int32_t delta, float *const *outs, int32_t nthreads) {
+  return pct_xfer_expand_from(bitmaps, packed, chunk_off, n, cells, delta, outs, nthreads,
+                              nullptr);
 }

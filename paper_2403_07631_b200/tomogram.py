@@ -13,6 +13,7 @@ from __future__ import annotations
 import ctypes as C
 import math
 import os
+import time
 import weakref
 from dataclasses import dataclass
 
@@ -30,6 +31,9 @@ XFER_MIN_CELLS = 1 << 20
 # a stack's kept slices travel as a delta chain (each against the previous
 # kept slice) when at most this share of their cells differ
 XFER_DELTA_MAX = 0.25
+# the first delta chain crosses PCIe in parts ending at these slices (each
+# rebuilt while the next is in flight) so the host starts early
+XFER_SPLIT = (4, 12)
 
 
 class GridSizeError(ValueError):
@@ -116,10 +120,14 @@ class DeviceStack:
                 self.ctx.h, self.ptr, self.rows * self.cols, idx.ctypes.data, len(idx),
                 self.rows * self.cols, int(bool(delta)), out.ctypes.data), "xfer_count")
 
-    def compact_start(self, ks, totals, delta: bool = False):
+    def compact_start(self, ks, totals, delta: bool = False, split=(), fence=None):
         """Queue the compacted read-back of slices ks (pct_xfer_pack, then
         bitmaps, packed values and chunk offsets to pinned host memory);
-        finish with :meth:`compact_finish` once the copies have landed."""
+        finish with :meth:`compact_finish` once the copies have landed.
+        ``split`` = (m1, m2, ..) (delta chains): the copies go in parts
+        [0, m1), [m1, m2), .., and ``fence()`` is called after every part but
+        the last (so those slices are rebuilt while the rest still crosses
+        PCIe; see compact_finish)."""
         cells = self.rows * self.cols
         n = len(ks)
         idx = np.ascontiguousarray(ks, dtype=np.int32)
@@ -138,27 +146,54 @@ class DeviceStack:
         d_pk = _lib.DeviceBuffer(self.ctx, h_pk.nbytes)
         d_co = _lib.DeviceBuffer(self.ctx, h_co.nbytes)
         lib, h = self.ctx.lib, self.ctx.h
+        prof = os.environ.get("PCT_XFER_TRACE") == "2"  # diagnostic: pack / copy times
+        if prof:
+            t0 = time.perf_counter()
         with self.ctx.lock:
             self.ctx.check(lib.pct_xfer_pack(h, self.ptr, cells, idx.ctypes.data, n, cells,
                                              int(bool(delta)), off.ctypes.data, d_bm.ptr,
                                              d_pk.ptr, d_co.ptr), "xfer_pack")
-            for dst, src in ((h_bm, d_bm), (h_co, d_co)):
-                self.ctx.check(lib.pct_memcpy_d2h_async(h, dst.ctypes.data, src.ptr, dst.nbytes),
-                               "d2h")
-            if n_packed:
-                self.ctx.check(lib.pct_memcpy_d2h_async(h, h_pk.ctypes.data, d_pk.ptr,
-                                                        n_packed * 4), "d2h")
+            if prof:
+                lib.pct_sync(h)
+                t1 = time.perf_counter()
+            self.ctx.check(lib.pct_memcpy_d2h_async(h, h_co.ctypes.data, d_co.ptr, h_co.nbytes),
+                           "d2h")
+            cuts = [0] + sorted(m for m in set(split) if 0 < m < n) + [n] if delta else [0, n]
+            parts = list(zip(cuts[:-1], cuts[1:]))
+            ends = np.concatenate([off, [n_packed]])
+            for a, b in parts:
+                wb = h_bm.strides[0]
+                self.ctx.check(lib.pct_memcpy_d2h_async(h, h_bm.ctypes.data + a * wb,
+                                                        d_bm.ptr + a * wb, (b - a) * wb), "d2h")
+                p0, p1 = int(ends[a]), int(ends[b])
+                if p1 > p0:
+                    self.ctx.check(lib.pct_memcpy_d2h_async(h, h_pk.ctypes.data + 4 * p0,
+                                                            d_pk.ptr + 4 * p0, 4 * (p1 - p0)),
+                                   "d2h")
+                if b < n and fence is not None:
+                    fence()
+            if prof:
+                lib.pct_sync(h)
+                t2 = time.perf_counter()
+                import sys
+                sys.stderr.write(f"compact_start: pack {1e3 * (t1 - t0):.2f} ms, copies "
+                                 f"{1e3 * (t2 - t1):.2f} ms for {(h_bm.nbytes + h_co.nbytes + 4 * n_packed) / 1e6:.0f} MB\n")
         return (list(ks), block, h_bm, h_pk, h_co, (d_bm, d_pk, d_co), bool(delta))
 
-    def compact_finish(self, pending, threads: int) -> None:
-        """Expand the landed compacted slices into their host arrays."""
+    def compact_finish(self, pending, threads: int, part=None) -> None:
+        """Expand the landed compacted slices into their host arrays
+        (``part`` = (a, b): slices [a, b) of the list only; a delta chain's
+        part continues from slice a - 1, already rebuilt)."""
         ks, block, h_bm, h_pk, h_co, _dev, delta = pending
-        outs = (C.c_void_p * len(ks))(*[block[i].ctypes.data for i in range(len(ks))])
-        self.ctx.check(self.ctx.lib.pct_xfer_expand(
-            h_bm.ctypes.data, h_pk.ctypes.data, h_co.ctypes.data, len(ks),
-            self.rows * self.cols, int(delta), outs, int(threads)), "xfer_expand")
-        for i, k in enumerate(ks):
-            self._host[k] = block[i]
+        a, b = part if part is not None else (0, len(ks))
+        outs = (C.c_void_p * (b - a))(*[block[i].ctypes.data for i in range(a, b)])
+        base = block[a - 1].ctypes.data if (delta and a > 0) else None
+        self.ctx.check(self.ctx.lib.pct_xfer_expand_from(
+            h_bm.ctypes.data + a * h_bm.strides[0], h_pk.ctypes.data,
+            h_co.ctypes.data + a * h_co.strides[0], b - a, self.rows * self.cols, int(delta),
+            outs, int(threads), base), "xfer_expand")
+        for i in range(a, b):
+            self._host[ks[i]] = block[i]
 
     def host_all(self) -> np.ndarray:
         out = np.empty((self.n_slices, self.rows, self.cols), np.float32)
@@ -323,6 +358,13 @@ class Tomogram:
         compacted ones are expanded.  PCT_XFER_COMPACT=0: every slice dense;
         =nan: no delta chains.  cfg3: 127 ms dense, 110 ms NaN-compacted,
         64 ms with delta chains (host-memory bound: 6.7 GB written)."""
+        trace = os.environ.get("PCT_XFER_TRACE") == "1"
+        t_0 = time.perf_counter()
+        marks = []
+
+        def mark(what):
+            if trace:
+                marks.append((what, time.perf_counter() - t_0))
         groups = {}
         for s in self.slices:
             for l in (s.ground, s.ceiling, s.cost):
@@ -359,6 +401,7 @@ class Tomogram:
             for (st, ks), dt in zip(cands, counts(cands, True)):
                 if int(dt[1:].sum()) <= XFER_DELTA_MAX * (len(ks) - 1) * st.rows * st.cols:
                     chosen[id(st)] = (list(ks), [int(t) for t in dt], True)
+        mark("delta counts")
         rest = [(st, ks) for st, ks in big if id(st) not in chosen]
         for (st, ks), nt in zip(rest, counts(rest, False)):
             lim = (1.0 - XFER_MIN_EMPTY) * st.rows * st.cols
@@ -367,33 +410,63 @@ class Tomogram:
                 chosen[id(st)] = (ck, [int(t) for t in nt if t <= lim], False)
         # compacted copies first, stack by stack, each followed by an event
         # (slot = its position, up to 8 per context), then the dense copies
+        # The first delta chain's first XFER_SPLIT slices cross on their own,
+        # so the host starts rebuilding them while the rest is in flight.
         pending, slot_of = [], {}
+
+        def next_slot(ctx):
+            slot = slot_of.get(id(ctx), 0) % 8
+            slot_of[id(ctx)] = slot + 1
+            return slot
+        split_done = False
         for st, ks in todo:
             if id(st) in chosen:
                 ck, ct, delta = chosen[id(st)]
-                pending.append((st, st.compact_start(ck, ct, delta), ct))
-                slot = slot_of.get(id(st.ctx), 0) % 8
-                slot_of[id(st.ctx)] = slot + 1
+                split, early = (), []
+                if delta and not split_done and len(ck) >= 8:
+                    split = tuple(m for m in XFER_SPLIT if m < len(ck) - 2)
+                    split_done = True
+
+                def fence(st=st, early=early):
+                    early.append(next_slot(st.ctx))
+                    st.ctx.check(st.ctx.lib.pct_xfer_fence(st.ctx.h, early[-1]), "xfer_fence")
                 with st.ctx.lock:
+                    p = st.compact_start(ck, ct, delta, split=split, fence=fence)
+                    slot = next_slot(st.ctx)
                     st.ctx.check(st.ctx.lib.pct_xfer_fence(st.ctx.h, slot), "xfer_fence")
-                pending[-1] = pending[-1] + (slot,)
+                pending.append((st, p, ct, slot, split, early))
         dense = [(st, [k for k in ks if id(st) not in chosen or k not in set(chosen[id(st)][0])])
                  for st, ks in todo]
         # bytes that cross PCIe in this call (dense slices + compacted payloads)
         self.xfer_bytes = sum(len(ks) * st.plane_bytes for st, ks in dense) + \
-            sum(p[2].nbytes + 4 * int(sum(ct)) + p[4].nbytes for _, p, ct, _ in pending)
+            sum(p[2].nbytes + 4 * int(sum(ct)) + p[4].nbytes for _, p, ct, *_ in pending)
+        mark("packs queued")
         for stack, ks in dense:
             if ks:
                 stack.prefetch(ks, sync=False)
         # expand each stack as soon as its compacted data has landed (the later
         # stacks' copies and the dense ones still in flight)
         threads = int(os.environ.get("PCT_XFER_THREADS", 0)) or max(1, (os.cpu_count() or 1))
-        for stack, p, _, slot in pending:
-            stack.ctx.check(stack.ctx.lib.pct_xfer_wait(stack.ctx.h, slot), "xfer_wait")
-            stack.compact_finish(p, threads)
+        for stack, p, _, slot, split, early in pending:
+            if early:
+                cuts = [0] + list(split) + [len(p[0])]
+                for q, ev in enumerate(early + [slot]):
+                    stack.ctx.check(stack.ctx.lib.pct_xfer_wait(stack.ctx.h, ev), "xfer_wait")
+                    mark(f"part {q} landed")
+                    stack.compact_finish(p, threads, part=(cuts[q], cuts[q + 1]))
+            else:
+                stack.ctx.check(stack.ctx.lib.pct_xfer_wait(stack.ctx.h, slot), "xfer_wait")
+                mark("landed")
+                stack.compact_finish(p, threads)
+            mark("expanded")
         for ctx in ctxs.values():
             with ctx.lock:
                 ctx.check(ctx.lib.pct_sync(ctx.h), "sync")
+        mark("done")
+        if trace:
+            import sys
+            sys.stderr.write("materialize: " + ", ".join(f"{w} {1e3 * t:.1f}" for w, t in marks) +
+                             " ms\n")
         return self
 
     def _stack(self, attr):

@@ -59,6 +59,23 @@ def test_compacted_slices_are_bit_exact(rows, cols):
             assert int(t) == int((u[k] != prev).sum())
             assert np.array_equal(g.view(np.uint32), u[k]), f"delta slice {k}"
             prev = u[k]
+    # a delta chain copied and rebuilt in parts (pct_xfer_expand_from: the
+    # second part continues from the rebuilt slice before it; ragged tails)
+    for split in ((1,), (2,), (4,), (1, 3), (2, 3, 5)):
+        ks = [0, 1, 2, 3, 4, 5]
+        st = DeviceStack(ctx, buf.ptr, n, rows, cols, buf)
+        tot = st.count_nonempty(ks, delta=True)
+        fences = []
+        p = st.compact_start(ks, [int(t) for t in tot], True, split=split,
+                             fence=lambda: fences.append(1))
+        assert len(fences) == len(split)
+        with st.ctx.lock:
+            st.ctx.check(st.ctx.lib.pct_sync(st.ctx.h), "sync")
+        cuts = [0, *split, len(ks)]
+        for a, b in zip(cuts[:-1], cuts[1:]):
+            st.compact_finish(p, 8, part=(a, b))
+        for k in ks:
+            assert np.array_equal(st._host[k].view(np.uint32), u[k]), f"split {split} slice {k}"
 
 
 @pytest.mark.parametrize("mode", ["1", "nan", "0"])
