@@ -2,10 +2,12 @@
 # Round-end evidence in one gpurun call: GPU tests, every bench line, ncu
 # launch lists (cfg0-3) and --set full captures of the timed step's kernels
 # (cfg3: the build / evaluate / simplify kernels; cfg1: the small-map ones).
-mkdir -p gpurun_out
+mkdir -p gpurun_out; export PYTHONPATH=$PWD
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"; tail -1 gpurun_out/smoke.log
 timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1
 echo "pytest rc=$?"; tail -1 gpurun_out/pytest_gpu.log
 bash scripts/bench_all.sh
+PCT_XFER_TRACE=1 timeout 600 python scripts/e2e_split.py > gpurun_out/e2e_split.txt 2>&1; echo "e2e_split rc=$?"
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/red_peak scripts/red_peak.cu && /tmp/red_peak > gpurun_out/red_peak.json
 for c in 0 1 2 3; do
   timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
