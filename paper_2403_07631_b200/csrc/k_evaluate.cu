@@ -1054,7 +1054,10 @@ int launch_evaluate_batch(pct_ctx *ctx, int n_maps, float *const *ground, float 
                           const pct_frame *frames, const pct_trav_params &p,
                           const float *kernel_w, int kside, float *const *cost) {
   if (n_maps <= 0) return PCT_OK;
-  constexpr int R = 4, PR = 3, TH = 32, TW = 32, BNT = 128;
+#ifndef PCT_BNB_BATCH_TH
+#define PCT_BNB_BATCH_TH 24  // (32: cfg4 5.438 vs 5.41 ms)
+#endif
+  constexpr int R = 4, PR = 3, TH = PCT_BNB_BATCH_TH, TW = 32, BNT = 128;
   std::vector<float> bw;
   const double r_g = frames[0].r_g;
   bool same_rg = true;

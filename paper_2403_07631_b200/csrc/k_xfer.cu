@@ -166,17 +166,30 @@ __global__ void __launch_bounds__(kXThreads) xfer_pack_kernel(const XferSlices *
   const unsigned lt = (1u << lane) - 1u;
   const int64_t w0 = base / 32;
   uint32_t *bm = bitmaps + (int64_t)m * W;
-  constexpr int U = 8;
+#ifndef PCT_XFER_PACK_U
+#define PCT_XFER_PACK_U 8
+#endif
+  constexpr int U = PCT_XFER_PACK_U;  // words in flight
+  // branch-free loads (clamped addresses, the base slice read from `s`
+  // itself when there is none) so the U words' loads issue together
+  const bool use_b = bs != nullptr;
+  const float *bsrc = use_b ? bs : s;
 #pragma unroll 1
   for (int i0 = 0; i0 < 32; i0 += U) {
     float v[U];
+    uint32_t bv[U];
     bool d[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t cell = base + (i0 + u) * 32 + lane;
-      const bool in = cell < cells;
-      v[u] = in ? __ldg(s + cell) : bits_f32(kNaNBits);
-      d[u] = in && differs(v[u], bs, cell);
+      const int64_t cc = cell < cells ? cell : cells - 1;
+      v[u] = __ldg(s + cc);
+      bv[u] = f32_bits(__ldg(bsrc + cc));
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t cell = base + (i0 + u) * 32 + lane;
+      d[u] = cell < cells && f32_bits(v[u]) != (use_b ? bv[u] : kNaNBits);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
