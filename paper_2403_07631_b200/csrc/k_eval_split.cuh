@@ -123,7 +123,12 @@ __device__ __forceinline__ void walk_body(const float *__restrict__ ground,
   const int64_t pidx = (int64_t)blockIdx.x * kWalkNT + threadIdx.x;
   const int lane = threadIdx.x & 31;
   const int pcols = wpr * 32;
-  const int i0_ = (int)(pidx / pcols), j0_ = (int)(pidx - (int64_t)i0_ * pcols);
+  // (32-bit division when the padded grid has < 2^32 cells: a 64-bit
+  // division by a run-time value is a ~100-instruction subroutine)
+  const int i0_ = (int64_t)rows * pcols <= 0xFFFFFFFFll
+                      ? (int)((uint32_t)pidx / (uint32_t)pcols)
+                      : (int)(pidx / pcols);
+  const int j0_ = (int)(pidx - (int64_t)i0_ * pcols);
   const bool live = i0_ < rows && j0_ < cols;
   const int i = i0_ < rows ? i0_ : rows - 1;
   const int j = j0_ < cols ? j0_ : cols - 1;  // clamped: address formation only
@@ -304,7 +309,12 @@ __global__ void PCT_WALK_BOUNDS terrain_walk_skip_kernel(
   const int64_t pidx = (int64_t)blockIdx.x * kWalkNT + threadIdx.x;
   const int lane = threadIdx.x & 31;
   const int pcols = wpr * 32;
-  const int i0_ = (int)(pidx / pcols), j0_ = (int)(pidx - (int64_t)i0_ * pcols);
+  // (32-bit division when the padded grid has < 2^32 cells: a 64-bit
+  // division by a run-time value is a ~100-instruction subroutine)
+  const int i0_ = (int64_t)rows * pcols <= 0xFFFFFFFFll
+                      ? (int)((uint32_t)pidx / (uint32_t)pcols)
+                      : (int)(pidx / pcols);
+  const int j0_ = (int)(pidx - (int64_t)i0_ * pcols);
   const bool live = i0_ < rows && j0_ < cols;
   const int i = i0_ < rows ? i0_ : rows - 1;
   const int j = j0_ < cols ? j0_ : cols - 1;  // clamped: address formation only

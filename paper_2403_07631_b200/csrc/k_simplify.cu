@@ -229,8 +229,19 @@ __global__ void __launch_bounds__(kWinNT) window_skip_kernel(SimpArgs A, SimpMas
     const int64_t c0 = live ? cell : 0;
     unsigned long long vm = 1ull;
     if (live) {
-      const int i = (int)(c0 / M.cols), j = (int)(c0 - (int64_t)i * M.cols);
-      vm |= __ldg(M.gm + c0) | __ldg(M.tcm + (int64_t)(i / M.th) * M.tx + j / M.tw);
+      // 32-bit divisions when the map has < 2^32 cells (a 64-bit division
+      // by a run-time value is a ~100-instruction subroutine per warp)
+      int i, j;
+      if (A.cells <= 0xFFFFFFFFll) {
+        const uint32_t c = (uint32_t)c0, q = c / (uint32_t)M.cols;
+        i = (int)q;
+        j = (int)(c - q * (uint32_t)M.cols);
+      } else {
+        i = (int)(c0 / M.cols);
+        j = (int)(c0 - (int64_t)i * M.cols);
+      }
+      const uint32_t ti = (uint32_t)i / (uint32_t)M.th, tj = (uint32_t)j / (uint32_t)M.tw;
+      vm |= __ldg(M.gm + c0) | __ldg(M.tcm + (int64_t)ti * M.tx + tj);
     }
     const unsigned lo = __reduce_or_sync(0xFFFFFFFFu, (unsigned)vm);
     const unsigned hi = __reduce_or_sync(0xFFFFFFFFu, (unsigned)(vm >> 32));
