@@ -215,6 +215,18 @@ int pct_xfer_wait(pct_ctx *ctx, int32_t slot);
 int pct_xfer_expand(const uint32_t *bitmaps, const float *packed, const int64_t *chunk_off,
                     int32_t n, int64_t cells, int32_t delta, float *const *outs,
                     int32_t nthreads);
+/* pct_xfer_count_keep: pct_xfer_count_async that also keeps the chunk and
+   warp counts in counts_dev (device, pct_xfer_counts_bytes(cells, n) bytes);
+   pct_xfer_pack_counted: pct_xfer_pack from those counts (same slices, same
+   delta flag, the stack unchanged in between) without counting again. */
+int64_t pct_xfer_counts_bytes(int64_t cells, int32_t n);
+int pct_xfer_count_keep(pct_ctx *ctx, const float *src, int64_t slice_stride,
+                        const int32_t *slice_idx_host, int32_t n, int64_t cells, int32_t delta,
+                        int64_t *totals_host, uint32_t *counts_dev);
+int pct_xfer_pack_counted(pct_ctx *ctx, const float *src, int64_t slice_stride,
+                          const int32_t *slice_idx_host, int32_t n, int64_t cells, int32_t delta,
+                          const int64_t *packed_off_host, const uint32_t *counts_dev,
+                          uint32_t *bitmaps, float *packed, int64_t *chunk_off);
 int pct_xfer_expand_from(const uint32_t *bitmaps, const float *packed, const int64_t *chunk_off,
                          int32_t n, int64_t cells, int32_t delta, float *const *outs,
                          int32_t nthreads, const float *base);

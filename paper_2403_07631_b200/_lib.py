@@ -92,6 +92,10 @@ _SIGS = {
     "pct_xfer_wait": ([_vp, _i32], C.c_int),
     "pct_xfer_expand": ([_vp, _vp, _vp, _i32, _i64, _i32, _vp, _i32], C.c_int),
     "pct_xfer_expand_from": ([_vp, _vp, _vp, _i32, _i64, _i32, _vp, _i32, _vp], C.c_int),
+    "pct_xfer_counts_bytes": ([_i64, _i32], C.c_int64),
+    "pct_xfer_count_keep": ([_vp, _vp, _i64, _vp, _i32, _i64, _i32, _vp, _vp], C.c_int),
+    "pct_xfer_pack_counted": ([_vp, _vp, _i64, _vp, _i32, _i64, _i32, _vp, _vp, _vp, _vp, _vp],
+                              C.c_int),
     "pct_simplify_window": ([_vp, _vp, _vp, _i32, _i64, _i64, _d, _d, _vp], C.c_int),
     "pct_simplify_triples": ([_vp, _vp, _vp, _i32, _i64, _i64, _d, _d, _vp, _i32, _vp], C.c_int),
     "pct_planner_context": ([_vp, _vp, _vp, _i32, _i32, _i32, _d, _vp, _vp], C.c_int),

@@ -239,7 +239,7 @@ using namespace pct;
 
 static int xfer_count(pct_ctx *ctx, const float *src, int64_t slice_stride,
                       const int32_t *slice_idx_host, int32_t n, int64_t cells, int32_t delta,
-                      int64_t *totals_host, bool sync) {
+                      int64_t *totals_host, bool sync, uint32_t *keep = nullptr) {
   XferSlices *da = nullptr;
   int nchunk = 0;
   if (int rc = setup(ctx, src, slice_stride, slice_idx_host, n, cells, delta, &da, &nchunk))
@@ -249,11 +249,14 @@ static int xfer_count(pct_ctx *ctx, const float *src, int64_t slice_stride,
   const size_t abytes = (sizeof(XferSlices) + 255) & ~(size_t)255;
   const size_t cbytes = ((size_t)n * nchunk * 4 + 255) & ~(size_t)255;
   const size_t obytes = ((size_t)n * nchunk * 8 + 255) & ~(size_t)255;
-  unsigned *cnt = reinterpret_cast<unsigned *>(b + abytes);
+  // kept counts (pct_xfer_count_keep): chunk counts [n][nchunk] then warp
+  // counts [n][nchunk][8] in the caller's device buffer, for pct_xfer_pack_counted
+  unsigned *cnt = keep ? keep : reinterpret_cast<unsigned *>(b + abytes);
+  unsigned *wcnt = keep ? keep + (size_t)n * nchunk : nullptr;
   int64_t *coff = reinterpret_cast<int64_t *>(b + abytes + cbytes);
   int64_t *tot = reinterpret_cast<int64_t *>(b + abytes + cbytes + obytes);
   xfer_count_kernel<<<dim3((unsigned)nchunk, (unsigned)n), kXThreads, 0, ctx->stream>>>(
-      da, cnt, nchunk, nullptr);
+      da, cnt, nchunk, wcnt);
   if (int rc = check_launch(ctx, "xfer_count_kernel")) return rc;
   xfer_scan_kernel<<<(unsigned)n, 1024, 0, ctx->stream>>>(cnt, nchunk, nullptr, coff, tot);
   if (int rc = check_launch(ctx, "xfer_scan_kernel")) return rc;
@@ -326,3 +329,42 @@ extern "C" int pct_xfer_wait(pct_ctx *ctx, int32_t slot) {
 
 // The host side, pct_xfer_expand, is in xfer_host.cpp (g++, AVX-512 when the
 // host has it).
+
+extern "C" int64_t pct_xfer_counts_bytes(int64_t cells, int32_t n) {
+  if (cells <= 0 || n <= 0) return 0;
+  const int64_t nc = (cells + kXChunk - 1) / kXChunk;
+  return (int64_t)n * nc * (1 + kXThreads / 32) * 4;
+}
+
+extern "C" int pct_xfer_count_keep(pct_ctx *ctx, const float *src, int64_t slice_stride,
+                                   const int32_t *slice_idx_host, int32_t n, int64_t cells,
+                                   int32_t delta, int64_t *totals_host, uint32_t *counts_dev) {
+  if (!counts_dev) return fail(ctx, PCT_E_INVALID, "pct_xfer_count_keep: counts_dev is NULL");
+  return xfer_count(ctx, src, slice_stride, slice_idx_host, n, cells, delta, totals_host, false,
+                    counts_dev);
+}
+
+extern "C" int pct_xfer_pack_counted(pct_ctx *ctx, const float *src, int64_t slice_stride,
+                                     const int32_t *slice_idx_host, int32_t n, int64_t cells,
+                                     int32_t delta, const int64_t *packed_off_host,
+                                     const uint32_t *counts_dev, uint32_t *bitmaps, float *packed,
+                                     int64_t *chunk_off) {
+  XferSlices *da = nullptr;
+  int nchunk = 0;
+  if (int rc = setup(ctx, src, slice_stride, slice_idx_host, n, cells, delta, &da, &nchunk))
+    return rc;
+  if (!packed_off_host || !counts_dev || !bitmaps || !packed || !chunk_off)
+    return fail(ctx, PCT_E_INVALID, "pct_xfer_pack_counted: NULL buffer");
+  char *b = static_cast<char *>(ctx->scratch);
+  const size_t abytes = (sizeof(XferSlices) + 255) & ~(size_t)255;
+  const size_t cbytes = ((size_t)n * nchunk * 4 + 255) & ~(size_t)255;
+  const size_t obytes = ((size_t)n * nchunk * 8 + 255) & ~(size_t)255;
+  int64_t *doff = reinterpret_cast<int64_t *>(b + abytes + cbytes + obytes);
+  PCT_CUDA(ctx, upload_async(ctx, doff, packed_off_host, (size_t)n * 8));
+  xfer_scan_kernel<<<(unsigned)n, 1024, 0, ctx->stream>>>(counts_dev, nchunk, doff, chunk_off,
+                                                         nullptr);
+  if (int rc = check_launch(ctx, "xfer_scan_kernel")) return rc;
+  xfer_pack_kernel<<<dim3((unsigned)nchunk, (unsigned)n), kXThreads, 0, ctx->stream>>>(
+      da, chunk_off, counts_dev + (size_t)n * nchunk, nchunk, bitmaps, packed);
+  return check_launch(ctx, "xfer_pack_kernel");
+}

@@ -58,6 +58,7 @@ class DeviceStack:
         self.cols = int(cols)
         self.owner = owner
         self._host = {}
+        self._kept = None  # (slices, delta, device counts) of the last kept count pass
 
     @property
     def plane_bytes(self) -> int:
@@ -105,20 +106,32 @@ class DeviceStack:
         m - 1 of the list instead."""
         idx = np.ascontiguousarray(ks, dtype=np.int32)
         tot = np.empty(len(idx), np.int64)
+        self._kept = None
         with self.ctx.lock:
             self.ctx.check(self.ctx.lib.pct_xfer_count(
                 self.ctx.h, self.ptr, self.rows * self.cols, idx.ctypes.data, len(idx),
                 self.rows * self.cols, int(bool(delta)), tot.ctypes.data), "xfer_count")
         return tot
 
-    def count_nonempty_async(self, ks, delta: bool, out: np.ndarray) -> None:
+    def count_nonempty_async(self, ks, delta: bool, out: np.ndarray, keep: bool = False) -> None:
         """count_nonempty into ``out`` (page-locked int64), stream-ordered:
-        valid once the context's stream has synchronised."""
+        valid once the context's stream has synchronised.  ``keep``: the
+        per-chunk counts stay on the device for a compact_start of the same
+        slices (pct_xfer_pack_counted: no second count pass)."""
         idx = np.ascontiguousarray(ks, dtype=np.int32)
+        cells = self.rows * self.cols
         with self.ctx.lock:
-            self.ctx.check(self.ctx.lib.pct_xfer_count_async(
-                self.ctx.h, self.ptr, self.rows * self.cols, idx.ctypes.data, len(idx),
-                self.rows * self.cols, int(bool(delta)), out.ctypes.data), "xfer_count")
+            if keep:
+                lib = self.ctx.lib
+                buf = _lib.DeviceBuffer(self.ctx, int(lib.pct_xfer_counts_bytes(cells, len(idx))))
+                self.ctx.check(lib.pct_xfer_count_keep(
+                    self.ctx.h, self.ptr, cells, idx.ctypes.data, len(idx), cells,
+                    int(bool(delta)), out.ctypes.data, buf.ptr), "xfer_count")
+                self._kept = (tuple(int(k) for k in ks), bool(delta), buf)
+            else:
+                self.ctx.check(self.ctx.lib.pct_xfer_count_async(
+                    self.ctx.h, self.ptr, cells, idx.ctypes.data, len(idx), cells,
+                    int(bool(delta)), out.ctypes.data), "xfer_count")
 
     def compact_start(self, ks, totals, delta: bool = False, split=(), fence=None):
         """Queue the compacted read-back of slices ks (pct_xfer_pack, then
@@ -149,10 +162,16 @@ class DeviceStack:
         prof = os.environ.get("PCT_XFER_TRACE") == "2"  # diagnostic: pack / copy times
         if prof:
             t0 = time.perf_counter()
+        kept, self._kept = self._kept, None
         with self.ctx.lock:
-            self.ctx.check(lib.pct_xfer_pack(h, self.ptr, cells, idx.ctypes.data, n, cells,
-                                             int(bool(delta)), off.ctypes.data, d_bm.ptr,
-                                             d_pk.ptr, d_co.ptr), "xfer_pack")
+            if kept is not None and kept[0] == tuple(int(k) for k in ks) and kept[1] == bool(delta):
+                self.ctx.check(lib.pct_xfer_pack_counted(
+                    h, self.ptr, cells, idx.ctypes.data, n, cells, int(bool(delta)),
+                    off.ctypes.data, kept[2].ptr, d_bm.ptr, d_pk.ptr, d_co.ptr), "xfer_pack")
+            else:
+                self.ctx.check(lib.pct_xfer_pack(h, self.ptr, cells, idx.ctypes.data, n, cells,
+                                                 int(bool(delta)), off.ctypes.data, d_bm.ptr,
+                                                 d_pk.ptr, d_co.ptr), "xfer_pack")
             if prof:
                 lib.pct_sync(h)
                 t1 = time.perf_counter()
@@ -382,11 +401,12 @@ class Tomogram:
                 todo.append((stack, ks))
 
         def counts(cands, delta):
-            # every candidate stack's counts queued, one synchronisation
+            # every candidate stack's counts queued, one synchronisation (a
+            # delta chain's chunk counts stay on the device for its pack)
             outs = []
             for stack, ks in cands:
                 out = _lib.pinned_pool(stack.ctx).array((len(ks),), np.int64)
-                stack.count_nonempty_async(ks, delta, out)
+                stack.count_nonempty_async(ks, delta, out, keep=delta)
                 outs.append(out)
             for ctx in {id(st.ctx): st.ctx for st, _ in cands}.values():
                 with ctx.lock:

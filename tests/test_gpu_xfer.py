@@ -59,6 +59,22 @@ def test_compacted_slices_are_bit_exact(rows, cols):
             assert int(t) == int((u[k] != prev).sum())
             assert np.array_equal(g.view(np.uint32), u[k]), f"delta slice {k}"
             prev = u[k]
+    # the pack from the count pass's kept chunk counts (pct_xfer_pack_counted)
+    for delta in (False, True):
+        ks = [0, 1, 2, 3, 4, 5]
+        st = DeviceStack(ctx, buf.ptr, n, rows, cols, buf)
+        tot = _lib.pinned_pool(ctx).array((len(ks),), np.int64)
+        st.count_nonempty_async(ks, delta, tot, keep=True)
+        with st.ctx.lock:
+            st.ctx.check(st.ctx.lib.pct_sync(st.ctx.h), "sync")
+        assert st._kept is not None
+        p = st.compact_start(ks, [int(t) for t in tot], delta)
+        assert st._kept is None
+        with st.ctx.lock:
+            st.ctx.check(st.ctx.lib.pct_sync(st.ctx.h), "sync")
+        st.compact_finish(p, 8)
+        for k in ks:
+            assert np.array_equal(st._host[k].view(np.uint32), u[k]), f"kept {delta} slice {k}"
     # a delta chain copied and rebuilt in parts (pct_xfer_expand_from: the
     # second part continues from the rebuilt slice before it; ragged tails)
     for split in ((1,), (2,), (4,), (1, 3), (2, 3, 5)):
