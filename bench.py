@@ -10,8 +10,10 @@ ONE JSON line (rank 0).  Modes (by config, --mode overrides):
   sharded  (config 3, default): ONE map.  N = 1: the single-GPU library call
            (pct_tomo_run).  N > 1: row bands over the ranks (device partition
            + NCCL all-to-all of points, NCCL halo rows, any()-tables
-           all-reduced for simplify, surviving slices gathered on rank 0);
-           every rank draws only its own share of the cloud.  "strong".
+           all-reduced for simplify); each rank's surviving band stays on
+           its GPU, as the N = 1 stacks stay on theirs (e2e: the bands
+           written into one host Tomogram); every rank draws only its own
+           share of the cloud.  "strong".
   replica  (configs 0-2): every rank processes its own independently seeded
            map, no data-path collective; scaling "weak".
   batch    (config 4): 256 independent 250k-point maps split over the ranks,
@@ -231,7 +233,8 @@ def make_config(args, cfg, world, total_pts, R, Cc, S, keep, desc, maps_per_rank
             "l2": f"flushed between steps ({L2_FLUSH_BYTES >> 20} MiB write), "
                   "flush excluded from step time",
             "parallelism": {"replica": f"{world} independent maps (one per GPU)",
-                            "sharded": (f"1 map in {world} row bands (NCCL), gathered on rank 0"
+                            "sharded": (f"1 map in {world} row bands (NCCL), each band's "
+                                        "surviving slices resident on its rank"
                                         if world > 1 else "1 map on 1 GPU"),
                             "batch": f"{maps_per_rank} maps per GPU x {world}"}[args.mode]}
 
@@ -519,15 +522,17 @@ def run_b200(args):
             evs = {}
             with torch.cuda.stream(stream):
                 e0 = pipe.ev()
+                # the surviving bands stay on their ranks (device-resident
+                # result, as at N = 1); the e2e leg assembles one host Tomogram
                 gen = sharded.band_pipeline(dmaps[0], d_s, r_g, pct.TravParams(), rank, world,
-                                            device=local, events=evs, gather_to=0)
+                                            device=local, events=evs, gather_to=None)
                 res = sharded.run_torch(gen)
                 e1 = pipe.ev()
             band_info.update(S=len(res.heights), R=res.rows, C=res.cols, keep=len(res.keep),
                              nrows=res.nrows, res=res, cs_band=evs["cell_slices"])
             ea, eb = evs["evaluate"]
             # build = bounds .. evaluate start (incl. point exchange and halo
-            # exchange), simplify = evaluate end .. step end (incl. the gather)
+            # exchange), simplify = evaluate end .. step end (tables all-reduced)
             return {"total": [(e0, e1)], "bounds+build": [(e0, ea)], "evaluate": [(ea, eb)],
                     "simplify": [(eb, e1)]}
         out = {"bounds+build": [], "evaluate": [], "simplify": [], "total": []}
@@ -598,7 +603,8 @@ def run_b200(args):
         "config": make_config(args, cfg, world, total_pts if args.mode != "batch" else
                               len(maps[0]), R, Cc, S, info["keep"], desc, len(maps),
                               "bounds+build+evaluate+simplify, device-resident points" +
-                              (" (+ gather of the surviving slices on rank 0)" if banded else "")),
+                              (" (row bands: point and halo exchange included, surviving "
+                               "bands resident on their ranks)" if banded else "")),
         "stages_ms": {k: statistics.mean(v) for k, v in per.items()},
         "wall_s_timed_region": t_wall,
         "gpu_launches": launches,
@@ -817,9 +823,10 @@ def parity(args, cfg, cpu_res, pipe, dmaps, maps, tom, rank, world, banded, band
 
     N = 1 (and replica rank 0): one more untimed device pass keeping the
     stacks: every slice of ground / ceiling / cost bitwise, the keep list,
-    plane heights.  Banded: the simplified Tomogram gathered on rank 0 (its
-    kept slices bitwise).  Both: the reference bench's archive checksum of
-    the public API's simplified tomogram against the CPU port's."""
+    plane heights.  Banded: the keep list, and the archive checksum of the
+    host Tomogram the e2e leg assembled from every rank's band (its kept
+    slices bitwise).  Both: the reference bench's archive checksum of the
+    public API's simplified tomogram against the CPU port's."""
     if rank != 0:
         return None
     t, cost, keep = cpu_res
