@@ -123,6 +123,17 @@ int pct_evaluate_masked(pct_ctx *ctx, const float *ground, const float *ceiling,
                         int32_t rows, int32_t cols, double r_g, const pct_trav_params *p,
                         const float *kernel_w, int32_t kside, const uint64_t *masks,
                         float *cost);
+/* pct_evaluate_masked that also records, per evaluation tile, the slices
+   whose costs may differ from the slice below: tile_masks (device uint64,
+   pct_tile_masks_bytes(rows, cols) bytes), tile_geom[2] = the tile height
+   and width (0, 0 when this evaluation path recorded none).  With the
+   build's masks they let pct_simplify_masked read only where values
+   change. */
+int64_t pct_tile_masks_bytes(int32_t rows, int32_t cols);
+int pct_evaluate_tiles(pct_ctx *ctx, const float *ground, const float *ceiling, int32_t n_slices,
+                       int32_t rows, int32_t cols, double r_g, const pct_trav_params *p,
+                       const float *kernel_w, int32_t kside, const uint64_t *masks, float *cost,
+                       uint64_t *tile_masks, int32_t *tile_geom);
 /* per-op entry points on one (rows, cols) layer, device pointers */
 int pct_interval_cost(pct_ctx *ctx, const float *ground, const float *ceiling, int32_t rows,
                       int32_t cols, const pct_trav_params *p, float *out);      /* :59-73 */
@@ -147,6 +158,13 @@ int pct_terrain_cost_values(pct_ctx *ctx, const double *m_xy, const double *m_gr
 int pct_simplify(pct_ctx *ctx, const float *ground, const float *cost, int32_t n_slices,
                  int32_t rows, int32_t cols, double eps_e, double c_barrier,
                  int32_t *keep_host, int32_t *n_keep);
+/* pct_simplify with the build's slice-change masks of the ground stack and
+   the tile masks pct_evaluate_tiles recorded for the cost stack (same
+   slices); NULL / zero geometry behaves as pct_simplify. */
+int pct_simplify_masked(pct_ctx *ctx, const float *ground, const float *cost, int32_t n_slices,
+                        int32_t rows, int32_t cols, double eps_e, double c_barrier,
+                        const uint64_t *masks, const uint64_t *tile_masks,
+                        const int32_t *tile_geom, int32_t *keep_host, int32_t *n_keep);
 /* unique-cell mask of slice k given neighbour slices (-1 = none), simplify.py:31-53 */
 int pct_unique_mask(pct_ctx *ctx, const float *ground, const float *cost, int32_t rows,
                     int32_t cols, int32_t k, int32_t below, int32_t above, double eps_e,

@@ -70,6 +70,11 @@ _SIGS = {
     "pct_evaluate_masked": ([_vp, _vp, _vp, _i32, _i32, _i32, _d, C.POINTER(TravParamsC), _vp,
                              _i32, _vp, _vp], C.c_int),
     "pct_tomo_masks": ([_vp], _vp),
+    "pct_tile_masks_bytes": ([_i32, _i32], C.c_int64),
+    "pct_evaluate_tiles": ([_vp, _vp, _vp, _i32, _i32, _i32, _d, C.POINTER(TravParamsC), _vp,
+                            _i32, _vp, _vp, _vp, _vp], C.c_int),
+    "pct_simplify_masked": ([_vp, _vp, _vp, _i32, _i32, _i32, _d, _d, _vp, _vp, _vp, _vp, _vp],
+                            C.c_int),
     "pct_interval_cost": ([_vp, _vp, _vp, _i32, _i32, C.POINTER(TravParamsC), _vp], C.c_int),
     "pct_ground_cost": ([_vp, _vp, _i32, _i32, _d, C.POINTER(TravParamsC), _vp], C.c_int),
     "pct_slope_magnitudes": ([_vp, _vp, _i32, _i32, _d, _vp, _vp, _vp], C.c_int),

@@ -440,6 +440,50 @@ int pct_evaluate_masked(pct_ctx *ctx, const float *ground, const float *ceiling,
   return rc;
 }
 
+int64_t pct_tile_masks_bytes(int32_t rows, int32_t cols) {
+  if (rows <= 0 || cols <= 0) return 0;
+  return (int64_t)((rows + 15) / 16) * ((cols + 31) / 32) * 8;  // tiles >= 16 x 32
+}
+
+int pct_evaluate_tiles(pct_ctx *ctx, const float *ground, const float *ceiling, int32_t n_slices,
+                       int32_t rows, int32_t cols, double r_g, const pct_trav_params *p,
+                       const float *kernel_w, int32_t kside, const uint64_t *masks, float *cost,
+                       uint64_t *tile_masks, int32_t *tile_geom) {
+  CTX_GUARD(ctx);
+  if (tile_geom) tile_geom[0] = tile_geom[1] = 0;
+  ctx->eval_masks = n_slices <= 64 ? reinterpret_cast<const unsigned long long *>(masks) : nullptr;
+  ctx->eval_tcm = (ctx->eval_masks && tile_masks && tile_geom)
+                      ? reinterpret_cast<unsigned long long *>(tile_masks)
+                      : nullptr;
+  ctx->eval_tcm_written = false;
+  const int rc = pct_evaluate(ctx, ground, ceiling, n_slices, rows, cols, r_g, p, kernel_w, kside,
+                              cost);
+  if (rc == PCT_OK && ctx->eval_tcm && ctx->eval_tcm_written) {
+    tile_geom[0] = ctx->tcm_th;
+    tile_geom[1] = ctx->tcm_tw;
+  }
+  ctx->eval_masks = nullptr;
+  ctx->eval_tcm = nullptr;
+  return rc;
+}
+
+int pct_simplify_masked(pct_ctx *ctx, const float *ground, const float *cost, int32_t n_slices,
+                        int32_t rows, int32_t cols, double eps_e, double c_barrier,
+                        const uint64_t *masks, const uint64_t *tile_masks,
+                        const int32_t *tile_geom, int32_t *keep_host, int32_t *n_keep) {
+  CTX_GUARD(ctx);
+  if (masks && tile_masks && tile_geom && tile_geom[0] > 0 && tile_geom[1] > 0) {
+    ctx->simp_gm = reinterpret_cast<const unsigned long long *>(masks);
+    ctx->simp_tcm = reinterpret_cast<const unsigned long long *>(tile_masks);
+    ctx->simp_th = tile_geom[0];
+    ctx->simp_tw = tile_geom[1];
+  }
+  const int rc = pct_simplify(ctx, ground, cost, n_slices, rows, cols, eps_e, c_barrier, keep_host,
+                              n_keep);
+  ctx->simp_gm = ctx->simp_tcm = nullptr;
+  return rc;
+}
+
 const uint64_t *pct_tomo_masks(const pct_tomo *t) {
   return t ? reinterpret_cast<const uint64_t *>(t->masks) : nullptr;
 }

@@ -37,6 +37,22 @@ def _stack_ptr(ctx, layers, keep):
     return st.ptr
 
 
+def _change_info(slices):
+    """The slice-change information of the slices' stacks (the build's
+    ground masks, the evaluation's tile masks) when the slices are exactly
+    the whole ground stack of one device build and the whole cost stack its
+    evaluation wrote (values untouched on the host), else None."""
+    g = device_run([s.ground for s in slices])
+    c = device_run([s.cost for s in slices])
+    if g is None or c is None or g[1] != 0 or c[1] != 0:
+        return None
+    info = c[0].change_info
+    if info is None or info["ground"] is not g[0] or g[0].n_slices != len(slices) or \
+            c[0].n_slices != len(slices) or c[0].ctx is not g[0].ctx:
+        return None
+    return info
+
+
 def _ctx(slices):
     for s in slices:
         d = s.ground.device if isinstance(s.ground, Layer) else None
@@ -59,9 +75,16 @@ def simplify_tomogram(tomogram: Tomogram, eps_e: float = DEFAULT_EPS_E,
             c = _stack_ptr(ctx, [s.cost for s in slices], keepalive)
             idx = np.empty(len(slices), np.int32)
             n = C.c_int32(0)
-            ctx.check(ctx.lib.pct_simplify(ctx.h, g, c, len(slices), rows, cols, float(eps_e),
-                                           float(c_barrier), idx.ctypes.data, C.byref(n)),
-                      "pct_simplify")
+            info = _change_info(slices)
+            if info is not None:  # whole stacks of one build + evaluation
+                ctx.check(ctx.lib.pct_simplify_masked(
+                    ctx.h, g, c, len(slices), rows, cols, float(eps_e), float(c_barrier),
+                    info["masks"], info["tiles"].ptr, info["geom"].ctypes.data,
+                    idx.ctypes.data, C.byref(n)), "pct_simplify")
+            else:
+                ctx.check(ctx.lib.pct_simplify(ctx.h, g, c, len(slices), rows, cols,
+                                               float(eps_e), float(c_barrier), idx.ctypes.data,
+                                               C.byref(n)), "pct_simplify")
         slices = [slices[i] for i in idx[:n.value]]
     out = [TomogramSlice(s.ground, s.ceiling, s.plane_height, i, s.cost)
            for i, s in enumerate(slices)]

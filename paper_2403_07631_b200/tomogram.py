@@ -59,6 +59,9 @@ class DeviceStack:
         self.owner = owner
         self._host = {}
         self._kept = None  # (slices, delta, device counts) of the last kept count pass
+        # evaluation outputs: the ground stack they came from, its build masks
+        # and the tile masks of this (cost) stack (traversability._evaluate_layers)
+        self.change_info = None
 
     @property
     def plane_bytes(self) -> int:

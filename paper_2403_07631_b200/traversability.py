@@ -268,10 +268,24 @@ def _evaluate_layers(ctx, grounds, ceilings, r_g, params, w):
             gsrc[0].owner is csrc[0].owner and gsrc[0].n_slices == S and \
             isinstance(gsrc[0].owner, DeviceTomogram) and gsrc[0].ctx is ctx:
         masks = ctx.lib.pct_tomo_masks(gsrc[0].owner.handle)
-    ctx.check(ctx.lib.pct_evaluate_masked(ctx.h, gptr, cptr, S, rows, cols, float(r_g),
-                                          C.byref(_lib.trav_params_c(params, r_g)),
-                                          w.ctypes.data, w.shape[0], masks, out.ptr),
-              "pct_evaluate")
+    if masks:
+        # per evaluation tile, the slices whose costs may change: with the
+        # build's masks the simplify window then reads only where values
+        # change (simplify_tomogram -> pct_simplify_masked)
+        tm = _lib.DeviceBuffer(ctx, int(ctx.lib.pct_tile_masks_bytes(rows, cols)))
+        geom = np.zeros(2, np.int32)
+        ctx.check(ctx.lib.pct_evaluate_tiles(ctx.h, gptr, cptr, S, rows, cols, float(r_g),
+                                             C.byref(_lib.trav_params_c(params, r_g)),
+                                             w.ctypes.data, w.shape[0], masks, out.ptr, tm.ptr,
+                                             geom.ctypes.data), "pct_evaluate")
+        if geom[0] > 0:
+            # (the ground stack's owner keeps its masks alive as long as this does)
+            out.change_info = {"ground": gsrc[0], "masks": masks, "tiles": tm, "geom": geom}
+    else:
+        ctx.check(ctx.lib.pct_evaluate_masked(ctx.h, gptr, cptr, S, rows, cols, float(r_g),
+                                              C.byref(_lib.trav_params_c(params, r_g)),
+                                              w.ctypes.data, w.shape[0], masks, out.ptr),
+                  "pct_evaluate")
     return out
 
 

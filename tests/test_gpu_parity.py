@@ -812,3 +812,26 @@ def test_partitioned_builds_at_cell_borders(monkeypatch, offset):
         tom = pct.build_tomogram(pct.PointCloud(xyz), d_s, r_g)
         _assert_layers_equal(tom.ground_stack(), ref["ground"], f"ground {build}")
         _assert_layers_equal(tom.ceiling_stack(), ref["ceiling"], f"ceiling {build}")
+
+
+def test_simplify_uses_change_masks_and_matches(golden):
+    """The drop-in chain's simplify reads only where values change (the
+    build's ground masks + the evaluation's tile masks, pct_simplify_masked)
+    and keeps the same slices as the unmasked sweep and the reference."""
+    from paper_2403_07631_b200 import simplify as simp_mod
+    name = "synth_cfg2_n2000000"
+    case = golden["cases"][name]
+    xyz = case_input(name, case)
+    ev = pct.evaluate_tomogram(pct.build_tomogram(pct.PointCloud(xyz), case["d_s"], case["r_g"]),
+                               pct.TravParams())
+    info = simp_mod._change_info(list(ev.slices))
+    assert info is not None and int(info["geom"][0]) > 0
+    got = [s.plane_height for s in pct.simplify_tomogram(ev).slices]
+    # the same sweep without the masks: a cost layer replaced on the host
+    # (same values) breaks the device run, so the plain path runs
+    ev2 = pct.evaluate_tomogram(pct.build_tomogram(pct.PointCloud(xyz), case["d_s"], case["r_g"]),
+                                pct.TravParams())
+    ev2.slices[0].cost.values = ev2.slices[0].cost.values.copy()
+    assert simp_mod._change_info(list(ev2.slices)) is None
+    want = [s.plane_height for s in pct.simplify_tomogram(ev2).slices]
+    assert got == want == [case["heights"][k] for k in case["keep"]]
