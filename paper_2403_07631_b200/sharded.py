@@ -496,10 +496,18 @@ def _host_gather(res, ctx, root, group, d_s, r_g):
     nbytes = 3 * K * R * Cc * 4
     box = [None, None]
     if rank == root:
-        seg, _ = _root_segment(ctx, nbytes)
-        box = [seg.name, nbytes]
+        # a /dev/shm too small for the segment (containers default to 64 MB)
+        # would fault on first touch: every rank sends its band to the root
+        # instead (NCCL), which reads them back alone
+        if _shm_free() >= nbytes + (256 << 20):
+            seg, _ = _root_segment(ctx, nbytes)
+            box = [seg.name, nbytes]
+        else:
+            box = ["", nbytes]
     dist.broadcast_object_list(box, src=_global(group, root), group=group)
     name, nb = box
+    if not name:
+        return _p2p_host_gather(res, ctx, root, group, d_s, r_g)
     seg = seg if rank == root else _attached_segment(ctx, name, nb)
     # this rank's rows of every kept slice of the three layers
     plane = R * Cc * 4
@@ -524,6 +532,59 @@ def _host_gather(res, ctx, root, group, d_s, r_g):
     from .tomogram import Layer, Tomogram, TomogramSlice
     arr = np.frombuffer(seg.mm, np.float32, count=3 * K * R * Cc).reshape(3, K, R, Cc)
     seg.view = weakref.ref(arr)
+    origin = res.origin
+    slices = [TomogramSlice(Layer(arr[0, m], r_g, origin), Layer(arr[1, m], r_g, origin),
+                            float(res.heights[k]), m, Layer(arr[2, m], r_g, origin))
+              for m, k in enumerate(res.keep)]
+    return Tomogram(slices=slices, d_s=float(d_s), z_min=float(res.z_min))
+
+
+def _shm_free() -> int:
+    import os
+    try:
+        st = os.statvfs("/dev/shm")
+        return int(st.f_bavail) * int(st.f_frsize)
+    except OSError:
+        return 0
+
+
+def _p2p_host_gather(res, ctx, root, group, d_s, r_g):
+    """_host_gather without a shared segment: every rank packs its band of
+    the kept slices (3, K, band rows, cols) on its GPU and sends it to the
+    root (NCCL P2P; host-staged for gloo), which copies each band into one
+    page-locked host array."""
+    import torch
+    import torch.distributed as dist
+    rank, size = dist.get_rank(group), dist.get_world_size(group)
+    nccl = dist.get_backend(group) == "nccl"
+    K, R, Cc = len(res.keep), res.rows, res.cols
+    dev = res.ground.device
+    buf = torch.empty((3, K, res.nrows, Cc), dtype=torch.float32, device=dev)
+    with ctx.lock:
+        if K and res.nrows:
+            for L, t in enumerate((res.ground, res.ceiling, res.cost)):
+                _copy_slices(ctx, _ptr(buf, L * K * res.nrows * Cc), res.nrows * Cc, t.data_ptr(),
+                             t.stride(0), K, res.nrows * Cc, idx=res.keep)
+        ctx.check(ctx.lib.pct_sync(ctx.h), "sync")
+    if rank != root:
+        if buf.numel():
+            dist.send(buf if nccl else buf.cpu(), dst=_global(group, root), group=group)
+        return None
+    arr = _lib.pinned_pool(ctx).array((3, K, R, Cc), np.float32)
+    host = torch.from_numpy(arr)
+    starts = band_starts(R, size)
+    for b in range(size):
+        a0, a1 = starts[b], starts[b + 1]
+        if a1 == a0 or K == 0:
+            continue
+        if b == rank:
+            part = buf
+        else:
+            part = torch.empty((3, K, a1 - a0, Cc), dtype=torch.float32,
+                               device=dev if nccl else "cpu")
+            dist.recv(part, src=_global(group, b), group=group)
+        host[:, :, a0:a1, :].copy_(part)
+    from .tomogram import Layer, Tomogram, TomogramSlice
     origin = res.origin
     slices = [TomogramSlice(Layer(arr[0, m], r_g, origin), Layer(arr[1, m], r_g, origin),
                             float(res.heights[k]), m, Layer(arr[2, m], r_g, origin))

@@ -157,6 +157,9 @@ def _gloo_worker(rank, size, port, q, n_points, gather="device"):
         torch.cuda.set_device(0)
         import paper_2403_07631_b200 as p
         from paper_2403_07631_b200 import sharded, synth
+        if gather == "host-p2p":  # no room in /dev/shm: bands sent to the root
+            sharded._shm_free = lambda: 0
+            gather = "host"
         xyz = synth.spiral_ramp(n_points, seed=4)
         mine = np.ascontiguousarray(xyz[rank::size])
         tom = sharded.tomogram_sharded(p.PointCloud(mine), 0.4, 0.1, root=0, gather=gather)
@@ -180,12 +183,13 @@ def _gloo_worker(rank, size, port, q, n_points, gather="device"):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("gather", ["device", "host"])
+@pytest.mark.parametrize("gather", ["device", "host", "host-p2p"])
 def test_two_processes_gloo_equal_single_gpu(gather):
     """The real band pipeline in two processes (gloo: collectives staged
     through host memory; both ranks share cuda:0) returns on rank 0 the
     Tomogram of the one-GPU chain, bit for bit -- gathered on the root's GPU,
-    or written by each rank into one shared host segment."""
+    written by each rank into one shared host segment, or (no room in
+    /dev/shm) sent to the root and read back there."""
     import hashlib
     import socket
     import torch.multiprocessing as mp
