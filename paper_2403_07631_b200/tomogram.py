@@ -418,7 +418,8 @@ class Tomogram:
 
         # plan: stack -> (compacted slices, their counts, delta chain)
         chosen = {}
-        big = [(st, ks) for st, ks in todo if compact and st.rows * st.cols >= XFER_MIN_CELLS]
+        min_cells = int(os.environ.get("PCT_XFER_MIN_CELLS", XFER_MIN_CELLS))
+        big = [(st, ks) for st, ks in todo if compact and st.rows * st.cols >= min_cells]
         if mode != "nan":
             cands = [(st, ks) for st, ks in big if len(ks) > 1]
             for (st, ks), dt in zip(cands, counts(cands, True)):
