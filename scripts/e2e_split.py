@@ -1,6 +1,7 @@
 """Where the cfg3 drop-in e2e step spends its time (diagnostic): raw pinned
 H2D of the points, build (upload + device build), evaluate, simplify,
 materialize; each stage synchronised and wall-clocked, 5 repetitions."""
+import os
 import time
 
 import numpy as np
@@ -10,7 +11,9 @@ import paper_2403_07631_b200 as pct
 from paper_2403_07631_b200 import _lib, synth
 
 ctx = _lib.context(0)
-xyz = synth.generate(3)
+CFG = int(os.environ.get("CFG", "3"))
+xyz = synth.generate(CFG)
+d_s, r_g = synth.CONFIGS[CFG]["d_s"], synth.CONFIGS[CFG]["r_g"]
 pin = _lib.PinnedBuffer(ctx, xyz.shape, np.float32)
 pin.array[...] = xyz
 cloud = pct.PointCloud(pin.array)
@@ -23,7 +26,7 @@ for rep in range(5):
     dev.copy_(src, non_blocking=True)
     torch.cuda.synchronize()
     t1 = time.perf_counter()
-    tom = pct.build_tomogram(cloud, 0.5, 0.1, device=0)
+    tom = pct.build_tomogram(cloud, d_s, r_g, device=0)
     torch.cuda.synchronize()
     t2 = time.perf_counter()
     ev = pct.evaluate_tomogram(tom, params)
