@@ -154,7 +154,12 @@ class DeviceStack:
         nchunk = (cells + chunk - 1) // chunk
         words = (cells + 31) // 32
         pool = _lib.pinned_pool(self.ctx)
-        block = pool.array((n, self.rows, self.cols), np.float32)
+        # one 64-byte aligned host slice each (the rebuild streams whole
+        # 64-byte lines with non-temporal stores; a slice of cells % 16 != 0
+        # cells packed back to back would put every later slice off the lines)
+        pc = (cells + 15) // 16 * 16
+        raw = pool.array((n, pc), np.float32)
+        block = [raw[i, :cells].reshape(self.rows, self.cols) for i in range(n)]
         h_bm = pool.array((n, words), np.uint32)
         h_pk = pool.array((max(n_packed, 1),), np.float32)
         h_co = pool.array((n, nchunk), np.int64)
