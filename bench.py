@@ -636,6 +636,15 @@ def run_b200(args):
                         "frac": achieved / peak, "traffic": traffic,
                         "algorithmic": f"12 B per cell-slice x {cs_eval} cell-slices per launch",
                         "peak_source": peak_src}
+    if not banded and args.mode != "batch":
+        # every stage against the same roofline (SURVEY.md 8 d bytes: build
+        # 12 N + 8 cs, evaluate 12 cs, simplify 8 cs); > 1 means the stage
+        # skips work the algorithmic count includes (change masks)
+        alg = {"bounds+build": 12 * n_map + 8 * cs, "evaluate": 12 * cs, "simplify": 8 * cs}
+        line["roofline_stages"] = {
+            k: {"algorithmic_bytes": int(b), "ms": statistics.mean(per[k]) / len(maps),
+                "frac": b / (statistics.mean(per[k]) / len(maps) * 1e-3) / 1e9 / peak}
+            for k, b in alg.items() if per.get(k)}
 
     # ---- e2e through the public API with host buffers
     last_tom = None
